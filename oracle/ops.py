@@ -1,0 +1,155 @@
+"""Primitive float64 ops with explicit VJPs (oracle; test infrastructure only).
+
+Each function returns ``(out, bwd)`` where ``bwd(g)`` returns the gradients of
+the inputs that carry them.  Restated from /root/reference/pkg/src/kunlun/
+tensor.py; the cited lines are the reference semantics being reproduced.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+# Activation tags in the reference's table order (tensor.py:431-440).  The
+# integer codes are the ones the C-ABI uses (include/kunlun_capi.h).
+ACT_CODES = {
+    "identity": 0,
+    "relu": 1,
+    "silu": 2,
+    "tanh": 3,
+    "sigmoid": 4,
+    "exp": 5,
+    "sqrt": 6,
+    "log": 7,
+}
+
+
+def sigmoid(x: np.ndarray) -> np.ndarray:
+    """Stable logistic (tensor.py:403-409)."""
+    x = np.asarray(x, dtype=np.float64)
+    out = np.empty_like(x)
+    pos = x >= 0
+    out[pos] = 1.0 / (1.0 + np.exp(-x[pos]))
+    ex = np.exp(x[~pos])
+    out[~pos] = ex / (1.0 + ex)
+    return out
+
+
+def act_fwd(kind: str, x: np.ndarray) -> np.ndarray:
+    """Forward of the activation table (tensor.py:431-440)."""
+    if kind == "identity":
+        return x.copy()
+    if kind == "relu":
+        return np.maximum(x, 0.0)
+    if kind == "silu":
+        return x * sigmoid(x)
+    if kind == "tanh":
+        return np.tanh(x)
+    if kind == "sigmoid":
+        return sigmoid(x)
+    if kind == "exp":
+        return np.exp(x)
+    if kind == "sqrt":
+        return np.sqrt(x)
+    if kind == "log":
+        return np.log(x)
+    raise ValueError(f"unknown activation {kind!r}")
+
+
+def act_dfn(kind: str, x: np.ndarray, y: np.ndarray) -> np.ndarray:
+    """Derivative dfn(x, y) of the activation table (tensor.py:425-440).
+
+    relu'(0) = 0 (tensor.py:433); silu' = s(1 + x(1 - s)) (tensor.py:425-427).
+    """
+    if kind == "identity":
+        return np.ones_like(x)
+    if kind == "relu":
+        return (x > 0).astype(np.float64)
+    if kind == "silu":
+        s = sigmoid(x)
+        return s * (1.0 + x * (1.0 - s))
+    if kind == "tanh":
+        return 1.0 - y * y
+    if kind == "sigmoid":
+        return y * (1.0 - y)
+    if kind == "exp":
+        return y.copy()
+    if kind == "sqrt":
+        return 0.5 / y
+    if kind == "log":
+        return 1.0 / x
+    raise ValueError(f"unknown activation {kind!r}")
+
+
+def masked_softmax(a: np.ndarray, mask: np.ndarray):
+    """Softmax over the last axis restricted to ``mask``; fully-masked rows
+    give 0 (tensor.py:485-505).  VJP y*(g - sum(g*y)) (tensor.py:501-503)."""
+    m = np.broadcast_to(mask, a.shape)
+    neg = np.where(m, a, -np.inf)
+    if a.shape[-1]:
+        rowmax = neg.max(axis=-1, keepdims=True)
+    else:
+        rowmax = np.zeros(a.shape[:-1] + (1,))
+    rowmax = np.where(np.isfinite(rowmax), rowmax, 0.0)
+    e = np.exp(np.where(m, a - rowmax, -np.inf))
+    denom = e.sum(axis=-1, keepdims=True)
+    y = np.divide(e, denom, out=np.zeros_like(e), where=denom > 0)
+
+    def bwd(g):
+        inner = (g * y).sum(axis=-1, keepdims=True)
+        return y * (g - inner)
+
+    return y, bwd
+
+
+def rms_norm(x: np.ndarray, gain: np.ndarray, eps: float = 1e-6):
+    """x / sqrt(mean(x^2) + eps) * gain, eps inside the sqrt (tensor.py:552-556)."""
+    d = x.shape[-1]
+    ms = (x * x).mean(axis=-1, keepdims=True)
+    s = 1.0 / np.sqrt(ms + eps)
+    xn = x * s
+    y = xn * gain
+
+    def bwd(g):
+        gg = g * gain
+        dx = s * gg - (s ** 3) / d * x * (gg * x).sum(axis=-1, keepdims=True)
+        dgain = (g * xn).reshape(-1, d).sum(axis=0)
+        return dx, dgain
+
+    return y, bwd
+
+
+def bce_with_logits(z: np.ndarray, y: np.ndarray):
+    """Mean BCE in nats, stable for large |z| (tensor.py:535-549)."""
+    z = np.asarray(z, dtype=np.float64)
+    y = np.asarray(y, dtype=np.float64)
+    n = max(z.size, 1)
+    loss = float((np.maximum(z, 0.0) - y * z + np.log1p(np.exp(-np.abs(z)))).sum() / n)
+
+    def bwd(g=1.0):
+        return (sigmoid(z) - y) * (float(g) / n)
+
+    return loss, bwd
+
+
+def mlp_rows(x: np.ndarray, ws, bs, acts):
+    """Rowwise (linear, bias, act) stack; "identity" skips the act (mlp.py:47-54)."""
+    caches = []
+    h = x
+    for w, b, act in zip(ws, bs, acts):
+        pre = h @ w.T + b
+        post = pre if act == "identity" else act_fwd(act, pre)
+        caches.append((h, pre, post))
+        h = post
+
+    def bwd(g):
+        dws, dbs = [None] * len(ws), [None] * len(ws)
+        for i in reversed(range(len(ws))):
+            hin, pre, post = caches[i]
+            if acts[i] != "identity":
+                g = g * act_dfn(acts[i], pre, post)
+            dws[i] = g.reshape(-1, g.shape[-1]).T @ hin.reshape(-1, hin.shape[-1])
+            dbs[i] = g.reshape(-1, g.shape[-1]).sum(axis=0)
+            g = g @ ws[i]
+        return g, dws, dbs
+
+    return h, bwd

@@ -1,0 +1,144 @@
+"""Pin the numpy oracle against golden vectors produced by the unmodified
+reference (tests/golden/make_golden.py).  CPU only."""
+
+import os
+
+import numpy as np
+import pytest
+
+from oracle import kunlun as K
+from oracle import model as OM
+
+G = os.path.join(os.path.dirname(__file__), "golden")
+TOL = 1e-10
+
+
+def load(name):
+    z = np.load(os.path.join(G, name))
+    params = {k[6:]: z[k] for k in z.files if k.startswith("param:")}
+    grads = {k[5:]: z[k] for k in z.files if k.startswith("grad:")}
+    return z, params, grads
+
+
+def rel(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    den = max(np.abs(b).max() if b.size else 0.0, 1e-300)
+    return (np.abs(a - b).max() if b.size else 0.0) / den
+
+
+@pytest.mark.parametrize("tag", ["default", "sigexp"])
+def test_gdpa(tag):
+    z, p, g = load(f"gdpa_{tag}.npz")
+    d, H, n_kv, n_sum, n_ctx, t_len = z["meta"]
+    acts = [str(a) for a in z["acts"]]
+    s, x, pool = p["in/S"], p["in/X"], p["pool"]
+    xs, xs_bwd = K.summarize_nonseq(x, pool)
+    kv, kv_bwd = K.generate_kv(xs, p, "g", int(n_kv))
+    y, y_bwd = K.gdpa_forward(s, kv, p, "g", float(t_len), acts)
+    assert rel(y, z["out_Y"]) < TOL
+    ds, dkvs, gr = y_bwd(z["cot_Y"])
+    dxs, gr2 = kv_bwd(dkvs)
+    dx, dpool = xs_bwd(dxs)
+    gr.update(gr2)
+    gr["in/S"], gr["in/X"], gr["pool"] = ds, dx, dpool
+    for k, v in g.items():
+        assert rel(gr[k], v) < TOL, k
+
+
+@pytest.mark.parametrize("tag", ["w3_len9", "w3_causal", "full_len7", "w0_len0"])
+def test_mha(tag):
+    z, p, g = load(f"mha_{tag}.npz")
+    d, H, t_len, w, causal, length, full = z["meta"]
+    length = None if length < 0 else int(length)
+    s = p["in/S"]
+    if full:
+        y, bwd = K.mha_full(s, p, "m", length)
+    else:
+        y, bwd = K.mha_window(s, p, "m", int(w), bool(causal), length)
+    assert rel(y, z["out_Y"]) < TOL
+    ds, gr = bwd(z["cot_Y"])
+    gr["in/S"] = ds
+    for k, v in g.items():
+        assert rel(gr[k], v) < TOL, k
+
+
+@pytest.mark.parametrize("tag", ["t10", "t1", "t0"])
+def test_hsp(tag):
+    z, p, g = load(f"hsp_{tag}.npz")
+    d, H, t_len, budget, n_seeds, rank = z["meta"]
+    rows, bwd = K.hsp_summarize(p["in/S"], p, "s", int(budget))
+    assert rel(rows, z["out_Y"]) < TOL
+    ds, gr = bwd(z["cot_Y"])
+    gr["in/S"] = ds
+    for k, v in g.items():
+        got = gr.get(k, np.zeros_like(v))
+        assert rel(got, v) < TOL or np.abs(v).max() == np.abs(got).max() == 0, k
+
+
+def test_gi():
+    z, p, g = load("gi.npz")
+    d, n_ctx, experts, hidden, *budgets = z["meta"]
+    rows = [p[f"in/R{e}"] for e in range(len(budgets))]
+    y, bwd = K.global_interaction(p["in/X"], rows, p, "gi", int(experts))
+    assert rel(y, z["out_Y"]) < TOL
+    dx, drows, gr = bwd(z["cot_Y"])
+    gr["in/X"] = dx
+    for e, dr in enumerate(drows):
+        gr[f"in/R{e}"] = dr
+    for k, v in g.items():
+        assert rel(gr[k], v) < TOL, k
+
+
+def _model_spec(compskip):
+    return OM.ModelSpec(L=2, d=16, heads=4, n_ctx=5, n_sum=2, n_kv=4, experts=2, compskip=compskip,
+                        events=[OM.EventSpec(T=12, w=3, budget=8, n_seeds=6, rank=2),
+                                OM.EventSpec(T=9, w=2, budget=4, n_seeds=3, rank=1)])
+
+
+@pytest.mark.parametrize("tag,compskip", [("noskip", False), ("compskip", True)])
+def test_model(tag, compskip):
+    z, p, g = load(f"model_{tag}.npz")
+    spec = _model_spec(compskip)
+    S = [z["S0"], z["S1"]]
+    lengths = [z["len0"], z["len1"]]
+    cot = [{"X": z[f"cot{l}_X"], "S": [z[f"cot{l}_S{e}"] for e in range(2)],
+            "H": [z[f"cot{l}_H{e}"] for e in range(2)]} for l in range(spec.L)]
+    r = OM.model_forward_backward(spec, p, z["X"], S, lengths, z["labels"], cot)
+    # the oracle's parity loss also covers padding rows (identity outputs);
+    # the reference sees only valid rows, so remove that constant term.
+    pad = sum(float((S[e][b, lengths[e][b]:] * cot[l]["S"][e][b, lengths[e][b]:]).sum())
+              for l in range(spec.L) for e in range(2) for b in range(S[e].shape[0]))
+    assert abs(r["loss"] - pad - float(z["loss"])) < 1e-10 * max(1.0, abs(float(z["loss"])))
+    assert rel(r["logits"], z["logits"]) < TOL
+    assert rel(r["dX"], z["dX"]) < TOL
+    for e in range(2):
+        assert rel(r["dS"][e], z[f"dS{e}"]) < TOL
+    for k, v in g.items():
+        assert rel(r["grads"][k], v) < TOL or (np.abs(v).max() == 0 and np.abs(r["grads"][k]).max() == 0), k
+
+
+def test_index_kats():
+    z = np.load(os.path.join(G, "index.npz"))
+    for k in z.files:
+        parts = k.split("_")
+        if parts[0] == "band":
+            t, w, c = map(int, parts[1:])
+            assert np.array_equal(K.band_mask(t, w, bool(c)), z[k])
+        elif parts[0] == "support":
+            t, w, c = map(int, parts[1:])
+            assert np.array_equal(K.band_support_sizes(t, w, bool(c)), z[k])
+        elif parts[0] == "experts":
+            tot, m = map(int, parts[1:])
+            assert np.array_equal(np.array(K.expert_ranges(tot, m)), z[k])
+        elif parts[0] == "split":
+            assert list(K.split_for_budget(int(parts[1]))) == list(z[k])
+
+
+def test_compskip_spec_examples():
+    # SPEC.md:480-482
+    assert OM.compskip_config(4) == [(True, False, False), (False, True, True)] * 2
+    assert OM.compskip_config(1) == [(True, False, False)]
+    assert OM.compskip_config(3, enabled=False) == [(False, False, False)] * 3
+    with pytest.raises(ValueError):
+        OM.compskip_config(0)
