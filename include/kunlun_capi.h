@@ -1,0 +1,218 @@
+/*
+ * kunlun_capi.h — C ABI of libkunlun_sm100a.so, the B200 (sm_100a) kernels
+ * behind the Kunlun layer hot path (arXiv 2602.10016).
+ *
+ * The reference (pkg/src/kunlun, numpy float64) has no native code; its
+ * plugin point for fused kernels is `record(out, parents, vjp)`
+ * (/root/reference/pkg/src/kunlun/tensor.py:185-195), with `gdpa_core`
+ * (gdpa.py:141-187) as the in-tree fused-op example.  Each entry point below
+ * is one device operation a `record`-style VJP (or a torch.autograd.Function
+ * in paper_2602_10016_b200) binds; the comment on each names the reference
+ * operation(s) it replaces.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  All pointers are device pointers unless
+ *    stated; the caller owns every buffer (the library never allocates).
+ *  - Every entry takes a cudaStream_t (as void*) and is stream-ordered and
+ *    reentrant.  Return 0 on success, KL_E* on failure with a message from
+ *    kl_last_error() (thread-local).
+ *  - Element strides are in elements (not bytes).
+ *  - dtype: KL_F32 (SIMT FFMA path, the 1e-5 parity path) or KL_BF16
+ *    (tcgen05/TMEM/TMA path on sm_100a, fp32 accumulation).
+ */
+#ifndef KUNLUN_CAPI_H
+#define KUNLUN_CAPI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KL_OK 0
+#define KL_EBADSHAPE 1    /* shape / stride contract violated (ShapeError)     */
+#define KL_EUNSUPPORTED 2 /* valid request the library cannot run (ValueError) */
+#define KL_ELAUNCH 3      /* CUDA launch / runtime failure (RuntimeError)      */
+
+#define KL_F32 0
+#define KL_BF16 1
+
+/* Activation tags, in the reference table order (tensor.py:431-440). */
+#define KL_ACT_IDENTITY 0
+#define KL_ACT_RELU 1
+#define KL_ACT_SILU 2
+#define KL_ACT_TANH 3
+#define KL_ACT_SIGMOID 4
+#define KL_ACT_EXP 5
+#define KL_ACT_SQRT 6
+#define KL_ACT_LOG 7
+
+#define KL_MAX_ACT_GROUPS 32
+
+int kl_version(void);
+const char* kl_last_error(void);
+/* Number of kernels this library launched since load (for bench accounting). */
+unsigned long long kl_launch_count(void);
+/* 1 when the device is sm_100 and the tcgen05 path is enabled. */
+int kl_tcgen05_available(void);
+/* Force the SIMT GEMM even for bf16 (debug / A-B testing).  0 = auto. */
+void kl_set_gemm_path(int path);
+
+/*
+ * Strided, batched, optionally batch-reducing GEMM with a fused epilogue.
+ * Replaces every matmul/matvec of the hot path and their VJPs
+ * (tensor.py:283-297: dA = g B^T, dB = A^T g) — projections, weight
+ * generation (gdpa.py:103-112), the folded GDPA contractions (gdpa.py:120-187),
+ * HSP/PMA pooling (seqsum.py:26-122), Wukong/aggregate maps
+ * (interaction.py:106-157) and rowwise MLPs (mlp.py:47-59).
+ *
+ *   for each (z1, z2):  acc = sum_k A[m,k] B[k,n]
+ *   out[m,n] = act_c( alpha*acc [* act'_c(aux[m,n]) if aux_mode==2] + bias[n] )
+ *              + beta*C[m,n] + R[m,n]                ([aux]=pre-act if aux_mode==1)
+ *   rows m >= row_limit[z1] (if row_limit) are written as 0 (pre-act 0 too).
+ * A batch index with red{1,2}=1 is summed into one output (its C stride is
+ * ignored).  act_c = act_codes[(n / act_group) % n_act] (n_act=0 -> identity).
+ */
+typedef struct kl_gemm_args {
+  int M, N, K;
+  int nb1, nb2;
+  int red1, red2;
+  int ab_dtype, c_dtype;
+  const void* A;
+  long long a_rs, a_cs, a_s1, a_s2;
+  const void* B;
+  long long b_rs, b_cs, b_s1, b_s2;
+  void* C;
+  long long c_rs, c_cs, c_s1, c_s2;
+  const void* R; /* residual, c_dtype, or NULL */
+  long long r_rs, r_cs, r_s1, r_s2;
+  void* aux; /* c_dtype, C's strides */
+  int aux_mode; /* 0 none, 1 write pre-activation, 2 multiply by act'(aux) */
+  float alpha, beta;
+  const float* bias; /* [N] fp32 or NULL */
+  const int* row_limit; /* [nb1] or NULL */
+  int n_act, act_group;
+  int act_codes[KL_MAX_ACT_GROUPS];
+} kl_gemm_args;
+
+int kl_gemm(const kl_gemm_args* args, void* stream);
+
+/*
+ * Sliding-window multi-head self-attention core (flash style; tiles outside
+ * the band are never visited).  Replaces the score/softmax/value part of
+ * `mha_window` / `mha_full` (attention.py:69-93 with band_mask & length mask,
+ * attention.py:96-129; masked_softmax_lastdim tensor.py:485-505).
+ *   QKV: (B, T, 3*H*d_h) packed [Q | K | V], row stride ld_qkv, batch stride bs_qkv.
+ *   O:   (B, T, H*d_h), rows >= length and fully-masked rows are 0.
+ *   LSE: (B, H, T) fp32 log-sum-exp of the scaled masked scores (for bwd).
+ * Mask: |i-j| <= w (and j <= i when causal), i, j < lengths[b].
+ */
+typedef struct kl_swa_args {
+  int B, T, H, d_h;
+  int w, causal;
+  int dtype;
+  float scale; /* 1/sqrt(d_h), attention.py:83 */
+  const int* lengths;
+  const void* QKV;
+  long long ld_qkv, bs_qkv;
+  void* O;
+  long long ld_o, bs_o;
+  float* LSE;
+  /* backward */
+  const void* dO;
+  void* dQKV; /* same layout as QKV; fully written */
+  float* Dbuf; /* (B, H, T) fp32 scratch: rowsum(dO * O) */
+} kl_swa_args;
+
+int kl_swa_fwd(const kl_swa_args* args, void* stream);
+int kl_swa_bwd(const kl_swa_args* args, void* stream);
+/* Bit-exact test hook: per-query key count the SWA kernels visit, written to
+ * support[b*T + i] (int32); must equal band_support_sizes (attention.py:132-139)
+ * restricted to valid rows (0 for rows >= length). */
+int kl_swa_debug_support(const kl_swa_args* args, int* support, void* stream);
+
+/*
+ * Column softmax over a (T x C) score block per batch, masked to rows
+ * t < lengths[b]; writes P (same layout, dtype) and per-column LSE (fp32).
+ * Fully-masked columns (length 0) give P = 0.  Used by HSP/PMA pooling
+ * (seqsum.py:26-34, 96-102 via attention.py:69-93 with queries as columns).
+ */
+typedef struct kl_colsoftmax_args {
+  int Bn, T, C;
+  int dtype_in, dtype_out;
+  const void* X;
+  long long x_rs, x_bs;
+  void* P;
+  long long p_rs, p_bs;
+  float* LSE; /* (Bn, C) or NULL */
+  const int* lengths;
+  /* backward: dX = P * (dP - Dcol), Dcol[c] = sum_t P[t,c] dP[t,c] */
+  const void* dP;
+  long long dp_rs, dp_bs;
+  void* dX;
+  long long dx_rs, dx_bs;
+} kl_colsoftmax_args;
+
+int kl_colsoftmax_fwd(const kl_colsoftmax_args* args, void* stream);
+int kl_colsoftmax_bwd(const kl_colsoftmax_args* args, void* stream);
+
+/* RMSNorm over the last axis, eps inside the sqrt (tensor.py:552-556).
+ * x (rows, d) fp32; y = x / sqrt(mean(x^2)+eps) * gain.  bwd writes dx and
+ * dgain (fp32, dgain fully written). */
+int kl_rmsnorm_fwd(int rows, int d, float eps, const float* x, const float* gain, float* y, void* stream);
+int kl_rmsnorm_bwd(int rows, int d, float eps, const float* x, const float* gain, const float* dy,
+                   float* dx, float* dgain, void* stream);
+
+/* recent_rows (seqsum.py:186-196): out[b, r] = S[b, len-n+r] for len-n+r >= 0
+ * else 0; dtype_s for S/out.  bwd accumulates into dS (dS[b, t] += dOut[b, r]). */
+int kl_recent_rows_fwd(int B, int T, int d, int n_recent, int dtype, const void* S, long long s_bs,
+                       const int* lengths, void* out, long long o_bs, void* stream);
+int kl_recent_rows_bwd(int B, int T, int d, int n_recent, int dtype, const void* dout, long long o_bs,
+                       const int* lengths, void* dS, long long s_bs, void* stream);
+
+/* Wukong pairwise-dot block (interaction.py:63-76, 106-121):
+ * tri[b, p] = x[b, r_p] . x[b, c_p] over np.triu_indices(n) order.
+ * bwd: dx[b] += (dG + dG^T) x[b] with dG scattered from dtri. */
+int kl_gram_triu_fwd(int B, int n, int d, int dtype, const void* x, long long x_rs, long long x_bs,
+                     void* tri, long long t_bs, void* stream);
+int kl_gram_triu_bwd(int B, int n, int d, int dtype, const void* x, long long x_rs, long long x_bs,
+                     const void* dtri, long long t_bs, void* dx, long long dx_rs, long long dx_bs,
+                     void* stream);
+
+/* Gated residual of a Wukong expert: out = x + gd*deep + gt*dot, gates are
+ * device fp32 scalars (shape (1,), interaction.py:97-98).  bwd: ddeep = g*gd,
+ * ddot = g*gt, dx += g, dgate_{deep,dot} = sum(g*deep), sum(g*dot) (fp32,
+ * written).  All tensors (rows, d) contiguous with row strides given. */
+int kl_gated_sum_fwd(int rows, int d, int dtype, const void* x, long long x_rs, const void* deep,
+                     const void* dot, const float* gd, const float* gt, void* out, long long o_rs,
+                     void* stream);
+int kl_gated_sum_bwd(int rows, int d, int dtype, const void* g, long long g_rs, const void* deep,
+                     const void* dot, const float* gd, const float* gt, void* ddeep, void* ddot,
+                     float* dgd, float* dgt, float* scratch, void* stream);
+
+/* Mean BCE with logits (tensor.py:535-549): loss[0] = mean(...), dz = (sig(z)-y)/n.
+ * z, y, dz fp32 (n,). */
+int kl_bce_fwd_bwd(int n, const float* z, const float* y, float* loss, float* dz, void* stream);
+
+/* dtype conversion copy (fp32 <-> bf16), n elements, contiguous. */
+int kl_cast(long long n, int dtype_in, const void* x, int dtype_out, void* y, void* stream);
+
+/* Elementwise activation forward / backward with per-column-group codes
+ * (same coding as kl_gemm).  (rows, cols) contiguous, row stride ld. */
+int kl_act_fwd(int rows, int cols, int dtype, const void* x, long long ld, void* y, long long ld_y,
+               int n_act, int act_group, const int* act_codes_host, void* stream);
+
+/* y = g * act'(x) elementwise (the VJP of kl_act_fwd; dfn of tensor.py:431-440). */
+int kl_act_bwd(int rows, int cols, int dtype, const void* g, long long ldg, const void* x, long long ldx, void* y,
+               long long ld_y, int n_act, int act_group, const int* act_codes_host, void* stream);
+
+/* Non-finite scan: atomically ORs 1 into *flag if any element of x is NaN/Inf
+ * (NumericsError, tensor.py:21-27). */
+int kl_check_finite(long long n, int dtype, const void* x, unsigned int* flag, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KUNLUN_CAPI_H */

@@ -1,0 +1,262 @@
+"""ctypes binding of libkunlun_sm100a.so (include/kunlun_capi.h).
+
+The product path has no fallback: if the library is missing, or no CUDA
+device is present when an op runs, the call raises.  Python ints/pointers
+only cross the boundary — no torch types in the C signatures.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+from .tensor import NumericsError, ShapeError
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libkunlun_sm100a.so")
+
+KL_OK, KL_EBADSHAPE, KL_EUNSUPPORTED, KL_ELAUNCH = 0, 1, 2, 3
+KL_F32, KL_BF16 = 0, 1
+MAX_ACT = 32
+
+ACT_CODES = {"identity": 0, "relu": 1, "silu": 2, "tanh": 3, "sigmoid": 4, "exp": 5, "sqrt": 6, "log": 7}
+
+
+class GemmArgs(C.Structure):
+    _fields_ = [
+        ("M", C.c_int), ("N", C.c_int), ("K", C.c_int),
+        ("nb1", C.c_int), ("nb2", C.c_int), ("red1", C.c_int), ("red2", C.c_int),
+        ("ab_dtype", C.c_int), ("c_dtype", C.c_int),
+        ("A", C.c_void_p), ("a_rs", C.c_longlong), ("a_cs", C.c_longlong), ("a_s1", C.c_longlong), ("a_s2", C.c_longlong),
+        ("B", C.c_void_p), ("b_rs", C.c_longlong), ("b_cs", C.c_longlong), ("b_s1", C.c_longlong), ("b_s2", C.c_longlong),
+        ("C", C.c_void_p), ("c_rs", C.c_longlong), ("c_cs", C.c_longlong), ("c_s1", C.c_longlong), ("c_s2", C.c_longlong),
+        ("R", C.c_void_p), ("r_rs", C.c_longlong), ("r_cs", C.c_longlong), ("r_s1", C.c_longlong), ("r_s2", C.c_longlong),
+        ("aux", C.c_void_p), ("aux_mode", C.c_int),
+        ("alpha", C.c_float), ("beta", C.c_float),
+        ("bias", C.c_void_p), ("row_limit", C.c_void_p),
+        ("n_act", C.c_int), ("act_group", C.c_int),
+        ("act_codes", C.c_int * MAX_ACT),
+    ]
+
+
+class SwaArgs(C.Structure):
+    _fields_ = [
+        ("B", C.c_int), ("T", C.c_int), ("H", C.c_int), ("d_h", C.c_int),
+        ("w", C.c_int), ("causal", C.c_int), ("dtype", C.c_int), ("scale", C.c_float),
+        ("lengths", C.c_void_p),
+        ("QKV", C.c_void_p), ("ld_qkv", C.c_longlong), ("bs_qkv", C.c_longlong),
+        ("O", C.c_void_p), ("ld_o", C.c_longlong), ("bs_o", C.c_longlong),
+        ("LSE", C.c_void_p),
+        ("dO", C.c_void_p), ("dQKV", C.c_void_p), ("Dbuf", C.c_void_p),
+    ]
+
+
+class ColSoftmaxArgs(C.Structure):
+    _fields_ = [
+        ("Bn", C.c_int), ("T", C.c_int), ("C", C.c_int),
+        ("dtype_in", C.c_int), ("dtype_out", C.c_int),
+        ("X", C.c_void_p), ("x_rs", C.c_longlong), ("x_bs", C.c_longlong),
+        ("P", C.c_void_p), ("p_rs", C.c_longlong), ("p_bs", C.c_longlong),
+        ("LSE", C.c_void_p), ("lengths", C.c_void_p),
+        ("dP", C.c_void_p), ("dp_rs", C.c_longlong), ("dp_bs", C.c_longlong),
+        ("dX", C.c_void_p), ("dx_rs", C.c_longlong), ("dx_bs", C.c_longlong),
+    ]
+
+
+_lib = None
+
+_SIGS = {
+    "kl_version": ([], C.c_int),
+    "kl_last_error": ([], C.c_char_p),
+    "kl_launch_count": ([], C.c_ulonglong),
+    "kl_tcgen05_available": ([], C.c_int),
+    "kl_set_gemm_path": ([C.c_int], None),
+    "kl_gemm": ([C.POINTER(GemmArgs), C.c_void_p], C.c_int),
+    "kl_swa_fwd": ([C.POINTER(SwaArgs), C.c_void_p], C.c_int),
+    "kl_swa_bwd": ([C.POINTER(SwaArgs), C.c_void_p], C.c_int),
+    "kl_swa_debug_support": ([C.POINTER(SwaArgs), C.c_void_p, C.c_void_p], C.c_int),
+    "kl_colsoftmax_fwd": ([C.POINTER(ColSoftmaxArgs), C.c_void_p], C.c_int),
+    "kl_colsoftmax_bwd": ([C.POINTER(ColSoftmaxArgs), C.c_void_p], C.c_int),
+    "kl_rmsnorm_fwd": ([C.c_int, C.c_int, C.c_float, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
+    "kl_rmsnorm_bwd": ([C.c_int, C.c_int, C.c_float] + [C.c_void_p] * 6, C.c_int),
+    "kl_recent_rows_fwd": ([C.c_int] * 5 + [C.c_void_p, C.c_longlong, C.c_void_p, C.c_void_p, C.c_longlong, C.c_void_p], C.c_int),
+    "kl_recent_rows_bwd": ([C.c_int] * 5 + [C.c_void_p, C.c_longlong, C.c_void_p, C.c_void_p, C.c_longlong, C.c_void_p], C.c_int),
+    "kl_gram_triu_fwd": ([C.c_int] * 4 + [C.c_void_p, C.c_longlong, C.c_longlong, C.c_void_p, C.c_longlong, C.c_void_p], C.c_int),
+    "kl_gram_triu_bwd": ([C.c_int] * 4 + [C.c_void_p, C.c_longlong, C.c_longlong, C.c_void_p, C.c_longlong,
+                                          C.c_void_p, C.c_longlong, C.c_longlong, C.c_void_p], C.c_int),
+    "kl_gated_sum_fwd": ([C.c_int] * 3 + [C.c_void_p, C.c_longlong] + [C.c_void_p] * 5 + [C.c_longlong, C.c_void_p], C.c_int),
+    "kl_gated_sum_bwd": ([C.c_int] * 3 + [C.c_void_p, C.c_longlong] + [C.c_void_p] * 10, C.c_int),
+    "kl_bce_fwd_bwd": ([C.c_int] + [C.c_void_p] * 5, C.c_int),
+    "kl_cast": ([C.c_longlong, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p], C.c_int),
+    "kl_act_fwd": ([C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_longlong, C.c_void_p, C.c_longlong, C.c_int, C.c_int,
+                    C.c_void_p, C.c_void_p], C.c_int),
+    "kl_act_bwd": ([C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_longlong, C.c_void_p, C.c_longlong, C.c_void_p,
+                    C.c_longlong, C.c_int, C.c_int, C.c_void_p, C.c_void_p], C.c_int),
+    "kl_check_finite": ([C.c_longlong, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
+}
+
+EXPORTED = tuple(_SIGS)
+
+
+def lib():
+    """Load the CUDA library (raises if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"libkunlun_sm100a.so not built ({LIB_PATH}); run `make` or __graft_entry__.build()")
+        L = C.CDLL(LIB_PATH)
+        for name, (args, res) in _SIGS.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = res
+        _lib = L
+    return _lib
+
+
+def _check(rc: int, what: str) -> None:
+    if rc == KL_OK:
+        return
+    msg = lib().kl_last_error().decode(errors="replace")
+    if rc == KL_EBADSHAPE:
+        raise ShapeError(f"{what}: {msg}")
+    if rc == KL_EUNSUPPORTED:
+        raise ValueError(f"{what}: {msg}")
+    raise RuntimeError(f"{what}: {msg}")
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _need_cuda(*ts) -> None:
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise RuntimeError("kunlun CUDA ops need CUDA tensors (no CPU fallback)")
+
+
+def dt(t: torch.Tensor) -> int:
+    if t.dtype == torch.float32:
+        return KL_F32
+    if t.dtype == torch.bfloat16:
+        return KL_BF16
+    raise ValueError(f"unsupported dtype {t.dtype}")
+
+
+def ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def _as4(t: torch.Tensor) -> torch.Tensor:
+    while t.dim() < 4:
+        t = t.unsqueeze(0)
+    if t.dim() != 4:
+        raise ShapeError(f"gemm operands have at most 2 batch dims, got shape {tuple(t.shape)}")
+    return t
+
+
+def _bstride(t: torch.Tensor, i: int) -> int:
+    return 0 if t.shape[i] == 1 else t.stride(i)
+
+
+def gemm(A: torch.Tensor, B: torch.Tensor, out: torch.Tensor | None = None, *, out_dtype=None,
+         alpha: float = 1.0, beta: float = 0.0, bias: torch.Tensor | None = None, acts=None,
+         act_group: int = 1, aux: torch.Tensor | None = None, aux_mode: int = 0,
+         residual: torch.Tensor | None = None, row_limit: torch.Tensor | None = None,
+         reduce=(False, False)) -> torch.Tensor:
+    """out[z] = epi(A[z] @ B[z]) over up to two (broadcastable) batch dims.
+
+    A (..., M, K), B (..., K, N) are arbitrary strided views; ``reduce[i]``
+    sums batch dim i (of the 2 padded leading dims) into a single output.
+    ``out`` (..., M, N) is written in place when given (``beta`` reads it).
+    """
+    _need_cuda(A, B, out, bias, residual, aux, row_limit)
+    if A.dtype != B.dtype:
+        raise ValueError(f"gemm operand dtypes differ: {A.dtype} vs {B.dtype}")
+    A4, B4 = _as4(A), _as4(B)
+    M, K = A4.shape[2], A4.shape[3]
+    if B4.shape[2] != K:
+        raise ShapeError(f"gemm inner dims differ: {tuple(A.shape)} @ {tuple(B.shape)}")
+    N = B4.shape[3]
+    nb1 = max(A4.shape[0], B4.shape[0])
+    nb2 = max(A4.shape[1], B4.shape[1])
+    for t4 in (A4, B4):
+        if t4.shape[0] not in (1, nb1) or t4.shape[1] not in (1, nb2):
+            raise ShapeError("gemm batch dims do not broadcast")
+    red1, red2 = bool(reduce[0]), bool(reduce[1])
+    oshape = (1 if red1 else nb1, 1 if red2 else nb2, M, N)
+    if out is None:
+        lead = max(A.dim(), B.dim()) - 2
+        out = torch.empty(oshape[2 - lead:], device=A.device, dtype=out_dtype or A.dtype)
+    ret = out
+    O4 = _as4(out)
+    if tuple(O4.shape[2:]) != (M, N):
+        raise ShapeError(f"gemm output shape {tuple(out.shape)} != (.., {M}, {N})")
+    a = GemmArgs()
+    a.M, a.N, a.K = M, N, K
+    a.nb1, a.nb2, a.red1, a.red2 = nb1, nb2, int(red1), int(red2)
+    a.ab_dtype, a.c_dtype = dt(A), dt(out)
+    a.A = A4.data_ptr()
+    a.a_rs, a.a_cs, a.a_s1, a.a_s2 = A4.stride(2), A4.stride(3), _bstride(A4, 0), _bstride(A4, 1)
+    a.B = B4.data_ptr()
+    a.b_rs, a.b_cs, a.b_s1, a.b_s2 = B4.stride(2), B4.stride(3), _bstride(B4, 0), _bstride(B4, 1)
+    a.C = O4.data_ptr()
+    a.c_rs, a.c_cs, a.c_s1, a.c_s2 = O4.stride(2), O4.stride(3), _bstride(O4, 0), _bstride(O4, 1)
+    if residual is not None:
+        R4 = _as4(residual)
+        if residual.dtype != out.dtype:
+            raise ValueError("residual dtype must equal the output dtype")
+        a.R = R4.data_ptr()
+        a.r_rs, a.r_cs, a.r_s1, a.r_s2 = R4.stride(2), R4.stride(3), _bstride(R4, 0), _bstride(R4, 1)
+    if aux is not None:
+        X4 = _as4(aux)
+        if X4.stride() != O4.stride() or aux.dtype != out.dtype:
+            raise ShapeError("aux must share the output's strides and dtype")
+        a.aux = X4.data_ptr()
+    a.aux_mode = aux_mode
+    a.alpha, a.beta = alpha, beta
+    if bias is not None:
+        if bias.dtype != torch.float32 or not bias.is_contiguous():
+            raise ValueError("bias must be contiguous fp32")
+        a.bias = bias.data_ptr()
+    if row_limit is not None:
+        if row_limit.dtype != torch.int32:
+            raise ValueError("row_limit must be int32")
+        a.row_limit = row_limit.data_ptr()
+    if acts:
+        codes = [ACT_CODES[x] if isinstance(x, str) else int(x) for x in acts]
+        if len(codes) > MAX_ACT:
+            raise ValueError("too many activation groups")
+        a.n_act = len(codes)
+        a.act_group = act_group
+        for i, c in enumerate(codes):
+            a.act_codes[i] = c
+    _check(lib().kl_gemm(C.byref(a), _stream()), "kl_gemm")
+    return ret
+
+
+def swa_args(qkv, lengths, H, d_h, w, causal, O, LSE, dO=None, dqkv=None, Dbuf=None) -> SwaArgs:
+    B, T = qkv.shape[0], qkv.shape[1]
+    a = SwaArgs()
+    a.B, a.T, a.H, a.d_h, a.w, a.causal = B, T, H, d_h, int(w), int(causal)
+    a.dtype = dt(qkv)
+    a.scale = 1.0 / float(d_h) ** 0.5
+    a.lengths = lengths.data_ptr()
+    a.QKV, a.ld_qkv, a.bs_qkv = qkv.data_ptr(), qkv.stride(1), qkv.stride(0)
+    a.O, a.ld_o, a.bs_o = O.data_ptr(), O.stride(1), O.stride(0)
+    a.LSE = LSE.data_ptr()
+    if dO is not None:
+        if dO.stride() != O.stride():
+            raise ShapeError("dO must share O's strides")
+        a.dO = dO.data_ptr()
+        a.dQKV = dqkv.data_ptr()
+        a.Dbuf = Dbuf.data_ptr()
+    return a
+
+
+def call(name: str, *args):
+    _check(getattr(lib(), name)(*args), name)
+
+
+def launch_count() -> int:
+    return int(lib().kl_launch_count())

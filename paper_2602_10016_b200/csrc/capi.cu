@@ -1,0 +1,160 @@
+// extern "C" entry points of libkunlun_sm100a.so: argument validation,
+// error reporting, and dispatch between the tcgen05 (bf16) and SIMT paths.
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <atomic>
+
+#include "common.cuh"
+#include "gemm.h"
+#include "swa.h"
+
+namespace kl {
+
+static thread_local char g_err[512] = "";
+static std::atomic<unsigned long long> g_launches{0};
+static int g_gemm_path = 0;  // 0 auto, 1 force SIMT, 2 force tcgen05 (error if unsupported)
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int launch_check(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("%s: %s", what, cudaGetErrorString(e));
+    return KL_ELAUNCH;
+  }
+  return KL_OK;
+}
+
+void count_launch(unsigned n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+int gemm_path() { return g_gemm_path; }
+
+}  // namespace kl
+
+using namespace kl;
+
+extern "C" int kl_version(void) { return 1; }
+extern "C" const char* kl_last_error(void) { return g_err; }
+extern "C" unsigned long long kl_launch_count(void) { return g_launches.load(); }
+extern "C" void kl_set_gemm_path(int path) { g_gemm_path = path; }
+
+extern "C" int kl_tcgen05_available(void) {
+  int dev = 0, major = 0, minor = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  return (major == 10 && minor == 0) ? 1 : 0;
+}
+
+extern "C" int kl_gemm(const kl_gemm_args* a, void* stream) {
+  if (!a) {
+    set_error("kl_gemm: null args");
+    return KL_EBADSHAPE;
+  }
+  if (a->M < 0 || a->N < 0 || a->K < 0 || a->nb1 < 1 || a->nb2 < 1) {
+    set_error("kl_gemm: bad extents M=%d N=%d K=%d nb=(%d,%d)", a->M, a->N, a->K, a->nb1, a->nb2);
+    return KL_EBADSHAPE;
+  }
+  if ((a->ab_dtype != KL_F32 && a->ab_dtype != KL_BF16) || (a->c_dtype != KL_F32 && a->c_dtype != KL_BF16)) {
+    set_error("kl_gemm: bad dtype");
+    return KL_EUNSUPPORTED;
+  }
+  if (a->n_act < 0 || a->n_act > KL_MAX_ACT_GROUPS || (a->n_act > 1 && a->act_group < 1)) {
+    set_error("kl_gemm: bad activation groups (%d, %d)", a->n_act, a->act_group);
+    return KL_EBADSHAPE;
+  }
+  if (a->aux_mode && !a->aux) {
+    set_error("kl_gemm: aux_mode %d without aux buffer", a->aux_mode);
+    return KL_EBADSHAPE;
+  }
+  if (a->row_limit && a->red1) {
+    set_error("kl_gemm: row_limit needs a non-reduced first batch dim");
+    return KL_EBADSHAPE;
+  }
+  if (a->M == 0 || a->N == 0) return KL_OK;
+  GemmDesc g;
+  g.M = a->M; g.N = a->N; g.K = a->K;
+  g.nb1 = a->nb1; g.nb2 = a->nb2; g.red1 = a->red1; g.red2 = a->red2;
+  g.ab_dtype = a->ab_dtype; g.c_dtype = a->c_dtype;
+  g.A = a->A; g.a_rs = a->a_rs; g.a_cs = a->a_cs; g.a_s1 = a->a_s1; g.a_s2 = a->a_s2;
+  g.B = a->B; g.b_rs = a->b_rs; g.b_cs = a->b_cs; g.b_s1 = a->b_s1; g.b_s2 = a->b_s2;
+  g.C = a->C; g.c_rs = a->c_rs; g.c_cs = a->c_cs; g.c_s1 = a->c_s1; g.c_s2 = a->c_s2;
+  g.R = a->R; g.r_rs = a->r_rs; g.r_cs = a->r_cs; g.r_s1 = a->r_s1; g.r_s2 = a->r_s2;
+  g.aux = a->aux;
+  Epi e;
+  e.alpha = a->alpha; e.beta = a->beta; e.bias = a->bias; e.row_limit = a->row_limit;
+  e.aux_mode = a->aux_mode; e.n_act = a->n_act; e.act_group = a->act_group > 0 ? a->act_group : 1;
+  for (int i = 0; i < KL_MAX_ACT_GROUPS; ++i) e.act_codes[i] = a->act_codes[i];
+  cudaStream_t s = (cudaStream_t)stream;
+  if (a->ab_dtype == KL_BF16 && g_gemm_path != 1) {
+    int rc = gemm_tc(g, e, s);
+    if (rc != KL_EUNSUPPORTED) return rc;
+    if (g_gemm_path == 2) {
+      set_error("kl_gemm: tcgen05 path forced but shape unsupported (M=%d N=%d K=%d)", a->M, a->N, a->K);
+      return KL_EUNSUPPORTED;
+    }
+  }
+  return gemm_simt(g, e, s);
+}
+
+static int swa_validate(const kl_swa_args* a, const char* who, SwaP& p) {
+  if (!a || a->B < 0 || a->T < 0 || a->H < 1 || a->d_h < 1 || a->w < 0) {
+    set_error("%s: bad extents", who);
+    return KL_EBADSHAPE;
+  }
+  if (a->dtype != KL_F32 && a->dtype != KL_BF16) {
+    set_error("%s: bad dtype", who);
+    return KL_EUNSUPPORTED;
+  }
+  p.B = a->B; p.T = a->T; p.H = a->H; p.d_h = a->d_h; p.w = a->w; p.causal = a->causal; p.dtype = a->dtype;
+  p.scale = a->scale; p.lengths = a->lengths;
+  p.QKV = a->QKV; p.ld_qkv = a->ld_qkv; p.bs_qkv = a->bs_qkv;
+  p.O = a->O; p.ld_o = a->ld_o; p.bs_o = a->bs_o; p.LSE = a->LSE;
+  p.dO = a->dO; p.dQKV = a->dQKV; p.Dbuf = a->Dbuf;
+  return KL_OK;
+}
+
+extern "C" int kl_swa_fwd(const kl_swa_args* a, void* stream) {
+  SwaP p;
+  int rc = swa_validate(a, "kl_swa_fwd", p);
+  if (rc) return rc;
+  if (p.B == 0 || p.T == 0) return KL_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (p.dtype == KL_BF16 && g_gemm_path != 1) {
+    rc = swa_fwd_tc(p, s);
+    if (rc != KL_EUNSUPPORTED) return rc;
+  }
+  return swa_fwd_simt(p, s);
+}
+
+extern "C" int kl_swa_bwd(const kl_swa_args* a, void* stream) {
+  SwaP p;
+  int rc = swa_validate(a, "kl_swa_bwd", p);
+  if (rc) return rc;
+  if (p.B == 0 || p.T == 0) return KL_OK;
+  if (!p.dO || !p.dQKV || !p.Dbuf || !p.LSE) {
+    set_error("kl_swa_bwd: dO, dQKV, Dbuf and LSE are required");
+    return KL_EBADSHAPE;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  if (p.dtype == KL_BF16 && g_gemm_path != 1) {
+    rc = swa_bwd_tc(p, s);
+    if (rc != KL_EUNSUPPORTED) return rc;
+  }
+  return swa_bwd_simt(p, s);
+}
+
+extern "C" int kl_swa_debug_support(const kl_swa_args* a, int* support, void* stream) {
+  SwaP p;
+  int rc = swa_validate(a, "kl_swa_debug_support", p);
+  if (rc) return rc;
+  if (p.B == 0 || p.T == 0) return KL_OK;
+  return swa_support(p, support, (cudaStream_t)stream);
+}

@@ -1,0 +1,487 @@
+// Small-dimension glue kernels of the Kunlun layer (HBM / latency bound):
+// column softmax for HSP/PMA pooling, RMSNorm, recent rows, Wukong
+// pairwise-dot (gram + triu), gated expert residual, BCE, casts, activation,
+// non-finite scan.  Each cites the reference op it reproduces.
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace kl {
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// Column softmax over rows t < len (queries are columns):
+// masked_softmax_lastdim (tensor.py:485-505) applied to the transposed HSP/PMA
+// score block of multi_head_attention (attention.py:89-91).
+template <typename TI, typename TO>
+__global__ void __launch_bounds__(256) colsoftmax_fwd_kernel(kl_colsoftmax_args a) {
+  __shared__ float red[8][33];
+  const int b = blockIdx.y;
+  const int cl = threadIdx.x & 31, rg = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + cl;
+  const int len = a.lengths[b];
+  const TI* X = (const TI*)a.X + (long long)b * a.x_bs;
+  TO* P = (TO*)a.P + (long long)b * a.p_bs;
+  float m = -INFINITY;
+  if (c < a.C)
+    for (int t = rg; t < len; t += 8) m = fmaxf(m, ldf(X + (long long)t * a.x_rs + c));
+  red[rg][cl] = m;
+  __syncthreads();
+  m = red[0][cl];
+#pragma unroll
+  for (int i = 1; i < 8; ++i) m = fmaxf(m, red[i][cl]);
+  __syncthreads();
+  float ssum = 0.f;
+  if (c < a.C)
+    for (int t = rg; t < len; t += 8) ssum += expf(ldf(X + (long long)t * a.x_rs + c) - m);
+  red[rg][cl] = ssum;
+  __syncthreads();
+  ssum = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) ssum += red[i][cl];
+  if (c >= a.C) return;
+  const float inv = ssum > 0.f ? 1.f / ssum : 0.f;
+  for (int t = rg; t < a.T; t += 8) {
+    float v = t < len ? expf(ldf(X + (long long)t * a.x_rs + c) - m) * inv : 0.f;
+    stf(P + (long long)t * a.p_rs + c, v);
+  }
+  if (rg == 0 && a.LSE) a.LSE[(long long)b * a.C + c] = len > 0 ? m + logf(ssum) : INFINITY;
+}
+
+// dX = P * (dP - sum_t P dP)   (tensor.py:501-503)
+template <typename TP, typename TG, typename TO>
+__global__ void __launch_bounds__(256) colsoftmax_bwd_kernel(kl_colsoftmax_args a) {
+  __shared__ float red[8][33];
+  const int b = blockIdx.y;
+  const int cl = threadIdx.x & 31, rg = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + cl;
+  const int len = a.lengths[b];
+  const TP* P = (const TP*)a.P + (long long)b * a.p_bs;
+  const TG* G = (const TG*)a.dP + (long long)b * a.dp_bs;
+  TO* D = (TO*)a.dX + (long long)b * a.dx_bs;
+  float acc = 0.f;
+  if (c < a.C)
+    for (int t = rg; t < len; t += 8) acc += ldf(P + (long long)t * a.p_rs + c) * ldf(G + (long long)t * a.dp_rs + c);
+  red[rg][cl] = acc;
+  __syncthreads();
+  acc = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc += red[i][cl];
+  if (c >= a.C) return;
+  for (int t = rg; t < a.T; t += 8) {
+    float v = 0.f;
+    if (t < len) {
+      float pr = ldf(P + (long long)t * a.p_rs + c);
+      v = pr * (ldf(G + (long long)t * a.dp_rs + c) - acc);
+    }
+    stf(D + (long long)t * a.dx_rs + c, v);
+  }
+}
+
+// ---------------------------------------------------------------------------
+__device__ float block_sum(float v, float* sh) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  float t = 0.f;
+  const int nw = blockDim.x >> 5;
+  for (int i = 0; i < nw; ++i) t += sh[i];
+  return t;
+}
+
+// rms_norm (tensor.py:552-556): one block per row.
+__global__ void rmsnorm_fwd_kernel(int d, float eps, const float* x, const float* gain, float* y) {
+  __shared__ float sh[32];
+  const float* xr = x + (long long)blockIdx.x * d;
+  float ss = 0.f;
+  for (int c = threadIdx.x; c < d; c += blockDim.x) ss += xr[c] * xr[c];
+  ss = block_sum(ss, sh);
+  const float s = 1.f / sqrtf(ss / d + eps);
+  for (int c = threadIdx.x; c < d; c += blockDim.x) y[(long long)blockIdx.x * d + c] = xr[c] * s * gain[c];
+}
+
+// Single block: dx = s*gg - s^3/d * x * sum(gg*x), gg = dy*gain; dgain = sum_rows dy*x*s.
+__global__ void rmsnorm_bwd_kernel(int rows, int d, float eps, const float* x, const float* gain,
+                                   const float* dy, float* dx, float* dgain) {
+  __shared__ float sh[32];
+  for (int c = threadIdx.x; c < d; c += blockDim.x) dgain[c] = 0.f;
+  for (int r = 0; r < rows; ++r) {
+    const float* xr = x + (long long)r * d;
+    const float* gr = dy + (long long)r * d;
+    float ss = 0.f, gx = 0.f;
+    for (int c = threadIdx.x; c < d; c += blockDim.x) {
+      ss += xr[c] * xr[c];
+      gx += gr[c] * gain[c] * xr[c];
+    }
+    ss = block_sum(ss, sh);
+    gx = block_sum(gx, sh);
+    const float s = 1.f / sqrtf(ss / d + eps);
+    const float k = s * s * s / d * gx;
+    for (int c = threadIdx.x; c < d; c += blockDim.x) {
+      dx[(long long)r * d + c] = s * gr[c] * gain[c] - k * xr[c];
+      dgain[c] += gr[c] * xr[c] * s;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// recent_rows (seqsum.py:186-196)
+template <typename T>
+__global__ void recent_fwd_kernel(int B, int T_, int d, int n, const T* S, long long s_bs, const int* lengths,
+                                  T* out, long long o_bs) {
+  long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)B * n * d) return;
+  int c = idx % d, r = (idx / d) % n, b = idx / ((long long)d * n);
+  int t = lengths[b] - n + r;
+  float v = t >= 0 ? ldf(S + (long long)b * s_bs + (long long)t * d + c) : 0.f;
+  stf(out + (long long)b * o_bs + (long long)r * d + c, v);
+}
+
+template <typename T>
+__global__ void recent_bwd_kernel(int B, int T_, int d, int n, const T* dout, long long o_bs, const int* lengths,
+                                  T* dS, long long s_bs) {
+  long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)B * n * d) return;
+  int c = idx % d, r = (idx / d) % n, b = idx / ((long long)d * n);
+  int t = lengths[b] - n + r;
+  if (t < 0) return;
+  T* p = dS + (long long)b * s_bs + (long long)t * d + c;
+  stf(p, ldf(p) + ldf(dout + (long long)b * o_bs + (long long)r * d + c));
+}
+
+// ---------------------------------------------------------------------------
+// triu_flatten(x x^T) (interaction.py:63-76, 117): np.triu_indices row-major.
+__device__ __forceinline__ int triu_index(int r, int c, int n) { return r * n - r * (r - 1) / 2 + (c - r); }
+
+template <typename T>
+__global__ void gram_triu_fwd_kernel(int B, int n, int d, const T* x, long long x_rs, long long x_bs, T* tri,
+                                     long long t_bs) {
+  const int np_ = n * (n + 1) / 2;
+  long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)B * np_) return;
+  int pidx = idx % np_, b = idx / np_;
+  int r = 0;
+  while (triu_index(r + 1, r + 1, n) <= pidx && r + 1 < n) ++r;
+  int c = r + (pidx - triu_index(r, r, n));
+  const T* xr = x + (long long)b * x_bs + (long long)r * x_rs;
+  const T* xc = x + (long long)b * x_bs + (long long)c * x_rs;
+  float acc = 0.f;
+  for (int k = 0; k < d; ++k) acc = fmaf(ldf(xr + k), ldf(xc + k), acc);
+  stf(tri + (long long)b * t_bs + pidx, acc);
+}
+
+template <typename T>
+__global__ void gram_triu_bwd_kernel(int B, int n, int d, const T* x, long long x_rs, long long x_bs,
+                                     const T* dtri, long long t_bs, T* dx, long long dx_rs, long long dx_bs) {
+  long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)B * n * d) return;
+  int k = idx % d, r = (idx / d) % n, b = idx / ((long long)d * n);
+  const T* xb = x + (long long)b * x_bs;
+  const T* db = dtri + (long long)b * t_bs;
+  float acc = 0.f;
+  for (int j = 0; j < n; ++j) {
+    int lo = min(r, j), hi = max(r, j);
+    float wgt = ldf(db + triu_index(lo, hi, n)) * (r == j ? 2.f : 1.f);
+    acc = fmaf(wgt, ldf(xb + (long long)j * x_rs + k), acc);
+  }
+  T* p = dx + (long long)b * dx_bs + (long long)r * dx_rs + k;
+  stf(p, ldf(p) + acc);
+}
+
+// ---------------------------------------------------------------------------
+// wukong_expert residual: x + gate_deep*deep + gate_dot*dot (interaction.py:121)
+template <typename T>
+__global__ void gated_fwd_kernel(int rows, int d, const T* x, long long x_rs, const T* deep, const T* dot,
+                                 const float* gd, const float* gt, T* out, long long o_rs) {
+  long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)rows * d) return;
+  int c = idx % d;
+  long long r = idx / d;
+  float v = ldf(x + r * x_rs + c) + gd[0] * ldf(deep + idx) + gt[0] * ldf(dot + idx);
+  stf(out + r * o_rs + c, v);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) gated_bwd_kernel(int rows, int d, const T* g, long long g_rs, const T* deep,
+                                                        const T* dot, const float* gd, const float* gt, T* ddeep,
+                                                        T* ddot, float* partial) {
+  __shared__ float sh[32];
+  float a = 0.f, b = 0.f;
+  const long long total = (long long)rows * d;
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    int c = idx % d;
+    long long r = idx / d;
+    float gv = ldf(g + r * g_rs + c);
+    a += gv * ldf(deep + idx);
+    b += gv * ldf(dot + idx);
+    stf(ddeep + idx, gv * gd[0]);
+    stf(ddot + idx, gv * gt[0]);
+  }
+  a = block_sum(a, sh);
+  b = block_sum(b, sh);
+  if (threadIdx.x == 0) {
+    partial[2 * blockIdx.x] = a;
+    partial[2 * blockIdx.x + 1] = b;
+  }
+}
+
+__global__ void reduce_pairs_kernel(int nblk, const float* partial, float* o0, float* o1) {
+  __shared__ float sh[32];
+  float a = 0.f, b = 0.f;
+  for (int i = threadIdx.x; i < nblk; i += blockDim.x) {
+    a += partial[2 * i];
+    b += partial[2 * i + 1];
+  }
+  a = block_sum(a, sh);
+  b = block_sum(b, sh);
+  if (threadIdx.x == 0) {
+    o0[0] = a;
+    o1[0] = b;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// bce_with_logits (tensor.py:535-549)
+__global__ void bce_kernel(int n, const float* z, const float* y, float* loss, float* dz) {
+  __shared__ float sh[32];
+  float acc = 0.f;
+  const float inv = 1.f / (float)max(n, 1);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    float zi = z[i], yi = y[i];
+    acc += fmaxf(zi, 0.f) - yi * zi + log1pf(expf(-fabsf(zi)));
+    dz[i] = (sigmoidf_(zi) - yi) * inv;
+  }
+  acc = block_sum(acc, sh);
+  if (threadIdx.x == 0) loss[0] = acc * inv;
+}
+
+template <typename TI, typename TO>
+__global__ void cast_kernel(long long n, const TI* x, TO* y) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    stf(y + i, ldf(x + i));
+}
+
+struct ActCodes {
+  int n_act, group;
+  int codes[KL_MAX_ACT_GROUPS];
+};
+
+template <typename T>
+__global__ void act_kernel(int rows, int cols, const T* x, long long ld, T* y, long long ld_y, ActCodes ac) {
+  long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)rows * cols) return;
+  int c = idx % cols;
+  long long r = idx / cols;
+  int code = ac.n_act == 0 ? 0 : ac.codes[(c / ac.group) % ac.n_act];
+  stf(y + r * ld_y + c, act_apply(code, ldf(x + r * ld + c)));
+}
+
+template <typename T>
+__global__ void act_bwd_kernel(int rows, int cols, const T* g, long long ldg, const T* x, long long ldx, T* y,
+                               long long ld_y, ActCodes ac) {
+  long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)rows * cols) return;
+  int c = idx % cols;
+  long long r = idx / cols;
+  int code = ac.n_act == 0 ? 0 : ac.codes[(c / ac.group) % ac.n_act];
+  stf(y + r * ld_y + c, ldf(g + r * ldg + c) * act_deriv(code, ldf(x + r * ldx + c)));
+}
+
+template <typename T>
+__global__ void finite_kernel(long long n, const T* x, unsigned int* flag) {
+  bool bad = false;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    bad |= !isfinite(ldf(x + i));
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
+}
+
+inline unsigned nblk(long long n, int t = 256) { return (unsigned)((n + t - 1) / t); }
+
+}  // namespace
+
+}  // namespace kl
+
+using namespace kl;
+
+extern "C" int kl_colsoftmax_fwd(const kl_colsoftmax_args* a, void* stream) {
+  if (!a || a->Bn < 0 || a->T < 0 || a->C < 0) { set_error("kl_colsoftmax_fwd: bad args"); return KL_EBADSHAPE; }
+  if (a->Bn == 0 || a->C == 0 || a->T == 0) return KL_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  dim3 grid((a->C + 31) / 32, a->Bn);
+  if (a->dtype_in == KL_F32 && a->dtype_out == KL_F32) colsoftmax_fwd_kernel<float, float><<<grid, 256, 0, s>>>(*a);
+  else if (a->dtype_in == KL_F32) colsoftmax_fwd_kernel<float, bf16><<<grid, 256, 0, s>>>(*a);
+  else if (a->dtype_out == KL_F32) colsoftmax_fwd_kernel<bf16, float><<<grid, 256, 0, s>>>(*a);
+  else colsoftmax_fwd_kernel<bf16, bf16><<<grid, 256, 0, s>>>(*a);
+  count_launch();
+  return launch_check("colsoftmax_fwd");
+}
+
+extern "C" int kl_colsoftmax_bwd(const kl_colsoftmax_args* a, void* stream) {
+  if (!a) { set_error("kl_colsoftmax_bwd: null args"); return KL_EBADSHAPE; }
+  if (a->Bn == 0 || a->C == 0 || a->T == 0) return KL_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  dim3 grid((a->C + 31) / 32, a->Bn);
+  // P and dP share dtype_out's storage type; dX uses dtype_in's
+  if (a->dtype_out == KL_F32 && a->dtype_in == KL_F32) colsoftmax_bwd_kernel<float, float, float><<<grid, 256, 0, s>>>(*a);
+  else if (a->dtype_out == KL_F32) colsoftmax_bwd_kernel<float, float, bf16><<<grid, 256, 0, s>>>(*a);
+  else if (a->dtype_in == KL_F32) colsoftmax_bwd_kernel<bf16, bf16, float><<<grid, 256, 0, s>>>(*a);
+  else colsoftmax_bwd_kernel<bf16, bf16, bf16><<<grid, 256, 0, s>>>(*a);
+  count_launch();
+  return launch_check("colsoftmax_bwd");
+}
+
+extern "C" int kl_rmsnorm_fwd(int rows, int d, float eps, const float* x, const float* gain, float* y, void* stream) {
+  if (rows <= 0 || d <= 0) return KL_OK;
+  rmsnorm_fwd_kernel<<<rows, 256, 0, (cudaStream_t)stream>>>(d, eps, x, gain, y);
+  count_launch();
+  return launch_check("rmsnorm_fwd");
+}
+
+extern "C" int kl_rmsnorm_bwd(int rows, int d, float eps, const float* x, const float* gain, const float* dy,
+                              float* dx, float* dgain, void* stream) {
+  if (d <= 0) return KL_OK;
+  rmsnorm_bwd_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(rows, d, eps, x, gain, dy, dx, dgain);
+  count_launch();
+  return launch_check("rmsnorm_bwd");
+}
+
+extern "C" int kl_recent_rows_fwd(int B, int T, int d, int n, int dtype, const void* S, long long s_bs,
+                                  const int* lengths, void* out, long long o_bs, void* stream) {
+  long long tot = (long long)B * n * d;
+  if (tot == 0) return KL_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == KL_F32) recent_fwd_kernel<float><<<nblk(tot), 256, 0, s>>>(B, T, d, n, (const float*)S, s_bs, lengths, (float*)out, o_bs);
+  else recent_fwd_kernel<bf16><<<nblk(tot), 256, 0, s>>>(B, T, d, n, (const bf16*)S, s_bs, lengths, (bf16*)out, o_bs);
+  count_launch();
+  return launch_check("recent_rows_fwd");
+}
+
+extern "C" int kl_recent_rows_bwd(int B, int T, int d, int n, int dtype, const void* dout, long long o_bs,
+                                  const int* lengths, void* dS, long long s_bs, void* stream) {
+  long long tot = (long long)B * n * d;
+  if (tot == 0) return KL_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == KL_F32) recent_bwd_kernel<float><<<nblk(tot), 256, 0, s>>>(B, T, d, n, (const float*)dout, o_bs, lengths, (float*)dS, s_bs);
+  else recent_bwd_kernel<bf16><<<nblk(tot), 256, 0, s>>>(B, T, d, n, (const bf16*)dout, o_bs, lengths, (bf16*)dS, s_bs);
+  count_launch();
+  return launch_check("recent_rows_bwd");
+}
+
+extern "C" int kl_gram_triu_fwd(int B, int n, int d, int dtype, const void* x, long long x_rs, long long x_bs,
+                                void* tri, long long t_bs, void* stream) {
+  long long tot = (long long)B * n * (n + 1) / 2;
+  if (tot == 0) return KL_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == KL_F32) gram_triu_fwd_kernel<float><<<nblk(tot), 256, 0, s>>>(B, n, d, (const float*)x, x_rs, x_bs, (float*)tri, t_bs);
+  else gram_triu_fwd_kernel<bf16><<<nblk(tot), 256, 0, s>>>(B, n, d, (const bf16*)x, x_rs, x_bs, (bf16*)tri, t_bs);
+  count_launch();
+  return launch_check("gram_triu_fwd");
+}
+
+extern "C" int kl_gram_triu_bwd(int B, int n, int d, int dtype, const void* x, long long x_rs, long long x_bs,
+                                const void* dtri, long long t_bs, void* dx, long long dx_rs, long long dx_bs,
+                                void* stream) {
+  long long tot = (long long)B * n * d;
+  if (tot == 0) return KL_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == KL_F32)
+    gram_triu_bwd_kernel<float><<<nblk(tot), 256, 0, s>>>(B, n, d, (const float*)x, x_rs, x_bs, (const float*)dtri, t_bs, (float*)dx, dx_rs, dx_bs);
+  else
+    gram_triu_bwd_kernel<bf16><<<nblk(tot), 256, 0, s>>>(B, n, d, (const bf16*)x, x_rs, x_bs, (const bf16*)dtri, t_bs, (bf16*)dx, dx_rs, dx_bs);
+  count_launch();
+  return launch_check("gram_triu_bwd");
+}
+
+extern "C" int kl_gated_sum_fwd(int rows, int d, int dtype, const void* x, long long x_rs, const void* deep,
+                                const void* dot, const float* gd, const float* gt, void* out, long long o_rs,
+                                void* stream) {
+  long long tot = (long long)rows * d;
+  if (tot == 0) return KL_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == KL_F32)
+    gated_fwd_kernel<float><<<nblk(tot), 256, 0, s>>>(rows, d, (const float*)x, x_rs, (const float*)deep, (const float*)dot, gd, gt, (float*)out, o_rs);
+  else
+    gated_fwd_kernel<bf16><<<nblk(tot), 256, 0, s>>>(rows, d, (const bf16*)x, x_rs, (const bf16*)deep, (const bf16*)dot, gd, gt, (bf16*)out, o_rs);
+  count_launch();
+  return launch_check("gated_sum_fwd");
+}
+
+extern "C" int kl_gated_sum_bwd(int rows, int d, int dtype, const void* g, long long g_rs, const void* deep,
+                                const void* dot, const float* gd, const float* gt, void* ddeep, void* ddot,
+                                float* dgd, float* dgt, float* scratch, void* stream) {
+  long long tot = (long long)rows * d;
+  cudaStream_t s = (cudaStream_t)stream;
+  int nb = (int)std::min<long long>(512, (tot + 255) / 256);
+  if (nb < 1) nb = 1;
+  if (dtype == KL_F32)
+    gated_bwd_kernel<float><<<nb, 256, 0, s>>>(rows, d, (const float*)g, g_rs, (const float*)deep, (const float*)dot, gd, gt, (float*)ddeep, (float*)ddot, scratch);
+  else
+    gated_bwd_kernel<bf16><<<nb, 256, 0, s>>>(rows, d, (const bf16*)g, g_rs, (const bf16*)deep, (const bf16*)dot, gd, gt, (bf16*)ddeep, (bf16*)ddot, scratch);
+  reduce_pairs_kernel<<<1, 256, 0, s>>>(nb, scratch, dgd, dgt);
+  count_launch(2);
+  return launch_check("gated_sum_bwd");
+}
+
+extern "C" int kl_bce_fwd_bwd(int n, const float* z, const float* y, float* loss, float* dz, void* stream) {
+  bce_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(n, z, y, loss, dz);
+  count_launch();
+  return launch_check("bce");
+}
+
+extern "C" int kl_cast(long long n, int dtype_in, const void* x, int dtype_out, void* y, void* stream) {
+  if (n == 0) return KL_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  unsigned g = (unsigned)std::min<long long>((n + 255) / 256, 148 * 16);
+  if (dtype_in == KL_F32 && dtype_out == KL_BF16) cast_kernel<float, bf16><<<g, 256, 0, s>>>(n, (const float*)x, (bf16*)y);
+  else if (dtype_in == KL_BF16 && dtype_out == KL_F32) cast_kernel<bf16, float><<<g, 256, 0, s>>>(n, (const bf16*)x, (float*)y);
+  else if (dtype_in == KL_F32) cast_kernel<float, float><<<g, 256, 0, s>>>(n, (const float*)x, (float*)y);
+  else cast_kernel<bf16, bf16><<<g, 256, 0, s>>>(n, (const bf16*)x, (bf16*)y);
+  count_launch();
+  return launch_check("cast");
+}
+
+extern "C" int kl_act_fwd(int rows, int cols, int dtype, const void* x, long long ld, void* y, long long ld_y,
+                          int n_act, int act_group, const int* codes, void* stream) {
+  long long tot = (long long)rows * cols;
+  if (tot == 0) return KL_OK;
+  if (n_act < 0 || n_act > KL_MAX_ACT_GROUPS) { set_error("kl_act_fwd: n_act %d", n_act); return KL_EBADSHAPE; }
+  ActCodes ac{};
+  ac.n_act = n_act;
+  ac.group = act_group > 0 ? act_group : 1;
+  for (int i = 0; i < n_act; ++i) ac.codes[i] = codes[i];
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == KL_F32) act_kernel<float><<<nblk(tot), 256, 0, s>>>(rows, cols, (const float*)x, ld, (float*)y, ld_y, ac);
+  else act_kernel<bf16><<<nblk(tot), 256, 0, s>>>(rows, cols, (const bf16*)x, ld, (bf16*)y, ld_y, ac);
+  count_launch();
+  return launch_check("act_fwd");
+}
+
+extern "C" int kl_act_bwd(int rows, int cols, int dtype, const void* g, long long ldg, const void* x, long long ldx,
+                          void* y, long long ld_y, int n_act, int act_group, const int* codes, void* stream) {
+  long long tot = (long long)rows * cols;
+  if (tot == 0) return KL_OK;
+  if (n_act < 0 || n_act > KL_MAX_ACT_GROUPS) { set_error("kl_act_bwd: n_act %d", n_act); return KL_EBADSHAPE; }
+  ActCodes ac{};
+  ac.n_act = n_act;
+  ac.group = act_group > 0 ? act_group : 1;
+  for (int i = 0; i < n_act; ++i) ac.codes[i] = codes[i];
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == KL_F32) act_bwd_kernel<float><<<nblk(tot), 256, 0, s>>>(rows, cols, (const float*)g, ldg, (const float*)x, ldx, (float*)y, ld_y, ac);
+  else act_bwd_kernel<bf16><<<nblk(tot), 256, 0, s>>>(rows, cols, (const bf16*)g, ldg, (const bf16*)x, ldx, (bf16*)y, ld_y, ac);
+  count_launch();
+  return launch_check("act_bwd");
+}
+
+extern "C" int kl_check_finite(long long n, int dtype, const void* x, unsigned int* flag, void* stream) {
+  if (n == 0) return KL_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  unsigned g = (unsigned)std::min<long long>((n + 255) / 256, 148 * 8);
+  if (dtype == KL_F32) finite_kernel<float><<<g, 256, 0, s>>>(n, (const float*)x, flag);
+  else finite_kernel<bf16><<<g, 256, 0, s>>>(n, (const bf16*)x, flag);
+  count_launch();
+  return launch_check("check_finite");
+}

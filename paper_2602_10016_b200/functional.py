@@ -1,0 +1,543 @@
+"""Differentiable device ops of the Kunlun hot path.
+
+Each ``torch.autograd.Function`` here is the B200 analogue of the reference's
+``record(out, parents, vjp)`` plugin hook (tensor.py:185-195): forward and
+VJP both run hand-written sm_100a kernels from libkunlun_sm100a.so via the C
+ABI (``_capi``).  There is no CPU or library fallback.
+
+Parameters are not autograd leaves one by one: they live in the flat
+``Params`` buffer, kernels read the compute-dtype mirror and the backward
+kernels *accumulate* fp32 weight gradients straight into ``Params.gflat``
+(beta=1 epilogues).  Every parameter-consuming Function takes
+``Params.flat`` (requires_grad) as a dummy input so autograd always runs its
+backward.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _capi
+from ._capi import gemm
+from .tensor import ACTIVATIONS, ShapeError
+
+
+class PRef:
+    """A parameter operand: block ``key`` of ``P`` seen through ``fn``."""
+
+    __slots__ = ("P", "key", "fn")
+
+    def __init__(self, P, key, fn=None):
+        self.P, self.key, self.fn = P, key, fn
+
+    def w(self):
+        v = self.P.w(self.key)
+        return self.fn(v) if self.fn else v
+
+    def g(self):
+        v = self.P.g(self.key)
+        return self.fn(v) if self.fn else v
+
+
+def _codes(acts):
+    if acts is None:
+        return []
+    if isinstance(acts, str):
+        acts = [acts]
+    return [ACTIVATIONS[a] for a in acts]
+
+
+def _stream():
+    return _capi._stream()
+
+
+def _as4(t):
+    while t.dim() < 4:
+        t = t.unsqueeze(0)
+    return t
+
+
+def _bcast_reduce(op4, out4):
+    """Batch dims where an operand was broadcast against the output."""
+    return (op4.shape[0] == 1 and out4.shape[0] > 1, op4.shape[1] == 1 and out4.shape[1] > 1)
+
+
+# ---------------------------------------------------------------------------
+class _MM(torch.autograd.Function):
+    """C = alpha * A @ B (+ residual) over up to two broadcast batch dims,
+    optionally summing batch dims (``reduce``).  Operands are tensors or
+    parameter references.  VJP: dA = g B^T, dB = A^T g (tensor.py:283-289),
+    reducing over batch dims where an operand was broadcast."""
+
+    @staticmethod
+    def forward(ctx, a, b, flat, aref, bref, reduce, alpha, residual):
+        A = aref.w() if aref is not None else a
+        Bm = bref.w() if bref is not None else b
+        out = gemm(A, Bm, alpha=alpha, reduce=reduce, residual=residual)
+        ctx.aref, ctx.bref, ctx.alpha = aref, bref, alpha
+        ctx.has_res = residual is not None
+        ctx.save_for_backward(a if aref is None else None, b if bref is None else None)
+        ctx.ashape = tuple(A.shape)
+        ctx.bshape = tuple(Bm.shape)
+        return out
+
+    @staticmethod
+    def backward(ctx, g):
+        a_t, b_t = ctx.saved_tensors
+        A = ctx.aref.w() if ctx.aref is not None else a_t
+        Bm = ctx.bref.w() if ctx.bref is not None else b_t
+        g4 = _as4(g)
+        nb = (max(_as4(A).shape[0], _as4(Bm).shape[0]), max(_as4(A).shape[1], _as4(Bm).shape[1]))
+        g4 = g4.expand(nb[0], nb[1], g4.shape[2], g4.shape[3])
+        da = db = None
+        A4, B4 = _as4(A), _as4(Bm)
+        if ctx.aref is not None or ctx.needs_input_grad[0]:
+            red = _bcast_reduce(A4, g4)
+            if ctx.aref is not None:
+                gemm(g4, B4.transpose(2, 3), _as4(ctx.aref.g()), alpha=ctx.alpha, beta=1.0, reduce=red)
+            else:
+                da = gemm(g4, B4.transpose(2, 3), alpha=ctx.alpha, reduce=red)
+                da = da.reshape(a_t.shape)
+        if ctx.bref is not None or ctx.needs_input_grad[1]:
+            red = _bcast_reduce(B4, g4)
+            if ctx.bref is not None:
+                gemm(A4.transpose(2, 3), g4, _as4(ctx.bref.g()), alpha=ctx.alpha, beta=1.0, reduce=red)
+            else:
+                db = gemm(A4.transpose(2, 3), g4, alpha=ctx.alpha, reduce=red)
+                db = db.reshape(b_t.shape)
+        dres = g if ctx.has_res else None
+        return da, db, None, None, None, None, None, dres
+
+
+def mm(a, b, P=None, *, reduce=(False, False), alpha=1.0, residual=None):
+    """Batched matmul of tensors / ``PRef`` parameters (see ``_MM``)."""
+    aref = a if isinstance(a, PRef) else None
+    bref = b if isinstance(b, PRef) else None
+    P = P or (aref.P if aref else (bref.P if bref else None))
+    flat = P.flat if P is not None else None
+    return _MM.apply(None if aref else a, None if bref else b, flat, aref, bref, tuple(reduce), float(alpha),
+                     residual)
+
+
+# ---------------------------------------------------------------------------
+class _Linear(torch.autograd.Function):
+    """y = act(x W^T + b) + residual; W (N, K) in the reference (out, in)
+    layout (mlp.py:47-59, attention projections).  Saves the pre-activation
+    (epilogue aux) for the VJP."""
+
+    @staticmethod
+    def forward(ctx, x, flat, P, wkey, bkey, act, residual):
+        W = P.w(wkey)
+        N = W.shape[0]
+        codes = _codes(act) if act and act != "identity" else []
+        pre = None
+        bias = P.w32(bkey) if bkey else None
+        x4 = x if x.dim() >= 2 else x.unsqueeze(0)
+        if codes:
+            pre = torch.empty(x4.shape[:-1] + (N,), device=x.device, dtype=x.dtype)
+        y = gemm(x4, W.t(), bias=bias, acts=codes or None, aux=pre, aux_mode=1 if codes else 0,
+                 residual=residual)
+        ctx.P, ctx.wkey, ctx.bkey, ctx.codes = P, wkey, bkey, codes
+        ctx.has_res = residual is not None
+        ctx.xshape = x.shape
+        ctx.save_for_backward(x4, pre)
+        return y if x.dim() >= 2 else y.squeeze(0)
+
+    @staticmethod
+    def backward(ctx, g):
+        x4, pre = ctx.saved_tensors
+        P = ctx.P
+        W = P.w(ctx.wkey)
+        g = g.contiguous()
+        if g.dim() < x4.dim():
+            g = g.unsqueeze(0)
+        gp = g
+        if ctx.codes:
+            gp = torch.empty_like(g)
+            cols = g.shape[-1]
+            rows = g.numel() // cols
+            codes = (C.c_int * len(ctx.codes))(*ctx.codes)
+            _capi.call("kl_act_bwd", rows, cols, _capi.dt(g), g.data_ptr(), cols, pre.data_ptr(), cols,
+                       gp.data_ptr(), cols, len(ctx.codes), 1, codes, _stream())
+        dx = None
+        if ctx.needs_input_grad[0]:
+            dx = gemm(gp, W)
+            dx = dx.reshape(ctx.xshape)
+        # dW = sum over rows (and batch dims) of gp^T x
+        gp4, x44 = _as4(gp), _as4(x4)
+        gemm(gp4.transpose(2, 3), x44, P.g(ctx.wkey), beta=1.0, reduce=(True, True))
+        if ctx.bkey:
+            rows = gp.numel() // gp.shape[-1]
+            ones = _ones(rows, gp.dtype, gp.device)
+            gemm(ones.view(1, rows), gp.reshape(rows, gp.shape[-1]) if gp.is_contiguous() else gp.contiguous().view(rows, -1),
+                 P.g(ctx.bkey).view(1, -1), beta=1.0)
+        dres = g.reshape(ctx.xshape[:-1] + (g.shape[-1],)) if ctx.has_res else None
+        return dx, None, None, None, None, None, dres
+
+
+_ONES = {}
+
+
+def _ones(n, dtype, device):
+    key = (dtype, device)
+    t = _ONES.get(key)
+    if t is None or t.numel() < n:
+        t = torch.ones(max(n, 1024), dtype=dtype, device=device)
+        _ONES[key] = t
+    return t[:n]
+
+
+def linear(x, P, wkey, bkey=None, act=None, residual=None):
+    return _Linear.apply(x, P.flat, P, wkey, bkey, act, residual)
+
+
+# ---------------------------------------------------------------------------
+class _GdpaCore(torch.autograd.Function):
+    """Folded GDPA core per sample (gdpa.py:120-187):
+        Z = S Kt^T / tau,  A = Act_h(Z) (per n_kv column block),
+        Y = S + A Vt;   rows >= length pass through (Y = S).
+    VJP: dZ = (G Vt^T) * Act'(Z) / tau, dS = G + dZ Kt, dKt = dZ^T S, dVt = A^T G."""
+
+    @staticmethod
+    def forward(ctx, S, Kt, Vt, lengths, codes, n_kv, inv_tau):
+        B, T, d = S.shape
+        HK = Kt.shape[1]
+        Z = torch.empty(B, T, HK, device=S.device, dtype=S.dtype)
+        A = torch.empty_like(Z)
+        gemm(S, Kt.transpose(1, 2), A, alpha=inv_tau, acts=codes, act_group=n_kv, aux=Z, aux_mode=1,
+             row_limit=lengths)
+        Y = gemm(A, Vt, residual=S)
+        ctx.save_for_backward(S, Kt, Vt, Z, A, lengths)
+        ctx.codes, ctx.n_kv, ctx.inv_tau = codes, n_kv, inv_tau
+        return Y
+
+    @staticmethod
+    def backward(ctx, g):
+        S, Kt, Vt, Z, A, lengths = ctx.saved_tensors
+        g = g.contiguous()
+        dZ = torch.empty_like(Z)
+        gemm(g, Vt.transpose(1, 2), dZ, alpha=ctx.inv_tau, acts=ctx.codes, act_group=ctx.n_kv, aux=Z, aux_mode=2,
+             row_limit=lengths)
+        dS = gemm(dZ, Kt, residual=g)
+        dKt = gemm(dZ.transpose(1, 2), S)
+        dVt = gemm(A.transpose(1, 2), g)
+        return dS, dKt, dVt, None, None, None, None
+
+
+def gdpa_core(S, Kt, Vt, lengths, acts, n_kv, inv_tau):
+    return _GdpaCore.apply(S, Kt, Vt, lengths, _codes(acts), int(n_kv), float(inv_tau))
+
+
+# ---------------------------------------------------------------------------
+class _SwaCore(torch.autograd.Function):
+    """Banded flash attention core (attention.py:69-129); QKV packed."""
+
+    @staticmethod
+    def forward(ctx, qkv, lengths, H, d_h, w, causal):
+        B, T, _ = qkv.shape
+        O = torch.empty(B, T, H * d_h, device=qkv.device, dtype=qkv.dtype)
+        LSE = torch.empty(B, H, T, device=qkv.device, dtype=torch.float32)
+        a = _capi.swa_args(qkv, lengths, H, d_h, w, causal, O, LSE)
+        _capi.call("kl_swa_fwd", C.byref(a), _stream())
+        ctx.save_for_backward(qkv, lengths, O, LSE)
+        ctx.cfg = (H, d_h, w, causal)
+        return O
+
+    @staticmethod
+    def backward(ctx, g):
+        qkv, lengths, O, LSE = ctx.saved_tensors
+        H, d_h, w, causal = ctx.cfg
+        g = g.contiguous()
+        dqkv = torch.empty_like(qkv)
+        Dbuf = torch.empty_like(LSE)
+        a = _capi.swa_args(qkv, lengths, H, d_h, w, causal, O, LSE, g, dqkv, Dbuf)
+        _capi.call("kl_swa_bwd", C.byref(a), _stream())
+        return dqkv, None, None, None, None, None
+
+
+def swa_core(qkv, lengths, H, d_h, w, causal=False):
+    if not qkv.is_contiguous():
+        qkv = qkv.contiguous()
+    return _SwaCore.apply(qkv, lengths, int(H), int(d_h), int(w), bool(causal))
+
+
+# ---------------------------------------------------------------------------
+def _colsm_args(X, P, lengths, LSE=None):
+    a = _capi.ColSoftmaxArgs()
+    a.Bn, a.T, a.C = X.shape[0], X.shape[1], X.shape[2]
+    a.dtype_in, a.dtype_out = _capi.dt(X), _capi.dt(P)
+    a.X, a.x_rs, a.x_bs = X.data_ptr(), X.stride(1), X.stride(0)
+    a.P, a.p_rs, a.p_bs = P.data_ptr(), P.stride(1), P.stride(0)
+    a.LSE = LSE.data_ptr() if LSE is not None else None
+    a.lengths = lengths.data_ptr()
+    return a
+
+
+class _HspPool(torch.autograd.Function):
+    """Seed/CLS-query cross-attention pooling with keys = values = S
+    (hsp_seed_attend / pma, seqsum.py:26-34, 96-102, reassociated as
+    P = softmax_t(S Q^T), pooled = P^T S — SURVEY.md §7.3 item 7).
+    Q (HQ, d) is batch-shared and pre-scaled by 1/sqrt(d_h).  Length-0
+    samples pool to zeros with no gradient (seqsum.py:32-33, 99-100)."""
+
+    @staticmethod
+    def forward(ctx, S, Q, lengths):
+        B, T, d = S.shape
+        HQ = Q.shape[0]
+        sc = gemm(S, Q.t(), out_dtype=torch.float32)  # (B, T, HQ)
+        Pm = torch.empty(B, T, HQ, device=S.device, dtype=S.dtype)
+        a = _colsm_args(sc, Pm, lengths)
+        _capi.call("kl_colsoftmax_fwd", C.byref(a), _stream())
+        pooled = gemm(Pm.transpose(1, 2), S)  # (B, HQ, d)
+        ctx.save_for_backward(S, Q, lengths, Pm)
+        return pooled
+
+    @staticmethod
+    def backward(ctx, g):
+        S, Q, lengths, Pm = ctx.saved_tensors
+        g = g.contiguous()
+        dP = gemm(S, g.transpose(1, 2), out_dtype=torch.float32)  # (B, T, HQ)
+        dsc = torch.empty_like(Pm)
+        a = _colsm_args(dsc, Pm, lengths)  # dtype_in = dsc dtype, dtype_out = P dtype
+        a.dP, a.dp_rs, a.dp_bs = dP.data_ptr(), dP.stride(1), dP.stride(0)
+        a.dX, a.dx_rs, a.dx_bs = dsc.data_ptr(), dsc.stride(1), dsc.stride(0)
+        if Pm.dtype == dP.dtype:
+            _capi.call("kl_colsoftmax_bwd", C.byref(a), _stream())
+        else:
+            _colsm_bwd_mixed(a, Pm, dP, dsc)
+        dS = gemm(Pm, g)
+        gemm(dsc, Q.unsqueeze(0).expand(S.shape[0], -1, -1), dS, beta=1.0)
+        dQ = gemm(dsc.transpose(1, 2).unsqueeze(0), S.unsqueeze(0), reduce=(False, True)).reshape(Q.shape)
+        return dS, dQ, None
+
+
+def _colsm_bwd_mixed(a, Pm, dP, dsc):
+    # dP is fp32 while P is bf16: convert dP to P's dtype is lossy; instead run
+    # the kernel in fp32 on an fp32 copy of P (P is a probability; exact in fp32).
+    P32 = torch.empty(Pm.shape, device=Pm.device, dtype=torch.float32)
+    _capi.call("kl_cast", Pm.numel(), _capi.dt(Pm), Pm.data_ptr(), _capi.KL_F32, P32.data_ptr(), _stream())
+    a.P, a.p_rs, a.p_bs = P32.data_ptr(), P32.stride(1), P32.stride(0)
+    a.dtype_out = _capi.KL_F32
+    a.dtype_in = _capi.dt(dsc)
+    _capi.call("kl_colsoftmax_bwd", C.byref(a), _stream())
+
+
+def hsp_pool(S, Q, lengths):
+    return _HspPool.apply(S, Q, lengths)
+
+
+# ---------------------------------------------------------------------------
+class _RmsNorm(torch.autograd.Function):
+    """rms_norm (tensor.py:552-556) on a batch-shared fp32 parameter block;
+    dgain is written straight into the gradient buffer."""
+
+    @staticmethod
+    def forward(ctx, flat, P, xkey, gkey, eps):
+        x = P.w32(xkey)
+        gain = P.w32(gkey)
+        rows, d = x.shape
+        y = torch.empty(rows, d, device=x.device, dtype=torch.float32)
+        _capi.call("kl_rmsnorm_fwd", rows, d, eps, x.data_ptr(), gain.data_ptr(), y.data_ptr(), _stream())
+        ctx.P, ctx.xkey, ctx.gkey, ctx.eps = P, xkey, gkey, eps
+        return y
+
+    @staticmethod
+    def backward(ctx, g):
+        P = ctx.P
+        x, gain = P.w32(ctx.xkey), P.w32(ctx.gkey)
+        rows, d = x.shape
+        g = g.contiguous().float()
+        dx = torch.empty_like(g)
+        dgain = torch.empty(d, device=g.device, dtype=torch.float32)
+        _capi.call("kl_rmsnorm_bwd", rows, d, ctx.eps, x.data_ptr(), gain.data_ptr(), g.data_ptr(), dx.data_ptr(),
+                   dgain.data_ptr(), _stream())
+        P.g(ctx.xkey).add_(dx)
+        P.g(ctx.gkey).add_(dgain)
+        return None, None, None, None, None
+
+
+def rms_norm_param(P, xkey, gkey, eps=1e-6):
+    return _RmsNorm.apply(P.flat, P, xkey, gkey, float(eps))
+
+
+class _Recent(torch.autograd.Function):
+    """recent_rows (seqsum.py:186-196) on a padded batch."""
+
+    @staticmethod
+    def forward(ctx, S, lengths, n):
+        B, T, d = S.shape
+        out = torch.empty(B, n, d, device=S.device, dtype=S.dtype)
+        _capi.call("kl_recent_rows_fwd", B, T, d, n, _capi.dt(S), S.data_ptr(), S.stride(0), lengths.data_ptr(),
+                   out.data_ptr(), out.stride(0), _stream())
+        ctx.save_for_backward(lengths)
+        ctx.shape = S.shape
+        return out
+
+    @staticmethod
+    def backward(ctx, g):
+        (lengths,) = ctx.saved_tensors
+        B, T, d = ctx.shape
+        g = g.contiguous()
+        dS = torch.zeros(B, T, d, device=g.device, dtype=g.dtype)
+        _capi.call("kl_recent_rows_bwd", B, T, d, g.shape[1], _capi.dt(g), g.data_ptr(), g.stride(0),
+                   lengths.data_ptr(), dS.data_ptr(), dS.stride(0), _stream())
+        return dS, None, None
+
+
+def recent_rows(S, lengths, n):
+    if n == 0:
+        return S.new_zeros(S.shape[0], 0, S.shape[2])
+    if not S.is_contiguous():
+        S = S.contiguous()
+    return _Recent.apply(S, lengths, int(n))
+
+
+class _GramTriu(torch.autograd.Function):
+    """triu_flatten(x x^T) per sample (interaction.py:63-76, 116-117)."""
+
+    @staticmethod
+    def forward(ctx, x):
+        B, n, d = x.shape
+        if x.stride(2) != 1:
+            raise ShapeError("gram_triu needs unit column stride")
+        tri = torch.empty(B, n * (n + 1) // 2, device=x.device, dtype=x.dtype)
+        _capi.call("kl_gram_triu_fwd", B, n, d, _capi.dt(x), x.data_ptr(), x.stride(1), x.stride(0),
+                   tri.data_ptr(), tri.stride(0), _stream())
+        ctx.save_for_backward(x)
+        return tri
+
+    @staticmethod
+    def backward(ctx, g):
+        (x,) = ctx.saved_tensors
+        B, n, d = x.shape
+        g = g.contiguous()
+        dx = torch.zeros(B, n, d, device=x.device, dtype=x.dtype)
+        _capi.call("kl_gram_triu_bwd", B, n, d, _capi.dt(x), x.data_ptr(), x.stride(1), x.stride(0),
+                   g.data_ptr(), g.stride(0), dx.data_ptr(), dx.stride(1), dx.stride(0), _stream())
+        return dx
+
+
+def gram_triu(x):
+    return _GramTriu.apply(x)
+
+
+class _Gated(torch.autograd.Function):
+    """x + gate_deep*deep + gate_dot*dot (interaction.py:121); gates are
+    (1,)-shaped fp32 parameters (interaction.py:97-98 with tensor.py:36)."""
+
+    @staticmethod
+    def forward(ctx, x, deep, dot, flat, P, gdkey, gtkey):
+        B, n, d = deep.shape
+        deep = deep.contiguous()
+        dot = dot.contiguous()
+        out = torch.empty(B, n, d, device=x.device, dtype=x.dtype)
+        if x.stride(2) != 1 or x.stride(0) != n * x.stride(1):
+            x = x.contiguous()
+        _capi.call("kl_gated_sum_fwd", B * n, d, _capi.dt(x), x.data_ptr(), x.stride(1), deep.data_ptr(),
+                   dot.data_ptr(), P.w32(gdkey).data_ptr(), P.w32(gtkey).data_ptr(), out.data_ptr(), d, _stream())
+        ctx.save_for_backward(deep, dot)
+        ctx.P, ctx.gdkey, ctx.gtkey = P, gdkey, gtkey
+        return out
+
+    @staticmethod
+    def backward(ctx, g):
+        deep, dot = ctx.saved_tensors
+        P = ctx.P
+        B, n, d = deep.shape
+        g = g.contiguous()
+        ddeep = torch.empty_like(deep)
+        ddot = torch.empty_like(dot)
+        scratch = torch.empty(2 * 512, device=g.device, dtype=torch.float32)
+        dgd = torch.empty(1, device=g.device, dtype=torch.float32)
+        dgt = torch.empty(1, device=g.device, dtype=torch.float32)
+        _capi.call("kl_gated_sum_bwd", B * n, d, _capi.dt(g), g.data_ptr(), d, deep.data_ptr(), dot.data_ptr(),
+                   P.w32(ctx.gdkey).data_ptr(), P.w32(ctx.gtkey).data_ptr(), ddeep.data_ptr(), ddot.data_ptr(),
+                   dgd.data_ptr(), dgt.data_ptr(), scratch.data_ptr(), _stream())
+        P.g(ctx.gdkey).add_(dgd)
+        P.g(ctx.gtkey).add_(dgt)
+        return g, ddeep, ddot, None, None, None, None
+
+
+def gated_sum(x, deep, dot, P, gdkey, gtkey):
+    return _Gated.apply(x, deep, dot, P.flat, P, gdkey, gtkey)
+
+
+class _BCE(torch.autograd.Function):
+    """Mean BCE with logits (tensor.py:535-549), fp32."""
+
+    @staticmethod
+    def forward(ctx, z, y):
+        z = z.contiguous().float()
+        y = y.contiguous().float()
+        loss = torch.empty(1, device=z.device, dtype=torch.float32)
+        dz = torch.empty_like(z)
+        _capi.call("kl_bce_fwd_bwd", z.numel(), z.data_ptr(), y.data_ptr(), loss.data_ptr(), dz.data_ptr(), _stream())
+        ctx.save_for_backward(dz)
+        return loss.view(())
+
+    @staticmethod
+    def backward(ctx, g):
+        (dz,) = ctx.saved_tensors
+        return dz * g, None
+
+
+def bce_with_logits(z, y):
+    return _BCE.apply(z, y)
+
+
+class _Cast(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, dtype):
+        ctx.src = x.dtype
+        if x.dtype == dtype:
+            return x
+        x = x.contiguous()
+        y = torch.empty(x.shape, device=x.device, dtype=dtype)
+        _capi.call("kl_cast", x.numel(), _capi.dt(x), x.data_ptr(), _capi.dt(y), y.data_ptr(), _stream())
+        return y
+
+    @staticmethod
+    def backward(ctx, g):
+        if g.dtype == ctx.src:
+            return g, None
+        g = g.contiguous()
+        y = torch.empty(g.shape, device=g.device, dtype=ctx.src)
+        _capi.call("kl_cast", g.numel(), _capi.dt(g), g.data_ptr(), _capi.dt(y), y.data_ptr(), _stream())
+        return y, None
+
+
+def cast(x, dtype):
+    return _Cast.apply(x, dtype)
+
+
+class _HeadProj(torch.autograd.Function):
+    """Per-head value projection + head concat of multi_head_attention
+    (attention.py:88-92): out[b, i, h*d_h + c] = sum_f X[b,h,i,f] W_h[c,f]."""
+
+    @staticmethod
+    def forward(ctx, X, flat, wref):
+        B, H, n, d = X.shape
+        W = wref.w()  # (H, d_h, d)
+        d_h = W.shape[1]
+        out = torch.empty(B, n, H, d_h, device=X.device, dtype=X.dtype)
+        gemm(X, W.transpose(1, 2), out.permute(0, 2, 1, 3))
+        ctx.save_for_backward(X)
+        ctx.wref = wref
+        return out.view(B, n, H * d_h)
+
+    @staticmethod
+    def backward(ctx, g):
+        (X,) = ctx.saved_tensors
+        B, H, n, d = X.shape
+        W = ctx.wref.w()
+        d_h = W.shape[1]
+        gv = g.contiguous().view(B, n, H, d_h).permute(0, 2, 1, 3)
+        dX = gemm(gv, W.unsqueeze(0).expand(B, H, d_h, d))
+        gemm(gv.transpose(2, 3), X, ctx.wref.g().unsqueeze(0), beta=1.0, reduce=(True, False))
+        return dX, None, None
+
+
+def head_proj(X, wref):
+    return _HeadProj.apply(X, wref.P.flat, wref)

@@ -1,0 +1,224 @@
+"""Kunlun model assembly on B200: event configs, CompSkip (Alg. 4), the
+layer forward (Alg. 1) and the prediction head.
+
+The reference ships no ``model`` module; this follows
+SPEC.md:451-533 and PAPER.md:515-541 / 586-603 exactly as SURVEY.md
+Appendix A.1 pins the composition (the oracle's ``oracle/model.py`` restates
+the same order).  CompSkip is host-side kernel selection: a skipped
+sub-module launches nothing.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import functional as F
+from .attention import MhaParams, WindowSpec, mha_window
+from .gdpa import GdpaConfig, WeightGenParams, fold_kv, generate_kv, summarize_nonseq
+from .interaction import ExpertPartition, InteractionParams, global_interaction
+from .mlp import Mlp
+from .seqsum import SummarizerParams, SummarySplit, hsp_summarize
+from .tensor import Params, ShapeError
+
+DEFAULT_ACTIVATION_CYCLE = ("silu", "relu", "identity", "tanh")
+
+
+@dataclass
+class EventConfig:
+    """Per-event sequence knobs: padded length T, window
+    half-width w, summary token budget, HSP seeds and SumKron rank."""
+
+    T: int
+    w: int
+    budget: int
+    n_seeds: int
+    rank: int
+    causal: bool = False
+    name: str = ""
+
+    def __post_init__(self):
+        if min(self.T, self.budget, self.n_seeds, self.rank) < 1 or self.w < 0:
+            raise ValueError("event config values must be positive")
+
+
+@dataclass
+class LayerSkipFlags:
+    """Alg. 4 per-layer flags."""
+
+    skip_self_attention: bool = False
+    skip_hsp: bool = False
+    skip_pffn: bool = False
+
+    def as_tuple(self):
+        return (self.skip_self_attention, self.skip_hsp, self.skip_pffn)
+
+
+def compskip_config(L: int, enabled: bool = True) -> list:
+    """Alg. 4: even l -> skip self-attention
+    (fresh HSP + PFFN); odd l -> reuse H_prev and skip PFFN."""
+    if L < 1:
+        raise ValueError("need at least one layer")
+    if not enabled:
+        return [LayerSkipFlags() for _ in range(L)]
+    return [LayerSkipFlags(True, False, False) if l % 2 == 0 else LayerSkipFlags(False, True, True)
+            for l in range(L)]
+
+
+@dataclass
+class ModelConfig:
+    """global layers, width, heads, non-sequence tokens n+1,
+    events, n_sum, n_kv, experts M, CompSkip."""
+
+    L: int
+    d: int
+    heads: int
+    n_ctx: int
+    events: list
+    n_sum: int = 4
+    n_kv: int = 16
+    experts: int = 2
+    compskip: bool = False
+    gdpa_acts: tuple = ()
+    expert_hidden: int = 0
+    head_hidden: int = 0
+
+    def __post_init__(self):
+        if self.d % self.heads:
+            raise ValueError(f"dim {self.d} not divisible by {self.heads} heads")
+        if not self.gdpa_acts:
+            c = DEFAULT_ACTIVATION_CYCLE
+            self.gdpa_acts = tuple(c[h % len(c)] for h in range(self.heads))
+        self.expert_hidden = self.expert_hidden or 2 * self.d
+        self.head_hidden = self.head_hidden or 4 * self.d
+        ExpertPartition.contiguous(self.n_tot, self.experts)
+
+    @property
+    def n_tot(self) -> int:
+        return self.n_ctx + sum(e.budget for e in self.events)
+
+    def gdpa_cfg(self, e: int) -> GdpaConfig:
+        # tau = the event's padded max length
+        return GdpaConfig(self.d, self.heads, self.n_kv, float(self.events[e].T), tuple(self.gdpa_acts))
+
+
+@dataclass
+class LayerParams:
+    pool: str
+    wg: list
+    mha: list
+    summ: list
+    gi: InteractionParams
+
+
+class _Boundary(torch.autograd.Function):
+    """Identity on a layer's inputs whose backward fires after every
+    backward kernel of that layer: the data-parallel reducer's hook point
+    (dist.py) for launching that layer's gradient bucket."""
+
+    @staticmethod
+    def forward(ctx, hook, layer, *xs):
+        ctx.hook, ctx.layer = hook, layer
+        return xs if len(xs) > 1 else xs[0]
+
+    @staticmethod
+    def backward(ctx, *gs):
+        ctx.hook(ctx.layer)
+        return (None, None) + gs
+
+
+class KunlunModel:
+    """Parameters + batched forward of the Kunlun model on one device.
+
+    Registry names (SURVEY.md Appendix A.3 with our layer/event prefixes):
+    ``L{l}/pool``, ``L{l}/ev{e}/gdpa/...``, ``L{l}/ev{e}/mha/...``,
+    ``L{l}/ev{e}/summ/...``, ``L{l}/gi/...``, ``head/w0..b1`` — identical to
+    ``oracle/model.py``."""
+
+    def __init__(self, cfg: ModelConfig, device="cuda", dtype=torch.bfloat16, seed: int = 0):
+        self.cfg = cfg
+        self.dtype = dtype
+        rng = np.random.default_rng(seed)
+        P = Params()
+        self.P = P
+        d, H = cfg.d, cfg.heads
+        part = ExpertPartition.contiguous(cfg.n_tot, cfg.experts)
+        self.layers = []
+        for l in range(cfg.L):
+            pool = P.add(f"L{l}/pool", rng.normal(0.0, 1.0 / np.sqrt(cfg.n_ctx), (cfg.n_sum, cfg.n_ctx)))
+            wg, mh, sm = [], [], []
+            for e, ev in enumerate(cfg.events):
+                wg.append(WeightGenParams.create(P, f"L{l}/ev{e}/gdpa", cfg.gdpa_cfg(e), cfg.n_sum, d, rng))
+                mh.append(MhaParams.create(P, f"L{l}/ev{e}/mha", d, H, rng))
+                sm.append(SummarizerParams.create(P, f"L{l}/ev{e}/summ", d, SummarySplit.for_budget(ev.budget),
+                                                  ev.n_seeds, ev.rank, H, rng))
+            gi = InteractionParams.create(P, f"L{l}/gi", part, cfg.n_ctx, d, cfg.expert_hidden, rng)
+            self.layers.append(LayerParams(pool, wg, mh, sm, gi))
+        self.head = Mlp.create(P, "head", [cfg.n_ctx * d, cfg.head_hidden, 1], ["silu", "identity"], rng)
+        P.finalize(device, dtype)
+        self.flags = compskip_config(cfg.L, cfg.compskip)
+        self.layer_hook = None  # set by dist.GradReducer
+
+    # ------------------------------------------------------------------
+    def layer_forward(self, l: int, flags: LayerSkipFlags, X, S_list, lengths, H_prev, live_seq=True):
+        """One Kunlun layer (Alg. 1), batched.  ``live_seq=False`` skips the
+        sequence branch (GDPA + SWA) when its output cannot reach the loss
+        (liveness pruning); the returned S' is then
+        the input S."""
+        cfg = self.cfg
+        lp = self.layers[l]
+        if flags.skip_hsp and H_prev is None:
+            raise ValueError("skip_hsp on a layer without H_prev")
+        if self.layer_hook is not None:
+            outs = _Boundary.apply(self.layer_hook, l, X, *S_list)
+            X, S_list = outs[0], list(outs[1:])
+        xsum = summarize_nonseq(X, F.PRef(self.P, lp.pool)) if (not flags.skip_pffn and live_seq) else None
+        H_list = []
+        for e in range(len(cfg.events)):
+            if flags.skip_hsp:
+                H_list.append(H_prev[e])
+            else:
+                H_list.append(hsp_summarize(S_list[e], lp.summ[e], lengths[e]).rows())
+        Xn = global_interaction(X, H_list, lp.gi)
+        S_out = []
+        for e, ev in enumerate(cfg.events):
+            s = S_list[e]
+            if live_seq and not flags.skip_pffn:
+                k, v = generate_kv(xsum, lp.wg[e], cfg.gdpa_cfg(e))
+                kt, vt = fold_kv(k, v, lp.wg[e])
+                s = F.gdpa_core(s, kt, vt, lengths[e], cfg.gdpa_acts, cfg.n_kv, 1.0 / float(ev.T))
+            if live_seq and not flags.skip_self_attention:
+                s = mha_window(s, lp.mha[e], WindowSpec(ev.w, ev.causal), lengths[e])
+            S_out.append(s)
+        return Xn, S_out, H_list
+
+    def seq_live(self) -> list:
+        """Layers whose sequence output can still reach a later HSP (and so
+        the loss): l is live iff some l' > l does not skip HSP."""
+        L = self.cfg.L
+        return [any(not self.flags[j].skip_hsp for j in range(l + 1, L)) for l in range(L)]
+
+    def forward(self, X, S_list, lengths, keep_outputs=False, prune_dead=True):
+        """X (B, n+1, d), S_list[e] (B, T_e, d) in the compute dtype,
+        lengths[e] (B,) int32.  Returns logits (B,) fp32 and, if asked, every
+        layer's (X', S', H)."""
+        live = self.seq_live() if prune_dead else [True] * self.cfg.L
+        H = None
+        outs = []
+        for l in range(self.cfg.L):
+            X, S_list, H = self.layer_forward(l, self.flags[l], X, S_list, lengths, H, live_seq=live[l])
+            if keep_outputs:
+                outs.append((X, list(S_list), list(H)))
+        B = X.shape[0]
+        z = self.head.apply_rows(X.reshape(B, -1))
+        logits = F.cast(z, torch.float32).reshape(B)
+        return (logits, outs) if keep_outputs else logits
+
+    def loss(self, X, S_list, lengths, labels, prune_dead=True):
+        logits = self.forward(X, S_list, lengths, prune_dead=prune_dead)
+        return F.bce_with_logits(logits, labels), logits
+
+    def count_params(self) -> int:
+        return self.P.count()

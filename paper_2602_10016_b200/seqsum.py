@@ -1,0 +1,240 @@
+"""Sequence summarization on B200: PMA, Hierarchical Seed Pooling with
+SumKronLinear, recent rows, and the three-part summary bundle.
+
+Mirrors /root/reference/pkg/src/kunlun/seqsum.py (names, dataclasses,
+validation, init distributions and draw order, registry names).
+
+Execution: the seed queries (RMSNorm'd seeds, seqsum.py:96-102) and the CLS
+queries (pma, seqsum.py:26-34) are batch-shared, so their key projection is
+folded into the queries once per step (``Qt_h = q W_q^h^T W_k^h / sqrt(d_h)``)
+and both query sets pool over S in ONE pass
+(``P = softmax_t(S Qt^T)``, ``pooled = P^T S``), followed by the value and
+output projections.  SumKronLinear runs as two
+batched GEMMs.  Empty sequences give zeros with no gradient.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import functional as F
+from .attention import MhaParams, multi_head_attention, shared_queries, _lengths
+from .tensor import Params, ShapeError
+
+
+def pma(s, queries, p: MhaParams, lengths=None):
+    """Pooling by multi-head attention with learnable queries (seqsum.py:26-34)."""
+    return multi_head_attention(queries, s, p, lengths=lengths)
+
+
+def seed_token_bounds(n_seeds: int, n_tokens: int) -> np.ndarray:
+    """Seed->token block bounds of the mean-pooling init (seqsum.py:67-71):
+    float linspace truncated to int, exactly as the reference computes it."""
+    return np.linspace(0, n_seeds, n_tokens + 1).astype(int)
+
+
+def seed_init_base(n_seeds: int, n_tokens: int) -> np.ndarray:
+    """Mean-pooling start of the token-mixing maps (seqsum.py:65-71)."""
+    base = np.zeros((n_seeds, n_tokens))
+    b = seed_token_bounds(n_seeds, n_tokens)
+    for j in range(n_tokens):
+        lo, hi = int(b[j]), max(int(b[j + 1]), int(b[j]) + 1)
+        base[lo:hi, j] = 1.0 / (hi - lo)
+    return base
+
+
+@dataclass
+class HspParams:
+    """Seeds, their RMSNorm gain, the seed-attention weights and the rank-k
+    compression pairs (seqsum.py:37-93).  Packed: ``zs`` (k, n_seeds,
+    n_tokens) and ``ws`` (k, d, d)."""
+
+    P: Params
+    prefix: str
+    attn: MhaParams
+    n_seeds: int
+    n_tokens: int
+    rank: int
+    dim: int
+
+    def __post_init__(self):
+        if self.n_seeds <= self.n_tokens:
+            raise ValueError(
+                f"need more seeds than output tokens for an overcomplete stage, "
+                f"got {self.n_seeds} seeds for {self.n_tokens} tokens")
+        if self.rank < 1:
+            raise ValueError("need k >= 1 aligned (seq_map, emb_map) pairs")
+
+    @property
+    def seeds(self):
+        return f"{self.prefix}/seeds"
+
+    @property
+    def gain(self):
+        return f"{self.prefix}/norm_gain"
+
+    @property
+    def zs(self):
+        return f"{self.prefix}#seq_maps"
+
+    @property
+    def ws(self):
+        return f"{self.prefix}#emb_maps"
+
+    @classmethod
+    def create(cls, params: Params, prefix: str, dim: int, n_seeds: int, n_tokens: int, rank: int, heads: int,
+               rng: np.random.Generator | None = None) -> "HspParams":
+        if n_seeds <= n_tokens:
+            raise ValueError("n_seeds must exceed n_tokens")
+        rng = rng if rng is not None else np.random.default_rng(0)
+        params.add(f"{prefix}/seeds", rng.normal(0.0, 1.0 / np.sqrt(dim), (n_seeds, dim)))
+        params.add(f"{prefix}/norm_gain", np.ones(dim))
+        attn = MhaParams.create(params, f"{prefix}/attn", dim, heads, rng)
+        base = seed_init_base(n_seeds, n_tokens)
+        p = cls(params, prefix, attn, n_seeds, n_tokens, rank, dim)
+        params.block(p.zs, (rank, n_seeds, n_tokens))
+        params.block(p.ws, (rank, dim, dim))
+        for i in range(rank):
+            z = base / rank + rng.normal(0.0, 0.02, (n_seeds, n_tokens))
+            w = np.eye(dim) + rng.normal(0.0, 0.02, (dim, dim))
+            params.add(f"{prefix}/kron{i}/seq_map", z, block=p.zs, index=i)
+            params.add(f"{prefix}/kron{i}/emb_map", w, block=p.ws, index=i)
+        return p
+
+    def compression_param_count(self) -> int:
+        return self.rank * (self.n_seeds * self.n_tokens + self.dim * self.dim)
+
+
+def hsp_queries(p: HspParams) -> torch.Tensor:
+    """Qt for the seed set: RMSNorm(seeds)*gain (tensor.py:552-556) folded
+    through W_q, W_k (H, n_seeds, d)."""
+    qn = F.rms_norm_param(p.P, p.seeds, p.gain)
+    qn = F.cast(qn, p.P.compute_dtype)
+    return shared_queries(qn, p.attn)
+
+
+def sumkronlinear(x: torch.Tensor, p: HspParams) -> torch.Tensor:
+    """Y = sum_i Z_i^T X W_i (seqsum.py:105-122) on (B, n_seeds, d)."""
+    if x.shape[-2] != p.n_seeds or x.shape[-1] != p.dim:
+        raise ShapeError(f"map shapes incompatible with input {tuple(x.shape)}")
+    squeeze = x.dim() == 2
+    if squeeze:
+        x = x.unsqueeze(0)
+    B = x.shape[0]
+    v = F.mm(x.unsqueeze(1), F.PRef(p.P, p.ws, lambda w: w.unsqueeze(0)))  # (B, k, n_s, d)
+    y = F.mm(F.PRef(p.P, p.zs, lambda z: z.transpose(1, 2).unsqueeze(0)), v, reduce=(False, True))
+    y = y.view(B, p.n_tokens, p.dim)
+    return y.squeeze(0) if squeeze else y
+
+
+def hsp_seed_attend(s, p: HspParams, lengths=None):
+    """MHA(RMSNorm(E)*g, S, S), zeros for empty sequences (seqsum.py:96-102)."""
+    kv = s.unsqueeze(0) if s.dim() == 2 else s
+    out = multi_head_attention(F.cast(F.rms_norm_param(p.P, p.seeds, p.gain), p.P.compute_dtype), kv, p.attn,
+                               lengths=lengths)
+    return out.squeeze(0) if s.dim() == 2 else out
+
+
+@dataclass
+class SummarySplit:
+    """Token budget split (seqsum.py:125-145)."""
+
+    n_cls: int
+    n_tokens: int
+    n_recent: int
+
+    def __post_init__(self):
+        if min(self.n_cls, self.n_tokens, self.n_recent) < 0 or self.n_tokens < 1:
+            raise ValueError("split counts must be >= 0 with at least one compressed token")
+
+    @property
+    def total(self) -> int:
+        return self.n_cls + self.n_tokens + self.n_recent
+
+    @classmethod
+    def for_budget(cls, budget: int) -> "SummarySplit":
+        q = budget // 4
+        return cls(q, budget - 2 * q, q)
+
+
+@dataclass
+class SummaryBundle:
+    """[CLS | compressed seeds | recent] (seqsum.py:148-162), each (B, n, d)."""
+
+    cls_tokens: torch.Tensor
+    hsp_tokens: torch.Tensor
+    recent_tokens: torch.Tensor
+
+    def rows(self) -> torch.Tensor:
+        parts = [t for t in (self.cls_tokens, self.hsp_tokens, self.recent_tokens) if t.shape[-2] > 0]
+        return parts[0] if len(parts) == 1 else torch.cat(parts, dim=-2)
+
+    @property
+    def total_rows(self) -> int:
+        return self.cls_tokens.shape[-2] + self.hsp_tokens.shape[-2] + self.recent_tokens.shape[-2]
+
+
+@dataclass
+class SummarizerParams:
+    """Everything for one event type's SummaryBundle (seqsum.py:165-183)."""
+
+    hsp: HspParams
+    cls_queries: str | None
+    cls_attn: MhaParams | None
+    split: SummarySplit
+
+    @classmethod
+    def create(cls, params: Params, prefix: str, dim: int, split: SummarySplit, n_seeds: int, rank: int,
+               heads: int, rng: np.random.Generator | None = None) -> "SummarizerParams":
+        rng = rng if rng is not None else np.random.default_rng(0)
+        hsp = HspParams.create(params, f"{prefix}/hsp", dim, n_seeds, split.n_tokens, rank, heads, rng)
+        queries = attn = None
+        if split.n_cls > 0:
+            queries = params.add(f"{prefix}/cls_queries", rng.normal(0.0, 1.0 / np.sqrt(dim), (split.n_cls, dim)))
+            attn = MhaParams.create(params, f"{prefix}/cls_attn", dim, heads, rng)
+        return cls(hsp, queries, attn, split)
+
+
+def recent_rows(s, n_recent: int, lengths=None):
+    """Last n_recent valid rows, zero-padded at the front (seqsum.py:186-196)."""
+    squeeze = s.dim() == 2
+    ss = s.unsqueeze(0) if squeeze else s
+    out = F.recent_rows(ss, _lengths(ss, lengths), n_recent)
+    return out.squeeze(0) if squeeze else out
+
+
+def hsp_summarize(s, p: SummarizerParams, lengths=None) -> SummaryBundle:
+    """Full three-part summary [CLS | compressed seeds | recent]
+    (seqsum.py:199-210).  The seed and CLS query sets pool over S in a single
+    kernel pass."""
+    squeeze = s.dim() == 2
+    S = s.unsqueeze(0) if squeeze else s
+    B, T, d = S.shape
+    lens = _lengths(S, lengths)
+    hp = p.hsp
+    H = hp.attn.heads
+    qs = hsp_queries(hp)  # (H, n_s, d)
+    n_s = hp.n_seeds
+    n_cls = p.split.n_cls
+    if n_cls > 0:
+        qc = shared_queries(F.PRef(hp.P, p.cls_queries), p.cls_attn)  # (H, n_cls, d)
+        q_all = torch.cat([qs, qc], dim=1)
+    else:
+        q_all = qs
+    n_q = n_s + n_cls
+    pooled = F.hsp_pool(S, q_all.reshape(H * n_q, d), lens).view(B, H, n_q, d)
+    hseed = F.linear(F.head_proj(pooled[:, :, :n_s], hp.attn.ref(2)), hp.P, hp.attn.wout)
+    hsp_tok = sumkronlinear(hseed, hp)
+    if n_cls > 0:
+        cls_tok = F.linear(F.head_proj(pooled[:, :, n_s:], p.cls_attn.ref(2)), hp.P, p.cls_attn.wout)
+    else:
+        cls_tok = S.new_zeros(B, 0, d)
+    rec = F.recent_rows(S, lens, p.split.n_recent)
+    bundle = SummaryBundle(cls_tok, hsp_tok, rec)
+    if squeeze:
+        bundle = SummaryBundle(cls_tok[0], hsp_tok[0], rec[0])
+    assert bundle.total_rows == p.split.total
+    return bundle

@@ -1,0 +1,337 @@
+"""Kernel parity on the B200: every device op and the composed model vs the
+float64 numpy oracle (itself pinned to the reference's golden vectors).
+
+Metric: relative error = max|gpu - oracle| / max|oracle| per tensor.
+Tolerances (BASELINE.json north_star): FP32 path <= 1e-5, BF16 path <= 2e-2.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import kunlun as K
+from oracle import model as OM
+
+pytestmark = pytest.mark.gpu
+
+TOL = {torch.float32: 1e-5, torch.bfloat16: 2e-2}
+DTYPES = [torch.float32, torch.bfloat16]
+
+
+def rel(a, b):
+    a = a.detach().double().cpu().numpy() if isinstance(a, torch.Tensor) else np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    if b.size == 0:
+        return 0.0
+    den = np.abs(b).max()
+    if den == 0:
+        return float(np.abs(a).max())
+    return float(np.abs(a - b).max() / den)
+
+
+def dev(x, dtype=torch.float32, grad=False):
+    t = torch.tensor(np.asarray(x), dtype=dtype, device="cuda")
+    return t.requires_grad_(grad)
+
+
+@pytest.fixture(autouse=True)
+def _lib():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2602_10016_b200 import _capi
+
+    _capi.lib()
+
+
+# ---------------------------------------------------------------------------
+# generic GEMM vs a torch fp32 reference of the same op
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("M,N,K", [(1, 1, 1), (7, 5, 3), (64, 64, 64), (130, 200, 70), (256, 384, 256),
+                                   (1000, 96, 40)])
+def test_gemm_plain(dtype, M, N, K):
+    from paper_2602_10016_b200._capi import gemm
+
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N)
+    A = torch.randn(M, K, device="cuda", generator=g).to(dtype)
+    B = torch.randn(K, N, device="cuda", generator=g).to(dtype)
+    ref = A.double() @ B.double()
+    out = gemm(A, B, out_dtype=torch.float32)
+    assert rel(out, ref.cpu().numpy()) < (1e-6 if dtype == torch.float32 else 1e-2)
+    # transposed operand layouts
+    out2 = gemm(A.t().contiguous().t(), B.t().contiguous().t(), out_dtype=torch.float32)
+    assert rel(out2, ref.cpu().numpy()) < (1e-6 if dtype == torch.float32 else 1e-2)
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_gemm_batched_reduce_epilogue(dtype):
+    from paper_2602_10016_b200._capi import gemm
+
+    g = torch.Generator(device="cuda").manual_seed(3)
+    A = torch.randn(3, 4, 33, 20, device="cuda", generator=g).to(dtype)
+    B = torch.randn(1, 4, 20, 48, device="cuda", generator=g).to(dtype)
+    ref = (A.double() @ B.double()).sum(0, keepdim=True)
+    out = gemm(A, B, out_dtype=torch.float32, reduce=(True, False))
+    tol = 1e-6 if dtype == torch.float32 else 1e-2
+    assert out.shape == (1, 4, 33, 48)
+    assert rel(out, ref.cpu().numpy()) < tol
+    # epilogue: act(alpha*acc + bias) + beta*C + R with per-column-group codes and row limit
+    Cin = torch.randn(3, 4, 33, 48, device="cuda", generator=g)
+    R = torch.randn(3, 4, 33, 48, device="cuda", generator=g)
+    bias = torch.randn(48, device="cuda", generator=g)
+    lim = torch.tensor([33, 10, 0], device="cuda", dtype=torch.int32)
+    out = Cin.clone()
+    pre = torch.empty_like(out)
+    gemm(A, B, out, alpha=0.5, beta=1.0, bias=bias, acts=["silu", "tanh", "relu"], act_group=16, aux=pre, aux_mode=1,
+         residual=R, row_limit=lim)
+    z = 0.5 * (A.double() @ B.double()) + bias.double()
+    act = torch.cat([torch.nn.functional.silu(z[..., :16]), torch.tanh(z[..., 16:32]), torch.relu(z[..., 32:])], -1)
+    full = act + Cin.double() + R.double()
+    rows = torch.arange(33, device="cuda")[None, None, :, None]
+    full = torch.where(rows < lim.view(3, 1, 1, 1), full, torch.zeros_like(full))
+    assert rel(out, full.cpu().numpy()) < tol
+    assert rel(pre, torch.where(rows < lim.view(3, 1, 1, 1), z, torch.zeros_like(z)).cpu().numpy()) < tol
+
+
+# ---------------------------------------------------------------------------
+
+
+def _params_gdpa(dtype, H=4, d=32, n_kv=4, n_sum=2, n_ctx=5, T=20, seed=0):
+    from paper_2602_10016_b200 import gdpa as G
+    from paper_2602_10016_b200.tensor import Params
+
+    rng = np.random.default_rng(seed)
+    P = Params()
+    cfg = G.GdpaConfig(dim=d, heads=H, n_kv=n_kv, tau=float(T))
+    wg = G.WeightGenParams.create(P, "g", cfg, n_sum, d, rng)
+    P.add("pool", rng.normal(0, 1 / np.sqrt(n_ctx), (n_sum, n_ctx)))
+    P.finalize("cuda", dtype)
+    named = {n: P[n].double().cpu().numpy() for n in P.names()}
+    return P, cfg, wg, named
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_gdpa_vs_oracle(dtype):
+    from paper_2602_10016_b200 import functional as F
+    from paper_2602_10016_b200 import gdpa as G
+
+    H, d, n_kv, n_sum, n_ctx, T = 4, 32, 4, 2, 5, 20
+    P, cfg, wg, named = _params_gdpa(dtype, H, d, n_kv, n_sum, n_ctx, T)
+    rng = np.random.default_rng(1)
+    lengths = np.array([20, 7, 0, 1])
+    B = len(lengths)
+    S = rng.normal(0, 1 / np.sqrt(d), (B, T, d))
+    X = rng.normal(0, 1, (B, n_ctx, d))
+    R = rng.normal(0, 1, (B, T, d))
+    S_t, X_t = dev(S, grad=True), dev(X, grad=True)
+    xs = G.summarize_nonseq(F.cast(X_t, dtype), F.PRef(P, "pool"))
+    y = G.gdpa_forward(F.cast(S_t, dtype), xs, cfg, wg, lengths=lengths)
+    P.zero_grad()
+    (F.cast(y, torch.float32) * dev(R)).sum().backward()
+    tol = TOL[dtype]
+    grads = {}
+    for b in range(B):
+        L = lengths[b]
+        xsum, xs_bwd = K.summarize_nonseq(X[b], named["pool"])
+        kv, kv_bwd = K.generate_kv(xsum, named, "g", n_kv)
+        yo, y_bwd = K.gdpa_forward(S[b, :L], kv, named, "g", float(T), cfg.activations)
+        assert rel(y[b, :L].float(), yo) < tol
+        assert rel(y[b, L:].float(), S[b, L:]) < (1e-7 if dtype == torch.float32 else 1e-2)
+        ds, dkvs, gr = y_bwd(R[b, :L])
+        dxs, gr2 = kv_bwd(dkvs)
+        dx, dpool = xs_bwd(dxs)
+        for k, v in list(gr.items()) + list(gr2.items()) + [("pool", dpool)]:
+            K._acc(grads, k, v)
+        assert rel(S_t.grad[b, :L], ds) < tol
+        assert rel(S_t.grad[b, L:], R[b, L:]) < 1e-6
+        assert rel(X_t.grad[b], dx) < tol
+    for k, v in grads.items():
+        assert rel(P.grad(k), v) < tol, k
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("T,w,causal,d,H", [(40, 3, False, 32, 2), (200, 64, False, 64, 4), (130, 17, True, 64, 4),
+                                            (96, 200, False, 32, 2)])
+def test_swa_vs_oracle(dtype, T, w, causal, d, H):
+    from paper_2602_10016_b200 import attention as A
+    from paper_2602_10016_b200 import functional as F
+    from paper_2602_10016_b200.tensor import Params
+
+    rng = np.random.default_rng(T + w)
+    P = Params()
+    mp = A.MhaParams.create(P, "m", d, H, rng)
+    P.finalize("cuda", dtype)
+    named = {n: P[n].double().cpu().numpy() for n in P.names()}
+    lengths = np.array([T, T - 1, 1, 0, max(T // 3, 1)])
+    B = len(lengths)
+    S = rng.normal(0, 1, (B, T, d))
+    R = rng.normal(0, 1, (B, T, d))
+    S_t = dev(S, grad=True)
+    y = A.mha_window(F.cast(S_t, dtype), mp, A.WindowSpec(w, causal), lengths)
+    P.zero_grad()
+    (F.cast(y, torch.float32) * dev(R)).sum().backward()
+    tol = TOL[dtype]
+    grads = {}
+    for b in range(B):
+        L = lengths[b]
+        yo, bwd = K.mha_window(S[b, :L], named, "m", w, causal)
+        assert rel(y[b, :L].float(), yo) < tol
+        assert np.array_equal(y[b, L:].float().cpu().numpy(), F.cast(dev(S[b, L:]), dtype).float().cpu().numpy())
+        ds, gr = bwd(R[b, :L])
+        for k, v in gr.items():
+            K._acc(grads, k, v)
+        assert rel(S_t.grad[b, :L], ds) < tol
+    for k, v in grads.items():
+        assert rel(P.grad(k), v) < tol, k
+
+
+def test_swa_support_bitexact():
+    from paper_2602_10016_b200 import attention as A
+
+    for T, w, causal in [(1, 0, False), (6, 2, False), (130, 64, False), (257, 128, True), (300, 5, False)]:
+        lengths = np.array([T, max(T - 3, 0), 1, 0])
+        sup = A.swa_support(lengths, T, w, causal)
+        for b, L in enumerate(lengths):
+            exp = np.zeros(T, dtype=np.int64)
+            if L:
+                exp[:L] = K.band_support_sizes(L, w, causal)
+                assert np.array_equal(exp[:L], (K.band_mask(L, w, causal)).sum(1))
+            assert np.array_equal(sup[b], exp), (T, w, causal, b)
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("T", [37, 1])
+def test_hsp_vs_oracle(dtype, T):
+    from paper_2602_10016_b200 import functional as F
+    from paper_2602_10016_b200 import seqsum as Q
+    from paper_2602_10016_b200.tensor import Params
+
+    d, H, budget, n_seeds, rank = 32, 2, 8, 6, 2
+    rng = np.random.default_rng(5)
+    P = Params()
+    sp = Q.SummarizerParams.create(P, "s", d, Q.SummarySplit.for_budget(budget), n_seeds, rank, H, rng)
+    P.finalize("cuda", dtype)
+    named = {n: P[n].double().cpu().numpy() for n in P.names()}
+    lengths = np.array([T, 0, max(T - 5, 1), 1])
+    B = len(lengths)
+    S = rng.normal(0, 1, (B, T, d))
+    R = rng.normal(0, 1, (B, budget, d))
+    S_t = dev(S, grad=True)
+    rows = Q.hsp_summarize(F.cast(S_t, dtype), sp, lengths).rows()
+    P.zero_grad()
+    (F.cast(rows, torch.float32) * dev(R)).sum().backward()
+    tol = TOL[dtype]
+    grads = {}
+    for b in range(B):
+        L = lengths[b]
+        ro, bwd = K.hsp_summarize(S[b, :L], named, "s", budget)
+        assert rel(rows[b].float(), ro) < tol
+        ds, gr = bwd(R[b])
+        for k, v in gr.items():
+            K._acc(grads, k, v)
+        assert rel(S_t.grad[b, :L], ds) < tol
+        assert float(S_t.grad[b, L:].abs().max() if L < T else 0.0) == 0.0
+    for k, v in grads.items():
+        assert rel(P.grad(k), v) < tol, k
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_gi_vs_oracle(dtype):
+    from paper_2602_10016_b200 import functional as F
+    from paper_2602_10016_b200 import interaction as I
+    from paper_2602_10016_b200.tensor import Params
+
+    d, n_ctx, experts, hidden = 16, 5, 2, 32
+    budgets = [8, 4]
+    total = n_ctx + sum(budgets)
+    rng = np.random.default_rng(9)
+    P = Params()
+    ip = I.InteractionParams.create(P, "gi", I.ExpertPartition.contiguous(total, experts), n_ctx, d, hidden, rng)
+    P.finalize("cuda", dtype)
+    named = {n: P[n].double().cpu().numpy() for n in P.names()}
+    B = 3
+    X = rng.normal(0, 1, (B, n_ctx, d))
+    Rows = [rng.normal(0, 1, (B, b, d)) for b in budgets]
+    Rc = rng.normal(0, 1, (B, n_ctx, d))
+    X_t = dev(X, grad=True)
+    rows_t = [dev(r, grad=True) for r in Rows]
+    y = I.global_interaction(F.cast(X_t, dtype), [F.cast(r, dtype) for r in rows_t], ip)
+    P.zero_grad()
+    (F.cast(y, torch.float32) * dev(Rc)).sum().backward()
+    tol = TOL[dtype]
+    grads = {}
+    for b in range(B):
+        yo, bwd = K.global_interaction(X[b], [r[b] for r in Rows], named, "gi", experts)
+        assert rel(y[b].float(), yo) < tol
+        dx, drows, gr = bwd(Rc[b])
+        for k, v in gr.items():
+            K._acc(grads, k, v)
+        assert rel(X_t.grad[b], dx) < tol
+        for e in range(2):
+            assert rel(rows_t[e].grad[b], drows[e]) < tol
+    for k, v in grads.items():
+        assert rel(P.grad(k), v) < tol, k
+
+
+# ---------------------------------------------------------------------------
+
+
+def _spec(compskip, d=16, heads=4):
+    return OM.ModelSpec(L=2, d=d, heads=heads, n_ctx=5, n_sum=2, n_kv=4, experts=2, compskip=compskip,
+                        events=[OM.EventSpec(T=12, w=3, budget=8, n_seeds=6, rank=2),
+                                OM.EventSpec(T=9, w=2, budget=4, n_seeds=3, rank=1)])
+
+
+def _gpu_model(spec, dtype):
+    from paper_2602_10016_b200.model import EventConfig, KunlunModel, ModelConfig
+
+    cfg = ModelConfig(L=spec.L, d=spec.d, heads=spec.heads, n_ctx=spec.n_ctx, n_sum=spec.n_sum, n_kv=spec.n_kv,
+                      experts=spec.experts, compskip=spec.compskip,
+                      events=[EventConfig(T=e.T, w=e.w, budget=e.budget, n_seeds=e.n_seeds, rank=e.rank)
+                              for e in spec.events])
+    return KunlunModel(cfg, "cuda", dtype)
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("compskip", [False, True])
+def test_model_vs_oracle(dtype, compskip):
+    """full 2-layer, 2-event model with a parity loss that
+    touches every layer output (so dead branches' backward kernels run too)."""
+    from paper_2602_10016_b200 import functional as F
+
+    spec = _spec(compskip)
+    pnp = OM.init_params(spec, seed=11)
+    model = _gpu_model(spec, dtype)
+    model.P.load(pnp)
+    rng = np.random.default_rng(4)
+    B = 3
+    lengths = [np.array([12, 5, 0]), np.array([9, 1, 9])]
+    X = rng.normal(0, 1 / np.sqrt(spec.d), (B, spec.n_ctx, spec.d))
+    S = [rng.normal(0, 1 / np.sqrt(spec.d), (B, ev.T, spec.d)) for ev in spec.events]
+    labels = (rng.random(B) < 0.4).astype(np.float64)
+    cot = [{"X": rng.normal(0, 0.1, X.shape), "S": [rng.normal(0, 0.1, s.shape) for s in S],
+            "H": [rng.normal(0, 0.1, (B, ev.budget, spec.d)) for ev in spec.events]} for _ in range(spec.L)]
+    ref = OM.model_forward_backward(spec, pnp, X, S, lengths, labels, cot)
+
+    X_t = dev(X, grad=True)
+    S_t = [dev(s, grad=True) for s in S]
+    lens = [torch.tensor(L, dtype=torch.int32, device="cuda") for L in lengths]
+    logits, outs = model.forward(F.cast(X_t, dtype), [F.cast(s, dtype) for s in S_t], lens, keep_outputs=True,
+                                 prune_dead=False)
+    loss = F.bce_with_logits(logits, dev(labels))
+    for l, (xo, so, ho) in enumerate(outs):
+        loss = loss + (F.cast(xo, torch.float32) * dev(cot[l]["X"])).sum()
+        for e in range(2):
+            loss = loss + (F.cast(so[e], torch.float32) * dev(cot[l]["S"][e])).sum()
+            loss = loss + (F.cast(ho[e], torch.float32) * dev(cot[l]["H"][e])).sum()
+    model.P.zero_grad()
+    loss.backward()
+    tol = TOL[dtype]
+    assert rel(logits, ref["logits"]) < tol
+    assert abs(float(loss) - ref["loss"]) / max(1.0, abs(ref["loss"])) < tol
+    assert rel(X_t.grad, ref["dX"]) < tol
+    for e in range(2):
+        assert rel(S_t[e].grad, ref["dS"][e]) < tol
+    for k, v in ref["grads"].items():
+        assert rel(model.P.grad(k), v) < tol, k
