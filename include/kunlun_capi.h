@@ -70,7 +70,8 @@ void kl_set_gemm_path(int path);
  *   for each (z1, z2):  acc = sum_k A[m,k] B[k,n]
  *   out[m,n] = act_c( alpha*acc [* act'_c(aux[m,n]) if aux_mode==2] + bias[n] )
  *              + beta*C[m,n] + R[m,n]                ([aux]=pre-act if aux_mode==1)
- *   rows m >= row_limit[z1] (if row_limit) are written as 0 (pre-act 0 too).
+ *   rows m >= row_limit[z1*nb2 + z2] (if row_limit; no batch reduction) are
+ *   written as 0 (pre-act 0 too).
  * A batch index with red{1,2}=1 is summed into one output (its C stride is
  * ignored).  act_c = act_codes[(n / act_group) % n_act] (n_act=0 -> identity).
  */
@@ -91,7 +92,7 @@ typedef struct kl_gemm_args {
   int aux_mode; /* 0 none, 1 write pre-activation, 2 multiply by act'(aux) */
   float alpha, beta;
   const float* bias; /* [N] fp32 or NULL */
-  const int* row_limit; /* [nb1] or NULL */
+  const int* row_limit; /* [nb1*nb2] or NULL */
   int n_act, act_group;
   int act_codes[KL_MAX_ACT_GROUPS];
 } kl_gemm_args;
@@ -152,6 +153,7 @@ typedef struct kl_colsoftmax_args {
   long long dp_rs, dp_bs;
   void* dX;
   long long dx_rs, dx_bs;
+  void* dX_lo; /* optional: dX - round(dX) in dX's dtype (bf16 hi/lo split) */
 } kl_colsoftmax_args;
 
 int kl_colsoftmax_fwd(const kl_colsoftmax_args* args, void* stream);
@@ -183,7 +185,8 @@ int kl_gram_triu_bwd(int B, int n, int d, int dtype, const void* x, long long x_
 /* Gated residual of a Wukong expert: out = x + gd*deep + gt*dot, gates are
  * device fp32 scalars (shape (1,), interaction.py:97-98).  bwd: ddeep = g*gd,
  * ddot = g*gt, dx += g, dgate_{deep,dot} = sum(g*deep), sum(g*dot) (fp32,
- * written).  All tensors (rows, d) contiguous with row strides given. */
+ * written; fp64 accumulation; scratch >= 2*512 doubles).  All tensors
+ * (rows, d) contiguous with row strides given. */
 int kl_gated_sum_fwd(int rows, int d, int dtype, const void* x, long long x_rs, const void* deep,
                      const void* dot, const float* gd, const float* gt, void* out, long long o_rs,
                      void* stream);

@@ -1,0 +1,48 @@
+"""Parity metrics (test infrastructure only).
+
+Relative error of a tensor = max|got - ref| / max|ref| (norm-wise; an
+elementwise ratio is meaningless near zeros).
+Parameter gradients: in FP32 every tensor with more than one element is
+held to its own scale; scalar gradients (Wukong gates, the head's output
+bias — sums with heavy cancellation) and, in BF16, every gradient are held
+to the max of their module's gradients (norm-wise over the module).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+TOL_FP32 = 1e-5
+TOL_BF16 = 2e-2
+
+
+def rel(a, b) -> float:
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    if b.size == 0:
+        return 0.0
+    den = float(np.abs(b).max())
+    num = float(np.abs(a - b).max())
+    return num / den if den > 0 else num
+
+
+def group(name: str) -> str:
+    """Module of a registry name, without per-head / per-map indices."""
+    parts = [q for q in name.split("/")[:-1]
+             if not ((q.startswith("head") and q[4:].isdigit()) or (q.startswith("kron") and q[4:].isdigit()))]
+    return "/".join(parts)
+
+
+def grad_errors(got: dict, ref: dict, fp32: bool) -> dict:
+    """name -> relative error under the rule in the module docstring."""
+    scale: dict = {}
+    for k, v in ref.items():
+        g = group(k)
+        scale[g] = max(scale.get(g, 0.0), float(np.abs(v).max()) if v.size else 0.0)
+    out = {}
+    for k, v in ref.items():
+        a = np.asarray(got[k], dtype=np.float64)
+        num = float(np.abs(a - v).max()) if v.size else 0.0
+        den = float(np.abs(v).max()) if (fp32 and v.size > 1) else scale[group(k)]
+        out[k] = num / den if den > 0 else num
+    return out

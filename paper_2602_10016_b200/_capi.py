@@ -61,6 +61,7 @@ class ColSoftmaxArgs(C.Structure):
         ("LSE", C.c_void_p), ("lengths", C.c_void_p),
         ("dP", C.c_void_p), ("dp_rs", C.c_longlong), ("dp_bs", C.c_longlong),
         ("dX", C.c_void_p), ("dx_rs", C.c_longlong), ("dx_bs", C.c_longlong),
+        ("dX_lo", C.c_void_p),
     ]
 
 

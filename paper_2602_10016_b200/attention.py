@@ -61,13 +61,13 @@ class MhaParams:
         params.add(p.wout, rng.normal(0.0, out_scale * sigma, (dim, dim)))
         return p
 
-    def ref(self, j: int, per_head: bool = True) -> F.PRef:
+    def ref(self, j: int, per_head: bool = True, fp32: bool = False) -> F.PRef:
         """PRef to the Q (j=0), K (1) or V (2) projections, (H, d_h, d)."""
         H, d_h, d = self.heads, self.head_dim, self.dim
         lo = j * H * d_h
         if per_head:
-            return F.PRef(self.P, self.wqkv, lambda w: w[lo: lo + H * d_h].view(H, d_h, d))
-        return F.PRef(self.P, self.wqkv, lambda w: w[lo: lo + H * d_h])
+            return F.PRef(self.P, self.wqkv, lambda w: w[lo: lo + H * d_h].view(H, d_h, d), fp32=fp32)
+        return F.PRef(self.P, self.wqkv, lambda w: w[lo: lo + H * d_h], fp32=fp32)
 
 
 @dataclass
@@ -142,15 +142,19 @@ def mha_full(s, p: MhaParams, length=None):
     return _self_attention(s, p, max(s.shape[-2] - 1, 0), False, length)
 
 
-def shared_queries(q: torch.Tensor, p: MhaParams, scale: float | None = None) -> torch.Tensor:
-    """Qt_h = (q W_q^h^T) W_k^h * scale -> (H, n_q, d): the batch-shared
-    reassociated query set of attention.py:85-89 (keys = S W_k^T)."""
+def shared_queries(q, p: MhaParams, scale: float | None = None) -> torch.Tensor:
+    """Qt_h = (q W_q^h^T) W_k^h * scale -> (H, n_q, d), fp32: the batch-shared
+    reassociated query set of attention.py:85-89 (keys = S W_k^T).  It is a
+    per-step (n_q x d) computation, so it stays in fp32 in every mode; only
+    the T-length pooling GEMMs run in the compute dtype.  ``q`` is an fp32
+    tensor or a PRef (read in fp32)."""
     H, d_h = p.heads, p.head_dim
     scale = 1.0 / np.sqrt(d_h) if scale is None else scale
-    qr = q if isinstance(q, F.PRef) else q
-    qh = F.mm(qr, F.PRef(p.P, p.wqkv, lambda w: w[: H * d_h].t()), p.P)  # (n_q, H*d_h)
+    if isinstance(q, F.PRef):
+        q = F.PRef(q.P, q.key, q.fn, fp32=True)
+    qh = F.mm(q, F.PRef(p.P, p.wqkv, lambda w: w[: H * d_h].t(), fp32=True), p.P)  # (n_q, H*d_h)
     n_q = qh.shape[0]
-    return F.mm(qh.view(n_q, H, d_h).permute(1, 0, 2), p.ref(1), alpha=scale)
+    return F.mm(qh.view(n_q, H, d_h).permute(1, 0, 2), p.ref(1, fp32=True), alpha=scale)
 
 
 def multi_head_attention(queries, keys_values, p: MhaParams, mask=None, lengths=None):

@@ -74,8 +74,8 @@ extern "C" int kl_gemm(const kl_gemm_args* a, void* stream) {
     set_error("kl_gemm: aux_mode %d without aux buffer", a->aux_mode);
     return KL_EBADSHAPE;
   }
-  if (a->row_limit && a->red1) {
-    set_error("kl_gemm: row_limit needs a non-reduced first batch dim");
+  if (a->row_limit && (a->red1 || a->red2)) {
+    set_error("kl_gemm: row_limit cannot be combined with batch reduction");
     return KL_EBADSHAPE;
   }
   if (a->M == 0 || a->N == 0) return KL_OK;

@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmDesc g, Epi e) {
   TC* C = (TC*)g.C + (long long)z1o * (g.red1 ? 0 : g.c_s1) + (long long)z2o * (g.red2 ? 0 : g.c_s2);
   const TC* R = g.R ? (const TC*)g.R + (long long)z1o * (g.red1 ? 0 : g.r_s1) + (long long)z2o * (g.red2 ? 0 : g.r_s2) : nullptr;
   TC* X = g.aux ? (TC*)g.aux + (long long)z1o * (g.red1 ? 0 : g.c_s1) + (long long)z2o * (g.red2 ? 0 : g.c_s2) : nullptr;
-  const int lim = e.row_limit ? e.row_limit[z1o] : 0x7fffffff;
+  const int lim = e.row_limit ? e.row_limit[zo] : 0x7fffffff;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int m = m0 + ty * 4 + i;

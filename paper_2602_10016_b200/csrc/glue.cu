@@ -76,6 +76,12 @@ __global__ void __launch_bounds__(256) colsoftmax_bwd_kernel(kl_colsoftmax_args 
       v = pr * (ldf(G + (long long)t * a.dp_rs + c) - acc);
     }
     stf(D + (long long)t * a.dx_rs + c, v);
+    if (a.dX_lo) {
+      // bf16 residual of the rounded value: hi + lo carries ~16 mantissa bits
+      // into the cancellation-heavy reduction dQ = sum_t dX S (seqsum VJP)
+      TO* L = (TO*)a.dX_lo + (long long)b * a.dx_bs;
+      stf(L + (long long)t * a.dx_rs + c, v - ldf(D + (long long)t * a.dx_rs + c));
+    }
   }
 }
 
@@ -87,6 +93,18 @@ __device__ float block_sum(float v, float* sh) {
   if (l == 0) sh[w] = v;
   __syncthreads();
   float t = 0.f;
+  const int nw = blockDim.x >> 5;
+  for (int i = 0; i < nw; ++i) t += sh[i];
+  return t;
+}
+
+__device__ double block_sum_d(double v, double* sh) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  double t = 0.0;
   const int nw = blockDim.x >> 5;
   for (int i = 0; i < nw; ++i) t += sh[i];
   return t;
@@ -107,7 +125,9 @@ __global__ void rmsnorm_fwd_kernel(int d, float eps, const float* x, const float
 __global__ void rmsnorm_bwd_kernel(int rows, int d, float eps, const float* x, const float* gain,
                                    const float* dy, float* dx, float* dgain) {
   __shared__ float sh[32];
-  for (int c = threadIdx.x; c < d; c += blockDim.x) dgain[c] = 0.f;
+  constexpr int MAXC = 8;  // d <= 8 * blockDim
+  double dg[MAXC];
+  for (int i = 0; i < MAXC; ++i) dg[i] = 0.0;
   for (int r = 0; r < rows; ++r) {
     const float* xr = x + (long long)r * d;
     const float* gr = dy + (long long)r * d;
@@ -122,9 +142,10 @@ __global__ void rmsnorm_bwd_kernel(int rows, int d, float eps, const float* x, c
     const float k = s * s * s / d * gx;
     for (int c = threadIdx.x; c < d; c += blockDim.x) {
       dx[(long long)r * d + c] = s * gr[c] * gain[c] - k * xr[c];
-      dgain[c] += gr[c] * xr[c] * s;
+      dg[c / blockDim.x] += (double)gr[c] * (double)xr[c] * (double)s;
     }
   }
+  for (int c = threadIdx.x; c < d; c += blockDim.x) dgain[c] = (float)dg[c / blockDim.x];
 }
 
 // ---------------------------------------------------------------------------
@@ -207,40 +228,40 @@ __global__ void gated_fwd_kernel(int rows, int d, const T* x, long long x_rs, co
 template <typename T>
 __global__ void __launch_bounds__(256) gated_bwd_kernel(int rows, int d, const T* g, long long g_rs, const T* deep,
                                                         const T* dot, const float* gd, const float* gt, T* ddeep,
-                                                        T* ddot, float* partial) {
-  __shared__ float sh[32];
-  float a = 0.f, b = 0.f;
+                                                        T* ddot, double* partial) {
+  __shared__ double shd[32];
+  double a = 0.0, b = 0.0;
   const long long total = (long long)rows * d;
   for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
     int c = idx % d;
     long long r = idx / d;
     float gv = ldf(g + r * g_rs + c);
-    a += gv * ldf(deep + idx);
-    b += gv * ldf(dot + idx);
+    a += (double)gv * (double)ldf(deep + idx);
+    b += (double)gv * (double)ldf(dot + idx);
     stf(ddeep + idx, gv * gd[0]);
     stf(ddot + idx, gv * gt[0]);
   }
-  a = block_sum(a, sh);
-  b = block_sum(b, sh);
+  a = block_sum_d(a, shd);
+  b = block_sum_d(b, shd);
   if (threadIdx.x == 0) {
     partial[2 * blockIdx.x] = a;
     partial[2 * blockIdx.x + 1] = b;
   }
 }
 
-__global__ void reduce_pairs_kernel(int nblk, const float* partial, float* o0, float* o1) {
-  __shared__ float sh[32];
-  float a = 0.f, b = 0.f;
+__global__ void reduce_pairs_kernel(int nblk, const double* partial, float* o0, float* o1) {
+  __shared__ double sh[32];
+  double a = 0.0, b = 0.0;
   for (int i = threadIdx.x; i < nblk; i += blockDim.x) {
     a += partial[2 * i];
     b += partial[2 * i + 1];
   }
-  a = block_sum(a, sh);
-  b = block_sum(b, sh);
+  a = block_sum_d(a, sh);
+  b = block_sum_d(b, sh);
   if (threadIdx.x == 0) {
-    o0[0] = a;
-    o1[0] = b;
+    o0[0] = (float)a;
+    o1[0] = (float)b;
   }
 }
 
@@ -344,6 +365,7 @@ extern "C" int kl_rmsnorm_fwd(int rows, int d, float eps, const float* x, const 
 extern "C" int kl_rmsnorm_bwd(int rows, int d, float eps, const float* x, const float* gain, const float* dy,
                               float* dx, float* dgain, void* stream) {
   if (d <= 0) return KL_OK;
+  if (d > 8 * 256) { set_error("kl_rmsnorm_bwd: d %d > 2048", d); return KL_EUNSUPPORTED; }
   rmsnorm_bwd_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(rows, d, eps, x, gain, dy, dx, dgain);
   count_launch();
   return launch_check("rmsnorm_bwd");
@@ -418,10 +440,10 @@ extern "C" int kl_gated_sum_bwd(int rows, int d, int dtype, const void* g, long 
   int nb = (int)std::min<long long>(512, (tot + 255) / 256);
   if (nb < 1) nb = 1;
   if (dtype == KL_F32)
-    gated_bwd_kernel<float><<<nb, 256, 0, s>>>(rows, d, (const float*)g, g_rs, (const float*)deep, (const float*)dot, gd, gt, (float*)ddeep, (float*)ddot, scratch);
+    gated_bwd_kernel<float><<<nb, 256, 0, s>>>(rows, d, (const float*)g, g_rs, (const float*)deep, (const float*)dot, gd, gt, (float*)ddeep, (float*)ddot, (double*)scratch);
   else
-    gated_bwd_kernel<bf16><<<nb, 256, 0, s>>>(rows, d, (const bf16*)g, g_rs, (const bf16*)deep, (const bf16*)dot, gd, gt, (bf16*)ddeep, (bf16*)ddot, scratch);
-  reduce_pairs_kernel<<<1, 256, 0, s>>>(nb, scratch, dgd, dgt);
+    gated_bwd_kernel<bf16><<<nb, 256, 0, s>>>(rows, d, (const bf16*)g, g_rs, (const bf16*)deep, (const bf16*)dot, gd, gt, (bf16*)ddeep, (bf16*)ddot, (double*)scratch);
+  reduce_pairs_kernel<<<1, 256, 0, s>>>(nb, (const double*)scratch, dgd, dgt);
   count_launch(2);
   return launch_check("gated_sum_bwd");
 }

@@ -317,24 +317,28 @@ int launch_bwd(const SwaP& p, cudaStream_t s) {
 template <typename T>
 int fwd_dh(const SwaP& p, cudaStream_t s) {
   switch (p.d_h) {
+    case 4: return launch_fwd<T, 4>(p, s);
+    case 8: return launch_fwd<T, 8>(p, s);
     case 16: return launch_fwd<T, 16>(p, s);
     case 32: return launch_fwd<T, 32>(p, s);
     case 64: return launch_fwd<T, 64>(p, s);
     case 128: return launch_fwd<T, 128>(p, s);
   }
-  set_error("kl_swa_fwd: head dim %d unsupported (16/32/64/128)", p.d_h);
+  set_error("kl_swa_fwd: head dim %d unsupported (4/8/16/32/64/128)", p.d_h);
   return KL_EUNSUPPORTED;
 }
 
 template <typename T>
 int bwd_dh(const SwaP& p, cudaStream_t s) {
   switch (p.d_h) {
+    case 4: return launch_bwd<T, 4>(p, s);
+    case 8: return launch_bwd<T, 8>(p, s);
     case 16: return launch_bwd<T, 16>(p, s);
     case 32: return launch_bwd<T, 32>(p, s);
     case 64: return launch_bwd<T, 64>(p, s);
     case 128: return launch_bwd<T, 128>(p, s);
   }
-  set_error("kl_swa_bwd: head dim %d unsupported (16/32/64/128)", p.d_h);
+  set_error("kl_swa_bwd: head dim %d unsupported (4/8/16/32/64/128)", p.d_h);
   return KL_EUNSUPPORTED;
 }
 

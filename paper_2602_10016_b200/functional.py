@@ -27,13 +27,13 @@ from .tensor import ACTIVATIONS, ShapeError
 class PRef:
     """A parameter operand: block ``key`` of ``P`` seen through ``fn``."""
 
-    __slots__ = ("P", "key", "fn")
+    __slots__ = ("P", "key", "fn", "fp32")
 
-    def __init__(self, P, key, fn=None):
-        self.P, self.key, self.fn = P, key, fn
+    def __init__(self, P, key, fn=None, fp32=False):
+        self.P, self.key, self.fn, self.fp32 = P, key, fn, fp32
 
     def w(self):
-        v = self.P.w(self.key)
+        v = self.P.w32(self.key) if self.fp32 else self.P.w(self.key)
         return self.fn(v) if self.fn else v
 
     def g(self):
@@ -283,9 +283,16 @@ class _HspPool(torch.autograd.Function):
     samples pool to zeros with no gradient (seqsum.py:32-33, 99-100)."""
 
     @staticmethod
-    def forward(ctx, S, Q, lengths):
+    def forward(ctx, S, Q32, lengths):
+        # Q arrives in fp32 (the batch-shared query path is computed in fp32);
+        # the T-length GEMMs run in S's dtype and dQ is returned in fp32.
         B, T, d = S.shape
-        HQ = Q.shape[0]
+        HQ = Q32.shape[0]
+        Q = Q32
+        if Q32.dtype != S.dtype:
+            Q = torch.empty(Q32.shape, device=S.device, dtype=S.dtype)
+            _capi.call("kl_cast", Q.numel(), _capi.dt(Q32), Q32.contiguous().data_ptr(), _capi.dt(Q), Q.data_ptr(),
+                       _stream())
         sc = gemm(S, Q.t(), out_dtype=torch.float32)  # (B, T, HQ)
         Pm = torch.empty(B, T, HQ, device=S.device, dtype=S.dtype)
         a = _colsm_args(sc, Pm, lengths)
@@ -300,16 +307,23 @@ class _HspPool(torch.autograd.Function):
         g = g.contiguous()
         dP = gemm(S, g.transpose(1, 2), out_dtype=torch.float32)  # (B, T, HQ)
         dsc = torch.empty_like(Pm)
+        lo = torch.empty_like(Pm) if Pm.dtype != torch.float32 else None
         a = _colsm_args(dsc, Pm, lengths)  # dtype_in = dsc dtype, dtype_out = P dtype
         a.dP, a.dp_rs, a.dp_bs = dP.data_ptr(), dP.stride(1), dP.stride(0)
         a.dX, a.dx_rs, a.dx_bs = dsc.data_ptr(), dsc.stride(1), dsc.stride(0)
+        a.dX_lo = lo.data_ptr() if lo is not None else None
         if Pm.dtype == dP.dtype:
             _capi.call("kl_colsoftmax_bwd", C.byref(a), _stream())
         else:
             _colsm_bwd_mixed(a, Pm, dP, dsc)
         dS = gemm(Pm, g)
         gemm(dsc, Q.unsqueeze(0).expand(S.shape[0], -1, -1), dS, beta=1.0)
-        dQ = gemm(dsc.transpose(1, 2).unsqueeze(0), S.unsqueeze(0), reduce=(False, True)).reshape(Q.shape)
+        # dQ = sum_b dsc^T S: softmax-VJP rows sum to zero over t, so this
+        # reduction cancels; bf16 runs it on the hi + lo split of dsc.
+        dQ = gemm(dsc.transpose(1, 2).unsqueeze(0), S.unsqueeze(0), reduce=(False, True), out_dtype=torch.float32)
+        if lo is not None:
+            gemm(lo.transpose(1, 2).unsqueeze(0), S.unsqueeze(0), dQ, beta=1.0, reduce=(False, True))
+        dQ = dQ.reshape(Q.shape)
         return dS, dQ, None
 
 
@@ -449,7 +463,7 @@ class _Gated(torch.autograd.Function):
         g = g.contiguous()
         ddeep = torch.empty_like(deep)
         ddot = torch.empty_like(dot)
-        scratch = torch.empty(2 * 512, device=g.device, dtype=torch.float32)
+        scratch = torch.empty(2 * 512, device=g.device, dtype=torch.float64)
         dgd = torch.empty(1, device=g.device, dtype=torch.float32)
         dgt = torch.empty(1, device=g.device, dtype=torch.float32)
         _capi.call("kl_gated_sum_bwd", B * n, d, _capi.dt(g), g.data_ptr(), d, deep.data_ptr(), dot.data_ptr(),

@@ -111,9 +111,7 @@ class HspParams:
 def hsp_queries(p: HspParams) -> torch.Tensor:
     """Qt for the seed set: RMSNorm(seeds)*gain (tensor.py:552-556) folded
     through W_q, W_k (H, n_seeds, d)."""
-    qn = F.rms_norm_param(p.P, p.seeds, p.gain)
-    qn = F.cast(qn, p.P.compute_dtype)
-    return shared_queries(qn, p.attn)
+    return shared_queries(F.rms_norm_param(p.P, p.seeds, p.gain), p.attn)
 
 
 def sumkronlinear(x: torch.Tensor, p: HspParams) -> torch.Tensor:
@@ -133,8 +131,7 @@ def sumkronlinear(x: torch.Tensor, p: HspParams) -> torch.Tensor:
 def hsp_seed_attend(s, p: HspParams, lengths=None):
     """MHA(RMSNorm(E)*g, S, S), zeros for empty sequences (seqsum.py:96-102)."""
     kv = s.unsqueeze(0) if s.dim() == 2 else s
-    out = multi_head_attention(F.cast(F.rms_norm_param(p.P, p.seeds, p.gain), p.P.compute_dtype), kv, p.attn,
-                               lengths=lengths)
+    out = multi_head_attention(F.rms_norm_param(p.P, p.seeds, p.gain), kv, p.attn, lengths=lengths)
     return out.squeeze(0) if s.dim() == 2 else out
 
 

@@ -29,6 +29,17 @@ def rel(a, b):
     return float(np.abs(a - b).max() / den)
 
 
+def check_grads(got, ref, dtype):
+    """Parameter-gradient parity with the rule of oracle/parity.py."""
+    from oracle.parity import grad_errors
+
+    vals = {k: got(k).detach().double().cpu().numpy() for k in ref}
+    errs = grad_errors(vals, ref, dtype == torch.float32)
+    for k, e in errs.items():
+        assert e < TOL[dtype], (k, e)
+    return max(errs.values()) if errs else 0.0
+
+
 def dev(x, dtype=torch.float32, grad=False):
     t = torch.tensor(np.asarray(x), dtype=dtype, device="cuda")
     return t.requires_grad_(grad)
@@ -84,7 +95,7 @@ def test_gemm_batched_reduce_epilogue(dtype):
     out = Cin.clone()
     pre = torch.empty_like(out)
     gemm(A, B, out, alpha=0.5, beta=1.0, bias=bias, acts=["silu", "tanh", "relu"], act_group=16, aux=pre, aux_mode=1,
-         residual=R, row_limit=lim)
+         residual=R, row_limit=lim.repeat_interleave(4))
     z = 0.5 * (A.double() @ B.double()) + bias.double()
     act = torch.cat([torch.nn.functional.silu(z[..., :16]), torch.tanh(z[..., 16:32]), torch.relu(z[..., 32:])], -1)
     full = act + Cin.double() + R.double()
@@ -144,10 +155,9 @@ def test_gdpa_vs_oracle(dtype):
         for k, v in list(gr.items()) + list(gr2.items()) + [("pool", dpool)]:
             K._acc(grads, k, v)
         assert rel(S_t.grad[b, :L], ds) < tol
-        assert rel(S_t.grad[b, L:], R[b, L:]) < 1e-6
+        assert rel(S_t.grad[b, L:], R[b, L:]) < (1e-6 if dtype == torch.float32 else 1e-2)
         assert rel(X_t.grad[b], dx) < tol
-    for k, v in grads.items():
-        assert rel(P.grad(k), v) < tol, k
+    check_grads(P.grad, grads, dtype)
 
 
 @pytest.mark.parametrize("dtype", DTYPES)
@@ -177,13 +187,13 @@ def test_swa_vs_oracle(dtype, T, w, causal, d, H):
         L = lengths[b]
         yo, bwd = K.mha_window(S[b, :L], named, "m", w, causal)
         assert rel(y[b, :L].float(), yo) < tol
-        assert np.array_equal(y[b, L:].float().cpu().numpy(), F.cast(dev(S[b, L:]), dtype).float().cpu().numpy())
+        assert np.array_equal(y[b, L:].detach().float().cpu().numpy(),
+                              F.cast(dev(S[b, L:]), dtype).float().cpu().numpy())
         ds, gr = bwd(R[b, :L])
         for k, v in gr.items():
             K._acc(grads, k, v)
         assert rel(S_t.grad[b, :L], ds) < tol
-    for k, v in grads.items():
-        assert rel(P.grad(k), v) < tol, k
+    check_grads(P.grad, grads, dtype)
 
 
 def test_swa_support_bitexact():
@@ -232,8 +242,7 @@ def test_hsp_vs_oracle(dtype, T):
             K._acc(grads, k, v)
         assert rel(S_t.grad[b, :L], ds) < tol
         assert float(S_t.grad[b, L:].abs().max() if L < T else 0.0) == 0.0
-    for k, v in grads.items():
-        assert rel(P.grad(k), v) < tol, k
+    check_grads(P.grad, grads, dtype)
 
 
 @pytest.mark.parametrize("dtype", DTYPES)
@@ -270,8 +279,7 @@ def test_gi_vs_oracle(dtype):
         assert rel(X_t.grad[b], dx) < tol
         for e in range(2):
             assert rel(rows_t[e].grad[b], drows[e]) < tol
-    for k, v in grads.items():
-        assert rel(P.grad(k), v) < tol, k
+    check_grads(P.grad, grads, dtype)
 
 
 # ---------------------------------------------------------------------------
@@ -333,5 +341,4 @@ def test_model_vs_oracle(dtype, compskip):
     assert rel(X_t.grad, ref["dX"]) < tol
     for e in range(2):
         assert rel(S_t[e].grad, ref["dS"][e]) < tol
-    for k, v in ref["grads"].items():
-        assert rel(model.P.grad(k), v) < tol, k
+    check_grads(model.P.grad, ref["grads"], dtype)
