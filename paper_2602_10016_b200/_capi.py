@@ -94,6 +94,8 @@ _SIGS = {
                     C.c_void_p, C.c_void_p], C.c_int),
     "kl_act_bwd": ([C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_longlong, C.c_void_p, C.c_longlong, C.c_void_p,
                     C.c_longlong, C.c_int, C.c_int, C.c_void_p, C.c_void_p], C.c_int),
+    "kl_adam_step": ([C.c_longlong, C.c_float, C.c_float, C.c_float, C.c_float, C.c_int] + [C.c_void_p] * 6,
+                     C.c_int),
     "kl_check_finite": ([C.c_longlong, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
 }
 
@@ -255,7 +257,18 @@ def swa_args(qkv, lengths, H, d_h, w, causal, O, LSE, dO=None, dqkv=None, Dbuf=N
     return a
 
 
+TIMED = None  # {entry-point name: [(start, end) CUDA events]} while bench.py times ops
+
+
 def call(name: str, *args):
+    if TIMED is not None and name in TIMED:
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        rc = getattr(lib(), name)(*args)
+        e.record()
+        TIMED[name].append((s, e))
+        _check(rc, name)
+        return
     _check(getattr(lib(), name)(*args), name)
 
 

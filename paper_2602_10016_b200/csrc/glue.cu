@@ -507,3 +507,37 @@ extern "C" int kl_check_finite(long long n, int dtype, const void* x, unsigned i
   count_launch();
   return launch_check("check_finite");
 }
+
+// ---------------------------------------------------------------------------
+// Fused Adam over the flat fp32 parameter buffer (SPEC.md:672-675 trainer
+// default: beta1 .9, beta2 .999, eps 1e-8), writing the bf16 compute mirror in
+// the same pass so no separate cast kernel runs before the next forward.
+namespace kl {
+namespace {
+__global__ void adam_kernel(long long n, float lr, float b1, float b2, float eps, float c1, float c2, float* w,
+                            const float* g, float* m, float* v, bf16* wc) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    float gi = g[i];
+    float mi = b1 * m[i] + (1.f - b1) * gi;
+    float vi = b2 * v[i] + (1.f - b2) * gi * gi;
+    m[i] = mi;
+    v[i] = vi;
+    float wi = w[i] - lr * (mi * c1) / (sqrtf(vi * c2) + eps);
+    w[i] = wi;
+    if (wc) wc[i] = __float2bfloat16(wi);
+  }
+}
+}  // namespace
+}  // namespace kl
+
+extern "C" int kl_adam_step(long long n, float lr, float beta1, float beta2, float eps, int step, float* w,
+                            const float* g, float* m, float* v, void* w_bf16, void* stream) {
+  if (n == 0) return KL_OK;
+  if (step < 1) { set_error("kl_adam_step: step must be >= 1"); return KL_EBADSHAPE; }
+  const float c1 = 1.f / (1.f - powf(beta1, (float)step));
+  const float c2 = 1.f / (1.f - powf(beta2, (float)step));
+  unsigned grid = (unsigned)std::min<long long>((n + 255) / 256, 148 * 16);
+  adam_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(n, lr, beta1, beta2, eps, c1, c2, w, g, m, v, (bf16*)w_bf16);
+  count_launch();
+  return launch_check("adam_step");
+}

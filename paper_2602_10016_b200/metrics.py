@@ -1,0 +1,90 @@
+"""FLOPs ledger and MFU, single source
+of truth for the bench.
+
+Convention (PaLM, cited by PAPER.md:77): count matmul MACs
+only, 1 MAC = 2 FLOPs, training = 3 x forward.  Two ledgers:
+
+* ``reference`` — the matmuls of the reference formulation
+  (gdpa.py:120-138, attention.py:69-93/142-145, seqsum.py:26-122,
+  interaction.py:106-157), band support (not dense T^2) for the window.
+* ``executed`` — the matmuls the B200 path actually launches (folded GDPA,
+  reassociated HSP pooling, SumKronLinear as two GEMMs), honouring CompSkip
+  and liveness pruning.  This is the MFU numerator; FLOPs removed by
+  reassociation are never claimed.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .attention import band_support_sizes
+from .interaction import ExpertPartition
+from .seqsum import SummarySplit
+
+
+def _support(T: int, w: int, causal: bool, length: int | None = None) -> int:
+    L = T if length is None else length
+    return int(band_support_sizes(L, w, causal).sum()) if L > 0 else 0
+
+
+def layer_macs(cfg, flags, live_seq: bool = True, formulation: str = "executed", lengths=None) -> dict:
+    """Per-sample forward MACs of one layer, by component."""
+    d, H = cfg.d, cfg.heads
+    d_h = d // H
+    out = {"wgen": 0, "gdpa": 0, "swa_proj": 0, "swa_core": 0, "hsp": 0, "sumkron": 0, "gi": 0}
+    for e, ev in enumerate(cfg.events):
+        T = ev.T if lengths is None else int(lengths[e])
+        split = SummarySplit.for_budget(ev.budget)
+        n_s, n_cls, n_tok = ev.n_seeds, split.n_cls, split.n_tokens
+        if live_seq and not flags.skip_pffn:
+            out["wgen"] += cfg.n_sum * cfg.n_ctx * d + 2 * cfg.n_kv * d_h * H * cfg.n_sum * d
+            if formulation == "executed":
+                out["gdpa"] += 2 * cfg.n_kv * d * d + 2 * T * d * H * cfg.n_kv
+            else:
+                out["gdpa"] += 2 * T * d * d + 2 * T * cfg.n_kv * d
+        if live_seq and not flags.skip_self_attention:
+            out["swa_proj"] += 4 * T * d * d
+            out["swa_core"] += 2 * _support(ev.T, ev.w, ev.causal, T) * d
+        if not flags.skip_hsp:
+            n_q = n_s + n_cls
+            if formulation == "executed":
+                # scores S Qt^T and pooling P^T S over all H*n_q queries, then
+                # value + output projections; batch-shared query folding is
+                # amortised over the batch and omitted (< 0.1%).
+                out["hsp"] += 2 * T * d * H * n_q + n_q * d * d + n_q * d * d
+                out["sumkron"] += ev.rank * (n_s * d * d + n_tok * n_s * d)
+            else:
+                out["hsp"] += (n_s * d * d + 2 * T * d * d + 2 * n_s * T * d + n_s * d * d)
+                if n_cls:
+                    out["hsp"] += (n_cls * d * d + 2 * T * d * d + 2 * n_cls * T * d + n_cls * d * d)
+                out["sumkron"] += ev.rank * (n_tok * n_s * d + n_tok * d * d)
+    part = ExpertPartition.contiguous(cfg.n_tot, cfg.experts)
+    for a, b in part.ranges:
+        n_i = b - a
+        n_pairs = n_i * (n_i + 1) // 2
+        gram = n_pairs * d if formulation == "executed" else n_i * n_i * d
+        out["gi"] += gram + n_pairs * n_i * d + 2 * n_i * d * cfg.expert_hidden
+    out["gi"] += cfg.n_ctx * cfg.n_tot * d
+    return out
+
+
+def model_macs(cfg, flags, live, formulation: str = "executed", lengths=None) -> dict:
+    """Per-sample forward MACs of the whole model (layers + head)."""
+    tot = {}
+    for l in range(cfg.L):
+        for k, v in layer_macs(cfg, flags[l], live[l], formulation, lengths).items():
+            tot[k] = tot.get(k, 0) + v
+    tot["head"] = cfg.n_ctx * cfg.d * cfg.head_hidden + cfg.head_hidden
+    tot["total"] = sum(tot.values())
+    return tot
+
+
+def train_flops_per_sample(cfg, flags, live, formulation: str = "executed") -> float:
+    """2 FLOPs per MAC, x3 for forward + backward."""
+    return 6.0 * model_macs(cfg, flags, live, formulation)["total"]
+
+
+def mfu(flops_per_sample: float, samples_per_s: float, peak_tflops: float) -> float:
+    """MFU = achieved FLOP/s / peak: 1e9 FLOPs x 100/s on a
+    1e12 peak -> 0.1."""
+    return flops_per_sample * samples_per_s / (peak_tflops * 1e12)
