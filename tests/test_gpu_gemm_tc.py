@@ -1,0 +1,119 @@
+"""tcgen05 GEMM (sm_100a) vs a torch float64 reference of the same op, over
+operand majors, tails, batching, batch reduction and the fused epilogue.
+The tcgen05 path is forced (kl_set_gemm_path(2)) so a shape it cannot take
+fails loudly instead of silently using the SIMT kernel."""
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(autouse=True)
+def force_tc():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2602_10016_b200 import _capi
+
+    _capi.lib().kl_set_gemm_path(2)
+    yield
+    _capi.lib().kl_set_gemm_path(0)
+
+
+def rel(a, b):
+    a, b = a.double(), b.double()
+    return float((a - b).abs().max() / b.abs().max().clamp_min(1e-30))
+
+
+def operand(shape, kmajor, g):
+    """(…, R, C) tensor whose last dim is contiguous if kmajor else the one before."""
+    t = torch.randn(*shape, device="cuda", generator=g).to(torch.bfloat16)
+    if kmajor:
+        return t
+    return t.transpose(-1, -2).contiguous().transpose(-1, -2)
+
+
+@pytest.mark.parametrize("a_k", [True, False])
+@pytest.mark.parametrize("b_n", [True, False])
+@pytest.mark.parametrize("M,N,K", [(128, 64, 64), (304, 160, 200), (1024, 768, 256), (64, 256, 1024), (264, 48, 72)])
+def test_tc_plain(a_k, b_n, M, N, K):
+    from paper_2602_10016_b200._capi import gemm
+
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    A = operand((M, K), a_k, g)
+    B = operand((K, N), b_n, g)
+    ref = A.double() @ B.double()
+    out = gemm(A, B, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    assert rel(out, ref) < 1e-5
+    outb = gemm(A, B)  # bf16 output
+    assert rel(outb, ref) < 1e-2
+
+
+@pytest.mark.parametrize("a_k", [True, False])
+def test_tc_batched_reduce(a_k):
+    from paper_2602_10016_b200._capi import gemm
+
+    g = torch.Generator(device="cuda").manual_seed(7)
+    A = operand((3, 4, 200, 96), a_k, g)
+    B = operand((1, 4, 96, 144), True, g)
+    ref = A.double() @ B.double()
+    out = gemm(A, B, out_dtype=torch.float32)
+    assert rel(out, ref) < 1e-5
+    out = gemm(A, B, out_dtype=torch.float32, reduce=(True, False))
+    assert rel(out, ref.sum(0, keepdim=True)) < 1e-5
+    out = gemm(A, B.expand(3, 4, 96, 144), out_dtype=torch.float32, reduce=(True, True))
+    assert rel(out, ref.sum((0, 1), keepdim=True)) < 1e-5
+
+
+def test_tc_epilogue():
+    from paper_2602_10016_b200._capi import gemm
+
+    g = torch.Generator(device="cuda").manual_seed(9)
+    A = operand((2, 300, 128), True, g)
+    B = operand((128, 96), False, g)
+    R = torch.randn(2, 300, 96, device="cuda", generator=g)
+    Cin = torch.randn(2, 300, 96, device="cuda", generator=g)
+    bias = torch.randn(96, device="cuda", generator=g)
+    lim = torch.tensor([300, 77], device="cuda", dtype=torch.int32)
+    out = Cin.clone()
+    pre = torch.empty_like(out)
+    gemm(A, B, out, alpha=0.25, beta=1.0, bias=bias, acts=["silu", "tanh"], act_group=48, aux=pre, aux_mode=1,
+         residual=R, row_limit=lim)
+    z = 0.25 * (A.double() @ B.double()) + bias.double()
+    act = torch.cat([torch.nn.functional.silu(z[..., :48]), torch.tanh(z[..., 48:])], -1)
+    full = act + Cin.double() + R.double()
+    rows = torch.arange(300, device="cuda")[None, :, None]
+    keep = rows < lim.view(2, 1, 1)
+    assert rel(torch.where(keep, out.double(), 0), torch.where(keep, full, 0)) < 1e-5
+    assert float(out[1, 77:].abs().max()) == 0.0
+    # dact mode: out = acc * act'(aux)
+    d = torch.empty_like(out)
+    gemm(A, B, d, acts=["silu", "tanh"], act_group=48, aux=pre, aux_mode=2)
+    acc = A.double() @ B.double()
+    pz = pre.double()
+    s = torch.sigmoid(pz[..., :48])
+    der = torch.cat([s * (1 + pz[..., :48] * (1 - s)), 1 - torch.tanh(pz[..., 48:]) ** 2], -1)
+    assert rel(d, acc * der) < 1e-5
+
+
+def test_tc_strided_views():
+    """Operand views used by the model: head-strided W_out, transposed
+    activations, permuted outputs."""
+    from paper_2602_10016_b200._capi import gemm
+
+    g = torch.Generator(device="cuda").manual_seed(11)
+    H, dh, d, B, n = 4, 64, 256, 8, 160
+    W = torch.randn(d, d, device="cuda", generator=g).to(torch.bfloat16)
+    Wv = W.view(d, H, dh).permute(1, 2, 0)  # (H, dh, d), K-major B
+    V = torch.randn(B, H, n, dh, device="cuda", generator=g).to(torch.bfloat16)
+    out = gemm(V, Wv, out_dtype=torch.float32)
+    assert rel(out, V.double() @ Wv.double()) < 1e-5
+    S = torch.randn(B, 1024, d, device="cuda", generator=g).to(torch.bfloat16)
+    P = torch.randn(B, 1024, n, device="cuda", generator=g).to(torch.bfloat16)
+    pooled = gemm(P.transpose(1, 2), S, out_dtype=torch.float32)  # M-major A, N-major B
+    assert rel(pooled, P.double().transpose(1, 2) @ S.double()) < 1e-5
+    o = torch.empty(B, n, H, dh, device="cuda", dtype=torch.float32)
+    X = torch.randn(B, H, n, d, device="cuda", generator=g).to(torch.bfloat16)
+    gemm(X, Wv.transpose(1, 2), o.permute(0, 2, 1, 3))
+    assert rel(o.permute(0, 2, 1, 3), X.double() @ Wv.double().transpose(1, 2)) < 1e-5
