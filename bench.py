@@ -196,6 +196,7 @@ def main():
     ap.add_argument("--cpu-workers", type=int, default=32)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--gemm-census", action="store_true", help="log every kl_gemm shape/path of one step to stderr")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
 
@@ -260,6 +261,16 @@ def main():
     for _ in range(args.warmup):
         step(X, S, y)
     barrier()
+    if args.gemm_census:
+        _capi.GEMM_LOG = []
+        step(X, S, y)
+        torch.cuda.synchronize()
+        import collections
+
+        c = collections.Counter(_capi.GEMM_LOG)
+        for k, v in sorted(c.items(), key=lambda kv: -kv[0][0] * kv[0][1] * kv[0][2] * kv[0][3] * kv[0][4]):
+            print("gemm", v, "x", k, file=sys.stderr)
+        _capi.GEMM_LOG = None
 
     # ---- device-timed region: inputs resident in HBM ----------------------
     timed_ops = {"kl_swa_fwd": [], "kl_swa_bwd": []}

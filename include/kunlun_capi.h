@@ -58,6 +58,8 @@ unsigned long long kl_launch_count(void);
 int kl_tcgen05_available(void);
 /* Force the SIMT GEMM even for bf16 (debug / A-B testing).  0 = auto. */
 void kl_set_gemm_path(int path);
+/* Path the last kl_gemm call on this thread took: 1 tcgen05, 0 SIMT. */
+int kl_last_gemm_path(void);
 
 /*
  * Strided, batched, optionally batch-reducing GEMM with a fused epilogue.

@@ -73,6 +73,7 @@ _SIGS = {
     "kl_launch_count": ([], C.c_ulonglong),
     "kl_tcgen05_available": ([], C.c_int),
     "kl_set_gemm_path": ([C.c_int], None),
+    "kl_last_gemm_path": ([], C.c_int),
     "kl_gemm": ([C.POINTER(GemmArgs), C.c_void_p], C.c_int),
     "kl_swa_fwd": ([C.POINTER(SwaArgs), C.c_void_p], C.c_int),
     "kl_swa_bwd": ([C.POINTER(SwaArgs), C.c_void_p], C.c_int),
@@ -235,7 +236,13 @@ def gemm(A: torch.Tensor, B: torch.Tensor, out: torch.Tensor | None = None, *, o
         for i, c in enumerate(codes):
             a.act_codes[i] = c
     _check(lib().kl_gemm(C.byref(a), _stream()), "kl_gemm")
+    if GEMM_LOG is not None:
+        GEMM_LOG.append((M, N, K, nb1, nb2, int(red1), int(red2), (a.a_rs, a.a_cs), (a.b_rs, a.b_cs),
+                         (a.c_rs, a.c_cs), a.c_dtype, lib().kl_last_gemm_path()))
     return ret
+
+
+GEMM_LOG = None  # list of (M, N, K, nb1, nb2, red1, red2, A/B/C strides, c_dtype, path) when set
 
 
 def swa_args(qkv, lengths, H, d_h, w, causal, O, LSE, dO=None, dqkv=None, Dbuf=None) -> SwaArgs:

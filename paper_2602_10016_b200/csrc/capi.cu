@@ -15,6 +15,7 @@ namespace kl {
 static thread_local char g_err[512] = "";
 static std::atomic<unsigned long long> g_launches{0};
 static int g_gemm_path = 0;  // 0 auto, 1 force SIMT, 2 force tcgen05 (error if unsupported)
+static int g_last_path = -1; // path the last kl_gemm took: 1 tcgen05, 0 SIMT
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -44,6 +45,7 @@ extern "C" int kl_version(void) { return 1; }
 extern "C" const char* kl_last_error(void) { return g_err; }
 extern "C" unsigned long long kl_launch_count(void) { return g_launches.load(); }
 extern "C" void kl_set_gemm_path(int path) { g_gemm_path = path; }
+extern "C" int kl_last_gemm_path(void) { return kl::g_last_path; }
 
 extern "C" int kl_tcgen05_available(void) {
   int dev = 0, major = 0, minor = 0;
@@ -95,12 +97,14 @@ extern "C" int kl_gemm(const kl_gemm_args* a, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   if (a->ab_dtype == KL_BF16 && g_gemm_path != 1) {
     int rc = gemm_tc(g, e, s);
+    g_last_path = 1;
     if (rc != KL_EUNSUPPORTED) return rc;
     if (g_gemm_path == 2) {
       set_error("kl_gemm: tcgen05 path forced but shape unsupported (M=%d N=%d K=%d)", a->M, a->N, a->K);
       return KL_EUNSUPPORTED;
     }
   }
+  g_last_path = 0;
   return gemm_simt(g, e, s);
 }
 

@@ -4,6 +4,8 @@
 // cannot meet the 1e-5 contract) and the fallback for
 // shapes the tcgen05 kernel does not take (tiny M/N, unaligned strides).
 // 64x64 output tile, BK=16, 256 threads, 4x4 register micro-tile.
+#include <algorithm>
+
 #include "common.cuh"
 #include "gemm.h"
 
@@ -14,7 +16,7 @@ namespace {
 constexpr int BM = 64, BN = 64, BK = 16;
 
 template <typename TA, typename TC>
-__global__ void __launch_bounds__(256) gemm_simt_kernel(GemmDesc g, Epi e) {
+__global__ void __launch_bounds__(256) gemm_simt_kernel(GemmDesc g, Epi e, int splits) {
   __shared__ float As[BK][BM + 4];
   __shared__ float Bs[BK][BN + 4];
   const TA* __restrict__ A = (const TA*)g.A;
@@ -24,7 +26,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmDesc g, Epi e) {
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   // decompose the output batch index over the non-reduced batch dims
   const int nb2o = g.red2 ? 1 : g.nb2;
-  const int zo = blockIdx.z;
+  const int zo = blockIdx.z / splits, sp = blockIdx.z % splits;
   const int z1o = g.red1 ? 0 : zo / nb2o;
   const int z2o = g.red2 ? 0 : zo % nb2o;
   const int r1n = g.red1 ? g.nb1 : 1, r2n = g.red2 ? g.nb2 : 1;
@@ -37,13 +39,18 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmDesc g, Epi e) {
 
   const bool a_kfast = (g.a_cs == 1);
   const bool b_nfast = (g.b_cs == 1);
-  for (int r1 = 0; r1 < r1n; ++r1) {
-    for (int r2 = 0; r2 < r2n; ++r2) {
+  const int kbn = (g.K + BK - 1) / BK;
+  const int iters = r1n * r2n * kbn;
+  const int it0 = (int)((long long)iters * sp / splits), it1 = (int)((long long)iters * (sp + 1) / splits);
+  for (int it = it0; it < it1; ++it) {
+    {
+      const int r = it / kbn, k0 = (it % kbn) * BK;
+      const int r1 = r / r2n, r2 = r % r2n;
       const int z1 = g.red1 ? r1 : z1o;
       const int z2 = g.red2 ? r2 : z2o;
       const TA* Ab = A + (long long)z1 * g.a_s1 + (long long)z2 * g.a_s2;
       const TA* Bb = Bp + (long long)z1 * g.b_s1 + (long long)z2 * g.b_s2;
-      for (int k0 = 0; k0 < g.K; k0 += BK) {
+      {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           int e_ = tid + 256 * i;
@@ -91,7 +98,10 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmDesc g, Epi e) {
       const int n = n0 + tx * 4 + j;
       if (n >= g.N) continue;
       const long long off = (long long)m * g.c_rs + (long long)n * g.c_cs;
-      epilogue_store(e, C, R, X, off, (long long)m * g.r_rs + (long long)n * g.r_cs, m, n, lim, acc[i][j]);
+      if (splits > 1)
+        atomicAdd((float*)C + off, e.alpha * acc[i][j]);
+      else
+        epilogue_store(e, C, R, X, off, (long long)m * g.r_rs + (long long)n * g.r_cs, m, n, lim, acc[i][j]);
     }
   }
 }
@@ -100,19 +110,26 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmDesc g, Epi e) {
 
 int gemm_simt(const GemmDesc& g, const Epi& e, cudaStream_t s) {
   const int nout = (g.red1 ? 1 : g.nb1) * (g.red2 ? 1 : g.nb2);
-  dim3 grid((g.N + BN - 1) / BN, (g.M + BM - 1) / BM, nout);
+  const long long tiles = (long long)((g.N + BN - 1) / BN) * ((g.M + BM - 1) / BM) * nout;
+  const long long iters = (long long)(g.red1 ? g.nb1 : 1) * (g.red2 ? g.nb2 : 1) * ((g.K + BK - 1) / BK);
+  const bool accum_only = g.c_dtype == KL_F32 && e.beta == 1.f && !e.bias && !e.row_limit && !e.aux_mode &&
+                          e.n_act == 0 && !g.R;
+  int splits = 1;
+  if (accum_only && tiles < 4 * 148 && iters >= 16)
+    splits = (int)std::max<long long>(1, std::min<long long>((4 * 148) / tiles, iters / 8));
+  dim3 grid((g.N + BN - 1) / BN, (g.M + BM - 1) / BM, nout * splits);
   if (grid.y > 65535 || grid.z > 65535) {
     set_error("kl_gemm: grid too large (M=%d, batches=%d)", g.M, nout);
     return KL_EUNSUPPORTED;
   }
   if (g.ab_dtype == KL_F32 && g.c_dtype == KL_F32)
-    gemm_simt_kernel<float, float><<<grid, 256, 0, s>>>(g, e);
+    gemm_simt_kernel<float, float><<<grid, 256, 0, s>>>(g, e, splits);
   else if (g.ab_dtype == KL_F32 && g.c_dtype == KL_BF16)
-    gemm_simt_kernel<float, bf16><<<grid, 256, 0, s>>>(g, e);
+    gemm_simt_kernel<float, bf16><<<grid, 256, 0, s>>>(g, e, splits);
   else if (g.ab_dtype == KL_BF16 && g.c_dtype == KL_F32)
-    gemm_simt_kernel<bf16, float><<<grid, 256, 0, s>>>(g, e);
+    gemm_simt_kernel<bf16, float><<<grid, 256, 0, s>>>(g, e, splits);
   else
-    gemm_simt_kernel<bf16, bf16><<<grid, 256, 0, s>>>(g, e);
+    gemm_simt_kernel<bf16, bf16><<<grid, 256, 0, s>>>(g, e, splits);
   count_launch();
   return launch_check("gemm_simt");
 }

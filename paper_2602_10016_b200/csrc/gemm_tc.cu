@@ -36,6 +36,7 @@ struct TcParams {
   uint32_t a_stage_bytes, b_stage_bytes;
   uint32_t acc_stride;
   uint32_t tmem_cols;
+  int splits;  // split-K over the (reduced batch x k-block) iterations; >1 -> fp32 atomics
   void* C;
   long long c_rs, c_cs, c_s1, c_s2;
   const void* R;
@@ -43,7 +44,7 @@ struct TcParams {
   void* aux;
 };
 
-template <typename TC>
+template <typename TC, bool PLAIN>
 __global__ void __launch_bounds__(NTHREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcParams p,
                    Epi e) {
@@ -51,7 +52,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;
   uint8_t* sB = sA + p.stages * p.a_stage_bytes;
-  uint64_t* full = (uint64_t*)(sB + p.stages * p.b_stage_bytes);
+  float* stage_buf = (float*)(sB + p.stages * p.b_stage_bytes);  // 4 warps x 32 x 33 fp32
+  uint64_t* full = (uint64_t*)(stage_buf + 4 * 32 * 33);
   uint64_t* empty = full + p.stages;
   uint64_t* tfull = empty + p.stages;
   uint64_t* tempty = tfull + 2;
@@ -77,8 +79,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   tc::fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  const int total = p.tiles_m * p.tiles_n * p.n_out;
   const int n_red = (p.red1 ? p.nb1 : 1) * (p.red2 ? p.nb2 : 1);
+  const int iters = n_red * p.kblocks;
+  const int total = p.tiles_m * p.tiles_n * p.n_out * p.splits;
   const int nb2o = p.red2 ? 1 : p.nb2;
   const int r2n = p.red2 ? p.nb2 : 1;
 
@@ -87,17 +90,20 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       const uint32_t tx = p.a_stage_bytes + p.b_stage_bytes;
-      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+      for (int unit = blockIdx.x; unit < total; unit += gridDim.x) {
+        const int tile = unit / p.splits, sp = unit % p.splits;
+        const int it0 = (int)((long long)iters * sp / p.splits), it1 = (int)((long long)iters * (sp + 1) / p.splits);
         const int mb = tile % p.tiles_m;
         const int nb = (tile / p.tiles_m) % p.tiles_n;
         const int zo = tile / (p.tiles_m * p.tiles_n);
         const int z1o = p.red1 ? 0 : zo / nb2o, z2o = p.red2 ? 0 : zo % nb2o;
-        for (int r = 0; r < n_red; ++r) {
+        for (int it = it0; it < it1; ++it) {
+          const int r = it / p.kblocks, kb = it % p.kblocks;
           const int z1 = p.red1 ? r / r2n : z1o;
           const int z2 = p.red2 ? r % r2n : z2o;
           const int a1 = p.a_has1 ? z1 : 0, a2 = p.a_has2 ? z2 : 0;
           const int b1 = p.b_has1 ? z1 : 0, b2 = p.b_has2 ? z2 : 0;
-          for (int kb = 0; kb < p.kblocks; ++kb) {
+          {
             tc::mbar_wait(&empty[stage], phase ^ 1);
             tc::mbar_arrive_expect_tx(&full[stage], tx);
             uint8_t* da = sA + stage * p.a_stage_bytes;
@@ -128,14 +134,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int t = 0;
-      const int iters = n_red * p.kblocks;
-      for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++t) {
+      for (int unit = blockIdx.x; unit < total; unit += gridDim.x, ++t) {
+        const int sp = unit % p.splits;
+        const int it0 = (int)((long long)iters * sp / p.splits), it1 = (int)((long long)iters * (sp + 1) / p.splits);
         const int acc = t & 1;
         const uint32_t acc_phase = (t >> 1) & 1;
         tc::mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc::fence_after();
         const uint32_t d = tmem + acc * p.acc_stride;
-        for (int it = 0; it < iters; ++it) {
+        for (int it = it0; it < it1; ++it) {
           tc::mbar_wait(&full[stage], phase);
           tc::fence_after();
           const uint32_t a0 = tc::smem_u32(sA + stage * p.a_stage_bytes);
@@ -144,7 +151,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           for (int k = 0; k < BK / 16; ++k) {
             const uint64_t ad = p.a_mn ? tc::sdesc(a0 + k * 2048, 8192, 1024) : tc::sdesc(a0 + k * 32, 16, 1024);
             const uint64_t bd = p.b_mn ? tc::sdesc(b0 + k * 2048, 8192, 1024) : tc::sdesc(b0 + k * 32, 16, 1024);
-            tc::mma_bf16(d, ad, bd, idesc, (it > 0 || k > 0) ? 1u : 0u);
+            tc::mma_bf16(d, ad, bd, idesc, (it > it0 || k > 0) ? 1u : 0u);
           }
           tc::mma_commit(&empty[stage]);
           if (++stage == p.stages) {
@@ -158,7 +165,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   } else {
     const int lane_base = (warp & 3) * 32;
     int t = 0;
-    for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++t) {
+    for (int unit = blockIdx.x; unit < total; unit += gridDim.x, ++t) {
+      const int tile = unit / p.splits;
       const int acc = t & 1;
       const uint32_t acc_phase = (t >> 1) & 1;
       const int mb = tile % p.tiles_m;
@@ -171,22 +179,41 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       TC* X = p.aux ? (TC*)p.aux + (long long)z1o * (p.red1 ? 0 : p.c_s1) + (long long)z2o * (p.red2 ? 0 : p.c_s2)
                     : nullptr;
       const int lim = e.row_limit ? e.row_limit[zo] : 0x7fffffff;
-      const int m = mb * BM + lane_base + lane;
+      const int m0 = mb * BM + lane_base;
+      float* stg = stage_buf + (warp - 2) * 32 * 33;
       tc::mbar_wait(&tfull[acc], acc_phase);
       tc::fence_after();
       const uint32_t tbase = tmem + acc * p.acc_stride + ((uint32_t)lane_base << 16);
-      for (int c0 = 0; c0 < p.BN; c0 += 16) {
-        float v[16];
+      for (int c0 = 0; c0 < p.BN; c0 += 32) {
+        // TMEM row (lane) -> smem transpose -> lanes walk columns: coalesced
+        // global reads (residual / C) and writes, one row per iteration.
+        float v[32];
         tc::tmem_ld16(tbase + c0, v);
-        if (m < p.M) {
+        if (c0 + 16 < p.BN) tc::tmem_ld16(tbase + c0 + 16, v + 16);
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int n = nb * p.BN + c0 + j;
-            if (n < p.N && c0 + j < p.BN)
+        for (int j = 0; j < 32; ++j) stg[lane * 33 + j] = v[j];
+        __syncwarp();
+        const int n = nb * p.BN + c0 + lane;
+        const bool ncol = (n < p.N) && (c0 + lane < p.BN);
+        const int rows = min(32, p.M - m0);
+        if (p.splits > 1) {
+          // split-K partial: C += alpha * partial (fp32, beta == 1 accumulate)
+          float* cp = (float*)C + (long long)m0 * p.c_rs + (long long)n * p.c_cs;
+          for (int r = 0; r < rows; ++r)
+            if (ncol) atomicAdd(cp + (long long)r * p.c_rs, e.alpha * stg[r * 33 + lane]);
+        } else if (PLAIN) {
+          TC* cp = C + (long long)m0 * p.c_rs + (long long)n * p.c_cs;
+          for (int r = 0; r < rows; ++r)
+            if (ncol) stf(cp + (long long)r * p.c_rs, stg[r * 33 + lane]);
+        } else {
+          for (int r = 0; r < rows; ++r) {
+            const int m = m0 + r;
+            if (ncol)
               epilogue_store(e, C, R, X, (long long)m * p.c_rs + (long long)n * p.c_cs,
-                             (long long)m * p.r_rs + (long long)n * p.r_cs, m, n, lim, v[j]);
+                             (long long)m * p.r_rs + (long long)n * p.r_cs, m, n, lim, stg[r * 33 + lane]);
           }
         }
+        __syncwarp();
       }
       tc::fence_before();
       __syncwarp();
@@ -285,7 +312,7 @@ int gemm_tc(const GemmDesc& g, const Epi& e, cudaStream_t s) {
   p.a_stage_bytes = BM * BK * 2;
   p.b_stage_bytes = b_n ? p.b_boxes * 64 * BK * 2 : bn * BK * 2;
   const uint32_t stage = p.a_stage_bytes + p.b_stage_bytes;
-  p.stages = std::min<int>(8, (200 * 1024) / stage);
+  p.stages = std::min<int>(8, (190 * 1024) / stage);
   if (p.stages < 2) return KL_EUNSUPPORTED;
   p.acc_stride = bn > 128 ? 256 : (bn > 64 ? 128 : (bn > 32 ? 64 : 32));
   p.tmem_cols = 2 * p.acc_stride;
@@ -318,15 +345,32 @@ int gemm_tc(const GemmDesc& g, const Epi& e, cudaStream_t s) {
   p.r_s2 = g.r_s2;
   p.aux = g.aux;
 
-  const size_t smem = 1024 + (size_t)p.stages * stage + (2 * p.stages + 4) * 8 + 16;
-  const int total = p.tiles_m * p.tiles_n * p.n_out;
+  const size_t smem = 1024 + (size_t)p.stages * stage + 4 * 32 * 33 * 4 + (2 * p.stages + 4) * 8 + 16;
+  const int tiles = p.tiles_m * p.tiles_n * p.n_out;
+  const int iters = ((g.red1 ? g.nb1 : 1) * (g.red2 ? g.nb2 : 1)) * p.kblocks;
+  p.splits = 1;
+  // Weight-gradient shape: few output tiles, a long reduction.  Spread the
+  // reduction over the SMs; partial tiles accumulate with fp32 atomics, so
+  // only an fp32 accumulate-into-C epilogue (beta == 1, nothing else) qualifies.
+  const bool accum_only = g.c_dtype == KL_F32 && e.beta == 1.f && !e.bias && !e.row_limit && !e.aux_mode &&
+                          e.n_act == 0 && !g.R;
+  if (accum_only && tiles < num_sms() && iters >= 8) {
+    p.splits = std::max(1, std::min(num_sms() / tiles, iters / 4));
+  }
+  const int total = tiles * p.splits;
   const int grid = std::min(total, num_sms());
+  const bool plain = e.alpha == 1.f && e.beta == 0.f && !e.bias && !e.row_limit && !e.aux_mode && e.n_act == 0 &&
+                     !g.R;
+  auto launch = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<grid, NTHREADS, smem, s>>>(ta, tb, p, e);
+  };
   if (g.c_dtype == KL_BF16) {
-    cudaFuncSetAttribute(gemm_tc_kernel<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    gemm_tc_kernel<bf16><<<grid, NTHREADS, smem, s>>>(ta, tb, p, e);
+    if (plain) launch(gemm_tc_kernel<bf16, true>);
+    else launch(gemm_tc_kernel<bf16, false>);
   } else {
-    cudaFuncSetAttribute(gemm_tc_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    gemm_tc_kernel<float><<<grid, NTHREADS, smem, s>>>(ta, tb, p, e);
+    if (plain) launch(gemm_tc_kernel<float, true>);
+    else launch(gemm_tc_kernel<float, false>);
   }
   count_launch();
   return launch_check("gemm_tc");

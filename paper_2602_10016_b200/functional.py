@@ -320,7 +320,8 @@ class _HspPool(torch.autograd.Function):
         gemm(dsc, Q.unsqueeze(0).expand(S.shape[0], -1, -1), dS, beta=1.0)
         # dQ = sum_b dsc^T S: softmax-VJP rows sum to zero over t, so this
         # reduction cancels; bf16 runs it on the hi + lo split of dsc.
-        dQ = gemm(dsc.transpose(1, 2).unsqueeze(0), S.unsqueeze(0), reduce=(False, True), out_dtype=torch.float32)
+        dQ = torch.zeros(1, 1, Q.shape[0], Q.shape[1], device=S.device, dtype=torch.float32)
+        gemm(dsc.transpose(1, 2).unsqueeze(0), S.unsqueeze(0), dQ, beta=1.0, reduce=(False, True))
         if lo is not None:
             gemm(lo.transpose(1, 2).unsqueeze(0), S.unsqueeze(0), dQ, beta=1.0, reduce=(False, True))
         dQ = dQ.reshape(Q.shape)
