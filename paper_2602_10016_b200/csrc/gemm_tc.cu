@@ -377,3 +377,8 @@ int gemm_tc(const GemmDesc& g, const Epi& e, cudaStream_t s) {
 }
 
 }  // namespace kl
+
+namespace kl {
+PFN_cuTensorMapEncodeTiled_v12000 tc_encode_fn() { return encode_fn(); }
+int tc_num_sms() { return num_sms(); }
+}  // namespace kl

@@ -360,3 +360,19 @@ int swa_support(const SwaP& p, int* support, cudaStream_t s) {
 }
 
 }  // namespace kl
+
+namespace kl {
+// D[b,h,t] = rowsum(dO * O) for the tcgen05 backward kernels.
+int swa_rowdot(const SwaP& p, cudaStream_t s) {
+  long long total = (long long)p.B * p.H * p.T;
+  unsigned g = (unsigned)((total + 255) / 256);
+  if (p.dtype == KL_BF16 && p.d_h == 64) swa_rowdot_kernel<bf16, 64><<<g, 256, 0, s>>>(p);
+  else if (p.dtype == KL_F32 && p.d_h == 64) swa_rowdot_kernel<float, 64><<<g, 256, 0, s>>>(p);
+  else {
+    set_error("swa_rowdot: unsupported head dim %d", p.d_h);
+    return KL_EUNSUPPORTED;
+  }
+  count_launch();
+  return launch_check("swa_rowdot");
+}
+}  // namespace kl

@@ -1,0 +1,525 @@
+// Sliding-window multi-head attention on tcgen05 (sm_100a), head dim 64.
+//
+// Reference semantics: attention.py:69-129 (band |i-j| <= w, optional causal,
+// length mask; fully-masked rows -> 0 via masked_softmax_lastdim,
+// tensor.py:485-505), scale 1/sqrt(d_h) (attention.py:83).
+//
+// One CTA per (sample, head, 128-row block).  With w <= 128 a 128-query block
+// sees at most three 128-key blocks, so every score block of a tile fits in
+// TMEM at once (3 x 128 columns + the 64-column O accumulator): the softmax is
+// computed exactly (row max over all visible keys first, then exp / sum), no
+// online rescaling, and P never leaves the SM.  Key blocks outside the band are
+// never loaded.
+//
+//   warp 0      TMA: Q / K / V (/ dO) blocks, 128 x 64 bf16, SWIZZLE_128B
+//   warp 1      single-thread tcgen05.mma issue
+//   warps 2..5  softmax / gradient math, thread = TMEM lane = row
+//
+// Backward (FA2 structure): a KV-major kernel accumulates dK, dV in TMEM over
+// the <= 3 query blocks that see the key block; a Q-major kernel accumulates
+// dQ over the <= 3 key blocks; probabilities are recomputed from the forward
+// log-sum-exp.  No atomics.
+#include <cudaTypedefs.h>
+
+#include "swa.h"
+#include "tc_common.cuh"
+
+namespace kl {
+
+PFN_cuTensorMapEncodeTiled_v12000 tc_encode_fn();
+int tc_num_sms();
+
+namespace {
+
+constexpr int TB = 128;                 // query / key block
+constexpr int DH = 64;                  // head dim handled here
+constexpr int TILE = TB * DH * 2;       // 16 KB: a 128 x 64 bf16 block
+constexpr int PBLK = TB * TB * 2;       // 32 KB: a 128 x 128 bf16 P / dS block
+constexpr int NT = 192;
+
+constexpr uint32_t IDESC_S = tc::idesc_bf16(128, 128, 0, 0);   // S = X Y^T, both K-major
+constexpr uint32_t IDESC_PV = tc::idesc_bf16(128, 64, 0, 1);   // O += P V, V MN-major
+
+__device__ __forceinline__ uint64_t d_kmaj64(uint32_t base, int kk) { return tc::sdesc(base + kk * 32, 16, 1024); }
+__device__ __forceinline__ uint64_t d_p(uint32_t base, int kk) {
+  return tc::sdesc(base + (kk >> 2) * (TB * 128) + (kk & 3) * 32, 16, 1024);
+}
+__device__ __forceinline__ uint64_t d_mn(uint32_t base, int kk) { return tc::sdesc(base + kk * 2048, 8192, 1024); }
+
+__device__ __forceinline__ bool valid(int q, int k, int len, int w, int causal) {
+  if (q >= len || k >= len || k < 0) return false;
+  const int dd = q - k;
+  if (dd > w || -dd > w) return false;
+  return !(causal && k > q);
+}
+
+struct Band {
+  int lo, n;
+};
+// 128-blocks of keys seen by queries [q0, q0+128) (forward / dQ).
+__device__ __forceinline__ Band key_band(int q0, int len, int w, int causal) {
+  int lo = max(0, q0 - w);
+  int hi = min(len - 1, q0 + TB - 1 + w);
+  if (causal) hi = min(hi, q0 + TB - 1);
+  return {lo / TB, hi / TB - lo / TB + 1};
+}
+// 128-blocks of queries that see keys [k0, k0+128) (dK / dV).
+__device__ __forceinline__ Band query_band(int k0, int len, int w, int causal) {
+  int lo = max(0, k0 - w);
+  if (causal) lo = max(lo, k0);
+  int hi = min(len - 1, k0 + TB - 1 + w);
+  return {lo / TB, hi / TB - lo / TB + 1};
+}
+
+// Store a 64-wide fp32 TMEM row (two tcgen05.ld.x32) as bf16, scaled.  The
+// TMEM loads are warp-collective (.sync.aligned): every lane executes them and
+// only the global store is predicated on `ok`.
+__device__ __forceinline__ void store_row64(bf16* dst, uint32_t taddr, float scale, bool ok) {
+  float v[32];
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    tc::tmem_ld32(taddr + half * 32, v);
+    if (!ok) continue;
+    uint4* o = reinterpret_cast<uint4*>(dst + half * 32);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      uint4 u;
+      u.x = tc::pack_bf16(v[8 * c + 0] * scale, v[8 * c + 1] * scale);
+      u.y = tc::pack_bf16(v[8 * c + 2] * scale, v[8 * c + 3] * scale);
+      u.z = tc::pack_bf16(v[8 * c + 4] * scale, v[8 * c + 5] * scale);
+      u.w = tc::pack_bf16(v[8 * c + 6] * scale, v[8 * c + 7] * scale);
+      o[c] = u;
+    }
+  }
+}
+
+// Write 32 bf16 (one tcgen05.ld.x32 worth) of row r, columns [c0, c0+32), into
+// a K-major SWIZZLE_128B 128 x 128 block.
+__device__ __forceinline__ void store_sw(uint8_t* blk, int r, int c0, const uint32_t* pk) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    uint4 u = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+    *reinterpret_cast<uint4*>(blk + tc::sw128_off(r, c0 + 8 * c, TB)) = u;
+  }
+}
+
+__device__ __forceinline__ void zero_rows(bf16* base, long long ld, int r0, int rows, int T, int tid, int nthr) {
+  for (int i = tid; i < rows * DH; i += nthr) {
+    const int r = r0 + i / DH;
+    if (r < T) base[(long long)r * ld + i % DH] = __float2bfloat16(0.f);
+  }
+}
+
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(NT, 1) swa_fwd_tc_kernel(const __grid_constant__ CUtensorMap tq, SwaP p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sQ = sm;
+  uint8_t* sK = sQ + TILE;
+  uint8_t* sV = sK + 3 * TILE;
+  uint8_t* sP = sV + 3 * TILE;
+  uint64_t* bar = (uint64_t*)(sP + 3 * PBLK);  // qk, v, s, p, o
+  uint32_t* tslot = (uint32_t*)(bar + 8);
+
+  const int b = blockIdx.z, h = blockIdx.y, q0 = blockIdx.x * TB;
+  const int len = p.lengths[b];
+  const int HD = p.H * DH;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  bf16* O = (bf16*)p.O + (long long)b * p.bs_o + h * DH;
+  if (q0 >= len) {  // padding-only tile: O = 0, LSE = +inf
+    zero_rows(O, p.ld_o, q0, TB, p.T, threadIdx.x, NT);
+    for (int r = threadIdx.x; r < TB; r += NT)
+      if (q0 + r < p.T) p.LSE[((long long)b * p.H + h) * p.T + q0 + r] = INFINITY;
+    return;
+  }
+  const Band kb = key_band(q0, len, p.w, p.causal);
+  if (warp == 0 && lane == 0) {
+    tc::prefetch_tmap(&tq);
+    tc::mbar_init(&bar[0], 1);
+    tc::mbar_init(&bar[1], 1);
+    tc::mbar_init(&bar[2], 1);
+    tc::mbar_init(&bar[3], 4);
+    tc::mbar_init(&bar[4], 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tslot, 512);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      tc::mbar_arrive_expect_tx(&bar[0], (1 + kb.n) * TILE);
+      tc::tma_load_3d(sQ, &tq, &bar[0], h * DH, q0, b);
+      for (int j = 0; j < kb.n; ++j) tc::tma_load_3d(sK + j * TILE, &tq, &bar[0], HD + h * DH, (kb.lo + j) * TB, b);
+      tc::mbar_arrive_expect_tx(&bar[1], kb.n * TILE);
+      for (int j = 0; j < kb.n; ++j)
+        tc::tma_load_3d(sV + j * TILE, &tq, &bar[1], 2 * HD + h * DH, (kb.lo + j) * TB, b);
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      tc::mbar_wait(&bar[0], 0);
+      tc::fence_after();
+      const uint32_t q = tc::smem_u32(sQ);
+      for (int j = 0; j < kb.n; ++j) {
+        const uint32_t k = tc::smem_u32(sK + j * TILE);
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk)
+          tc::mma_bf16(tmem + j * TB, d_kmaj64(q, kk), d_kmaj64(k, kk), IDESC_S, kk > 0);
+      }
+      tc::mma_commit(&bar[2]);
+      tc::mbar_wait(&bar[3], 0);
+      tc::mbar_wait(&bar[1], 0);
+      tc::fence_after();
+      for (int j = 0; j < kb.n; ++j) {
+        const uint32_t pp = tc::smem_u32(sP + j * PBLK), v = tc::smem_u32(sV + j * TILE);
+#pragma unroll
+        for (int kk = 0; kk < TB / 16; ++kk) tc::mma_bf16(tmem + 384, d_p(pp, kk), d_mn(v, kk), IDESC_PV, (j | kk) > 0);
+      }
+      tc::mma_commit(&bar[4]);
+    }
+  } else {
+    const int lb = (warp & 3) * 32, r = lb + lane, q = q0 + r;
+    const uint32_t trow = tmem + ((uint32_t)lb << 16);
+    const float sc = p.scale;
+    tc::mbar_wait(&bar[2], 0);
+    tc::fence_after();
+    float m = -INFINITY;
+    for (int j = 0; j < kb.n; ++j) {
+      for (int c0 = 0; c0 < TB; c0 += 32) {
+        float v[32];
+        tc::tmem_ld32(trow + j * TB + c0, v);
+        const int k0 = (kb.lo + j) * TB + c0;
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (valid(q, k0 + i, len, p.w, p.causal)) m = fmaxf(m, v[i] * sc);
+      }
+    }
+    float l = 0.f;
+    for (int j = 0; j < kb.n; ++j) {
+      for (int c0 = 0; c0 < TB; c0 += 32) {
+        float v[32];
+        uint32_t pk[16];
+        tc::tmem_ld32(trow + j * TB + c0, v);
+        const int k0 = (kb.lo + j) * TB + c0;
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          const float a = valid(q, k0 + i, len, p.w, p.causal) ? __expf(v[i] * sc - m) : 0.f;
+          const float bb = valid(q, k0 + i + 1, len, p.w, p.causal) ? __expf(v[i + 1] * sc - m) : 0.f;
+          l += a + bb;
+          pk[i >> 1] = tc::pack_bf16(a, bb);
+        }
+        store_sw(sP + j * PBLK, r, c0, pk);
+      }
+    }
+    tc::fence_async_smem();
+    tc::fence_before();
+    __syncwarp();
+    if (lane == 0) tc::mbar_arrive(&bar[3]);
+    tc::mbar_wait(&bar[4], 0);
+    tc::fence_after();
+    store_row64(O + (long long)q * p.ld_o, trow + 384, l > 0.f ? 1.f / l : 0.f, q < p.T);
+    if (q < p.T) p.LSE[((long long)b * p.H + h) * p.T + q] = l > 0.f ? m + logf(l) : INFINITY;
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tmem, 512);
+}
+
+// ---------------------------------------------------------------------------
+// dK, dV for one 128-key block.
+__global__ void __launch_bounds__(NT, 1)
+    swa_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tdo, SwaP p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sK = sm;
+  uint8_t* sV = sK + TILE;
+  uint8_t* sQ = sV + TILE;
+  uint8_t* sG = sQ + 3 * TILE;
+  uint8_t* sPT = sG + 3 * TILE;
+  uint8_t* sDT = sPT + PBLK;
+  float* lse = (float*)(sDT + PBLK);
+  float* dd = lse + 3 * TB;
+  uint64_t* bar = (uint64_t*)(dd + 3 * TB);  // ld, sdp, pds, mm
+  uint32_t* tslot = (uint32_t*)(bar + 8);
+
+  const int b = blockIdx.z, h = blockIdx.y, k0 = blockIdx.x * TB;
+  const int len = p.lengths[b];
+  const int HD = p.H * DH;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  bf16* dqkv = (bf16*)p.dQKV + (long long)b * p.bs_qkv;
+  if (k0 >= len) {
+    zero_rows(dqkv + HD + h * DH, p.ld_qkv, k0, TB, p.T, threadIdx.x, NT);
+    zero_rows(dqkv + 2 * HD + h * DH, p.ld_qkv, k0, TB, p.T, threadIdx.x, NT);
+    return;
+  }
+  const Band qb = query_band(k0, len, p.w, p.causal);
+  if (warp == 0 && lane == 0) {
+    tc::prefetch_tmap(&tq);
+    tc::prefetch_tmap(&tdo);
+    tc::mbar_init(&bar[0], 1);
+    tc::mbar_init(&bar[1], 1);
+    tc::mbar_init(&bar[2], 4);
+    tc::mbar_init(&bar[3], 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tslot, 512);
+  if (warp >= 2) {  // stage LSE / D of the query blocks
+    const float* LSE = p.LSE + ((long long)b * p.H + h) * p.T;
+    const float* D = p.Dbuf + ((long long)b * p.H + h) * p.T;
+    for (int i = threadIdx.x - 64; i < qb.n * TB; i += 128) {
+      const int q = qb.lo * TB + i;
+      lse[i] = q < len ? LSE[q] : INFINITY;
+      dd[i] = q < len ? D[q] : 0.f;
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tslot;
+  const uint32_t T_S = 0, T_DP = 128, T_DV = 256, T_DK = 320;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      tc::mbar_arrive_expect_tx(&bar[0], (2 + 2 * qb.n) * TILE);
+      tc::tma_load_3d(sK, &tq, &bar[0], HD + h * DH, k0, b);
+      tc::tma_load_3d(sV, &tq, &bar[0], 2 * HD + h * DH, k0, b);
+      for (int i = 0; i < qb.n; ++i) {
+        tc::tma_load_3d(sQ + i * TILE, &tq, &bar[0], h * DH, (qb.lo + i) * TB, b);
+        tc::tma_load_3d(sG + i * TILE, &tdo, &bar[0], h * DH, (qb.lo + i) * TB, b);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      tc::mbar_wait(&bar[0], 0);
+      const uint32_t k = tc::smem_u32(sK), v = tc::smem_u32(sV);
+      const uint32_t pt = tc::smem_u32(sPT), dt = tc::smem_u32(sDT);
+      for (int i = 0; i < qb.n; ++i) {
+        tc::fence_after();
+        const uint32_t q = tc::smem_u32(sQ + i * TILE), g = tc::smem_u32(sG + i * TILE);
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk) tc::mma_bf16(tmem + T_S, d_kmaj64(k, kk), d_kmaj64(q, kk), IDESC_S, kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk) tc::mma_bf16(tmem + T_DP, d_kmaj64(v, kk), d_kmaj64(g, kk), IDESC_S, kk > 0);
+        tc::mma_commit(&bar[1]);
+        tc::mbar_wait(&bar[2], i & 1);
+        tc::fence_after();
+#pragma unroll
+        for (int kk = 0; kk < TB / 16; ++kk)
+          tc::mma_bf16(tmem + T_DV, d_p(pt, kk), d_mn(g, kk), IDESC_PV, (i | kk) > 0);
+#pragma unroll
+        for (int kk = 0; kk < TB / 16; ++kk)
+          tc::mma_bf16(tmem + T_DK, d_p(dt, kk), d_mn(q, kk), IDESC_PV, (i | kk) > 0);
+        tc::mma_commit(&bar[3]);
+      }
+    }
+  } else {
+    const int lb = (warp & 3) * 32, r = lb + lane, key = k0 + r;
+    const uint32_t trow = tmem + ((uint32_t)lb << 16);
+    const float sc = p.scale;
+    for (int i = 0; i < qb.n; ++i) {
+      tc::mbar_wait(&bar[1], i & 1);
+      if (i > 0) tc::mbar_wait(&bar[3], (i - 1) & 1);  // previous MMAs done with sPT / sDT
+      tc::fence_after();
+      const int qbase = (qb.lo + i) * TB;
+      for (int c0 = 0; c0 < TB; c0 += 32) {
+        float s[32], dp[32];
+        uint32_t pp[16], pd[16];
+        tc::tmem_ld32(trow + T_S + c0, s);
+        tc::tmem_ld32(trow + T_DP + c0, dp);
+#pragma unroll
+        for (int j = 0; j < 32; j += 2) {
+          float pr[2], ds[2];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int qi = qbase + c0 + j + u;
+            const int li = i * TB + c0 + j + u;
+            pr[u] = valid(qi, key, len, p.w, p.causal) ? __expf(s[j + u] * sc - lse[li]) : 0.f;
+            ds[u] = pr[u] * (dp[j + u] - dd[li]);
+          }
+          pp[j >> 1] = tc::pack_bf16(pr[0], pr[1]);
+          pd[j >> 1] = tc::pack_bf16(ds[0], ds[1]);
+        }
+        store_sw(sPT, r, c0, pp);
+        store_sw(sDT, r, c0, pd);
+      }
+      tc::fence_async_smem();
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&bar[2]);
+    }
+    tc::mbar_wait(&bar[3], (qb.n - 1) & 1);
+    tc::fence_after();
+    store_row64(dqkv + (long long)key * p.ld_qkv + HD + h * DH, trow + T_DK, sc, key < p.T);
+    store_row64(dqkv + (long long)key * p.ld_qkv + 2 * HD + h * DH, trow + T_DV, 1.f, key < p.T);
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tmem, 512);
+}
+
+// ---------------------------------------------------------------------------
+// dQ for one 128-query block.
+__global__ void __launch_bounds__(NT, 1)
+    swa_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tdo, SwaP p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sQ = sm;
+  uint8_t* sG = sQ + TILE;
+  uint8_t* sK = sG + TILE;
+  uint8_t* sV = sK + 3 * TILE;
+  uint8_t* sDS = sV + 3 * TILE;
+  uint64_t* bar = (uint64_t*)(sDS + PBLK);  // ld, sdp, ds, mm
+  uint32_t* tslot = (uint32_t*)(bar + 8);
+
+  const int b = blockIdx.z, h = blockIdx.y, q0 = blockIdx.x * TB;
+  const int len = p.lengths[b];
+  const int HD = p.H * DH;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  bf16* dqkv = (bf16*)p.dQKV + (long long)b * p.bs_qkv;
+  if (q0 >= len) {
+    zero_rows(dqkv + h * DH, p.ld_qkv, q0, TB, p.T, threadIdx.x, NT);
+    return;
+  }
+  const Band kb = key_band(q0, len, p.w, p.causal);
+  if (warp == 0 && lane == 0) {
+    tc::prefetch_tmap(&tq);
+    tc::prefetch_tmap(&tdo);
+    tc::mbar_init(&bar[0], 1);
+    tc::mbar_init(&bar[1], 1);
+    tc::mbar_init(&bar[2], 4);
+    tc::mbar_init(&bar[3], 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tslot, 512);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tslot;
+  const uint32_t T_S = 0, T_DP = 128, T_DQ = 256;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      tc::mbar_arrive_expect_tx(&bar[0], (2 + 2 * kb.n) * TILE);
+      tc::tma_load_3d(sQ, &tq, &bar[0], h * DH, q0, b);
+      tc::tma_load_3d(sG, &tdo, &bar[0], h * DH, q0, b);
+      for (int j = 0; j < kb.n; ++j) {
+        tc::tma_load_3d(sK + j * TILE, &tq, &bar[0], HD + h * DH, (kb.lo + j) * TB, b);
+        tc::tma_load_3d(sV + j * TILE, &tq, &bar[0], 2 * HD + h * DH, (kb.lo + j) * TB, b);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      tc::mbar_wait(&bar[0], 0);
+      const uint32_t q = tc::smem_u32(sQ), g = tc::smem_u32(sG), ds = tc::smem_u32(sDS);
+      for (int j = 0; j < kb.n; ++j) {
+        tc::fence_after();
+        const uint32_t k = tc::smem_u32(sK + j * TILE), v = tc::smem_u32(sV + j * TILE);
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk) tc::mma_bf16(tmem + T_S, d_kmaj64(q, kk), d_kmaj64(k, kk), IDESC_S, kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk) tc::mma_bf16(tmem + T_DP, d_kmaj64(g, kk), d_kmaj64(v, kk), IDESC_S, kk > 0);
+        tc::mma_commit(&bar[1]);
+        tc::mbar_wait(&bar[2], j & 1);
+        tc::fence_after();
+#pragma unroll
+        for (int kk = 0; kk < TB / 16; ++kk)
+          tc::mma_bf16(tmem + T_DQ, d_p(ds, kk), d_mn(k, kk), IDESC_PV, (j | kk) > 0);
+        tc::mma_commit(&bar[3]);
+      }
+    }
+  } else {
+    const int lb = (warp & 3) * 32, r = lb + lane, q = q0 + r;
+    const uint32_t trow = tmem + ((uint32_t)lb << 16);
+    const float sc = p.scale;
+    const float lse_r = q < len ? p.LSE[((long long)b * p.H + h) * p.T + q] : INFINITY;
+    const float d_r = q < len ? p.Dbuf[((long long)b * p.H + h) * p.T + q] : 0.f;
+    for (int j = 0; j < kb.n; ++j) {
+      tc::mbar_wait(&bar[1], j & 1);
+      if (j > 0) tc::mbar_wait(&bar[3], (j - 1) & 1);
+      tc::fence_after();
+      const int kbase = (kb.lo + j) * TB;
+      for (int c0 = 0; c0 < TB; c0 += 32) {
+        float s[32], dp[32];
+        uint32_t pd[16];
+        tc::tmem_ld32(trow + T_S + c0, s);
+        tc::tmem_ld32(trow + T_DP + c0, dp);
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          float ds[2];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const float pr = valid(q, kbase + c0 + i + u, len, p.w, p.causal) ? __expf(s[i + u] * sc - lse_r) : 0.f;
+            ds[u] = pr * (dp[i + u] - d_r);
+          }
+          pd[i >> 1] = tc::pack_bf16(ds[0], ds[1]);
+        }
+        store_sw(sDS, r, c0, pd);
+      }
+      tc::fence_async_smem();
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&bar[2]);
+    }
+    tc::mbar_wait(&bar[3], (kb.n - 1) & 1);
+    tc::fence_after();
+    store_row64(dqkv + (long long)q * p.ld_qkv + h * DH, trow + T_DQ, sc, q < p.T);
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tmem, 512);
+}
+
+bool map3(CUtensorMap* m, const void* ptr, long long inner, int T, int B, long long ld, long long bs) {
+  auto fn = tc_encode_fn();
+  if (!fn) return false;
+  if (((uintptr_t)ptr & 15) || (ld * 2) % 16 || (bs * 2) % 16) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)T, (cuuint64_t)B};
+  cuuint64_t strides[2] = {(cuuint64_t)(ld * 2), (cuuint64_t)(bs * 2)};
+  cuuint32_t box[3] = {64, 128, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool supported(const SwaP& p) {
+  return p.dtype == KL_BF16 && p.d_h == DH && p.w <= TB && kl_tcgen05_available();
+}
+
+}  // namespace
+
+int swa_rowdot(const SwaP& p, cudaStream_t s);
+
+int swa_fwd_tc(const SwaP& p, cudaStream_t s) {
+  if (!supported(p)) return KL_EUNSUPPORTED;
+  CUtensorMap tq;
+  if (!map3(&tq, p.QKV, 3LL * p.H * DH, p.T, p.B, p.ld_qkv, p.bs_qkv)) return KL_EUNSUPPORTED;
+  const size_t smem = 1024 + 7 * TILE + 3 * PBLK + 64 + 16;
+  cudaFuncSetAttribute(swa_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  dim3 grid((p.T + TB - 1) / TB, p.H, p.B);
+  swa_fwd_tc_kernel<<<grid, NT, smem, s>>>(tq, p);
+  count_launch();
+  return launch_check("swa_fwd_tc");
+}
+
+int swa_bwd_tc(const SwaP& p, cudaStream_t s) {
+  if (!supported(p)) return KL_EUNSUPPORTED;
+  CUtensorMap tq, tdo;
+  if (!map3(&tq, p.QKV, 3LL * p.H * DH, p.T, p.B, p.ld_qkv, p.bs_qkv)) return KL_EUNSUPPORTED;
+  if (!map3(&tdo, p.dO, (long long)p.H * DH, p.T, p.B, p.ld_o, p.bs_o)) return KL_EUNSUPPORTED;
+  int rc = swa_rowdot(p, s);
+  if (rc) return rc;
+  dim3 grid((p.T + TB - 1) / TB, p.H, p.B);
+  const size_t smem1 = 1024 + 8 * TILE + 2 * PBLK + 6 * TB * 4 + 64 + 16;
+  cudaFuncSetAttribute(swa_bwd_dkv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
+  swa_bwd_dkv_tc_kernel<<<grid, NT, smem1, s>>>(tq, tdo, p);
+  const size_t smem2 = 1024 + 8 * TILE + PBLK + 64 + 16;
+  cudaFuncSetAttribute(swa_bwd_dq_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+  swa_bwd_dq_tc_kernel<<<grid, NT, smem2, s>>>(tq, tdo, p);
+  count_launch(2);
+  return launch_check("swa_bwd_tc");
+}
+
+}  // namespace kl
