@@ -42,27 +42,258 @@ struct TcParams {
   const void* R;
   long long r_rs, r_cs, r_s1, r_s2;
   void* aux;
+  int vec_c;  // C rows admit paired (4 B bf16 / 8 B fp32) stores at even columns
+  int vec_r;  // same for the residual
+  int r_boxes;  // >0: residual tile staged by TMA in r_boxes 64-column boxes
+  int r_has1, r_has2;
 };
+
+constexpr int SLD = 66;  // epilogue staging row stride (floats): 64 columns + pad, 8-byte aligned
+
+__device__ __forceinline__ void st2(bf16* p, float a, float b) {
+  *reinterpret_cast<__nv_bfloat162*>(p) = __floats2bfloat162_rn(a, b);
+}
+__device__ __forceinline__ void st2(float* p, float a, float b) { *reinterpret_cast<float2*>(p) = make_float2(a, b); }
+
+template <typename TC>
+__device__ __forceinline__ void store_pair(TC* p, long long cs, float a, float b, bool ok0, bool ok1, int vec) {
+  if (vec && ok0 && ok1) {
+    st2(p, a, b);
+  } else {
+    if (ok0) stf(p, a);
+    if (ok1) stf(p + cs, b);
+  }
+}
+
+template <typename TC>
+__device__ __forceinline__ void ld_pair(const TC* p, long long cs, bool ok0, bool ok1, int vec, float& a, float& b) {
+  if (vec && ok0 && ok1) {
+    if constexpr (sizeof(TC) == 2) {
+      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(p));
+      a = f.x;
+      b = f.y;
+    } else {
+      const float2 f = *reinterpret_cast<const float2*>(p);
+      a = f.x;
+      b = f.y;
+    }
+  } else {
+    a = ok0 ? ldf(p) : 0.f;
+    b = ok1 ? ldf(p + cs) : 0.f;
+  }
+}
+
+// Activation / derivative over 8 values of one column: the tag switch is hoisted
+// out of the row loop (one branch per 8 rows).  bf16-path intrinsics (__expf,
+// __fdividef): the result is rounded to bf16.
+__device__ __forceinline__ float fsig(float x) { return __fdividef(1.f, 1.f + __expf(-x)); }
+
+__device__ __forceinline__ void act8(int code, float* v) {
+  switch (code) {
+    case KL_ACT_RELU:
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = fmaxf(v[i], 0.f);
+      break;
+    case KL_ACT_SILU:
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = v[i] * fsig(v[i]);
+      break;
+    case KL_ACT_TANH:
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = tanhf(v[i]);
+      break;
+    case KL_ACT_SIGMOID:
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = fsig(v[i]);
+      break;
+    case KL_ACT_EXP:
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = __expf(v[i]);
+      break;
+    case KL_ACT_SQRT:
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = sqrtf(v[i]);
+      break;
+    case KL_ACT_LOG:
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = __logf(v[i]);
+      break;
+    default:
+      break;
+  }
+}
+
+__device__ __forceinline__ void dact8(int code, float* v, const float* x) {
+  switch (code) {
+    case KL_ACT_RELU:
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = x[i] > 0.f ? v[i] : 0.f;
+      break;
+    case KL_ACT_SILU:
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float s = fsig(x[i]);
+        v[i] *= s * (1.f + x[i] * (1.f - s));
+      }
+      break;
+    case KL_ACT_TANH:
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float y = tanhf(x[i]);
+        v[i] *= 1.f - y * y;
+      }
+      break;
+    case KL_ACT_SIGMOID:
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float y = fsig(x[i]);
+        v[i] *= y * (1.f - y);
+      }
+      break;
+    case KL_ACT_EXP:
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] *= __expf(x[i]);
+      break;
+    case KL_ACT_SQRT:
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] *= __fdividef(0.5f, sqrtf(x[i]));
+      break;
+    case KL_ACT_LOG:
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] *= __fdividef(1.f, x[i]);
+      break;
+    default:
+      break;
+  }
+}
+
+// Generic epilogue over a lane's column pair, eight rows at a time.  Every
+// optional feature is a warp-uniform branch around its own unrolled 8-row
+// loop, so its 16 loads are in flight together and disabled features cost one
+// branch per 8 rows.
+template <typename TC>
+__device__ __forceinline__ void epi_generic(const TcParams& p, const Epi& e, const float* stg, TC* C, const TC* R,
+                                            TC* X, int m0, int rows, int n, bool ok0, bool ok1, int lim,
+                                            const bf16* Rs, int rrow0, int rcol) {
+  const int lane = threadIdx.x & 31;
+  const int code0 = epi_code(e, n), code1 = epi_code(e, n + 1);
+  const float b0 = (e.bias && ok0) ? e.bias[n] : 0.f, b1 = (e.bias && ok1) ? e.bias[n + 1] : 0.f;
+  const long long cbase = (long long)m0 * p.c_rs + (long long)n * p.c_cs;
+  const long long rbase = (long long)m0 * p.r_rs + (long long)n * p.r_cs;
+  for (int r0 = 0; r0 < rows; r0 += 8) {
+    float v0[8], v1[8];
+    bool in[8], live[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float2 a = *reinterpret_cast<const float2*>(&stg[(r0 + i) * SLD + 2 * lane]);
+      in[i] = (r0 + i < rows);
+      live[i] = (m0 + r0 + i < lim);
+      v0[i] = e.alpha * a.x + b0;
+      v1[i] = e.alpha * a.y + b1;
+    }
+    if (e.aux_mode == 2) {  // dgrad of an activation: acc * act'(pre), bias (if any) after
+      float x0[8], x1[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        ld_pair(X + cbase + (long long)(r0 + i) * p.c_rs, p.c_cs, ok0 && in[i], ok1 && in[i], p.vec_c, x0[i], x1[i]);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        v0[i] -= b0;
+        v1[i] -= b1;
+      }
+      dact8(code0, v0, x0);
+      dact8(code1, v1, x1);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        v0[i] += b0;
+        v1[i] += b1;
+      }
+    }
+    if (e.row_limit) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (!live[i]) v0[i] = v1[i] = 0.f;
+    }
+    if (e.aux_mode == 1) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (in[i]) store_pair(X + cbase + (long long)(r0 + i) * p.c_rs, p.c_cs, v0[i], v1[i], ok0, ok1, p.vec_c);
+    }
+    if (e.aux_mode != 2 && e.n_act) {
+      act8(code0, v0);
+      act8(code1, v1);
+      if (e.row_limit) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          if (!live[i]) v0[i] = v1[i] = 0.f;
+      }
+    }
+    if (e.beta != 0.f) {
+      float c0[8], c1[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        ld_pair(C + cbase + (long long)(r0 + i) * p.c_rs, p.c_cs, ok0 && in[i], ok1 && in[i], p.vec_c, c0[i], c1[i]);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        v0[i] += e.beta * c0[i];
+        v1[i] += e.beta * c1[i];
+      }
+    }
+    if (Rs) {
+      // residual tile staged in smem by the TMA producer (row-major 64-col boxes)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int rr = rrow0 + r0 + i;
+        const float2 f = __bfloat1622float2(
+            *reinterpret_cast<const __nv_bfloat162*>(Rs + (rcol >> 6) * (128 * 64) + rr * 64 + (rcol & 63)));
+        v0[i] += f.x;
+        v1[i] += f.y;
+      }
+    } else if (R) {
+      float q0[8], q1[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        ld_pair(R + rbase + (long long)(r0 + i) * p.r_rs, p.r_cs, ok0 && in[i], ok1 && in[i], p.vec_r, q0[i], q1[i]);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        v0[i] += q0[i];
+        v1[i] += q1[i];
+      }
+    }
+    if (e.row_limit && (e.beta != 0.f || R || Rs)) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (!live[i]) v0[i] = v1[i] = 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (in[i]) store_pair(C + cbase + (long long)(r0 + i) * p.c_rs, p.c_cs, v0[i], v1[i], ok0, ok1, p.vec_c);
+  }
+}
 
 template <typename TC, bool PLAIN>
 __global__ void __launch_bounds__(NTHREADS, 1)
-    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcParams p,
-                   Epi e) {
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmR, TcParams p, Epi e) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;
   uint8_t* sB = sA + p.stages * p.a_stage_bytes;
-  float* stage_buf = (float*)(sB + p.stages * p.b_stage_bytes);  // 4 warps x 32 x 33 fp32
-  uint64_t* full = (uint64_t*)(stage_buf + 4 * 32 * 33);
+  uint8_t* sR = sB + p.stages * p.b_stage_bytes;  // 2 x r_boxes x 16 KB residual tiles (TMA)
+  __shared__ __align__(16) float stage_s[4 * 32 * SLD];  // epilogue transpose, one 32 x 64 slab per warp
+  uint64_t* full = (uint64_t*)(sR + (p.r_boxes ? 2 * p.r_boxes * 16384 : 0));
   uint64_t* empty = full + p.stages;
   uint64_t* tfull = empty + p.stages;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+  uint64_t* rfull = tempty + 2;
+  uint64_t* rempty = rfull + 2;
+  uint32_t* tmem_slot = (uint32_t*)(rempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
     tc::prefetch_tmap(&tmA);
     tc::prefetch_tmap(&tmB);
+    if (p.r_boxes) tc::prefetch_tmap(&tmR);
     for (int s = 0; s < p.stages; ++s) {
       tc::mbar_init(&full[s], 1);
       tc::mbar_init(&empty[s], 1);
@@ -70,6 +301,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&tfull[i], 1);
       tc::mbar_init(&tempty[i], 4);
+      tc::mbar_init(&rfull[i], 1);
+      tc::mbar_init(&rempty[i], 4);
     }
     tc::fence_barrier_init();
   }
@@ -90,13 +323,23 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       const uint32_t tx = p.a_stage_bytes + p.b_stage_bytes;
-      for (int unit = blockIdx.x; unit < total; unit += gridDim.x) {
+      int t = 0;
+      for (int unit = blockIdx.x; unit < total; unit += gridDim.x, ++t) {
         const int tile = unit / p.splits, sp = unit % p.splits;
         const int it0 = (int)((long long)iters * sp / p.splits), it1 = (int)((long long)iters * (sp + 1) / p.splits);
         const int mb = tile % p.tiles_m;
         const int nb = (tile / p.tiles_m) % p.tiles_n;
         const int zo = tile / (p.tiles_m * p.tiles_n);
         const int z1o = p.red1 ? 0 : zo / nb2o, z2o = p.red2 ? 0 : zo % nb2o;
+        if (p.r_boxes) {
+          // residual tile for this output tile, double-buffered against the epilogue
+          const int rb = t & 1;
+          tc::mbar_wait(&rempty[rb], ((t >> 1) & 1) ^ 1);
+          tc::mbar_arrive_expect_tx(&rfull[rb], p.r_boxes * 16384);
+          for (int j = 0; j < p.r_boxes; ++j)
+            tc::tma_load_4d(sR + (rb * p.r_boxes + j) * 16384, &tmR, &rfull[rb], nb * p.BN + j * 64, mb * BM,
+                            p.r_has2 ? z2o : 0, p.r_has1 ? z1o : 0);
+        }
         for (int it = it0; it < it1; ++it) {
           const int r = it / p.kblocks, kb = it % p.kblocks;
           const int z1 = p.red1 ? r / r2n : z1o;
@@ -180,44 +423,60 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     : nullptr;
       const int lim = e.row_limit ? e.row_limit[zo] : 0x7fffffff;
       const int m0 = mb * BM + lane_base;
-      float* stg = stage_buf + (warp - 2) * 32 * 33;
+      float* stg = stage_s + (warp - 2) * (32 * SLD);
       tc::mbar_wait(&tfull[acc], acc_phase);
       tc::fence_after();
       const uint32_t tbase = tmem + acc * p.acc_stride + ((uint32_t)lane_base << 16);
-      for (int c0 = 0; c0 < p.BN; c0 += 32) {
-        // TMEM row (lane) -> smem transpose -> lanes walk columns: coalesced
-        // global reads (residual / C) and writes, one row per iteration.
-        float v[32];
-        tc::tmem_ld16(tbase + c0, v);
-        if (c0 + 16 < p.BN) tc::tmem_ld16(tbase + c0 + 16, v + 16);
+      const int rows = min(32, p.M - m0);
+      for (int c0 = 0; c0 < p.BN; c0 += 64) {
+        // TMEM (thread = row) -> smem transpose -> each lane owns a column
+        // pair and walks the warp's 32 rows: every global access of a warp is
+        // one contiguous 128 B (bf16) / 256 B (fp32) row segment.
 #pragma unroll
-        for (int j = 0; j < 32; ++j) stg[lane * 33 + j] = v[j];
+        for (int q4 = 0; q4 < 4; ++q4) {
+          if (c0 + 16 * q4 < p.BN) {
+            float v[16];
+            tc::tmem_ld16(tbase + c0 + 16 * q4, v);
+#pragma unroll
+            for (int j = 0; j < 16; j += 2)
+              *reinterpret_cast<float2*>(&stg[lane * SLD + 16 * q4 + j]) = make_float2(v[j], v[j + 1]);
+          }
+        }
         __syncwarp();
-        const int n = nb * p.BN + c0 + lane;
-        const bool ncol = (n < p.N) && (c0 + lane < p.BN);
-        const int rows = min(32, p.M - m0);
+        const int cl = c0 + 2 * lane;
+        const int n = nb * p.BN + cl;
+        const bool ok0 = cl < p.BN && n < p.N, ok1 = cl + 1 < p.BN && n + 1 < p.N;
         if (p.splits > 1) {
           // split-K partial: C += alpha * partial (fp32, beta == 1 accumulate)
           float* cp = (float*)C + (long long)m0 * p.c_rs + (long long)n * p.c_cs;
-          for (int r = 0; r < rows; ++r)
-            if (ncol) atomicAdd(cp + (long long)r * p.c_rs, e.alpha * stg[r * 33 + lane]);
+          for (int r = 0; r < rows; ++r) {
+            const float2 a = *reinterpret_cast<const float2*>(&stg[r * SLD + 2 * lane]);
+            if (ok0) atomicAdd(cp + (long long)r * p.c_rs, e.alpha * a.x);
+            if (ok1) atomicAdd(cp + (long long)r * p.c_rs + p.c_cs, e.alpha * a.y);
+          }
         } else if (PLAIN) {
           TC* cp = C + (long long)m0 * p.c_rs + (long long)n * p.c_cs;
-          for (int r = 0; r < rows; ++r)
-            if (ncol) stf(cp + (long long)r * p.c_rs, stg[r * 33 + lane]);
-        } else {
+#pragma unroll 4
           for (int r = 0; r < rows; ++r) {
-            const int m = m0 + r;
-            if (ncol)
-              epilogue_store(e, C, R, X, (long long)m * p.c_rs + (long long)n * p.c_cs,
-                             (long long)m * p.r_rs + (long long)n * p.r_cs, m, n, lim, stg[r * 33 + lane]);
+            const float2 a = *reinterpret_cast<const float2*>(&stg[r * SLD + 2 * lane]);
+            store_pair(cp + (long long)r * p.c_rs, p.c_cs, a.x, a.y, ok0, ok1, p.vec_c);
           }
+        } else {
+          const bf16* Rs = nullptr;
+          if (p.r_boxes) {
+            if (c0 == 0) tc::mbar_wait(&rfull[t & 1], (t >> 1) & 1);
+            Rs = reinterpret_cast<const bf16*>(sR + (t & 1) * p.r_boxes * 16384);
+          }
+          epi_generic(p, e, stg, C, R, X, m0, rows, n, ok0, ok1, lim, Rs, lane_base, cl);
         }
         __syncwarp();
       }
       tc::fence_before();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        tc::mbar_arrive(&tempty[acc]);
+        if (p.r_boxes) tc::mbar_arrive(&rempty[t & 1]);
+      }
     }
   }
   __syncthreads();
@@ -241,7 +500,8 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // 4-D bf16 tensor map: dims (inner, outer, b2, b1), element strides; a batch
 // dim with stride 0 (broadcast) becomes extent 1.
 bool make_map(CUtensorMap* m, const void* ptr, long long inner, long long outer, long long s_outer, int nb2,
-              long long s2, int nb1, long long s1, uint32_t box_inner, uint32_t box_outer, int* has2, int* has1) {
+              long long s2, int nb1, long long s1, uint32_t box_inner, uint32_t box_outer, int* has2, int* has1,
+              bool swizzle = true) {
   auto fn = encode_fn();
   if (!fn) return false;
   *has2 = (s2 != 0 && nb2 > 1);
@@ -259,7 +519,8 @@ bool make_map(CUtensorMap* m, const void* ptr, long long inner, long long outer,
   cuuint32_t box[4] = {box_inner, box_outer, 1, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -279,11 +540,22 @@ int num_sms() {
 
 int gemm_path();
 
-int gemm_tc(const GemmDesc& g, const Epi& e, cudaStream_t s) {
-  if (g.ab_dtype != KL_BF16) return KL_EUNSUPPORTED;
+int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
+  if (g0.ab_dtype != KL_BF16) return KL_EUNSUPPORTED;
   if (!kl_tcgen05_available()) return KL_EUNSUPPORTED;
   // small problems go to the SIMT kernel unless forced
-  if (gemm_path() != 2 && (long long)g.M * g.N * g.K < (1ll << 18)) return KL_EUNSUPPORTED;
+  if (gemm_path() != 2 && (long long)g0.M * g0.N * g0.K < (1ll << 18)) return KL_EUNSUPPORTED;
+  GemmDesc g = g0;
+  Epi e = e0;
+  // C += ... on a bf16 output is the residual epilogue with R = C
+  if (g.c_dtype == KL_BF16 && e.beta == 1.f && !g.R) {
+    g.R = g.C;
+    g.r_rs = g.c_rs;
+    g.r_cs = g.c_cs;
+    g.r_s1 = g.red1 ? 0 : g.c_s1;
+    g.r_s2 = g.red2 ? 0 : g.c_s2;
+    e.beta = 0.f;
+  }
   const bool a_k = (g.a_cs == 1), a_m = (g.a_rs == 1) && !a_k;
   const bool b_k = (g.b_rs == 1), b_n = (g.b_cs == 1) && !b_k;
   if (!(a_k || a_m) || !(b_k || b_n)) return KL_EUNSUPPORTED;
@@ -293,7 +565,13 @@ int gemm_tc(const GemmDesc& g, const Epi& e, cudaStream_t s) {
   p.M = g.M;
   p.N = g.N;
   p.K = g.K;
-  int tiles_n = (g.N + 255) / 256;
+  // residual tiles arrive by TMA when their layout allows (bf16, unit column
+  // stride, 16-byte aligned rows); those GEMMs use N tiles of <= 128 so the
+  // double-buffered residual fits next to the operand ring.
+  CUtensorMap tr;
+  bool use_r = g.R && g.c_dtype == KL_BF16 && g.r_cs == 1 && !g.red1 && !g.red2;
+  const int bn_max = use_r ? 128 : 256;
+  int tiles_n = (g.N + bn_max - 1) / bn_max;
   int bn = (g.N + tiles_n - 1) / tiles_n;
   bn = (bn + 15) / 16 * 16;
   if (bn < 16) bn = 16;
@@ -312,7 +590,17 @@ int gemm_tc(const GemmDesc& g, const Epi& e, cudaStream_t s) {
   p.a_stage_bytes = BM * BK * 2;
   p.b_stage_bytes = b_n ? p.b_boxes * 64 * BK * 2 : bn * BK * 2;
   const uint32_t stage = p.a_stage_bytes + p.b_stage_bytes;
-  p.stages = std::min<int>(8, (190 * 1024) / stage);
+  if (use_r) {
+    int h2 = 0, h1 = 0;
+    use_r = ((uintptr_t)g.R & 15) == 0 &&
+            make_map(&tr, g.R, g.N, g.M, g.r_rs, g.nb2, g.r_s2, g.nb1, g.r_s1, 64, BM, &h2, &h1, false);
+    p.r_has2 = h2;
+    p.r_has1 = h1;
+  }
+  p.r_boxes = use_r ? (bn + 63) / 64 : 0;
+  const uint32_t rbytes = 2u * p.r_boxes * 16384;
+  // dynamic smem budget: 227 KB minus the 33 KB static epilogue staging
+  p.stages = std::min<int>(8, (int)((188 * 1024 - rbytes) / stage));
   if (p.stages < 2) return KL_EUNSUPPORTED;
   p.acc_stride = bn > 128 ? 256 : (bn > 64 ? 128 : (bn > 32 ? 64 : 32));
   p.tmem_cols = 2 * p.acc_stride;
@@ -344,8 +632,15 @@ int gemm_tc(const GemmDesc& g, const Epi& e, cudaStream_t s) {
   p.r_s1 = g.r_s1;
   p.r_s2 = g.r_s2;
   p.aux = g.aux;
+  {
+    const int esz = g.c_dtype == KL_BF16 ? 2 : 4;
+    auto al = [&](const void* q) { return ((uintptr_t)q % (2 * esz)) == 0; };
+    p.vec_c = g.c_cs == 1 && g.c_rs % 2 == 0 && (g.c_s1 % 2 == 0) && (g.c_s2 % 2 == 0) && al(g.C) &&
+              (!g.aux || al(g.aux));
+    p.vec_r = g.R && g.r_cs == 1 && g.r_rs % 2 == 0 && (g.r_s1 % 2 == 0) && (g.r_s2 % 2 == 0) && al(g.R);
+  }
 
-  const size_t smem = 1024 + (size_t)p.stages * stage + 4 * 32 * 33 * 4 + (2 * p.stages + 4) * 8 + 16;
+  const size_t smem = 1024 + (size_t)p.stages * stage + rbytes + (2 * p.stages + 8) * 8 + 16;
   const int tiles = p.tiles_m * p.tiles_n * p.n_out;
   const int iters = ((g.red1 ? g.nb1 : 1) * (g.red2 ? g.nb2 : 1)) * p.kblocks;
   p.splits = 1;
@@ -363,7 +658,7 @@ int gemm_tc(const GemmDesc& g, const Epi& e, cudaStream_t s) {
                      !g.R;
   auto launch = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<grid, NTHREADS, smem, s>>>(ta, tb, p, e);
+    kern<<<grid, NTHREADS, smem, s>>>(ta, tb, use_r ? tr : ta, p, e);
   };
   if (g.c_dtype == KL_BF16) {
     if (plain) launch(gemm_tc_kernel<bf16, true>);
