@@ -363,12 +363,51 @@ int swa_support(const SwaP& p, int* support, cudaStream_t s) {
 
 namespace kl {
 // D[b,h,t] = rowsum(dO * O) for the tcgen05 backward kernels.
+// Warp per (b, t) row of a bf16 (B, T, H*64) pair: each lane owns 8 contiguous
+// elements (16-byte loads, the warp reads the row's 512 B... H*128 B), the 8 lanes
+// of a head reduce with shuffles.  Coalesced; one pass over O and dO.
+__global__ void swa_rowdot_bf16_h64(SwaP p) {
+  const long long row = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= (long long)p.B * p.T) return;
+  const int lane = threadIdx.x & 31;
+  const int b = row / p.T, t = row % p.T;
+  const bf16* o = (const bf16*)p.O + (long long)b * p.bs_o + (long long)t * p.ld_o;
+  const bf16* g = (const bf16*)p.dO + (long long)b * p.bs_o + (long long)t * p.ld_o;
+  const int HD = p.H * 64;
+  for (int c0 = lane * 8; c0 < HD; c0 += 256) {
+    const uint4 a = *reinterpret_cast<const uint4*>(o + c0);
+    const uint4 d = *reinterpret_cast<const uint4*>(g + c0);
+    const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
+    const __nv_bfloat162* d2 = reinterpret_cast<const __nv_bfloat162*>(&d);
+    float acc = 0.f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 x = __bfloat1622float2(a2[i]), y = __bfloat1622float2(d2[i]);
+      acc = fmaf(x.x, y.x, fmaf(x.y, y.y, acc));
+    }
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+    if ((lane & 7) == 0) {
+      const int h = c0 / 64;
+      p.Dbuf[((long long)b * p.H + h) * p.T + t] = acc;
+    }
+  }
+}
+
 int swa_rowdot(const SwaP& p, cudaStream_t s) {
   long long total = (long long)p.B * p.H * p.T;
   unsigned g = (unsigned)((total + 255) / 256);
-  if (p.dtype == KL_BF16 && p.d_h == 64) swa_rowdot_kernel<bf16, 64><<<g, 256, 0, s>>>(p);
-  else if (p.dtype == KL_F32 && p.d_h == 64) swa_rowdot_kernel<float, 64><<<g, 256, 0, s>>>(p);
-  else {
+  const bool vec = p.dtype == KL_BF16 && p.d_h == 64 && p.ld_o % 8 == 0 && p.bs_o % 8 == 0 &&
+                   ((uintptr_t)p.O & 15) == 0 && ((uintptr_t)p.dO & 15) == 0;
+  if (vec) {
+    const long long rows = (long long)p.B * p.T;
+    swa_rowdot_bf16_h64<<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(p);
+  } else if (p.dtype == KL_BF16 && p.d_h == 64) {
+    swa_rowdot_kernel<bf16, 64><<<g, 256, 0, s>>>(p);
+  } else if (p.dtype == KL_F32 && p.d_h == 64) {
+    swa_rowdot_kernel<float, 64><<<g, 256, 0, s>>>(p);
+  } else {
     set_error("swa_rowdot: unsupported head dim %d", p.d_h);
     return KL_EUNSUPPORTED;
   }

@@ -409,6 +409,10 @@ def recent_rows(S, lengths, n):
     return _Recent.apply(S, lengths, int(n))
 
 
+def pad8(n: int) -> int:
+    return (n + 7) // 8 * 8
+
+
 class _GramTriu(torch.autograd.Function):
     """triu_flatten(x x^T) per sample (interaction.py:63-76, 116-117)."""
 
@@ -417,7 +421,9 @@ class _GramTriu(torch.autograd.Function):
         B, n, d = x.shape
         if x.stride(2) != 1:
             raise ShapeError("gram_triu needs unit column stride")
-        tri = torch.empty(B, n * (n + 1) // 2, device=x.device, dtype=x.dtype)
+        # pairs padded to a multiple of 8 (zeros) so the DotMap GEMM's rows are
+        # 16-byte aligned for TMA; the padding multiplies zero weight columns
+        tri = torch.zeros(B, pad8(n * (n + 1) // 2), device=x.device, dtype=x.dtype)
         _capi.call("kl_gram_triu_fwd", B, n, d, _capi.dt(x), x.data_ptr(), x.stride(1), x.stride(0),
                    tri.data_ptr(), tri.stride(0), _stream())
         ctx.save_for_backward(x)
