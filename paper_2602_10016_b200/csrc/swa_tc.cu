@@ -20,6 +20,9 @@
 // dQ over the <= 3 key blocks; probabilities are recomputed from the forward
 // log-sum-exp.  No atomics.
 #include <cudaTypedefs.h>
+#include <stdlib.h>
+
+#include <algorithm>
 
 #include "swa.h"
 #include "tc_common.cuh"
@@ -471,6 +474,326 @@ __global__ void __launch_bounds__(NT, 1)
   if (warp == 1) tc::tmem_dealloc(tmem, 512);
 }
 
+// ===========================================================================
+// Forward v2: persistent, pipelined.
+//
+// Each CTA owns a contiguous range of (sample, head, 128-row block) work items
+// in sequence order, so consecutive items are consecutive query blocks of one
+// sequence: a key/value block is loaded once and reused by the (<= 3) query
+// blocks that see it (3-slot ring, block j in slot j % 3).  Roles overlap
+// across items: TMA prefetches the next Q / K / V while the MMA warp computes
+// the next tile's scores as soon as the softmax warps have drained the current
+// ones, and P V of a tile streams block by block through a 2-slot P ring.
+// Eight softmax warps: warps q and q+4 share TMEM lane quarter q (rows) and
+// split each 128-key block into two 64-key halves; row max / sum are combined
+// through shared memory with one named barrier each.
+// ===========================================================================
+namespace v2 {
+
+constexpr int NT2 = 320;  // warp 0 TMA, warp 1 MMA, warps 2..9 softmax
+constexpr int KVS = 3;    // key/value ring slots
+
+struct Item {
+  int b, h, q0, len, lo, n;
+  bool real;
+};
+
+__device__ __forceinline__ Item decode(const SwaP& p, int idx, int nT) {
+  Item it;
+  const int qt = idx % nT, bh = idx / nT;
+  it.h = bh % p.H;
+  it.b = bh / p.H;
+  it.q0 = qt * TB;
+  it.len = p.lengths[it.b];
+  it.real = it.q0 < it.len;
+  if (it.real) {
+    const Band kb = key_band(it.q0, it.len, p.w, p.causal);
+    it.lo = kb.lo;
+    it.n = kb.n;
+  } else {
+    it.lo = 0;
+    it.n = 0;
+  }
+  return it;
+}
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
+
+__global__ void __launch_bounds__(NT2, 1) swa_fwd_tc2_kernel(const __grid_constant__ CUtensorMap tq, SwaP p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sQ = sm;                       // 2 x 16 KB
+  uint8_t* sKV = sQ + 2 * TILE;           // KVS x (K 16 KB | V 16 KB)
+  uint8_t* sP = sKV + KVS * 2 * TILE;     // 2 x 32 KB
+  float* red = (float*)(sP + 2 * PBLK);   // [2 halves][128 rows] max, then sum
+  uint64_t* bar = (uint64_t*)(red + 2 * TB);
+  uint64_t* q_full = bar;        // [2]
+  uint64_t* q_empty = bar + 2;   // [2]
+  uint64_t* kv_full = bar + 4;   // [3]
+  uint64_t* kv_empty = bar + 7;  // [3]
+  uint64_t* p_full = bar + 10;   // [2]
+  uint64_t* p_empty = bar + 12;  // [2]
+  uint64_t* s_full = bar + 14;
+  uint64_t* s_empty = bar + 15;
+  uint64_t* o_full = bar + 16;
+  uint64_t* o_empty = bar + 17;
+  uint32_t* tslot = (uint32_t*)(bar + 18);
+
+  const int nT = (p.T + TB - 1) / TB;
+  const int W = p.B * p.H * nT;
+  const int i0 = (int)((long long)W * blockIdx.x / gridDim.x);
+  const int i1 = (int)((long long)W * (blockIdx.x + 1) / gridDim.x);
+  const int HD = p.H * DH;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    tc::prefetch_tmap(&tq);
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&q_full[i], 1);
+      tc::mbar_init(&q_empty[i], 1);
+      tc::mbar_init(&p_full[i], 8);
+      tc::mbar_init(&p_empty[i], 1);
+    }
+    for (int i = 0; i < KVS; ++i) {
+      tc::mbar_init(&kv_full[i], 1);
+      tc::mbar_init(&kv_empty[i], 1);
+    }
+    tc::mbar_init(s_full, 1);
+    tc::mbar_init(s_empty, 8);
+    tc::mbar_init(o_full, 1);
+    tc::mbar_init(o_empty, 8);
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tslot, 512);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tslot;
+  const uint32_t T_O = 384;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int qcount = 0, cur_bh = -1, hi_loaded = -1;
+      int kv_use[KVS] = {0, 0, 0};
+      for (int idx = i0; idx < i1; ++idx) {
+        const Item it = decode(p, idx, nT);
+        if (!it.real) continue;
+        const int bh = idx / nT;
+        if (bh != cur_bh) {
+          cur_bh = bh;
+          hi_loaded = -1;
+        }
+        const int qs = qcount & 1;
+        tc::mbar_wait(&q_empty[qs], ((qcount >> 1) & 1) ^ 1);
+        tc::mbar_arrive_expect_tx(&q_full[qs], TILE);
+        tc::tma_load_3d(sQ + qs * TILE, &tq, &q_full[qs], it.h * DH, it.q0, it.b);
+        ++qcount;
+        for (int j = it.lo; j < it.lo + it.n; ++j) {
+          if (j <= hi_loaded) continue;
+          const int s = j % KVS;
+          tc::mbar_wait(&kv_empty[s], (kv_use[s] & 1) ^ 1);
+          tc::mbar_arrive_expect_tx(&kv_full[s], 2 * TILE);
+          tc::tma_load_3d(sKV + s * 2 * TILE, &tq, &kv_full[s], HD + it.h * DH, j * TB, it.b);
+          tc::tma_load_3d(sKV + s * 2 * TILE + TILE, &tq, &kv_full[s], 2 * HD + it.h * DH, j * TB, it.b);
+          ++kv_use[s];
+          hi_loaded = j;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int qcount = 0, cur_bh = -1, hi_seen = -1, t = 0, pcount = 0;
+      int kv_use[KVS] = {0, 0, 0};
+      for (int idx = i0; idx < i1; ++idx) {
+        const Item it = decode(p, idx, nT);
+        if (!it.real) continue;
+        const int bh = idx / nT;
+        if (bh != cur_bh) {
+          cur_bh = bh;
+          hi_seen = -1;
+        }
+        const int qs = qcount & 1;
+        tc::mbar_wait(&q_full[qs], (qcount >> 1) & 1);
+        tc::mbar_wait(s_empty, (t & 1) ^ 1);  // softmax has drained the previous tile's scores
+        const uint32_t qa = tc::smem_u32(sQ + qs * TILE);
+        for (int jj = 0; jj < it.n; ++jj) {
+          const int j = it.lo + jj, s = j % KVS;
+          if (j > hi_seen) {
+            tc::mbar_wait(&kv_full[s], kv_use[s] & 1);
+            ++kv_use[s];
+            hi_seen = j;
+          }
+          tc::fence_after();
+          const uint32_t ka = tc::smem_u32(sKV + s * 2 * TILE);
+#pragma unroll
+          for (int kk = 0; kk < DH / 16; ++kk)
+            tc::mma_bf16(tmem + jj * TB, d_kmaj64(qa, kk), d_kmaj64(ka, kk), IDESC_S, kk > 0);
+        }
+        tc::mma_commit(s_full);
+        tc::mma_commit(&q_empty[qs]);
+        ++qcount;
+        tc::mbar_wait(o_empty, (t & 1) ^ 1);  // epilogue has read the previous O
+        for (int jj = 0; jj < it.n; ++jj) {
+          const int ps = pcount & 1;
+          tc::mbar_wait(&p_full[ps], (pcount >> 1) & 1);
+          tc::fence_after();
+          const uint32_t pa = tc::smem_u32(sP + ps * PBLK);
+          const uint32_t va = tc::smem_u32(sKV + ((it.lo + jj) % KVS) * 2 * TILE + TILE);
+#pragma unroll
+          for (int kk = 0; kk < TB / 16; ++kk) tc::mma_bf16(tmem + T_O, d_p(pa, kk), d_mn(va, kk), IDESC_PV, (jj | kk) > 0);
+          tc::mma_commit(&p_empty[ps]);
+          ++pcount;
+        }
+        tc::mma_commit(o_full);
+        // release the key/value blocks the next item of this sequence no longer needs
+        int keep_lo = it.lo + it.n;  // default: sequence ends here, release all
+        if (idx + 1 < i1 && (idx + 1) / nT == bh) {
+          const Item nx = decode(p, idx + 1, nT);
+          if (nx.real) keep_lo = nx.lo;
+        }
+        for (int j = it.lo; j < it.lo + it.n && j < keep_lo; ++j) tc::mma_commit(&kv_empty[j % KVS]);
+        ++t;
+      }
+    }
+  } else {
+    const int qtr = warp & 3, hf = (warp - 2) >> 2;
+    const int r = qtr * 32 + lane;
+    const uint32_t trow = tmem + ((uint32_t)(qtr * 32) << 16);
+    const float c2 = p.scale * 1.4426950408889634f;  // scores in log2 units
+    int t = 0, pcount = 0;
+    bf16* Obase = (bf16*)p.O;
+    for (int idx = i0; idx < i1; ++idx) {
+      const Item it = decode(p, idx, nT);
+      bf16* O = Obase + (long long)it.b * p.bs_o + it.h * DH;
+      if (!it.real) {  // padding-only tile
+        const int tid = threadIdx.x - 64;
+        zero_rows(O, p.ld_o, it.q0, TB, p.T, tid, 256);
+        for (int rr = tid; rr < TB; rr += 256)
+          if (it.q0 + rr < p.T) p.LSE[((long long)it.b * p.H + it.h) * p.T + it.q0 + rr] = INFINITY;
+        continue;
+      }
+      const int q = it.q0 + r;
+      int klo = max(0, q - p.w), khi = min(it.len - 1, q + p.w);
+      if (p.causal) khi = min(khi, q);
+      if (q >= it.len) khi = -1;  // padding row: nothing visible
+      tc::mbar_wait(s_full, t & 1);
+      tc::fence_after();
+      // pass 1: row max over this half's columns
+      float m = -INFINITY;
+      for (int jj = 0; jj < it.n; ++jj) {
+#pragma unroll
+        for (int c = 0; c < 64; c += 32) {
+          const int col = hf * 64 + c;
+          const int k0 = (it.lo + jj) * TB + col;
+          float v[32];
+          tc::tmem_ld32(trow + jj * TB + col, v);
+          if (k0 >= klo && k0 + 31 <= khi) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) m = fmaxf(m, v[i]);
+          } else if (k0 <= khi && k0 + 31 >= klo) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (k0 + i >= klo && k0 + i <= khi) m = fmaxf(m, v[i]);
+          }
+        }
+      }
+      red[hf * TB + r] = m;
+      named_bar(1, 256);
+      m = fmaxf(red[r], red[TB + r]);
+      const float mb = (m == -INFINITY) ? 0.f : m * c2;
+      // pass 2: P = exp2(s*c2 - m*c2) into the P ring, partial row sums
+      float l = 0.f;
+      for (int jj = 0; jj < it.n; ++jj) {
+        const int ps = pcount & 1;
+        tc::mbar_wait(&p_empty[ps], ((pcount >> 1) & 1) ^ 1);
+        uint8_t* pblk = sP + ps * PBLK;
+#pragma unroll
+        for (int c = 0; c < 64; c += 32) {
+          const int col = hf * 64 + c;
+          const int k0 = (it.lo + jj) * TB + col;
+          uint32_t pk[16];
+          float v[32];
+          tc::tmem_ld32(trow + jj * TB + col, v);  // warp-collective: every lane loads
+          if (k0 > khi || k0 + 31 < klo) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) pk[i] = 0u;
+          } else {
+            if (k0 >= klo && k0 + 31 <= khi) {
+#pragma unroll
+              for (int i = 0; i < 32; i += 2) {
+                const float a = ex2(fmaf(v[i], c2, -mb)), bq = ex2(fmaf(v[i + 1], c2, -mb));
+                l += a + bq;
+                pk[i >> 1] = tc::pack_bf16(a, bq);
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; i += 2) {
+                const bool ok0 = k0 + i >= klo && k0 + i <= khi, ok1 = k0 + i + 1 >= klo && k0 + i + 1 <= khi;
+                const float a = ok0 ? ex2(fmaf(v[i], c2, -mb)) : 0.f;
+                const float bq = ok1 ? ex2(fmaf(v[i + 1], c2, -mb)) : 0.f;
+                l += a + bq;
+                pk[i >> 1] = tc::pack_bf16(a, bq);
+              }
+            }
+          }
+          store_sw(pblk, r, col, pk);
+        }
+        tc::fence_async_smem();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&p_full[ps]);
+        ++pcount;
+      }
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(s_empty);
+      red[hf * TB + r] = l;
+      named_bar(1, 256);
+      l = red[r] + red[TB + r];
+      named_bar(1, 256);  // red reused by the next tile's max
+      // epilogue: O (this half's 32 columns) / l -> bf16
+      tc::mbar_wait(o_full, t & 1);
+      tc::fence_after();
+      {
+        float v[32];
+        tc::tmem_ld32(trow + T_O + hf * 32, v);
+        if (q < p.T) {
+          const float inv = l > 0.f ? 1.f / l : 0.f;
+          uint4* o = reinterpret_cast<uint4*>(O + (long long)q * p.ld_o + hf * 32);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            uint4 u;
+            u.x = tc::pack_bf16(v[8 * c + 0] * inv, v[8 * c + 1] * inv);
+            u.y = tc::pack_bf16(v[8 * c + 2] * inv, v[8 * c + 3] * inv);
+            u.z = tc::pack_bf16(v[8 * c + 4] * inv, v[8 * c + 5] * inv);
+            u.w = tc::pack_bf16(v[8 * c + 6] * inv, v[8 * c + 7] * inv);
+            o[c] = u;
+          }
+          if (hf == 0)
+            p.LSE[((long long)it.b * p.H + it.h) * p.T + q] =
+                l > 0.f ? (mb + __log2f(l)) * 0.6931471805599453f : INFINITY;
+        }
+      }
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(o_empty);
+      ++t;
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tmem, 512);
+}
+
+size_t smem_bytes() { return 1024 + 2 * TILE + KVS * 2 * TILE + 2 * PBLK + 2 * TB * 4 + 18 * 8 + 16; }
+
+}  // namespace v2
+
 bool map3(CUtensorMap* m, const void* ptr, long long inner, int T, int B, long long ld, long long bs) {
   auto fn = tc_encode_fn();
   if (!fn) return false;
@@ -496,10 +819,18 @@ int swa_fwd_tc(const SwaP& p, cudaStream_t s) {
   if (!supported(p)) return KL_EUNSUPPORTED;
   CUtensorMap tq;
   if (!map3(&tq, p.QKV, 3LL * p.H * DH, p.T, p.B, p.ld_qkv, p.bs_qkv)) return KL_EUNSUPPORTED;
-  const size_t smem = 1024 + 7 * TILE + 3 * PBLK + 64 + 16;
-  cudaFuncSetAttribute(swa_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  dim3 grid((p.T + TB - 1) / TB, p.H, p.B);
-  swa_fwd_tc_kernel<<<grid, NT, smem, s>>>(tq, p);
+  if (getenv("KL_SWA_FWD_V1")) {
+    const size_t smem = 1024 + 7 * TILE + 3 * PBLK + 64 + 16;
+    cudaFuncSetAttribute(swa_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    dim3 grid((p.T + TB - 1) / TB, p.H, p.B);
+    swa_fwd_tc_kernel<<<grid, NT, smem, s>>>(tq, p);
+  } else {
+    const size_t smem = v2::smem_bytes();
+    cudaFuncSetAttribute(v2::swa_fwd_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int W = p.B * p.H * ((p.T + TB - 1) / TB);
+    const int grid = std::min(W, tc_num_sms());
+    v2::swa_fwd_tc2_kernel<<<grid, v2::NT2, smem, s>>>(tq, p);
+  }
   count_launch();
   return launch_check("swa_fwd_tc");
 }
