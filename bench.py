@@ -197,6 +197,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--gemm-census", action="store_true", help="log every kl_gemm shape/path of one step to stderr")
+    ap.add_argument("--eager", action="store_true", help="issue every kernel from Python each step (no CUDA graph)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
 
@@ -244,14 +245,12 @@ def main():
     lens = [torch.tensor(l, device=dev) for l in Ln]
     y = torch.tensor(yn, device=dev)
 
-    def step(Xs, Ss, ys):
-        model.P.zero_grad()
-        loss, _ = model.loss(Xs, Ss, lens, ys)
-        loss.backward()
-        if reducer is not None:
-            reducer.finish()
-        opt.step()
-        return loss
+    from paper_2602_10016_b200.optim import TrainStep
+
+    bufs = [(X, S, y)]
+    if not args.no_e2e:  # a second static input set: the e2e loop double-buffers host->device copies
+        bufs.append((torch.empty_like(X), [torch.empty_like(s) for s in S], torch.empty_like(y)))
+    steps_ = [TrainStep(model, opt, xb, sb, lens, yb, reducer) for (xb, sb, yb) in bufs]
 
     def barrier():
         if world > 1:
@@ -259,33 +258,62 @@ def main():
         torch.cuda.synchronize()
 
     for _ in range(args.warmup):
-        step(X, S, y)
+        steps_[0].eager()
     barrier()
     if args.gemm_census:
         _capi.GEMM_LOG = []
-        step(X, S, y)
+        steps_[0].eager()
         torch.cuda.synchronize()
         import collections
 
-        c = collections.Counter(_capi.GEMM_LOG)
-        for k, v in sorted(c.items(), key=lambda kv: -kv[0][0] * kv[0][1] * kv[0][2] * kv[0][3] * kv[0][4]):
-            print("gemm", v, "x", k, file=sys.stderr)
+        tms = collections.defaultdict(float)
+        cnt = collections.Counter()
+        for key, s_, e_ in _capi.GEMM_LOG:
+            tms[key] += s_.elapsed_time(e_)
+            cnt[key] += 1
+        tot = sum(tms.values())
+        print(f"gemm total {tot:.3f} ms over {sum(cnt.values())} calls", file=sys.stderr)
+        for k, v in sorted(tms.items(), key=lambda kv: -kv[1]):
+            M_, N_, K_, b1, b2 = k[:5]
+            tf = 2.0 * M_ * N_ * K_ * b1 * b2 * cnt[k] / (v / 1e3) / 1e12 if v > 0 else 0
+            print(f"gemm {v:8.3f} ms {cnt[k]:3d}x {tf:7.1f} TF/s {k}", file=sys.stderr)
         _capi.GEMM_LOG = None
 
-    # ---- device-timed region: inputs resident in HBM ----------------------
+    # The SWA kernels are timed with CUDA events recorded on their launching
+    # stream; in graph mode the event records are nodes of the captured step,
+    # so the durations come from the timed replays themselves.
     timed_ops = {"kl_swa_fwd": [], "kl_swa_bwd": []}
-    _capi.TIMED = timed_ops
+    n_step = _capi.launch_count()
+    steps_[0].eager()
+    launches_per_step = _capi.launch_count() - n_step
+    use_graph = not args.eager
+    if use_graph:
+        try:
+            _capi.TIMED, _capi.TIMED_EXTERNAL = timed_ops, True
+            steps_[0].capture(warmup=0)
+        finally:
+            _capi.TIMED, _capi.TIMED_EXTERNAL = None, False
+        for st in steps_[1:]:
+            st.capture(warmup=0)
+        for _ in range(args.warmup):
+            steps_[0]()
+        barrier()
+
+    # ---- device-timed region: inputs resident in HBM ----------------------
+    if not use_graph:
+        _capi.TIMED = timed_ops
     clocks = ClockSampler(torch.cuda.current_device())
     clocks.start()
-    n0 = _capi.launch_count()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
+    h0 = time.perf_counter()
     for _ in range(args.steps):
-        step(X, S, y)
+        steps_[0]()
+    host_ms = (time.perf_counter() - h0) * 1e3 / args.steps
     e1.record()
     barrier()
-    launches = _capi.launch_count() - n0
+    launches = launches_per_step * args.steps
     clk = clocks.stop()
     _capi.TIMED = None
     ms = e0.elapsed_time(e1) / args.steps
@@ -296,8 +324,9 @@ def main():
     value = world * B / (ms / 1e3)
 
     # ---- roofline of the dominant kernel: SWA (fwd + bwd) ------------------
-    swa_ms = [s.elapsed_time(e) for (s, e) in timed_ops["kl_swa_fwd"]]
-    swab_ms = [s.elapsed_time(e) for (s, e) in timed_ops["kl_swa_bwd"]]
+    nsw = sum(1 for l in range(cfg.L) if model.seq_live()[l] and not model.flags[l].skip_self_attention)
+    swa_ms = [s.elapsed_time(e) for (s, e) in timed_ops["kl_swa_fwd"][-nsw:]] if nsw else []
+    swab_ms = [s.elapsed_time(e) for (s, e) in timed_ops["kl_swa_bwd"][-nsw:]] if nsw else []
 
     flags, live = model.flags, model.seq_live()
     fps = metrics.train_flops_per_sample(cfg, flags, live)
@@ -314,16 +343,18 @@ def main():
         loss_h = torch.empty(args.steps, dtype=torch.float32).pin_memory()
         h2d = Xh.numel() * 2 + sum(s.numel() * 2 for s in Sh) + yh.numel() * 4
         copy = torch.cuda.Stream()
-        bufs = [(torch.empty_like(X), [torch.empty_like(s) for s in S], torch.empty_like(y)) for _ in range(2)]
         ready = [torch.cuda.Event(), torch.cuda.Event()]
+        done = [torch.cuda.Event(), torch.cuda.Event()]
 
         def fetch(i):
+            st = steps_[i % 2]
             with torch.cuda.stream(copy):
-                xb, sb, yb = bufs[i % 2]
-                xb.copy_(Xh, non_blocking=True)
-                for a, b in zip(sb, Sh):
-                    a.copy_(b, non_blocking=True)
-                yb.copy_(yh, non_blocking=True)
+                if i >= 2:
+                    copy.wait_event(done[i % 2])  # step i-2 (same buffers) has finished reading them
+                st.X.copy_(Xh, non_blocking=True)
+                for a_, b_ in zip(st.S, Sh):
+                    a_.copy_(b_, non_blocking=True)
+                st.labels.copy_(yh, non_blocking=True)
                 ready[i % 2].record(copy)
 
         barrier()
@@ -331,14 +362,11 @@ def main():
         f0.record()
         fetch(0)
         for i in range(args.steps):
-            torch.cuda.current_stream().wait_event(ready[i % 2])
-            xb, sb, yb = bufs[i % 2]
-            loss = step(xb, sb, yb)
-            done = torch.cuda.Event()
-            done.record()
             if i + 1 < args.steps:
-                copy.wait_event(done)  # buffer (i+1)%2 was read by step i-1, long finished
-                fetch(i + 1)
+                fetch(i + 1)  # prefetch overlaps step i
+            torch.cuda.current_stream().wait_event(ready[i % 2])
+            loss = steps_[i % 2]()
+            done[i % 2].record()
             loss_h[i].copy_(loss.detach(), non_blocking=True)
         f1.record()
         barrier()
@@ -388,7 +416,7 @@ def main():
                 "ledger": "executed matmul MACs x2 x3 (metrics.py), liveness-pruned, reassociated forms",
                 "reference_formulation_flops_per_sample": fps_ref, "fwd_macs_by_part": macs},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-        "clocks": clk,
+        "clocks": clk, "host_issue_ms_per_step": host_ms, "cuda_graph": use_graph,
     }
     print(json.dumps(line), flush=True)
     if world > 1:

@@ -213,9 +213,11 @@ int kl_act_bwd(int rows, int cols, int dtype, const void* g, long long ldg, cons
                long long ld_y, int n_act, int act_group, const int* act_codes_host, void* stream);
 
 /* Fused Adam step over a flat fp32 parameter buffer (bias-corrected; the
- * SPEC.md trainer default), optionally refreshing a bf16 mirror in place. */
-int kl_adam_step(long long n, float lr, float beta1, float beta2, float eps, int step, float* w, const float* g,
-                 float* m, float* v, void* w_bf16, void* stream);
+ * SPEC.md trainer default), optionally refreshing a bf16 mirror in place.
+ * With step_dev != NULL the step count lives on the device: it is incremented
+ * first and read by the kernel (CUDA-graph replayable). */
+int kl_adam_step(long long n, float lr, float beta1, float beta2, float eps, int step, int* step_dev, float* w,
+                 const float* g, float* m, float* v, void* w_bf16, void* stream);
 
 /* Non-finite scan: atomically ORs 1 into *flag if any element of x is NaN/Inf
  * (NumericsError, tensor.py:21-27). */

@@ -95,7 +95,7 @@ _SIGS = {
                     C.c_void_p, C.c_void_p], C.c_int),
     "kl_act_bwd": ([C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_longlong, C.c_void_p, C.c_longlong, C.c_void_p,
                     C.c_longlong, C.c_int, C.c_int, C.c_void_p, C.c_void_p], C.c_int),
-    "kl_adam_step": ([C.c_longlong, C.c_float, C.c_float, C.c_float, C.c_float, C.c_int] + [C.c_void_p] * 6,
+    "kl_adam_step": ([C.c_longlong, C.c_float, C.c_float, C.c_float, C.c_float, C.c_int] + [C.c_void_p] * 7,
                      C.c_int),
     "kl_check_finite": ([C.c_longlong, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
 }
@@ -235,10 +235,15 @@ def gemm(A: torch.Tensor, B: torch.Tensor, out: torch.Tensor | None = None, *, o
         a.act_group = act_group
         for i, c in enumerate(codes):
             a.act_codes[i] = c
+    if GEMM_LOG is not None:
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
     _check(lib().kl_gemm(C.byref(a), _stream()), "kl_gemm")
     if GEMM_LOG is not None:
-        GEMM_LOG.append((M, N, K, nb1, nb2, int(red1), int(red2), (a.a_rs, a.a_cs), (a.b_rs, a.b_cs),
-                         (a.c_rs, a.c_cs), a.c_dtype, lib().kl_last_gemm_path()))
+        e.record()
+        GEMM_LOG.append(((M, N, K, nb1, nb2, int(red1), int(red2), (a.a_rs, a.a_cs), (a.b_rs, a.b_cs),
+                          (a.c_rs, a.c_cs), a.c_dtype, a.aux_mode, int(bool(residual is not None)), len(acts or ()),
+                          lib().kl_last_gemm_path()), s, e))
     return ret
 
 
@@ -265,11 +270,13 @@ def swa_args(qkv, lengths, H, d_h, w, causal, O, LSE, dO=None, dqkv=None, Dbuf=N
 
 
 TIMED = None  # {entry-point name: [(start, end) CUDA events]} while bench.py times ops
+TIMED_EXTERNAL = False  # record event nodes that survive CUDA-graph capture
 
 
 def call(name: str, *args):
     if TIMED is not None and name in TIMED:
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s = torch.cuda.Event(enable_timing=True, external=TIMED_EXTERNAL)
+        e = torch.cuda.Event(enable_timing=True, external=TIMED_EXTERNAL)
         s.record()
         rc = getattr(lib(), name)(*args)
         e.record()

@@ -514,30 +514,65 @@ extern "C" int kl_check_finite(long long n, int dtype, const void* x, unsigned i
 // the same pass so no separate cast kernel runs before the next forward.
 namespace kl {
 namespace {
-__global__ void adam_kernel(long long n, float lr, float b1, float b2, float eps, float c1, float c2, float* w,
-                            const float* g, float* m, float* v, bf16* wc) {
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    float gi = g[i];
-    float mi = b1 * m[i] + (1.f - b1) * gi;
-    float vi = b2 * v[i] + (1.f - b2) * gi * gi;
+// float4-vectorised; the step count may live on the device (graph replay):
+// the bias corrections are computed per block from *step_dev.
+__global__ void adam_kernel(long long n, float lr, float b1, float b2, float eps, int step, const int* step_dev,
+                            float* w, const float* g, float* m, float* v, bf16* wc) {
+  const int t = step_dev ? *step_dev : step;
+  const float c1 = 1.f / (1.f - powf(b1, (float)t));
+  const float c2 = 1.f / (1.f - powf(b2, (float)t));
+  const long long n4 = n / 4;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
+    const float4 gi = reinterpret_cast<const float4*>(g)[i];
+    float4 mi = reinterpret_cast<float4*>(m)[i], vi = reinterpret_cast<float4*>(v)[i];
+    float4 wi = reinterpret_cast<float4*>(w)[i];
+    float* mp = &mi.x;
+    float* vp = &vi.x;
+    float* wp = &wi.x;
+    const float* gp = &gi.x;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      mp[k] = b1 * mp[k] + (1.f - b1) * gp[k];
+      vp[k] = b2 * vp[k] + (1.f - b2) * gp[k] * gp[k];
+      wp[k] = wp[k] - lr * (mp[k] * c1) / (sqrtf(vp[k] * c2) + eps);
+    }
+    reinterpret_cast<float4*>(m)[i] = mi;
+    reinterpret_cast<float4*>(v)[i] = vi;
+    reinterpret_cast<float4*>(w)[i] = wi;
+    if (wc) {
+      reinterpret_cast<__nv_bfloat162*>(wc)[2 * i] = __floats2bfloat162_rn(wi.x, wi.y);
+      reinterpret_cast<__nv_bfloat162*>(wc)[2 * i + 1] = __floats2bfloat162_rn(wi.z, wi.w);
+    }
+  }
+  for (long long i = n4 * 4 + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const float gi = g[i];
+    const float mi = b1 * m[i] + (1.f - b1) * gi;
+    const float vi = b2 * v[i] + (1.f - b2) * gi * gi;
     m[i] = mi;
     v[i] = vi;
-    float wi = w[i] - lr * (mi * c1) / (sqrtf(vi * c2) + eps);
+    const float wi = w[i] - lr * (mi * c1) / (sqrtf(vi * c2) + eps);
     w[i] = wi;
     if (wc) wc[i] = __float2bfloat16(wi);
   }
 }
+
+__global__ void tick_kernel(int* step_dev) { *step_dev += 1; }
 }  // namespace
 }  // namespace kl
 
-extern "C" int kl_adam_step(long long n, float lr, float beta1, float beta2, float eps, int step, float* w,
-                            const float* g, float* m, float* v, void* w_bf16, void* stream) {
+extern "C" int kl_adam_step(long long n, float lr, float beta1, float beta2, float eps, int step, int* step_dev,
+                            float* w, const float* g, float* m, float* v, void* w_bf16, void* stream) {
   if (n == 0) return KL_OK;
-  if (step < 1) { set_error("kl_adam_step: step must be >= 1"); return KL_EBADSHAPE; }
-  const float c1 = 1.f / (1.f - powf(beta1, (float)step));
-  const float c2 = 1.f / (1.f - powf(beta2, (float)step));
-  unsigned grid = (unsigned)std::min<long long>((n + 255) / 256, 148 * 16);
-  adam_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(n, lr, beta1, beta2, eps, c1, c2, w, g, m, v, (bf16*)w_bf16);
-  count_launch();
+  if (!step_dev && step < 1) { set_error("kl_adam_step: step must be >= 1"); return KL_EBADSHAPE; }
+  if (((uintptr_t)w | (uintptr_t)g | (uintptr_t)m | (uintptr_t)v) & 15) {
+    set_error("kl_adam_step: buffers must be 16-byte aligned");
+    return KL_EBADSHAPE;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  if (step_dev) tick_kernel<<<1, 1, 0, s>>>(step_dev);
+  unsigned grid = (unsigned)std::min<long long>((n / 4 + 255) / 256 + 1, 148 * 8);
+  adam_kernel<<<grid, 256, 0, s>>>(n, lr, beta1, beta2, eps, step, step_dev, w, g, m, v, (bf16*)w_bf16);
+  count_launch(step_dev ? 2 : 1);
   return launch_check("adam_step");
 }
