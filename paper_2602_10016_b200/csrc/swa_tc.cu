@@ -792,6 +792,530 @@ __global__ void __launch_bounds__(NT2, 1) swa_fwd_tc2_kernel(const __grid_consta
 
 size_t smem_bytes() { return 1024 + 2 * TILE + KVS * 2 * TILE + 2 * PBLK + 2 * TB * 4 + 18 * 8 + 16; }
 
+// ---------------------------------------------------------------------------
+// dQ v2: persistent over query blocks (same item order and K/V ring as the
+// forward).  Per key block j: S = Q K_j^T and dP = dO V_j^T land in TMEM
+// (single buffer; the next block's pair is issued as soon as the compute warps
+// have read the current one), the compute warps write dS = P (dP - D) (bf16)
+// into a 2-slot ring, and dQ += dS K_j accumulates in TMEM.
+__global__ void __launch_bounds__(NT2, 1)
+    swa_bwd_dq_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tdo, SwaP p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sQG = sm;                      // 2 x (Q 16 KB | dO 16 KB)
+  uint8_t* sKV = sQG + 2 * 2 * TILE;      // KVS x (K | V)
+  uint8_t* sDS = sKV + KVS * 2 * TILE;    // 2 x 32 KB
+  uint64_t* bar = (uint64_t*)(sDS + 2 * PBLK);
+  uint64_t* qg_full = bar;       // [2]
+  uint64_t* qg_empty = bar + 2;  // [2]
+  uint64_t* kv_full = bar + 4;   // [3]
+  uint64_t* kv_empty = bar + 7;  // [3]
+  uint64_t* ds_full = bar + 10;  // [2]
+  uint64_t* ds_empty = bar + 12; // [2]
+  uint64_t* sdp_full = bar + 14;
+  uint64_t* sdp_empty = bar + 15;
+  uint64_t* dq_full = bar + 16;
+  uint64_t* dq_empty = bar + 17;
+  uint32_t* tslot = (uint32_t*)(bar + 18);
+
+  const int nT = (p.T + TB - 1) / TB;
+  const int W = p.B * p.H * nT;
+  const int i0 = (int)((long long)W * blockIdx.x / gridDim.x);
+  const int i1 = (int)((long long)W * (blockIdx.x + 1) / gridDim.x);
+  const int HD = p.H * DH;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    tc::prefetch_tmap(&tq);
+    tc::prefetch_tmap(&tdo);
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&qg_full[i], 1);
+      tc::mbar_init(&qg_empty[i], 1);
+      tc::mbar_init(&ds_full[i], 8);
+      tc::mbar_init(&ds_empty[i], 1);
+    }
+    for (int i = 0; i < KVS; ++i) {
+      tc::mbar_init(&kv_full[i], 1);
+      tc::mbar_init(&kv_empty[i], 1);
+    }
+    tc::mbar_init(sdp_full, 1);
+    tc::mbar_init(sdp_empty, 8);
+    tc::mbar_init(dq_full, 1);
+    tc::mbar_init(dq_empty, 8);
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tslot, 512);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tslot;
+  const uint32_t T_S = 0, T_DP = 128, T_DQ = 256;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int qcount = 0, cur_bh = -1, hi_loaded = -1;
+      int kv_use[KVS] = {0, 0, 0};
+      for (int idx = i0; idx < i1; ++idx) {
+        const Item it = decode(p, idx, nT);
+        if (!it.real) continue;
+        const int bh = idx / nT;
+        if (bh != cur_bh) {
+          cur_bh = bh;
+          hi_loaded = -1;
+        }
+        const int qs = qcount & 1;
+        tc::mbar_wait(&qg_empty[qs], ((qcount >> 1) & 1) ^ 1);
+        tc::mbar_arrive_expect_tx(&qg_full[qs], 2 * TILE);
+        tc::tma_load_3d(sQG + qs * 2 * TILE, &tq, &qg_full[qs], it.h * DH, it.q0, it.b);
+        tc::tma_load_3d(sQG + qs * 2 * TILE + TILE, &tdo, &qg_full[qs], it.h * DH, it.q0, it.b);
+        ++qcount;
+        for (int j = it.lo; j < it.lo + it.n; ++j) {
+          if (j <= hi_loaded) continue;
+          const int s = j % KVS;
+          tc::mbar_wait(&kv_empty[s], (kv_use[s] & 1) ^ 1);
+          tc::mbar_arrive_expect_tx(&kv_full[s], 2 * TILE);
+          tc::tma_load_3d(sKV + s * 2 * TILE, &tq, &kv_full[s], HD + it.h * DH, j * TB, it.b);
+          tc::tma_load_3d(sKV + s * 2 * TILE + TILE, &tq, &kv_full[s], 2 * HD + it.h * DH, j * TB, it.b);
+          ++kv_use[s];
+          hi_loaded = j;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int qcount = 0, cur_bh = -1, hi_seen = -1, t = 0, sdp = 0, dsc = 0;
+      int kv_use[KVS] = {0, 0, 0};
+      auto score = [&](uint32_t qa, uint32_t ga, int j) {
+        const uint32_t ka = tc::smem_u32(sKV + (j % KVS) * 2 * TILE), va = ka + TILE;
+        tc::mbar_wait(sdp_empty, (sdp & 1) ^ 1);
+        tc::fence_after();
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk) tc::mma_bf16(tmem + T_S, d_kmaj64(qa, kk), d_kmaj64(ka, kk), IDESC_S, kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk) tc::mma_bf16(tmem + T_DP, d_kmaj64(ga, kk), d_kmaj64(va, kk), IDESC_S, kk > 0);
+        tc::mma_commit(sdp_full);
+        ++sdp;
+      };
+      for (int idx = i0; idx < i1; ++idx) {
+        const Item it = decode(p, idx, nT);
+        if (!it.real) continue;
+        const int bh = idx / nT;
+        if (bh != cur_bh) {
+          cur_bh = bh;
+          hi_seen = -1;
+        }
+        const int qs = qcount & 1;
+        tc::mbar_wait(&qg_full[qs], (qcount >> 1) & 1);
+        const uint32_t qa = tc::smem_u32(sQG + qs * 2 * TILE), ga = qa + TILE;
+        for (int jj = 0; jj < it.n; ++jj) {
+          const int j = it.lo + jj, s = j % KVS;
+          if (j > hi_seen) {
+            tc::mbar_wait(&kv_full[s], kv_use[s] & 1);
+            ++kv_use[s];
+            hi_seen = j;
+          }
+        }
+        score(qa, ga, it.lo);
+        tc::mbar_wait(dq_empty, (t & 1) ^ 1);
+        for (int jj = 0; jj < it.n; ++jj) {
+          if (jj + 1 < it.n) score(qa, ga, it.lo + jj + 1);  // waits until block jj's S/dP were read
+          else tc::mma_commit(&qg_empty[qs]);
+          const int ds = dsc & 1;
+          tc::mbar_wait(&ds_full[ds], (dsc >> 1) & 1);
+          tc::fence_after();
+          const uint32_t da = tc::smem_u32(sDS + ds * PBLK);
+          const uint32_t ka = tc::smem_u32(sKV + ((it.lo + jj) % KVS) * 2 * TILE);
+#pragma unroll
+          for (int kk = 0; kk < TB / 16; ++kk) tc::mma_bf16(tmem + T_DQ, d_p(da, kk), d_mn(ka, kk), IDESC_PV, (jj | kk) > 0);
+          tc::mma_commit(&ds_empty[ds]);
+          ++dsc;
+        }
+        tc::mma_commit(dq_full);
+        ++qcount;
+        int keep_lo = it.lo + it.n;
+        if (idx + 1 < i1 && (idx + 1) / nT == bh) {
+          const Item nx = decode(p, idx + 1, nT);
+          if (nx.real) keep_lo = nx.lo;
+        }
+        for (int j = it.lo; j < it.lo + it.n && j < keep_lo; ++j) tc::mma_commit(&kv_empty[j % KVS]);
+        ++t;
+      }
+    }
+  } else {
+    const int qtr = warp & 3, hf = (warp - 2) >> 2;
+    const int r = qtr * 32 + lane;
+    const uint32_t trow = tmem + ((uint32_t)(qtr * 32) << 16);
+    const float c2 = p.scale * 1.4426950408889634f;
+    int t = 0, sdp = 0, dsc = 0;
+    bf16* dq = (bf16*)p.dQKV;
+    for (int idx = i0; idx < i1; ++idx) {
+      const Item it = decode(p, idx, nT);
+      bf16* out = dq + (long long)it.b * p.bs_qkv + it.h * DH;
+      if (!it.real) {
+        zero_rows(out, p.ld_qkv, it.q0, TB, p.T, threadIdx.x - 64, 256);
+        continue;
+      }
+      const int q = it.q0 + r;
+      int klo = max(0, q - p.w), khi = min(it.len - 1, q + p.w);
+      if (p.causal) khi = min(khi, q);
+      float lse2 = 0.f, dr = 0.f;
+      if (q < it.len) {
+        lse2 = p.LSE[((long long)it.b * p.H + it.h) * p.T + q] * 1.4426950408889634f;
+        dr = p.Dbuf[((long long)it.b * p.H + it.h) * p.T + q];
+      } else {
+        khi = -1;
+      }
+      for (int jj = 0; jj < it.n; ++jj) {
+        tc::mbar_wait(sdp_full, sdp & 1);
+        const int ds = dsc & 1;
+        tc::mbar_wait(&ds_empty[ds], ((dsc >> 1) & 1) ^ 1);
+        tc::fence_after();
+        uint8_t* dblk = sDS + ds * PBLK;
+#pragma unroll
+        for (int c = 0; c < 64; c += 32) {
+          const int col = hf * 64 + c;
+          const int k0 = (it.lo + jj) * TB + col;
+          float s[32], g[32];
+          uint32_t pk[16];
+          tc::tmem_ld32(trow + T_S + col, s);
+          tc::tmem_ld32(trow + T_DP + col, g);
+          if (k0 > khi || k0 + 31 < klo) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) pk[i] = 0u;
+          } else if (k0 >= klo && k0 + 31 <= khi) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) {
+              const float a = ex2(fmaf(s[i], c2, -lse2)) * (g[i] - dr);
+              const float bq = ex2(fmaf(s[i + 1], c2, -lse2)) * (g[i + 1] - dr);
+              pk[i >> 1] = tc::pack_bf16(a, bq);
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) {
+              const bool ok0 = k0 + i >= klo && k0 + i <= khi, ok1 = k0 + i + 1 >= klo && k0 + i + 1 <= khi;
+              const float a = ok0 ? ex2(fmaf(s[i], c2, -lse2)) * (g[i] - dr) : 0.f;
+              const float bq = ok1 ? ex2(fmaf(s[i + 1], c2, -lse2)) * (g[i + 1] - dr) : 0.f;
+              pk[i >> 1] = tc::pack_bf16(a, bq);
+            }
+          }
+          store_sw(dblk, r, col, pk);
+        }
+        tc::fence_before();
+        tc::fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tc::mbar_arrive(sdp_empty);
+          tc::mbar_arrive(&ds_full[ds]);
+        }
+        ++sdp;
+        ++dsc;
+      }
+      tc::mbar_wait(dq_full, t & 1);
+      tc::fence_after();
+      {
+        float v[32];
+        tc::tmem_ld32(trow + T_DQ + hf * 32, v);
+        if (q < p.T) {
+          uint4* o = reinterpret_cast<uint4*>(out + (long long)q * p.ld_qkv + hf * 32);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            uint4 u;
+            u.x = tc::pack_bf16(v[8 * c + 0] * p.scale, v[8 * c + 1] * p.scale);
+            u.y = tc::pack_bf16(v[8 * c + 2] * p.scale, v[8 * c + 3] * p.scale);
+            u.z = tc::pack_bf16(v[8 * c + 4] * p.scale, v[8 * c + 5] * p.scale);
+            u.w = tc::pack_bf16(v[8 * c + 6] * p.scale, v[8 * c + 7] * p.scale);
+            o[c] = u;
+          }
+        }
+      }
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(dq_empty);
+      ++t;
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tmem, 512);
+}
+
+size_t dq_smem_bytes() { return 1024 + 4 * TILE + KVS * 2 * TILE + 2 * PBLK + 18 * 8 + 16; }
+
+// ---------------------------------------------------------------------------
+// dK, dV v2: persistent over key blocks in sequence order; the (<= 3) query
+// blocks a key block sees come from a 3-slot Q / dO ring reused across
+// consecutive key blocks.  Per query block i: S^T = K Q_i^T, dP^T = V dO_i^T
+// (TMEM), compute warps write P^T and dS^T (bf16, smem), then
+// dV += P^T dO_i and dK += dS^T Q_i accumulate in TMEM.  LSE / D of the query
+// block are staged in smem by the compute warps.
+__global__ void __launch_bounds__(NT2, 1)
+    swa_bwd_dkv_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tdo, SwaP p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sKVb = sm;                      // K 16 KB | V 16 KB
+  uint8_t* sQG = sKVb + 2 * TILE;          // KVS x (Q | dO)
+  uint8_t* sPT = sQG + KVS * 2 * TILE;     // 32 KB
+  uint8_t* sDT = sPT + PBLK;               // 32 KB
+  float* sLD = (float*)(sDT + PBLK);       // 2 x (lse[128] | D[128])
+  uint64_t* bar = (uint64_t*)(sLD + 4 * TB);
+  uint64_t* kv_full = bar;
+  uint64_t* kv_empty = bar + 1;
+  uint64_t* qg_full = bar + 2;   // [3]
+  uint64_t* qg_empty = bar + 5;  // [3]
+  uint64_t* sdp_full = bar + 8;
+  uint64_t* sdp_empty = bar + 9;
+  uint64_t* pd_full = bar + 10;
+  uint64_t* pd_empty = bar + 11;
+  uint64_t* acc_full = bar + 12;
+  uint64_t* acc_empty = bar + 13;
+  uint32_t* tslot = (uint32_t*)(bar + 14);
+
+  const int nT = (p.T + TB - 1) / TB;
+  const int W = p.B * p.H * nT;
+  const int i0 = (int)((long long)W * blockIdx.x / gridDim.x);
+  const int i1 = (int)((long long)W * (blockIdx.x + 1) / gridDim.x);
+  const int HD = p.H * DH;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  auto qband = [&](int idx, int& b, int& h, int& k0, int& len, int& lo, int& n) {
+    const int kt = idx % nT, bh = idx / nT;
+    h = bh % p.H;
+    b = bh / p.H;
+    k0 = kt * TB;
+    len = p.lengths[b];
+    if (k0 >= len) {
+      lo = n = 0;
+      return false;
+    }
+    const Band qb = query_band(k0, len, p.w, p.causal);
+    lo = qb.lo;
+    n = qb.n;
+    return true;
+  };
+  if (warp == 0 && lane == 0) {
+    tc::prefetch_tmap(&tq);
+    tc::prefetch_tmap(&tdo);
+    tc::mbar_init(kv_full, 1);
+    tc::mbar_init(kv_empty, 1);
+    for (int i = 0; i < KVS; ++i) {
+      tc::mbar_init(&qg_full[i], 1);
+      tc::mbar_init(&qg_empty[i], 1);
+    }
+    tc::mbar_init(sdp_full, 1);
+    tc::mbar_init(sdp_empty, 8);
+    tc::mbar_init(pd_full, 8);
+    tc::mbar_init(pd_empty, 1);
+    tc::mbar_init(acc_full, 1);
+    tc::mbar_init(acc_empty, 8);
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tslot, 512);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tslot;
+  const uint32_t T_S = 0, T_DP = 128, T_DV = 256, T_DK = 320;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int t = 0, cur_bh = -1, hi_loaded = -1;
+      int qg_use[KVS] = {0, 0, 0};
+      for (int idx = i0; idx < i1; ++idx) {
+        int b, h, k0, len, lo, n;
+        if (!qband(idx, b, h, k0, len, lo, n)) continue;
+        const int bh = idx / nT;
+        if (bh != cur_bh) {
+          cur_bh = bh;
+          hi_loaded = -1;
+        }
+        tc::mbar_wait(kv_empty, (t & 1) ^ 1);
+        tc::mbar_arrive_expect_tx(kv_full, 2 * TILE);
+        tc::tma_load_3d(sKVb, &tq, kv_full, HD + h * DH, k0, b);
+        tc::tma_load_3d(sKVb + TILE, &tq, kv_full, 2 * HD + h * DH, k0, b);
+        for (int i = lo; i < lo + n; ++i) {
+          if (i <= hi_loaded) continue;
+          const int s = i % KVS;
+          tc::mbar_wait(&qg_empty[s], (qg_use[s] & 1) ^ 1);
+          tc::mbar_arrive_expect_tx(&qg_full[s], 2 * TILE);
+          tc::tma_load_3d(sQG + s * 2 * TILE, &tq, &qg_full[s], h * DH, i * TB, b);
+          tc::tma_load_3d(sQG + s * 2 * TILE + TILE, &tdo, &qg_full[s], h * DH, i * TB, b);
+          ++qg_use[s];
+          hi_loaded = i;
+        }
+        ++t;
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int t = 0, cur_bh = -1, hi_seen = -1, sdp = 0, pdc = 0;
+      int qg_use[KVS] = {0, 0, 0};
+      const uint32_t ka = tc::smem_u32(sKVb), va = ka + TILE;
+      const uint32_t pt = tc::smem_u32(sPT), dt = tc::smem_u32(sDT);
+      for (int idx = i0; idx < i1; ++idx) {
+        int b, h, k0, len, lo, n;
+        if (!qband(idx, b, h, k0, len, lo, n)) continue;
+        const int bh = idx / nT;
+        if (bh != cur_bh) {
+          cur_bh = bh;
+          hi_seen = -1;
+        }
+        tc::mbar_wait(kv_full, t & 1);
+        for (int i = lo; i < lo + n; ++i) {
+          if (i <= hi_seen) continue;
+          const int s = i % KVS;
+          tc::mbar_wait(&qg_full[s], qg_use[s] & 1);
+          ++qg_use[s];
+          hi_seen = i;
+        }
+        auto score = [&](int i) {
+          const uint32_t qa = tc::smem_u32(sQG + (i % KVS) * 2 * TILE), ga = qa + TILE;
+          tc::mbar_wait(sdp_empty, (sdp & 1) ^ 1);
+          tc::fence_after();
+#pragma unroll
+          for (int kk = 0; kk < DH / 16; ++kk) tc::mma_bf16(tmem + T_S, d_kmaj64(ka, kk), d_kmaj64(qa, kk), IDESC_S, kk > 0);
+#pragma unroll
+          for (int kk = 0; kk < DH / 16; ++kk) tc::mma_bf16(tmem + T_DP, d_kmaj64(va, kk), d_kmaj64(ga, kk), IDESC_S, kk > 0);
+          tc::mma_commit(sdp_full);
+          ++sdp;
+        };
+        score(lo);
+        tc::mbar_wait(acc_empty, (t & 1) ^ 1);
+        for (int ii = 0; ii < n; ++ii) {
+          const int i = lo + ii;
+          if (ii + 1 < n) score(i + 1);
+          else tc::mma_commit(kv_empty);  // K / V of this block no longer read
+          tc::mbar_wait(pd_full, pdc & 1);
+          tc::fence_after();
+          const uint32_t qa = tc::smem_u32(sQG + (i % KVS) * 2 * TILE), ga = qa + TILE;
+#pragma unroll
+          for (int kk = 0; kk < TB / 16; ++kk) tc::mma_bf16(tmem + T_DV, d_p(pt, kk), d_mn(ga, kk), IDESC_PV, (ii | kk) > 0);
+#pragma unroll
+          for (int kk = 0; kk < TB / 16; ++kk) tc::mma_bf16(tmem + T_DK, d_p(dt, kk), d_mn(qa, kk), IDESC_PV, (ii | kk) > 0);
+          tc::mma_commit(pd_empty);
+          ++pdc;
+        }
+        tc::mma_commit(acc_full);
+        int keep_lo = lo + n;
+        if (idx + 1 < i1 && (idx + 1) / nT == bh) {
+          int b2, h2, k02, len2, lo2, n2;
+          if (qband(idx + 1, b2, h2, k02, len2, lo2, n2)) keep_lo = lo2;
+        }
+        for (int i = lo; i < lo + n && i < keep_lo; ++i) tc::mma_commit(&qg_empty[i % KVS]);
+        ++t;
+      }
+    }
+  } else {
+    const int qtr = warp & 3, hf = (warp - 2) >> 2;
+    const int r = qtr * 32 + lane;
+    const int ctid = threadIdx.x - 64;
+    const uint32_t trow = tmem + ((uint32_t)(qtr * 32) << 16);
+    const float c2 = p.scale * 1.4426950408889634f;
+    int t = 0, sdp = 0, pdc = 0;
+    bf16* dqkv = (bf16*)p.dQKV;
+    for (int idx = i0; idx < i1; ++idx) {
+      int b, h, k0, len, lo, n;
+      const bool real = qband(idx, b, h, k0, len, lo, n);
+      bf16* out = dqkv + (long long)b * p.bs_qkv + h * DH;
+      if (!real) {
+        zero_rows(out + HD, p.ld_qkv, k0, TB, p.T, ctid, 256);
+        zero_rows(out + 2 * HD, p.ld_qkv, k0, TB, p.T, ctid, 256);
+        continue;
+      }
+      const int key = k0 + r;
+      int qlo = max(0, key - p.w), qhi = min(len - 1, key + p.w);
+      if (p.causal) qlo = max(qlo, key);
+      if (key >= len) qhi = -1;
+      const float* LSE = p.LSE + ((long long)b * p.H + h) * p.T;
+      const float* D = p.Dbuf + ((long long)b * p.H + h) * p.T;
+      for (int ii = 0; ii < n; ++ii) {
+        const int qb0 = (lo + ii) * TB;
+        float* ls = sLD + (pdc & 1) * 2 * TB;
+        float* dd = ls + TB;
+        if (ctid < TB) {
+          const int q = qb0 + ctid;
+          ls[ctid] = q < len ? LSE[q] * 1.4426950408889634f : INFINITY;
+        } else {
+          const int q = qb0 + ctid - TB;
+          dd[ctid - TB] = q < len ? D[q] : 0.f;
+        }
+        named_bar(1, 256);
+        tc::mbar_wait(sdp_full, sdp & 1);
+        tc::mbar_wait(pd_empty, (pdc & 1) ^ 1);
+        tc::fence_after();
+#pragma unroll
+        for (int c = 0; c < 64; c += 32) {
+          const int col = hf * 64 + c;
+          const int q0c = qb0 + col;
+          float s[32], g[32];
+          uint32_t pp[16], pd[16];
+          tc::tmem_ld32(trow + T_S + col, s);
+          tc::tmem_ld32(trow + T_DP + col, g);
+          if (q0c > qhi || q0c + 31 < qlo) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) pp[i] = pd[i] = 0u;
+          } else {
+            const bool full = q0c >= qlo && q0c + 31 <= qhi;
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) {
+              float pr[2], dsv[2];
+#pragma unroll
+              for (int u = 0; u < 2; ++u) {
+                const int qi = q0c + i + u;
+                const bool ok = full || (qi >= qlo && qi <= qhi);
+                pr[u] = ok ? ex2(fmaf(s[i + u], c2, -ls[col + i + u])) : 0.f;
+                dsv[u] = pr[u] * (g[i + u] - dd[col + i + u]);
+              }
+              pp[i >> 1] = tc::pack_bf16(pr[0], pr[1]);
+              pd[i >> 1] = tc::pack_bf16(dsv[0], dsv[1]);
+            }
+          }
+          store_sw(sPT, r, col, pp);
+          store_sw(sDT, r, col, pd);
+        }
+        tc::fence_before();
+        tc::fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tc::mbar_arrive(sdp_empty);
+          tc::mbar_arrive(pd_full);
+        }
+        ++sdp;
+        ++pdc;
+      }
+      tc::mbar_wait(acc_full, t & 1);
+      tc::fence_after();
+      {
+        float v[32];
+        const bool ok = key < p.T;
+#pragma unroll
+        for (int which = 0; which < 2; ++which) {  // 0: dK (scaled), 1: dV
+          tc::tmem_ld32(trow + (which ? T_DV : T_DK) + hf * 32, v);
+          const float sc = which ? 1.f : p.scale;
+          if (ok) {
+            uint4* o = reinterpret_cast<uint4*>(out + (long long)key * p.ld_qkv + (which ? 2 : 1) * HD + hf * 32);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              uint4 u;
+              u.x = tc::pack_bf16(v[8 * c + 0] * sc, v[8 * c + 1] * sc);
+              u.y = tc::pack_bf16(v[8 * c + 2] * sc, v[8 * c + 3] * sc);
+              u.z = tc::pack_bf16(v[8 * c + 4] * sc, v[8 * c + 5] * sc);
+              u.w = tc::pack_bf16(v[8 * c + 6] * sc, v[8 * c + 7] * sc);
+              o[c] = u;
+            }
+          }
+        }
+      }
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(acc_empty);
+      ++t;
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tmem, 512);
+}
+
+size_t dkv_smem_bytes() { return 1024 + 2 * TILE + KVS * 2 * TILE + 2 * PBLK + 4 * TB * 4 + 14 * 8 + 16; }
+
 }  // namespace v2
 
 bool map3(CUtensorMap* m, const void* ptr, long long inner, int T, int B, long long ld, long long bs) {
@@ -842,6 +1366,17 @@ int swa_bwd_tc(const SwaP& p, cudaStream_t s) {
   if (!map3(&tdo, p.dO, (long long)p.H * DH, p.T, p.B, p.ld_o, p.bs_o)) return KL_EUNSUPPORTED;
   int rc = swa_rowdot(p, s);
   if (rc) return rc;
+  if (!getenv("KL_SWA_BWD_V1")) {
+    const int W = p.B * p.H * ((p.T + TB - 1) / TB);
+    const int grid = std::min(W, tc_num_sms());
+    const size_t s1 = v2::dkv_smem_bytes(), s2 = v2::dq_smem_bytes();
+    cudaFuncSetAttribute(v2::swa_bwd_dkv_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1);
+    v2::swa_bwd_dkv_tc2_kernel<<<grid, v2::NT2, s1, s>>>(tq, tdo, p);
+    cudaFuncSetAttribute(v2::swa_bwd_dq_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2);
+    v2::swa_bwd_dq_tc2_kernel<<<grid, v2::NT2, s2, s>>>(tq, tdo, p);
+    count_launch(2);
+    return launch_check("swa_bwd_tc2");
+  }
   dim3 grid((p.T + TB - 1) / TB, p.H, p.B);
   const size_t smem1 = 1024 + 8 * TILE + 2 * PBLK + 6 * TB * 4 + 64 + 16;
   cudaFuncSetAttribute(swa_bwd_dkv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
