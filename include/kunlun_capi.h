@@ -97,6 +97,10 @@ typedef struct kl_gemm_args {
   const int* row_limit; /* [nb1*nb2] or NULL */
   int n_act, act_group;
   int act_codes[KL_MAX_ACT_GROUPS];
+  /* optional fp32 scratch for split-K of few-tile GEMMs with any epilogue
+   * (partials then a reduce + epilogue pass); NULL disables it */
+  void* workspace;
+  long long workspace_bytes;
 } kl_gemm_args;
 
 int kl_gemm(const kl_gemm_args* args, void* stream);

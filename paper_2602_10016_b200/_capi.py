@@ -37,6 +37,7 @@ class GemmArgs(C.Structure):
         ("bias", C.c_void_p), ("row_limit", C.c_void_p),
         ("n_act", C.c_int), ("act_group", C.c_int),
         ("act_codes", C.c_int * MAX_ACT),
+        ("workspace", C.c_void_p), ("workspace_bytes", C.c_longlong),
     ]
 
 
@@ -159,6 +160,18 @@ def _as4(t: torch.Tensor) -> torch.Tensor:
     return t
 
 
+_WS = {}
+WS_BYTES = 64 << 20  # split-K scratch per device (GEMMs run stream-ordered, so one buffer is reused)
+
+
+def _workspace(device) -> torch.Tensor:
+    ws = _WS.get(device)
+    if ws is None:
+        ws = torch.empty(WS_BYTES // 4, dtype=torch.float32, device=device)
+        _WS[device] = ws
+    return ws
+
+
 def _bstride(t: torch.Tensor, i: int) -> int:
     return 0 if t.shape[i] == 1 else t.stride(i)
 
@@ -238,6 +251,8 @@ def gemm(A: torch.Tensor, B: torch.Tensor, out: torch.Tensor | None = None, *, o
     if GEMM_LOG is not None:
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
+    ws = _workspace(A.device)
+    a.workspace, a.workspace_bytes = ws.data_ptr(), ws.numel() * 4
     _check(lib().kl_gemm(C.byref(a), _stream()), "kl_gemm")
     if GEMM_LOG is not None:
         e.record()

@@ -90,6 +90,8 @@ extern "C" int kl_gemm(const kl_gemm_args* a, void* stream) {
   g.C = a->C; g.c_rs = a->c_rs; g.c_cs = a->c_cs; g.c_s1 = a->c_s1; g.c_s2 = a->c_s2;
   g.R = a->R; g.r_rs = a->r_rs; g.r_cs = a->r_cs; g.r_s1 = a->r_s1; g.r_s2 = a->r_s2;
   g.aux = a->aux;
+  g.ws = (float*)a->workspace;
+  g.ws_bytes = a->workspace ? a->workspace_bytes : 0;
   Epi e;
   e.alpha = a->alpha; e.beta = a->beta; e.bias = a->bias; e.row_limit = a->row_limit;
   e.aux_mode = a->aux_mode; e.n_act = a->n_act; e.act_group = a->act_group > 0 ? a->act_group : 1;

@@ -18,6 +18,8 @@ struct GemmDesc {
   const void* R;
   long long r_rs, r_cs, r_s1, r_s2;
   void* aux;
+  float* ws;  // split-K scratch (fp32) or NULL
+  long long ws_bytes;
 };
 
 // out = act(alpha*acc [* act'(aux)] + bias) [pre-act -> aux] + beta*C + R;

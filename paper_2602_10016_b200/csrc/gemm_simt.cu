@@ -3,7 +3,10 @@
 // This is the FP32 parity path of kl_gemm (kind::tf32 is ~1e-3 accurate and
 // cannot meet the 1e-5 contract) and the fallback for
 // shapes the tcgen05 kernel does not take (tiny M/N, unaligned strides).
-// 64x64 output tile, BK=16, 256 threads, 4x4 register micro-tile.
+// Output tile BM x 64 (BM = 64, or 16 for the many small-M batched products of
+// the summarizers / folds), BK = 16, 256 threads, (BM/16) x 4 register tile.
+// A reduction over the batch / K space may be split across CTAs (fp32
+// atomics into an accumulate-only output).
 #include <algorithm>
 
 #include "common.cuh"
@@ -13,10 +16,12 @@ namespace kl {
 
 namespace {
 
-constexpr int BM = 64, BN = 64, BK = 16;
+constexpr int BN = 64, BK = 16;
 
-template <typename TA, typename TC>
+template <typename TA, typename TC, int BM>
 __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmDesc g, Epi e, int splits) {
+  constexpr int TM = BM / 16;       // rows per thread
+  constexpr int AL = BM * BK / 256;  // A elements loaded per thread per k-step
   __shared__ float As[BK][BM + 4];
   __shared__ float Bs[BK][BN + 4];
   const TA* __restrict__ A = (const TA*)g.A;
@@ -31,9 +36,9 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmDesc g, Epi e, int s
   const int z2o = g.red2 ? 0 : zo % nb2o;
   const int r1n = g.red1 ? g.nb1 : 1, r2n = g.red2 ? g.nb2 : 1;
 
-  float acc[4][4];
+  float acc[TM][4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < TM; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
 
@@ -43,55 +48,66 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmDesc g, Epi e, int s
   const int iters = r1n * r2n * kbn;
   const int it0 = (int)((long long)iters * sp / splits), it1 = (int)((long long)iters * (sp + 1) / splits);
   for (int it = it0; it < it1; ++it) {
-    {
-      const int r = it / kbn, k0 = (it % kbn) * BK;
-      const int r1 = r / r2n, r2 = r % r2n;
-      const int z1 = g.red1 ? r1 : z1o;
-      const int z2 = g.red2 ? r2 : z2o;
-      const TA* Ab = A + (long long)z1 * g.a_s1 + (long long)z2 * g.a_s2;
-      const TA* Bb = Bp + (long long)z1 * g.b_s1 + (long long)z2 * g.b_s2;
-      {
+    const int r = it / kbn, k0 = (it % kbn) * BK;
+    const int r1 = r / r2n, r2 = r % r2n;
+    const int z1 = g.red1 ? r1 : z1o;
+    const int z2 = g.red2 ? r2 : z2o;
+    const TA* Ab = A + (long long)z1 * g.a_s1 + (long long)z2 * g.a_s2;
+    const TA* Bb = Bp + (long long)z1 * g.b_s1 + (long long)z2 * g.b_s2;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          int e_ = tid + 256 * i;
-          int kk, mm;
-          if (a_kfast) { kk = e_ % BK; mm = e_ / BK; }
-          else { mm = e_ % BM; kk = e_ / BM; }
-          int m = m0 + mm, k = k0 + kk;
-          As[kk][mm] = (m < g.M && k < g.K) ? ldf(Ab + (long long)m * g.a_rs + (long long)k * g.a_cs) : 0.f;
-          int nn;
-          if (b_nfast) { nn = e_ % BN; kk = e_ / BN; }
-          else { kk = e_ % BK; nn = e_ / BK; }
-          int n = n0 + nn;
-          k = k0 + kk;
-          Bs[kk][nn] = (n < g.N && k < g.K) ? ldf(Bb + (long long)k * g.b_rs + (long long)n * g.b_cs) : 0.f;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int kk = 0; kk < BK; ++kk) {
-          float a[4], b[4];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
-        }
-        __syncthreads();
+    for (int i = 0; i < AL; ++i) {
+      const int e_ = tid + 256 * i;
+      int kk, mm;
+      if (a_kfast) {
+        kk = e_ % BK;
+        mm = e_ / BK;
+      } else {
+        mm = e_ % BM;
+        kk = e_ / BM;
       }
+      const int m = m0 + mm, k = k0 + kk;
+      As[kk][mm] = (m < g.M && k < g.K) ? ldf(Ab + (long long)m * g.a_rs + (long long)k * g.a_cs) : 0.f;
     }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int e_ = tid + 256 * i;
+      int kk, nn;
+      if (b_nfast) {
+        nn = e_ % BN;
+        kk = e_ / BN;
+      } else {
+        kk = e_ % BK;
+        nn = e_ / BK;
+      }
+      const int n = n0 + nn, k = k0 + kk;
+      Bs[kk][nn] = (n < g.N && k < g.K) ? ldf(Bb + (long long)k * g.b_rs + (long long)n * g.b_cs) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      float a[TM], b[4];
+#pragma unroll
+      for (int i = 0; i < TM; ++i) a[i] = As[kk][ty * TM + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
   }
 
   // epilogue
   TC* C = (TC*)g.C + (long long)z1o * (g.red1 ? 0 : g.c_s1) + (long long)z2o * (g.red2 ? 0 : g.c_s2);
-  const TC* R = g.R ? (const TC*)g.R + (long long)z1o * (g.red1 ? 0 : g.r_s1) + (long long)z2o * (g.red2 ? 0 : g.r_s2) : nullptr;
-  TC* X = g.aux ? (TC*)g.aux + (long long)z1o * (g.red1 ? 0 : g.c_s1) + (long long)z2o * (g.red2 ? 0 : g.c_s2) : nullptr;
+  const TC* R = g.R ? (const TC*)g.R + (long long)z1o * (g.red1 ? 0 : g.r_s1) + (long long)z2o * (g.red2 ? 0 : g.r_s2)
+                    : nullptr;
+  TC* X = g.aux ? (TC*)g.aux + (long long)z1o * (g.red1 ? 0 : g.c_s1) + (long long)z2o * (g.red2 ? 0 : g.c_s2)
+                : nullptr;
   const int lim = e.row_limit ? e.row_limit[zo] : 0x7fffffff;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int m = m0 + ty * 4 + i;
+  for (int i = 0; i < TM; ++i) {
+    const int m = m0 + ty * TM + i;
     if (m >= g.M) continue;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -106,9 +122,8 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmDesc g, Epi e, int s
   }
 }
 
-}  // namespace
-
-int gemm_simt(const GemmDesc& g, const Epi& e, cudaStream_t s) {
+template <int BM>
+int launch(const GemmDesc& g, const Epi& e, cudaStream_t s) {
   const int nout = (g.red1 ? 1 : g.nb1) * (g.red2 ? 1 : g.nb2);
   const long long tiles = (long long)((g.N + BN - 1) / BN) * ((g.M + BM - 1) / BM) * nout;
   const long long iters = (long long)(g.red1 ? g.nb1 : 1) * (g.red2 ? g.nb2 : 1) * ((g.K + BK - 1) / BK);
@@ -123,15 +138,21 @@ int gemm_simt(const GemmDesc& g, const Epi& e, cudaStream_t s) {
     return KL_EUNSUPPORTED;
   }
   if (g.ab_dtype == KL_F32 && g.c_dtype == KL_F32)
-    gemm_simt_kernel<float, float><<<grid, 256, 0, s>>>(g, e, splits);
+    gemm_simt_kernel<float, float, BM><<<grid, 256, 0, s>>>(g, e, splits);
   else if (g.ab_dtype == KL_F32 && g.c_dtype == KL_BF16)
-    gemm_simt_kernel<float, bf16><<<grid, 256, 0, s>>>(g, e, splits);
+    gemm_simt_kernel<float, bf16, BM><<<grid, 256, 0, s>>>(g, e, splits);
   else if (g.ab_dtype == KL_BF16 && g.c_dtype == KL_F32)
-    gemm_simt_kernel<bf16, float><<<grid, 256, 0, s>>>(g, e, splits);
+    gemm_simt_kernel<bf16, float, BM><<<grid, 256, 0, s>>>(g, e, splits);
   else
-    gemm_simt_kernel<bf16, bf16><<<grid, 256, 0, s>>>(g, e, splits);
+    gemm_simt_kernel<bf16, bf16, BM><<<grid, 256, 0, s>>>(g, e, splits);
   count_launch();
   return launch_check("gemm_simt");
+}
+
+}  // namespace
+
+int gemm_simt(const GemmDesc& g, const Epi& e, cudaStream_t s) {
+  return g.M <= 16 ? launch<16>(g, e, s) : launch<64>(g, e, s);
 }
 
 }  // namespace kl

@@ -46,6 +46,7 @@ struct TcParams {
   int vec_r;  // same for the residual
   int r_boxes;  // >0: residual tile staged by TMA in r_boxes 64-column boxes
   int r_has1, r_has2;
+  float* ws;    // split-K partials [split][out batch][M][N] (fp32) or NULL (atomics)
 };
 
 constexpr int SLD = 66;  // epilogue staging row stride (floats): 64 columns + pad, 8-byte aligned
@@ -446,7 +447,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const int cl = c0 + 2 * lane;
         const int n = nb * p.BN + cl;
         const bool ok0 = cl < p.BN && n < p.N, ok1 = cl + 1 < p.BN && n + 1 < p.N;
-        if (p.splits > 1) {
+        if (p.splits > 1 && p.ws) {
+          // split-K partial tile -> workspace; a second pass reduces + applies the epilogue
+          float* wp = p.ws + ((long long)(unit % p.splits) * p.n_out + zo) * p.M * p.N + (long long)m0 * p.N + n;
+          for (int r = 0; r < rows; ++r) {
+            const float2 a = *reinterpret_cast<const float2*>(&stg[r * SLD + 2 * lane]);
+            store_pair(wp + (long long)r * p.N, 1, a.x, a.y, ok0, ok1, (p.N % 2) == 0);
+          }
+        } else if (p.splits > 1) {
           // split-K partial: C += alpha * partial (fp32, beta == 1 accumulate)
           float* cp = (float*)C + (long long)m0 * p.c_rs + (long long)n * p.c_cs;
           for (int r = 0; r < rows; ++r) {
@@ -481,6 +489,30 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   }
   __syncthreads();
   if (warp == 1) tc::tmem_dealloc(tmem, p.tmem_cols);
+}
+
+// Sum the split-K partials and apply the full epilogue (element-wise).
+template <typename TC>
+__global__ void splitk_reduce_kernel(GemmDesc g, Epi e, const float* ws, int splits, int n_out) {
+  const long long MN = (long long)g.M * g.N, total = MN * n_out;
+  const int nb2o = g.red2 ? 1 : g.nb2;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int zo = (int)(i / MN);
+    const long long mn = i % MN;
+    const int m = (int)(mn / g.N), n = (int)(mn % g.N);
+    float acc = 0.f;
+    for (int s = 0; s < splits; ++s) acc += ws[(long long)s * total + i];
+    const int z1o = g.red1 ? 0 : zo / nb2o, z2o = g.red2 ? 0 : zo % nb2o;
+    TC* C = (TC*)g.C + (long long)z1o * (g.red1 ? 0 : g.c_s1) + (long long)z2o * (g.red2 ? 0 : g.c_s2);
+    const TC* R = g.R ? (const TC*)g.R + (long long)z1o * (g.red1 ? 0 : g.r_s1) + (long long)z2o * (g.red2 ? 0 : g.r_s2)
+                      : nullptr;
+    TC* X = g.aux ? (TC*)g.aux + (long long)z1o * (g.red1 ? 0 : g.c_s1) + (long long)z2o * (g.red2 ? 0 : g.c_s2)
+                  : nullptr;
+    const int lim = e.row_limit ? e.row_limit[zo] : 0x7fffffff;
+    epilogue_store(e, C, R, X, (long long)m * g.c_rs + (long long)n * g.c_cs,
+                   (long long)m * g.r_rs + (long long)n * g.r_cs, m, n, lim, acc);
+  }
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -649,8 +681,19 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
   // only an fp32 accumulate-into-C epilogue (beta == 1, nothing else) qualifies.
   const bool accum_only = g.c_dtype == KL_F32 && e.beta == 1.f && !e.bias && !e.row_limit && !e.aux_mode &&
                           e.n_act == 0 && !g.R;
+  p.ws = nullptr;
   if (accum_only && tiles < num_sms() && iters >= 8) {
     p.splits = std::max(1, std::min(num_sms() / tiles, iters / 4));
+  } else if (!accum_only && g.ws && tiles * 2 <= num_sms() && iters >= 8 && !use_r) {
+    // few output tiles with any epilogue: fp32 partials in the workspace, then
+    // one reduce + epilogue pass
+    int sp = std::max(1, std::min(num_sms() / tiles, iters / 4));
+    const long long per = (long long)p.n_out * g.M * g.N * 4;
+    while (sp > 1 && per * sp > g.ws_bytes) --sp;
+    if (sp > 1) {
+      p.splits = sp;
+      p.ws = g.ws;
+    }
   }
   const int total = tiles * p.splits;
   const int grid = std::min(total, num_sms());
@@ -668,7 +711,16 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
     else launch(gemm_tc_kernel<float, false>);
   }
   count_launch();
-  return launch_check("gemm_tc");
+  int rc = launch_check("gemm_tc");
+  if (rc || !p.ws) return rc;
+  const long long total_el = (long long)p.n_out * g.M * g.N;
+  const unsigned rg = (unsigned)std::min<long long>((total_el + 255) / 256, 148 * 16);
+  if (g.c_dtype == KL_BF16)
+    splitk_reduce_kernel<bf16><<<rg, 256, 0, s>>>(g, e, p.ws, p.splits, p.n_out);
+  else
+    splitk_reduce_kernel<float><<<rg, 256, 0, s>>>(g, e, p.ws, p.splits, p.n_out);
+  count_launch();
+  return launch_check("gemm_tc_splitk_reduce");
 }
 
 }  // namespace kl

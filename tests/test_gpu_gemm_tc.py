@@ -117,3 +117,22 @@ def test_tc_strided_views():
     X = torch.randn(B, H, n, d, device="cuda", generator=g).to(torch.bfloat16)
     gemm(X, Wv.transpose(1, 2), o.permute(0, 2, 1, 3))
     assert rel(o.permute(0, 2, 1, 3), X.double() @ Wv.double().transpose(1, 2)) < 1e-5
+
+
+@pytest.mark.parametrize("out_dtype", [torch.bfloat16, torch.float32])
+def test_tc_splitk_workspace(out_dtype):
+    """Few output tiles + long K with a non-accumulating epilogue: split-K
+    through the fp32 workspace and the reduce + epilogue pass."""
+    from paper_2602_10016_b200._capi import gemm
+
+    g = torch.Generator(device="cuda").manual_seed(13)
+    A = operand((128, 6144), True, g)
+    B = operand((6144, 304), False, g)
+    bias = torch.randn(304, device="cuda", generator=g)
+    out = gemm(A, B, out_dtype=out_dtype, bias=bias, acts=["tanh"])
+    ref = torch.tanh(A.double() @ B.double() + bias.double())
+    assert rel(out, ref) < (1e-2 if out_dtype == torch.bfloat16 else 1e-4)  # fp32 accumulation over K=6144
+    R = torch.randn(128, 304, device="cuda", generator=g).to(out_dtype)
+    out = gemm(A, B, out_dtype=out_dtype, residual=R, alpha=0.5)
+    ref = 0.5 * (A.double() @ B.double()) + R.double()
+    assert rel(out, ref) < (1e-2 if out_dtype == torch.bfloat16 else 1e-4)  # fp32 accumulation over K=6144
