@@ -1252,19 +1252,33 @@ __global__ void __launch_bounds__(NT2, 1)
 #pragma unroll
             for (int i = 0; i < 16; ++i) pp[i] = pd[i] = 0u;
           } else {
-            const bool full = q0c >= qlo && q0c + 31 <= qhi;
+            // the 32 columns' LSE / D come from smem as float4 broadcasts
+            float lv[32], dv[32];
 #pragma unroll
-            for (int i = 0; i < 32; i += 2) {
-              float pr[2], dsv[2];
+            for (int i = 0; i < 32; i += 4) {
+              *reinterpret_cast<float4*>(&lv[i]) = *reinterpret_cast<const float4*>(&ls[col + i]);
+              *reinterpret_cast<float4*>(&dv[i]) = *reinterpret_cast<const float4*>(&dd[col + i]);
+            }
+            if (q0c >= qlo && q0c + 31 <= qhi) {
 #pragma unroll
-              for (int u = 0; u < 2; ++u) {
-                const int qi = q0c + i + u;
-                const bool ok = full || (qi >= qlo && qi <= qhi);
-                pr[u] = ok ? ex2(fmaf(s[i + u], c2, -ls[col + i + u])) : 0.f;
-                dsv[u] = pr[u] * (g[i + u] - dd[col + i + u]);
+              for (int i = 0; i < 32; i += 2) {
+                const float p0 = ex2(fmaf(s[i], c2, -lv[i])), p1 = ex2(fmaf(s[i + 1], c2, -lv[i + 1]));
+                pp[i >> 1] = tc::pack_bf16(p0, p1);
+                pd[i >> 1] = tc::pack_bf16(p0 * (g[i] - dv[i]), p1 * (g[i + 1] - dv[i + 1]));
               }
-              pp[i >> 1] = tc::pack_bf16(pr[0], pr[1]);
-              pd[i >> 1] = tc::pack_bf16(dsv[0], dsv[1]);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; i += 2) {
+                float pr[2], dsv[2];
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                  const int qi = q0c + i + u;
+                  pr[u] = (qi >= qlo && qi <= qhi) ? ex2(fmaf(s[i + u], c2, -lv[i + u])) : 0.f;
+                  dsv[u] = pr[u] * (g[i + u] - dv[i + u]);
+                }
+                pp[i >> 1] = tc::pack_bf16(pr[0], pr[1]);
+                pd[i >> 1] = tc::pack_bf16(dsv[0], dsv[1]);
+              }
             }
           }
           store_sw(sPT, r, col, pp);
