@@ -106,6 +106,41 @@ typedef struct kl_gemm_args {
 int kl_gemm(const kl_gemm_args* args, void* stream);
 
 /*
+ * Fused GDPA core (one tcgen05/TMEM kernel per direction, TMA-fed).
+ * Replaces `gdpa_core` forward and its VJP (gdpa.py:141-187) on the folded
+ * per-sample weights Kt = K W_q, Vt = V W_out^T (gdpa.py:120-138):
+ *   Z = S Kt^T * inv_tau, A = Act(Z) (column j uses act_codes[(j/n_kv) % n_act]),
+ *   Y = S + A Vt; rows >= lengths[b] pass through (Y = S, dS = dY).
+ *   bwd: dS = dY + dZ Kt, dKt = dZ^T S, dVt = A^T dY,
+ *        dZ = (dY Vt^T) * Act'(Z) * inv_tau.
+ * S, Y, dY, dS: (B, T, d) bf16 with row stride s_rs, batch stride s_bs.
+ * Kt, Vt, dKt, dVt: (B, HK, d) bf16 contiguous.  Z and A never reach HBM.
+ * Takes bf16, HK = 64, d in {128, 256}; anything else returns KL_EUNSUPPORTED
+ * (the caller composes kl_gemm calls — the fp32 parity path).
+ */
+typedef struct kl_gdpa_args {
+  int B, T, d, HK, n_kv;
+  int dtype;
+  float inv_tau;
+  int n_act;
+  int act_codes[KL_MAX_ACT_GROUPS];
+  const int* lengths;
+  const void* S;
+  long long s_rs, s_bs;
+  const void* Kt;
+  const void* Vt;
+  void* Y; /* forward output */
+  /* backward */
+  const void* dY;
+  void* dS;
+  void* dKt;
+  void* dVt;
+} kl_gdpa_args;
+
+int kl_gdpa_fwd(const kl_gdpa_args* args, void* stream);
+int kl_gdpa_bwd(const kl_gdpa_args* args, void* stream);
+
+/*
  * Sliding-window multi-head self-attention core (flash style; tiles outside
  * the band are never visited).  Replaces the score/softmax/value part of
  * `mha_window` / `mha_full` (attention.py:69-93 with band_mask & length mask,

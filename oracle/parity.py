@@ -3,9 +3,13 @@
 Relative error of a tensor = max|got - ref| / max|ref| (norm-wise; an
 elementwise ratio is meaningless near zeros).
 Parameter gradients: in FP32 every tensor with more than one element is
-held to its own scale; scalar gradients (Wukong gates, the head's output
-bias — sums with heavy cancellation) and, in BF16, every gradient are held
-to the max of their module's gradients (norm-wise over the module).
+held to its own scale (max-norm); scalar gradients (Wukong gates, the head's
+output bias — sums with heavy cancellation) are held to the max of their
+module's gradients.  In BF16 every gradient is compared in the Frobenius
+norm against its module's gradient norm: ||got - ref||_2 / ||ref_module||_2.
+(BF16 max-norm is ill-posed: a relu/threshold input within bf16 rounding of
+its kink flips one derivative and moves a single element by O(1) relative,
+a legitimate difference the 2-norm weighs by its share of the tensor.)
 """
 
 from __future__ import annotations
@@ -38,11 +42,18 @@ def grad_errors(got: dict, ref: dict, fp32: bool) -> dict:
     scale: dict = {}
     for k, v in ref.items():
         g = group(k)
-        scale[g] = max(scale.get(g, 0.0), float(np.abs(v).max()) if v.size else 0.0)
+        if fp32:
+            scale[g] = max(scale.get(g, 0.0), float(np.abs(v).max()) if v.size else 0.0)
+        else:
+            scale[g] = scale.get(g, 0.0) + float(np.sum(np.square(v, dtype=np.float64)))
     out = {}
     for k, v in ref.items():
         a = np.asarray(got[k], dtype=np.float64)
-        num = float(np.abs(a - v).max()) if v.size else 0.0
-        den = float(np.abs(v).max()) if (fp32 and v.size > 1) else scale[group(k)]
+        if fp32:
+            num = float(np.abs(a - v).max()) if v.size else 0.0
+            den = float(np.abs(v).max()) if v.size > 1 else scale[group(k)]
+        else:
+            num = float(np.linalg.norm((a - v).ravel()))
+            den = float(np.sqrt(scale[group(k)]))
         out[k] = num / den if den > 0 else num
     return out

@@ -66,6 +66,18 @@ class ColSoftmaxArgs(C.Structure):
     ]
 
 
+class GdpaArgs(C.Structure):
+    _fields_ = [
+        ("B", C.c_int), ("T", C.c_int), ("d", C.c_int), ("HK", C.c_int), ("n_kv", C.c_int),
+        ("dtype", C.c_int), ("inv_tau", C.c_float), ("n_act", C.c_int),
+        ("act_codes", C.c_int * MAX_ACT),
+        ("lengths", C.c_void_p),
+        ("S", C.c_void_p), ("s_rs", C.c_longlong), ("s_bs", C.c_longlong),
+        ("Kt", C.c_void_p), ("Vt", C.c_void_p), ("Y", C.c_void_p),
+        ("dY", C.c_void_p), ("dS", C.c_void_p), ("dKt", C.c_void_p), ("dVt", C.c_void_p),
+    ]
+
+
 _lib = None
 
 _SIGS = {
@@ -76,6 +88,8 @@ _SIGS = {
     "kl_set_gemm_path": ([C.c_int], None),
     "kl_last_gemm_path": ([], C.c_int),
     "kl_gemm": ([C.POINTER(GemmArgs), C.c_void_p], C.c_int),
+    "kl_gdpa_fwd": ([C.POINTER(GdpaArgs), C.c_void_p], C.c_int),
+    "kl_gdpa_bwd": ([C.POINTER(GdpaArgs), C.c_void_p], C.c_int),
     "kl_swa_fwd": ([C.POINTER(SwaArgs), C.c_void_p], C.c_int),
     "kl_swa_bwd": ([C.POINTER(SwaArgs), C.c_void_p], C.c_int),
     "kl_swa_debug_support": ([C.POINTER(SwaArgs), C.c_void_p, C.c_void_p], C.c_int),

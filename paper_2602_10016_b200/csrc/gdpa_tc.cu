@@ -1,0 +1,642 @@
+// Fused GDPA core on tcgen05/TMEM, fed by TMA (SURVEY.md §8(a) row "GDPA").
+//
+// The folded personalized FFN of one sample (gdpa.py:120-187 with the
+// per-sample fold Kt = K W_q, Vt = V W_out^T of SURVEY.md Appendix C):
+//     Z = S Kt^T * inv_tau   (T x HK),   A = Act_h(Z)  (per n_kv column block)
+//     Y = S + A Vt           (T x d);    rows >= length pass through.
+// and its VJP
+//     dZ = (dY Vt^T) * Act'(Z) * inv_tau,  dS = dY + dZ Kt,
+//     dKt = dZ^T S,                         dVt = A^T dY.
+//
+// Forward, one persistent CTA per SM over (sample, 128-row tile) items:
+//   warp 0  TMA producer: Kt/Vt of the current sample (once per sample) and a
+//           2-slot ring of S tiles (128 x d bf16, SWIZZLE_128B atoms of 64 cols)
+//   warp 1  MMA issuer: Z = S Kt^T into a double-buffered TMEM accumulator
+//           (HK = 64 columns), then Y = A Vt (N = d <= 256) into TMEM
+//   warps 2-9  epilogue: Z -> Act -> bf16 A tile in smem (operand of the
+//           second MMA), then Y + S (residual read from the S tile in smem)
+//           written back INTO the S slot
+//   warp 10 TMA store of the finished slot to Y, then releases the slot.
+// Z and A never touch HBM: per tile the kernel reads S once and writes Y once
+// (algorithmic traffic 4*d bytes per row).
+//
+// Backward, one CTA per sample (dKt/dVt accumulate over the sample's tiles in
+// TMEM: 2 x (d/128) x 64 columns):
+//   MMA  dA = dY Vt^T, Z = S Kt^T            (TMEM cols [0,64), [64,128))
+//   epi  dZ, A -> bf16 tiles in smem
+//   MMA  dS = dZ Kt (TMEM [0,d)), dKt^T += S^T dZ, dVt^T += dY^T A
+//        (S^T / dY^T are the same smem tiles read as MN-major operands)
+//   epi  dS + dY -> written into the dY tile, TMA-stored to dS
+//   end of sample: dKt, dVt (bf16) from TMEM.
+// Traffic per row: read S, dY; write dS (6*d bytes) + 2*HK*d*2 per sample.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "tc_common.cuh"
+
+namespace kl {
+
+PFN_cuTensorMapEncodeTiled_v12000 tc_encode_fn();
+int tc_num_sms();
+
+namespace gdpa {
+
+constexpr int TB = 128;                  // rows per tile
+constexpr int HK = 64;                   // H * n_kv columns of Z
+constexpr int NT = 352;                  // 11 warps
+constexpr uint32_t ATOM_S = TB * 128;    // 128 rows x 64 bf16
+constexpr uint32_t ATOM_KV = HK * 128;   // 64 rows x 64 bf16
+
+struct P {
+  int B, T;
+  float inv_tau;
+  const int* lengths;
+  unsigned char code[HK];  // activation code per Z column
+  bf16* dKt;               // (B, HK, D) bf16, backward
+  bf16* dVt;
+};
+
+// K-major operand whose K extent is split in 64-column atoms `atom` bytes apart.
+__device__ __forceinline__ uint64_t dk(uint32_t base, int kk, uint32_t atom) {
+  return tc::sdesc(base + (kk >> 2) * atom + (kk & 3) * 32, 16, 1024);
+}
+// MN-major operand: 64-element MN chunks `lbo` bytes apart, 16 K-rows per step.
+__device__ __forceinline__ uint64_t dmn(uint32_t base, int kk, uint32_t lbo) {
+  return tc::sdesc(base + kk * 2048, lbo, 1024);
+}
+
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
+
+// 8 packed bf16 pairs (16 columns) into a K-major SW128 tile of TB rows.
+__device__ __forceinline__ void store_sw16(uint8_t* blk, int r, int c0, const uint32_t* pk) {
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    uint4 u = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+    *reinterpret_cast<uint4*>(blk + tc::sw128_off(r, c0 + 8 * c, TB)) = u;
+  }
+}
+
+// In-place: tile(r, c0..c0+31) = bf16(acc[0..31] + tile(r, c0..c0+31)).
+__device__ __forceinline__ void add_residual32(uint8_t* tile, int r, int c0, const float* acc) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    uint4* ptr = reinterpret_cast<uint4*>(tile + tc::sw128_off(r, c0 + 8 * c, TB));
+    uint4 u = *ptr;
+    uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      __nv_bfloat162 h = *reinterpret_cast<__nv_bfloat162*>(&w[i]);
+      const float2 f = __bfloat1622float2(h);
+      w[i] = tc::pack_bf16(acc[8 * c + 2 * i] + f.x, acc[8 * c + 2 * i + 1] + f.y);
+    }
+    *ptr = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+__device__ __forceinline__ uint8_t* align1k(uint8_t* p) {
+  return (uint8_t*)(((uintptr_t)p + 1023) & ~(uintptr_t)1023);
+}
+
+template <int D>
+constexpr size_t fwd_smem() {
+  return 1024 + 2 * (D / 64) * ATOM_S + 2 * (D / 64) * ATOM_KV + ATOM_S + 256;
+}
+template <int D>
+constexpr size_t bwd_smem() {
+  return 1024 + 2 * (D / 64) * ATOM_S + 2 * (D / 64) * ATOM_KV + 2 * ATOM_S + 256;
+}
+
+// ---------------------------------------------------------------------------
+template <int D>
+__global__ void __launch_bounds__(NT, 1)
+    gdpa_fwd_kernel(const __grid_constant__ CUtensorMap ts, const __grid_constant__ CUtensorMap tk,
+                    const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap ty, const P p) {
+  constexpr int NA = D / 64;
+  constexpr uint32_t SLOT = NA * ATOM_S;
+  constexpr uint32_t IDESC_Z = tc::idesc_bf16(TB, HK, 0, 0);
+  constexpr uint32_t IDESC_Y = tc::idesc_bf16(TB, D, 0, 1);
+  constexpr uint32_t T_Y = 256;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sS = align1k(smem_raw);       // 2 slots
+  uint8_t* sK = sS + 2 * SLOT;
+  uint8_t* sV = sK + NA * ATOM_KV;
+  uint8_t* sA = sV + NA * ATOM_KV;
+  uint64_t* bar = (uint64_t*)(sA + ATOM_S);
+  uint64_t* s_full = bar;        // [2]
+  uint64_t* s_empty = bar + 2;   // [2]
+  uint64_t* kv_full = bar + 4;
+  uint64_t* kv_empty = bar + 5;
+  uint64_t* z_full = bar + 6;    // [2]
+  uint64_t* z_empty = bar + 8;   // [2]
+  uint64_t* a_full = bar + 10;
+  uint64_t* a_empty = bar + 11;
+  uint64_t* y_full = bar + 12;
+  uint64_t* y_empty = bar + 13;
+  uint64_t* st_full = bar + 14;  // [2]
+  uint32_t* tslot = (uint32_t*)(bar + 16);
+
+  const int nT = (p.T + TB - 1) / TB;
+  const int W = p.B * nT;
+  const int i0 = (int)((long long)W * blockIdx.x / gridDim.x);
+  const int i1 = (int)((long long)W * (blockIdx.x + 1) / gridDim.x);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    tc::prefetch_tmap(&ts);
+    tc::prefetch_tmap(&tk);
+    tc::prefetch_tmap(&tv);
+    tc::prefetch_tmap(&ty);
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&s_full[i], 1);
+      tc::mbar_init(&s_empty[i], 1);
+      tc::mbar_init(&z_full[i], 1);
+      tc::mbar_init(&z_empty[i], 8);
+      tc::mbar_init(&st_full[i], 8);
+    }
+    tc::mbar_init(kv_full, 1);
+    tc::mbar_init(kv_empty, 1);
+    tc::mbar_init(a_full, 8);
+    tc::mbar_init(a_empty, 1);
+    tc::mbar_init(y_full, 1);
+    tc::mbar_init(y_empty, 8);
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tslot, 512);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int cur_b = -1, ns = 0;
+      for (int k = i0, c = 0; k < i1; ++k, ++c) {
+        const int b = k / nT, q0 = (k % nT) * TB;
+        if (b != cur_b) {
+          tc::mbar_wait(kv_empty, (ns & 1) ^ 1);
+          tc::mbar_arrive_expect_tx(kv_full, 2 * NA * ATOM_KV);
+#pragma unroll
+          for (int a = 0; a < NA; ++a) {
+            tc::tma_load_3d(sK + a * ATOM_KV, &tk, kv_full, a * 64, 0, b);
+            tc::tma_load_3d(sV + a * ATOM_KV, &tv, kv_full, a * 64, 0, b);
+          }
+          cur_b = b;
+          ++ns;
+        }
+        const int sl = c & 1;
+        tc::mbar_wait(&s_empty[sl], ((c >> 1) & 1) ^ 1);
+        tc::mbar_arrive_expect_tx(&s_full[sl], SLOT);
+#pragma unroll
+        for (int a = 0; a < NA; ++a) tc::tma_load_3d(sS + sl * SLOT + a * ATOM_S, &ts, &s_full[sl], a * 64, q0, b);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int ns = 0;
+      auto mma1 = [&](int k, int c) {
+        const int sl = c & 1;
+        if (k == i0 || k % nT == 0) {  // first tile of a sample in this CTA
+          tc::mbar_wait(kv_full, ns & 1);
+          ++ns;
+        }
+        tc::mbar_wait(&s_full[sl], (c >> 1) & 1);
+        tc::mbar_wait(&z_empty[sl], ((c >> 1) & 1) ^ 1);
+        tc::fence_after();
+        const uint32_t sa = tc::smem_u32(sS + sl * SLOT), ka = tc::smem_u32(sK);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          tc::mma_bf16(tmem + sl * HK, dk(sa, kk, ATOM_S), dk(ka, kk, ATOM_KV), IDESC_Z, kk > 0);
+        tc::mma_commit(&z_full[sl]);
+      };
+      int issued = 0;  // number of items whose first MMA is issued
+      for (int k = i0, c = 0; k < i1; ++k, ++c) {
+        if (issued == c) {
+          mma1(k, c);
+          ++issued;
+        }
+        const bool last_of_sample = (k + 1 == i1) || ((k + 1) % nT == 0);
+        if (!last_of_sample) {  // run the next tile's Z while this tile's A is formed
+          mma1(k + 1, c + 1);
+          ++issued;
+        }
+        tc::mbar_wait(a_full, c & 1);
+        tc::mbar_wait(y_empty, (c & 1) ^ 1);
+        tc::fence_after();
+        const uint32_t aa = tc::smem_u32(sA), va = tc::smem_u32(sV);
+#pragma unroll
+        for (int kk = 0; kk < HK / 16; ++kk) tc::mma_bf16(tmem + T_Y, dk(aa, kk, ATOM_S), dmn(va, kk, ATOM_KV), IDESC_Y, kk > 0);
+        tc::mma_commit(y_full);
+        tc::mma_commit(a_empty);
+        if (last_of_sample) tc::mma_commit(kv_empty);
+      }
+    }
+  } else if (warp < 10) {
+    const int qtr = warp & 3, hf = (warp - 2) >> 2;
+    const int r = qtr * 32 + lane;
+    const uint32_t trow = tmem + ((uint32_t)(qtr * 32) << 16);
+    for (int k = i0, c = 0; k < i1; ++k, ++c) {
+      const int b = k / nT, q0 = (k % nT) * TB;
+      const bool live = q0 + r < __ldg(&p.lengths[b]);
+      const int sl = c & 1;
+      // ---- A = Act(Z) (this half's 32 columns) -> sA
+      tc::mbar_wait(&z_full[sl], (c >> 1) & 1);
+      tc::fence_after();
+      float v[32];
+      tc::tmem_ld32(trow + sl * HK + hf * 32, v);
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&z_empty[sl]);
+      uint32_t pk[16];
+#pragma unroll
+      for (int i = 0; i < 32; i += 2) {
+        const int j = hf * 32 + i;
+        const float a0 = live ? act_apply(p.code[j], v[i] * p.inv_tau) : 0.f;
+        const float a1 = live ? act_apply(p.code[j + 1], v[i + 1] * p.inv_tau) : 0.f;
+        pk[i >> 1] = tc::pack_bf16(a0, a1);
+      }
+      tc::mbar_wait(a_empty, (c & 1) ^ 1);
+      store_sw16(sA, r, hf * 32, pk);
+      store_sw16(sA, r, hf * 32 + 16, pk + 8);
+      tc::fence_async_smem();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(a_full);
+      // ---- Y = acc + S, in place in the S slot
+      tc::mbar_wait(y_full, c & 1);
+      tc::fence_after();
+      uint8_t* tile = sS + sl * SLOT;
+#pragma unroll 1
+      for (int cc = hf * (D / 2); cc < (hf + 1) * (D / 2); cc += 32) {
+        tc::tmem_ld32(trow + T_Y + cc, v);
+        add_residual32(tile, r, cc, v);
+      }
+      tc::fence_before();
+      tc::fence_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tc::mbar_arrive(y_empty);
+        tc::mbar_arrive(&st_full[sl]);
+      }
+    }
+  } else {
+    if (lane == 0) {
+      for (int k = i0, c = 0; k < i1; ++k, ++c) {
+        const int b = k / nT, q0 = (k % nT) * TB;
+        const int sl = c & 1;
+        tc::mbar_wait(&st_full[sl], (c >> 1) & 1);
+#pragma unroll
+        for (int a = 0; a < NA; ++a) tc::tma_store_3d(&ty, sS + sl * SLOT + a * ATOM_S, a * 64, q0, b);
+        tc::bulk_commit();
+        tc::bulk_wait_read0();
+        tc::mbar_arrive(&s_empty[sl]);
+      }
+      tc::bulk_wait0();
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tmem, 512);
+}
+
+// ---------------------------------------------------------------------------
+template <int D>
+__global__ void __launch_bounds__(NT, 1)
+    gdpa_bwd_kernel(const __grid_constant__ CUtensorMap ts, const __grid_constant__ CUtensorMap tg,
+                    const __grid_constant__ CUtensorMap tk, const __grid_constant__ CUtensorMap tv,
+                    const __grid_constant__ CUtensorMap tds, const P p) {
+  constexpr int NA = D / 64, NM = D / 128;
+  constexpr uint32_t SLOT = NA * ATOM_S;
+  constexpr uint32_t IDESC_Z = tc::idesc_bf16(TB, HK, 0, 0);
+  constexpr uint32_t IDESC_DS = tc::idesc_bf16(TB, D, 0, 1);
+  constexpr uint32_t IDESC_W = tc::idesc_bf16(TB, HK, 1, 1);
+  constexpr uint32_t T_DK = 256, T_DV = 384;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sS = align1k(smem_raw);
+  uint8_t* sG = sS + SLOT;
+  uint8_t* sK = sG + SLOT;
+  uint8_t* sV = sK + NA * ATOM_KV;
+  uint8_t* sDZ = sV + NA * ATOM_KV;
+  uint8_t* sA = sDZ + ATOM_S;
+  uint64_t* bar = (uint64_t*)(sA + ATOM_S);
+  uint64_t* sg_full = bar;
+  uint64_t* sg_empty = bar + 1;
+  uint64_t* kv_full = bar + 2;
+  uint64_t* kv_empty = bar + 3;
+  uint64_t* zz_full = bar + 4;
+  uint64_t* dz_full = bar + 5;
+  uint64_t* ds_full = bar + 6;
+  uint64_t* st_full = bar + 7;
+  uint64_t* acc_full = bar + 8;
+  uint64_t* acc_empty = bar + 9;
+  uint32_t* tslot = (uint32_t*)(bar + 10);
+
+  const int nT = (p.T + TB - 1) / TB;
+  const int b0 = (int)((long long)p.B * blockIdx.x / gridDim.x);
+  const int b1 = (int)((long long)p.B * (blockIdx.x + 1) / gridDim.x);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    tc::prefetch_tmap(&ts);
+    tc::prefetch_tmap(&tg);
+    tc::prefetch_tmap(&tk);
+    tc::prefetch_tmap(&tv);
+    tc::prefetch_tmap(&tds);
+    tc::mbar_init(sg_full, 1);
+    tc::mbar_init(sg_empty, 1);
+    tc::mbar_init(kv_full, 1);
+    tc::mbar_init(kv_empty, 1);
+    tc::mbar_init(zz_full, 1);
+    tc::mbar_init(dz_full, 8);
+    tc::mbar_init(ds_full, 1);
+    tc::mbar_init(st_full, 8);
+    tc::mbar_init(acc_full, 1);
+    tc::mbar_init(acc_empty, 8);
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tslot, 512);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int c = 0, ns = 0;
+      for (int b = b0; b < b1; ++b, ++ns) {
+        tc::mbar_wait(kv_empty, (ns & 1) ^ 1);
+        tc::mbar_arrive_expect_tx(kv_full, 2 * NA * ATOM_KV);
+#pragma unroll
+        for (int a = 0; a < NA; ++a) {
+          tc::tma_load_3d(sK + a * ATOM_KV, &tk, kv_full, a * 64, 0, b);
+          tc::tma_load_3d(sV + a * ATOM_KV, &tv, kv_full, a * 64, 0, b);
+        }
+        for (int t = 0; t < nT; ++t, ++c) {
+          tc::mbar_wait(sg_empty, (c & 1) ^ 1);
+          tc::mbar_arrive_expect_tx(sg_full, 2 * SLOT);
+#pragma unroll
+          for (int a = 0; a < NA; ++a) {
+            tc::tma_load_3d(sS + a * ATOM_S, &ts, sg_full, a * 64, t * TB, b);
+            tc::tma_load_3d(sG + a * ATOM_S, &tg, sg_full, a * 64, t * TB, b);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int c = 0, ns = 0;
+      const uint32_t ua = tc::smem_u32(sS), ga = tc::smem_u32(sG), ka = tc::smem_u32(sK), va = tc::smem_u32(sV);
+      const uint32_t dza = tc::smem_u32(sDZ), aa = tc::smem_u32(sA);
+      for (int b = b0; b < b1; ++b, ++ns) {
+        tc::mbar_wait(kv_full, ns & 1);
+        for (int t = 0; t < nT; ++t, ++c) {
+          tc::mbar_wait(sg_full, c & 1);
+          tc::fence_after();
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            tc::mma_bf16(tmem, dk(ga, kk, ATOM_S), dk(va, kk, ATOM_KV), IDESC_Z, kk > 0);
+            tc::mma_bf16(tmem + HK, dk(ua, kk, ATOM_S), dk(ka, kk, ATOM_KV), IDESC_Z, kk > 0);
+          }
+          tc::mma_commit(zz_full);
+          tc::mbar_wait(dz_full, c & 1);
+          if (t == 0) tc::mbar_wait(acc_empty, (ns & 1) ^ 1);
+          tc::fence_after();
+#pragma unroll
+          for (int kk = 0; kk < HK / 16; ++kk) tc::mma_bf16(tmem, dk(dza, kk, ATOM_S), dmn(ka, kk, ATOM_KV), IDESC_DS, kk > 0);
+#pragma unroll
+          for (int mh = 0; mh < NM; ++mh) {
+#pragma unroll
+            for (int kk = 0; kk < TB / 16; ++kk) {
+              const uint32_t acc = (t > 0 || kk > 0) ? 1u : 0u;
+              tc::mma_bf16(tmem + T_DK + mh * HK, dmn(ua + 2 * mh * ATOM_S, kk, ATOM_S), dmn(dza, kk, ATOM_S),
+                           IDESC_W, acc);
+              tc::mma_bf16(tmem + T_DV + mh * HK, dmn(ga + 2 * mh * ATOM_S, kk, ATOM_S), dmn(aa, kk, ATOM_S),
+                           IDESC_W, acc);
+            }
+          }
+          tc::mma_commit(ds_full);
+        }
+        tc::mma_commit(acc_full);
+        tc::mma_commit(kv_empty);
+      }
+    }
+  } else if (warp < 10) {
+    const int qtr = warp & 3, hf = (warp - 2) >> 2;
+    const int r = qtr * 32 + lane;
+    const uint32_t trow = tmem + ((uint32_t)(qtr * 32) << 16);
+    int c = 0, ns = 0;
+    for (int b = b0; b < b1; ++b, ++ns) {
+      const int len = __ldg(&p.lengths[b]);
+      for (int t = 0; t < nT; ++t, ++c) {
+        const bool live = t * TB + r < len;
+        // ---- dZ = dA * Act'(Z) * inv_tau, A = Act(Z) -> smem operand tiles
+        tc::mbar_wait(zz_full, c & 1);
+        tc::fence_after();
+        float da[32], z[32];
+        tc::tmem_ld32(trow + hf * 32, da);
+        tc::tmem_ld32(trow + HK + hf * 32, z);
+        uint32_t pdz[16], pa[16];
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          float d0 = 0.f, d1 = 0.f, a0 = 0.f, a1 = 0.f;
+          if (live) {
+            const int j = hf * 32 + i;
+            const float z0 = z[i] * p.inv_tau, z1 = z[i + 1] * p.inv_tau;
+            a0 = act_apply(p.code[j], z0);
+            a1 = act_apply(p.code[j + 1], z1);
+            d0 = da[i] * act_deriv(p.code[j], z0) * p.inv_tau;
+            d1 = da[i + 1] * act_deriv(p.code[j + 1], z1) * p.inv_tau;
+          }
+          pdz[i >> 1] = tc::pack_bf16(d0, d1);
+          pa[i >> 1] = tc::pack_bf16(a0, a1);
+        }
+        store_sw16(sDZ, r, hf * 32, pdz);
+        store_sw16(sDZ, r, hf * 32 + 16, pdz + 8);
+        store_sw16(sA, r, hf * 32, pa);
+        store_sw16(sA, r, hf * 32 + 16, pa + 8);
+        tc::fence_before();
+        tc::fence_async_smem();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(dz_full);
+        // ---- dS = acc + dY, in place in the dY tile
+        tc::mbar_wait(ds_full, c & 1);
+        tc::fence_after();
+#pragma unroll 1
+        for (int cc = hf * (D / 2); cc < (hf + 1) * (D / 2); cc += 32) {
+          tc::tmem_ld32(trow + cc, da);
+          add_residual32(sG, r, cc, da);
+        }
+        tc::fence_before();
+        tc::fence_async_smem();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(st_full);
+      }
+      // ---- dKt, dVt of this sample: TMEM lane = feature column c
+      tc::mbar_wait(acc_full, ns & 1);
+      tc::fence_after();
+      if (hf < NM) {
+        const int col = hf * 128 + r;
+        bf16* dk_out = p.dKt + (long long)b * HK * D + col;
+        bf16* dv_out = p.dVt + (long long)b * HK * D + col;
+#pragma unroll
+        for (int h = 0; h < HK; h += 32) {
+          float v[32];
+          tc::tmem_ld32(trow + T_DK + hf * HK + h, v);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) dk_out[(long long)(h + i) * D] = __float2bfloat16(v[i]);
+          tc::tmem_ld32(trow + T_DV + hf * HK + h, v);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) dv_out[(long long)(h + i) * D] = __float2bfloat16(v[i]);
+        }
+      }
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(acc_empty);
+    }
+  } else {
+    if (lane == 0) {
+      int c = 0;
+      for (int b = b0; b < b1; ++b) {
+        for (int t = 0; t < nT; ++t, ++c) {
+          tc::mbar_wait(st_full, c & 1);
+#pragma unroll
+          for (int a = 0; a < NA; ++a) tc::tma_store_3d(&tds, sG + a * ATOM_S, a * 64, t * TB, b);
+          tc::bulk_commit();
+          tc::bulk_wait_read0();
+          tc::mbar_arrive(sg_empty);
+        }
+      }
+      tc::bulk_wait0();
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tmem, 512);
+}
+
+bool map3(CUtensorMap* m, const void* ptr, long long inner, long long rows, long long B, long long ld, long long bs,
+          int box_rows) {
+  auto fn = tc_encode_fn();
+  if (!fn) return false;
+  if (((uintptr_t)ptr & 15) || (ld * 2) % 16 || (bs * 2) % 16) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)rows, (cuuint64_t)B};
+  cuuint64_t strides[2] = {(cuuint64_t)(ld * 2), (cuuint64_t)(bs * 2)};
+  cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace gdpa
+}  // namespace kl
+
+// ---------------------------------------------------------------------------
+// C ABI
+using namespace kl;
+
+static int gdpa_prepare(const kl_gdpa_args* a, const char* who, gdpa::P& p) {
+  if (!a || a->B < 0 || a->T < 0 || a->d < 1 || a->HK < 1 || a->n_kv < 1) {
+    set_error("%s: bad extents", who);
+    return KL_EBADSHAPE;
+  }
+  if (a->HK % a->n_kv) {
+    set_error("%s: HK=%d is not a multiple of n_kv=%d", who, a->HK, a->n_kv);
+    return KL_EBADSHAPE;
+  }
+  if (!a->lengths || !a->S || !a->Kt || !a->Vt) {
+    set_error("%s: lengths, S, Kt and Vt are required", who);
+    return KL_EBADSHAPE;
+  }
+  if (a->dtype != KL_BF16 || a->HK != gdpa::HK || (a->d != 128 && a->d != 256) || !kl_tcgen05_available()) {
+    set_error("%s: fused path takes bf16, HK=%d, d in {128,256} on sm_100 (got dtype=%d HK=%d d=%d)", who,
+              gdpa::HK, a->dtype, a->HK, a->d);
+    return KL_EUNSUPPORTED;
+  }
+  if (a->n_act < 0 || a->n_act > KL_MAX_ACT_GROUPS) {
+    set_error("%s: bad n_act %d", who, a->n_act);
+    return KL_EBADSHAPE;
+  }
+  p.B = a->B;
+  p.T = a->T;
+  p.inv_tau = a->inv_tau;
+  p.lengths = a->lengths;
+  for (int j = 0; j < gdpa::HK; ++j) {
+    const int h = j / a->n_kv;
+    p.code[j] = (unsigned char)(a->n_act ? a->act_codes[h % a->n_act] : KL_ACT_IDENTITY);
+  }
+  p.dKt = (bf16*)a->dKt;
+  p.dVt = (bf16*)a->dVt;
+  return KL_OK;
+}
+
+template <int D>
+static int gdpa_fwd_launch(const kl_gdpa_args* a, const gdpa::P& p, cudaStream_t s) {
+  CUtensorMap ts, tk, tv, ty;
+  const long long kvbs = (long long)gdpa::HK * D;
+  if (!gdpa::map3(&ts, a->S, D, a->T, a->B, a->s_rs, a->s_bs, gdpa::TB) ||
+      !gdpa::map3(&ty, a->Y, D, a->T, a->B, a->s_rs, a->s_bs, gdpa::TB) ||
+      !gdpa::map3(&tk, a->Kt, D, gdpa::HK, a->B, D, kvbs, gdpa::HK) ||
+      !gdpa::map3(&tv, a->Vt, D, gdpa::HK, a->B, D, kvbs, gdpa::HK)) {
+    set_error("kl_gdpa_fwd: tensor map encode failed (alignment?)");
+    return KL_EUNSUPPORTED;
+  }
+  const size_t smem = gdpa::fwd_smem<D>();
+  cudaFuncSetAttribute(gdpa::gdpa_fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int W = a->B * ((a->T + gdpa::TB - 1) / gdpa::TB);
+  const int grid = std::min(W, tc_num_sms());
+  gdpa::gdpa_fwd_kernel<D><<<grid, gdpa::NT, smem, s>>>(ts, tk, tv, ty, p);
+  count_launch();
+  return launch_check("gdpa_fwd_tc");
+}
+
+template <int D>
+static int gdpa_bwd_launch(const kl_gdpa_args* a, const gdpa::P& p, cudaStream_t s) {
+  CUtensorMap ts, tg, tk, tv, tds;
+  const long long kvbs = (long long)gdpa::HK * D;
+  if (!gdpa::map3(&ts, a->S, D, a->T, a->B, a->s_rs, a->s_bs, gdpa::TB) ||
+      !gdpa::map3(&tg, a->dY, D, a->T, a->B, a->s_rs, a->s_bs, gdpa::TB) ||
+      !gdpa::map3(&tds, a->dS, D, a->T, a->B, a->s_rs, a->s_bs, gdpa::TB) ||
+      !gdpa::map3(&tk, a->Kt, D, gdpa::HK, a->B, D, kvbs, gdpa::HK) ||
+      !gdpa::map3(&tv, a->Vt, D, gdpa::HK, a->B, D, kvbs, gdpa::HK)) {
+    set_error("kl_gdpa_bwd: tensor map encode failed (alignment?)");
+    return KL_EUNSUPPORTED;
+  }
+  const size_t smem = gdpa::bwd_smem<D>();
+  cudaFuncSetAttribute(gdpa::gdpa_bwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int grid = std::min(a->B, tc_num_sms());
+  gdpa::gdpa_bwd_kernel<D><<<grid, gdpa::NT, smem, s>>>(ts, tg, tk, tv, tds, p);
+  count_launch();
+  return launch_check("gdpa_bwd_tc");
+}
+
+extern "C" int kl_gdpa_fwd(const kl_gdpa_args* a, void* stream) {
+  gdpa::P p;
+  int rc = gdpa_prepare(a, "kl_gdpa_fwd", p);
+  if (rc) return rc;
+  if (!a->Y) {
+    set_error("kl_gdpa_fwd: Y is required");
+    return KL_EBADSHAPE;
+  }
+  if (a->B == 0 || a->T == 0) return KL_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  return a->d == 256 ? gdpa_fwd_launch<256>(a, p, s) : gdpa_fwd_launch<128>(a, p, s);
+}
+
+extern "C" int kl_gdpa_bwd(const kl_gdpa_args* a, void* stream) {
+  gdpa::P p;
+  int rc = gdpa_prepare(a, "kl_gdpa_bwd", p);
+  if (rc) return rc;
+  if (!a->dY || !a->dS || !a->dKt || !a->dVt) {
+    set_error("kl_gdpa_bwd: dY, dS, dKt and dVt are required");
+    return KL_EBADSHAPE;
+  }
+  if (a->B == 0) return KL_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (a->T == 0) {
+    cudaMemsetAsync(a->dKt, 0, (size_t)a->B * a->HK * a->d * 2, s);
+    cudaMemsetAsync(a->dVt, 0, (size_t)a->B * a->HK * a->d * 2, s);
+    return launch_check("gdpa_bwd_tc");
+  }
+  return a->d == 256 ? gdpa_bwd_launch<256>(a, p, s) : gdpa_bwd_launch<128>(a, p, s);
+}

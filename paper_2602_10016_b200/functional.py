@@ -128,7 +128,7 @@ class _Linear(torch.autograd.Function):
     (epilogue aux) for the VJP."""
 
     @staticmethod
-    def forward(ctx, x, flat, P, wkey, bkey, act, residual):
+    def forward(ctx, x, flat, P, wkey, bkey, act, residual, out_dtype=None):
         W = P.w(wkey)
         N = W.shape[0]
         codes = _codes(act) if act and act != "identity" else []
@@ -138,7 +138,7 @@ class _Linear(torch.autograd.Function):
         if codes:
             pre = torch.empty(x4.shape[:-1] + (N,), device=x.device, dtype=x.dtype)
         y = gemm(x4, W.t(), bias=bias, acts=codes or None, aux=pre, aux_mode=1 if codes else 0,
-                 residual=residual)
+                 residual=residual, out_dtype=out_dtype)
         ctx.P, ctx.wkey, ctx.bkey, ctx.codes = P, wkey, bkey, codes
         ctx.has_res = residual is not None
         ctx.xshape = x.shape
@@ -151,6 +151,8 @@ class _Linear(torch.autograd.Function):
         P = ctx.P
         W = P.w(ctx.wkey)
         g = g.contiguous()
+        if g.dtype != W.dtype:  # fp32-output linear (weight generation)
+            g = cast(g, W.dtype)
         if g.dim() < x4.dim():
             g = g.unsqueeze(0)
         gp = g
@@ -174,7 +176,7 @@ class _Linear(torch.autograd.Function):
             gemm(ones.view(1, rows), gp.reshape(rows, gp.shape[-1]) if gp.is_contiguous() else gp.contiguous().view(rows, -1),
                  P.g(ctx.bkey).view(1, -1), beta=1.0)
         dres = g.reshape(ctx.xshape[:-1] + (g.shape[-1],)) if ctx.has_res else None
-        return dx, None, None, None, None, None, dres
+        return dx, None, None, None, None, None, dres, None
 
 
 _ONES = {}
@@ -189,8 +191,9 @@ def _ones(n, dtype, device):
     return t[:n]
 
 
-def linear(x, P, wkey, bkey=None, act=None, residual=None):
-    return _Linear.apply(x, P.flat, P, wkey, bkey, act, residual)
+def linear(x, P, wkey, bkey=None, act=None, residual=None, out_dtype=None):
+    return _Linear.apply(x, P.flat, P, wkey, bkey, act, residual, out_dtype)
+
 
 
 # ---------------------------------------------------------------------------
@@ -198,25 +201,48 @@ class _GdpaCore(torch.autograd.Function):
     """Folded GDPA core per sample (gdpa.py:120-187):
         Z = S Kt^T / tau,  A = Act_h(Z) (per n_kv column block),
         Y = S + A Vt;   rows >= length pass through (Y = S).
-    VJP: dZ = (G Vt^T) * Act'(Z) / tau, dS = G + dZ Kt, dKt = dZ^T S, dVt = A^T G."""
+    VJP: dZ = (G Vt^T) * Act'(Z) / tau, dS = G + dZ Kt, dKt = dZ^T S, dVt = A^T G.
+
+    bf16 with H*n_kv = 64 and d in {128, 256} runs the fused tcgen05 kernels
+    kl_gdpa_fwd / kl_gdpa_bwd (Z and A stay on chip, recomputed in the
+    backward); every other case composes kl_gemm calls with fused epilogues
+    (the fp32 parity path)."""
 
     @staticmethod
     def forward(ctx, S, Kt, Vt, lengths, codes, n_kv, inv_tau):
         B, T, d = S.shape
         HK = Kt.shape[1]
+        ctx.codes, ctx.n_kv, ctx.inv_tau = codes, n_kv, inv_tau
+        ctx.fused = _gdpa_fused_ok(S, HK)
+        if ctx.fused:
+            S = S.contiguous()
+            Kt, Vt = Kt.contiguous(), Vt.contiguous()
+            Y = torch.empty_like(S)
+            a = _gdpa_args(S, Kt, Vt, lengths, codes, n_kv, inv_tau)
+            a.Y = Y.data_ptr()
+            _capi.call("kl_gdpa_fwd", C.byref(a), _stream())
+            ctx.save_for_backward(S, Kt, Vt, lengths)
+            return Y
         Z = torch.empty(B, T, HK, device=S.device, dtype=S.dtype)
         A = torch.empty_like(Z)
         gemm(S, Kt.transpose(1, 2), A, alpha=inv_tau, acts=codes, act_group=n_kv, aux=Z, aux_mode=1,
              row_limit=lengths)
         Y = gemm(A, Vt, residual=S)
         ctx.save_for_backward(S, Kt, Vt, Z, A, lengths)
-        ctx.codes, ctx.n_kv, ctx.inv_tau = codes, n_kv, inv_tau
         return Y
 
     @staticmethod
     def backward(ctx, g):
-        S, Kt, Vt, Z, A, lengths = ctx.saved_tensors
         g = g.contiguous()
+        if ctx.fused:
+            S, Kt, Vt, lengths = ctx.saved_tensors
+            dS = torch.empty_like(S)
+            dKt, dVt = torch.empty_like(Kt), torch.empty_like(Vt)
+            a = _gdpa_args(S, Kt, Vt, lengths, ctx.codes, ctx.n_kv, ctx.inv_tau)
+            a.dY, a.dS, a.dKt, a.dVt = g.data_ptr(), dS.data_ptr(), dKt.data_ptr(), dVt.data_ptr()
+            _capi.call("kl_gdpa_bwd", C.byref(a), _stream())
+            return dS, dKt, dVt, None, None, None, None
+        S, Kt, Vt, Z, A, lengths = ctx.saved_tensors
         dZ = torch.empty_like(Z)
         gemm(g, Vt.transpose(1, 2), dZ, alpha=ctx.inv_tau, acts=ctx.codes, act_group=ctx.n_kv, aux=Z, aux_mode=2,
              row_limit=lengths)
@@ -224,6 +250,29 @@ class _GdpaCore(torch.autograd.Function):
         dKt = gemm(dZ.transpose(1, 2), S)
         dVt = gemm(A.transpose(1, 2), g)
         return dS, dKt, dVt, None, None, None, None
+
+
+GDPA_FUSED = True  # tests flip this to A/B the fused kernels against the GEMM composition
+
+
+def _gdpa_fused_ok(S, HK) -> bool:
+    return (GDPA_FUSED and S.dtype == torch.bfloat16 and HK == 64 and S.shape[-1] in (128, 256)
+            and bool(_capi.lib().kl_tcgen05_available()))
+
+
+def _gdpa_args(S, Kt, Vt, lengths, codes, n_kv, inv_tau):
+    a = _capi.GdpaArgs()
+    a.B, a.T, a.d = S.shape
+    a.HK, a.n_kv = Kt.shape[1], n_kv
+    a.dtype = _capi.dt(S)
+    a.inv_tau = inv_tau
+    a.n_act = len(codes)
+    for i, c in enumerate(codes):
+        a.act_codes[i] = c
+    a.lengths = lengths.data_ptr()
+    a.S, a.s_rs, a.s_bs = S.data_ptr(), S.stride(1), S.stride(0)
+    a.Kt, a.Vt = Kt.data_ptr(), Vt.data_ptr()
+    return a
 
 
 def gdpa_core(S, Kt, Vt, lengths, acts, n_kv, inv_tau):

@@ -29,6 +29,14 @@ def rel(a, b):
     return float(np.abs(a - b).max() / den)
 
 
+def relf(a, b):
+    """Frobenius-relative error (the norm-wise rule of oracle/parity.py)."""
+    a = a.detach().double().cpu().numpy() if isinstance(a, torch.Tensor) else np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    den = np.linalg.norm(b)
+    return float(np.linalg.norm(a - b) / den) if den > 0 else float(np.linalg.norm(a))
+
+
 def check_grads(got, ref, dtype):
     """Parameter-gradient parity with the rule of oracle/parity.py."""
     from oracle.parity import grad_errors
@@ -38,6 +46,10 @@ def check_grads(got, ref, dtype):
     for k, e in errs.items():
         assert e < TOL[dtype], (k, e)
     return max(errs.values()) if errs else 0.0
+
+
+def _round(x, dtype):
+    return torch.tensor(np.asarray(x)).to(dtype).double().numpy()
 
 
 def dev(x, dtype=torch.float32, grad=False):
@@ -108,13 +120,13 @@ def test_gemm_batched_reduce_epilogue(dtype):
 # ---------------------------------------------------------------------------
 
 
-def _params_gdpa(dtype, H=4, d=32, n_kv=4, n_sum=2, n_ctx=5, T=20, seed=0):
+def _params_gdpa(dtype, H=4, d=32, n_kv=4, n_sum=2, n_ctx=5, T=20, seed=0, acts=()):
     from paper_2602_10016_b200 import gdpa as G
     from paper_2602_10016_b200.tensor import Params
 
     rng = np.random.default_rng(seed)
     P = Params()
-    cfg = G.GdpaConfig(dim=d, heads=H, n_kv=n_kv, tau=float(T))
+    cfg = G.GdpaConfig(dim=d, heads=H, n_kv=n_kv, tau=float(T), activations=tuple(acts))
     wg = G.WeightGenParams.create(P, "g", cfg, n_sum, d, rng)
     P.add("pool", rng.normal(0, 1 / np.sqrt(n_ctx), (n_sum, n_ctx)))
     P.finalize("cuda", dtype)
@@ -123,18 +135,35 @@ def _params_gdpa(dtype, H=4, d=32, n_kv=4, n_sum=2, n_ctx=5, T=20, seed=0):
 
 
 @pytest.mark.parametrize("dtype", DTYPES)
-def test_gdpa_vs_oracle(dtype):
+@pytest.mark.parametrize("H,d,n_kv,T,acts", [(4, 32, 4, 20, ()), (4, 128, 16, 300, ("silu", "tanh", "identity", "sigmoid")),
+                                             (4, 256, 16, 257, ("tanh", "silu", "sigmoid", "identity")),
+                                             (2, 256, 32, 128, ("silu", "tanh"))])
+def test_gdpa_vs_oracle(dtype, H, d, n_kv, T, acts):
+    """d in {128, 256} with H*n_kv = 64 runs the fused tcgen05 kernels in bf16.
+    bf16 is compared norm-wise: a relu column whose Z sits within bf16
+    rounding of 0 flips Act' between the device and the fp64 oracle, a
+    legitimate single-row jump that an elementwise max-norm magnifies.
+    The large-d cases use kink-free activations: with tau = T the scores are
+    O(1/T), so bf16 rounding of the generated weights flips relu' on enough
+    entries to move the (cancellation-heavy) input gradient dX by ~2%, an
+    ill-posed comparison (relu is covered at d=32 here, device-vs-device
+    at large d by test_gdpa_fused_vs_gemm_composition, and in the model
+    tests).  Emulated in numpy: relu heads 1.6%, smooth heads 0.4% on dX."""
     from paper_2602_10016_b200 import functional as F
     from paper_2602_10016_b200 import gdpa as G
 
-    H, d, n_kv, n_sum, n_ctx, T = 4, 32, 4, 2, 5, 20
-    P, cfg, wg, named = _params_gdpa(dtype, H, d, n_kv, n_sum, n_ctx, T)
+    n_sum, n_ctx = 2, 5
+    P, cfg, wg, named = _params_gdpa(dtype, H, d, n_kv, n_sum, n_ctx, T, acts=acts)
     rng = np.random.default_rng(1)
-    lengths = np.array([20, 7, 0, 1])
+    lengths = np.array([T, 7, 0, 1, max(T - 130, 1)])
     B = len(lengths)
     S = rng.normal(0, 1 / np.sqrt(d), (B, T, d))
     X = rng.normal(0, 1, (B, n_ctx, d))
     R = rng.normal(0, 1, (B, T, d))
+    if dtype == torch.bfloat16:
+        # identical inputs: the oracle sees the bf16 values the device reads
+        # (weights: the fp32 masters, as everywhere)
+        S, X, R = _round(S, dtype), _round(X, dtype), _round(R, dtype)
     S_t, X_t = dev(S, grad=True), dev(X, grad=True)
     xs = G.summarize_nonseq(F.cast(X_t, dtype), F.PRef(P, "pool"))
     y = G.gdpa_forward(F.cast(S_t, dtype), xs, cfg, wg, lengths=lengths)
@@ -147,17 +176,52 @@ def test_gdpa_vs_oracle(dtype):
         xsum, xs_bwd = K.summarize_nonseq(X[b], named["pool"])
         kv, kv_bwd = K.generate_kv(xsum, named, "g", n_kv)
         yo, y_bwd = K.gdpa_forward(S[b, :L], kv, named, "g", float(T), cfg.activations)
-        assert rel(y[b, :L].float(), yo) < tol
+        assert (rel if dtype == torch.float32 else relf)(y[b, :L].float(), yo) < tol
         assert rel(y[b, L:].float(), S[b, L:]) < (1e-7 if dtype == torch.float32 else 1e-2)
         ds, dkvs, gr = y_bwd(R[b, :L])
         dxs, gr2 = kv_bwd(dkvs)
         dx, dpool = xs_bwd(dxs)
         for k, v in list(gr.items()) + list(gr2.items()) + [("pool", dpool)]:
             K._acc(grads, k, v)
-        assert rel(S_t.grad[b, :L], ds) < tol
+        err = rel if dtype == torch.float32 else relf
+        assert err(S_t.grad[b, :L], ds) < tol
         assert rel(S_t.grad[b, L:], R[b, L:]) < (1e-6 if dtype == torch.float32 else 1e-2)
-        assert rel(X_t.grad[b], dx) < tol
+        assert err(X_t.grad[b], dx) < tol
     check_grads(P.grad, grads, dtype)
+
+
+@pytest.mark.parametrize("d,T,acts", [(256, 1024, ("silu", "relu", "identity", "tanh")),
+                                      (128, 333, ("sigmoid", "tanh", "silu", "relu")),
+                                      (256, 100, ("relu", "relu", "relu", "relu"))])
+def test_gdpa_fused_vs_gemm_composition(d, T, acts):
+    """The fused kernels against the kl_gemm composition (Z/A through HBM) on
+    the same bf16 inputs: both round A and dZ to bf16 for the second
+    contraction, so they agree to bf16 output rounding."""
+    from paper_2602_10016_b200 import functional as F
+
+    torch.manual_seed(d + T)
+    B, HK, n_kv = 6, 64, 16
+    S = (torch.randn(B, T, d, device="cuda") / d ** 0.5).bfloat16().requires_grad_()
+    Kt = (torch.randn(B, HK, d, device="cuda") / 2).bfloat16().requires_grad_()
+    Vt = (torch.randn(B, HK, d, device="cuda") / 8).bfloat16().requires_grad_()
+    lengths = torch.tensor([T, T - 1, 0, 1, T // 2, 129], dtype=torch.int32, device="cuda").clamp(max=T)
+    G = torch.randn(B, T, d, device="cuda").bfloat16()
+    outs = []
+    for fused in (True, False):
+        F.GDPA_FUSED = fused
+        try:
+            S.grad = Kt.grad = Vt.grad = None
+            y = F.gdpa_core(S, Kt, Vt, lengths, acts, n_kv, 1.0 / 3.0)
+            y.backward(G)
+            outs.append([y.detach().float(), S.grad.float(), Kt.grad.float(), Vt.grad.float()])
+        finally:
+            F.GDPA_FUSED = True
+    for name, a, b in zip(("Y", "dS", "dKt", "dVt"), outs[0], outs[1]):
+        err = ((a - b).norm() / b.norm().clamp_min(1e-30)).item()
+        assert err < 1e-2, (name, err)
+    # pass-through rows are exact copies
+    assert torch.equal(outs[0][0][2], S.detach()[2].float())
+    assert torch.equal(outs[0][1][2], G[2].float())
 
 
 @pytest.mark.parametrize("dtype", DTYPES)
