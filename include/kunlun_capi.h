@@ -135,6 +135,8 @@ typedef struct kl_gdpa_args {
   void* dS;
   void* dKt;
   void* dVt;
+  /* debug: if non-NULL, 32 x 16 clock64 stamps of CTA 0's pipeline stages */
+  unsigned long long* trace;
 } kl_gdpa_args;
 
 int kl_gdpa_fwd(const kl_gdpa_args* args, void* stream);

@@ -75,6 +75,7 @@ class GdpaArgs(C.Structure):
         ("S", C.c_void_p), ("s_rs", C.c_longlong), ("s_bs", C.c_longlong),
         ("Kt", C.c_void_p), ("Vt", C.c_void_p), ("Y", C.c_void_p),
         ("dY", C.c_void_p), ("dS", C.c_void_p), ("dKt", C.c_void_p), ("dVt", C.c_void_p),
+        ("trace", C.c_void_p),
     ]
 
 

@@ -15,8 +15,9 @@
 //           (HK = 64 columns), then Y = A Vt (N = d <= 256) into TMEM
 //   warps 2-9  epilogue: Z -> Act -> bf16 A tile in smem (operand of the
 //           second MMA), then Y + S (residual read from the S tile in smem)
-//           written back INTO the S slot
-//   warp 10 TMA store of the finished slot to Y, then releases the slot.
+//           written back INTO the S slot, then copied out with coalesced
+//           16-byte stores (one 512 B row per warp instruction) and the
+//           slot released.
 // Z and A never touch HBM: per tile the kernel reads S once and writes Y once
 // (algorithmic traffic 4*d bytes per row).
 //
@@ -26,7 +27,7 @@
 //   epi  dZ, A -> bf16 tiles in smem
 //   MMA  dS = dZ Kt (TMEM [0,d)), dKt^T += S^T dZ, dVt^T += dY^T A
 //        (S^T / dY^T are the same smem tiles read as MN-major operands)
-//   epi  dS + dY -> written into the dY tile, TMA-stored to dS
+//   epi  dS + dY -> written into the dY tile, copied out to dS
 //   end of sample: dKt, dVt (bf16) from TMEM.
 // Traffic per row: read S, dY; write dS (6*d bytes) + 2*HK*d*2 per sample.
 #include <cudaTypedefs.h>
@@ -51,9 +52,13 @@ constexpr uint32_t ATOM_KV = HK * 128;   // 64 rows x 64 bf16
 
 struct P {
   int B, T;
+  bf16* out;               // Y (fwd) or dS (bwd): (B, T, D), rows o_rs apart
+  long long o_rs, o_bs;
   float inv_tau;
   const int* lengths;
   unsigned char code[HK];  // activation code per Z column
+  int uniform16;           // every 16-column group shares one code
+  unsigned long long* trace;  // debug: per-tile clock64 stamps of CTA 0, or NULL
   bf16* dKt;               // (B, HK, D) bf16, backward
   bf16* dVt;
 };
@@ -67,6 +72,11 @@ __device__ __forceinline__ uint64_t dmn(uint32_t base, int kk, uint32_t lbo) {
   return tc::sdesc(base + kk * 2048, lbo, 1024);
 }
 
+#define TR(c, slot)                                                    \
+  do {                                                                 \
+    if (p.trace && blockIdx.x == 0 && (c) < 32) p.trace[(c) * 16 + (slot)] = clock64(); \
+  } while (0)
+
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
 
 // 8 packed bf16 pairs (16 columns) into a K-major SW128 tile of TB rows.
@@ -75,6 +85,104 @@ __device__ __forceinline__ void store_sw16(uint8_t* blk, int r, int c0, const ui
   for (int c = 0; c < 2; ++c) {
     uint4 u = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
     *reinterpret_cast<uint4*>(blk + tc::sw128_off(r, c0 + 8 * c, TB)) = u;
+  }
+}
+
+// Activation over a run of N columns sharing one code (the per-head column
+// block): y = Act(z*s) and, for the VJP, dy = g * Act'(z*s) * s.  Hardware
+// approximations (ex2/rcp/tanh.approx, rel. err <= 2^-11) — A and dZ are
+// rounded to bf16 (2^-9) right after.  Codes as tensor.py:431-440.
+__device__ __forceinline__ float tanh_fast(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcp_fast(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float sigm_fast(float x) { return rcp_fast(1.f + __expf(-x)); }
+
+template <int N, bool BWD>
+__device__ __forceinline__ void act_run(int code, const float* z, const float* g, float s, float* y, float* dy) {
+  switch (code) {
+    case KL_ACT_RELU:
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const float x = z[i] * s;
+        y[i] = fmaxf(x, 0.f);
+        if (BWD) dy[i] = x > 0.f ? g[i] * s : 0.f;
+      }
+      break;
+    case KL_ACT_SILU:
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const float x = z[i] * s, sg = sigm_fast(x);
+        y[i] = x * sg;
+        if (BWD) dy[i] = g[i] * s * sg * (1.f + x * (1.f - sg));
+      }
+      break;
+    case KL_ACT_TANH:
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const float t = tanh_fast(z[i] * s);
+        y[i] = t;
+        if (BWD) dy[i] = g[i] * s * (1.f - t * t);
+      }
+      break;
+    case KL_ACT_SIGMOID:
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const float sg = sigm_fast(z[i] * s);
+        y[i] = sg;
+        if (BWD) dy[i] = g[i] * s * sg * (1.f - sg);
+      }
+      break;
+    case KL_ACT_EXP:
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const float e = __expf(z[i] * s);
+        y[i] = e;
+        if (BWD) dy[i] = g[i] * s * e;
+      }
+      break;
+    case KL_ACT_SQRT:
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const float q = sqrtf(z[i] * s);
+        y[i] = q;
+        if (BWD) dy[i] = g[i] * s * 0.5f / q;
+      }
+      break;
+    case KL_ACT_LOG:
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const float x = z[i] * s;
+        y[i] = __logf(x);
+        if (BWD) dy[i] = g[i] * s / x;
+      }
+      break;
+    default:
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        y[i] = z[i] * s;
+        if (BWD) dy[i] = g[i] * s;
+      }
+  }
+}
+
+// This thread's 32 Z columns [c0, c0+32): per-head runs of 16 when every
+// 16-column group has one code (n_kv % 16 == 0), else per column.
+template <bool BWD>
+__device__ __forceinline__ void act_cols32(const unsigned char* code, int c0, bool uniform16, const float* z,
+                                           const float* g, float s, float* y, float* dy) {
+  if (uniform16) {
+    act_run<16, BWD>(code[c0], z, g, s, y, dy);
+    act_run<16, BWD>(code[c0 + 16], z + 16, g + 16, s, y + 16, dy + 16);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) act_run<1, BWD>(code[c0 + i], z + i, g + i, s, y + i, dy + i);
   }
 }
 
@@ -92,6 +200,20 @@ __device__ __forceinline__ void add_residual32(uint8_t* tile, int r, int c0, con
       w[i] = tc::pack_bf16(acc[8 * c + 2 * i] + f.x, acc[8 * c + 2 * i + 1] + f.y);
     }
     *ptr = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+// The 8 epilogue warps (256 threads, named barrier 1) copy a finished
+// swizzled 128 x D tile to global rows q0.. (< T): one warp writes 512
+// contiguous bytes per instruction.
+template <int D>
+__device__ __forceinline__ void copy_out(const uint8_t* tile, bf16* out, long long rs, int q0, int T, int tid) {
+  constexpr int CPR = D / 8;  // 16-byte chunks per row
+#pragma unroll 4
+  for (int q = tid; q < TB * CPR; q += 256) {
+    const int row = q / CPR, col = (q % CPR) * 8;
+    const uint4 v = *reinterpret_cast<const uint4*>(tile + tc::sw128_off(row, col, TB));
+    if (q0 + row < T) *reinterpret_cast<uint4*>(out + (long long)(q0 + row) * rs + col) = v;
   }
 }
 
@@ -142,6 +264,8 @@ __global__ void __launch_bounds__(NT, 1)
   const int i0 = (int)((long long)W * blockIdx.x / gridDim.x);
   const int i1 = (int)((long long)W * (blockIdx.x + 1) / gridDim.x);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __shared__ unsigned char code[HK];
+  if (threadIdx.x < HK) code[threadIdx.x] = p.code[threadIdx.x];
 
   if (warp == 0 && lane == 0) {
     tc::prefetch_tmap(&ts);
@@ -187,6 +311,7 @@ __global__ void __launch_bounds__(NT, 1)
         }
         const int sl = c & 1;
         tc::mbar_wait(&s_empty[sl], ((c >> 1) & 1) ^ 1);
+        TR(c, 0);
         tc::mbar_arrive_expect_tx(&s_full[sl], SLOT);
 #pragma unroll
         for (int a = 0; a < NA; ++a) tc::tma_load_3d(sS + sl * SLOT + a * ATOM_S, &ts, &s_full[sl], a * 64, q0, b);
@@ -202,6 +327,7 @@ __global__ void __launch_bounds__(NT, 1)
           ++ns;
         }
         tc::mbar_wait(&s_full[sl], (c >> 1) & 1);
+        TR(c, 1);
         tc::mbar_wait(&z_empty[sl], ((c >> 1) & 1) ^ 1);
         tc::fence_after();
         const uint32_t sa = tc::smem_u32(sS + sl * SLOT), ka = tc::smem_u32(sK);
@@ -210,19 +336,13 @@ __global__ void __launch_bounds__(NT, 1)
           tc::mma_bf16(tmem + sl * HK, dk(sa, kk, ATOM_S), dk(ka, kk, ATOM_KV), IDESC_Z, kk > 0);
         tc::mma_commit(&z_full[sl]);
       };
-      int issued = 0;  // number of items whose first MMA is issued
+      if (i0 < i1) mma1(i0, 0);
       for (int k = i0, c = 0; k < i1; ++k, ++c) {
-        if (issued == c) {
-          mma1(k, c);
-          ++issued;
-        }
         const bool last_of_sample = (k + 1 == i1) || ((k + 1) % nT == 0);
-        if (!last_of_sample) {  // run the next tile's Z while this tile's A is formed
-          mma1(k + 1, c + 1);
-          ++issued;
-        }
         tc::mbar_wait(a_full, c & 1);
+        TR(c, 2);
         tc::mbar_wait(y_empty, (c & 1) ^ 1);
+        TR(c, 3);
         tc::fence_after();
         const uint32_t aa = tc::smem_u32(sA), va = tc::smem_u32(sV);
 #pragma unroll
@@ -230,6 +350,8 @@ __global__ void __launch_bounds__(NT, 1)
         tc::mma_commit(y_full);
         tc::mma_commit(a_empty);
         if (last_of_sample) tc::mma_commit(kv_empty);
+        // the next tile's Z runs while this tile's Y epilogue drains
+        if (k + 1 < i1) mma1(k + 1, c + 1);
       }
     }
   } else if (warp < 10) {
@@ -238,25 +360,30 @@ __global__ void __launch_bounds__(NT, 1)
     const uint32_t trow = tmem + ((uint32_t)(qtr * 32) << 16);
     for (int k = i0, c = 0; k < i1; ++k, ++c) {
       const int b = k / nT, q0 = (k % nT) * TB;
-      const bool live = q0 + r < __ldg(&p.lengths[b]);
+      int len = __ldg(&p.lengths[b]);
+      asm volatile("" : "+r"(len));  // materialise before the barrier wait
+      const bool live = q0 + r < len;
       const int sl = c & 1;
       // ---- A = Act(Z) (this half's 32 columns) -> sA
       tc::mbar_wait(&z_full[sl], (c >> 1) & 1);
+      if (warp == 2 && lane == 0) TR(c, 4);
       tc::fence_after();
       float v[32];
       tc::tmem_ld32(trow + sl * HK + hf * 32, v);
+      if (warp == 2 && lane == 0) TR(c, 9);
       tc::fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&z_empty[sl]);
       uint32_t pk[16];
+      {
+        float y[32];
+        act_cols32<false>(code, hf * 32, p.uniform16, v, nullptr, p.inv_tau, y, nullptr);
 #pragma unroll
-      for (int i = 0; i < 32; i += 2) {
-        const int j = hf * 32 + i;
-        const float a0 = live ? act_apply(p.code[j], v[i] * p.inv_tau) : 0.f;
-        const float a1 = live ? act_apply(p.code[j + 1], v[i + 1] * p.inv_tau) : 0.f;
-        pk[i >> 1] = tc::pack_bf16(a0, a1);
+        for (int i = 0; i < 32; i += 2) pk[i >> 1] = live ? tc::pack_bf16(y[i], y[i + 1]) : 0u;
       }
+      if (warp == 2 && lane == 0) TR(c, 10);
       tc::mbar_wait(a_empty, (c & 1) ^ 1);
+      if (warp == 2 && lane == 0) TR(c, 5);
       store_sw16(sA, r, hf * 32, pk);
       store_sw16(sA, r, hf * 32 + 16, pk + 8);
       tc::fence_async_smem();
@@ -264,13 +391,20 @@ __global__ void __launch_bounds__(NT, 1)
       if (lane == 0) tc::mbar_arrive(a_full);
       // ---- Y = acc + S, in place in the S slot
       tc::mbar_wait(y_full, c & 1);
+      if (warp == 2 && lane == 0) TR(c, 6);
       tc::fence_after();
       uint8_t* tile = sS + sl * SLOT;
 #pragma unroll 1
-      for (int cc = hf * (D / 2); cc < (hf + 1) * (D / 2); cc += 32) {
-        tc::tmem_ld32(trow + T_Y + cc, v);
-        add_residual32(tile, r, cc, v);
+      for (int cc = hf * (D / 2); cc < (hf + 1) * (D / 2); cc += 64) {
+        uint32_t u[64];
+        tc::tmem_ld32_nowait(trow + T_Y + cc, u);
+        tc::tmem_ld32_nowait(trow + T_Y + cc + 32, u + 32);
+        tc::tmem_wait_ld();
+        tc::reg_fence<64>(u);
+        add_residual32(tile, r, cc, reinterpret_cast<const float*>(u));
+        add_residual32(tile, r, cc + 32, reinterpret_cast<const float*>(u + 32));
       }
+      if (warp == 2 && lane == 0) TR(c, 7);
       tc::fence_before();
       tc::fence_async_smem();
       __syncwarp();
@@ -279,20 +413,18 @@ __global__ void __launch_bounds__(NT, 1)
         tc::mbar_arrive(&st_full[sl]);
       }
     }
-  } else {
-    if (lane == 0) {
-      for (int k = i0, c = 0; k < i1; ++k, ++c) {
-        const int b = k / nT, q0 = (k % nT) * TB;
-        const int sl = c & 1;
-        tc::mbar_wait(&st_full[sl], (c >> 1) & 1);
+  } else if (lane == 0) {  // warp 10: TMA store of finished slots
+    for (int k = i0, c = 0; k < i1; ++k, ++c) {
+      const int b = k / nT, q0 = (k % nT) * TB, sl = c & 1;
+      tc::mbar_wait(&st_full[sl], (c >> 1) & 1);
 #pragma unroll
-        for (int a = 0; a < NA; ++a) tc::tma_store_3d(&ty, sS + sl * SLOT + a * ATOM_S, a * 64, q0, b);
-        tc::bulk_commit();
-        tc::bulk_wait_read0();
-        tc::mbar_arrive(&s_empty[sl]);
-      }
-      tc::bulk_wait0();
+      for (int a = 0; a < NA; ++a) tc::tma_store_3d(&ty, sS + sl * SLOT + a * ATOM_S, a * 64, q0, b);
+      tc::bulk_commit();
+      tc::bulk_wait_read0();
+      TR(c, 8);
+      tc::mbar_arrive(&s_empty[sl]);
     }
+    tc::bulk_wait0();
   }
   tc::fence_before();
   __syncthreads();
@@ -326,30 +458,32 @@ __global__ void __launch_bounds__(NT, 1)
   uint64_t* zz_full = bar + 4;
   uint64_t* dz_full = bar + 5;
   uint64_t* ds_full = bar + 6;
-  uint64_t* st_full = bar + 7;
-  uint64_t* acc_full = bar + 8;
-  uint64_t* acc_empty = bar + 9;
+  uint64_t* acc_full = bar + 7;
+  uint64_t* acc_empty = bar + 8;
+  uint64_t* st_full = bar + 9;
   uint32_t* tslot = (uint32_t*)(bar + 10);
 
   const int nT = (p.T + TB - 1) / TB;
   const int b0 = (int)((long long)p.B * blockIdx.x / gridDim.x);
   const int b1 = (int)((long long)p.B * (blockIdx.x + 1) / gridDim.x);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __shared__ unsigned char code[HK];
+  if (threadIdx.x < HK) code[threadIdx.x] = p.code[threadIdx.x];
 
   if (warp == 0 && lane == 0) {
     tc::prefetch_tmap(&ts);
     tc::prefetch_tmap(&tg);
     tc::prefetch_tmap(&tk);
     tc::prefetch_tmap(&tv);
-    tc::prefetch_tmap(&tds);
     tc::mbar_init(sg_full, 1);
+    tc::prefetch_tmap(&tds);
     tc::mbar_init(sg_empty, 1);
+    tc::mbar_init(st_full, 8);
     tc::mbar_init(kv_full, 1);
     tc::mbar_init(kv_empty, 1);
     tc::mbar_init(zz_full, 1);
     tc::mbar_init(dz_full, 8);
     tc::mbar_init(ds_full, 1);
-    tc::mbar_init(st_full, 8);
     tc::mbar_init(acc_full, 1);
     tc::mbar_init(acc_empty, 8);
     tc::fence_barrier_init();
@@ -373,6 +507,7 @@ __global__ void __launch_bounds__(NT, 1)
         }
         for (int t = 0; t < nT; ++t, ++c) {
           tc::mbar_wait(sg_empty, (c & 1) ^ 1);
+          TR(c, 0);
           tc::mbar_arrive_expect_tx(sg_full, 2 * SLOT);
 #pragma unroll
           for (int a = 0; a < NA; ++a) {
@@ -391,6 +526,7 @@ __global__ void __launch_bounds__(NT, 1)
         tc::mbar_wait(kv_full, ns & 1);
         for (int t = 0; t < nT; ++t, ++c) {
           tc::mbar_wait(sg_full, c & 1);
+          TR(c, 1);
           tc::fence_after();
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk) {
@@ -399,6 +535,7 @@ __global__ void __launch_bounds__(NT, 1)
           }
           tc::mma_commit(zz_full);
           tc::mbar_wait(dz_full, c & 1);
+          TR(c, 2);
           if (t == 0) tc::mbar_wait(acc_empty, (ns & 1) ^ 1);
           tc::fence_after();
 #pragma unroll
@@ -415,6 +552,7 @@ __global__ void __launch_bounds__(NT, 1)
             }
           }
           tc::mma_commit(ds_full);
+          TR(c, 3);
         }
         tc::mma_commit(acc_full);
         tc::mma_commit(kv_empty);
@@ -431,24 +569,23 @@ __global__ void __launch_bounds__(NT, 1)
         const bool live = t * TB + r < len;
         // ---- dZ = dA * Act'(Z) * inv_tau, A = Act(Z) -> smem operand tiles
         tc::mbar_wait(zz_full, c & 1);
+        if (warp == 2 && lane == 0) TR(c, 4);
         tc::fence_after();
         float da[32], z[32];
-        tc::tmem_ld32(trow + hf * 32, da);
-        tc::tmem_ld32(trow + HK + hf * 32, z);
+        tc::tmem_ld32_nowait(trow + hf * 32, reinterpret_cast<uint32_t*>(da));
+        tc::tmem_ld32_nowait(trow + HK + hf * 32, reinterpret_cast<uint32_t*>(z));
+        tc::tmem_wait_ld();
+        tc::reg_fence<32>(reinterpret_cast<uint32_t*>(da));
+        tc::reg_fence<32>(reinterpret_cast<uint32_t*>(z));
         uint32_t pdz[16], pa[16];
+        {
+          float y[32], dy[32];
+          act_cols32<true>(code, hf * 32, p.uniform16, z, da, p.inv_tau, y, dy);
 #pragma unroll
-        for (int i = 0; i < 32; i += 2) {
-          float d0 = 0.f, d1 = 0.f, a0 = 0.f, a1 = 0.f;
-          if (live) {
-            const int j = hf * 32 + i;
-            const float z0 = z[i] * p.inv_tau, z1 = z[i + 1] * p.inv_tau;
-            a0 = act_apply(p.code[j], z0);
-            a1 = act_apply(p.code[j + 1], z1);
-            d0 = da[i] * act_deriv(p.code[j], z0) * p.inv_tau;
-            d1 = da[i + 1] * act_deriv(p.code[j + 1], z1) * p.inv_tau;
+          for (int i = 0; i < 32; i += 2) {
+            pdz[i >> 1] = live ? tc::pack_bf16(dy[i], dy[i + 1]) : 0u;
+            pa[i >> 1] = live ? tc::pack_bf16(y[i], y[i + 1]) : 0u;
           }
-          pdz[i >> 1] = tc::pack_bf16(d0, d1);
-          pa[i >> 1] = tc::pack_bf16(a0, a1);
         }
         store_sw16(sDZ, r, hf * 32, pdz);
         store_sw16(sDZ, r, hf * 32 + 16, pdz + 8);
@@ -460,12 +597,19 @@ __global__ void __launch_bounds__(NT, 1)
         if (lane == 0) tc::mbar_arrive(dz_full);
         // ---- dS = acc + dY, in place in the dY tile
         tc::mbar_wait(ds_full, c & 1);
+        if (warp == 2 && lane == 0) TR(c, 6);
         tc::fence_after();
 #pragma unroll 1
-        for (int cc = hf * (D / 2); cc < (hf + 1) * (D / 2); cc += 32) {
-          tc::tmem_ld32(trow + cc, da);
-          add_residual32(sG, r, cc, da);
+        for (int cc = hf * (D / 2); cc < (hf + 1) * (D / 2); cc += 64) {
+          uint32_t u[64];
+          tc::tmem_ld32_nowait(trow + cc, u);
+          tc::tmem_ld32_nowait(trow + cc + 32, u + 32);
+          tc::tmem_wait_ld();
+          tc::reg_fence<64>(u);
+          add_residual32(sG, r, cc, reinterpret_cast<const float*>(u));
+          add_residual32(sG, r, cc + 32, reinterpret_cast<const float*>(u + 32));
         }
+        if (warp == 2 && lane == 0) TR(c, 7);
         tc::fence_before();
         tc::fence_async_smem();
         __syncwarp();
@@ -493,21 +637,20 @@ __global__ void __launch_bounds__(NT, 1)
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(acc_empty);
     }
-  } else {
-    if (lane == 0) {
-      int c = 0;
-      for (int b = b0; b < b1; ++b) {
-        for (int t = 0; t < nT; ++t, ++c) {
-          tc::mbar_wait(st_full, c & 1);
+  } else if (lane == 0) {  // warp 10: TMA store of dS tiles
+    int c = 0;
+    for (int b = b0; b < b1; ++b) {
+      for (int t = 0; t < nT; ++t, ++c) {
+        tc::mbar_wait(st_full, c & 1);
 #pragma unroll
-          for (int a = 0; a < NA; ++a) tc::tma_store_3d(&tds, sG + a * ATOM_S, a * 64, t * TB, b);
-          tc::bulk_commit();
-          tc::bulk_wait_read0();
-          tc::mbar_arrive(sg_empty);
-        }
+        for (int a = 0; a < NA; ++a) tc::tma_store_3d(&tds, sG + a * ATOM_S, a * 64, t * TB, b);
+        tc::bulk_commit();
+        tc::bulk_wait_read0();
+        TR(c, 8);
+        tc::mbar_arrive(sg_empty);
       }
-      tc::bulk_wait0();
     }
+    tc::bulk_wait0();
   }
   tc::fence_before();
   __syncthreads();
@@ -565,6 +708,12 @@ static int gdpa_prepare(const kl_gdpa_args* a, const char* who, gdpa::P& p) {
     const int h = j / a->n_kv;
     p.code[j] = (unsigned char)(a->n_act ? a->act_codes[h % a->n_act] : KL_ACT_IDENTITY);
   }
+  p.uniform16 = 1;
+  for (int j = 0; j < gdpa::HK; ++j)
+    if (p.code[j] != p.code[j & ~15]) p.uniform16 = 0;
+  p.o_rs = a->s_rs;
+  p.o_bs = a->s_bs;
+  p.trace = (unsigned long long*)a->trace;
   p.dKt = (bf16*)a->dKt;
   p.dVt = (bf16*)a->dVt;
   return KL_OK;
@@ -585,7 +734,9 @@ static int gdpa_fwd_launch(const kl_gdpa_args* a, const gdpa::P& p, cudaStream_t
   cudaFuncSetAttribute(gdpa::gdpa_fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int W = a->B * ((a->T + gdpa::TB - 1) / gdpa::TB);
   const int grid = std::min(W, tc_num_sms());
-  gdpa::gdpa_fwd_kernel<D><<<grid, gdpa::NT, smem, s>>>(ts, tk, tv, ty, p);
+  gdpa::P q = p;
+  q.out = (bf16*)a->Y;
+  gdpa::gdpa_fwd_kernel<D><<<grid, gdpa::NT, smem, s>>>(ts, tk, tv, ty, q);
   count_launch();
   return launch_check("gdpa_fwd_tc");
 }
@@ -605,7 +756,9 @@ static int gdpa_bwd_launch(const kl_gdpa_args* a, const gdpa::P& p, cudaStream_t
   const size_t smem = gdpa::bwd_smem<D>();
   cudaFuncSetAttribute(gdpa::gdpa_bwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int grid = std::min(a->B, tc_num_sms());
-  gdpa::gdpa_bwd_kernel<D><<<grid, gdpa::NT, smem, s>>>(ts, tg, tk, tv, tds, p);
+  gdpa::P q = p;
+  q.out = (bf16*)a->dS;
+  gdpa::gdpa_bwd_kernel<D><<<grid, gdpa::NT, smem, s>>>(ts, tg, tk, tv, tds, q);
   count_launch();
   return launch_check("gdpa_bwd_tc");
 }
