@@ -271,9 +271,12 @@ def gemm(A: torch.Tensor, B: torch.Tensor, out: torch.Tensor | None = None, *, o
     _check(lib().kl_gemm(C.byref(a), _stream()), "kl_gemm")
     if GEMM_LOG is not None:
         e.record()
+        import traceback
+
+        site = [f"{os.path.basename(f.filename)}:{f.lineno}:{f.name}" for f in traceback.extract_stack(limit=4)[:-1]]
         GEMM_LOG.append(((M, N, K, nb1, nb2, int(red1), int(red2), (a.a_rs, a.a_cs), (a.b_rs, a.b_cs),
                           (a.c_rs, a.c_cs), a.c_dtype, a.aux_mode, int(bool(residual is not None)), len(acts or ()),
-                          lib().kl_last_gemm_path()), s, e))
+                          lib().kl_last_gemm_path(), "<".join(reversed(site))), s, e))
     return ret
 
 

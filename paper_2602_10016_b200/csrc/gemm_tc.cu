@@ -11,6 +11,8 @@
 // batch dim may be reduced (its tiles accumulate into one TMEM tile).
 #include <cudaTypedefs.h>
 
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "gemm.h"
@@ -47,6 +49,8 @@ struct TcParams {
   int r_boxes;  // >0: residual tile staged by TMA in r_boxes 64-column boxes
   int r_has1, r_has2;
   float* ws;    // split-K partials [split][out batch][M][N] (fp32) or NULL (atomics)
+  int c_has1, c_has2;  // MODE 2: C tensor-map batch dims present
+  int reduce_c;        // MODE 2: TMA reduce-add into C (fp32 accumulate / split-K)
 };
 
 constexpr int SLD = 66;  // epilogue staging row stride (floats): 64 columns + pad, 8-byte aligned
@@ -272,16 +276,170 @@ __device__ __forceinline__ void epi_generic(const TcParams& p, const Epi& e, con
   }
 }
 
-template <typename TC, bool PLAIN>
+// MODE 2 epilogue: thread = output row.  Each 32-column TMEM slab gets the
+// epilogue in registers (alpha, bias, activation, row limit, residual from the
+// TMA-staged SWIZZLE_128B tile) and is written as swizzled 16-byte chunks into
+// one of the warp's two 32-row x 128-byte staging boxes, which a single TMA
+// store (or fp32 reduce-add, for accumulate-into-C and split-K) writes out.
+// Activation of a 32-column slab sharing one code (MODE 3; bf16-operand
+// GEMMs, hardware approximations: ex2/rcp/tanh.approx, rel. err <= 2^-11).
+__device__ __forceinline__ float tanh_apx(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcp_apx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ void act32(int code, float* v) {
+  switch (code) {
+    case KL_ACT_RELU:
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
+      break;
+    case KL_ACT_SILU:
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = v[i] * rcp_apx(1.f + __expf(-v[i]));
+      break;
+    case KL_ACT_TANH:
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = tanh_apx(v[i]);
+      break;
+    case KL_ACT_SIGMOID:
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = rcp_apx(1.f + __expf(-v[i]));
+      break;
+    case KL_ACT_EXP:
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = __expf(v[i]);
+      break;
+    case KL_ACT_SQRT:
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = sqrtf(v[i]);
+      break;
+    case KL_ACT_LOG:
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = __logf(v[i]);
+      break;
+    default:
+      break;
+  }
+}
+
+template <typename TC, bool FULL>
+__device__ __forceinline__ void epi_tma(const TcParams& p, const Epi& e, const CUtensorMap* tmC, uint32_t tbase,
+                                        uint8_t* stg, float* bsm, int mb, int nb, int zc2, int zc1, int lane_base,
+                                        int lim, const uint8_t* Rs, int& nbox) {
+  const int lane = threadIdx.x & 31;
+  constexpr int SPB = 128 / (int)sizeof(TC) / 32;  // 32-column slabs per 128-byte box row: 2 bf16, 1 fp32
+  const int row = lane_base + lane;
+  const bool live = mb * BM + row < lim;
+  if (FULL && e.bias) {  // this tile's bias -> the warp's smem row (read back as broadcasts)
+    for (int c = lane; c < p.BN; c += 32) {
+      const int n = nb * p.BN + c;
+      bsm[c] = n < p.N ? __ldg(&e.bias[n]) : 0.f;
+    }
+    __syncwarp();
+  }
+  uint8_t* buf = stg;
+#pragma unroll 1
+  for (int c = 0; c < p.BN; c += 32) {
+    const int hb = (c >> 5) % SPB;
+    if (hb == 0) {
+      buf = stg + (nbox & 1) * 4096;
+      if (lane == 0) tc::bulk_wait_read1();
+      __syncwarp();
+    }
+    float v[32];
+    tc::tmem_ld32(tbase + c, v);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] *= e.alpha;
+    if (FULL) {
+      if (e.bias) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float4 b4 = *reinterpret_cast<const float4*>(bsm + c + 4 * q);
+          v[4 * q] += b4.x;
+          v[4 * q + 1] += b4.y;
+          v[4 * q + 2] += b4.z;
+          v[4 * q + 3] += b4.w;
+        }
+      }
+      if (e.n_act) act32(epi_code(e, nb * p.BN + c), v);  // slab-uniform (host-checked)
+    }
+    if (Rs) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int cc = c + 8 * q;
+        const uint4 u = *reinterpret_cast<const uint4*>(Rs + (cc >> 6) * 16384 + tc::sw128_off(row, cc & 63, BM));
+        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[k]));
+          v[8 * q + 2 * k] += f.x;
+          v[8 * q + 2 * k + 1] += f.y;
+        }
+      }
+    }
+    if (!live) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = 0.f;
+    }
+    uint8_t* rowp = buf + lane * 128;
+    if constexpr (sizeof(TC) == 2) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int chunk = hb * 4 + q;
+        uint4 u;
+        u.x = tc::pack_bf16(v[8 * q], v[8 * q + 1]);
+        u.y = tc::pack_bf16(v[8 * q + 2], v[8 * q + 3]);
+        u.z = tc::pack_bf16(v[8 * q + 4], v[8 * q + 5]);
+        u.w = tc::pack_bf16(v[8 * q + 6], v[8 * q + 7]);
+        *reinterpret_cast<uint4*>(rowp + ((chunk ^ (lane & 7)) << 4)) = u;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint4 u = make_uint4(__float_as_uint(v[4 * q]), __float_as_uint(v[4 * q + 1]),
+                                   __float_as_uint(v[4 * q + 2]), __float_as_uint(v[4 * q + 3]));
+        *reinterpret_cast<uint4*>(rowp + ((q ^ (lane & 7)) << 4)) = u;
+      }
+    }
+    if (hb == SPB - 1 || c + 32 >= p.BN) {
+      tc::fence_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        const int gc = nb * p.BN + c - 32 * hb, gr = mb * BM + lane_base;
+        if (p.reduce_c)
+          tc::tma_reduce_add_4d(tmC, buf, gc, gr, zc2, zc1);
+        else
+          tc::tma_store_4d(tmC, buf, gc, gr, zc2, zc1);
+        tc::bulk_commit();
+      }
+      ++nbox;
+    }
+  }
+  if (FULL && e.bias) __syncwarp();  // bsm reused by the next tile
+}
+
+// MODE 0: plain store, 1: generic epilogue (lane = column pair), 2/3: TMA-store
+// epilogue (thread = row; see epi_tma) without / with bias and activations.
+template <typename TC, int MODE>
 __global__ void __launch_bounds__(NTHREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const __grid_constant__ CUtensorMap tmR, TcParams p, Epi e) {
+                   const __grid_constant__ CUtensorMap tmR, const __grid_constant__ CUtensorMap tmC, TcParams p,
+                   Epi e) {
+  constexpr bool PLAIN = MODE == 0;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sA = smem;
   uint8_t* sB = sA + p.stages * p.a_stage_bytes;
   uint8_t* sR = sB + p.stages * p.b_stage_bytes;  // 2 x r_boxes x 16 KB residual tiles (TMA)
-  __shared__ __align__(16) float stage_s[4 * 32 * SLD];  // epilogue transpose, one 32 x 64 slab per warp
+  // epilogue staging: MODE 0/1 transpose (one 32 x 64 fp32 slab per warp);
+  // MODE 2 two 4 KB swizzled TMA boxes per warp
+  __shared__ __align__(1024) float stage_s[4 * 32 * SLD];
   uint64_t* full = (uint64_t*)(sR + (p.r_boxes ? 2 * p.r_boxes * 16384 : 0));
   uint64_t* empty = full + p.stages;
   uint64_t* tfull = empty + p.stages;
@@ -295,6 +453,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     tc::prefetch_tmap(&tmA);
     tc::prefetch_tmap(&tmB);
     if (p.r_boxes) tc::prefetch_tmap(&tmR);
+    if (MODE >= 2) tc::prefetch_tmap(&tmC);
     for (int s = 0; s < p.stages; ++s) {
       tc::mbar_init(&full[s], 1);
       tc::mbar_init(&empty[s], 1);
@@ -408,7 +567,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
   } else {
     const int lane_base = (warp & 3) * 32;
-    int t = 0;
+    int t = 0, nbox = 0;
     for (int unit = blockIdx.x; unit < total; unit += gridDim.x, ++t) {
       const int tile = unit / p.splits;
       const int acc = t & 1;
@@ -429,6 +588,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       tc::fence_after();
       const uint32_t tbase = tmem + acc * p.acc_stride + ((uint32_t)lane_base << 16);
       const int rows = min(32, p.M - m0);
+      if constexpr (MODE >= 2) {
+        const uint8_t* Rs = nullptr;
+        if (p.r_boxes) {
+          tc::mbar_wait(&rfull[t & 1], (t >> 1) & 1);
+          Rs = sR + (t & 1) * p.r_boxes * 16384;
+        }
+        epi_tma<TC, MODE == 3>(p, e, &tmC, tbase, reinterpret_cast<uint8_t*>(stage_s) + (warp - 2) * 8192,
+                               reinterpret_cast<float*>(rempty + 2 + 2) + (warp - 2) * 256, mb, nb,
+                    p.c_has2 ? z2o : 0, p.c_has1 ? z1o : 0, lane_base, lim, Rs, nbox);
+      } else
       for (int c0 = 0; c0 < p.BN; c0 += 64) {
         // TMEM (thread = row) -> smem transpose -> each lane owns a column
         // pair and walks the warp's 32 rows: every global access of a warp is
@@ -486,6 +655,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if (p.r_boxes) tc::mbar_arrive(&rempty[t & 1]);
       }
     }
+    if (MODE >= 2 && lane == 0) tc::bulk_wait0();
   }
   __syncthreads();
   if (warp == 1) tc::tmem_dealloc(tmem, p.tmem_cols);
@@ -533,16 +703,16 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // dim with stride 0 (broadcast) becomes extent 1.
 bool make_map(CUtensorMap* m, const void* ptr, long long inner, long long outer, long long s_outer, int nb2,
               long long s2, int nb1, long long s1, uint32_t box_inner, uint32_t box_outer, int* has2, int* has1,
-              bool swizzle = true) {
+              bool swizzle = true, int esz = 2) {
   auto fn = encode_fn();
   if (!fn) return false;
   *has2 = (s2 != 0 && nb2 > 1);
   *has1 = (s1 != 0 && nb1 > 1);
   cuuint64_t dims[4] = {(cuuint64_t)inner, (cuuint64_t)outer, (cuuint64_t)(*has2 ? nb2 : 1),
                         (cuuint64_t)(*has1 ? nb1 : 1)};
-  long long so = s_outer * 2;
-  long long b2 = *has2 ? s2 * 2 : std::max<long long>(so * outer, 16);
-  long long b1 = *has1 ? s1 * 2 : std::max<long long>(b2 * (long long)dims[2], 16);
+  long long so = s_outer * esz;
+  long long b2 = *has2 ? s2 * esz : std::max<long long>(so * outer, 16);
+  long long b1 = *has1 ? s1 * esz : std::max<long long>(b2 * (long long)dims[2], 16);
   auto bad = [](long long s) { return s <= 0 || (s % 16) != 0 || s >= (1ll << 40); };
   if (bad(so) || bad(b2) || bad(b1)) return false;
   b2 = (b2 + 15) / 16 * 16;
@@ -550,7 +720,8 @@ bool make_map(CUtensorMap* m, const void* ptr, long long inner, long long outer,
   cuuint64_t strides[3] = {(cuuint64_t)so, (cuuint64_t)b2, (cuuint64_t)b1};
   cuuint32_t box[4] = {box_inner, box_outer, 1, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), dims, strides, box, estr,
+  CUresult r = fn(m, esz == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4,
+                  const_cast<void*>(ptr), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -571,6 +742,13 @@ int num_sms() {
 }  // namespace
 
 int gemm_path();
+
+// KL_GEMM_EPI1=1 forces the MODE 0/1 epilogues (A/B testing).
+static bool getenv_flag_epi1() {
+  static int v = -1;
+  if (v < 0) v = getenv("KL_GEMM_EPI1") ? 1 : 0;
+  return v == 1;
+}
 
 int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
   if (g0.ab_dtype != KL_BF16) return KL_EUNSUPPORTED;
@@ -622,12 +800,33 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
   p.a_stage_bytes = BM * BK * 2;
   p.b_stage_bytes = b_n ? p.b_boxes * 64 * BK * 2 : bn * BK * 2;
   const uint32_t stage = p.a_stage_bytes + p.b_stage_bytes;
+  // MODE 2 (TMA-store epilogue): contiguous, 16-byte aligned C rows, no aux
+  // output, N tiles in 32-column slabs; fp32 C only plain (beta 0) or
+  // accumulate-only (beta 1 -> TMA reduce-add).
+  const int esz_c = g.c_dtype == KL_BF16 ? 2 : 4;
+  const bool accum_only0 = g.c_dtype == KL_F32 && e.beta == 1.f && !e.bias && !e.row_limit && !e.aux_mode &&
+                           e.n_act == 0 && !g.R;
+  bool mode2 = !getenv_flag_epi1() && g.c_cs == 1 && ((uintptr_t)g.C & 15) == 0 && (g.c_rs * esz_c) % 16 == 0 &&
+               (g.c_s1 * esz_c) % 16 == 0 && (g.c_s2 * esz_c) % 16 == 0 && !e.aux_mode && bn % 32 == 0 &&
+               (g.c_dtype == KL_BF16 ? e.beta == 0.f : (e.beta == 0.f && !g.R) || accum_only0) &&
+               (!g.R || use_r) && (e.n_act <= 1 || (e.act_group > 0 && e.act_group % 32 == 0));
   if (use_r) {
     int h2 = 0, h1 = 0;
     use_r = ((uintptr_t)g.R & 15) == 0 &&
-            make_map(&tr, g.R, g.N, g.M, g.r_rs, g.nb2, g.r_s2, g.nb1, g.r_s1, 64, BM, &h2, &h1, false);
+            make_map(&tr, g.R, g.N, g.M, g.r_rs, g.nb2, g.r_s2, g.nb1, g.r_s1, 64, BM, &h2, &h1, mode2);
     p.r_has2 = h2;
     p.r_has1 = h1;
+    if (!use_r) mode2 = false;
+  }
+  CUtensorMap tc_map;
+  if (mode2) {
+    int h2 = 0, h1 = 0;
+    const long long s1c = g.red1 ? 0 : g.c_s1, s2c = g.red2 ? 0 : g.c_s2;
+    mode2 = make_map(&tc_map, g.C, g.N, g.M, g.c_rs, g.red2 ? 1 : g.nb2, s2c, g.red1 ? 1 : g.nb1, s1c,
+                     128 / esz_c, 32, &h2, &h1, true, esz_c);
+    p.c_has2 = h2;
+    p.c_has1 = h1;
+    p.reduce_c = accum_only0 ? 1 : 0;
   }
   p.r_boxes = use_r ? (bn + 63) / 64 : 0;
   const uint32_t rbytes = 2u * p.r_boxes * 16384;
@@ -672,7 +871,7 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
     p.vec_r = g.R && g.r_cs == 1 && g.r_rs % 2 == 0 && (g.r_s1 % 2 == 0) && (g.r_s2 % 2 == 0) && al(g.R);
   }
 
-  const size_t smem = 1024 + (size_t)p.stages * stage + rbytes + (2 * p.stages + 8) * 8 + 16;
+  const size_t smem = 1024 + (size_t)p.stages * stage + rbytes + (2 * p.stages + 8) * 8 + 16 + 4 * 256 * 4;
   const int tiles = p.tiles_m * p.tiles_n * p.n_out;
   const int iters = ((g.red1 ? g.nb1 : 1) * (g.red2 ? g.nb2 : 1)) * p.kblocks;
   p.splits = 1;
@@ -701,14 +900,18 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
                      !g.R;
   auto launch = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<grid, NTHREADS, smem, s>>>(ta, tb, use_r ? tr : ta, p, e);
+    kern<<<grid, NTHREADS, smem, s>>>(ta, tb, use_r ? tr : ta, mode2 ? tc_map : ta, p, e);
   };
-  if (g.c_dtype == KL_BF16) {
-    if (plain) launch(gemm_tc_kernel<bf16, true>);
-    else launch(gemm_tc_kernel<bf16, false>);
+  if (mode2 && !p.ws) {
+    const bool full = e.bias || e.n_act;
+    if (g.c_dtype == KL_BF16) full ? launch(gemm_tc_kernel<bf16, 3>) : launch(gemm_tc_kernel<bf16, 2>);
+    else full ? launch(gemm_tc_kernel<float, 3>) : launch(gemm_tc_kernel<float, 2>);
+  } else if (g.c_dtype == KL_BF16) {
+    if (plain) launch(gemm_tc_kernel<bf16, 0>);
+    else launch(gemm_tc_kernel<bf16, 1>);
   } else {
-    if (plain) launch(gemm_tc_kernel<float, true>);
-    else launch(gemm_tc_kernel<float, false>);
+    if (plain) launch(gemm_tc_kernel<float, 0>);
+    else launch(gemm_tc_kernel<float, 1>);
   }
   count_launch();
   int rc = launch_check("gemm_tc");

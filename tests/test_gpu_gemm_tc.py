@@ -136,3 +136,32 @@ def test_tc_splitk_workspace(out_dtype):
     out = gemm(A, B, out_dtype=out_dtype, residual=R, alpha=0.5)
     ref = 0.5 * (A.double() @ B.double()) + R.double()
     assert rel(out, ref) < (1e-2 if out_dtype == torch.bfloat16 else 1e-4)  # fp32 accumulation over K=6144
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("N", [96, 256, 320, 768])
+def test_tc_tma_epilogue(N):
+    """TMA-store epilogue (thread = row, swizzled staging boxes): bias +
+    slab-uniform activations + row limit + TMA-staged residual into bf16,
+    and fp32 accumulate-into-C through the TMA reduce-add (also split-K)."""
+    from paper_2602_10016_b200._capi import gemm
+
+    g = torch.Generator(device="cuda").manual_seed(N)
+    A = operand((3, 333, 256), True, g)
+    B = operand((256, N), False, g)
+    bias = torch.randn(N, device="cuda", generator=g)
+    R = torch.randn(3, 333, N, device="cuda", generator=g).to(torch.bfloat16)
+    lim = torch.tensor([333, 200, 0], device="cuda", dtype=torch.int32)
+    z = A.double() @ B.double() * 0.5 + bias.double()
+    cols = torch.arange(N, device="cuda") // 32 % 2
+    act = torch.where(cols == 0, torch.nn.functional.silu(z), torch.relu(z)) + R.double()
+    rows = torch.arange(333, device="cuda")[None, :, None]
+    ref = torch.where(rows < lim.view(3, 1, 1), act, torch.zeros_like(act))
+    out = gemm(A, B, alpha=0.5, bias=bias, acts=["silu", "relu"], act_group=32, residual=R, row_limit=lim)
+    assert rel(out, ref) < 1e-2
+    # fp32 C += A^T B summed over the batch (weight-gradient form)
+    C0 = torch.randn(256, N, device="cuda", generator=g)
+    C = C0.clone()
+    gemm(A.transpose(1, 2), R, C, beta=1.0, reduce=(False, True))
+    ref = C0.double() + (A.double().transpose(1, 2) @ R.double()).sum(0)
+    assert rel(C, ref) < 1e-5
