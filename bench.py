@@ -175,6 +175,54 @@ def run_reference(args, cfg, B, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def graph_census(log, step, use_graph):
+    """Per-call-site device time of one (graph-replayed) training step:
+    CUPTI kernel records (torch.profiler) of the step, matched in launch order
+    to the C-ABI calls of an eager step (``log``: entry, shape, site, isolated
+    ms, kernels launched).  Printed to stderr."""
+    import collections
+
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        step()
+        torch.cuda.synchronize()
+    kern = sorted([e for e in prof.events() if e.device_type.name == "CUDA"], key=lambda e: e.time_range.start)
+    ours = [e for e in kern if e.name.startswith(("kl::", "void kl::", "gdpa::", "void gdpa::"))]
+    other = [e for e in kern if e not in ours]
+    step_us = (kern[-1].time_range.end - kern[0].time_range.start) if kern else 0.0
+    sites = []
+    for name, shape, site, _, nl in log:
+        sites += [(name, shape, site)] * nl
+    by_fn, by_site, cnt = collections.defaultdict(float), collections.defaultdict(float), collections.Counter()
+    for i, e in enumerate(ours):
+        nm, shape, site = sites[i] if i < len(sites) else ("?", "", "?")
+        dur = e.time_range.end - e.time_range.start
+        by_fn[(nm, site.split("<")[0])] += dur
+        by_site[(nm, shape, site)] += dur
+        cnt[(nm, shape, site)] += 1
+    kt = collections.defaultdict(float)
+    for e in kern:
+        kt[e.name[:90]] += e.time_range.end - e.time_range.start
+    tot = sum(kt.values())
+    print(f"graph census ({'graph' if use_graph else 'eager'} step): {len(kern)} kernels, {len(ours)} ours "
+          f"({len(sites)} expected), kernel time {tot / 1e3:.3f} ms, first->last {step_us / 1e3:.3f} ms; "
+          f"torch-native kernels {sum(e.time_range.end - e.time_range.start for e in other) / 1e3:.3f} ms",
+          file=sys.stderr)
+    durs = sorted(e.time_range.end - e.time_range.start for e in kern)
+    for lo_, hi_ in ((0, 5), (5, 10), (10, 20), (20, 50), (50, 1e9)):
+        sel = [x for x in durs if lo_ <= x < hi_]
+        print(f"  kernels {lo_:>3}-{hi_:<4} us: {len(sel):4d}, {sum(sel) / 1e3:7.3f} ms", file=sys.stderr)
+    print("--- by kernel", file=sys.stderr)
+    for k, v in sorted(kt.items(), key=lambda kv: -kv[1])[:30]:
+        print(f"{v / 1e3:8.3f} ms {100 * v / tot:5.1f}%  {k}", file=sys.stderr)
+    print("--- by call site", file=sys.stderr)
+    for k, v in sorted(by_site.items(), key=lambda kv: -kv[1])[:150]:
+        print(f"{v / 1e3:8.3f} ms {100 * v / tot:5.1f}% {cnt[k]:4d}k  {k[0]:18s} {k[1]:24s} {k[2]}", file=sys.stderr)
+
+
 def workload(args, cfg, B, world):
     ev = cfg.events[0]
     return {"workload": f"kunlun_{args.config}_train_step", "model": "kunlun", "layers": cfg.L, "d": cfg.d,
@@ -197,6 +245,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--gemm-census", action="store_true", help="log every kl_gemm shape/path of one step to stderr")
+    ap.add_argument("--op-census", action="store_true",
+                    help="time every C-ABI call of one eager step in isolation, grouped by call site (stderr)")
     ap.add_argument("--eager", action="store_true", help="issue every kernel from Python each step (no CUDA graph)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
@@ -279,6 +329,14 @@ def main():
             print(f"gemm {v:8.3f} ms {cnt[k]:3d}x {tf:7.1f} TF/s {k}", file=sys.stderr)
         _capi.GEMM_LOG = None
 
+    census_log = None
+    if args.op_census:
+        torch.cuda.synchronize()
+        _capi.OP_LOG = []
+        steps_[0].eager()
+        torch.cuda.synchronize()
+        census_log, _capi.OP_LOG = _capi.OP_LOG, None
+
     # The SWA kernels are timed with CUDA events recorded on their launching
     # stream; in graph mode the event records are nodes of the captured step,
     # so the durations come from the timed replays themselves.
@@ -298,6 +356,9 @@ def main():
         for _ in range(args.warmup):
             steps_[0]()
         barrier()
+
+    if census_log is not None:
+        graph_census(census_log, steps_[0], use_graph)
 
     # ---- device-timed region: inputs resident in HBM ----------------------
     if not use_graph:

@@ -58,6 +58,9 @@ unsigned long long kl_launch_count(void);
 int kl_tcgen05_available(void);
 /* Force the SIMT GEMM even for bf16 (debug / A-B testing).  0 = auto. */
 void kl_set_gemm_path(int path);
+/* Programmatic dependent launch of every library kernel (default off; env
+ * KL_PDL=1 or kl_set_pdl(1) turns it on). */
+void kl_set_pdl(int on);
 /* Path the last kl_gemm call on this thread took: 1 tcgen05, 0 SIMT. */
 int kl_last_gemm_path(void);
 
@@ -197,6 +200,10 @@ typedef struct kl_colsoftmax_args {
   void* dX;
   long long dx_rs, dx_bs;
   void* dX_lo; /* optional: dX - round(dX) in dX's dtype (bf16 hi/lo split) */
+  int dtype_dp; /* backward: dP's dtype (KL_F32 when zero-initialised) */
+  /* backward, optional: precomputed Dcol (Bn, C) fp32 (= rowsum(dO * O) of the
+   * pooled output); NULL -> reduced over t here (two passes) */
+  const float* Dcol;
 } kl_colsoftmax_args;
 
 int kl_colsoftmax_fwd(const kl_colsoftmax_args* args, void* stream);

@@ -63,6 +63,8 @@ class ColSoftmaxArgs(C.Structure):
         ("dP", C.c_void_p), ("dp_rs", C.c_longlong), ("dp_bs", C.c_longlong),
         ("dX", C.c_void_p), ("dx_rs", C.c_longlong), ("dx_bs", C.c_longlong),
         ("dX_lo", C.c_void_p),
+        ("dtype_dp", C.c_int),
+        ("Dcol", C.c_void_p),
     ]
 
 
@@ -87,6 +89,7 @@ _SIGS = {
     "kl_launch_count": ([], C.c_ulonglong),
     "kl_tcgen05_available": ([], C.c_int),
     "kl_set_gemm_path": ([C.c_int], None),
+    "kl_set_pdl": ([C.c_int], None),
     "kl_last_gemm_path": ([], C.c_int),
     "kl_gemm": ([C.POINTER(GemmArgs), C.c_void_p], C.c_int),
     "kl_gdpa_fwd": ([C.POINTER(GdpaArgs), C.c_void_p], C.c_int),
@@ -224,6 +227,14 @@ def gemm(A: torch.Tensor, B: torch.Tensor, out: torch.Tensor | None = None, *, o
     O4 = _as4(out)
     if tuple(O4.shape[2:]) != (M, N):
         raise ShapeError(f"gemm output shape {tuple(out.shape)} != (.., {M}, {N})")
+    if (SWAP_SMALL_M and A.dtype == torch.bfloat16 and M < 64 and N >= 2 * M and N >= 64 and bias is None
+            and not acts and aux is None and row_limit is None):
+        # Small-M product on the 128-row tcgen05 tile: compute C^T = B^T A^T so
+        # the long dimension fills the MMA rows (element-wise epilogue only).
+        R4 = _as4(residual).transpose(2, 3) if residual is not None else None
+        gemm(B4.transpose(2, 3), A4.transpose(2, 3), O4.transpose(2, 3), alpha=alpha, beta=beta,
+             residual=R4, reduce=reduce)
+        return ret
     a = GemmArgs()
     a.M, a.N, a.K = M, N, K
     a.nb1, a.nb2, a.red1, a.red2 = nb1, nb2, int(red1), int(red2)
@@ -264,11 +275,15 @@ def gemm(A: torch.Tensor, B: torch.Tensor, out: torch.Tensor | None = None, *, o
         for i, c in enumerate(codes):
             a.act_codes[i] = c
     if GEMM_LOG is not None:
+        torch.cuda.synchronize()  # isolate this GEMM: no host-issue gaps inside the window
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
     ws = _workspace(A.device)
     a.workspace, a.workspace_bytes = ws.data_ptr(), ws.numel() * 4
-    _check(lib().kl_gemm(C.byref(a), _stream()), "kl_gemm")
+    if OP_LOG is not None:
+        _logged("kl_gemm", f"{M}x{N}x{K} b{nb1}x{nb2} r{int(red1)}{int(red2)}", lib().kl_gemm, C.byref(a), _stream())
+    else:
+        _check(lib().kl_gemm(C.byref(a), _stream()), "kl_gemm")
     if GEMM_LOG is not None:
         e.record()
         import traceback
@@ -280,6 +295,7 @@ def gemm(A: torch.Tensor, B: torch.Tensor, out: torch.Tensor | None = None, *, o
     return ret
 
 
+SWAP_SMALL_M = True  # tests flip this to A/B the operand-swapped small-M form
 GEMM_LOG = None  # list of (M, N, K, nb1, nb2, red1, red2, A/B/C strides, c_dtype, path) when set
 
 
@@ -306,7 +322,35 @@ TIMED = None  # {entry-point name: [(start, end) CUDA events]} while bench.py ti
 TIMED_EXTERNAL = False  # record event nodes that survive CUDA-graph capture
 
 
+OP_LOG = None  # list of (entry, shape, call site, ms) while bench.py --op-census runs one eager step
+
+
+def _site() -> str:
+    import traceback
+
+    fr = [f for f in traceback.extract_stack()[:-3] if "paper_2602_10016_b200" in f.filename
+          and not f.filename.endswith("_capi.py")]
+    return "<".join(f"{os.path.basename(f.filename)[:-3]}:{f.name}:{f.lineno}" for f in reversed(fr[-3:]))
+
+
+def _logged(name, shape, fn, *args):
+    """Times one C-ABI call alone on the device (synchronize on both sides)."""
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda._sleep(200000)  # keeps the device busy while the host prepares the launch
+    s.record()
+    n0 = launch_count()
+    rc = fn(*args)
+    e.record()
+    e.synchronize()
+    OP_LOG.append((name, shape, _site(), s.elapsed_time(e), launch_count() - n0))
+    _check(rc, name)
+
+
 def call(name: str, *args):
+    if OP_LOG is not None:
+        _logged(name, "", getattr(lib(), name), *args)
+        return
     if TIMED is not None and name in TIMED:
         s = torch.cuda.Event(enable_timing=True, external=TIMED_EXTERNAL)
         e = torch.cuda.Event(enable_timing=True, external=TIMED_EXTERNAL)

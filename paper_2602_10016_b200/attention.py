@@ -176,8 +176,9 @@ def multi_head_attention(queries, keys_values, p: MhaParams, mask=None, lengths=
     qt = shared_queries(queries, p)  # (H, n_q, d)
     H, n_q = qt.shape[0], qt.shape[1]
     lens = _lengths(kv, lengths)
-    pooled = F.hsp_pool(kv, qt.reshape(H * n_q, p.dim), lens).view(kv.shape[0], H, n_q, p.dim)
-    o = F.head_proj(pooled, p.ref(2))
+    q_rows = qt.transpose(0, 1).reshape(n_q * H, p.dim)  # rows (query, head)
+    (pooled,) = F.hsp_pool(kv, q_rows, lens)
+    o = F.head_proj(pooled.view(kv.shape[0], n_q, H, p.dim), p.ref(2))
     out = F.linear(o, p.P, p.wout)
     return out.squeeze(0) if squeeze else out
 

@@ -2,6 +2,7 @@
 // error reporting, and dispatch between the tcgen05 (bf16) and SIMT paths.
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <atomic>
@@ -37,6 +38,15 @@ void count_launch(unsigned n) { g_launches.fetch_add(n, std::memory_order_relaxe
 
 int gemm_path() { return g_gemm_path; }
 
+static int g_pdl = -1;  // -1: from KL_PDL (default off: measured neutral on the c2 step)
+bool pdl_enabled() {
+  if (g_pdl < 0) {
+    const char* v = getenv("KL_PDL");
+    g_pdl = (v && v[0] == '1') ? 1 : 0;
+  }
+  return g_pdl == 1;
+}
+
 }  // namespace kl
 
 using namespace kl;
@@ -45,6 +55,7 @@ extern "C" int kl_version(void) { return 1; }
 extern "C" const char* kl_last_error(void) { return g_err; }
 extern "C" unsigned long long kl_launch_count(void) { return g_launches.load(); }
 extern "C" void kl_set_gemm_path(int path) { g_gemm_path = path; }
+extern "C" void kl_set_pdl(int on) { kl::g_pdl = on ? 1 : 0; }
 extern "C" int kl_last_gemm_path(void) { return kl::g_last_path; }
 
 extern "C" int kl_tcgen05_available(void) {

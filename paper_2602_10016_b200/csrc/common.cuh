@@ -6,6 +6,8 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "../../include/kunlun_capi.h"
 
 namespace kl {
@@ -16,12 +18,46 @@ typedef __nv_bfloat16 bf16;
 void set_error(const char* fmt, ...);
 int launch_check(const char* what);
 void count_launch(unsigned n = 1);
+bool pdl_enabled();
+
+// ---- launches: programmatic dependent launch (PDL) --------------------------
+// Every kernel of the library starts with KL_PDL_ENTRY() and, when PDL is on
+// (kl_set_pdl / KL_PDL=1), is launched with programmatic stream
+// serialization: it lets the next kernel in the
+// stream be scheduled while this one drains, and waits (griddepcontrol.wait)
+// for the full completion + memory flush of its predecessor before touching
+// global memory.  Inside a captured CUDA graph the launch becomes a
+// programmatic edge, hiding most of the per-kernel launch gap.
+#define KL_PDL_ENTRY()                                             \
+  do {                                                             \
+    asm volatile("griddepcontrol.wait;" ::: "memory");             \
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); \
+  } while (0)
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                            Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // ---- typed load / store -----------------------------------------------------
 __device__ __forceinline__ float ldf(const float* p) { return *p; }
 __device__ __forceinline__ float ldf(const bf16* p) { return __bfloat162float(*p); }
 __device__ __forceinline__ void stf(float* p, float v) { *p = v; }
 __device__ __forceinline__ void stf(bf16* p, float v) { *p = __float2bfloat16(v); }
+// value as stored in T (round-trip through the storage type)
+__device__ __forceinline__ float rtf(float v, const float*) { return v; }
+__device__ __forceinline__ float rtf(float v, const bf16*) { return __bfloat162float(__float2bfloat16(v)); }
 
 // ---- activation table (tensor.py:431-440), accurate fp32 libm -------------
 __device__ __forceinline__ float sigmoidf_(float x) {

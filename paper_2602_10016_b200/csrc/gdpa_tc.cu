@@ -235,6 +235,7 @@ template <int D>
 __global__ void __launch_bounds__(NT, 1)
     gdpa_fwd_kernel(const __grid_constant__ CUtensorMap ts, const __grid_constant__ CUtensorMap tk,
                     const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap ty, const P p) {
+  KL_PDL_ENTRY();
   constexpr int NA = D / 64;
   constexpr uint32_t SLOT = NA * ATOM_S;
   constexpr uint32_t IDESC_Z = tc::idesc_bf16(TB, HK, 0, 0);
@@ -437,6 +438,7 @@ __global__ void __launch_bounds__(NT, 1)
     gdpa_bwd_kernel(const __grid_constant__ CUtensorMap ts, const __grid_constant__ CUtensorMap tg,
                     const __grid_constant__ CUtensorMap tk, const __grid_constant__ CUtensorMap tv,
                     const __grid_constant__ CUtensorMap tds, const P p) {
+  KL_PDL_ENTRY();
   constexpr int NA = D / 64, NM = D / 128;
   constexpr uint32_t SLOT = NA * ATOM_S;
   constexpr uint32_t IDESC_Z = tc::idesc_bf16(TB, HK, 0, 0);
@@ -736,7 +738,7 @@ static int gdpa_fwd_launch(const kl_gdpa_args* a, const gdpa::P& p, cudaStream_t
   const int grid = std::min(W, tc_num_sms());
   gdpa::P q = p;
   q.out = (bf16*)a->Y;
-  gdpa::gdpa_fwd_kernel<D><<<grid, gdpa::NT, smem, s>>>(ts, tk, tv, ty, q);
+  launch_k(gdpa::gdpa_fwd_kernel<D>, grid, gdpa::NT, smem, s, ts, tk, tv, ty, q);
   count_launch();
   return launch_check("gdpa_fwd_tc");
 }
@@ -758,7 +760,7 @@ static int gdpa_bwd_launch(const kl_gdpa_args* a, const gdpa::P& p, cudaStream_t
   const int grid = std::min(a->B, tc_num_sms());
   gdpa::P q = p;
   q.out = (bf16*)a->dS;
-  gdpa::gdpa_bwd_kernel<D><<<grid, gdpa::NT, smem, s>>>(ts, tg, tk, tv, tds, q);
+  launch_k(gdpa::gdpa_bwd_kernel<D>, grid, gdpa::NT, smem, s, ts, tg, tk, tv, tds, q);
   count_launch();
   return launch_check("gdpa_bwd_tc");
 }

@@ -46,6 +46,9 @@ __device__ __forceinline__ void epilogue_store(const Epi& e, TC* C, const TC* R,
 }
 
 int gemm_simt(const GemmDesc& g, const Epi& e, cudaStream_t s);
+// Sums split-K partials ws[split][out batch][M][N] (fp32) and applies the
+// full epilogue.
+int splitk_reduce(const GemmDesc& g, const Epi& e, const float* ws, int splits, int n_out, cudaStream_t s);
 // Returns KL_EUNSUPPORTED (without error text) when the shape/layout is not
 // one the tcgen05 kernel takes; the caller then uses the SIMT kernel.
 int gemm_tc(const GemmDesc& g, const Epi& e, cudaStream_t s);

@@ -20,6 +20,7 @@ constexpr int BN = 64, BK = 16;
 
 template <typename TA, typename TC, int BM>
 __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmDesc g, Epi e, int splits) {
+  KL_PDL_ENTRY();
   constexpr int TM = BM / 16;       // rows per thread
   constexpr int AL = BM * BK / 256;  // A elements loaded per thread per k-step
   __shared__ float As[BK][BM + 4];
@@ -105,6 +106,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmDesc g, Epi e, int s
   TC* X = g.aux ? (TC*)g.aux + (long long)z1o * (g.red1 ? 0 : g.c_s1) + (long long)z2o * (g.red2 ? 0 : g.c_s2)
                 : nullptr;
   const int lim = e.row_limit ? e.row_limit[zo] : 0x7fffffff;
+  const int nout = gridDim.z / splits;
 #pragma unroll
   for (int i = 0; i < TM; ++i) {
     const int m = m0 + ty * TM + i;
@@ -114,7 +116,9 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmDesc g, Epi e, int s
       const int n = n0 + tx * 4 + j;
       if (n >= g.N) continue;
       const long long off = (long long)m * g.c_rs + (long long)n * g.c_cs;
-      if (splits > 1)
+      if (splits > 1 && g.ws)
+        g.ws[((long long)sp * nout + zo) * g.M * g.N + (long long)m * g.N + n] = acc[i][j];
+      else if (splits > 1)
         atomicAdd((float*)C + off, e.alpha * acc[i][j]);
       else
         epilogue_store(e, C, R, X, off, (long long)m * g.r_rs + (long long)n * g.r_cs, m, n, lim, acc[i][j]);
@@ -130,23 +134,38 @@ int launch(const GemmDesc& g, const Epi& e, cudaStream_t s) {
   const bool accum_only = g.c_dtype == KL_F32 && e.beta == 1.f && !e.bias && !e.row_limit && !e.aux_mode &&
                           e.n_act == 0 && !g.R;
   int splits = 1;
-  if (accum_only && tiles < 4 * 148 && iters >= 16)
+  GemmDesc gd = g;
+  gd.ws = nullptr;
+  if (accum_only && tiles < 4 * 148 && iters >= 16) {
     splits = (int)std::max<long long>(1, std::min<long long>((4 * 148) / tiles, iters / 8));
+  } else if (!accum_only && g.ws && tiles < 2 * 148 && iters >= 16) {
+    // few output tiles with any epilogue: fp32 partials in the workspace, then
+    // one reduce + epilogue pass
+    int sp = (int)std::max<long long>(1, std::min<long long>((4 * 148) / tiles, iters / 8));
+    const long long per = (long long)nout * g.M * g.N * 4;
+    while (sp > 1 && per * sp > g.ws_bytes) --sp;
+    if (sp > 1) {
+      splits = sp;
+      gd.ws = g.ws;
+    }
+  }
   dim3 grid((g.N + BN - 1) / BN, (g.M + BM - 1) / BM, nout * splits);
   if (grid.y > 65535 || grid.z > 65535) {
     set_error("kl_gemm: grid too large (M=%d, batches=%d)", g.M, nout);
     return KL_EUNSUPPORTED;
   }
   if (g.ab_dtype == KL_F32 && g.c_dtype == KL_F32)
-    gemm_simt_kernel<float, float, BM><<<grid, 256, 0, s>>>(g, e, splits);
+    launch_k(gemm_simt_kernel<float, float, BM>, grid, 256, 0, s, gd, e, splits);
   else if (g.ab_dtype == KL_F32 && g.c_dtype == KL_BF16)
-    gemm_simt_kernel<float, bf16, BM><<<grid, 256, 0, s>>>(g, e, splits);
+    launch_k(gemm_simt_kernel<float, bf16, BM>, grid, 256, 0, s, gd, e, splits);
   else if (g.ab_dtype == KL_BF16 && g.c_dtype == KL_F32)
-    gemm_simt_kernel<bf16, float, BM><<<grid, 256, 0, s>>>(g, e, splits);
+    launch_k(gemm_simt_kernel<bf16, float, BM>, grid, 256, 0, s, gd, e, splits);
   else
-    gemm_simt_kernel<bf16, bf16, BM><<<grid, 256, 0, s>>>(g, e, splits);
+    launch_k(gemm_simt_kernel<bf16, bf16, BM>, grid, 256, 0, s, gd, e, splits);
   count_launch();
-  return launch_check("gemm_simt");
+  int rc = launch_check("gemm_simt");
+  if (rc || !gd.ws) return rc;
+  return splitk_reduce(g, e, gd.ws, splits, nout, s);
 }
 
 }  // namespace

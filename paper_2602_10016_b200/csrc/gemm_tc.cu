@@ -431,6 +431,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmR, const __grid_constant__ CUtensorMap tmC, TcParams p,
                    Epi e) {
+  KL_PDL_ENTRY();
   constexpr bool PLAIN = MODE == 0;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -661,30 +662,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   if (warp == 1) tc::tmem_dealloc(tmem, p.tmem_cols);
 }
 
-// Sum the split-K partials and apply the full epilogue (element-wise).
-template <typename TC>
-__global__ void splitk_reduce_kernel(GemmDesc g, Epi e, const float* ws, int splits, int n_out) {
-  const long long MN = (long long)g.M * g.N, total = MN * n_out;
-  const int nb2o = g.red2 ? 1 : g.nb2;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int zo = (int)(i / MN);
-    const long long mn = i % MN;
-    const int m = (int)(mn / g.N), n = (int)(mn % g.N);
-    float acc = 0.f;
-    for (int s = 0; s < splits; ++s) acc += ws[(long long)s * total + i];
-    const int z1o = g.red1 ? 0 : zo / nb2o, z2o = g.red2 ? 0 : zo % nb2o;
-    TC* C = (TC*)g.C + (long long)z1o * (g.red1 ? 0 : g.c_s1) + (long long)z2o * (g.red2 ? 0 : g.c_s2);
-    const TC* R = g.R ? (const TC*)g.R + (long long)z1o * (g.red1 ? 0 : g.r_s1) + (long long)z2o * (g.red2 ? 0 : g.r_s2)
-                      : nullptr;
-    TC* X = g.aux ? (TC*)g.aux + (long long)z1o * (g.red1 ? 0 : g.c_s1) + (long long)z2o * (g.red2 ? 0 : g.c_s2)
-                  : nullptr;
-    const int lim = e.row_limit ? e.row_limit[zo] : 0x7fffffff;
-    epilogue_store(e, C, R, X, (long long)m * g.c_rs + (long long)n * g.c_cs,
-                   (long long)m * g.r_rs + (long long)n * g.r_cs, m, n, lim, acc);
-  }
-}
-
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static bool tried = false;
@@ -781,10 +758,75 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
   CUtensorMap tr;
   bool use_r = g.R && g.c_dtype == KL_BF16 && g.r_cs == 1 && !g.red1 && !g.red2;
   const int bn_max = use_r ? 128 : 256;
-  int tiles_n = (g.N + bn_max - 1) / bn_max;
-  int bn = (g.N + tiles_n - 1) / tiles_n;
-  bn = (bn + 15) / 16 * 16;
-  if (bn < 16) bn = 16;
+  const int n_out0 = (g.red1 ? 1 : g.nb1) * (g.red2 ? 1 : g.nb2);
+  const long long k_tot = (long long)((g.red1 ? g.nb1 : 1) * (g.red2 ? g.nb2 : 1)) * g.K;
+  auto split_n = [&](int cap) {
+    int tn = (g.N + cap - 1) / cap;
+    int b = (g.N + tn - 1) / tn;
+    b = (b + 15) / 16 * 16;
+    return b < 16 ? 16 : b;
+  };
+  int bn = split_n(bn_max);
+  // Split-K plan for a tile count: weight-gradient shapes (few output tiles,
+  // a long reduction) spread the reduction over the SMs; with an fp32
+  // accumulate-only epilogue the partial tiles add with fp32 atomics, any
+  // other epilogue goes through fp32 partials in the workspace + one reduce /
+  // epilogue pass.  Returns the split count; *ws_path tells which.
+  const bool accum_only = g.c_dtype == KL_F32 && e.beta == 1.f && !e.bias && !e.row_limit && !e.aux_mode &&
+                          e.n_act == 0 && !g.R;
+  const int kblocks0 = (g.K + BK - 1) / BK;
+  const int iters0 = ((g.red1 ? g.nb1 : 1) * (g.red2 ? g.nb2 : 1)) * kblocks0;
+  auto plan_splits = [&](long long tiles, bool* ws_path) {
+    *ws_path = false;
+    if (accum_only && tiles < num_sms() && iters0 >= 8)
+      return (int)std::max<long long>(1, std::min<long long>(num_sms() / tiles, iters0 / 4));
+    if (!accum_only && g.ws && tiles * 2 <= num_sms() && iters0 >= 8 && !use_r) {
+      int sp = (int)std::max<long long>(1, std::min<long long>(num_sms() / tiles, iters0 / 4));
+      const long long per = (long long)n_out0 * g.M * g.N * 4;
+      while (sp > 1 && per * sp > g.ws_bytes) --sp;
+      if (sp > 1) {
+        *ws_path = true;
+        return sp;
+      }
+    }
+    return 1;
+  };
+  {
+    // Tile width from a cycle model of one SM: a 128 x BN tile streams
+    // (128 + BN) bf16 operand columns per k (~64 B/clk of L2 bandwidth per SM)
+    // and issues 128*BN MACs per k (~2780 MAC/clk dense bf16), plus a fixed
+    // pipeline fill and a BN-wide epilogue; total = waves x tile cost (+ the
+    // workspace split-K reduce).  Few M tiles -> narrower N tiles or split-K
+    // instead of idle SMs.
+    const int tiles_m0 = (g.M + BM - 1) / BM;
+    double best = -1.0;
+    const int caps[4] = {256, 128, 64, 32};
+    for (int ci = 0; ci < 4; ++ci) {
+      const int cap = caps[ci];
+      if (cap > bn_max) continue;
+      // MN-major B is staged in 64-column boxes; bf16 C is stored in 64-column
+      // TMA boxes: neither may be split below 64 columns
+      if (cap < 64 && (!b_k || g.c_dtype == KL_BF16)) continue;
+      const int b = split_n(cap);
+      const long long tiles = (long long)tiles_m0 * ((g.N + b - 1) / b) * n_out0;
+      bool wsp = false;
+      const int sp = plan_splits(tiles, &wsp);
+      const long long waves = (tiles * sp + num_sms() - 1) / num_sms();
+      const double per_k = std::max(128.0 * b / 2780.0, (128.0 + b) * 2.0 / 64.0);
+      double cost = (double)waves * ((double)k_tot / sp * per_k + 500.0 + 4.0 * b);
+      if (wsp) cost += (double)n_out0 * g.M * g.N * 4.0 * (sp + 1) / 3100.0 + 2000.0;
+      if (best < 0 || cost < best * 0.97) {  // ties -> the wider tile
+        best = cost;
+        bn = b;
+      }
+    }
+    static int force = -1;
+    if (force < 0) {
+      const char* v = getenv("KL_GEMM_BN");
+      force = v ? atoi(v) : 0;
+    }
+    if (force >= 16) bn = std::min(split_n(bn_max), (force + 15) / 16 * 16);
+  }
   p.BN = bn;
   p.tiles_n = (g.N + bn - 1) / bn;
   p.tiles_m = (g.M + BM - 1) / BM;
@@ -874,25 +916,11 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
   const size_t smem = 1024 + (size_t)p.stages * stage + rbytes + (2 * p.stages + 8) * 8 + 16 + 4 * 256 * 4;
   const int tiles = p.tiles_m * p.tiles_n * p.n_out;
   const int iters = ((g.red1 ? g.nb1 : 1) * (g.red2 ? g.nb2 : 1)) * p.kblocks;
-  p.splits = 1;
-  // Weight-gradient shape: few output tiles, a long reduction.  Spread the
-  // reduction over the SMs; partial tiles accumulate with fp32 atomics, so
-  // only an fp32 accumulate-into-C epilogue (beta == 1, nothing else) qualifies.
-  const bool accum_only = g.c_dtype == KL_F32 && e.beta == 1.f && !e.bias && !e.row_limit && !e.aux_mode &&
-                          e.n_act == 0 && !g.R;
   p.ws = nullptr;
-  if (accum_only && tiles < num_sms() && iters >= 8) {
-    p.splits = std::max(1, std::min(num_sms() / tiles, iters / 4));
-  } else if (!accum_only && g.ws && tiles * 2 <= num_sms() && iters >= 8 && !use_r) {
-    // few output tiles with any epilogue: fp32 partials in the workspace, then
-    // one reduce + epilogue pass
-    int sp = std::max(1, std::min(num_sms() / tiles, iters / 4));
-    const long long per = (long long)p.n_out * g.M * g.N * 4;
-    while (sp > 1 && per * sp > g.ws_bytes) --sp;
-    if (sp > 1) {
-      p.splits = sp;
-      p.ws = g.ws;
-    }
+  {
+    bool wsp = false;
+    p.splits = plan_splits(tiles, &wsp);
+    if (wsp) p.ws = g.ws;
   }
   const int total = tiles * p.splits;
   const int grid = std::min(total, num_sms());
@@ -900,7 +928,7 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
                      !g.R;
   auto launch = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<grid, NTHREADS, smem, s>>>(ta, tb, use_r ? tr : ta, mode2 ? tc_map : ta, p, e);
+    launch_k(kern, grid, NTHREADS, smem, s, ta, tb, use_r ? tr : ta, mode2 ? tc_map : ta, p, e);
   };
   if (mode2 && !p.ws) {
     const bool full = e.bias || e.n_act;
@@ -916,14 +944,7 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
   count_launch();
   int rc = launch_check("gemm_tc");
   if (rc || !p.ws) return rc;
-  const long long total_el = (long long)p.n_out * g.M * g.N;
-  const unsigned rg = (unsigned)std::min<long long>((total_el + 255) / 256, 148 * 16);
-  if (g.c_dtype == KL_BF16)
-    splitk_reduce_kernel<bf16><<<rg, 256, 0, s>>>(g, e, p.ws, p.splits, p.n_out);
-  else
-    splitk_reduce_kernel<float><<<rg, 256, 0, s>>>(g, e, p.ws, p.splits, p.n_out);
-  count_launch();
-  return launch_check("gemm_tc_splitk_reduce");
+  return splitk_reduce(g, e, p.ws, p.splits, p.n_out, s);
 }
 
 }  // namespace kl
@@ -931,4 +952,43 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
 namespace kl {
 PFN_cuTensorMapEncodeTiled_v12000 tc_encode_fn() { return encode_fn(); }
 int tc_num_sms() { return num_sms(); }
+}  // namespace kl
+
+namespace kl {
+// Sum the split-K partials and apply the full epilogue (element-wise).
+template <typename TC>
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(GemmDesc g, Epi e, const float* ws, int splits, int n_out) {
+  KL_PDL_ENTRY();
+  const long long MN = (long long)g.M * g.N, total = MN * n_out;
+  const int nb2o = g.red2 ? 1 : g.nb2;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int zo = (int)(i / MN);
+    const long long mn = i % MN;
+    const int m = (int)(mn / g.N), n = (int)(mn % g.N);
+    float acc = 0.f;
+    for (int s = 0; s < splits; ++s) acc += ws[(long long)s * total + i];
+    const int z1o = g.red1 ? 0 : zo / nb2o, z2o = g.red2 ? 0 : zo % nb2o;
+    TC* C = (TC*)g.C + (long long)z1o * (g.red1 ? 0 : g.c_s1) + (long long)z2o * (g.red2 ? 0 : g.c_s2);
+    const TC* R = g.R ? (const TC*)g.R + (long long)z1o * (g.red1 ? 0 : g.r_s1) + (long long)z2o * (g.red2 ? 0 : g.r_s2)
+                      : nullptr;
+    TC* X = g.aux ? (TC*)g.aux + (long long)z1o * (g.red1 ? 0 : g.c_s1) + (long long)z2o * (g.red2 ? 0 : g.c_s2)
+                  : nullptr;
+    const int lim = e.row_limit ? e.row_limit[zo] : 0x7fffffff;
+    epilogue_store(e, C, R, X, (long long)m * g.c_rs + (long long)n * g.c_cs,
+                   (long long)m * g.r_rs + (long long)n * g.r_cs, m, n, lim, acc);
+  }
+}
+
+
+int splitk_reduce(const GemmDesc& g, const Epi& e, const float* ws, int splits, int n_out, cudaStream_t s) {
+  const long long total_el = (long long)n_out * g.M * g.N;
+  const unsigned rg = (unsigned)std::min<long long>((total_el + 255) / 256, 148 * 16);
+  if (g.c_dtype == KL_BF16)
+    launch_k(splitk_reduce_kernel<bf16>, rg, 256, 0, s, g, e, ws, splits, n_out);
+  else
+    launch_k(splitk_reduce_kernel<float>, rg, 256, 0, s, g, e, ws, splits, n_out);
+  count_launch();
+  return launch_check("gemm_splitk_reduce");
+}
 }  // namespace kl

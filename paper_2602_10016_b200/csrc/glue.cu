@@ -14,73 +14,130 @@ namespace {
 // Column softmax over rows t < len (queries are columns):
 // masked_softmax_lastdim (tensor.py:485-505) applied to the transposed HSP/PMA
 // score block of multi_head_attention (attention.py:89-91).
+// Block = 32 columns x 8 row groups; each thread keeps CS_U independent
+// online (max, sum) pairs so CS_U row loads are in flight at once (the kernels
+// are HBM/L2 bound: one stats pass + one write pass over the score block).
+constexpr int CS_U = 8;
+
 template <typename TI, typename TO>
 __global__ void __launch_bounds__(256) colsoftmax_fwd_kernel(kl_colsoftmax_args a) {
-  __shared__ float red[8][33];
+  KL_PDL_ENTRY();
+  __shared__ float redm[8][33], reds[8][33];
   const int b = blockIdx.y;
   const int cl = threadIdx.x & 31, rg = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + cl;
   const int len = a.lengths[b];
-  const TI* X = (const TI*)a.X + (long long)b * a.x_bs;
-  TO* P = (TO*)a.P + (long long)b * a.p_bs;
-  float m = -INFINITY;
-  if (c < a.C)
-    for (int t = rg; t < len; t += 8) m = fmaxf(m, ldf(X + (long long)t * a.x_rs + c));
-  red[rg][cl] = m;
-  __syncthreads();
-  m = red[0][cl];
+  const TI* X = (const TI*)a.X + (long long)b * a.x_bs + c;
+  TO* P = (TO*)a.P + (long long)b * a.p_bs + c;
+  float m[CS_U], sm[CS_U];
 #pragma unroll
-  for (int i = 1; i < 8; ++i) m = fmaxf(m, red[i][cl]);
+  for (int u = 0; u < CS_U; ++u) {
+    m[u] = -INFINITY;
+    sm[u] = 0.f;
+  }
+  if (c < a.C) {
+    for (int t0 = rg; t0 < len; t0 += 8 * CS_U) {
+      float v[CS_U];
+#pragma unroll
+      for (int u = 0; u < CS_U; ++u) {
+        const int t = t0 + 8 * u;
+        v[u] = t < len ? ldf(X + (long long)t * a.x_rs) : -INFINITY;
+      }
+#pragma unroll
+      for (int u = 0; u < CS_U; ++u) {
+        if (v[u] == -INFINITY) continue;
+        const float mn = fmaxf(m[u], v[u]);
+        sm[u] = sm[u] * __expf(m[u] - mn) + __expf(v[u] - mn);
+        m[u] = mn;
+      }
+    }
+  }
+  float mt = m[0];
+#pragma unroll
+  for (int u = 1; u < CS_U; ++u) mt = fmaxf(mt, m[u]);
+  float st = 0.f;
+#pragma unroll
+  for (int u = 0; u < CS_U; ++u) st += m[u] == -INFINITY ? 0.f : sm[u] * __expf(m[u] - mt);
+  redm[rg][cl] = mt;
+  reds[rg][cl] = st;
   __syncthreads();
+  float mx = redm[0][cl];
+#pragma unroll
+  for (int i = 1; i < 8; ++i) mx = fmaxf(mx, redm[i][cl]);
   float ssum = 0.f;
-  if (c < a.C)
-    for (int t = rg; t < len; t += 8) ssum += expf(ldf(X + (long long)t * a.x_rs + c) - m);
-  red[rg][cl] = ssum;
-  __syncthreads();
-  ssum = 0.f;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) ssum += red[i][cl];
+  for (int i = 0; i < 8; ++i) ssum += redm[i][cl] == -INFINITY ? 0.f : reds[i][cl] * __expf(redm[i][cl] - mx);
   if (c >= a.C) return;
   const float inv = ssum > 0.f ? 1.f / ssum : 0.f;
-  for (int t = rg; t < a.T; t += 8) {
-    float v = t < len ? expf(ldf(X + (long long)t * a.x_rs + c) - m) * inv : 0.f;
-    stf(P + (long long)t * a.p_rs + c, v);
+  for (int t0 = rg; t0 < a.T; t0 += 8 * CS_U) {
+    float v[CS_U];
+#pragma unroll
+    for (int u = 0; u < CS_U; ++u) {
+      const int t = t0 + 8 * u;
+      v[u] = t < len ? ldf(X + (long long)t * a.x_rs) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < CS_U; ++u) {
+      const int t = t0 + 8 * u;
+      if (t < a.T) stf(P + (long long)t * a.p_rs, t < len ? expf(v[u] - mx) * inv : 0.f);
+    }
   }
-  if (rg == 0 && a.LSE) a.LSE[(long long)b * a.C + c] = len > 0 ? m + logf(ssum) : INFINITY;
+  if (rg == 0 && a.LSE) a.LSE[(long long)b * a.C + c] = len > 0 ? mx + logf(ssum) : INFINITY;
 }
 
-// dX = P * (dP - sum_t P dP)   (tensor.py:501-503)
+// dX = P * (dP - sum_t P dP)   (tensor.py:501-503); P in TP, dP in TG, dX in TO.
 template <typename TP, typename TG, typename TO>
 __global__ void __launch_bounds__(256) colsoftmax_bwd_kernel(kl_colsoftmax_args a) {
+  KL_PDL_ENTRY();
   __shared__ float red[8][33];
   const int b = blockIdx.y;
   const int cl = threadIdx.x & 31, rg = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + cl;
   const int len = a.lengths[b];
-  const TP* P = (const TP*)a.P + (long long)b * a.p_bs;
-  const TG* G = (const TG*)a.dP + (long long)b * a.dp_bs;
-  TO* D = (TO*)a.dX + (long long)b * a.dx_bs;
-  float acc = 0.f;
-  if (c < a.C)
-    for (int t = rg; t < len; t += 8) acc += ldf(P + (long long)t * a.p_rs + c) * ldf(G + (long long)t * a.dp_rs + c);
-  red[rg][cl] = acc;
-  __syncthreads();
-  acc = 0.f;
+  const TP* P = (const TP*)a.P + (long long)b * a.p_bs + c;
+  const TG* G = (const TG*)a.dP + (long long)b * a.dp_bs + c;
+  TO* D = (TO*)a.dX + (long long)b * a.dx_bs + c;
+  TO* L = a.dX_lo ? (TO*)a.dX_lo + (long long)b * a.dx_bs + c : nullptr;
+  float acc[CS_U];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) acc += red[i][cl];
-  if (c >= a.C) return;
-  for (int t = rg; t < a.T; t += 8) {
-    float v = 0.f;
-    if (t < len) {
-      float pr = ldf(P + (long long)t * a.p_rs + c);
-      v = pr * (ldf(G + (long long)t * a.dp_rs + c) - acc);
+  for (int u = 0; u < CS_U; ++u) acc[u] = 0.f;
+  if (c < a.C && !a.Dcol)
+    for (int t0 = rg; t0 < len; t0 += 8 * CS_U) {
+#pragma unroll
+      for (int u = 0; u < CS_U; ++u) {
+        const int t = t0 + 8 * u;
+        if (t < len) acc[u] += ldf(P + (long long)t * a.p_rs) * ldf(G + (long long)t * a.dp_rs);
+      }
     }
-    stf(D + (long long)t * a.dx_rs + c, v);
-    if (a.dX_lo) {
-      // bf16 residual of the rounded value: hi + lo carries ~16 mantissa bits
-      // into the cancellation-heavy reduction dQ = sum_t dX S (seqsum VJP)
-      TO* L = (TO*)a.dX_lo + (long long)b * a.dx_bs;
-      stf(L + (long long)t * a.dx_rs + c, v - ldf(D + (long long)t * a.dx_rs + c));
+  float at = 0.f;
+#pragma unroll
+  for (int u = 0; u < CS_U; ++u) at += acc[u];
+  red[rg][cl] = at;
+  __syncthreads();
+  float dsum = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) dsum += red[i][cl];
+  if (c >= a.C) return;
+  if (a.Dcol) dsum = a.Dcol[(long long)b * a.C + c];
+  for (int t0 = rg; t0 < a.T; t0 += 8 * CS_U) {
+    float pv[CS_U], gv[CS_U];
+#pragma unroll
+    for (int u = 0; u < CS_U; ++u) {
+      const int t = t0 + 8 * u;
+      pv[u] = t < len ? ldf(P + (long long)t * a.p_rs) : 0.f;
+      gv[u] = t < len ? ldf(G + (long long)t * a.dp_rs) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < CS_U; ++u) {
+      const int t = t0 + 8 * u;
+      if (t >= a.T) continue;
+      const float v = t < len ? pv[u] * (gv[u] - dsum) : 0.f;
+      stf(D + (long long)t * a.dx_rs, v);
+      if (L) {
+        // bf16 residual of the rounded value: hi + lo carries ~16 mantissa bits
+        // into the cancellation-heavy reduction dQ = sum_t dX S (seqsum VJP)
+        stf(L + (long long)t * a.dx_rs, v - rtf(v, D));
+      }
     }
   }
 }
@@ -112,6 +169,7 @@ __device__ double block_sum_d(double v, double* sh) {
 
 // rms_norm (tensor.py:552-556): one block per row.
 __global__ void rmsnorm_fwd_kernel(int d, float eps, const float* x, const float* gain, float* y) {
+  KL_PDL_ENTRY();
   __shared__ float sh[32];
   const float* xr = x + (long long)blockIdx.x * d;
   float ss = 0.f;
@@ -122,30 +180,45 @@ __global__ void rmsnorm_fwd_kernel(int d, float eps, const float* x, const float
 }
 
 // Single block: dx = s*gg - s^3/d * x * sum(gg*x), gg = dy*gain; dgain = sum_rows dy*x*s.
-__global__ void rmsnorm_bwd_kernel(int rows, int d, float eps, const float* x, const float* gain,
-                                   const float* dy, float* dx, float* dgain) {
-  __shared__ float sh[32];
-  constexpr int MAXC = 8;  // d <= 8 * blockDim
-  double dg[MAXC];
-  for (int i = 0; i < MAXC; ++i) dg[i] = 0.0;
-  for (int r = 0; r < rows; ++r) {
+// Phase 1: one warp per row computes s and k = s^3/d * sum(gg*x) into smem;
+// phase 2: one thread per column writes dx for every row and accumulates
+// dgain in fp64.
+__global__ void __launch_bounds__(256) rmsnorm_bwd_kernel(int rows, int d, float eps, const float* x,
+                                                         const float* gain, const float* dy, float* dx,
+                                                         float* dgain) {
+  KL_PDL_ENTRY();
+  extern __shared__ float rs[];  // s[rows], k[rows]
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  for (int r = w; r < rows; r += blockDim.x >> 5) {
     const float* xr = x + (long long)r * d;
     const float* gr = dy + (long long)r * d;
     float ss = 0.f, gx = 0.f;
-    for (int c = threadIdx.x; c < d; c += blockDim.x) {
-      ss += xr[c] * xr[c];
-      gx += gr[c] * gain[c] * xr[c];
+    for (int c = l; c < d; c += 32) {
+      const float xv = xr[c];
+      ss += xv * xv;
+      gx += gr[c] * gain[c] * xv;
     }
-    ss = block_sum(ss, sh);
-    gx = block_sum(gx, sh);
-    const float s = 1.f / sqrtf(ss / d + eps);
-    const float k = s * s * s / d * gx;
-    for (int c = threadIdx.x; c < d; c += blockDim.x) {
-      dx[(long long)r * d + c] = s * gr[c] * gain[c] - k * xr[c];
-      dg[c / blockDim.x] += (double)gr[c] * (double)xr[c] * (double)s;
+    for (int o = 16; o > 0; o >>= 1) {
+      ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      gx += __shfl_xor_sync(0xffffffffu, gx, o);
+    }
+    if (l == 0) {
+      const float sv = 1.f / sqrtf(ss / d + eps);
+      rs[r] = sv;
+      rs[rows + r] = sv * sv * sv / d * gx;
     }
   }
-  for (int c = threadIdx.x; c < d; c += blockDim.x) dgain[c] = (float)dg[c / blockDim.x];
+  __syncthreads();
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    double dg = 0.0;
+    const float gc = gain[c];
+    for (int r = 0; r < rows; ++r) {
+      const float xv = x[(long long)r * d + c], gv = dy[(long long)r * d + c];
+      dx[(long long)r * d + c] = rs[r] * gv * gc - rs[rows + r] * xv;
+      dg += (double)gv * (double)xv * (double)rs[r];
+    }
+    dgain[c] = (float)dg;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -153,6 +226,7 @@ __global__ void rmsnorm_bwd_kernel(int rows, int d, float eps, const float* x, c
 template <typename T>
 __global__ void recent_fwd_kernel(int B, int T_, int d, int n, const T* S, long long s_bs, const int* lengths,
                                   T* out, long long o_bs) {
+  KL_PDL_ENTRY();
   long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (long long)B * n * d) return;
   int c = idx % d, r = (idx / d) % n, b = idx / ((long long)d * n);
@@ -164,6 +238,7 @@ __global__ void recent_fwd_kernel(int B, int T_, int d, int n, const T* S, long 
 template <typename T>
 __global__ void recent_bwd_kernel(int B, int T_, int d, int n, const T* dout, long long o_bs, const int* lengths,
                                   T* dS, long long s_bs) {
+  KL_PDL_ENTRY();
   long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (long long)B * n * d) return;
   int c = idx % d, r = (idx / d) % n, b = idx / ((long long)d * n);
@@ -177,39 +252,60 @@ __global__ void recent_bwd_kernel(int B, int T_, int d, int n, const T* dout, lo
 // triu_flatten(x x^T) (interaction.py:63-76, 117): np.triu_indices row-major.
 __device__ __forceinline__ int triu_index(int r, int c, int n) { return r * n - r * (r - 1) / 2 + (c - r); }
 
+// One block per sample: x[b] (n x d) staged in smem as fp32; one warp per
+// pair (lanes split the d-length dot product).
 template <typename T>
-__global__ void gram_triu_fwd_kernel(int B, int n, int d, const T* x, long long x_rs, long long x_bs, T* tri,
-                                     long long t_bs) {
+__global__ void __launch_bounds__(256) gram_triu_fwd_kernel(int n, int d, const T* x, long long x_rs,
+                                                           long long x_bs, T* tri, long long t_bs) {
+  KL_PDL_ENTRY();
+  extern __shared__ float xs[];
+  const int b = blockIdx.x;
+  const T* xb = x + (long long)b * x_bs;
+  for (int i = threadIdx.x; i < n * d; i += blockDim.x) xs[i] = ldf(xb + (long long)(i / d) * x_rs + i % d);
+  __syncthreads();
   const int np_ = n * (n + 1) / 2;
-  long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= (long long)B * np_) return;
-  int pidx = idx % np_, b = idx / np_;
-  int r = 0;
-  while (triu_index(r + 1, r + 1, n) <= pidx && r + 1 < n) ++r;
-  int c = r + (pidx - triu_index(r, r, n));
-  const T* xr = x + (long long)b * x_bs + (long long)r * x_rs;
-  const T* xc = x + (long long)b * x_bs + (long long)c * x_rs;
-  float acc = 0.f;
-  for (int k = 0; k < d; ++k) acc = fmaf(ldf(xr + k), ldf(xc + k), acc);
-  stf(tri + (long long)b * t_bs + pidx, acc);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+  int r = 0, rbase = 0;  // pair p = rbase + (c - r) for row r
+  for (int p = w; p < np_; p += nw) {
+    while (p >= rbase + (n - r)) {
+      rbase += n - r;
+      ++r;
+    }
+    const int c = r + (p - rbase);
+    const float* xr = xs + r * d;
+    const float* xc = xs + c * d;
+    float acc = 0.f;
+    for (int k = l; k < d; k += 32) acc = fmaf(xr[k], xc[k], acc);
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (l == 0) stf(tri + (long long)b * t_bs + p, acc);
+  }
 }
 
+// dx[b, r, k] += sum_j W[r][j] x[b, j, k], W symmetric from dtri (diagonal x2).
 template <typename T>
-__global__ void gram_triu_bwd_kernel(int B, int n, int d, const T* x, long long x_rs, long long x_bs,
-                                     const T* dtri, long long t_bs, T* dx, long long dx_rs, long long dx_bs) {
-  long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= (long long)B * n * d) return;
-  int k = idx % d, r = (idx / d) % n, b = idx / ((long long)d * n);
+__global__ void __launch_bounds__(256) gram_triu_bwd_kernel(int n, int d, const T* x, long long x_rs,
+                                                           long long x_bs, const T* dtri, long long t_bs, T* dx,
+                                                           long long dx_rs, long long dx_bs) {
+  KL_PDL_ENTRY();
+  extern __shared__ float sm[];
+  float* xs = sm;          // n x d
+  float* W = sm + n * d;   // n x n
+  const int b = blockIdx.x;
   const T* xb = x + (long long)b * x_bs;
   const T* db = dtri + (long long)b * t_bs;
-  float acc = 0.f;
-  for (int j = 0; j < n; ++j) {
-    int lo = min(r, j), hi = max(r, j);
-    float wgt = ldf(db + triu_index(lo, hi, n)) * (r == j ? 2.f : 1.f);
-    acc = fmaf(wgt, ldf(xb + (long long)j * x_rs + k), acc);
+  for (int i = threadIdx.x; i < n * d; i += blockDim.x) xs[i] = ldf(xb + (long long)(i / d) * x_rs + i % d);
+  for (int i = threadIdx.x; i < n * n; i += blockDim.x) {
+    const int r = i / n, j = i % n, lo = min(r, j), hi = max(r, j);
+    W[i] = ldf(db + triu_index(lo, hi, n)) * (r == j ? 2.f : 1.f);
   }
-  T* p = dx + (long long)b * dx_bs + (long long)r * dx_rs + k;
-  stf(p, ldf(p) + acc);
+  __syncthreads();
+  for (int i = threadIdx.x; i < n * d; i += blockDim.x) {
+    const int r = i / d, k = i % d;
+    float acc = 0.f;
+    for (int j = 0; j < n; ++j) acc = fmaf(W[r * n + j], xs[j * d + k], acc);
+    T* p = dx + (long long)b * dx_bs + (long long)r * dx_rs + k;
+    stf(p, ldf(p) + acc);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -217,6 +313,7 @@ __global__ void gram_triu_bwd_kernel(int B, int n, int d, const T* x, long long 
 template <typename T>
 __global__ void gated_fwd_kernel(int rows, int d, const T* x, long long x_rs, const T* deep, const T* dot,
                                  const float* gd, const float* gt, T* out, long long o_rs) {
+  KL_PDL_ENTRY();
   long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (long long)rows * d) return;
   int c = idx % d;
@@ -229,6 +326,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) gated_bwd_kernel(int rows, int d, const T* g, long long g_rs, const T* deep,
                                                         const T* dot, const float* gd, const float* gt, T* ddeep,
                                                         T* ddot, double* partial) {
+  KL_PDL_ENTRY();
   __shared__ double shd[32];
   double a = 0.0, b = 0.0;
   const long long total = (long long)rows * d;
@@ -251,6 +349,7 @@ __global__ void __launch_bounds__(256) gated_bwd_kernel(int rows, int d, const T
 }
 
 __global__ void reduce_pairs_kernel(int nblk, const double* partial, float* o0, float* o1) {
+  KL_PDL_ENTRY();
   __shared__ double sh[32];
   double a = 0.0, b = 0.0;
   for (int i = threadIdx.x; i < nblk; i += blockDim.x) {
@@ -268,6 +367,7 @@ __global__ void reduce_pairs_kernel(int nblk, const double* partial, float* o0, 
 // ---------------------------------------------------------------------------
 // bce_with_logits (tensor.py:535-549)
 __global__ void bce_kernel(int n, const float* z, const float* y, float* loss, float* dz) {
+  KL_PDL_ENTRY();
   __shared__ float sh[32];
   float acc = 0.f;
   const float inv = 1.f / (float)max(n, 1);
@@ -282,6 +382,7 @@ __global__ void bce_kernel(int n, const float* z, const float* y, float* loss, f
 
 template <typename TI, typename TO>
 __global__ void cast_kernel(long long n, const TI* x, TO* y) {
+  KL_PDL_ENTRY();
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     stf(y + i, ldf(x + i));
 }
@@ -293,6 +394,7 @@ struct ActCodes {
 
 template <typename T>
 __global__ void act_kernel(int rows, int cols, const T* x, long long ld, T* y, long long ld_y, ActCodes ac) {
+  KL_PDL_ENTRY();
   long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (long long)rows * cols) return;
   int c = idx % cols;
@@ -304,6 +406,7 @@ __global__ void act_kernel(int rows, int cols, const T* x, long long ld, T* y, l
 template <typename T>
 __global__ void act_bwd_kernel(int rows, int cols, const T* g, long long ldg, const T* x, long long ldx, T* y,
                                long long ld_y, ActCodes ac) {
+  KL_PDL_ENTRY();
   long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (long long)rows * cols) return;
   int c = idx % cols;
@@ -314,6 +417,7 @@ __global__ void act_bwd_kernel(int rows, int cols, const T* g, long long ldg, co
 
 template <typename T>
 __global__ void finite_kernel(long long n, const T* x, unsigned int* flag) {
+  KL_PDL_ENTRY();
   bool bad = false;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     bad |= !isfinite(ldf(x + i));
@@ -333,10 +437,10 @@ extern "C" int kl_colsoftmax_fwd(const kl_colsoftmax_args* a, void* stream) {
   if (a->Bn == 0 || a->C == 0 || a->T == 0) return KL_OK;
   cudaStream_t s = (cudaStream_t)stream;
   dim3 grid((a->C + 31) / 32, a->Bn);
-  if (a->dtype_in == KL_F32 && a->dtype_out == KL_F32) colsoftmax_fwd_kernel<float, float><<<grid, 256, 0, s>>>(*a);
-  else if (a->dtype_in == KL_F32) colsoftmax_fwd_kernel<float, bf16><<<grid, 256, 0, s>>>(*a);
-  else if (a->dtype_out == KL_F32) colsoftmax_fwd_kernel<bf16, float><<<grid, 256, 0, s>>>(*a);
-  else colsoftmax_fwd_kernel<bf16, bf16><<<grid, 256, 0, s>>>(*a);
+  if (a->dtype_in == KL_F32 && a->dtype_out == KL_F32) launch_k(colsoftmax_fwd_kernel<float, float>, grid, 256, 0, s, *a);
+  else if (a->dtype_in == KL_F32) launch_k(colsoftmax_fwd_kernel<float, bf16>, grid, 256, 0, s, *a);
+  else if (a->dtype_out == KL_F32) launch_k(colsoftmax_fwd_kernel<bf16, float>, grid, 256, 0, s, *a);
+  else launch_k(colsoftmax_fwd_kernel<bf16, bf16>, grid, 256, 0, s, *a);
   count_launch();
   return launch_check("colsoftmax_fwd");
 }
@@ -346,18 +450,24 @@ extern "C" int kl_colsoftmax_bwd(const kl_colsoftmax_args* a, void* stream) {
   if (a->Bn == 0 || a->C == 0 || a->T == 0) return KL_OK;
   cudaStream_t s = (cudaStream_t)stream;
   dim3 grid((a->C + 31) / 32, a->Bn);
-  // P and dP share dtype_out's storage type; dX uses dtype_in's
-  if (a->dtype_out == KL_F32 && a->dtype_in == KL_F32) colsoftmax_bwd_kernel<float, float, float><<<grid, 256, 0, s>>>(*a);
-  else if (a->dtype_out == KL_F32) colsoftmax_bwd_kernel<float, float, bf16><<<grid, 256, 0, s>>>(*a);
-  else if (a->dtype_in == KL_F32) colsoftmax_bwd_kernel<bf16, bf16, float><<<grid, 256, 0, s>>>(*a);
-  else colsoftmax_bwd_kernel<bf16, bf16, bf16><<<grid, 256, 0, s>>>(*a);
+  // P in dtype_out, dP in dtype_dp, dX (and dX_lo) in dtype_in
+  const int tp = a->dtype_out, tg = a->dtype_dp, to = a->dtype_in;
+  if (tp == KL_F32 && tg == KL_F32 && to == KL_F32) launch_k(colsoftmax_bwd_kernel<float, float, float>, grid, 256, 0, s, *a);
+  else if (tp == KL_F32 && tg == KL_F32) launch_k(colsoftmax_bwd_kernel<float, float, bf16>, grid, 256, 0, s, *a);
+  else if (tp == KL_BF16 && tg == KL_F32 && to == KL_BF16) launch_k(colsoftmax_bwd_kernel<bf16, float, bf16>, grid, 256, 0, s, *a);
+  else if (tp == KL_BF16 && tg == KL_F32) launch_k(colsoftmax_bwd_kernel<bf16, float, float>, grid, 256, 0, s, *a);
+  else if (tp == KL_BF16 && tg == KL_BF16 && to == KL_BF16) launch_k(colsoftmax_bwd_kernel<bf16, bf16, bf16>, grid, 256, 0, s, *a);
+  else {
+    set_error("kl_colsoftmax_bwd: unsupported dtype combination (P %d, dP %d, dX %d)", tp, tg, to);
+    return KL_EUNSUPPORTED;
+  }
   count_launch();
   return launch_check("colsoftmax_bwd");
 }
 
 extern "C" int kl_rmsnorm_fwd(int rows, int d, float eps, const float* x, const float* gain, float* y, void* stream) {
   if (rows <= 0 || d <= 0) return KL_OK;
-  rmsnorm_fwd_kernel<<<rows, 256, 0, (cudaStream_t)stream>>>(d, eps, x, gain, y);
+  launch_k(rmsnorm_fwd_kernel, rows, 256, 0, (cudaStream_t)stream, d, eps, x, gain, y);
   count_launch();
   return launch_check("rmsnorm_fwd");
 }
@@ -365,8 +475,10 @@ extern "C" int kl_rmsnorm_fwd(int rows, int d, float eps, const float* x, const 
 extern "C" int kl_rmsnorm_bwd(int rows, int d, float eps, const float* x, const float* gain, const float* dy,
                               float* dx, float* dgain, void* stream) {
   if (d <= 0) return KL_OK;
-  if (d > 8 * 256) { set_error("kl_rmsnorm_bwd: d %d > 2048", d); return KL_EUNSUPPORTED; }
-  rmsnorm_bwd_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(rows, d, eps, x, gain, dy, dx, dgain);
+  if (rows > 8192) { set_error("kl_rmsnorm_bwd: rows %d > 8192", rows); return KL_EUNSUPPORTED; }
+  const size_t sm = 2 * (size_t)std::max(rows, 1) * sizeof(float);
+  if (sm > 48 * 1024) cudaFuncSetAttribute(rmsnorm_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  launch_k(rmsnorm_bwd_kernel, 1, 256, sm, (cudaStream_t)stream, rows, d, eps, x, gain, dy, dx, dgain);
   count_launch();
   return launch_check("rmsnorm_bwd");
 }
@@ -376,8 +488,8 @@ extern "C" int kl_recent_rows_fwd(int B, int T, int d, int n, int dtype, const v
   long long tot = (long long)B * n * d;
   if (tot == 0) return KL_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  if (dtype == KL_F32) recent_fwd_kernel<float><<<nblk(tot), 256, 0, s>>>(B, T, d, n, (const float*)S, s_bs, lengths, (float*)out, o_bs);
-  else recent_fwd_kernel<bf16><<<nblk(tot), 256, 0, s>>>(B, T, d, n, (const bf16*)S, s_bs, lengths, (bf16*)out, o_bs);
+  if (dtype == KL_F32) launch_k(recent_fwd_kernel<float>, nblk(tot), 256, 0, s, B, T, d, n, (const float*)S, s_bs, lengths, (float*)out, o_bs);
+  else launch_k(recent_fwd_kernel<bf16>, nblk(tot), 256, 0, s, B, T, d, n, (const bf16*)S, s_bs, lengths, (bf16*)out, o_bs);
   count_launch();
   return launch_check("recent_rows_fwd");
 }
@@ -387,19 +499,25 @@ extern "C" int kl_recent_rows_bwd(int B, int T, int d, int n, int dtype, const v
   long long tot = (long long)B * n * d;
   if (tot == 0) return KL_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  if (dtype == KL_F32) recent_bwd_kernel<float><<<nblk(tot), 256, 0, s>>>(B, T, d, n, (const float*)dout, o_bs, lengths, (float*)dS, s_bs);
-  else recent_bwd_kernel<bf16><<<nblk(tot), 256, 0, s>>>(B, T, d, n, (const bf16*)dout, o_bs, lengths, (bf16*)dS, s_bs);
+  if (dtype == KL_F32) launch_k(recent_bwd_kernel<float>, nblk(tot), 256, 0, s, B, T, d, n, (const float*)dout, o_bs, lengths, (float*)dS, s_bs);
+  else launch_k(recent_bwd_kernel<bf16>, nblk(tot), 256, 0, s, B, T, d, n, (const bf16*)dout, o_bs, lengths, (bf16*)dS, s_bs);
   count_launch();
   return launch_check("recent_rows_bwd");
 }
 
 extern "C" int kl_gram_triu_fwd(int B, int n, int d, int dtype, const void* x, long long x_rs, long long x_bs,
                                 void* tri, long long t_bs, void* stream) {
-  long long tot = (long long)B * n * (n + 1) / 2;
-  if (tot == 0) return KL_OK;
+  if ((long long)B * n == 0) return KL_OK;
+  const size_t sm = (size_t)n * d * sizeof(float);
+  if (sm > 200 * 1024) { set_error("kl_gram_triu_fwd: n*d = %d too large", n * d); return KL_EUNSUPPORTED; }
   cudaStream_t s = (cudaStream_t)stream;
-  if (dtype == KL_F32) gram_triu_fwd_kernel<float><<<nblk(tot), 256, 0, s>>>(B, n, d, (const float*)x, x_rs, x_bs, (float*)tri, t_bs);
-  else gram_triu_fwd_kernel<bf16><<<nblk(tot), 256, 0, s>>>(B, n, d, (const bf16*)x, x_rs, x_bs, (bf16*)tri, t_bs);
+  if (dtype == KL_F32) {
+    cudaFuncSetAttribute(gram_triu_fwd_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    launch_k(gram_triu_fwd_kernel<float>, B, 256, sm, s, n, d, (const float*)x, x_rs, x_bs, (float*)tri, t_bs);
+  } else {
+    cudaFuncSetAttribute(gram_triu_fwd_kernel<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    launch_k(gram_triu_fwd_kernel<bf16>, B, 256, sm, s, n, d, (const bf16*)x, x_rs, x_bs, (bf16*)tri, t_bs);
+  }
   count_launch();
   return launch_check("gram_triu_fwd");
 }
@@ -407,13 +525,19 @@ extern "C" int kl_gram_triu_fwd(int B, int n, int d, int dtype, const void* x, l
 extern "C" int kl_gram_triu_bwd(int B, int n, int d, int dtype, const void* x, long long x_rs, long long x_bs,
                                 const void* dtri, long long t_bs, void* dx, long long dx_rs, long long dx_bs,
                                 void* stream) {
-  long long tot = (long long)B * n * d;
-  if (tot == 0) return KL_OK;
+  if ((long long)B * n * d == 0) return KL_OK;
+  const size_t sm = ((size_t)n * d + (size_t)n * n) * sizeof(float);
+  if (sm > 200 * 1024) { set_error("kl_gram_triu_bwd: n*d = %d too large", n * d); return KL_EUNSUPPORTED; }
   cudaStream_t s = (cudaStream_t)stream;
-  if (dtype == KL_F32)
-    gram_triu_bwd_kernel<float><<<nblk(tot), 256, 0, s>>>(B, n, d, (const float*)x, x_rs, x_bs, (const float*)dtri, t_bs, (float*)dx, dx_rs, dx_bs);
-  else
-    gram_triu_bwd_kernel<bf16><<<nblk(tot), 256, 0, s>>>(B, n, d, (const bf16*)x, x_rs, x_bs, (const bf16*)dtri, t_bs, (bf16*)dx, dx_rs, dx_bs);
+  if (dtype == KL_F32) {
+    cudaFuncSetAttribute(gram_triu_bwd_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    launch_k(gram_triu_bwd_kernel<float>, B, 256, sm, s, n, d, (const float*)x, x_rs, x_bs, (const float*)dtri, t_bs,
+                                                    (float*)dx, dx_rs, dx_bs);
+  } else {
+    cudaFuncSetAttribute(gram_triu_bwd_kernel<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    launch_k(gram_triu_bwd_kernel<bf16>, B, 256, sm, s, n, d, (const bf16*)x, x_rs, x_bs, (const bf16*)dtri, t_bs,
+                                                   (bf16*)dx, dx_rs, dx_bs);
+  }
   count_launch();
   return launch_check("gram_triu_bwd");
 }
@@ -425,9 +549,9 @@ extern "C" int kl_gated_sum_fwd(int rows, int d, int dtype, const void* x, long 
   if (tot == 0) return KL_OK;
   cudaStream_t s = (cudaStream_t)stream;
   if (dtype == KL_F32)
-    gated_fwd_kernel<float><<<nblk(tot), 256, 0, s>>>(rows, d, (const float*)x, x_rs, (const float*)deep, (const float*)dot, gd, gt, (float*)out, o_rs);
+    launch_k(gated_fwd_kernel<float>, nblk(tot), 256, 0, s, rows, d, (const float*)x, x_rs, (const float*)deep, (const float*)dot, gd, gt, (float*)out, o_rs);
   else
-    gated_fwd_kernel<bf16><<<nblk(tot), 256, 0, s>>>(rows, d, (const bf16*)x, x_rs, (const bf16*)deep, (const bf16*)dot, gd, gt, (bf16*)out, o_rs);
+    launch_k(gated_fwd_kernel<bf16>, nblk(tot), 256, 0, s, rows, d, (const bf16*)x, x_rs, (const bf16*)deep, (const bf16*)dot, gd, gt, (bf16*)out, o_rs);
   count_launch();
   return launch_check("gated_sum_fwd");
 }
@@ -440,16 +564,16 @@ extern "C" int kl_gated_sum_bwd(int rows, int d, int dtype, const void* g, long 
   int nb = (int)std::min<long long>(512, (tot + 255) / 256);
   if (nb < 1) nb = 1;
   if (dtype == KL_F32)
-    gated_bwd_kernel<float><<<nb, 256, 0, s>>>(rows, d, (const float*)g, g_rs, (const float*)deep, (const float*)dot, gd, gt, (float*)ddeep, (float*)ddot, (double*)scratch);
+    launch_k(gated_bwd_kernel<float>, nb, 256, 0, s, rows, d, (const float*)g, g_rs, (const float*)deep, (const float*)dot, gd, gt, (float*)ddeep, (float*)ddot, (double*)scratch);
   else
-    gated_bwd_kernel<bf16><<<nb, 256, 0, s>>>(rows, d, (const bf16*)g, g_rs, (const bf16*)deep, (const bf16*)dot, gd, gt, (bf16*)ddeep, (bf16*)ddot, (double*)scratch);
-  reduce_pairs_kernel<<<1, 256, 0, s>>>(nb, (const double*)scratch, dgd, dgt);
+    launch_k(gated_bwd_kernel<bf16>, nb, 256, 0, s, rows, d, (const bf16*)g, g_rs, (const bf16*)deep, (const bf16*)dot, gd, gt, (bf16*)ddeep, (bf16*)ddot, (double*)scratch);
+  launch_k(reduce_pairs_kernel, 1, 256, 0, s, nb, (const double*)scratch, dgd, dgt);
   count_launch(2);
   return launch_check("gated_sum_bwd");
 }
 
 extern "C" int kl_bce_fwd_bwd(int n, const float* z, const float* y, float* loss, float* dz, void* stream) {
-  bce_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(n, z, y, loss, dz);
+  launch_k(bce_kernel, 1, 256, 0, (cudaStream_t)stream, n, z, y, loss, dz);
   count_launch();
   return launch_check("bce");
 }
@@ -458,10 +582,10 @@ extern "C" int kl_cast(long long n, int dtype_in, const void* x, int dtype_out, 
   if (n == 0) return KL_OK;
   cudaStream_t s = (cudaStream_t)stream;
   unsigned g = (unsigned)std::min<long long>((n + 255) / 256, 148 * 16);
-  if (dtype_in == KL_F32 && dtype_out == KL_BF16) cast_kernel<float, bf16><<<g, 256, 0, s>>>(n, (const float*)x, (bf16*)y);
-  else if (dtype_in == KL_BF16 && dtype_out == KL_F32) cast_kernel<bf16, float><<<g, 256, 0, s>>>(n, (const bf16*)x, (float*)y);
-  else if (dtype_in == KL_F32) cast_kernel<float, float><<<g, 256, 0, s>>>(n, (const float*)x, (float*)y);
-  else cast_kernel<bf16, bf16><<<g, 256, 0, s>>>(n, (const bf16*)x, (bf16*)y);
+  if (dtype_in == KL_F32 && dtype_out == KL_BF16) launch_k(cast_kernel<float, bf16>, g, 256, 0, s, n, (const float*)x, (bf16*)y);
+  else if (dtype_in == KL_BF16 && dtype_out == KL_F32) launch_k(cast_kernel<bf16, float>, g, 256, 0, s, n, (const bf16*)x, (float*)y);
+  else if (dtype_in == KL_F32) launch_k(cast_kernel<float, float>, g, 256, 0, s, n, (const float*)x, (float*)y);
+  else launch_k(cast_kernel<bf16, bf16>, g, 256, 0, s, n, (const bf16*)x, (bf16*)y);
   count_launch();
   return launch_check("cast");
 }
@@ -476,8 +600,8 @@ extern "C" int kl_act_fwd(int rows, int cols, int dtype, const void* x, long lon
   ac.group = act_group > 0 ? act_group : 1;
   for (int i = 0; i < n_act; ++i) ac.codes[i] = codes[i];
   cudaStream_t s = (cudaStream_t)stream;
-  if (dtype == KL_F32) act_kernel<float><<<nblk(tot), 256, 0, s>>>(rows, cols, (const float*)x, ld, (float*)y, ld_y, ac);
-  else act_kernel<bf16><<<nblk(tot), 256, 0, s>>>(rows, cols, (const bf16*)x, ld, (bf16*)y, ld_y, ac);
+  if (dtype == KL_F32) launch_k(act_kernel<float>, nblk(tot), 256, 0, s, rows, cols, (const float*)x, ld, (float*)y, ld_y, ac);
+  else launch_k(act_kernel<bf16>, nblk(tot), 256, 0, s, rows, cols, (const bf16*)x, ld, (bf16*)y, ld_y, ac);
   count_launch();
   return launch_check("act_fwd");
 }
@@ -492,8 +616,8 @@ extern "C" int kl_act_bwd(int rows, int cols, int dtype, const void* g, long lon
   ac.group = act_group > 0 ? act_group : 1;
   for (int i = 0; i < n_act; ++i) ac.codes[i] = codes[i];
   cudaStream_t s = (cudaStream_t)stream;
-  if (dtype == KL_F32) act_bwd_kernel<float><<<nblk(tot), 256, 0, s>>>(rows, cols, (const float*)g, ldg, (const float*)x, ldx, (float*)y, ld_y, ac);
-  else act_bwd_kernel<bf16><<<nblk(tot), 256, 0, s>>>(rows, cols, (const bf16*)g, ldg, (const bf16*)x, ldx, (bf16*)y, ld_y, ac);
+  if (dtype == KL_F32) launch_k(act_bwd_kernel<float>, nblk(tot), 256, 0, s, rows, cols, (const float*)g, ldg, (const float*)x, ldx, (float*)y, ld_y, ac);
+  else launch_k(act_bwd_kernel<bf16>, nblk(tot), 256, 0, s, rows, cols, (const bf16*)g, ldg, (const bf16*)x, ldx, (bf16*)y, ld_y, ac);
   count_launch();
   return launch_check("act_bwd");
 }
@@ -502,8 +626,8 @@ extern "C" int kl_check_finite(long long n, int dtype, const void* x, unsigned i
   if (n == 0) return KL_OK;
   cudaStream_t s = (cudaStream_t)stream;
   unsigned g = (unsigned)std::min<long long>((n + 255) / 256, 148 * 8);
-  if (dtype == KL_F32) finite_kernel<float><<<g, 256, 0, s>>>(n, (const float*)x, flag);
-  else finite_kernel<bf16><<<g, 256, 0, s>>>(n, (const bf16*)x, flag);
+  if (dtype == KL_F32) launch_k(finite_kernel<float>, g, 256, 0, s, n, (const float*)x, flag);
+  else launch_k(finite_kernel<bf16>, g, 256, 0, s, n, (const bf16*)x, flag);
   count_launch();
   return launch_check("check_finite");
 }
@@ -518,6 +642,7 @@ namespace {
 // the bias corrections are computed per block from *step_dev.
 __global__ void adam_kernel(long long n, float lr, float b1, float b2, float eps, int step, const int* step_dev,
                             float* w, const float* g, float* m, float* v, bf16* wc) {
+  KL_PDL_ENTRY();
   const int t = step_dev ? *step_dev : step;
   const float c1 = 1.f / (1.f - powf(b1, (float)t));
   const float c2 = 1.f / (1.f - powf(b2, (float)t));
@@ -557,7 +682,8 @@ __global__ void adam_kernel(long long n, float lr, float b1, float b2, float eps
   }
 }
 
-__global__ void tick_kernel(int* step_dev) { *step_dev += 1; }
+__global__ void tick_kernel(int* step_dev) {
+  KL_PDL_ENTRY(); *step_dev += 1; }
 }  // namespace
 }  // namespace kl
 
@@ -570,9 +696,9 @@ extern "C" int kl_adam_step(long long n, float lr, float beta1, float beta2, flo
     return KL_EBADSHAPE;
   }
   cudaStream_t s = (cudaStream_t)stream;
-  if (step_dev) tick_kernel<<<1, 1, 0, s>>>(step_dev);
+  if (step_dev) launch_k(tick_kernel, 1, 1, 0, s, step_dev);
   unsigned grid = (unsigned)std::min<long long>((n / 4 + 255) / 256 + 1, 148 * 8);
-  adam_kernel<<<grid, 256, 0, s>>>(n, lr, beta1, beta2, eps, step, step_dev, w, g, m, v, (bf16*)w_bf16);
+  launch_k(adam_kernel, grid, 256, 0, s, n, lr, beta1, beta2, eps, step, step_dev, w, g, m, v, (bf16*)w_bf16);
   count_launch(step_dev ? 2 : 1);
   return launch_check("adam_step");
 }

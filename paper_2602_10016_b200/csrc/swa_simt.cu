@@ -22,6 +22,7 @@ __device__ __forceinline__ bool key_ok(int qi, int kj, int len, int hi, int w, i
 
 template <typename T, int DH>
 __global__ void __launch_bounds__(256) swa_fwd_kernel(SwaP p) {
+  KL_PDL_ENTRY();
   extern __shared__ float sm[];
   constexpr int LD = DH + 1;
   float* Qs = sm;
@@ -101,6 +102,7 @@ __global__ void __launch_bounds__(256) swa_fwd_kernel(SwaP p) {
 
 template <typename T, int DH>
 __global__ void swa_rowdot_kernel(SwaP p) {
+  KL_PDL_ENTRY();
   // D[b,h,t] = sum_c dO * O (the softmax-VJP inner product, tensor.py:501-503)
   long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   long long total = (long long)p.B * p.H * p.T;
@@ -118,6 +120,7 @@ __global__ void swa_rowdot_kernel(SwaP p) {
 
 template <typename T, int DH>
 __global__ void __launch_bounds__(256) swa_bwd_dkv_kernel(SwaP p) {
+  KL_PDL_ENTRY();
   extern __shared__ float sm[];
   constexpr int LD = DH + 1;
   float* Ks = sm;
@@ -207,6 +210,7 @@ __global__ void __launch_bounds__(256) swa_bwd_dkv_kernel(SwaP p) {
 
 template <typename T, int DH>
 __global__ void __launch_bounds__(256) swa_bwd_dq_kernel(SwaP p) {
+  KL_PDL_ENTRY();
   extern __shared__ float sm[];
   constexpr int LD = DH + 1;
   float* Qs = sm;
@@ -275,6 +279,7 @@ __global__ void __launch_bounds__(256) swa_bwd_dq_kernel(SwaP p) {
 }
 
 __global__ void swa_support_kernel(SwaP p, int* support) {
+  KL_PDL_ENTRY();
   long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (long long)p.B * p.T) return;
   const int b = idx / p.T, qi = idx % p.T;
@@ -294,7 +299,7 @@ int launch_fwd(const SwaP& p, cudaStream_t s) {
   const size_t smem = (3 * TQ * (DH + 1) + TQ * (TQ + 1)) * sizeof(float);
   cudaFuncSetAttribute(swa_fwd_kernel<T, DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   dim3 grid((p.T + TQ - 1) / TQ, p.H, p.B);
-  swa_fwd_kernel<T, DH><<<grid, 256, smem, s>>>(p);
+  launch_k(swa_fwd_kernel<T, DH>, grid, 256, smem, s, p);
   count_launch();
   return launch_check("swa_fwd_simt");
 }
@@ -302,14 +307,14 @@ int launch_fwd(const SwaP& p, cudaStream_t s) {
 template <typename T, int DH>
 int launch_bwd(const SwaP& p, cudaStream_t s) {
   long long total = (long long)p.B * p.H * p.T;
-  swa_rowdot_kernel<T, DH><<<(unsigned)((total + 255) / 256), 256, 0, s>>>(p);
+  launch_k(swa_rowdot_kernel<T, DH>, (unsigned)((total + 255) / 256), 256, 0, s, p);
   const size_t smem1 = (4 * TQ * (DH + 1) + 2 * TQ * (TQ + 1) + 2 * TQ) * sizeof(float);
   cudaFuncSetAttribute(swa_bwd_dkv_kernel<T, DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
   dim3 grid((p.T + TQ - 1) / TQ, p.H, p.B);
-  swa_bwd_dkv_kernel<T, DH><<<grid, 256, smem1, s>>>(p);
+  launch_k(swa_bwd_dkv_kernel<T, DH>, grid, 256, smem1, s, p);
   const size_t smem2 = (4 * TQ * (DH + 1) + TQ * (TQ + 1)) * sizeof(float);
   cudaFuncSetAttribute(swa_bwd_dq_kernel<T, DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
-  swa_bwd_dq_kernel<T, DH><<<grid, 256, smem2, s>>>(p);
+  launch_k(swa_bwd_dq_kernel<T, DH>, grid, 256, smem2, s, p);
   count_launch(3);
   return launch_check("swa_bwd_simt");
 }
@@ -354,7 +359,7 @@ int swa_bwd_simt(const SwaP& p, cudaStream_t s) {
 
 int swa_support(const SwaP& p, int* support, cudaStream_t s) {
   long long total = (long long)p.B * p.T;
-  swa_support_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(p, support);
+  launch_k(swa_support_kernel, (unsigned)((total + 255) / 256), 256, 0, s, p, support);
   count_launch();
   return launch_check("swa_support");
 }
@@ -367,6 +372,7 @@ namespace kl {
 // elements (16-byte loads, the warp reads the row's 512 B... H*128 B), the 8 lanes
 // of a head reduce with shuffles.  Coalesced; one pass over O and dO.
 __global__ void swa_rowdot_bf16_h64(SwaP p) {
+  KL_PDL_ENTRY();
   const long long row = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= (long long)p.B * p.T) return;
   const int lane = threadIdx.x & 31;
@@ -402,11 +408,11 @@ int swa_rowdot(const SwaP& p, cudaStream_t s) {
                    ((uintptr_t)p.O & 15) == 0 && ((uintptr_t)p.dO & 15) == 0;
   if (vec) {
     const long long rows = (long long)p.B * p.T;
-    swa_rowdot_bf16_h64<<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(p);
+    launch_k(swa_rowdot_bf16_h64, (unsigned)((rows + 7) / 8), 256, 0, s, p);
   } else if (p.dtype == KL_BF16 && p.d_h == 64) {
-    swa_rowdot_kernel<bf16, 64><<<g, 256, 0, s>>>(p);
+    launch_k(swa_rowdot_kernel<bf16, 64>, g, 256, 0, s, p);
   } else if (p.dtype == KL_F32 && p.d_h == 64) {
-    swa_rowdot_kernel<float, 64><<<g, 256, 0, s>>>(p);
+    launch_k(swa_rowdot_kernel<float, 64>, g, 256, 0, s, p);
   } else {
     set_error("swa_rowdot: unsupported head dim %d", p.d_h);
     return KL_EUNSUPPORTED;

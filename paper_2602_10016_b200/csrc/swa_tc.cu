@@ -115,6 +115,7 @@ __device__ __forceinline__ void zero_rows(bf16* base, long long ld, int r0, int 
 
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(NT, 1) swa_fwd_tc_kernel(const __grid_constant__ CUtensorMap tq, SwaP p) {
+  KL_PDL_ENTRY();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sQ = sm;
@@ -234,6 +235,7 @@ __global__ void __launch_bounds__(NT, 1) swa_fwd_tc_kernel(const __grid_constant
 // dK, dV for one 128-key block.
 __global__ void __launch_bounds__(NT, 1)
     swa_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tdo, SwaP p) {
+  KL_PDL_ENTRY();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sK = sm;
@@ -366,6 +368,7 @@ __global__ void __launch_bounds__(NT, 1)
 // dQ for one 128-query block.
 __global__ void __launch_bounds__(NT, 1)
     swa_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tdo, SwaP p) {
+  KL_PDL_ENTRY();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sQ = sm;
@@ -526,13 +529,16 @@ __device__ __forceinline__ float ex2(float x) {
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
 
 __global__ void __launch_bounds__(NT2, 1) swa_fwd_tc2_kernel(const __grid_constant__ CUtensorMap tq, SwaP p) {
+  KL_PDL_ENTRY();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sQ = sm;                       // 2 x 16 KB
   uint8_t* sKV = sQ + 2 * TILE;           // KVS x (K 16 KB | V 16 KB)
   uint8_t* sP = sKV + KVS * 2 * TILE;     // 2 x 32 KB
-  float* red = (float*)(sP + 2 * PBLK);   // [2 halves][128 rows] max, then sum
-  uint64_t* bar = (uint64_t*)(red + 2 * TB);
+  // [2 halves][128 rows] max, then sum: a static array so the compiler emits
+  // LDS/STS (pointers derived from the aligned dynamic base are generic)
+  __shared__ float red[2 * TB];
+  uint64_t* bar = (uint64_t*)(sP + 2 * PBLK);
   uint64_t* q_full = bar;        // [2]
   uint64_t* q_empty = bar + 2;   // [2]
   uint64_t* kv_full = bar + 4;   // [3]
@@ -790,7 +796,7 @@ __global__ void __launch_bounds__(NT2, 1) swa_fwd_tc2_kernel(const __grid_consta
   if (warp == 1) tc::tmem_dealloc(tmem, 512);
 }
 
-size_t smem_bytes() { return 1024 + 2 * TILE + KVS * 2 * TILE + 2 * PBLK + 2 * TB * 4 + 18 * 8 + 16; }
+size_t smem_bytes() { return 1024 + 2 * TILE + KVS * 2 * TILE + 2 * PBLK + 18 * 8 + 16; }
 
 // ---------------------------------------------------------------------------
 // dQ v2: persistent over query blocks (same item order and K/V ring as the
@@ -800,6 +806,7 @@ size_t smem_bytes() { return 1024 + 2 * TILE + KVS * 2 * TILE + 2 * PBLK + 2 * T
 // into a 2-slot ring, and dQ += dS K_j accumulates in TMEM.
 __global__ void __launch_bounds__(NT2, 1)
     swa_bwd_dq_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tdo, SwaP p) {
+  KL_PDL_ENTRY();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sQG = sm;                      // 2 x (Q 16 KB | dO 16 KB)
@@ -1049,14 +1056,15 @@ size_t dq_smem_bytes() { return 1024 + 4 * TILE + KVS * 2 * TILE + 2 * PBLK + 18
 // block are staged in smem by the compute warps.
 __global__ void __launch_bounds__(NT2, 1)
     swa_bwd_dkv_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tdo, SwaP p) {
+  KL_PDL_ENTRY();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sKVb = sm;                      // K 16 KB | V 16 KB
   uint8_t* sQG = sKVb + 2 * TILE;          // KVS x (Q | dO)
   uint8_t* sPT = sQG + KVS * 2 * TILE;     // 32 KB
   uint8_t* sDT = sPT + PBLK;               // 32 KB
-  float* sLD = (float*)(sDT + PBLK);       // 2 x (lse[128] | D[128])
-  uint64_t* bar = (uint64_t*)(sLD + 4 * TB);
+  __shared__ __align__(16) float sLD[4 * TB];  // 2 x (lse[128] | D[128]), static: LDS.128 broadcasts
+  uint64_t* bar = (uint64_t*)(sDT + PBLK);
   uint64_t* kv_full = bar;
   uint64_t* kv_empty = bar + 1;
   uint64_t* qg_full = bar + 2;   // [3]
@@ -1225,18 +1233,21 @@ __global__ void __launch_bounds__(NT2, 1)
       if (key >= len) qhi = -1;
       const float* LSE = p.LSE + ((long long)b * p.H + h) * p.T;
       const float* D = p.Dbuf + ((long long)b * p.H + h) * p.T;
+      // thread ctid < 128 stages LSE (log2 units), the others D, of one query
+      // row; the next block's value is loaded while this block is processed
+      auto ld_ld = [&](int ii) {
+        const int q = (lo + ii) * TB + (ctid & (TB - 1));
+        if (ctid < TB) return q < len ? LSE[q] * 1.4426950408889634f : INFINITY;
+        return q < len ? D[q] : 0.f;
+      };
+      float nxt = ld_ld(0);
       for (int ii = 0; ii < n; ++ii) {
         const int qb0 = (lo + ii) * TB;
         float* ls = sLD + (pdc & 1) * 2 * TB;
         float* dd = ls + TB;
-        if (ctid < TB) {
-          const int q = qb0 + ctid;
-          ls[ctid] = q < len ? LSE[q] * 1.4426950408889634f : INFINITY;
-        } else {
-          const int q = qb0 + ctid - TB;
-          dd[ctid - TB] = q < len ? D[q] : 0.f;
-        }
+        ls[ctid] = nxt;  // ctid >= TB lands in dd
         named_bar(1, 256);
+        if (ii + 1 < n) nxt = ld_ld(ii + 1);
         tc::mbar_wait(sdp_full, sdp & 1);
         tc::mbar_wait(pd_empty, (pdc & 1) ^ 1);
         tc::fence_after();
@@ -1328,7 +1339,7 @@ __global__ void __launch_bounds__(NT2, 1)
   if (warp == 1) tc::tmem_dealloc(tmem, 512);
 }
 
-size_t dkv_smem_bytes() { return 1024 + 2 * TILE + KVS * 2 * TILE + 2 * PBLK + 4 * TB * 4 + 14 * 8 + 16; }
+size_t dkv_smem_bytes() { return 1024 + 2 * TILE + KVS * 2 * TILE + 2 * PBLK + 14 * 8 + 16; }
 
 }  // namespace v2
 
@@ -1361,13 +1372,13 @@ int swa_fwd_tc(const SwaP& p, cudaStream_t s) {
     const size_t smem = 1024 + 7 * TILE + 3 * PBLK + 64 + 16;
     cudaFuncSetAttribute(swa_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     dim3 grid((p.T + TB - 1) / TB, p.H, p.B);
-    swa_fwd_tc_kernel<<<grid, NT, smem, s>>>(tq, p);
+    launch_k(swa_fwd_tc_kernel, grid, NT, smem, s, tq, p);
   } else {
     const size_t smem = v2::smem_bytes();
     cudaFuncSetAttribute(v2::swa_fwd_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int W = p.B * p.H * ((p.T + TB - 1) / TB);
     const int grid = std::min(W, tc_num_sms());
-    v2::swa_fwd_tc2_kernel<<<grid, v2::NT2, smem, s>>>(tq, p);
+    launch_k(v2::swa_fwd_tc2_kernel, grid, v2::NT2, smem, s, tq, p);
   }
   count_launch();
   return launch_check("swa_fwd_tc");
@@ -1385,19 +1396,19 @@ int swa_bwd_tc(const SwaP& p, cudaStream_t s) {
     const int grid = std::min(W, tc_num_sms());
     const size_t s1 = v2::dkv_smem_bytes(), s2 = v2::dq_smem_bytes();
     cudaFuncSetAttribute(v2::swa_bwd_dkv_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1);
-    v2::swa_bwd_dkv_tc2_kernel<<<grid, v2::NT2, s1, s>>>(tq, tdo, p);
+    launch_k(v2::swa_bwd_dkv_tc2_kernel, grid, v2::NT2, s1, s, tq, tdo, p);
     cudaFuncSetAttribute(v2::swa_bwd_dq_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2);
-    v2::swa_bwd_dq_tc2_kernel<<<grid, v2::NT2, s2, s>>>(tq, tdo, p);
+    launch_k(v2::swa_bwd_dq_tc2_kernel, grid, v2::NT2, s2, s, tq, tdo, p);
     count_launch(2);
     return launch_check("swa_bwd_tc2");
   }
   dim3 grid((p.T + TB - 1) / TB, p.H, p.B);
   const size_t smem1 = 1024 + 8 * TILE + 2 * PBLK + 6 * TB * 4 + 64 + 16;
   cudaFuncSetAttribute(swa_bwd_dkv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
-  swa_bwd_dkv_tc_kernel<<<grid, NT, smem1, s>>>(tq, tdo, p);
+  launch_k(swa_bwd_dkv_tc_kernel, grid, NT, smem1, s, tq, tdo, p);
   const size_t smem2 = 1024 + 8 * TILE + PBLK + 64 + 16;
   cudaFuncSetAttribute(swa_bwd_dq_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
-  swa_bwd_dq_tc_kernel<<<grid, NT, smem2, s>>>(tq, tdo, p);
+  launch_k(swa_bwd_dq_tc_kernel, grid, NT, smem2, s, tq, tdo, p);
   count_launch(2);
   return launch_check("swa_bwd_tc");
 }

@@ -328,15 +328,20 @@ class _HspPool(torch.autograd.Function):
     """Seed/CLS-query cross-attention pooling with keys = values = S
     (hsp_seed_attend / pma, seqsum.py:26-34, 96-102, reassociated as
     P = softmax_t(S Q^T), pooled = P^T S — SURVEY.md §7.3 item 7).
-    Q (HQ, d) is batch-shared and pre-scaled by 1/sqrt(d_h).  Length-0
-    samples pool to zeros with no gradient (seqsum.py:32-33, 99-100)."""
+    Q (HQ, d) is batch-shared, pre-scaled by 1/sqrt(d_h), rows ordered
+    (query, head) so every pooled output (B, n, H, d) flattens to rows
+    (b, query) with one stride.  ``splits`` cuts the HQ query rows into
+    separately stored outputs (seed set, CLS set).  Length-0 samples pool to
+    zeros with no gradient (seqsum.py:32-33, 99-100)."""
 
     @staticmethod
-    def forward(ctx, S, Q32, lengths):
+    def forward(ctx, S, Q32, lengths, splits):
         # Q arrives in fp32 (the batch-shared query path is computed in fp32);
         # the T-length GEMMs run in S's dtype and dQ is returned in fp32.
         B, T, d = S.shape
         HQ = Q32.shape[0]
+        if sum(splits) != HQ:
+            raise ShapeError(f"query splits {splits} do not cover {HQ} rows")
         Q = Q32
         if Q32.dtype != S.dtype:
             Q = torch.empty(Q32.shape, device=S.device, dtype=S.dtype)
@@ -346,26 +351,43 @@ class _HspPool(torch.autograd.Function):
         Pm = torch.empty(B, T, HQ, device=S.device, dtype=S.dtype)
         a = _colsm_args(sc, Pm, lengths)
         _capi.call("kl_colsoftmax_fwd", C.byref(a), _stream())
-        pooled = gemm(Pm.transpose(1, 2), S)  # (B, HQ, d)
-        ctx.save_for_backward(S, Q, lengths, Pm)
-        return pooled
+        outs, c0 = [], 0
+        for n in splits:
+            outs.append(gemm(Pm[:, :, c0:c0 + n].transpose(1, 2), S))  # (B, n, d)
+            c0 += n
+        ctx.save_for_backward(S, Q, lengths, Pm, *outs)
+        ctx.splits = tuple(splits)
+        return tuple(outs)
 
     @staticmethod
-    def backward(ctx, g):
-        S, Q, lengths, Pm = ctx.saved_tensors
-        g = g.contiguous()
-        dP = gemm(S, g.transpose(1, 2), out_dtype=torch.float32)  # (B, T, HQ)
+    def backward(ctx, *gs):
+        S, Q, lengths, Pm, *outs = ctx.saved_tensors
+        B, T, d = S.shape
+        HQ = Q.shape[0]
+        dP = torch.empty(B, T, HQ, device=S.device, dtype=torch.float32)
+        # D[b, c] = sum_t P dP = dO[c] . pooled[c]: the softmax-VJP column term
+        # from the (B, HQ, d) pooled output instead of a pass over T
+        Dcol = torch.empty(B, HQ, device=S.device, dtype=torch.float32)
+        dS = None
+        c0 = 0
+        for g, n, o in zip(gs, ctx.splits, outs):
+            g = torch.zeros(B, n, d, device=S.device, dtype=S.dtype) if g is None else g.contiguous()
+            Dcol[:, c0:c0 + n] = torch.linalg.vecdot(g.float(), o.float())
+            gemm(S, g.transpose(1, 2), dP[:, :, c0:c0 + n])
+            if dS is None:
+                dS = gemm(Pm[:, :, c0:c0 + n], g)
+            else:
+                gemm(Pm[:, :, c0:c0 + n], g, dS, beta=1.0)
+            c0 += n
         dsc = torch.empty_like(Pm)
         lo = torch.empty_like(Pm) if Pm.dtype != torch.float32 else None
         a = _colsm_args(dsc, Pm, lengths)  # dtype_in = dsc dtype, dtype_out = P dtype
         a.dP, a.dp_rs, a.dp_bs = dP.data_ptr(), dP.stride(1), dP.stride(0)
         a.dX, a.dx_rs, a.dx_bs = dsc.data_ptr(), dsc.stride(1), dsc.stride(0)
         a.dX_lo = lo.data_ptr() if lo is not None else None
-        if Pm.dtype == dP.dtype:
-            _capi.call("kl_colsoftmax_bwd", C.byref(a), _stream())
-        else:
-            _colsm_bwd_mixed(a, Pm, dP, dsc)
-        dS = gemm(Pm, g)
+        a.dtype_dp = _capi.dt(dP)
+        a.Dcol = Dcol.data_ptr() if HSP_DCOL else None
+        _capi.call("kl_colsoftmax_bwd", C.byref(a), _stream())
         gemm(dsc, Q.unsqueeze(0).expand(S.shape[0], -1, -1), dS, beta=1.0)
         # dQ = sum_b dsc^T S: softmax-VJP rows sum to zero over t, so this
         # reduction cancels; bf16 runs it on the hi + lo split of dsc.
@@ -374,22 +396,16 @@ class _HspPool(torch.autograd.Function):
         if lo is not None:
             gemm(lo.transpose(1, 2).unsqueeze(0), S.unsqueeze(0), dQ, beta=1.0, reduce=(False, True))
         dQ = dQ.reshape(Q.shape)
-        return dS, dQ, None
+        return dS, dQ, None, None
 
 
-def _colsm_bwd_mixed(a, Pm, dP, dsc):
-    # dP is fp32 while P is bf16: convert dP to P's dtype is lossy; instead run
-    # the kernel in fp32 on an fp32 copy of P (P is a probability; exact in fp32).
-    P32 = torch.empty(Pm.shape, device=Pm.device, dtype=torch.float32)
-    _capi.call("kl_cast", Pm.numel(), _capi.dt(Pm), Pm.data_ptr(), _capi.KL_F32, P32.data_ptr(), _stream())
-    a.P, a.p_rs, a.p_bs = P32.data_ptr(), P32.stride(1), P32.stride(0)
-    a.dtype_out = _capi.KL_F32
-    a.dtype_in = _capi.dt(dsc)
-    _capi.call("kl_colsoftmax_bwd", C.byref(a), _stream())
+HSP_DCOL = True  # softmax-VJP column term from the pooled output (tests A/B it against the t-reduction)
 
 
-def hsp_pool(S, Q, lengths):
-    return _HspPool.apply(S, Q, lengths)
+def hsp_pool(S, Q, lengths, splits=None):
+    """Pooled outputs, one (B, n, d) tensor per entry of ``splits`` (default:
+    all HQ rows in one)."""
+    return _HspPool.apply(S, Q, lengths, tuple(splits) if splits else (Q.shape[0],))
 
 
 # ---------------------------------------------------------------------------
@@ -584,15 +600,18 @@ def cast(x, dtype):
 
 class _HeadProj(torch.autograd.Function):
     """Per-head value projection + head concat of multi_head_attention
-    (attention.py:88-92): out[b, i, h*d_h + c] = sum_f X[b,h,i,f] W_h[c,f]."""
+    (attention.py:88-92) on pooled rows laid out (B, n, H, d):
+    out[b, i, h*d_h + c] = sum_f X[b,i,h,f] W_h[c,f].  One GEMM batched over
+    the H heads with M = B*n rows (row stride H*d)."""
 
     @staticmethod
     def forward(ctx, X, flat, wref):
-        B, H, n, d = X.shape
+        B, n, H, d = X.shape
         W = wref.w()  # (H, d_h, d)
         d_h = W.shape[1]
-        out = torch.empty(B, n, H, d_h, device=X.device, dtype=X.dtype)
-        gemm(X, W.transpose(1, 2), out.permute(0, 2, 1, 3))
+        X = X.contiguous()
+        out = torch.empty(B * n, H, d_h, device=X.device, dtype=X.dtype)
+        gemm(X.view(B * n, H, d).permute(1, 0, 2), W.transpose(1, 2), out.permute(1, 0, 2))
         ctx.save_for_backward(X)
         ctx.wref = wref
         return out.view(B, n, H * d_h)
@@ -600,14 +619,16 @@ class _HeadProj(torch.autograd.Function):
     @staticmethod
     def backward(ctx, g):
         (X,) = ctx.saved_tensors
-        B, H, n, d = X.shape
+        B, n, H, d = X.shape
         W = ctx.wref.w()
         d_h = W.shape[1]
-        gv = g.contiguous().view(B, n, H, d_h).permute(0, 2, 1, 3)
-        dX = gemm(gv, W.unsqueeze(0).expand(B, H, d_h, d))
-        gemm(gv.transpose(2, 3), X, ctx.wref.g().unsqueeze(0), beta=1.0, reduce=(True, False))
+        gv = g.contiguous().view(B * n, H, d_h).permute(1, 0, 2)  # (H, B*n, d_h)
+        dX = torch.empty_like(X)
+        gemm(gv, W, dX.view(B * n, H, d).permute(1, 0, 2))
+        gemm(gv.transpose(1, 2), X.view(B * n, H, d).permute(1, 0, 2), ctx.wref.g(), beta=1.0)
         return dX, None, None
 
 
 def head_proj(X, wref):
+    """X (B, n, H, d) -> (B, n, H*d_h)."""
     return _HeadProj.apply(X, wref.P.flat, wref)

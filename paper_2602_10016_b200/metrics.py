@@ -52,7 +52,8 @@ def layer_macs(cfg, flags, live_seq: bool = True, formulation: str = "executed",
                 # value + output projections; batch-shared query folding is
                 # amortised over the batch and omitted (< 0.1%).
                 out["hsp"] += 2 * T * d * H * n_q + n_q * d * d + n_q * d * d
-                out["sumkron"] += ev.rank * (n_s * d * d + n_tok * n_s * d)
+                # U = Zp X (n_tok*k x n_s x d), then U' W_stack (k*d -> d)
+                out["sumkron"] += ev.rank * (n_tok * n_s * d + n_tok * d * d)
             else:
                 out["hsp"] += (n_s * d * d + 2 * T * d * d + 2 * n_s * T * d + n_s * d * d)
                 if n_cls:

@@ -49,8 +49,8 @@ def seed_init_base(n_seeds: int, n_tokens: int) -> np.ndarray:
 @dataclass
 class HspParams:
     """Seeds, their RMSNorm gain, the seed-attention weights and the rank-k
-    compression pairs (seqsum.py:37-93).  Packed: ``zs`` (k, n_seeds,
-    n_tokens) and ``ws`` (k, d, d)."""
+    compression pairs (seqsum.py:37-93).  Packed: ``zs`` (n_tokens, k, n_seeds)
+    and ``ws`` (k, d, d)."""
 
     P: Params
     prefix: str
@@ -95,12 +95,14 @@ class HspParams:
         attn = MhaParams.create(params, f"{prefix}/attn", dim, heads, rng)
         base = seed_init_base(n_seeds, n_tokens)
         p = cls(params, prefix, attn, n_seeds, n_tokens, rank, dim)
-        params.block(p.zs, (rank, n_seeds, n_tokens))
+        # seq maps packed (n_tokens, k, n_seeds): as a (n_tokens*k, n_seeds)
+        # matrix, row (t, i) is Z_i[:, t] (the reassociated SumKron's A operand)
+        params.block(p.zs, (n_tokens, rank, n_seeds))
         params.block(p.ws, (rank, dim, dim))
         for i in range(rank):
             z = base / rank + rng.normal(0.0, 0.02, (n_seeds, n_tokens))
             w = np.eye(dim) + rng.normal(0.0, 0.02, (dim, dim))
-            params.add(f"{prefix}/kron{i}/seq_map", z, block=p.zs, index=i)
+            params.add(f"{prefix}/kron{i}/seq_map", z, block=p.zs, index=lambda v, i=i: v[:, i, :].t())
             params.add(f"{prefix}/kron{i}/emb_map", w, block=p.ws, index=i)
         return p
 
@@ -115,16 +117,20 @@ def hsp_queries(p: HspParams) -> torch.Tensor:
 
 
 def sumkronlinear(x: torch.Tensor, p: HspParams) -> torch.Tensor:
-    """Y = sum_i Z_i^T X W_i (seqsum.py:105-122) on (B, n_seeds, d)."""
+    """Y = sum_i Z_i^T X W_i (seqsum.py:105-122) on (B, n_seeds, d),
+    in the reference's order sum_i (Z_i^T X) W_i: U = Zp X per sample (Zp rows
+    (t, i) = Z_i[:, t]; M = n_tokens*k), then one GEMM of the rows
+    (b, t) of U, (B*n_tokens, k*d), with the stacked W_i (k*d, d)."""
     if x.shape[-2] != p.n_seeds or x.shape[-1] != p.dim:
         raise ShapeError(f"map shapes incompatible with input {tuple(x.shape)}")
     squeeze = x.dim() == 2
     if squeeze:
         x = x.unsqueeze(0)
     B = x.shape[0]
-    v = F.mm(x.unsqueeze(1), F.PRef(p.P, p.ws, lambda w: w.unsqueeze(0)))  # (B, k, n_s, d)
-    y = F.mm(F.PRef(p.P, p.zs, lambda z: z.transpose(1, 2).unsqueeze(0)), v, reduce=(False, True))
-    y = y.view(B, p.n_tokens, p.dim)
+    k, n_tok, n_s, d = p.rank, p.n_tokens, p.n_seeds, p.dim
+    u = F.mm(F.PRef(p.P, p.zs, lambda z: z.view(n_tok * k, n_s)), x)  # (B, n_tok*k, d)
+    y = F.mm(u.view(B * n_tok, k * d), F.PRef(p.P, p.ws, lambda w: w.view(k * d, d)))
+    y = y.view(B, n_tok, d)
     return y.squeeze(0) if squeeze else y
 
 
@@ -222,11 +228,15 @@ def hsp_summarize(s, p: SummarizerParams, lengths=None) -> SummaryBundle:
     else:
         q_all = qs
     n_q = n_s + n_cls
-    pooled = F.hsp_pool(S, q_all.reshape(H * n_q, d), lens).view(B, H, n_q, d)
-    hseed = F.linear(F.head_proj(pooled[:, :, :n_s], hp.attn.ref(2)), hp.P, hp.attn.wout)
+    # query rows ordered (query, head): each pooled set is (B, n, H, d) and its
+    # projections run on B*n flattened rows
+    q_rows = q_all.transpose(0, 1).reshape(n_q * H, d)
+    splits = (n_s * H, n_cls * H) if n_cls > 0 else (n_s * H,)
+    pooled = F.hsp_pool(S, q_rows, lens, splits)
+    hseed = F.linear(F.head_proj(pooled[0].view(B, n_s, H, d), hp.attn.ref(2)), hp.P, hp.attn.wout)
     hsp_tok = sumkronlinear(hseed, hp)
     if n_cls > 0:
-        cls_tok = F.linear(F.head_proj(pooled[:, :, n_s:], p.cls_attn.ref(2)), hp.P, p.cls_attn.wout)
+        cls_tok = F.linear(F.head_proj(pooled[1].view(B, n_cls, H, d), p.cls_attn.ref(2)), hp.P, p.cls_attn.wout)
     else:
         cls_tok = S.new_zeros(B, 0, d)
     rec = F.recent_rows(S, lens, p.split.n_recent)

@@ -29,6 +29,12 @@ class NumericsError(ArithmeticError):
 ACTIVATIONS = {"identity": 0, "relu": 1, "silu": 2, "tanh": 3, "sigmoid": 4, "exp": 5, "sqrt": 6, "log": 7}
 
 
+def _sel(view: torch.Tensor, index):
+    """A registry name's view of its block: an index expression, or a
+    callable (e.g. a transposed slice) for blocks packed in a kernel layout."""
+    return index(view) if callable(index) else view[index]
+
+
 class Params:
     """Ordered registry of named learnable tensors (tensor.py:105-144),
     stored in one flat fp32 device buffer.
@@ -94,7 +100,7 @@ class Params:
             self.flat_c = torch.empty(n, dtype=compute_dtype, device=self.device)
         with torch.no_grad():
             for block, index, arr in self._pending:
-                self._view(self.flat.detach(), block)[index].copy_(torch.from_numpy(arr))
+                _sel(self._view(self.flat.detach(), block), index).copy_(torch.from_numpy(arr))
         self._pending = []
         self.refresh()
         return self
@@ -132,7 +138,7 @@ class Params:
     # -- reference-registry views --------------------------------------------
     def __getitem__(self, name: str) -> torch.Tensor:
         block, index = self._names[name]
-        return self.w32(block)[index]
+        return _sel(self.w32(block), index)
 
     def __contains__(self, name: str) -> bool:
         return name in self._names
@@ -152,7 +158,7 @@ class Params:
 
     def grad(self, name: str) -> torch.Tensor:
         block, index = self._names[name]
-        return self.g(block)[index]
+        return _sel(self.g(block), index)
 
     def set(self, name: str, data) -> None:
         """Replace a parameter's value (trainer-only, between steps)."""

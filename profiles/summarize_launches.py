@@ -1,6 +1,7 @@
-"""Summarise an `ncu --metrics gpu__time_duration.sum --csv` launch list:
-per-kernel share of the last training step (the last quarter of launches of a
-`bench.py --steps 1 --warmup 3` run).  usage: python summarize_launches.py launches.csv"""
+"""Summarise an `ncu --metrics gpu__time_duration.sum --csv` launch list of
+`bench.py --eager --steps K --warmup W`: per-kernel share of ONE training
+step, the launches between the last two fused-Adam launches (Adam closes
+every step).  usage: python summarize_launches.py launches.csv"""
 import collections
 import csv
 import sys
@@ -15,13 +16,15 @@ for r in data:
         vals.append((int(r[ii]), r[ki][:100], float(r[vi].replace(",", ""))))
     except (ValueError, IndexError):
         pass
-last = vals[int(len(vals) * 0.75):]
+adam = [i for i, (_, k, _) in enumerate(vals) if "adam_kernel" in k]
+last = vals[adam[-2] + 1:adam[-1] + 1] if len(adam) >= 2 else vals[int(len(vals) * 0.75):]
 tot, cnt = collections.defaultdict(float), collections.Counter()
 for _, k, v in last:
     tot[k] += v
     cnt[k] += 1
 s = sum(tot.values())
-print(f"launches captured: {len(vals)}; last-quarter kernel time: {s / 1e6:.2f} ms (ncu: serialised, cold cache)")
+print(f"launches captured: {len(vals)}; one step: {len(last)} launches, {s / 1e6:.2f} ms kernel time "
+      f"(ncu: serialised, cold cache)")
 print(f"{'share':>7} {'us':>9} {'n':>4}  kernel")
-for k, v in sorted(tot.items(), key=lambda x: -x[1])[:25]:
+for k, v in sorted(tot.items(), key=lambda x: -x[1])[:40]:
     print(f"{100 * v / s:6.2f}% {v / 1e3:9.0f} {cnt[k]:4d}  {k}")

@@ -11,7 +11,10 @@ from paper_2602_10016_b200 import functional as F  # noqa: E402
 stage = sys.argv[1]
 B, T, H, dh, w = int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4]), 64, int(sys.argv[5])
 causal = len(sys.argv) > 6 and sys.argv[6] == "1"
-lens_arg = [int(x) for x in sys.argv[7].split(",")] if len(sys.argv) > 7 else None
+lens_arg = None
+if len(sys.argv) > 7:
+    lens_arg = [T] * B if sys.argv[7] == "full" else [int(x) for x in sys.argv[7].split(",")]
+    assert len(lens_arg) == B, "need one length per sample"
 g = torch.Generator(device="cuda").manual_seed(0)
 qkv = torch.randn(B, T, 3 * H * dh, device="cuda", generator=g).to(torch.bfloat16)
 lens = torch.tensor(lens_arg or [T - 3 * i for i in range(B)], device="cuda", dtype=torch.int32).clamp_min(0)
