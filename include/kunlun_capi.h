@@ -146,6 +146,49 @@ int kl_gdpa_fwd(const kl_gdpa_args* args, void* stream);
 int kl_gdpa_bwd(const kl_gdpa_args* args, void* stream);
 
 /*
+ * Fused HSP / PMA pooling (seqsum.py:26-34, 96-102 = multi_head_attention of
+ * batch-shared queries over S, attention.py:69-93), with the key projection
+ * folded into the queries (Q = q W_q^T W_k / sqrt(d_h), rows ordered
+ * (query, head)):  pooled[b] = softmax_t<len(Q S[b]^T) S[b].
+ *   S:  (B, T, d) bf16, rows s_rs apart, samples s_bs apart.
+ *   Q:  (HQ, d) bf16 contiguous.
+ *   O1: query rows [0, n1) -> (B, n1, d) (batch stride o1_bs); O2: rows
+ *       [n1, HQ) -> (B, HQ - n1, d).  Empty samples give zero rows.
+ *   LSE: (B, HQ) fp32 natural-log normaliser (+inf for empty samples).
+ * Backward: dO1 = the gradient of ALL HQ pooled rows, (B, HQ, d) with batch
+ *   stride o1_bs (dO2 unused), Dq (B, HQ) fp32 = rowsum(dO * pooled), LSE ->
+ *   dS (B, T, d) bf16 (rows ds_rs apart; accumulated into when accumulate_ds),
+ *   dZ / dZ_lo (B, HQ, T) bf16: the score gradient split hi + lo (the input
+ *   of the batch-reduced query gradient dQ = sum_b dZ S).
+ * bf16, d in {128, 256}; anything else returns KL_EUNSUPPORTED.
+ */
+typedef struct kl_hsp_args {
+  int B, T, HQ, d, n1;
+  int dtype;
+  const int* lengths;
+  const void* S;
+  long long s_rs, s_bs;
+  const void* Q;
+  void* O1;
+  long long o1_bs;
+  void* O2;
+  long long o2_bs;
+  float* LSE;
+  /* backward */
+  const void* dO1;
+  const void* dO2;
+  void* dS;
+  long long ds_rs, ds_bs;
+  int accumulate_ds;
+  void* dZ;
+  void* dZ_lo;
+  const float* Dq;
+} kl_hsp_args;
+
+int kl_hsp_fwd(const kl_hsp_args* args, void* stream);
+int kl_hsp_bwd(const kl_hsp_args* args, void* stream);
+
+/*
  * Sliding-window multi-head self-attention core (flash style; tiles outside
  * the band are never visited).  Replaces the score/softmax/value part of
  * `mha_window` / `mha_full` (attention.py:69-93 with band_mask & length mask,

@@ -81,6 +81,24 @@ class GdpaArgs(C.Structure):
     ]
 
 
+class HspArgs(C.Structure):
+    _fields_ = [
+        ("B", C.c_int), ("T", C.c_int), ("HQ", C.c_int), ("d", C.c_int), ("n1", C.c_int),
+        ("dtype", C.c_int),
+        ("lengths", C.c_void_p),
+        ("S", C.c_void_p), ("s_rs", C.c_longlong), ("s_bs", C.c_longlong),
+        ("Q", C.c_void_p),
+        ("O1", C.c_void_p), ("o1_bs", C.c_longlong),
+        ("O2", C.c_void_p), ("o2_bs", C.c_longlong),
+        ("LSE", C.c_void_p),
+        ("dO1", C.c_void_p), ("dO2", C.c_void_p),
+        ("dS", C.c_void_p), ("ds_rs", C.c_longlong), ("ds_bs", C.c_longlong),
+        ("accumulate_ds", C.c_int),
+        ("dZ", C.c_void_p), ("dZ_lo", C.c_void_p),
+        ("Dq", C.c_void_p),
+    ]
+
+
 _lib = None
 
 _SIGS = {
@@ -94,6 +112,8 @@ _SIGS = {
     "kl_gemm": ([C.POINTER(GemmArgs), C.c_void_p], C.c_int),
     "kl_gdpa_fwd": ([C.POINTER(GdpaArgs), C.c_void_p], C.c_int),
     "kl_gdpa_bwd": ([C.POINTER(GdpaArgs), C.c_void_p], C.c_int),
+    "kl_hsp_fwd": ([C.POINTER(HspArgs), C.c_void_p], C.c_int),
+    "kl_hsp_bwd": ([C.POINTER(HspArgs), C.c_void_p], C.c_int),
     "kl_swa_fwd": ([C.POINTER(SwaArgs), C.c_void_p], C.c_int),
     "kl_swa_bwd": ([C.POINTER(SwaArgs), C.c_void_p], C.c_int),
     "kl_swa_debug_support": ([C.POINTER(SwaArgs), C.c_void_p, C.c_void_p], C.c_int),

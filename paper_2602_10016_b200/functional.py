@@ -337,7 +337,7 @@ class _HspPool(torch.autograd.Function):
     @staticmethod
     def forward(ctx, S, Q32, lengths, splits):
         # Q arrives in fp32 (the batch-shared query path is computed in fp32);
-        # the T-length GEMMs run in S's dtype and dQ is returned in fp32.
+        # the T-length work runs in S's dtype and dQ is returned in fp32.
         B, T, d = S.shape
         HQ = Q32.shape[0]
         if sum(splits) != HQ:
@@ -347,6 +347,16 @@ class _HspPool(torch.autograd.Function):
             Q = torch.empty(Q32.shape, device=S.device, dtype=S.dtype)
             _capi.call("kl_cast", Q.numel(), _capi.dt(Q32), Q32.contiguous().data_ptr(), _capi.dt(Q), Q.data_ptr(),
                        _stream())
+        ctx.splits = tuple(splits)
+        ctx.fused = _hsp_fused_ok(S, HQ, len(splits))
+        if ctx.fused:
+            S = S.contiguous()
+            outs = [torch.empty(B, n, d, device=S.device, dtype=S.dtype) for n in splits]
+            LSE = torch.empty(B, HQ, device=S.device, dtype=torch.float32)
+            a = _hsp_args(S, Q, lengths, splits[0], outs[0], outs[-1], LSE)
+            _capi.call("kl_hsp_fwd", C.byref(a), _stream())
+            ctx.save_for_backward(S, Q, lengths, LSE, *outs)
+            return tuple(outs)
         sc = gemm(S, Q.t(), out_dtype=torch.float32)  # (B, T, HQ)
         Pm = torch.empty(B, T, HQ, device=S.device, dtype=S.dtype)
         a = _colsm_args(sc, Pm, lengths)
@@ -361,6 +371,8 @@ class _HspPool(torch.autograd.Function):
 
     @staticmethod
     def backward(ctx, *gs):
+        if ctx.fused:
+            return _hsp_fused_bwd(ctx, gs)
         S, Q, lengths, Pm, *outs = ctx.saved_tensors
         B, T, d = S.shape
         HQ = Q.shape[0]
@@ -397,6 +409,52 @@ class _HspPool(torch.autograd.Function):
             gemm(lo.transpose(1, 2).unsqueeze(0), S.unsqueeze(0), dQ, beta=1.0, reduce=(False, True))
         dQ = dQ.reshape(Q.shape)
         return dS, dQ, None, None
+
+
+HSP_FUSED = True  # tests flip this to A/B the fused tcgen05 pooling against the GEMM composition
+
+
+def _hsp_fused_ok(S, HQ, n_splits) -> bool:
+    return (HSP_FUSED and S.dtype == torch.bfloat16 and S.shape[-1] in (128, 256) and n_splits <= 2
+            and bool(_capi.lib().kl_tcgen05_available()))
+
+
+def _hsp_args(S, Q, lengths, n1, O1, O2, LSE):
+    a = _capi.HspArgs()
+    a.B, a.T, a.d = S.shape
+    a.HQ, a.n1 = Q.shape[0], n1
+    a.dtype = _capi.dt(S)
+    a.lengths = lengths.data_ptr()
+    a.S, a.s_rs, a.s_bs = S.data_ptr(), S.stride(1), S.stride(0)
+    a.Q = Q.data_ptr()
+    a.O1, a.o1_bs = O1.data_ptr(), O1.stride(0)
+    a.O2, a.o2_bs = O2.data_ptr(), O2.stride(0)
+    a.LSE = LSE.data_ptr()
+    return a
+
+
+def _hsp_fused_bwd(ctx, gs):
+    """kl_hsp_bwd: dS and the hi/lo score gradient dZ in one pass over S; then
+    the batch-shared query gradient dQ = sum_b dZ S (hi + lo) as GEMMs."""
+    S, Q, lengths, LSE, *outs = ctx.saved_tensors
+    B, T, d = S.shape
+    HQ = Q.shape[0]
+    gl = [torch.zeros_like(o) if g is None else g for g, o in zip(gs, outs)]
+    dO = gl[0].contiguous() if len(gl) == 1 else torch.cat(gl, dim=1)
+    O = outs[0] if len(outs) == 1 else torch.cat(outs, dim=1)
+    Dq = torch.linalg.vecdot(dO.float(), O.float())  # rowsum(dO * pooled): the softmax-VJP term
+    dS = torch.empty_like(S)
+    dZ = torch.empty(B, HQ, T, device=S.device, dtype=S.dtype)
+    dZlo = torch.empty_like(dZ)
+    a = _hsp_args(S, Q, lengths, HQ, dO, dO, LSE)
+    a.dO1 = dO.data_ptr()
+    a.dS, a.ds_rs, a.ds_bs = dS.data_ptr(), dS.stride(1), dS.stride(0)
+    a.dZ, a.dZ_lo, a.Dq = dZ.data_ptr(), dZlo.data_ptr(), Dq.data_ptr()
+    _capi.call("kl_hsp_bwd", C.byref(a), _stream())
+    dQ = torch.zeros(1, 1, HQ, d, device=S.device, dtype=torch.float32)
+    gemm(dZ.unsqueeze(0), S.unsqueeze(0), dQ, beta=1.0, reduce=(False, True))
+    gemm(dZlo.unsqueeze(0), S.unsqueeze(0), dQ, beta=1.0, reduce=(False, True))
+    return dS, dQ.reshape(Q.shape), None, None
 
 
 HSP_DCOL = True  # softmax-VJP column term from the pooled output (tests A/B it against the t-reduction)

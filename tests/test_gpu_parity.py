@@ -276,13 +276,17 @@ def test_swa_support_bitexact():
 
 
 @pytest.mark.parametrize("dtype", DTYPES)
-@pytest.mark.parametrize("T", [37, 1])
-def test_hsp_vs_oracle(dtype, T):
+@pytest.mark.parametrize("T,d,H,n_seeds", [(37, 32, 2, 6), (1, 32, 2, 6), (300, 128, 2, 40), (257, 256, 4, 32),
+                                           (130, 256, 4, 12)])
+def test_hsp_vs_oracle(dtype, T, d, H, n_seeds):
+    """HSP + CLS pooling vs the oracle; d in {128, 256} in bf16 runs the fused
+    tcgen05 pooling kernels (kl_hsp_fwd / kl_hsp_bwd), with query tiles that
+    straddle the seed / CLS boundary and a partial second tile."""
     from paper_2602_10016_b200 import functional as F
     from paper_2602_10016_b200 import seqsum as Q
     from paper_2602_10016_b200.tensor import Params
 
-    d, H, budget, n_seeds, rank = 32, 2, 8, 6, 2
+    budget, rank = 8, 2
     rng = np.random.default_rng(5)
     P = Params()
     sp = Q.SummarizerParams.create(P, "s", d, Q.SummarySplit.for_budget(budget), n_seeds, rank, H, rng)
@@ -290,7 +294,7 @@ def test_hsp_vs_oracle(dtype, T):
     named = {n: P[n].double().cpu().numpy() for n in P.names()}
     lengths = np.array([T, 0, max(T - 5, 1), 1])
     B = len(lengths)
-    S = rng.normal(0, 1, (B, T, d))
+    S = rng.normal(0, 1, (B, T, d)) * (4.0 / np.sqrt(d) if d > 32 else 1.0)
     R = rng.normal(0, 1, (B, budget, d))
     S_t = dev(S, grad=True)
     rows = Q.hsp_summarize(F.cast(S_t, dtype), sp, lengths).rows()
