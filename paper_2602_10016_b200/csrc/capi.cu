@@ -7,6 +7,8 @@
 
 #include <atomic>
 
+#include <cuda.h>
+
 #include "common.cuh"
 #include "gemm.h"
 #include "swa.h"
@@ -37,6 +39,33 @@ int launch_check(const char* what) {
 void count_launch(unsigned n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 int gemm_path() { return g_gemm_path; }
+
+// Tensor-map encoding is a driver-API call that needs a current context.  The
+// autograd engine runs backward ops on its own worker thread, where the
+// runtime may not have bound the device's primary context yet (observed:
+// CUDA_ERROR_INVALID_CONTEXT from cuTensorMapEncodeTiled); bind the device of
+// the launch stream first.
+void bind_device(cudaStream_t s) {
+  typedef CUresult (*ctx_get_fn)(CUcontext*);
+  static ctx_get_fn get_ctx = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuCtxGetCurrent", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      get_ctx = (ctx_get_fn)f;
+  }
+  CUcontext c = nullptr;
+  if (get_ctx && get_ctx(&c) == CUDA_SUCCESS && c) return;  // the common case: nothing to do (capture-safe)
+  int dev = -1;
+  if (!s || cudaStreamGetDevice(s, &dev) != cudaSuccess) {
+    cudaGetLastError();
+    cudaGetDevice(&dev);
+  }
+  if (dev >= 0) cudaSetDevice(dev);
+}
 
 static int g_pdl = -1;  // -1: from KL_PDL (default off: measured neutral on the c2 step)
 bool pdl_enabled() {
@@ -108,6 +137,7 @@ extern "C" int kl_gemm(const kl_gemm_args* a, void* stream) {
   e.aux_mode = a->aux_mode; e.n_act = a->n_act; e.act_group = a->act_group > 0 ? a->act_group : 1;
   for (int i = 0; i < KL_MAX_ACT_GROUPS; ++i) e.act_codes[i] = a->act_codes[i];
   cudaStream_t s = (cudaStream_t)stream;
+  bind_device(s);
   if (a->ab_dtype == KL_BF16 && g_gemm_path != 1) {
     int rc = gemm_tc(g, e, s);
     g_last_path = 1;
@@ -144,6 +174,7 @@ extern "C" int kl_swa_fwd(const kl_swa_args* a, void* stream) {
   if (rc) return rc;
   if (p.B == 0 || p.T == 0) return KL_OK;
   cudaStream_t s = (cudaStream_t)stream;
+  bind_device(s);
   if (p.dtype == KL_BF16 && g_gemm_path != 1) {
     rc = swa_fwd_tc(p, s);
     if (rc != KL_EUNSUPPORTED) return rc;
@@ -161,6 +192,7 @@ extern "C" int kl_swa_bwd(const kl_swa_args* a, void* stream) {
     return KL_EBADSHAPE;
   }
   cudaStream_t s = (cudaStream_t)stream;
+  bind_device(s);
   if (p.dtype == KL_BF16 && g_gemm_path != 1) {
     rc = swa_bwd_tc(p, s);
     if (rc != KL_EUNSUPPORTED) return rc;

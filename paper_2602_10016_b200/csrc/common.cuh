@@ -19,6 +19,7 @@ void set_error(const char* fmt, ...);
 int launch_check(const char* what);
 void count_launch(unsigned n = 1);
 bool pdl_enabled();
+void bind_device(cudaStream_t s);
 
 // ---- launches: programmatic dependent launch (PDL) --------------------------
 // Every kernel of the library starts with KL_PDL_ENTRY() and, when PDL is on

@@ -659,18 +659,22 @@ __global__ void __launch_bounds__(NT, 1)
   if (warp == 1) tc::tmem_dealloc(tmem, 512);
 }
 
+static int last_rc = 0;
 bool map3(CUtensorMap* m, const void* ptr, long long inner, long long rows, long long B, long long ld, long long bs,
           int box_rows) {
   auto fn = tc_encode_fn();
+  last_rc = -1;
   if (!fn) return false;
+  last_rc = -2;
   if (((uintptr_t)ptr & 15) || (ld * 2) % 16 || (bs * 2) % 16) return false;
   cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)rows, (cuuint64_t)B};
   cuuint64_t strides[2] = {(cuuint64_t)(ld * 2), (cuuint64_t)(bs * 2)};
   cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
-  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, estr,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  last_rc = (int)fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return last_rc == (int)CUDA_SUCCESS;
 }
 
 }  // namespace gdpa
@@ -680,7 +684,8 @@ bool map3(CUtensorMap* m, const void* ptr, long long inner, long long rows, long
 // C ABI
 using namespace kl;
 
-static int gdpa_prepare(const kl_gdpa_args* a, const char* who, gdpa::P& p) {
+static int gdpa_prepare(const kl_gdpa_args* a, const char* who, gdpa::P& p, void* stream) {
+  bind_device((cudaStream_t)stream);
   if (!a || a->B < 0 || a->T < 0 || a->d < 1 || a->HK < 1 || a->n_kv < 1) {
     set_error("%s: bad extents", who);
     return KL_EBADSHAPE;
@@ -747,12 +752,14 @@ template <int D>
 static int gdpa_bwd_launch(const kl_gdpa_args* a, const gdpa::P& p, cudaStream_t s) {
   CUtensorMap ts, tg, tk, tv, tds;
   const long long kvbs = (long long)gdpa::HK * D;
-  if (!gdpa::map3(&ts, a->S, D, a->T, a->B, a->s_rs, a->s_bs, gdpa::TB) ||
-      !gdpa::map3(&tg, a->dY, D, a->T, a->B, a->s_rs, a->s_bs, gdpa::TB) ||
-      !gdpa::map3(&tds, a->dS, D, a->T, a->B, a->s_rs, a->s_bs, gdpa::TB) ||
-      !gdpa::map3(&tk, a->Kt, D, gdpa::HK, a->B, D, kvbs, gdpa::HK) ||
-      !gdpa::map3(&tv, a->Vt, D, gdpa::HK, a->B, D, kvbs, gdpa::HK)) {
-    set_error("kl_gdpa_bwd: tensor map encode failed (alignment?)");
+  const int ok = (gdpa::map3(&ts, a->S, D, a->T, a->B, a->s_rs, a->s_bs, gdpa::TB) ? 1 : 0) |
+                 (gdpa::map3(&tg, a->dY, D, a->T, a->B, a->s_rs, a->s_bs, gdpa::TB) ? 2 : 0) |
+                 (gdpa::map3(&tds, a->dS, D, a->T, a->B, a->s_rs, a->s_bs, gdpa::TB) ? 4 : 0) |
+                 (gdpa::map3(&tk, a->Kt, D, gdpa::HK, a->B, D, kvbs, gdpa::HK) ? 8 : 0) |
+                 (gdpa::map3(&tv, a->Vt, D, gdpa::HK, a->B, D, kvbs, gdpa::HK) ? 16 : 0);
+  if (ok != 31) {
+    set_error("kl_gdpa_bwd: tensor map encode failed (alignment?) rc=%d mask=%d S=%p dY=%p dS=%p Kt=%p Vt=%p rs=%lld bs=%lld",
+              gdpa::last_rc, ok, a->S, a->dY, a->dS, a->Kt, a->Vt, a->s_rs, a->s_bs);
     return KL_EUNSUPPORTED;
   }
   const size_t smem = gdpa::bwd_smem<D>();
@@ -767,7 +774,7 @@ static int gdpa_bwd_launch(const kl_gdpa_args* a, const gdpa::P& p, cudaStream_t
 
 extern "C" int kl_gdpa_fwd(const kl_gdpa_args* a, void* stream) {
   gdpa::P p;
-  int rc = gdpa_prepare(a, "kl_gdpa_fwd", p);
+  int rc = gdpa_prepare(a, "kl_gdpa_fwd", p, stream);
   if (rc) return rc;
   if (!a->Y) {
     set_error("kl_gdpa_fwd: Y is required");
@@ -780,7 +787,7 @@ extern "C" int kl_gdpa_fwd(const kl_gdpa_args* a, void* stream) {
 
 extern "C" int kl_gdpa_bwd(const kl_gdpa_args* a, void* stream) {
   gdpa::P p;
-  int rc = gdpa_prepare(a, "kl_gdpa_bwd", p);
+  int rc = gdpa_prepare(a, "kl_gdpa_bwd", p, stream);
   if (rc) return rc;
   if (!a->dY || !a->dS || !a->dKt || !a->dVt) {
     set_error("kl_gdpa_bwd: dY, dS, dKt and dVt are required");

@@ -4,7 +4,7 @@
 // cannot meet the 1e-5 contract) and the fallback for
 // shapes the tcgen05 kernel does not take (tiny M/N, unaligned strides).
 // Output tile BM x 64 (BM = 64, or 16 for the many small-M batched products of
-// the summarizers / folds), BK = 16, 256 threads, (BM/16) x 4 register tile.
+// the summarizers / folds, 32 for the batch-shared query folds), BK = 32, 256 threads, (BM/16) x 4 register tile.
 // A reduction over the batch / K space may be split across CTAs (fp32
 // atomics into an accumulate-only output).
 #include <algorithm>
@@ -16,15 +16,19 @@ namespace kl {
 
 namespace {
 
-constexpr int BN = 64, BK = 16;
+constexpr int BN = 64, BK = 32;
 
+// Output tile BM x 64, k-tiles of 32 double-buffered in smem: the global loads
+// of k-tile i+1 are in flight (registers) while k-tile i is multiplied, so a
+// small-M / long-K product is not one global-latency round trip per k-step.
 template <typename TA, typename TC, int BM>
 __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmDesc g, Epi e, int splits) {
   KL_PDL_ENTRY();
-  constexpr int TM = BM / 16;       // rows per thread
-  constexpr int AL = BM * BK / 256;  // A elements loaded per thread per k-step
-  __shared__ float As[BK][BM + 4];
-  __shared__ float Bs[BK][BN + 4];
+  constexpr int TM = BM / 16;        // rows per thread
+  constexpr int AL = BM * BK / 256;  // A elements loaded per thread per k-tile
+  constexpr int BL = BK * BN / 256;  // B elements loaded per thread per k-tile
+  __shared__ float As[2][BK][BM + 4];
+  __shared__ float Bs[2][BK][BN + 4];
   const TA* __restrict__ A = (const TA*)g.A;
   const TA* __restrict__ Bp = (const TA*)g.B;
   const int tid = threadIdx.x;
@@ -48,7 +52,8 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmDesc g, Epi e, int s
   const int kbn = (g.K + BK - 1) / BK;
   const int iters = r1n * r2n * kbn;
   const int it0 = (int)((long long)iters * sp / splits), it1 = (int)((long long)iters * (sp + 1) / splits);
-  for (int it = it0; it < it1; ++it) {
+  float ra[AL], rb[BL];
+  auto gload = [&](int it) {
     const int r = it / kbn, k0 = (it % kbn) * BK;
     const int r1 = r / r2n, r2 = r % r2n;
     const int z1 = g.red1 ? r1 : z1o;
@@ -58,44 +63,58 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmDesc g, Epi e, int s
 #pragma unroll
     for (int i = 0; i < AL; ++i) {
       const int e_ = tid + 256 * i;
-      int kk, mm;
-      if (a_kfast) {
-        kk = e_ % BK;
-        mm = e_ / BK;
-      } else {
-        mm = e_ % BM;
-        kk = e_ / BM;
-      }
+      const int kk = a_kfast ? e_ % BK : e_ / BM;
+      const int mm = a_kfast ? e_ / BK : e_ % BM;
       const int m = m0 + mm, k = k0 + kk;
-      As[kk][mm] = (m < g.M && k < g.K) ? ldf(Ab + (long long)m * g.a_rs + (long long)k * g.a_cs) : 0.f;
+      ra[i] = (m < g.M && k < g.K) ? ldf(Ab + (long long)m * g.a_rs + (long long)k * g.a_cs) : 0.f;
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < BL; ++i) {
       const int e_ = tid + 256 * i;
-      int kk, nn;
-      if (b_nfast) {
-        nn = e_ % BN;
-        kk = e_ / BN;
-      } else {
-        kk = e_ % BK;
-        nn = e_ / BK;
-      }
+      const int nn = b_nfast ? e_ % BN : e_ / BK;
+      const int kk = b_nfast ? e_ / BN : e_ % BK;
       const int n = n0 + nn, k = k0 + kk;
-      Bs[kk][nn] = (n < g.N && k < g.K) ? ldf(Bb + (long long)k * g.b_rs + (long long)n * g.b_cs) : 0.f;
+      rb[i] = (n < g.N && k < g.K) ? ldf(Bb + (long long)k * g.b_rs + (long long)n * g.b_cs) : 0.f;
     }
-    __syncthreads();
+  };
+  auto sstore = [&](int buf) {
+#pragma unroll
+    for (int i = 0; i < AL; ++i) {
+      const int e_ = tid + 256 * i;
+      const int kk = a_kfast ? e_ % BK : e_ / BM;
+      const int mm = a_kfast ? e_ / BK : e_ % BM;
+      As[buf][kk][mm] = ra[i];
+    }
+#pragma unroll
+    for (int i = 0; i < BL; ++i) {
+      const int e_ = tid + 256 * i;
+      const int nn = b_nfast ? e_ % BN : e_ / BK;
+      const int kk = b_nfast ? e_ / BN : e_ % BK;
+      Bs[buf][kk][nn] = rb[i];
+    }
+  };
+  if (it0 < it1) {
+    gload(it0);
+    sstore(0);
+  }
+  __syncthreads();
+  for (int it = it0; it < it1; ++it) {
+    const int buf = (it - it0) & 1;
+    const bool more = it + 1 < it1;
+    if (more) gload(it + 1);
 #pragma unroll
     for (int kk = 0; kk < BK; ++kk) {
       float a[TM], b[4];
 #pragma unroll
-      for (int i = 0; i < TM; ++i) a[i] = As[kk][ty * TM + i];
+      for (int i = 0; i < TM; ++i) a[i] = As[buf][kk][ty * TM + i];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
+      for (int j = 0; j < 4; ++j) b[j] = Bs[buf][kk][tx * 4 + j];
 #pragma unroll
       for (int i = 0; i < TM; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
     }
+    if (more) sstore(buf ^ 1);
     __syncthreads();
   }
 
@@ -136,12 +155,14 @@ int launch(const GemmDesc& g, const Epi& e, cudaStream_t s) {
   int splits = 1;
   GemmDesc gd = g;
   gd.ws = nullptr;
-  if (accum_only && tiles < 4 * 148 && iters >= 16) {
-    splits = (int)std::max<long long>(1, std::min<long long>((4 * 148) / tiles, iters / 8));
-  } else if (!accum_only && g.ws && tiles < 2 * 148 && iters >= 16) {
-    // few output tiles with any epilogue: fp32 partials in the workspace, then
-    // one reduce + epilogue pass
-    int sp = (int)std::max<long long>(1, std::min<long long>((4 * 148) / tiles, iters / 8));
+  // few output tiles: split the reduction down to 2 k-tiles per CTA so a tiny
+  // product still spreads over the SMs (its latency, not its FLOPs, is the cost)
+  if (accum_only && tiles < 4 * 148 && iters >= 4) {
+    splits = (int)std::max<long long>(1, std::min<long long>((4 * 148) / tiles, iters / 2));
+  } else if (!accum_only && g.ws && tiles < 2 * 148 && iters >= 4) {
+    // any other epilogue: fp32 partials in the workspace, then one reduce +
+    // epilogue pass
+    int sp = (int)std::max<long long>(1, std::min<long long>((4 * 148) / tiles, iters / 2));
     const long long per = (long long)nout * g.M * g.N * 4;
     while (sp > 1 && per * sp > g.ws_bytes) --sp;
     if (sp > 1) {
@@ -171,7 +192,7 @@ int launch(const GemmDesc& g, const Epi& e, cudaStream_t s) {
 }  // namespace
 
 int gemm_simt(const GemmDesc& g, const Epi& e, cudaStream_t s) {
-  return g.M <= 16 ? launch<16>(g, e, s) : launch<64>(g, e, s);
+  return g.M <= 16 ? launch<16>(g, e, s) : (g.M <= 32 ? launch<32>(g, e, s) : launch<64>(g, e, s));
 }
 
 }  // namespace kl

@@ -731,7 +731,8 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
   if (g0.ab_dtype != KL_BF16) return KL_EUNSUPPORTED;
   if (!kl_tcgen05_available()) return KL_EUNSUPPORTED;
   // small problems go to the SIMT kernel unless forced
-  if (gemm_path() != 2 && (long long)g0.M * g0.N * g0.K < (1ll << 18)) return KL_EUNSUPPORTED;
+  // (counting every batch: a batch of small products fills the SMs with tiles)
+  if (gemm_path() != 2 && (long long)g0.M * g0.N * g0.K * g0.nb1 * g0.nb2 < (1ll << 18)) return KL_EUNSUPPORTED;
   GemmDesc g = g0;
   Epi e = e0;
   // C += ... on a bf16 output is the residual epilogue with R = C

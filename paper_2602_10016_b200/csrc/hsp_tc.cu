@@ -697,6 +697,7 @@ extern "C" int kl_hsp_fwd(const kl_hsp_args* a, void* stream) {
     return KL_EUNSUPPORTED;
   }
   if (a->B == 0) return KL_OK;
+  bind_device((cudaStream_t)stream);
   hsp::FwdP p{};
   p.B = a->B;
   p.T = a->T;
@@ -748,6 +749,7 @@ extern "C" int kl_hsp_bwd(const kl_hsp_args* a, void* stream) {
     return KL_EBADSHAPE;
   }
   if (a->B == 0 || a->T == 0) return KL_OK;
+  bind_device((cudaStream_t)stream);
   hsp::BwdP p{};
   p.B = a->B;
   p.T = a->T;

@@ -15,7 +15,14 @@ w = torch.randn(256, 256, device=dev).to(bf)
 big = torch.randn(3072, 256, device=dev).to(bf)
 w2 = torch.randn(512, 256, device=dev).to(bf)
 o32 = torch.zeros(256, 256, device=dev)
+q32 = torch.randn(32, 4, 64, device=dev)
+wk = torch.randn(4, 64, 256, device=dev)
+xs = torch.randn(32, 256, device=dev)
+wq = torch.randn(256, 256, device=dev)
 cases = {
+    "fp32 32x256x256": lambda: gemm(xs, wq.t()),
+    "fp32 32x256x64 b4": lambda: gemm(q32.permute(1, 0, 2), wk),
+    "fp32 dW 256x256 K=32 +=": lambda: gemm(wq[:, :32], xs, o32, beta=1.0),
     "torch add (tiny)": lambda: torch.add(o32, 1.0),
     "4096x256x256 plain": lambda: gemm(x.view(-1, 256), w.t()),
     "3072x512x256 plain": lambda: gemm(big, w2.t()),
