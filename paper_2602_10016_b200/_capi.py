@@ -315,7 +315,7 @@ def gemm(A: torch.Tensor, B: torch.Tensor, out: torch.Tensor | None = None, *, o
     return ret
 
 
-SWAP_SMALL_M = True  # tests flip this to A/B the operand-swapped small-M form
+SWAP_SMALL_M = False  # operand-swapped small-M form (measured slower than the plain tcgen05 tile: strided epilogue)
 GEMM_LOG = None  # list of (M, N, K, nb1, nb2, red1, red2, A/B/C strides, c_dtype, path) when set
 
 
