@@ -124,9 +124,11 @@ def _self_attention(s, p: MhaParams, w: int, causal: bool, lengths):
     if s.shape[-1] != p.dim:
         raise ShapeError(f"attention needs (n, {p.dim}) inputs, got {tuple(s.shape)}")
     lens = _lengths(s, lengths)
-    qkv = F.linear(s, p.P, p.wqkv)
+    # the out-projection's residual gradient (dY) is added in the QKV dX epilogue
+    stash = F.ResidualStash()
+    qkv = F.linear(s, p.P, p.wqkv, stash_in=stash)
     o = F.swa_core(qkv, lens, p.heads, p.head_dim, w, causal)
-    y = F.linear(o, p.P, p.wout, residual=s)
+    y = F.linear(o, p.P, p.wout, residual=s, stash_out=stash)
     return y.squeeze(0) if squeeze else y
 
 

@@ -41,6 +41,38 @@ class PRef:
         return self.fn(v) if self.fn else v
 
 
+class GradSink:
+    """One gradient buffer shared by the consumers of a (B, T, d) sequence
+    tensor (HSP pooling, recent rows, the GDPA / attention branch).  The
+    first consumer whose backward runs registers its dS; consumers that can
+    accumulate in their own epilogue (HSP pooling, recent rows) add into it
+    and return no gradient, so autograd does not materialise and add one
+    (B, T, d) gradient per consumer."""
+
+    __slots__ = ("t",)
+
+    def __init__(self):
+        self.t = None
+
+    def take(self, like):
+        t = self.t
+        if t is not None and t.shape == like.shape and t.dtype == like.dtype and t.is_contiguous():
+            return t
+        return None
+
+
+class ResidualStash:
+    """Passes the residual gradient of a later op (out-projection: y = S + o
+    W^T) to an earlier op with the same input (the QKV projection), which
+    adds it in its dX GEMM epilogue: backward of the later op always runs
+    first (the earlier op's output gradient depends on it)."""
+
+    __slots__ = ("g",)
+
+    def __init__(self):
+        self.g = None
+
+
 def _codes(acts):
     if acts is None:
         return []
@@ -128,7 +160,7 @@ class _Linear(torch.autograd.Function):
     (epilogue aux) for the VJP."""
 
     @staticmethod
-    def forward(ctx, x, flat, P, wkey, bkey, act, residual, out_dtype=None):
+    def forward(ctx, x, flat, P, wkey, bkey, act, residual, out_dtype=None, stash_out=None, stash_in=None):
         W = P.w(wkey)
         N = W.shape[0]
         codes = _codes(act) if act and act != "identity" else []
@@ -142,6 +174,7 @@ class _Linear(torch.autograd.Function):
         ctx.P, ctx.wkey, ctx.bkey, ctx.codes = P, wkey, bkey, codes
         ctx.has_res = residual is not None
         ctx.xshape = x.shape
+        ctx.stash_out, ctx.stash_in = stash_out, stash_in
         ctx.save_for_backward(x4, pre)
         return y if x.dim() >= 2 else y.squeeze(0)
 
@@ -165,7 +198,12 @@ class _Linear(torch.autograd.Function):
                        gp.data_ptr(), cols, len(ctx.codes), 1, codes, _stream())
         dx = None
         if ctx.needs_input_grad[0]:
-            dx = gemm(gp, W)
+            res = None
+            if ctx.stash_in is not None and ctx.stash_in.g is not None:
+                res = ctx.stash_in.g  # a later op's residual gradient for the same input
+                ctx.stash_in.g = None
+                res = res.reshape(gp.shape[:-1] + (res.shape[-1],))
+            dx = gemm(gp, W, residual=res)
             dx = dx.reshape(ctx.xshape)
         # dW = sum over rows (and batch dims) of gp^T x
         gp4, x44 = _as4(gp), _as4(x4)
@@ -176,7 +214,10 @@ class _Linear(torch.autograd.Function):
             gemm(ones.view(1, rows), gp.reshape(rows, gp.shape[-1]) if gp.is_contiguous() else gp.contiguous().view(rows, -1),
                  P.g(ctx.bkey).view(1, -1), beta=1.0)
         dres = g.reshape(ctx.xshape[:-1] + (g.shape[-1],)) if ctx.has_res else None
-        return dx, None, None, None, None, None, dres, None
+        if dres is not None and ctx.stash_out is not None:
+            ctx.stash_out.g = dres  # added by the earlier op's dX epilogue instead
+            dres = None
+        return dx, None, None, None, None, None, dres, None, None, None
 
 
 _ONES = {}
@@ -191,8 +232,10 @@ def _ones(n, dtype, device):
     return t[:n]
 
 
-def linear(x, P, wkey, bkey=None, act=None, residual=None, out_dtype=None):
-    return _Linear.apply(x, P.flat, P, wkey, bkey, act, residual, out_dtype)
+def linear(x, P, wkey, bkey=None, act=None, residual=None, out_dtype=None, stash_out=None, stash_in=None):
+    """y = act(x W^T + b) + residual.  ``stash_out`` / ``stash_in``: a
+    ResidualStash shared with an earlier linear on the same input."""
+    return _Linear.apply(x, P.flat, P, wkey, bkey, act, residual, out_dtype, stash_out, stash_in)
 
 
 
@@ -209,10 +252,10 @@ class _GdpaCore(torch.autograd.Function):
     (the fp32 parity path)."""
 
     @staticmethod
-    def forward(ctx, S, Kt, Vt, lengths, codes, n_kv, inv_tau):
+    def forward(ctx, S, Kt, Vt, lengths, codes, n_kv, inv_tau, sink=None):
         B, T, d = S.shape
         HK = Kt.shape[1]
-        ctx.codes, ctx.n_kv, ctx.inv_tau = codes, n_kv, inv_tau
+        ctx.codes, ctx.n_kv, ctx.inv_tau, ctx.sink = codes, n_kv, inv_tau, sink
         ctx.fused = _gdpa_fused_ok(S, HK)
         if ctx.fused:
             S = S.contiguous()
@@ -241,7 +284,9 @@ class _GdpaCore(torch.autograd.Function):
             a = _gdpa_args(S, Kt, Vt, lengths, ctx.codes, ctx.n_kv, ctx.inv_tau)
             a.dY, a.dS, a.dKt, a.dVt = g.data_ptr(), dS.data_ptr(), dKt.data_ptr(), dVt.data_ptr()
             _capi.call("kl_gdpa_bwd", C.byref(a), _stream())
-            return dS, dKt, dVt, None, None, None, None
+            if ctx.sink is not None and ctx.sink.t is None:
+                ctx.sink.t = dS
+            return dS, dKt, dVt, None, None, None, None, None
         S, Kt, Vt, Z, A, lengths = ctx.saved_tensors
         dZ = torch.empty_like(Z)
         gemm(g, Vt.transpose(1, 2), dZ, alpha=ctx.inv_tau, acts=ctx.codes, act_group=ctx.n_kv, aux=Z, aux_mode=2,
@@ -249,7 +294,9 @@ class _GdpaCore(torch.autograd.Function):
         dS = gemm(dZ, Kt, residual=g)
         dKt = gemm(dZ.transpose(1, 2), S)
         dVt = gemm(A.transpose(1, 2), g)
-        return dS, dKt, dVt, None, None, None, None
+        if ctx.sink is not None and ctx.sink.t is None:
+            ctx.sink.t = dS
+        return dS, dKt, dVt, None, None, None, None, None
 
 
 GDPA_FUSED = True  # tests flip this to A/B the fused kernels against the GEMM composition
@@ -275,8 +322,8 @@ def _gdpa_args(S, Kt, Vt, lengths, codes, n_kv, inv_tau):
     return a
 
 
-def gdpa_core(S, Kt, Vt, lengths, acts, n_kv, inv_tau):
-    return _GdpaCore.apply(S, Kt, Vt, lengths, _codes(acts), int(n_kv), float(inv_tau))
+def gdpa_core(S, Kt, Vt, lengths, acts, n_kv, inv_tau, sink=None):
+    return _GdpaCore.apply(S, Kt, Vt, lengths, _codes(acts), int(n_kv), float(inv_tau), sink)
 
 
 # ---------------------------------------------------------------------------
@@ -335,7 +382,7 @@ class _HspPool(torch.autograd.Function):
     zeros with no gradient (seqsum.py:32-33, 99-100)."""
 
     @staticmethod
-    def forward(ctx, S, Q32, lengths, splits):
+    def forward(ctx, S, Q32, lengths, splits, n_recent=0, sink=None):
         # Q arrives in fp32 (the batch-shared query path is computed in fp32);
         # the T-length work runs in S's dtype and dQ is returned in fp32.
         B, T, d = S.shape
@@ -348,7 +395,9 @@ class _HspPool(torch.autograd.Function):
             _capi.call("kl_cast", Q.numel(), _capi.dt(Q32), Q32.contiguous().data_ptr(), _capi.dt(Q), Q.data_ptr(),
                        _stream())
         ctx.splits = tuple(splits)
+        ctx.n_recent, ctx.sink = n_recent, sink
         ctx.fused = _hsp_fused_ok(S, HQ, len(splits))
+        rec = _recent_fwd(S, lengths, n_recent) if n_recent > 0 else None
         if ctx.fused:
             S = S.contiguous()
             outs = [torch.empty(B, n, d, device=S.device, dtype=S.dtype) for n in splits]
@@ -356,7 +405,7 @@ class _HspPool(torch.autograd.Function):
             a = _hsp_args(S, Q, lengths, splits[0], outs[0], outs[-1], LSE)
             _capi.call("kl_hsp_fwd", C.byref(a), _stream())
             ctx.save_for_backward(S, Q, lengths, LSE, *outs)
-            return tuple(outs)
+            return tuple(outs) + ((rec,) if rec is not None else ())
         sc = gemm(S, Q.t(), out_dtype=torch.float32)  # (B, T, HQ)
         Pm = torch.empty(B, T, HQ, device=S.device, dtype=S.dtype)
         a = _colsm_args(sc, Pm, lengths)
@@ -366,49 +415,65 @@ class _HspPool(torch.autograd.Function):
             outs.append(gemm(Pm[:, :, c0:c0 + n].transpose(1, 2), S))  # (B, n, d)
             c0 += n
         ctx.save_for_backward(S, Q, lengths, Pm, *outs)
-        ctx.splits = tuple(splits)
-        return tuple(outs)
+        return tuple(outs) + ((rec,) if rec is not None else ())
 
     @staticmethod
     def backward(ctx, *gs):
+        g_rec = None
+        if ctx.n_recent > 0:
+            gs, g_rec = gs[:-1], gs[-1]
         if ctx.fused:
-            return _hsp_fused_bwd(ctx, gs)
-        S, Q, lengths, Pm, *outs = ctx.saved_tensors
-        B, T, d = S.shape
-        HQ = Q.shape[0]
-        dP = torch.empty(B, T, HQ, device=S.device, dtype=torch.float32)
-        # D[b, c] = sum_t P dP = dO[c] . pooled[c]: the softmax-VJP column term
-        # from the (B, HQ, d) pooled output instead of a pass over T
-        Dcol = torch.empty(B, HQ, device=S.device, dtype=torch.float32)
-        dS = None
-        c0 = 0
-        for g, n, o in zip(gs, ctx.splits, outs):
-            g = torch.zeros(B, n, d, device=S.device, dtype=S.dtype) if g is None else g.contiguous()
-            Dcol[:, c0:c0 + n] = torch.linalg.vecdot(g.float(), o.float())
-            gemm(S, g.transpose(1, 2), dP[:, :, c0:c0 + n])
-            if dS is None:
-                dS = gemm(Pm[:, :, c0:c0 + n], g)
-            else:
-                gemm(Pm[:, :, c0:c0 + n], g, dS, beta=1.0)
-            c0 += n
-        dsc = torch.empty_like(Pm)
-        lo = torch.empty_like(Pm) if Pm.dtype != torch.float32 else None
-        a = _colsm_args(dsc, Pm, lengths)  # dtype_in = dsc dtype, dtype_out = P dtype
-        a.dP, a.dp_rs, a.dp_bs = dP.data_ptr(), dP.stride(1), dP.stride(0)
-        a.dX, a.dx_rs, a.dx_bs = dsc.data_ptr(), dsc.stride(1), dsc.stride(0)
-        a.dX_lo = lo.data_ptr() if lo is not None else None
-        a.dtype_dp = _capi.dt(dP)
-        a.Dcol = Dcol.data_ptr() if HSP_DCOL else None
-        _capi.call("kl_colsoftmax_bwd", C.byref(a), _stream())
-        gemm(dsc, Q.unsqueeze(0).expand(S.shape[0], -1, -1), dS, beta=1.0)
-        # dQ = sum_b dsc^T S: softmax-VJP rows sum to zero over t, so this
-        # reduction cancels; bf16 runs it on the hi + lo split of dsc.
-        dQ = torch.zeros(1, 1, Q.shape[0], Q.shape[1], device=S.device, dtype=torch.float32)
-        gemm(dsc.transpose(1, 2).unsqueeze(0), S.unsqueeze(0), dQ, beta=1.0, reduce=(False, True))
-        if lo is not None:
-            gemm(lo.transpose(1, 2).unsqueeze(0), S.unsqueeze(0), dQ, beta=1.0, reduce=(False, True))
-        dQ = dQ.reshape(Q.shape)
-        return dS, dQ, None, None
+            dS, dQ = _hsp_fused_bwd(ctx, gs)
+        else:
+            dS, dQ = _hsp_gemm_bwd(ctx, gs)
+        if g_rec is not None:
+            _recent_bwd_into(dS, g_rec, ctx.saved_tensors[2])
+        if dS is not None and ctx.sink is not None:
+            if ctx.sink.t is dS:
+                dS = None  # accumulated into the sequence's shared gradient buffer
+            elif ctx.sink.t is None:
+                ctx.sink.t = dS
+        return dS, dQ, None, None, None, None
+
+
+def _hsp_gemm_bwd(ctx, gs):
+    """GEMM composition of the pooling VJP (fp32 parity path)."""
+    S, Q, lengths, Pm, *outs = ctx.saved_tensors
+    B, T, d = S.shape
+    HQ = Q.shape[0]
+    dP = torch.empty(B, T, HQ, device=S.device, dtype=torch.float32)
+    # D[b, c] = sum_t P dP = dO[c] . pooled[c]: the softmax-VJP column term
+    # from the (B, HQ, d) pooled output instead of a pass over T
+    Dcol = torch.empty(B, HQ, device=S.device, dtype=torch.float32)
+    dS = None
+    c0 = 0
+    for g, n, o in zip(gs, ctx.splits, outs):
+        g = torch.zeros(B, n, d, device=S.device, dtype=S.dtype) if g is None else g.contiguous()
+        Dcol[:, c0:c0 + n] = torch.linalg.vecdot(g.float(), o.float())
+        gemm(S, g.transpose(1, 2), dP[:, :, c0:c0 + n])
+        if dS is None:
+            dS = gemm(Pm[:, :, c0:c0 + n], g)
+        else:
+            gemm(Pm[:, :, c0:c0 + n], g, dS, beta=1.0)
+        c0 += n
+    dsc = torch.empty_like(Pm)
+    lo = torch.empty_like(Pm) if Pm.dtype != torch.float32 else None
+    a = _colsm_args(dsc, Pm, lengths)  # dtype_in = dsc dtype, dtype_out = P dtype
+    a.dP, a.dp_rs, a.dp_bs = dP.data_ptr(), dP.stride(1), dP.stride(0)
+    a.dX, a.dx_rs, a.dx_bs = dsc.data_ptr(), dsc.stride(1), dsc.stride(0)
+    a.dX_lo = lo.data_ptr() if lo is not None else None
+    a.dtype_dp = _capi.dt(dP)
+    a.Dcol = Dcol.data_ptr() if HSP_DCOL else None
+    _capi.call("kl_colsoftmax_bwd", C.byref(a), _stream())
+    gemm(dsc, Q.unsqueeze(0).expand(S.shape[0], -1, -1), dS, beta=1.0)
+    # dQ = sum_b dsc^T S: softmax-VJP rows sum to zero over t, so this
+    # reduction cancels; bf16 runs it on the hi + lo split of dsc.
+    dQ = torch.zeros(1, 1, Q.shape[0], Q.shape[1], device=S.device, dtype=torch.float32)
+    gemm(dsc.transpose(1, 2).unsqueeze(0), S.unsqueeze(0), dQ, beta=1.0, reduce=(False, True))
+    if lo is not None:
+        gemm(lo.transpose(1, 2).unsqueeze(0), S.unsqueeze(0), dQ, beta=1.0, reduce=(False, True))
+    dQ = dQ.reshape(Q.shape)
+    return dS, dQ
 
 
 HSP_FUSED = True  # tests flip this to A/B the fused tcgen05 pooling against the GEMM composition
@@ -443,27 +508,48 @@ def _hsp_fused_bwd(ctx, gs):
     dO = gl[0].contiguous() if len(gl) == 1 else torch.cat(gl, dim=1)
     O = outs[0] if len(outs) == 1 else torch.cat(outs, dim=1)
     Dq = torch.linalg.vecdot(dO.float(), O.float())  # rowsum(dO * pooled): the softmax-VJP term
-    dS = torch.empty_like(S)
+    acc = ctx.sink.take(S) if ctx.sink is not None else None
+    dS = acc if acc is not None else torch.empty_like(S)
     dZ = torch.empty(B, HQ, T, device=S.device, dtype=S.dtype)
     dZlo = torch.empty_like(dZ)
     a = _hsp_args(S, Q, lengths, HQ, dO, dO, LSE)
     a.dO1 = dO.data_ptr()
     a.dS, a.ds_rs, a.ds_bs = dS.data_ptr(), dS.stride(1), dS.stride(0)
+    a.accumulate_ds = 1 if acc is not None else 0
     a.dZ, a.dZ_lo, a.Dq = dZ.data_ptr(), dZlo.data_ptr(), Dq.data_ptr()
     _capi.call("kl_hsp_bwd", C.byref(a), _stream())
     dQ = torch.zeros(1, 1, HQ, d, device=S.device, dtype=torch.float32)
     gemm(dZ.unsqueeze(0), S.unsqueeze(0), dQ, beta=1.0, reduce=(False, True))
     gemm(dZlo.unsqueeze(0), S.unsqueeze(0), dQ, beta=1.0, reduce=(False, True))
-    return dS, dQ.reshape(Q.shape), None, None
+    return dS, dQ.reshape(Q.shape)
 
 
 HSP_DCOL = True  # softmax-VJP column term from the pooled output (tests A/B it against the t-reduction)
 
 
-def hsp_pool(S, Q, lengths, splits=None):
+def hsp_pool(S, Q, lengths, splits=None, n_recent=0, sink=None):
     """Pooled outputs, one (B, n, d) tensor per entry of ``splits`` (default:
-    all HQ rows in one)."""
-    return _HspPool.apply(S, Q, lengths, tuple(splits) if splits else (Q.shape[0],))
+    all HQ rows in one), then, if ``n_recent``, the recent rows (seqsum.py:
+    186-196) — one op, so the sequence gets one gradient buffer."""
+    return _HspPool.apply(S, Q, lengths, tuple(splits) if splits else (Q.shape[0],), int(n_recent), sink)
+
+
+def _recent_fwd(S, lengths, n):
+    B, T, d = S.shape
+    if not S.is_contiguous():
+        S = S.contiguous()
+    out = torch.empty(B, n, d, device=S.device, dtype=S.dtype)
+    _capi.call("kl_recent_rows_fwd", B, T, d, n, _capi.dt(S), S.data_ptr(), S.stride(0), lengths.data_ptr(),
+               out.data_ptr(), out.stride(0), _stream())
+    return out
+
+
+def _recent_bwd_into(dS, g, lengths):
+    """dS[b, len - n + r] += g[b, r] (kl_recent_rows_bwd accumulates)."""
+    B, T, d = dS.shape
+    g = g.contiguous()
+    _capi.call("kl_recent_rows_bwd", B, T, d, g.shape[1], _capi.dt(g), g.data_ptr(), g.stride(0),
+               lengths.data_ptr(), dS.data_ptr(), dS.stride(0), _stream())
 
 
 # ---------------------------------------------------------------------------

@@ -176,11 +176,14 @@ class KunlunModel:
             X, S_list = outs[0], list(outs[1:])
         xsum = summarize_nonseq(X, F.PRef(self.P, lp.pool)) if (not flags.skip_pffn and live_seq) else None
         H_list = []
+        # one shared dS buffer per event sequence: its consumers (the GDPA
+        # branch, HSP pooling + recent rows) accumulate into it
+        sinks = [F.GradSink() for _ in cfg.events]
         for e in range(len(cfg.events)):
             if flags.skip_hsp:
                 H_list.append(H_prev[e])
             else:
-                H_list.append(hsp_summarize(S_list[e], lp.summ[e], lengths[e]).rows())
+                H_list.append(hsp_summarize(S_list[e], lp.summ[e], lengths[e], sink=sinks[e]).rows())
         Xn = global_interaction(X, H_list, lp.gi)
         S_out = []
         for e, ev in enumerate(cfg.events):
@@ -188,7 +191,7 @@ class KunlunModel:
             if live_seq and not flags.skip_pffn:
                 k, v = generate_kv(xsum, lp.wg[e], cfg.gdpa_cfg(e))
                 kt, vt = fold_kv(k, v, lp.wg[e])
-                s = F.gdpa_core(s, kt, vt, lengths[e], cfg.gdpa_acts, cfg.n_kv, 1.0 / float(ev.T))
+                s = F.gdpa_core(s, kt, vt, lengths[e], cfg.gdpa_acts, cfg.n_kv, 1.0 / float(ev.T), sink=sinks[e])
             if live_seq and not flags.skip_self_attention:
                 s = mha_window(s, lp.mha[e], WindowSpec(ev.w, ev.causal), lengths[e])
             S_out.append(s)

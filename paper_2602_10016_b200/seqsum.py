@@ -209,10 +209,12 @@ def recent_rows(s, n_recent: int, lengths=None):
     return out.squeeze(0) if squeeze else out
 
 
-def hsp_summarize(s, p: SummarizerParams, lengths=None) -> SummaryBundle:
+def hsp_summarize(s, p: SummarizerParams, lengths=None, sink=None) -> SummaryBundle:
     """Full three-part summary [CLS | compressed seeds | recent]
     (seqsum.py:199-210).  The seed and CLS query sets pool over S in a single
-    kernel pass."""
+    kernel pass; the recent rows come from the same op, and ``sink`` (a
+    functional.GradSink) lets its S gradient accumulate into the buffer of
+    the sequence's other consumers."""
     squeeze = s.dim() == 2
     S = s.unsqueeze(0) if squeeze else s
     B, T, d = S.shape
@@ -232,14 +234,16 @@ def hsp_summarize(s, p: SummarizerParams, lengths=None) -> SummaryBundle:
     # projections run on B*n flattened rows
     q_rows = q_all.transpose(0, 1).reshape(n_q * H, d)
     splits = (n_s * H, n_cls * H) if n_cls > 0 else (n_s * H,)
-    pooled = F.hsp_pool(S, q_rows, lens, splits)
+    n_rec = p.split.n_recent
+    outs = F.hsp_pool(S, q_rows, lens, splits, n_recent=n_rec, sink=sink)
+    pooled = outs[:len(splits)]
     hseed = F.linear(F.head_proj(pooled[0].view(B, n_s, H, d), hp.attn.ref(2)), hp.P, hp.attn.wout)
     hsp_tok = sumkronlinear(hseed, hp)
     if n_cls > 0:
         cls_tok = F.linear(F.head_proj(pooled[1].view(B, n_cls, H, d), p.cls_attn.ref(2)), hp.P, p.cls_attn.wout)
     else:
         cls_tok = S.new_zeros(B, 0, d)
-    rec = F.recent_rows(S, lens, p.split.n_recent)
+    rec = outs[len(splits)] if n_rec > 0 else S.new_zeros(B, 0, d)
     bundle = SummaryBundle(cls_tok, hsp_tok, rec)
     if squeeze:
         bundle = SummaryBundle(cls_tok[0], hsp_tok[0], rec[0])
