@@ -58,8 +58,10 @@ unsigned long long kl_launch_count(void);
 int kl_tcgen05_available(void);
 /* Force the SIMT GEMM even for bf16 (debug / A-B testing).  0 = auto. */
 void kl_set_gemm_path(int path);
-/* Programmatic dependent launch of every library kernel (default off; env
- * KL_PDL=1 or kl_set_pdl(1) turns it on). */
+/* Programmatic dependent launch of every library kernel (default on; env
+ * KL_PDL=0 or kl_set_pdl(0) turns it off).  The tcgen05 kernels run their
+ * prologue (barrier init, TMEM alloc, tensor-map prefetch) before waiting on
+ * the previous kernel. */
 void kl_set_pdl(int on);
 /* Path the last kl_gemm call on this thread took: 1 tcgen05, 0 SIMT. */
 int kl_last_gemm_path(void);

@@ -67,11 +67,11 @@ void bind_device(cudaStream_t s) {
   if (dev >= 0) cudaSetDevice(dev);
 }
 
-static int g_pdl = -1;  // -1: from KL_PDL (default off: measured neutral on the c2 step)
+static int g_pdl = -1;  // -1: from KL_PDL (default on)
 bool pdl_enabled() {
   if (g_pdl < 0) {
     const char* v = getenv("KL_PDL");
-    g_pdl = (v && v[0] == '1') ? 1 : 0;
+    g_pdl = (v && v[0] == '0') ? 0 : 1;
   }
   return g_pdl == 1;
 }

@@ -22,9 +22,10 @@ bool pdl_enabled();
 void bind_device(cudaStream_t s);
 
 // ---- launches: programmatic dependent launch (PDL) --------------------------
-// Every kernel of the library starts with KL_PDL_ENTRY() and, when PDL is on
-// (kl_set_pdl / KL_PDL=1), is launched with programmatic stream
-// serialization: it lets the next kernel in the
+// Every kernel of the library calls KL_PDL_ENTRY() before its first global
+// memory access and, when PDL is on (default; kl_set_pdl / KL_PDL=0 turns it
+// off), is launched with programmatic stream serialization: it lets the next
+// kernel in the
 // stream be scheduled while this one drains, and waits (griddepcontrol.wait)
 // for the full completion + memory flush of its predecessor before touching
 // global memory.  Inside a captured CUDA graph the launch becomes a

@@ -5,4 +5,4 @@ timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu > gpurun_out/bench.js
 python -c "import json; d=json.load(open('gpurun_out/bench.json')); print('value', d['value'], 'ms', d['ms_per_step'], 'mfu', d['mfu']['value'], 'e2e', d['e2e']['value'])"
 tail -3 gpurun_out/bench.err
 timeout 600 python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --op-census > /dev/null 2> gpurun_out/census.err; echo census rc $?
-KL_PDL=1 timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu --no-e2e > gpurun_out/bench_nopdl.json 2>/dev/null; python -c "import json; d=json.load(open('gpurun_out/bench_nopdl.json')); print('PDL value', d['value'], 'ms', d['ms_per_step'])"
+KL_PDL=0 timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu --no-e2e > gpurun_out/bench_nopdl.json 2>/dev/null; python -c "import json; d=json.load(open('gpurun_out/bench_nopdl.json')); print('NO-PDL value', d['value'], 'ms', d['ms_per_step'])"
