@@ -260,6 +260,14 @@ int kl_colsoftmax_bwd(const kl_colsoftmax_args* args, void* stream);
 int kl_rmsnorm_fwd(int rows, int d, float eps, const float* x, const float* gain, float* y, void* stream);
 int kl_rmsnorm_bwd(int rows, int d, float eps, const float* x, const float* gain, const float* dy,
                    float* dx, float* dgain, void* stream);
+/* Batched forms: nb independent (rows, d) problems, element batch strides;
+ * the backward writes (accumulate = 0) or adds into (accumulate = 1) dx and
+ * dgain. */
+int kl_rmsnorm_fwd_b(int nb, int rows, int d, float eps, const float* x, long long x_bs, const float* gain,
+                     long long g_bs, float* y, long long y_bs, void* stream);
+int kl_rmsnorm_bwd_b(int nb, int rows, int d, float eps, const float* x, long long x_bs, const float* gain,
+                     long long g_bs, const float* dy, long long dy_bs, float* dx, long long dx_bs, float* dgain,
+                     long long dg_bs, int accumulate, void* stream);
 
 /* recent_rows (seqsum.py:186-196): out[b, r] = S[b, len-n+r] for len-n+r >= 0
  * else 0; dtype_s for S/out.  bwd accumulates into dS (dS[b, t] += dOut[b, r]). */

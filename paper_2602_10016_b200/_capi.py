@@ -121,6 +121,11 @@ _SIGS = {
     "kl_colsoftmax_bwd": ([C.POINTER(ColSoftmaxArgs), C.c_void_p], C.c_int),
     "kl_rmsnorm_fwd": ([C.c_int, C.c_int, C.c_float, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "kl_rmsnorm_bwd": ([C.c_int, C.c_int, C.c_float] + [C.c_void_p] * 6, C.c_int),
+    "kl_rmsnorm_fwd_b": ([C.c_int, C.c_int, C.c_int, C.c_float, C.c_void_p, C.c_longlong, C.c_void_p, C.c_longlong,
+                          C.c_void_p, C.c_longlong, C.c_void_p], C.c_int),
+    "kl_rmsnorm_bwd_b": ([C.c_int, C.c_int, C.c_int, C.c_float, C.c_void_p, C.c_longlong, C.c_void_p, C.c_longlong,
+                          C.c_void_p, C.c_longlong, C.c_void_p, C.c_longlong, C.c_void_p, C.c_longlong, C.c_int,
+                          C.c_void_p], C.c_int),
     "kl_recent_rows_fwd": ([C.c_int] * 5 + [C.c_void_p, C.c_longlong, C.c_void_p, C.c_void_p, C.c_longlong, C.c_void_p], C.c_int),
     "kl_recent_rows_bwd": ([C.c_int] * 5 + [C.c_void_p, C.c_longlong, C.c_void_p, C.c_void_p, C.c_longlong, C.c_void_p], C.c_int),
     "kl_gram_triu_fwd": ([C.c_int] * 4 + [C.c_void_p, C.c_longlong, C.c_longlong, C.c_void_p, C.c_longlong, C.c_void_p], C.c_int),

@@ -168,8 +168,12 @@ __device__ double block_sum_d(double v, double* sh) {
 }
 
 // rms_norm (tensor.py:552-556): one block per row.
-__global__ void rmsnorm_fwd_kernel(int d, float eps, const float* x, const float* gain, float* y) {
+__global__ void rmsnorm_fwd_kernel(int d, float eps, const float* x, const float* gain, float* y, long long x_bs,
+                                   long long g_bs, long long y_bs) {
   KL_PDL_ENTRY();
+  x += blockIdx.y * x_bs;
+  gain += blockIdx.y * g_bs;
+  y += blockIdx.y * y_bs;
   __shared__ float sh[32];
   const float* xr = x + (long long)blockIdx.x * d;
   float ss = 0.f;
@@ -185,8 +189,15 @@ __global__ void rmsnorm_fwd_kernel(int d, float eps, const float* x, const float
 // dgain in fp64.
 __global__ void __launch_bounds__(256) rmsnorm_bwd_kernel(int rows, int d, float eps, const float* x,
                                                          const float* gain, const float* dy, float* dx,
-                                                         float* dgain) {
+                                                         float* dgain, long long x_bs, long long g_bs,
+                                                         long long dy_bs, long long dx_bs, long long dg_bs,
+                                                         int acc) {
   KL_PDL_ENTRY();
+  x += blockIdx.x * x_bs;
+  gain += blockIdx.x * g_bs;
+  dy += blockIdx.x * dy_bs;
+  dx += blockIdx.x * dx_bs;
+  dgain += blockIdx.x * dg_bs;
   extern __shared__ float rs[];  // s[rows], k[rows]
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   for (int r = w; r < rows; r += blockDim.x >> 5) {
@@ -214,10 +225,11 @@ __global__ void __launch_bounds__(256) rmsnorm_bwd_kernel(int rows, int d, float
     const float gc = gain[c];
     for (int r = 0; r < rows; ++r) {
       const float xv = x[(long long)r * d + c], gv = dy[(long long)r * d + c];
-      dx[(long long)r * d + c] = rs[r] * gv * gc - rs[rows + r] * xv;
+      const float v = rs[r] * gv * gc - rs[rows + r] * xv;
+      dx[(long long)r * d + c] = acc ? dx[(long long)r * d + c] + v : v;
       dg += (double)gv * (double)xv * (double)rs[r];
     }
-    dgain[c] = (float)dg;
+    dgain[c] = acc ? dgain[c] + (float)dg : (float)dg;
   }
 }
 
@@ -466,19 +478,31 @@ extern "C" int kl_colsoftmax_bwd(const kl_colsoftmax_args* a, void* stream) {
 }
 
 extern "C" int kl_rmsnorm_fwd(int rows, int d, float eps, const float* x, const float* gain, float* y, void* stream) {
-  if (rows <= 0 || d <= 0) return KL_OK;
-  launch_k(rmsnorm_fwd_kernel, rows, 256, 0, (cudaStream_t)stream, d, eps, x, gain, y);
+  return kl_rmsnorm_fwd_b(1, rows, d, eps, x, 0, gain, 0, y, 0, stream);
+}
+
+extern "C" int kl_rmsnorm_fwd_b(int nb, int rows, int d, float eps, const float* x, long long x_bs, const float* gain,
+                                long long g_bs, float* y, long long y_bs, void* stream) {
+  if (nb <= 0 || rows <= 0 || d <= 0) return KL_OK;
+  launch_k(rmsnorm_fwd_kernel, dim3(rows, nb), 256, 0, (cudaStream_t)stream, d, eps, x, gain, y, x_bs, g_bs, y_bs);
   count_launch();
   return launch_check("rmsnorm_fwd");
 }
 
 extern "C" int kl_rmsnorm_bwd(int rows, int d, float eps, const float* x, const float* gain, const float* dy,
                               float* dx, float* dgain, void* stream) {
-  if (d <= 0) return KL_OK;
+  return kl_rmsnorm_bwd_b(1, rows, d, eps, x, 0, gain, 0, dy, 0, dx, 0, dgain, 0, 0, stream);
+}
+
+extern "C" int kl_rmsnorm_bwd_b(int nb, int rows, int d, float eps, const float* x, long long x_bs, const float* gain,
+                                long long g_bs, const float* dy, long long dy_bs, float* dx, long long dx_bs,
+                                float* dgain, long long dg_bs, int accumulate, void* stream) {
+  if (nb <= 0 || d <= 0) return KL_OK;
   if (rows > 8192) { set_error("kl_rmsnorm_bwd: rows %d > 8192", rows); return KL_EUNSUPPORTED; }
   const size_t sm = 2 * (size_t)std::max(rows, 1) * sizeof(float);
   if (sm > 48 * 1024) cudaFuncSetAttribute(rmsnorm_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  launch_k(rmsnorm_bwd_kernel, 1, 256, sm, (cudaStream_t)stream, rows, d, eps, x, gain, dy, dx, dgain);
+  launch_k(rmsnorm_bwd_kernel, nb, 256, sm, (cudaStream_t)stream, rows, d, eps, x, gain, dy, dx, dgain, x_bs, g_bs,
+           dy_bs, dx_bs, dg_bs, accumulate);
   count_launch();
   return launch_check("rmsnorm_bwd");
 }

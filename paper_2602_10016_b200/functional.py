@@ -553,6 +553,100 @@ def _recent_bwd_into(dS, g, lengths):
 
 
 # ---------------------------------------------------------------------------
+class _QueryFolds(torch.autograd.Function):
+    """The batch-shared HSP seed / CLS query folds of several layers at once
+    (seqsum.py:96-102, 26-34 with attention.py:85-89):
+        seeds: Qt[l, q, h] = (RMSNorm(E_l) g_l)[q] W_q,l^h^T W_k,l^h * scale
+        CLS:   Qt[l, q, h] = c_l[q] W_q,l'^h^T W_k,l'^h * scale
+    as batched fp32 GEMMs over the layers (the per-layer parameter blocks are
+    uniformly spaced in the flat buffer), rows ordered (query, head).  The
+    backward runs once, after every layer's pooling backward, and writes the
+    parameter gradients straight into the gradient buffer."""
+
+    @staticmethod
+    def forward(ctx, flat, P, keys, H, d_h, eps):
+        seeds_k, gain_k, wqkv_k, cls_k, cw_k = keys
+        E = P.stacked(seeds_k, "w32")
+        G = P.stacked(gain_k, "w32")
+        W = P.stacked(wqkv_k, "w32")
+        L, n_s, d = E.shape
+        Hd = H * d_h
+        scale = 1.0 / float(d_h) ** 0.5
+        xs = torch.empty(L, n_s, d, device=E.device, dtype=torch.float32)
+        _capi.call("kl_rmsnorm_fwd_b", L, n_s, d, eps, E.data_ptr(), E.stride(0), G.data_ptr(), G.stride(0),
+                   xs.data_ptr(), n_s * d, _stream())
+        n_cls = P.shape(cls_k[0])[0] if cls_k else 0
+        n_q = n_s + n_cls
+        Q = torch.empty(L, n_q, H, d, device=E.device, dtype=torch.float32)
+        qh_s = gemm(xs, W[:, :Hd].transpose(1, 2))  # (L, n_s, H*d_h)
+        gemm(qh_s.view(L, n_s, H, d_h).permute(0, 2, 1, 3), W[:, Hd:2 * Hd].view(L, H, d_h, d),
+             Q[:, :n_s].permute(0, 2, 1, 3), alpha=scale)
+        qh_c = None
+        if n_cls:
+            Cq = P.stacked(cls_k, "w32")
+            CW = P.stacked(cw_k, "w32")
+            qh_c = gemm(Cq, CW[:, :Hd].transpose(1, 2))
+            gemm(qh_c.view(L, n_cls, H, d_h).permute(0, 2, 1, 3), CW[:, Hd:2 * Hd].view(L, H, d_h, d),
+                 Q[:, n_s:].permute(0, 2, 1, 3), alpha=scale)
+        ctx.P, ctx.keys, ctx.H, ctx.d_h, ctx.eps = P, keys, H, d_h, eps
+        ctx.save_for_backward(xs, qh_s, qh_c)
+        Qr = Q.view(L, n_q * H, d)
+        return tuple(Qr[l] for l in range(L))
+
+    @staticmethod
+    def backward(ctx, *gs):
+        P, (seeds_k, gain_k, wqkv_k, cls_k, cw_k) = ctx.P, ctx.keys
+        xs, qh_s, qh_c = ctx.saved_tensors
+        H, d_h = ctx.H, ctx.d_h
+        L, n_s, d = xs.shape
+        Hd = H * d_h
+        scale = 1.0 / float(d_h) ** 0.5
+        n_q = gs[0].shape[0] // H if gs[0] is not None else n_s + (P.shape(cls_k[0])[0] if cls_k else 0)
+        dQ = torch.stack([torch.zeros(n_q * H, d, device=xs.device) if g is None else g for g in gs]).view(L, n_q, H, d)
+
+        def fold_bwd(dQs, qh, n, W, gW):
+            """dQs (L, H, n, d), qh (L, n, H*d_h): dW_k += scale qh^T dQ; returns
+            dqh = scale dQ W_k^T as (L, n, H*d_h)."""
+            dqh = torch.empty(L, n, H, d_h, device=xs.device, dtype=torch.float32)
+            gemm(dQs, W[:, Hd:2 * Hd].view(L, H, d_h, d).transpose(2, 3), dqh.permute(0, 2, 1, 3), alpha=scale)
+            gemm(qh.view(L, n, H, d_h).permute(0, 2, 3, 1), dQs, gW[:, Hd:2 * Hd].view(L, H, d_h, d),
+                 alpha=scale, beta=1.0)
+            return dqh.view(L, n, Hd)
+
+        # seeds
+        W = P.stacked(wqkv_k, "w32")
+        gW = P.stacked(wqkv_k, "g")
+        dq2 = fold_bwd(dQ[:, :n_s].permute(0, 2, 1, 3), qh_s, n_s, W, gW)
+        gemm(dq2.transpose(1, 2), xs, gW[:, :Hd], beta=1.0)  # dW_q
+        dxs = gemm(dq2, W[:, :Hd])  # (L, n_s, d)
+        E = P.stacked(seeds_k, "w32")
+        G = P.stacked(gain_k, "w32")
+        gE = P.stacked(seeds_k, "g")
+        gG = P.stacked(gain_k, "g")
+        _capi.call("kl_rmsnorm_bwd_b", L, n_s, d, ctx.eps, E.data_ptr(), E.stride(0), G.data_ptr(), G.stride(0),
+                   dxs.data_ptr(), n_s * d, gE.data_ptr(), gE.stride(0), gG.data_ptr(), gG.stride(0), 1, _stream())
+        if cls_k:
+            n_cls = P.shape(cls_k[0])[0]
+            CW = P.stacked(cw_k, "w32")
+            gCW = P.stacked(cw_k, "g")
+            Cq = P.stacked(cls_k, "w32")
+            dqc = fold_bwd(dQ[:, n_s:].permute(0, 2, 1, 3), qh_c, n_cls, CW, gCW)
+            gemm(dqc.transpose(1, 2), Cq, gCW[:, :Hd], beta=1.0)
+            gemm(dqc, CW[:, :Hd], P.stacked(cls_k, "g"), beta=1.0)
+        return None, None, None, None, None, None
+
+
+def query_folds(P, keys, H, d_h, eps=1e-6):
+    """Per-layer (HQ, d) fp32 query rows of every layer in ``keys`` (lists of
+    per-layer registry block keys), see _QueryFolds; None if the blocks are
+    not uniformly spaced."""
+    for ks in keys:
+        if ks and P.stacked(ks, "w32") is None:
+            return None
+    return _QueryFolds.apply(P.flat, P, keys, int(H), int(d_h), float(eps))
+
+
+# ---------------------------------------------------------------------------
 class _RmsNorm(torch.autograd.Function):
     """rms_norm (tensor.py:552-556) on a batch-shared fp32 parameter block;
     dgain is written straight into the gradient buffer."""

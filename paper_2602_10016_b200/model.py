@@ -24,6 +24,7 @@ from .seqsum import SummarizerParams, SummarySplit, hsp_summarize
 from .tensor import Params, ShapeError
 
 DEFAULT_ACTIVATION_CYCLE = ("silu", "relu", "identity", "tanh")
+FOLD_ALL_LAYERS = True  # fold every layer's HSP/CLS queries in one batched pass (tests A/B it)
 
 
 @dataclass
@@ -162,7 +163,28 @@ class KunlunModel:
         self.layer_hook = None  # set by dist.GradReducer
 
     # ------------------------------------------------------------------
-    def layer_forward(self, l: int, flags: LayerSkipFlags, X, S_list, lengths, H_prev, live_seq=True):
+    def query_rows(self):
+        """{(layer, event): (HQ, d) fp32 query rows} of every layer that runs
+        HSP, folded for all those layers at once per event
+        (functional.query_folds); {} if the layout does not allow it."""
+        cfg = self.cfg
+        out = {}
+        layers = [l for l in range(cfg.L) if not self.flags[l].skip_hsp]
+        if not layers:
+            return out
+        for e in range(len(cfg.events)):
+            sp = [self.layers[l].summ[e] for l in layers]
+            keys = ([s.hsp.seeds for s in sp], [s.hsp.gain for s in sp], [s.hsp.attn.wqkv for s in sp],
+                    [s.cls_queries for s in sp] if sp[0].cls_queries else [],
+                    [s.cls_attn.wqkv for s in sp] if sp[0].cls_queries else [])
+            qs = F.query_folds(self.P, keys, cfg.heads, cfg.d // cfg.heads)
+            if qs is None:
+                return {}
+            for l, q in zip(layers, qs):
+                out[(l, e)] = q
+        return out
+
+    def layer_forward(self, l: int, flags: LayerSkipFlags, X, S_list, lengths, H_prev, live_seq=True, qrows=None):
         """One Kunlun layer (Alg. 1), batched.  ``live_seq=False`` skips the
         sequence branch (GDPA + SWA) when its output cannot reach the loss
         (liveness pruning); the returned S' is then
@@ -183,7 +205,8 @@ class KunlunModel:
             if flags.skip_hsp:
                 H_list.append(H_prev[e])
             else:
-                H_list.append(hsp_summarize(S_list[e], lp.summ[e], lengths[e], sink=sinks[e]).rows())
+                qr = qrows.get((l, e)) if qrows else None
+                H_list.append(hsp_summarize(S_list[e], lp.summ[e], lengths[e], sink=sinks[e], q_rows=qr).rows())
         Xn = global_interaction(X, H_list, lp.gi)
         S_out = []
         for e, ev in enumerate(cfg.events):
@@ -210,8 +233,9 @@ class KunlunModel:
         live = self.seq_live() if prune_dead else [True] * self.cfg.L
         H = None
         outs = []
+        qrows = self.query_rows() if FOLD_ALL_LAYERS else None
         for l in range(self.cfg.L):
-            X, S_list, H = self.layer_forward(l, self.flags[l], X, S_list, lengths, H, live_seq=live[l])
+            X, S_list, H = self.layer_forward(l, self.flags[l], X, S_list, lengths, H, live_seq=live[l], qrows=qrows)
             if keep_outputs:
                 outs.append((X, list(S_list), list(H)))
         B = X.shape[0]

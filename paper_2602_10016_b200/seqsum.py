@@ -209,7 +209,7 @@ def recent_rows(s, n_recent: int, lengths=None):
     return out.squeeze(0) if squeeze else out
 
 
-def hsp_summarize(s, p: SummarizerParams, lengths=None, sink=None) -> SummaryBundle:
+def hsp_summarize(s, p: SummarizerParams, lengths=None, sink=None, q_rows=None) -> SummaryBundle:
     """Full three-part summary [CLS | compressed seeds | recent]
     (seqsum.py:199-210).  The seed and CLS query sets pool over S in a single
     kernel pass; the recent rows come from the same op, and ``sink`` (a
@@ -221,18 +221,19 @@ def hsp_summarize(s, p: SummarizerParams, lengths=None, sink=None) -> SummaryBun
     lens = _lengths(S, lengths)
     hp = p.hsp
     H = hp.attn.heads
-    qs = hsp_queries(hp)  # (H, n_s, d)
     n_s = hp.n_seeds
     n_cls = p.split.n_cls
-    if n_cls > 0:
-        qc = shared_queries(F.PRef(hp.P, p.cls_queries), p.cls_attn)  # (H, n_cls, d)
-        q_all = torch.cat([qs, qc], dim=1)
-    else:
-        q_all = qs
     n_q = n_s + n_cls
-    # query rows ordered (query, head): each pooled set is (B, n, H, d) and its
-    # projections run on B*n flattened rows
-    q_rows = q_all.transpose(0, 1).reshape(n_q * H, d)
+    if q_rows is None:  # (the model folds every layer's queries at once: functional.query_folds)
+        qs = hsp_queries(hp)  # (H, n_s, d)
+        if n_cls > 0:
+            qc = shared_queries(F.PRef(hp.P, p.cls_queries), p.cls_attn)  # (H, n_cls, d)
+            q_all = torch.cat([qs, qc], dim=1)
+        else:
+            q_all = qs
+        # query rows ordered (query, head): each pooled set is (B, n, H, d) and
+        # its projections run on B*n flattened rows
+        q_rows = q_all.transpose(0, 1).reshape(n_q * H, d)
     splits = (n_s * H, n_cls * H) if n_cls > 0 else (n_s * H,)
     n_rec = p.split.n_recent
     outs = F.hsp_pool(S, q_rows, lens, splits, n_recent=n_rec, sink=sink)

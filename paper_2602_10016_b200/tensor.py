@@ -132,6 +132,28 @@ class Params:
             _capi.call("kl_cast", self.flat.numel(), _capi.KL_F32, self.flat.data_ptr(), _capi.KL_BF16,
                        self.flat_c.data_ptr(), _capi._stream())
 
+    def stacked(self, keys, which: str = "w"):
+        """(len(keys),) + shape view over equally-shaped blocks whose offsets
+        are uniformly spaced in the flat buffers (e.g. one block per layer:
+        every layer creates its parameters in the same order), so a batched
+        GEMM can address all of them; ``which`` = "w" (compute dtype), "w32"
+        or "g".  None if the blocks are not uniformly spaced."""
+        offs = [self._blocks[k][0] for k in keys]
+        shape = self._blocks[keys[0]][1]
+        if any(self._blocks[k][1] != shape for k in keys):
+            return None
+        st = offs[1] - offs[0] if len(offs) > 1 else int(np.prod(shape)) if shape else 1
+        if st <= 0 or any(offs[i + 1] - offs[i] != st for i in range(len(offs) - 1)):
+            return None
+        base = {"w": self.flat_c if self.flat_c is not None else self.flat.detach(), "w32": self.flat.detach(),
+                "g": self.gflat}[which]
+        inner = []
+        acc = 1
+        for dim in reversed(shape):
+            inner.insert(0, acc)
+            acc *= dim
+        return base.as_strided((len(keys),) + tuple(shape), (st,) + tuple(inner), offs[0])
+
     def zero_grad(self) -> None:
         self.gflat.zero_()
 
