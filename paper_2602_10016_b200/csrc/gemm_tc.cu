@@ -1,3 +1,4 @@
+#include <cstdio>
 // Persistent, warp-specialized tcgen05 GEMM for sm_100a (bf16 x bf16 -> fp32
 // in TMEM) with the generic kl_gemm epilogue.
 //
@@ -328,10 +329,39 @@ __device__ __forceinline__ void act32(int code, float* v) {
   }
 }
 
+__device__ __forceinline__ void ld8_row(const float* p, float* o) {
+  const float4 a = *reinterpret_cast<const float4*>(p), b = *reinterpret_cast<const float4*>(p + 4);
+  o[0] = a.x; o[1] = a.y; o[2] = a.z; o[3] = a.w; o[4] = b.x; o[5] = b.y; o[6] = b.z; o[7] = b.w;
+}
+__device__ __forceinline__ void ld8_row(const bf16* p, float* o) {
+  const uint4 u = *reinterpret_cast<const uint4*>(p);
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[k]));
+    o[2 * k] = f.x;
+    o[2 * k + 1] = f.y;
+  }
+}
+__device__ __forceinline__ void st8_row(float* p, const float* v, bool live) {
+  *reinterpret_cast<float4*>(p) = live ? make_float4(v[0], v[1], v[2], v[3]) : make_float4(0.f, 0.f, 0.f, 0.f);
+  *reinterpret_cast<float4*>(p + 4) = live ? make_float4(v[4], v[5], v[6], v[7]) : make_float4(0.f, 0.f, 0.f, 0.f);
+}
+__device__ __forceinline__ void st8_row(bf16* p, const float* v, bool live) {
+  uint4 u = make_uint4(0u, 0u, 0u, 0u);
+  if (live) {
+    u.x = tc::pack_bf16(v[0], v[1]);
+    u.y = tc::pack_bf16(v[2], v[3]);
+    u.z = tc::pack_bf16(v[4], v[5]);
+    u.w = tc::pack_bf16(v[6], v[7]);
+  }
+  *reinterpret_cast<uint4*>(p) = u;
+}
+
 template <typename TC, bool FULL>
 __device__ __forceinline__ void epi_tma(const TcParams& p, const Epi& e, const CUtensorMap* tmC, uint32_t tbase,
                                         uint8_t* stg, float* bsm, int mb, int nb, int zc2, int zc1, int lane_base,
-                                        int lim, const uint8_t* Rs, int& nbox) {
+                                        int lim, const uint8_t* Rs, int& nbox, TC* X) {
   const int lane = threadIdx.x & 31;
   constexpr int SPB = 128 / (int)sizeof(TC) / 32;  // 32-column slabs per 128-byte box row: 2 bf16, 1 fp32
   const int row = lane_base + lane;
@@ -356,6 +386,24 @@ __device__ __forceinline__ void epi_tma(const TcParams& p, const Epi& e, const C
     tc::tmem_ld32(tbase + c, v);
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] *= e.alpha;
+    // aux (pre-activation) row segment of this slab: thread = row, 32 columns
+    const int m_row = mb * BM + row, n0 = nb * p.BN + c;
+    TC* xrow = (FULL && e.aux_mode && m_row < p.M) ? X + (long long)m_row * p.c_rs + n0 : nullptr;
+    if (FULL && e.aux_mode == 2 && xrow) {  // backward: v *= act'(pre-activation)
+      float a[32];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (n0 + 8 * q + 8 <= p.N) {
+          ld8_row(xrow + 8 * q, a + 8 * q);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) a[8 * q + i] = n0 + 8 * q + i < p.N ? ldf(xrow + 8 * q + i) : 0.f;
+        }
+      }
+      const int code = epi_code(e, n0);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] *= act_deriv(code, a[i]);
+    }
     if (FULL) {
       if (e.bias) {
 #pragma unroll
@@ -367,7 +415,19 @@ __device__ __forceinline__ void epi_tma(const TcParams& p, const Epi& e, const C
           v[4 * q + 3] += b4.w;
         }
       }
-      if (e.n_act) act32(epi_code(e, nb * p.BN + c), v);  // slab-uniform (host-checked)
+      if (e.aux_mode == 1 && xrow) {  // forward: keep the pre-activation for the backward
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (n0 + 8 * q + 8 <= p.N) {
+            st8_row(xrow + 8 * q, v + 8 * q, live);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              if (n0 + 8 * q + i < p.N) stf(xrow + 8 * q + i, live ? v[8 * q + i] : 0.f);
+          }
+        }
+      }
+      if (e.n_act && e.aux_mode != 2) act32(epi_code(e, nb * p.BN + c), v);  // slab-uniform (host-checked)
     }
     if (Rs) {
 #pragma unroll
@@ -599,7 +659,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         epi_tma<TC, MODE == 3>(p, e, &tmC, tbase, reinterpret_cast<uint8_t*>(stage_s) + (warp - 2) * 8192,
                                reinterpret_cast<float*>(rempty + 2 + 2) + (warp - 2) * 256, mb, nb,
-                    p.c_has2 ? z2o : 0, p.c_has1 ? z1o : 0, lane_base, lim, Rs, nbox);
+                    p.c_has2 ? z2o : 0, p.c_has1 ? z1o : 0, lane_base, lim, Rs, nbox, X);
       } else
       for (int c0 = 0; c0 < p.BN; c0 += 64) {
         // TMEM (thread = row) -> smem transpose -> each lane owns a column
@@ -737,6 +797,23 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
   if (gemm_path() != 2 && (long long)g0.M * g0.N * g0.K * g0.nb1 * g0.nb2 < (1ll << 18)) return KL_EUNSUPPORTED;
   GemmDesc g = g0;
   Epi e = e0;
+  // column-major C with an element-wise-free epilogue: compute C^T = B^T A^T
+  // instead, so C rows are contiguous for the TMA-store epilogue (operand
+  // majors swap roles; the kernel takes either major for A and B)
+  if (g.c_cs != 1 && g.c_rs == 1 && !e.bias && !e.aux_mode && e.n_act == 0 && !e.row_limit && !g.R) {
+    std::swap(g.M, g.N);
+    std::swap(g.A, g.B);
+    const long long ars = g.a_rs, acs = g.a_cs, as1 = g.a_s1, as2 = g.a_s2;
+    g.a_rs = g.b_cs;
+    g.a_cs = g.b_rs;
+    g.a_s1 = g.b_s1;
+    g.a_s2 = g.b_s2;
+    g.b_rs = acs;
+    g.b_cs = ars;
+    g.b_s1 = as1;
+    g.b_s2 = as2;
+    std::swap(g.c_rs, g.c_cs);
+  }
   // C += ... on a bf16 output is the residual epilogue with R = C
   if (g.c_dtype == KL_BF16 && e.beta == 1.f && !g.R) {
     g.R = g.C;
@@ -766,8 +843,8 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
   auto split_n = [&](int cap) {
     int tn = (g.N + cap - 1) / cap;
     int b = (g.N + tn - 1) / tn;
-    b = (b + 15) / 16 * 16;
-    return b < 16 ? 16 : b;
+    b = (b + 31) / 32 * 32;  // 32-column slabs (TMA-store epilogue)
+    return b;
   };
   int bn = split_n(bn_max);
   // Split-K plan for a tile count: weight-gradient shapes (few output tiles,
@@ -845,14 +922,16 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
   p.a_stage_bytes = BM * BK * 2;
   p.b_stage_bytes = b_n ? p.b_boxes * 64 * BK * 2 : bn * BK * 2;
   const uint32_t stage = p.a_stage_bytes + p.b_stage_bytes;
-  // MODE 2 (TMA-store epilogue): contiguous, 16-byte aligned C rows, no aux
-  // output, N tiles in 32-column slabs; fp32 C only plain (beta 0) or
+  // MODE 2 (TMA-store epilogue): contiguous, 16-byte aligned C rows (and aux
+  // rows, written / read per thread-row beside the TMA store), N tiles in
+  // 32-column slabs; fp32 C only plain (beta 0) or
   // accumulate-only (beta 1 -> TMA reduce-add).
   const int esz_c = g.c_dtype == KL_BF16 ? 2 : 4;
   const bool accum_only0 = g.c_dtype == KL_F32 && e.beta == 1.f && !e.bias && !e.row_limit && !e.aux_mode &&
                            e.n_act == 0 && !g.R;
   bool mode2 = !getenv_flag_epi1() && g.c_cs == 1 && ((uintptr_t)g.C & 15) == 0 && (g.c_rs * esz_c) % 16 == 0 &&
-               (g.c_s1 * esz_c) % 16 == 0 && (g.c_s2 * esz_c) % 16 == 0 && !e.aux_mode && bn % 32 == 0 &&
+               (g.c_s1 * esz_c) % 16 == 0 && (g.c_s2 * esz_c) % 16 == 0 &&
+               (!e.aux_mode || (g.aux && ((uintptr_t)g.aux & 15) == 0)) && bn % 32 == 0 &&
                (g.c_dtype == KL_BF16 ? e.beta == 0.f : (e.beta == 0.f && !g.R) || accum_only0) &&
                (!g.R || use_r) && (e.n_act <= 1 || (e.act_group > 0 && e.act_group % 32 == 0));
   if (use_r) {
@@ -929,12 +1008,21 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
   const int grid = std::min(total, num_sms());
   const bool plain = e.alpha == 1.f && e.beta == 0.f && !e.bias && !e.row_limit && !e.aux_mode && e.n_act == 0 &&
                      !g.R;
+  {
+    static int trace = -1;
+    if (trace < 0) trace = getenv("KL_GEMM_TRACE") ? 1 : 0;
+    if (trace)
+      fprintf(stderr, "gemm_tc M=%d N=%d K=%d nb=%dx%d red=%d%d c=%s beta=%g bias=%d aux=%d act=%d/%d R=%d lim=%d "
+              "mode2=%d bn=%d splits=%d ws=%d\n", g.M, g.N, g.K, g.nb1, g.nb2, g.red1, g.red2,
+              g.c_dtype == KL_BF16 ? "bf16" : "f32", e.beta, e.bias != nullptr, e.aux_mode, e.n_act, e.act_group,
+              g.R != nullptr, e.row_limit != nullptr, (int)mode2, bn, p.splits, p.ws != nullptr);
+  }
   auto launch = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     launch_k(kern, grid, NTHREADS, smem, s, ta, tb, use_r ? tr : ta, mode2 ? tc_map : ta, p, e);
   };
   if (mode2 && !p.ws) {
-    const bool full = e.bias || e.n_act;
+    const bool full = e.bias || e.n_act || e.aux_mode;
     if (g.c_dtype == KL_BF16) full ? launch(gemm_tc_kernel<bf16, 3>) : launch(gemm_tc_kernel<bf16, 2>);
     else full ? launch(gemm_tc_kernel<float, 3>) : launch(gemm_tc_kernel<float, 2>);
   } else if (g.c_dtype == KL_BF16) {

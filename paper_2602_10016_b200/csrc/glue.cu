@@ -264,19 +264,84 @@ __global__ void recent_bwd_kernel(int B, int T_, int d, int n, const T* dout, lo
 // triu_flatten(x x^T) (interaction.py:63-76, 117): np.triu_indices row-major.
 __device__ __forceinline__ int triu_index(int r, int c, int n) { return r * n - r * (r - 1) / 2 + (c - r); }
 
-// One block per sample: x[b] (n x d) staged in smem as fp32; one warp per
-// pair (lanes split the d-length dot product).
+// One block per sample: x[b] (n x d) staged in smem as fp32 (rows padded by 4
+// floats); one warp per pair (lanes split the d-length dot product).  With
+// VEC the rows are read as 16-byte vectors, all of a thread's loads issued
+// before any smem store (the scalar staging loop serialised one global-load
+// latency per element).
 template <typename T>
+__device__ __forceinline__ void ld8(const T* p, float* o);
+template <>
+__device__ __forceinline__ void ld8<float>(const float* p, float* o) {
+  float4 a = *reinterpret_cast<const float4*>(p), b = *reinterpret_cast<const float4*>(p + 4);
+  o[0] = a.x; o[1] = a.y; o[2] = a.z; o[3] = a.w; o[4] = b.x; o[5] = b.y; o[6] = b.z; o[7] = b.w;
+}
+template <>
+__device__ __forceinline__ void ld8<bf16>(const bf16* p, float* o) {
+  uint4 u = *reinterpret_cast<const uint4*>(p);
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 f = __bfloat1622float2(h[i]);
+    o[2 * i] = f.x;
+    o[2 * i + 1] = f.y;
+  }
+}
+template <typename T>
+__device__ __forceinline__ void st8(T* p, const float* v);
+template <>
+__device__ __forceinline__ void st8<float>(float* p, const float* v) {
+  *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  *reinterpret_cast<float4*>(p + 4) = make_float4(v[4], v[5], v[6], v[7]);
+}
+template <>
+__device__ __forceinline__ void st8<bf16>(bf16* p, const float* v) {
+  uint4 u;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+  *reinterpret_cast<uint4*>(p) = u;
+}
+
+// stage x[b] (n x d, row stride x_rs) into xs (row stride ld = d + 4) as fp32
+template <typename T, bool VEC>
+__device__ __forceinline__ void stage_rows(const T* xb, long long x_rs, int n, int d, float* xs, int ld) {
+  if constexpr (VEC) {
+    const int dv = d >> 3, nv = n * dv;
+    for (int i0 = threadIdx.x; i0 < nv; i0 += 4 * blockDim.x) {
+      float v[4][8];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u * blockDim.x;
+        if (i < nv) ld8(xb + (long long)(i / dv) * x_rs + (i % dv) * 8, v[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u * blockDim.x;
+        if (i < nv) {
+          float* q = xs + (i / dv) * ld + (i % dv) * 8;
+          *reinterpret_cast<float4*>(q) = make_float4(v[u][0], v[u][1], v[u][2], v[u][3]);
+          *reinterpret_cast<float4*>(q + 4) = make_float4(v[u][4], v[u][5], v[u][6], v[u][7]);
+        }
+      }
+    }
+  } else {
+    for (int i = threadIdx.x; i < n * d; i += blockDim.x) xs[(i / d) * ld + i % d] = ldf(xb + (long long)(i / d) * x_rs + i % d);
+  }
+}
+
+template <typename T, bool VEC>
 __global__ void __launch_bounds__(256) gram_triu_fwd_kernel(int n, int d, const T* x, long long x_rs,
                                                            long long x_bs, T* tri, long long t_bs) {
   KL_PDL_ENTRY();
   extern __shared__ float xs[];
-  const int b = blockIdx.x;
-  const T* xb = x + (long long)b * x_bs;
-  for (int i = threadIdx.x; i < n * d; i += blockDim.x) xs[i] = ldf(xb + (long long)(i / d) * x_rs + i % d);
+  const int b = blockIdx.x, ld = d + 4;
+  stage_rows<T, VEC>(x + (long long)b * x_bs, x_rs, n, d, xs, ld);
   __syncthreads();
   const int np_ = n * (n + 1) / 2;
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+  // blockIdx.y splits the pairs: more CTAs per sample, shorter warp chains
+  const int l = threadIdx.x & 31, nw = (blockDim.x >> 5) * gridDim.y;
+  const int w = blockIdx.y * (blockDim.x >> 5) + (threadIdx.x >> 5);
   int r = 0, rbase = 0;  // pair p = rbase + (c - r) for row r
   for (int p = w; p < np_; p += nw) {
     while (p >= rbase + (n - r)) {
@@ -284,39 +349,70 @@ __global__ void __launch_bounds__(256) gram_triu_fwd_kernel(int n, int d, const 
       ++r;
     }
     const int c = r + (p - rbase);
-    const float* xr = xs + r * d;
-    const float* xc = xs + c * d;
+    const float* xr = xs + r * ld;
+    const float* xc = xs + c * ld;
     float acc = 0.f;
-    for (int k = l; k < d; k += 32) acc = fmaf(xr[k], xc[k], acc);
+    if (VEC) {
+      for (int k = 4 * l; k < d; k += 128) {
+        const float4 a = *reinterpret_cast<const float4*>(xr + k), bb = *reinterpret_cast<const float4*>(xc + k);
+        acc = fmaf(a.x, bb.x, fmaf(a.y, bb.y, fmaf(a.z, bb.z, fmaf(a.w, bb.w, acc))));
+      }
+    } else {
+      for (int k = l; k < d; k += 32) acc = fmaf(xr[k], xc[k], acc);
+    }
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (l == 0) stf(tri + (long long)b * t_bs + p, acc);
   }
 }
 
 // dx[b, r, k] += sum_j W[r][j] x[b, j, k], W symmetric from dtri (diagonal x2).
-template <typename T>
+// VEC: thread = (row, 8 columns); the dx read-modify-write is one 16-byte
+// vector each way.
+template <typename T, bool VEC>
 __global__ void __launch_bounds__(256) gram_triu_bwd_kernel(int n, int d, const T* x, long long x_rs,
                                                            long long x_bs, const T* dtri, long long t_bs, T* dx,
                                                            long long dx_rs, long long dx_bs) {
   KL_PDL_ENTRY();
   extern __shared__ float sm[];
-  float* xs = sm;          // n x d
-  float* W = sm + n * d;   // n x n
+  const int ld = d + 4;
+  float* xs = sm;           // n x ld
+  float* W = sm + n * ld;   // n x n
   const int b = blockIdx.x;
-  const T* xb = x + (long long)b * x_bs;
   const T* db = dtri + (long long)b * t_bs;
-  for (int i = threadIdx.x; i < n * d; i += blockDim.x) xs[i] = ldf(xb + (long long)(i / d) * x_rs + i % d);
   for (int i = threadIdx.x; i < n * n; i += blockDim.x) {
     const int r = i / n, j = i % n, lo = min(r, j), hi = max(r, j);
     W[i] = ldf(db + triu_index(lo, hi, n)) * (r == j ? 2.f : 1.f);
   }
+  stage_rows<T, VEC>(x + (long long)b * x_bs, x_rs, n, d, xs, ld);
   __syncthreads();
-  for (int i = threadIdx.x; i < n * d; i += blockDim.x) {
-    const int r = i / d, k = i % d;
-    float acc = 0.f;
-    for (int j = 0; j < n; ++j) acc = fmaf(W[r * n + j], xs[j * d + k], acc);
-    T* p = dx + (long long)b * dx_bs + (long long)r * dx_rs + k;
-    stf(p, ldf(p) + acc);
+  T* dxb = dx + (long long)b * dx_bs;
+  if constexpr (VEC) {
+    const int dv = d >> 3;  // blockIdx.y splits the (row, 8-column) items
+    for (int i = blockIdx.y * blockDim.x + threadIdx.x; i < n * dv; i += blockDim.x * gridDim.y) {
+      const int r = i / dv, k = (i % dv) * 8;
+      T* p = dxb + (long long)r * dx_rs + k;
+      float acc[8];
+      ld8(p, acc);
+      const float* wr = W + r * n;
+      for (int j = 0; j < n; ++j) {
+        const float wj = wr[j];
+        const float4 a = *reinterpret_cast<const float4*>(xs + j * ld + k);
+        const float4 c = *reinterpret_cast<const float4*>(xs + j * ld + k + 4);
+        acc[0] = fmaf(wj, a.x, acc[0]); acc[1] = fmaf(wj, a.y, acc[1]);
+        acc[2] = fmaf(wj, a.z, acc[2]); acc[3] = fmaf(wj, a.w, acc[3]);
+        acc[4] = fmaf(wj, c.x, acc[4]); acc[5] = fmaf(wj, c.y, acc[5]);
+        acc[6] = fmaf(wj, c.z, acc[6]); acc[7] = fmaf(wj, c.w, acc[7]);
+      }
+      st8(p, acc);
+    }
+  } else {
+    for (int i = blockIdx.y * blockDim.x + threadIdx.x; i < n * d; i += blockDim.x * gridDim.y) {
+      const int r = i / d, k = i % d;
+      float acc = 0.f;
+      for (int j = 0; j < n; ++j) acc = fmaf(W[r * n + j], xs[j * ld + k], acc);
+      T* p = dxb + (long long)r * dx_rs + k;
+      stf(p, ldf(p) + acc);
+    }
   }
 }
 
@@ -529,39 +625,65 @@ extern "C" int kl_recent_rows_bwd(int B, int T, int d, int n, int dtype, const v
   return launch_check("recent_rows_bwd");
 }
 
+static inline bool vec8_ok(const void* p, long long rs, int d) {
+  return d % 8 == 0 && rs % 8 == 0 && ((uintptr_t)p & 15) == 0;
+}
+
+// CTAs per sample: enough that each warp / thread gets a few work items
+static inline unsigned gram_split(int items, int per_cta) {
+  int s = (items + 4 * per_cta - 1) / (4 * per_cta);
+  return (unsigned)std::max(1, std::min(s, 8));
+}
+
+template <typename T>
+static void gram_fwd_launch(int B, int n, int d, const T* x, long long x_rs, long long x_bs, T* tri, long long t_bs,
+                            size_t sm, cudaStream_t s) {
+  if (vec8_ok(x, x_rs, d) && x_bs % 8 == 0) {
+    cudaFuncSetAttribute(gram_triu_fwd_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    launch_k(gram_triu_fwd_kernel<T, true>, dim3(B, gram_split(n * (n + 1) / 2, 8)), 256, sm, s, n, d, x, x_rs, x_bs, tri, t_bs);
+  } else {
+    cudaFuncSetAttribute(gram_triu_fwd_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    launch_k(gram_triu_fwd_kernel<T, false>, dim3(B, gram_split(n * (n + 1) / 2, 8)), 256, sm, s, n, d, x, x_rs, x_bs, tri, t_bs);
+  }
+}
+
 extern "C" int kl_gram_triu_fwd(int B, int n, int d, int dtype, const void* x, long long x_rs, long long x_bs,
                                 void* tri, long long t_bs, void* stream) {
   if ((long long)B * n == 0) return KL_OK;
-  const size_t sm = (size_t)n * d * sizeof(float);
+  const size_t sm = (size_t)n * (d + 4) * sizeof(float);
   if (sm > 200 * 1024) { set_error("kl_gram_triu_fwd: n*d = %d too large", n * d); return KL_EUNSUPPORTED; }
   cudaStream_t s = (cudaStream_t)stream;
-  if (dtype == KL_F32) {
-    cudaFuncSetAttribute(gram_triu_fwd_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    launch_k(gram_triu_fwd_kernel<float>, B, 256, sm, s, n, d, (const float*)x, x_rs, x_bs, (float*)tri, t_bs);
-  } else {
-    cudaFuncSetAttribute(gram_triu_fwd_kernel<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    launch_k(gram_triu_fwd_kernel<bf16>, B, 256, sm, s, n, d, (const bf16*)x, x_rs, x_bs, (bf16*)tri, t_bs);
-  }
+  if (dtype == KL_F32)
+    gram_fwd_launch(B, n, d, (const float*)x, x_rs, x_bs, (float*)tri, t_bs, sm, s);
+  else
+    gram_fwd_launch(B, n, d, (const bf16*)x, x_rs, x_bs, (bf16*)tri, t_bs, sm, s);
   count_launch();
   return launch_check("gram_triu_fwd");
+}
+
+template <typename T>
+static void gram_bwd_launch(int B, int n, int d, const T* x, long long x_rs, long long x_bs, const T* dtri,
+                            long long t_bs, T* dx, long long dx_rs, long long dx_bs, size_t sm, cudaStream_t s) {
+  if (vec8_ok(x, x_rs, d) && x_bs % 8 == 0 && vec8_ok(dx, dx_rs, d) && dx_bs % 8 == 0) {
+    cudaFuncSetAttribute(gram_triu_bwd_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    launch_k(gram_triu_bwd_kernel<T, true>, dim3(B, gram_split(n * d / 8, 64)), 256, sm, s, n, d, x, x_rs, x_bs, dtri, t_bs, dx, dx_rs, dx_bs);
+  } else {
+    cudaFuncSetAttribute(gram_triu_bwd_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    launch_k(gram_triu_bwd_kernel<T, false>, dim3(B, gram_split(n * d, 512)), 256, sm, s, n, d, x, x_rs, x_bs, dtri, t_bs, dx, dx_rs, dx_bs);
+  }
 }
 
 extern "C" int kl_gram_triu_bwd(int B, int n, int d, int dtype, const void* x, long long x_rs, long long x_bs,
                                 const void* dtri, long long t_bs, void* dx, long long dx_rs, long long dx_bs,
                                 void* stream) {
   if ((long long)B * n * d == 0) return KL_OK;
-  const size_t sm = ((size_t)n * d + (size_t)n * n) * sizeof(float);
+  const size_t sm = ((size_t)n * (d + 4) + (size_t)n * n) * sizeof(float);
   if (sm > 200 * 1024) { set_error("kl_gram_triu_bwd: n*d = %d too large", n * d); return KL_EUNSUPPORTED; }
   cudaStream_t s = (cudaStream_t)stream;
-  if (dtype == KL_F32) {
-    cudaFuncSetAttribute(gram_triu_bwd_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    launch_k(gram_triu_bwd_kernel<float>, B, 256, sm, s, n, d, (const float*)x, x_rs, x_bs, (const float*)dtri, t_bs,
-                                                    (float*)dx, dx_rs, dx_bs);
-  } else {
-    cudaFuncSetAttribute(gram_triu_bwd_kernel<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    launch_k(gram_triu_bwd_kernel<bf16>, B, 256, sm, s, n, d, (const bf16*)x, x_rs, x_bs, (const bf16*)dtri, t_bs,
-                                                   (bf16*)dx, dx_rs, dx_bs);
-  }
+  if (dtype == KL_F32)
+    gram_bwd_launch(B, n, d, (const float*)x, x_rs, x_bs, (const float*)dtri, t_bs, (float*)dx, dx_rs, dx_bs, sm, s);
+  else
+    gram_bwd_launch(B, n, d, (const bf16*)x, x_rs, x_bs, (const bf16*)dtri, t_bs, (bf16*)dx, dx_rs, dx_bs, sm, s);
   count_launch();
   return launch_check("gram_triu_bwd");
 }

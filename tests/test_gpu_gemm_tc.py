@@ -165,3 +165,31 @@ def test_tc_tma_epilogue(N):
     gemm(A.transpose(1, 2), R, C, beta=1.0, reduce=(False, True))
     ref = C0.double() + (A.double().transpose(1, 2) @ R.double()).sum(0)
     assert rel(C, ref) < 1e-5
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("N,out_dtype", [(256, torch.bfloat16), (320, torch.float32), (200, torch.bfloat16)])
+def test_tc_tma_epilogue_aux(N, out_dtype):
+    """TMA-store epilogue with the aux side output: aux_mode 1 keeps the
+    pre-activation (row-limited rows zero) beside the activated C; aux_mode 2
+    multiplies the product by act'(aux) (the MLP backward)."""
+    from paper_2602_10016_b200._capi import gemm
+
+    g = torch.Generator(device="cuda").manual_seed(N + 7)
+    A = operand((2, 333, 256), True, g)
+    B = operand((256, N), False, g)
+    bias = torch.randn(N, device="cuda", generator=g)
+    lim = torch.tensor([333, 150], device="cuda", dtype=torch.int32)
+    out = torch.empty(2, 333, N, device="cuda", dtype=out_dtype)
+    pre = torch.empty(2, 333, N, device="cuda", dtype=out_dtype)
+    gemm(A, B, out, bias=bias, acts=["silu"], aux=pre, aux_mode=1, row_limit=lim)
+    z = A.double() @ B.double() + bias.double()
+    keep = torch.arange(333, device="cuda")[None, :, None] < lim.view(2, 1, 1)
+    tol = 1e-2 if out_dtype == torch.bfloat16 else 1e-5
+    assert rel(pre, torch.where(keep, z, 0)) < tol
+    assert rel(out, torch.where(keep, torch.nn.functional.silu(z), 0)) < (1e-2 if out_dtype == torch.bfloat16 else 2e-3)
+    d = torch.empty_like(out)
+    gemm(A, B, d, acts=["silu"], aux=pre, aux_mode=2)
+    pz = pre.double()
+    s = torch.sigmoid(pz)
+    assert rel(d, (A.double() @ B.double()) * s * (1 + pz * (1 - s))) < tol
