@@ -1347,13 +1347,465 @@ size_t dkv_smem_bytes() { return 1024 + 2 * TILE + KVS * 2 * TILE + 2 * PBLK + 1
 
 }  // namespace v2
 
-bool map3(CUtensorMap* m, const void* ptr, long long inner, int T, int B, long long ld, long long bs) {
+// ---------------------------------------------------------------------------
+// dK / dV v3: key-block-major like v2, but over 64-query half-blocks so the
+// score pair (S^T, dP^T: 2 x 64 TMEM columns) is triple-buffered next to the
+// dK / dV accumulators (3 x 128 + 128 = 512 columns).  Two issue warps: one
+// runs the S^T / dP^T products up to three half-blocks ahead, the other the
+// dV += P^T dO, dK += dS^T Q products of each block as soon as its P^T / dS^T
+// land in smem.  Two gradient warpgroups take alternate half-blocks
+// (ping-pong; one P^T / dS^T smem slot each).  K / V are double-buffered so
+// the next key block's scores start before the current block's products
+// finish; Q / dO arrive as 64-row boxes in a 4-slot ring, kept across
+// consecutive key blocks of a sequence (slots the next key block does not
+// see are released as soon as their products complete).  LSE / D of a tile's
+// query band are staged once per tile, the next tile's prefetched into
+// registers.  The issue warps walk their tiles with incremental coordinates:
+// a single thread's integer bookkeeping is on the critical path.
+namespace v3 {
+
+using v2::ex2;
+using v2::named_bar;
+constexpr int HB = 64;                  // query half-block
+constexpr int QR = 4;                   // Q | dO half-block ring slots
+constexpr int HTILE = HB * DH * 2;      // 8 KB: 64 x 64 bf16
+constexpr int PH = TB * HB * 2;         // 16 KB: 128 x 64 bf16 (P^T or dS^T)
+constexpr int MAXQ = 6 * HB;            // queries of a tile's band
+constexpr uint32_t IDESC_S64 = tc::idesc_bf16(128, 64, 0, 0);
+
+constexpr int NT3 = 352;  // warp 0 TMA, warp 1 S^T/dP^T MMAs, warps 2..9 gradients, warp 10 dV/dK MMAs
+
+struct Tile {
+  int b, h, k0, len, lo, n;  // lo, n: 64-query half-blocks that see keys [k0, k0 + 128)
+  bool real;
+};
+
+__device__ __forceinline__ void band_of(const SwaP& p, Tile& t) {
+  t.real = t.k0 < t.len;
+  t.lo = t.n = 0;
+  if (t.real) {
+    int lo = max(0, t.k0 - p.w);
+    if (p.causal) lo = max(lo, t.k0);
+    const int hi = min(t.len - 1, t.k0 + TB - 1 + p.w);
+    t.lo = lo / HB;
+    t.n = hi / HB - lo / HB + 1;
+  }
+}
+
+// Walks a CTA's contiguous tile range [i0, i1) with incremental coordinates
+// (no divisions on the issue threads' critical path).  Sequence order is
+// head-major: with contiguous per-CTA ranges, CTAs c, c + 148/H, ... work on
+// the same (sample, key block) of different heads at the same time, so the
+// heads' 128-byte row pieces of Q / K / V / dO are read from DRAM together.
+// Also keeps the ring position of each half-block's Q | dO load (loads are
+// issued once per block of a sequence, in increasing block order).
+struct Walk {
+  int idx, i1, nT, kt, bh, j, t;  // t: real-tile ordinal
+  int seg_bh, seg_base, seg_first, ld_end;
+  Tile tl;
+  bool done;
+};
+
+__device__ __forceinline__ void walk_fill(const SwaP& p, Walk& w) {
+  w.tl.k0 = w.kt * TB;
+  w.tl.len = p.lengths[w.tl.b];
+  band_of(p, w.tl);
+}
+__device__ __forceinline__ void walk_adv(const SwaP& p, Walk& w) {
+  ++w.idx;
+  if (++w.kt == w.nT) {
+    w.kt = 0;
+    ++w.bh;
+    if (++w.tl.b == p.B) {
+      w.tl.b = 0;
+      ++w.tl.h;
+    }
+  }
+}
+// Move to the next real tile at or after the current position.
+__device__ __forceinline__ void walk_settle(const SwaP& p, Walk& w) {
+  for (; w.idx < w.i1; walk_adv(p, w)) {
+    walk_fill(p, w);
+    if (!w.tl.real) continue;
+    if (w.bh != w.seg_bh) {
+      w.seg_bh = w.bh;
+      w.seg_base = w.ld_end;
+      w.seg_first = w.tl.lo;
+    }
+    w.ld_end = max(w.ld_end, w.seg_base + (w.tl.lo + w.tl.n - w.seg_first));
+    w.j = w.tl.lo;
+    ++w.t;
+    return;
+  }
+  w.done = true;
+}
+__device__ __forceinline__ void walk_init(const SwaP& p, Walk& w, int i0, int i1, int nT) {
+  w.idx = i0;
+  w.i1 = i1;
+  w.nT = nT;
+  w.kt = i0 % nT;
+  w.bh = i0 / nT;
+  w.tl.b = w.bh % p.B;
+  w.tl.h = w.bh / p.B;
+  w.t = -1;
+  w.seg_bh = -1;
+  w.seg_base = w.seg_first = w.ld_end = 0;
+  w.done = false;
+  walk_settle(p, w);
+}
+__device__ __forceinline__ void walk_next_tile(const SwaP& p, Walk& w) {
+  walk_adv(p, w);
+  walk_settle(p, w);
+}
+__device__ __forceinline__ void walk_step(const SwaP& p, Walk& w) {
+  if (w.j + 1 < w.tl.lo + w.tl.n)
+    ++w.j;
+  else
+    walk_next_tile(p, w);
+}
+__device__ __forceinline__ int load_index(const Walk& w, int j) { return w.seg_base + j - w.seg_first; }
+
+__global__ void __launch_bounds__(NT3, 1)
+    swa_bwd_dkv_tc3_kernel(const __grid_constant__ CUtensorMap tkv, const __grid_constant__ CUtensorMap tq64,
+                           const __grid_constant__ CUtensorMap tdo64, SwaP p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sKV = sm;                    // 2 x (K 16 KB | V 16 KB)
+  uint8_t* sQG = sKV + 2 * 2 * TILE;    // QR x (Q 8 KB | dO 8 KB)
+  uint8_t* sPD = sQG + QR * 2 * HTILE;  // 2 x (P^T 16 KB | dS^T 16 KB)
+  __shared__ __align__(16) float sLD[2][2][2][MAXQ];  // [warpgroup][tile parity][LSE (log2) | D][band query]
+  uint64_t* bar = (uint64_t*)(sPD + 2 * 2 * PH);
+  uint64_t* kv_full = bar;                 // [2]
+  uint64_t* kv_empty = bar + 2;            // [2]
+  uint64_t* qg_full = bar + 4;             // [QR]
+  uint64_t* qg_empty = qg_full + QR;       // [QR]
+  uint64_t* sd_full = qg_empty + QR;       // [3]
+  uint64_t* sd_empty = sd_full + 3;        // [3]
+  uint64_t* pd_full = sd_empty + 3;        // [2]
+  uint64_t* pd_empty = pd_full + 2;        // [2]
+  uint64_t* acc_full = pd_empty + 2;
+  uint64_t* acc_empty = acc_full + 1;
+  uint32_t* tslot = (uint32_t*)(acc_empty + 1);
+
+  const int nT = (p.T + TB - 1) / TB;
+  const int W = p.B * p.H * nT;
+  const int i0 = (int)((long long)W * blockIdx.x / gridDim.x);
+  const int i1 = (int)((long long)W * (blockIdx.x + 1) / gridDim.x);
+  const int HD = p.H * DH;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    tc::prefetch_tmap(&tkv);
+    tc::prefetch_tmap(&tq64);
+    tc::prefetch_tmap(&tdo64);
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&kv_full[i], 1);
+      tc::mbar_init(&kv_empty[i], 1);
+    }
+    for (int i = 0; i < QR; ++i) {
+      tc::mbar_init(&qg_full[i], 1);
+      tc::mbar_init(&qg_empty[i], 1);
+    }
+    for (int i = 0; i < 3; ++i) {
+      tc::mbar_init(&sd_full[i], 1);
+      tc::mbar_init(&sd_empty[i], 4);
+    }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&pd_full[i], 4);
+      tc::mbar_init(&pd_empty[i], 1);
+    }
+    tc::mbar_init(acc_full, 1);
+    tc::mbar_init(acc_empty, 4);
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tslot, 512);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tslot;
+  KL_PDL_ENTRY();
+  const uint32_t T_DV = 384, T_DK = 448;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      Walk w;
+      walk_init(p, w, i0, i1, nT);
+      int loaded = 0;  // Q | dO loads issued (ring position)
+      while (!w.done) {
+        const Tile& tl = w.tl;
+        const int kb = w.t & 1;
+        tc::mbar_wait(&kv_empty[kb], ((w.t >> 1) & 1) ^ 1);
+        tc::mbar_arrive_expect_tx(&kv_full[kb], 2 * TILE);
+        tc::tma_load_3d(sKV + kb * 2 * TILE, &tkv, &kv_full[kb], HD + tl.h * DH, tl.k0, tl.b);
+        tc::tma_load_3d(sKV + kb * 2 * TILE + TILE, &tkv, &kv_full[kb], 2 * HD + tl.h * DH, tl.k0, tl.b);
+        for (int j = tl.lo; j < tl.lo + tl.n; ++j) {
+          const int li = load_index(w, j);
+          if (li < loaded) continue;  // kept from the previous key block
+          const int s = li % QR;
+          tc::mbar_wait(&qg_empty[s], ((li / QR) & 1) ^ 1);
+          tc::mbar_arrive_expect_tx(&qg_full[s], 2 * HTILE);
+          tc::tma_load_3d(sQG + s * 2 * HTILE, &tq64, &qg_full[s], tl.h * DH, j * HB, tl.b);
+          tc::tma_load_3d(sQG + s * 2 * HTILE + HTILE, &tdo64, &qg_full[s], tl.h * DH, j * HB, tl.b);
+          loaded = li + 1;
+        }
+        walk_next_tile(p, w);
+      }
+    }
+  } else if (warp == 1) {
+    // S^T = K Q_j^T and dP^T = V dO_j^T into the 3-slot TMEM ring
+    if (lane == 0) {
+      Walk a;
+      walk_init(p, a, i0, i1, nT);
+      int n = 0, waited = 0;
+      const uint32_t kv0 = tc::smem_u32(sKV), qg0 = tc::smem_u32(sQG);
+      while (!a.done) {
+        const int kb = a.t & 1;
+        if (a.j == a.tl.lo) tc::mbar_wait(&kv_full[kb], (a.t >> 1) & 1);
+        const int li = load_index(a, a.j);
+        if (li >= waited) {
+          tc::mbar_wait(&qg_full[li % QR], (li / QR) & 1);
+          waited = li + 1;
+        }
+        const int ss = n % 3;
+        tc::mbar_wait(&sd_empty[ss], ((n / 3) & 1) ^ 1);
+        tc::fence_after();
+        const uint32_t ka = kv0 + kb * 2 * TILE, va = ka + TILE;
+        const uint32_t qa = qg0 + (li % QR) * 2 * HTILE, ga = qa + HTILE;
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk)
+          tc::mma_bf16(tmem + ss * 128, d_kmaj64(ka, kk), d_kmaj64(qa, kk), IDESC_S64, kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk)
+          tc::mma_bf16(tmem + ss * 128 + 64, d_kmaj64(va, kk), d_kmaj64(ga, kk), IDESC_S64, kk > 0);
+        tc::mma_commit(&sd_full[ss]);
+        if (a.j == a.tl.lo + a.tl.n - 1) tc::mma_commit(&kv_empty[kb]);  // K / V of this tile no longer read
+        ++n;
+        walk_step(p, a);
+      }
+    }
+  } else if (warp == 10) {
+    // dV += P^T dO_j, dK += dS^T Q_j into the TMEM accumulators
+    if (lane == 0) {
+      Walk b;
+      walk_init(p, b, i0, i1, nT);
+      int n = 0, keep = 0;
+      const uint32_t qg0 = tc::smem_u32(sQG), pd0 = tc::smem_u32(sPD);
+      while (!b.done) {
+        const bool first = b.j == b.tl.lo, last = b.j == b.tl.lo + b.tl.n - 1;
+        if (first) {
+          tc::mbar_wait(acc_empty, (b.t & 1) ^ 1);
+          // half-blocks below `keep` are not seen by the next key block of
+          // this sequence: their ring slots are released after their products
+          keep = b.tl.lo + b.tl.n;
+          if (b.idx + 1 < b.i1 && b.kt + 1 < nT) {
+            Tile nx;
+            nx.k0 = (b.kt + 1) * TB;
+            nx.len = b.tl.len;
+            band_of(p, nx);
+            if (nx.real) keep = nx.lo;
+          }
+        }
+        const int ps = n & 1;
+        tc::mbar_wait(&pd_full[ps], (n >> 1) & 1);
+        tc::fence_after();
+        const int li = load_index(b, b.j);
+        const uint32_t qa = qg0 + (li % QR) * 2 * HTILE, ga = qa + HTILE;
+        const uint32_t pt = pd0 + ps * 2 * PH, dt = pt + PH;
+#pragma unroll
+        for (int kk = 0; kk < HB / 16; ++kk)
+          tc::mma_bf16(tmem + T_DV, d_kmaj64(pt, kk), d_mn(ga, kk), IDESC_PV, (!first || kk > 0) ? 1u : 0u);
+#pragma unroll
+        for (int kk = 0; kk < HB / 16; ++kk)
+          tc::mma_bf16(tmem + T_DK, d_kmaj64(dt, kk), d_mn(qa, kk), IDESC_PV, (!first || kk > 0) ? 1u : 0u);
+        tc::mma_commit(&pd_empty[ps]);
+        if (b.j < keep) tc::mma_commit(&qg_empty[li % QR]);
+        if (last) tc::mma_commit(acc_full);
+        ++n;
+        walk_step(p, b);
+      }
+    }
+  } else {
+    // Two warpgroups take alternate half-blocks (ping-pong): one turns its
+    // S^T / dP^T into P^T / dS^T while the other loads its scores, so TMEM
+    // reads, the exp / FMA math and the smem stores of the two overlap.  A
+    // thread owns one key row and the 64 query columns of its items.
+    const int wg = (warp - 2) >> 2, qtr = warp & 3;
+    const int r = qtr * 32 + lane;
+    const int wtid = (warp - 2 - 4 * wg) * 32 + lane;  // 0..127 within the warpgroup
+    const uint32_t trow = tmem + ((uint32_t)(qtr * 32) << 16);
+    const float c2 = p.scale * 1.4426950408889634f;
+    bf16* dqkv = (bf16*)p.dQKV;
+    int n_item = 0, t = 0;
+    // the next real tile's LSE (log2 units) / D, 3 band entries per thread,
+    // prefetched into registers while the current tile runs
+    struct LD3 {
+      float l[3], d[3];
+    };
+    auto fetch = [](const SwaP& pp, const Tile& tl, int tid) {
+      LD3 v;
+      const float* LSE = pp.LSE + ((long long)tl.b * pp.H + tl.h) * pp.T;
+      const float* D = pp.Dbuf + ((long long)tl.b * pp.H + tl.h) * pp.T;
+#pragma unroll
+      for (int u = 0; u < 3; ++u) {
+        const int i = tid + u * 128, q = tl.lo * HB + i;
+        const bool in = i < tl.n * HB && q < tl.len;
+        v.l[u] = in ? LSE[q] * 1.4426950408889634f : INFINITY;
+        v.d[u] = in ? D[q] : 0.f;
+      }
+      return v;
+    };
+    Walk w;  // all tiles, real or not (padding key blocks get zero rows)
+    w.idx = i0;
+    w.i1 = i1;
+    w.nT = nT;
+    w.kt = i0 % nT;
+    w.bh = i0 / nT;
+    w.tl.b = w.bh % p.B;
+    w.tl.h = w.bh / p.B;
+    Walk pw = w;  // prefetch cursor: the next real tile after w
+    walk_fill(p, pw);
+    while (pw.idx < i1 && !pw.tl.real) {
+      walk_adv(p, pw);
+      if (pw.idx < i1) walk_fill(p, pw);
+    }
+    LD3 nx = {};
+    if (pw.idx < i1) nx = fetch(p, pw.tl, wtid);
+    for (; w.idx < i1; walk_adv(p, w)) {
+      walk_fill(p, w);
+      const Tile tl = w.tl;
+      bf16* out = dqkv + (long long)tl.b * p.bs_qkv + tl.h * DH;
+      if (!tl.real) {  // keys past the length: zero dK (warpgroup 0) / dV (1)
+        zero_rows(out + (1 + wg) * HD, p.ld_qkv, tl.k0, TB, p.T, wtid, 128);
+        continue;
+      }
+      float* ls = sLD[wg][t & 1][0];
+      float* dd = sLD[wg][t & 1][1];
+#pragma unroll
+      for (int u = 0; u < 3; ++u) {
+        ls[wtid + u * 128] = nx.l[u];
+        dd[wtid + u * 128] = nx.d[u];
+      }
+      named_bar(1 + wg, 128);
+      pw = w;
+      do {
+        walk_adv(p, pw);
+        if (pw.idx < i1) walk_fill(p, pw);
+      } while (pw.idx < i1 && !pw.tl.real);
+      if (pw.idx < i1) nx = fetch(p, pw.tl, wtid);
+      const int key = tl.k0 + r;
+      int qlo = max(0, key - p.w), qhi = min(tl.len - 1, key + p.w);
+      if (p.causal) qlo = max(qlo, key);
+      if (key >= tl.len) qhi = -1;
+      const int last_item = n_item + tl.n - 1;
+      for (int jj = 0; jj < tl.n; ++jj, ++n_item) {
+        if ((n_item & 1) != wg) continue;
+        const int ss = n_item % 3;
+        uint8_t* blk = sPD + wg * 2 * PH;
+        tc::mbar_wait(&sd_full[ss], (n_item / 3) & 1);
+        tc::fence_after();
+#pragma unroll 1
+        for (int ch = 0; ch < 2; ++ch) {
+          const int q0c = (tl.lo + jj) * HB + ch * 32;
+          const int lb = jj * HB + ch * 32;  // staged band index of column 0
+          float s[32], g[32];
+          tc::tmem_ld32(trow + ss * 128 + ch * 32, s);
+          tc::tmem_ld32(trow + ss * 128 + 64 + ch * 32, g);
+          if (ch == 1) {
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&sd_empty[ss]);
+          }
+          uint32_t pp[16], pd[16];
+          if (q0c > qhi || q0c + 31 < qlo) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) pp[i] = pd[i] = 0u;
+          } else if (q0c >= qlo && q0c + 31 <= qhi) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+              const float4 l4 = *reinterpret_cast<const float4*>(&ls[lb + i]);
+              const float4 d4 = *reinterpret_cast<const float4*>(&dd[lb + i]);
+              const float p0 = ex2(fmaf(s[i], c2, -l4.x)), p1 = ex2(fmaf(s[i + 1], c2, -l4.y));
+              const float p2 = ex2(fmaf(s[i + 2], c2, -l4.z)), p3 = ex2(fmaf(s[i + 3], c2, -l4.w));
+              pp[i >> 1] = tc::pack_bf16(p0, p1);
+              pp[(i >> 1) + 1] = tc::pack_bf16(p2, p3);
+              pd[i >> 1] = tc::pack_bf16(p0 * (g[i] - d4.x), p1 * (g[i + 1] - d4.y));
+              pd[(i >> 1) + 1] = tc::pack_bf16(p2 * (g[i + 2] - d4.z), p3 * (g[i + 3] - d4.w));
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) {
+              float pr[2], dsv[2];
+#pragma unroll
+              for (int u = 0; u < 2; ++u) {
+                const int qi = q0c + i + u;
+                pr[u] = (qi >= qlo && qi <= qhi) ? ex2(fmaf(s[i + u], c2, -ls[lb + i + u])) : 0.f;
+                dsv[u] = pr[u] * (g[i + u] - dd[lb + i + u]);
+              }
+              pp[i >> 1] = tc::pack_bf16(pr[0], pr[1]);
+              pd[i >> 1] = tc::pack_bf16(dsv[0], dsv[1]);
+            }
+          }
+          // this warpgroup's P^T / dS^T slot is free once the products of
+          // its previous item (two items back) have completed
+          if (ch == 0) tc::mbar_wait(&pd_empty[wg], ((n_item >> 1) & 1) ^ 1);
+          store_sw(blk, r, ch * 32, pp);
+          store_sw(blk + PH, r, ch * 32, pd);
+        }
+        tc::fence_async_smem();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&pd_full[wg]);
+      }
+      // the warpgroup that took the tile's last half-block writes dK / dV
+      if ((last_item & 1) == wg) {
+        tc::mbar_wait(acc_full, t & 1);
+        tc::fence_after();
+#pragma unroll 1
+        for (int which = 0; which < 2; ++which) {  // 0: dK (scaled), 1: dV
+          const float sc = which ? 1.f : p.scale;
+#pragma unroll 1
+          for (int ch = 0; ch < 2; ++ch) {
+            float v[32];
+            tc::tmem_ld32(trow + (which ? T_DV : T_DK) + ch * 32, v);
+            if (which == 1 && ch == 1) {
+              tc::fence_before();
+              __syncwarp();
+              if (lane == 0) tc::mbar_arrive(acc_empty);
+            }
+            if (key < p.T) {
+              uint4* o = reinterpret_cast<uint4*>(out + (long long)key * p.ld_qkv + (1 + which) * HD + ch * 32);
+#pragma unroll
+              for (int c = 0; c < 4; ++c) {
+                uint4 u;
+                u.x = tc::pack_bf16(v[8 * c + 0] * sc, v[8 * c + 1] * sc);
+                u.y = tc::pack_bf16(v[8 * c + 2] * sc, v[8 * c + 3] * sc);
+                u.z = tc::pack_bf16(v[8 * c + 4] * sc, v[8 * c + 5] * sc);
+                u.w = tc::pack_bf16(v[8 * c + 6] * sc, v[8 * c + 7] * sc);
+                o[c] = u;
+              }
+            }
+          }
+        }
+      }
+      ++t;
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tmem, 512);
+}
+
+size_t dkv_smem_bytes() { return 1024 + 2 * 2 * TILE + QR * 2 * HTILE + 2 * 2 * PH + (4 + 2 * QR + 6 + 4 + 2) * 8 + 16; }
+
+}  // namespace v3
+
+bool map3(CUtensorMap* m, const void* ptr, long long inner, int T, int B, long long ld, long long bs,
+          unsigned rows = 128) {
   auto fn = tc_encode_fn();
   if (!fn) return false;
   if (((uintptr_t)ptr & 15) || (ld * 2) % 16 || (bs * 2) % 16) return false;
   cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)T, (cuuint64_t)B};
   cuuint64_t strides[2] = {(cuuint64_t)(ld * 2), (cuuint64_t)(bs * 2)};
-  cuuint32_t box[3] = {64, 128, 1};
+  cuuint32_t box[3] = {64, rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -1398,9 +1850,20 @@ int swa_bwd_tc(const SwaP& p, cudaStream_t s) {
   if (!getenv("KL_SWA_BWD_V1")) {
     const int W = p.B * p.H * ((p.T + TB - 1) / TB);
     const int grid = std::min(W, tc_num_sms());
-    const size_t s1 = v2::dkv_smem_bytes(), s2 = v2::dq_smem_bytes();
-    cudaFuncSetAttribute(v2::swa_bwd_dkv_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1);
-    launch_k(v2::swa_bwd_dkv_tc2_kernel, grid, v2::NT2, s1, s, tq, tdo, p);
+    const size_t s2 = v2::dq_smem_bytes();
+    static int dkv_v = -1;
+    if (dkv_v < 0) dkv_v = getenv("KL_SWA_DKV_V2") ? 2 : 3;
+    CUtensorMap tq64, tdo64;
+    if (dkv_v == 3 && map3(&tq64, p.QKV, 3LL * p.H * DH, p.T, p.B, p.ld_qkv, p.bs_qkv, 64) &&
+        map3(&tdo64, p.dO, (long long)p.H * DH, p.T, p.B, p.ld_o, p.bs_o, 64)) {
+      const size_t s1 = v3::dkv_smem_bytes();
+      cudaFuncSetAttribute(v3::swa_bwd_dkv_tc3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1);
+      launch_k(v3::swa_bwd_dkv_tc3_kernel, grid, v3::NT3, s1, s, tq, tq64, tdo64, p);
+    } else {
+      const size_t s1 = v2::dkv_smem_bytes();
+      cudaFuncSetAttribute(v2::swa_bwd_dkv_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1);
+      launch_k(v2::swa_bwd_dkv_tc2_kernel, grid, v2::NT2, s1, s, tq, tdo, p);
+    }
     cudaFuncSetAttribute(v2::swa_bwd_dq_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2);
     launch_k(v2::swa_bwd_dq_tc2_kernel, grid, v2::NT2, s2, s, tq, tdo, p);
     count_launch(2);

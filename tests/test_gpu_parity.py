@@ -227,7 +227,9 @@ def test_gdpa_fused_vs_gemm_composition(d, T, acts):
 @pytest.mark.parametrize("dtype", DTYPES)
 @pytest.mark.parametrize("T,w,causal,d,H", [(40, 3, False, 32, 2), (200, 64, False, 64, 4), (130, 17, True, 64, 4),
                                             (96, 200, False, 32, 2), (300, 128, False, 128, 2),
-                                            (257, 100, True, 256, 4), (260, 5, False, 64, 1)])
+                                            (257, 100, True, 256, 4), (260, 5, False, 64, 1),
+                                            (1024, 128, False, 256, 4), (384, 64, False, 128, 2),
+                                            (200, 7, True, 128, 2), (700, 127, False, 128, 2)])
 def test_swa_vs_oracle(dtype, T, w, causal, d, H):
     from paper_2602_10016_b200 import attention as A
     from paper_2602_10016_b200 import functional as F
