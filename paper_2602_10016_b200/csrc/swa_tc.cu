@@ -1380,13 +1380,21 @@ struct Tile {
   bool real;
 };
 
+// Half-blocks of the band of 128-block k0: queries that see keys [k0, k0+128)
+// (dK / dV, QM = false) or keys seen by queries [k0, k0+128) (dQ, QM = true).
+template <bool QM = false>
 __device__ __forceinline__ void band_of(const SwaP& p, Tile& t) {
   t.real = t.k0 < t.len;
   t.lo = t.n = 0;
   if (t.real) {
     int lo = max(0, t.k0 - p.w);
-    if (p.causal) lo = max(lo, t.k0);
-    const int hi = min(t.len - 1, t.k0 + TB - 1 + p.w);
+    int hi = min(t.len - 1, t.k0 + TB - 1 + p.w);
+    if (p.causal) {
+      if (QM)
+        hi = min(hi, t.k0 + TB - 1);
+      else
+        lo = max(lo, t.k0);
+    }
     t.lo = lo / HB;
     t.n = hi / HB - lo / HB + 1;
   }
@@ -1406,10 +1414,11 @@ struct Walk {
   bool done;
 };
 
+template <bool QM = false>
 __device__ __forceinline__ void walk_fill(const SwaP& p, Walk& w) {
   w.tl.k0 = w.kt * TB;
   w.tl.len = p.lengths[w.tl.b];
-  band_of(p, w.tl);
+  band_of<QM>(p, w.tl);
 }
 __device__ __forceinline__ void walk_adv(const SwaP& p, Walk& w) {
   ++w.idx;
@@ -1423,9 +1432,10 @@ __device__ __forceinline__ void walk_adv(const SwaP& p, Walk& w) {
   }
 }
 // Move to the next real tile at or after the current position.
+template <bool QM = false>
 __device__ __forceinline__ void walk_settle(const SwaP& p, Walk& w) {
   for (; w.idx < w.i1; walk_adv(p, w)) {
-    walk_fill(p, w);
+    walk_fill<QM>(p, w);
     if (!w.tl.real) continue;
     if (w.bh != w.seg_bh) {
       w.seg_bh = w.bh;
@@ -1439,6 +1449,7 @@ __device__ __forceinline__ void walk_settle(const SwaP& p, Walk& w) {
   }
   w.done = true;
 }
+template <bool QM = false>
 __device__ __forceinline__ void walk_init(const SwaP& p, Walk& w, int i0, int i1, int nT) {
   w.idx = i0;
   w.i1 = i1;
@@ -1451,17 +1462,19 @@ __device__ __forceinline__ void walk_init(const SwaP& p, Walk& w, int i0, int i1
   w.seg_bh = -1;
   w.seg_base = w.seg_first = w.ld_end = 0;
   w.done = false;
-  walk_settle(p, w);
+  walk_settle<QM>(p, w);
 }
+template <bool QM = false>
 __device__ __forceinline__ void walk_next_tile(const SwaP& p, Walk& w) {
   walk_adv(p, w);
-  walk_settle(p, w);
+  walk_settle<QM>(p, w);
 }
+template <bool QM = false>
 __device__ __forceinline__ void walk_step(const SwaP& p, Walk& w) {
   if (w.j + 1 < w.tl.lo + w.tl.n)
     ++w.j;
   else
-    walk_next_tile(p, w);
+    walk_next_tile<QM>(p, w);
 }
 __device__ __forceinline__ int load_index(const Walk& w, int j) { return w.seg_base + j - w.seg_first; }
 
@@ -1796,6 +1809,301 @@ __global__ void __launch_bounds__(NT3, 1)
 
 size_t dkv_smem_bytes() { return 1024 + 2 * 2 * TILE + QR * 2 * HTILE + 2 * 2 * PH + (4 + 2 * QR + 6 + 4 + 2) * 8 + 16; }
 
+// ---------------------------------------------------------------------------
+// dQ v3: the query-block-major mirror of dK / dV v3.  A tile is a 128-query
+// block, its items the 64-key half-blocks of its key band: S = Q K_j^T and
+// dP = dO V_j^T (2 x 64 TMEM columns, triple-buffered) by one issue warp,
+// dQ += dS_j K_j by another, two gradient warpgroups ping-ponging on
+// alternate half-blocks (thread = query row: its LSE / D are two registers,
+// the next tile's prefetched).  Q / dO are double-buffered per tile; K / V
+// arrive as 64-row boxes in a 6-slot ring kept across consecutive query
+// blocks of a sequence.
+constexpr int KR = 6;  // K | V half-block ring slots
+
+__global__ void __launch_bounds__(NT3, 1)
+    swa_bwd_dq_tc3_kernel(const __grid_constant__ CUtensorMap tqg, const __grid_constant__ CUtensorMap tdo,
+                          const __grid_constant__ CUtensorMap tkv64, SwaP p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sQG = sm;                    // 2 x (Q 16 KB | dO 16 KB)
+  uint8_t* sKV = sQG + 2 * 2 * TILE;    // KR x (K 8 KB | V 8 KB)
+  uint8_t* sDS = sKV + KR * 2 * HTILE;  // 2 x dS 16 KB (one per warpgroup)
+  uint64_t* bar = (uint64_t*)(sDS + 2 * PH);
+  uint64_t* qg_full = bar;                 // [2]
+  uint64_t* qg_empty = bar + 2;            // [2]
+  uint64_t* kv_full = bar + 4;             // [KR]
+  uint64_t* kv_empty = kv_full + KR;       // [KR]
+  uint64_t* sd_full = kv_empty + KR;       // [3]
+  uint64_t* sd_empty = sd_full + 3;        // [3]
+  uint64_t* ds_full = sd_empty + 3;        // [2]
+  uint64_t* ds_empty = ds_full + 2;        // [2]
+  uint64_t* acc_full = ds_empty + 2;
+  uint64_t* acc_empty = acc_full + 1;
+  uint32_t* tslot = (uint32_t*)(acc_empty + 1);
+
+  const int nT = (p.T + TB - 1) / TB;
+  const int W = p.B * p.H * nT;
+  const int i0 = (int)((long long)W * blockIdx.x / gridDim.x);
+  const int i1 = (int)((long long)W * (blockIdx.x + 1) / gridDim.x);
+  const int HD = p.H * DH;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    tc::prefetch_tmap(&tqg);
+    tc::prefetch_tmap(&tdo);
+    tc::prefetch_tmap(&tkv64);
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&qg_full[i], 1);
+      tc::mbar_init(&qg_empty[i], 1);
+      tc::mbar_init(&ds_full[i], 4);
+      tc::mbar_init(&ds_empty[i], 1);
+    }
+    for (int i = 0; i < KR; ++i) {
+      tc::mbar_init(&kv_full[i], 1);
+      tc::mbar_init(&kv_empty[i], 1);
+    }
+    for (int i = 0; i < 3; ++i) {
+      tc::mbar_init(&sd_full[i], 1);
+      tc::mbar_init(&sd_empty[i], 4);
+    }
+    tc::mbar_init(acc_full, 1);
+    tc::mbar_init(acc_empty, 4);
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tslot, 512);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tslot;
+  KL_PDL_ENTRY();
+  const uint32_t T_DQ = 384;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      Walk w;
+      walk_init<true>(p, w, i0, i1, nT);
+      int loaded = 0;  // K | V loads issued (ring position)
+      while (!w.done) {
+        const Tile& tl = w.tl;
+        const int qb = w.t & 1;
+        tc::mbar_wait(&qg_empty[qb], ((w.t >> 1) & 1) ^ 1);
+        tc::mbar_arrive_expect_tx(&qg_full[qb], 2 * TILE);
+        tc::tma_load_3d(sQG + qb * 2 * TILE, &tqg, &qg_full[qb], tl.h * DH, tl.k0, tl.b);
+        tc::tma_load_3d(sQG + qb * 2 * TILE + TILE, &tdo, &qg_full[qb], tl.h * DH, tl.k0, tl.b);
+        for (int j = tl.lo; j < tl.lo + tl.n; ++j) {
+          const int li = load_index(w, j);
+          if (li < loaded) continue;  // kept from the previous query block
+          const int s = li % KR;
+          tc::mbar_wait(&kv_empty[s], ((li / KR) & 1) ^ 1);
+          tc::mbar_arrive_expect_tx(&kv_full[s], 2 * HTILE);
+          tc::tma_load_3d(sKV + s * 2 * HTILE, &tkv64, &kv_full[s], HD + tl.h * DH, j * HB, tl.b);
+          tc::tma_load_3d(sKV + s * 2 * HTILE + HTILE, &tkv64, &kv_full[s], 2 * HD + tl.h * DH, j * HB, tl.b);
+          loaded = li + 1;
+        }
+        walk_next_tile<true>(p, w);
+      }
+    }
+  } else if (warp == 1) {
+    // S = Q K_j^T and dP = dO V_j^T into the 3-slot TMEM ring
+    if (lane == 0) {
+      Walk a;
+      walk_init<true>(p, a, i0, i1, nT);
+      int n = 0, waited = 0;
+      const uint32_t qg0 = tc::smem_u32(sQG), kv0 = tc::smem_u32(sKV);
+      while (!a.done) {
+        const int qb = a.t & 1;
+        if (a.j == a.tl.lo) tc::mbar_wait(&qg_full[qb], (a.t >> 1) & 1);
+        const int li = load_index(a, a.j);
+        if (li >= waited) {
+          tc::mbar_wait(&kv_full[li % KR], (li / KR) & 1);
+          waited = li + 1;
+        }
+        const int ss = n % 3;
+        tc::mbar_wait(&sd_empty[ss], ((n / 3) & 1) ^ 1);
+        tc::fence_after();
+        const uint32_t qa = qg0 + qb * 2 * TILE, ga = qa + TILE;
+        const uint32_t ka = kv0 + (li % KR) * 2 * HTILE, va = ka + HTILE;
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk)
+          tc::mma_bf16(tmem + ss * 128, d_kmaj64(qa, kk), d_kmaj64(ka, kk), IDESC_S64, kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk)
+          tc::mma_bf16(tmem + ss * 128 + 64, d_kmaj64(ga, kk), d_kmaj64(va, kk), IDESC_S64, kk > 0);
+        tc::mma_commit(&sd_full[ss]);
+        if (a.j == a.tl.lo + a.tl.n - 1) tc::mma_commit(&qg_empty[qb]);  // Q / dO of this tile no longer read
+        ++n;
+        walk_step<true>(p, a);
+      }
+    }
+  } else if (warp == 10) {
+    // dQ += dS_j K_j into the TMEM accumulator
+    if (lane == 0) {
+      Walk b;
+      walk_init<true>(p, b, i0, i1, nT);
+      int n = 0, keep = 0;
+      const uint32_t kv0 = tc::smem_u32(sKV), ds0 = tc::smem_u32(sDS);
+      while (!b.done) {
+        const bool first = b.j == b.tl.lo, last = b.j == b.tl.lo + b.tl.n - 1;
+        if (first) {
+          tc::mbar_wait(acc_empty, (b.t & 1) ^ 1);
+          // key half-blocks below `keep` are not seen by the next query block
+          // of this sequence: their ring slots are released after the product
+          keep = b.tl.lo + b.tl.n;
+          if (b.idx + 1 < b.i1 && b.kt + 1 < nT) {
+            Tile nx;
+            nx.k0 = (b.kt + 1) * TB;
+            nx.len = b.tl.len;
+            band_of<true>(p, nx);
+            if (nx.real) keep = nx.lo;
+          }
+        }
+        const int ps = n & 1;
+        tc::mbar_wait(&ds_full[ps], (n >> 1) & 1);
+        tc::fence_after();
+        const int li = load_index(b, b.j);
+        const uint32_t ka = kv0 + (li % KR) * 2 * HTILE;
+        const uint32_t da = ds0 + ps * PH;
+#pragma unroll
+        for (int kk = 0; kk < HB / 16; ++kk)
+          tc::mma_bf16(tmem + T_DQ, d_kmaj64(da, kk), d_mn(ka, kk), IDESC_PV, (!first || kk > 0) ? 1u : 0u);
+        tc::mma_commit(&ds_empty[ps]);
+        if (b.j < keep) tc::mma_commit(&kv_empty[li % KR]);
+        if (last) tc::mma_commit(acc_full);
+        ++n;
+        walk_step<true>(p, b);
+      }
+    }
+  } else {
+    const int wg = (warp - 2) >> 2, qtr = warp & 3;
+    const int r = qtr * 32 + lane;
+    const int wtid = (warp - 2 - 4 * wg) * 32 + lane;
+    const uint32_t trow = tmem + ((uint32_t)(qtr * 32) << 16);
+    const float c2 = p.scale * 1.4426950408889634f;
+    bf16* dq = (bf16*)p.dQKV;
+    int n_item = 0, t = 0;
+    Walk w;  // all tiles, real or not (padding query blocks get zero rows)
+    w.idx = i0;
+    w.i1 = i1;
+    w.nT = nT;
+    w.kt = i0 % nT;
+    w.bh = i0 / nT;
+    w.tl.b = w.bh % p.B;
+    w.tl.h = w.bh / p.B;
+    // this row's LSE (log2 units) / D of the next real tile, prefetched
+    auto fetch = [&](const Tile& tl, float& l2, float& dr) {
+      const int q = tl.k0 + r;
+      const long long off = ((long long)tl.b * p.H + tl.h) * p.T + q;
+      l2 = q < tl.len ? p.LSE[off] * 1.4426950408889634f : 0.f;
+      dr = q < tl.len ? p.Dbuf[off] : 0.f;
+    };
+    Walk pw = w;
+    walk_fill<true>(p, pw);
+    while (pw.idx < i1 && !pw.tl.real) {
+      walk_adv(p, pw);
+      if (pw.idx < i1) walk_fill<true>(p, pw);
+    }
+    float nl = 0.f, nd = 0.f;
+    if (pw.idx < i1) fetch(pw.tl, nl, nd);
+    for (; w.idx < i1; walk_adv(p, w)) {
+      walk_fill<true>(p, w);
+      const Tile tl = w.tl;
+      bf16* out = dq + (long long)tl.b * p.bs_qkv + tl.h * DH;
+      if (!tl.real) {
+        zero_rows(out, p.ld_qkv, tl.k0, TB, p.T, wg * 128 + wtid, 256);
+        continue;
+      }
+      const float lse2 = nl, dr = nd;
+      pw = w;
+      do {
+        walk_adv(p, pw);
+        if (pw.idx < i1) walk_fill<true>(p, pw);
+      } while (pw.idx < i1 && !pw.tl.real);
+      if (pw.idx < i1) fetch(pw.tl, nl, nd);
+      const int q = tl.k0 + r;
+      int klo = max(0, q - p.w), khi = min(tl.len - 1, q + p.w);
+      if (p.causal) khi = min(khi, q);
+      if (q >= tl.len) khi = -1;
+      const int last_item = n_item + tl.n - 1;
+      for (int jj = 0; jj < tl.n; ++jj, ++n_item) {
+        if ((n_item & 1) != wg) continue;
+        const int ss = n_item % 3;
+        uint8_t* blk = sDS + wg * PH;
+        tc::mbar_wait(&sd_full[ss], (n_item / 3) & 1);
+        tc::fence_after();
+#pragma unroll 1
+        for (int ch = 0; ch < 2; ++ch) {
+          const int k0c = (tl.lo + jj) * HB + ch * 32;
+          float sv[32], g[32];
+          tc::tmem_ld32(trow + ss * 128 + ch * 32, sv);
+          tc::tmem_ld32(trow + ss * 128 + 64 + ch * 32, g);
+          if (ch == 1) {
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&sd_empty[ss]);
+          }
+          uint32_t pk[16];
+          if (k0c > khi || k0c + 31 < klo) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) pk[i] = 0u;
+          } else if (k0c >= klo && k0c + 31 <= khi) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) {
+              const float a0 = ex2(fmaf(sv[i], c2, -lse2)) * (g[i] - dr);
+              const float a1 = ex2(fmaf(sv[i + 1], c2, -lse2)) * (g[i + 1] - dr);
+              pk[i >> 1] = tc::pack_bf16(a0, a1);
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) {
+              const bool ok0 = k0c + i >= klo && k0c + i <= khi, ok1 = k0c + i + 1 >= klo && k0c + i + 1 <= khi;
+              const float a0 = ok0 ? ex2(fmaf(sv[i], c2, -lse2)) * (g[i] - dr) : 0.f;
+              const float a1 = ok1 ? ex2(fmaf(sv[i + 1], c2, -lse2)) * (g[i + 1] - dr) : 0.f;
+              pk[i >> 1] = tc::pack_bf16(a0, a1);
+            }
+          }
+          if (ch == 0) tc::mbar_wait(&ds_empty[wg], ((n_item >> 1) & 1) ^ 1);
+          store_sw(blk, r, ch * 32, pk);
+        }
+        tc::fence_async_smem();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&ds_full[wg]);
+      }
+      if ((last_item & 1) == wg) {
+        tc::mbar_wait(acc_full, t & 1);
+        tc::fence_after();
+#pragma unroll 1
+        for (int ch = 0; ch < 2; ++ch) {
+          float v[32];
+          tc::tmem_ld32(trow + T_DQ + ch * 32, v);
+          if (ch == 1) {
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(acc_empty);
+          }
+          if (q < p.T) {
+            uint4* o = reinterpret_cast<uint4*>(out + (long long)q * p.ld_qkv + ch * 32);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              uint4 u;
+              u.x = tc::pack_bf16(v[8 * c + 0] * p.scale, v[8 * c + 1] * p.scale);
+              u.y = tc::pack_bf16(v[8 * c + 2] * p.scale, v[8 * c + 3] * p.scale);
+              u.z = tc::pack_bf16(v[8 * c + 4] * p.scale, v[8 * c + 5] * p.scale);
+              u.w = tc::pack_bf16(v[8 * c + 6] * p.scale, v[8 * c + 7] * p.scale);
+              o[c] = u;
+            }
+          }
+        }
+      }
+      ++t;
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tmem, 512);
+}
+
+size_t dq_smem_bytes() { return 1024 + 2 * 2 * TILE + KR * 2 * HTILE + 2 * PH + (4 + 2 * KR + 6 + 4 + 2) * 8 + 16; }
+
 }  // namespace v3
 
 bool map3(CUtensorMap* m, const void* ptr, long long inner, int T, int B, long long ld, long long bs,
@@ -1864,8 +2172,15 @@ int swa_bwd_tc(const SwaP& p, cudaStream_t s) {
       cudaFuncSetAttribute(v2::swa_bwd_dkv_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1);
       launch_k(v2::swa_bwd_dkv_tc2_kernel, grid, v2::NT2, s1, s, tq, tdo, p);
     }
-    cudaFuncSetAttribute(v2::swa_bwd_dq_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2);
-    launch_k(v2::swa_bwd_dq_tc2_kernel, grid, v2::NT2, s2, s, tq, tdo, p);
+    CUtensorMap tkv64;
+    if (!getenv("KL_SWA_DQ_V2") && map3(&tkv64, p.QKV, 3LL * p.H * DH, p.T, p.B, p.ld_qkv, p.bs_qkv, 64)) {
+      const size_t s3 = v3::dq_smem_bytes();
+      cudaFuncSetAttribute(v3::swa_bwd_dq_tc3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s3);
+      launch_k(v3::swa_bwd_dq_tc3_kernel, grid, v3::NT3, s3, s, tq, tdo, tkv64, p);
+    } else {
+      cudaFuncSetAttribute(v2::swa_bwd_dq_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2);
+      launch_k(v2::swa_bwd_dq_tc2_kernel, grid, v2::NT2, s2, s, tq, tdo, p);
+    }
     count_launch(2);
     return launch_check("swa_bwd_tc2");
   }

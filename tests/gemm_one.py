@@ -20,6 +20,8 @@ for _ in range(3):
         gemm(S, W.t(), out3)
     elif which == "bias":
         gemm(S, W[:d].t(), out1, bias=bias)
+    elif which == "dx":  # attention-input gradient: dQKV @ Wqkv, accumulated onto the residual gradient
+        gemm(out3, W, out1, residual=out1)
     else:
         gemm(S, W[:d].t(), out1, residual=S)
 torch.cuda.synchronize()
