@@ -1819,6 +1819,7 @@ size_t dkv_smem_bytes() { return 1024 + 2 * 2 * TILE + QR * 2 * HTILE + 2 * 2 * 
 // arrive as 64-row boxes in a 6-slot ring kept across consecutive query
 // blocks of a sequence.
 constexpr int KR = 6;  // K | V half-block ring slots
+constexpr float RESCALE2 = 8.f;  // lazy-rescale threshold (log2 units)
 
 __global__ void __launch_bounds__(NT3, 1)
     swa_bwd_dq_tc3_kernel(const __grid_constant__ CUtensorMap tqg, const __grid_constant__ CUtensorMap tdo,
@@ -2104,6 +2105,267 @@ __global__ void __launch_bounds__(NT3, 1)
 
 size_t dq_smem_bytes() { return 1024 + 2 * 2 * TILE + KR * 2 * HTILE + 2 * PH + (4 + 2 * KR + 6 + 4 + 2) * 8 + 16; }
 
+// ---------------------------------------------------------------------------
+// Forward v3: 128-query tiles, 64-key half-block items, online softmax with
+// lazy rescaling (the reference max moves only when a block max exceeds it
+// by > 8 in log2 units; O is rescaled in TMEM then), two CTAs per SM.
+//   warp 0     TMA: the tile's Q (128 x 64), K / V half-blocks (64 x 64) in a
+//              3-slot ring
+//   warp 1     S_j = Q K_j^T (N = 64) into a 3-slot TMEM ring
+//   warp 2     O += P_j V_j (K = 64) into the TMEM accumulator
+//   warps 3-6  softmax, thread = query row: block max, rescale, P_j = exp2
+//              -> smem (2 slots), epilogue O / l -> bf16, LSE
+// TMEM 256 columns (3 x 64 S + 64 O) and ~97 KB smem per CTA: two CTAs share
+// an SM, so one CTA's softmax overlaps the other's MMAs and loads.
+constexpr int NTF = 224;
+constexpr int FNS = 3;  // S ring slots
+constexpr int FKR = 3;  // K | V ring slots
+
+__global__ void __launch_bounds__(NTF, 2)
+    swa_fwd_tc3_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tkv64, SwaP p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sQ = sm;                      // 16 KB
+  uint8_t* sKV = sQ + TILE;              // FKR x (K 8 KB | V 8 KB)
+  uint8_t* sP = sKV + FKR * 2 * HTILE;   // 2 x P 16 KB
+  uint64_t* bar = (uint64_t*)(sP + 2 * PH);
+  uint64_t* q_full = bar;
+  uint64_t* q_empty = bar + 1;
+  uint64_t* kv_full = bar + 2;            // [FKR]
+  uint64_t* kv_empty = kv_full + FKR;     // [FKR]
+  uint64_t* s_full = kv_empty + FKR;      // [FNS]
+  uint64_t* s_empty = s_full + FNS;       // [FNS]
+  uint64_t* p_full = s_empty + FNS;       // [2]
+  uint64_t* p_empty = p_full + 2;         // [2]
+  uint64_t* o_full = p_empty + 2;
+  uint64_t* o_empty = o_full + 1;
+  uint32_t* tslot = (uint32_t*)(o_empty + 1);
+
+  const int nT = (p.T + TB - 1) / TB;
+  const int W = p.B * p.H * nT;
+  const int i0 = (int)((long long)W * blockIdx.x / gridDim.x);
+  const int i1 = (int)((long long)W * (blockIdx.x + 1) / gridDim.x);
+  const int HD = p.H * DH;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    tc::prefetch_tmap(&tq);
+    tc::prefetch_tmap(&tkv64);
+    tc::mbar_init(q_full, 1);
+    tc::mbar_init(q_empty, 1);
+    for (int i = 0; i < FKR; ++i) {
+      tc::mbar_init(&kv_full[i], 1);
+      tc::mbar_init(&kv_empty[i], 1);
+    }
+    for (int i = 0; i < FNS; ++i) {
+      tc::mbar_init(&s_full[i], 1);
+      tc::mbar_init(&s_empty[i], 4);
+    }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&p_full[i], 4);
+      tc::mbar_init(&p_empty[i], 1);
+    }
+    tc::mbar_init(o_full, 1);
+    tc::mbar_init(o_empty, 4);
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tslot, 256);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tslot;
+  KL_PDL_ENTRY();
+  const uint32_t T_O = FNS * 64;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      Walk w;
+      walk_init<true>(p, w, i0, i1, nT);
+      int n = 0;
+      while (!w.done) {
+        const Tile& tl = w.tl;
+        tc::mbar_wait(q_empty, (w.t & 1) ^ 1);
+        tc::mbar_arrive_expect_tx(q_full, TILE);
+        tc::tma_load_3d(sQ, &tq, q_full, tl.h * DH, tl.k0, tl.b);
+        for (int j = tl.lo; j < tl.lo + tl.n; ++j, ++n) {
+          const int s = n % FKR;
+          tc::mbar_wait(&kv_empty[s], ((n / FKR) & 1) ^ 1);
+          tc::mbar_arrive_expect_tx(&kv_full[s], 2 * HTILE);
+          tc::tma_load_3d(sKV + s * 2 * HTILE, &tkv64, &kv_full[s], HD + tl.h * DH, j * HB, tl.b);
+          tc::tma_load_3d(sKV + s * 2 * HTILE + HTILE, &tkv64, &kv_full[s], 2 * HD + tl.h * DH, j * HB, tl.b);
+        }
+        walk_next_tile<true>(p, w);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      Walk a;
+      walk_init<true>(p, a, i0, i1, nT);
+      int n = 0;
+      const uint32_t qa = tc::smem_u32(sQ), kv0 = tc::smem_u32(sKV);
+      while (!a.done) {
+        if (a.j == a.tl.lo) tc::mbar_wait(q_full, a.t & 1);
+        const int s = n % FKR, ss = n % FNS;
+        tc::mbar_wait(&kv_full[s], (n / FKR) & 1);
+        tc::mbar_wait(&s_empty[ss], ((n / FNS) & 1) ^ 1);
+        tc::fence_after();
+        const uint32_t ka = kv0 + s * 2 * HTILE;
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk)
+          tc::mma_bf16(tmem + ss * 64, d_kmaj64(qa, kk), d_kmaj64(ka, kk), IDESC_S64, kk > 0);
+        tc::mma_commit(&s_full[ss]);
+        if (a.j == a.tl.lo + a.tl.n - 1) tc::mma_commit(q_empty);
+        ++n;
+        walk_step<true>(p, a);
+      }
+    }
+  } else if (warp == 2) {
+    if (lane == 0) {
+      Walk b;
+      walk_init<true>(p, b, i0, i1, nT);
+      int n = 0;
+      const uint32_t kv0 = tc::smem_u32(sKV), p0 = tc::smem_u32(sP);
+      while (!b.done) {
+        const bool first = b.j == b.tl.lo, last = b.j == b.tl.lo + b.tl.n - 1;
+        if (first) tc::mbar_wait(o_empty, (b.t & 1) ^ 1);
+        const int ps = n & 1, s = n % FKR;
+        tc::mbar_wait(&p_full[ps], (n >> 1) & 1);
+        tc::fence_after();
+        const uint32_t va = kv0 + s * 2 * HTILE + HTILE, pa = p0 + ps * PH;
+#pragma unroll
+        for (int kk = 0; kk < HB / 16; ++kk)
+          tc::mma_bf16(tmem + T_O, d_kmaj64(pa, kk), d_mn(va, kk), IDESC_PV, (!first || kk > 0) ? 1u : 0u);
+        tc::mma_commit(&p_empty[ps]);
+        tc::mma_commit(&kv_empty[s]);  // S_j was read before P_j existed: K_j and V_j are done
+        if (last) tc::mma_commit(o_full);
+        ++n;
+        walk_step<true>(p, b);
+      }
+    }
+  } else {
+    const int qtr = warp & 3;
+    const int r = qtr * 32 + lane;
+    const int ctid = threadIdx.x - 96;
+    const uint32_t trow = tmem + ((uint32_t)(qtr * 32) << 16);
+    const float c2 = p.scale * 1.4426950408889634f;
+    bf16* Obase = (bf16*)p.O;
+    int n = 0, t = 0;
+    Walk w;
+    w.idx = i0;
+    w.i1 = i1;
+    w.nT = nT;
+    w.kt = i0 % nT;
+    w.bh = i0 / nT;
+    w.tl.b = w.bh % p.B;
+    w.tl.h = w.bh / p.B;
+    for (; w.idx < i1; walk_adv(p, w)) {
+      walk_fill<true>(p, w);
+      const Tile tl = w.tl;
+      bf16* O = Obase + (long long)tl.b * p.bs_o + tl.h * DH;
+      float* LSE = p.LSE + ((long long)tl.b * p.H + tl.h) * p.T;
+      if (!tl.real) {  // padding-only query block
+        zero_rows(O, p.ld_o, tl.k0, TB, p.T, ctid, 128);
+        if (tl.k0 + ctid < p.T) LSE[tl.k0 + ctid] = INFINITY;
+        continue;
+      }
+      const int q = tl.k0 + r;
+      int klo = max(0, q - p.w), khi = min(tl.len - 1, q + p.w);
+      if (p.causal) khi = min(khi, q);
+      if (q >= tl.len) khi = -1;
+      float mref = -INFINITY, l = 0.f;
+      for (int jj = 0; jj < tl.n; ++jj, ++n) {
+        const int ss = n % FNS, ps = n & 1;
+        const int k0 = (tl.lo + jj) * HB;
+        float v[64];
+        tc::mbar_wait(&s_full[ss], (n / FNS) & 1);
+        tc::fence_after();
+        tc::tmem_ld32(trow + ss * 64, v);
+        tc::tmem_ld32(trow + ss * 64 + 32, v + 32);
+        tc::fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&s_empty[ss]);
+        // mask to -inf outside [klo, khi]; block max in log2 units
+        float mb = -INFINITY;
+        if (k0 >= klo && k0 + 63 <= khi) {
+#pragma unroll
+          for (int i = 0; i < 64; ++i) mb = fmaxf(mb, v[i]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 64; ++i) {
+            const bool ok = k0 + i >= klo && k0 + i <= khi;
+            v[i] = ok ? v[i] : -INFINITY;
+            mb = fmaxf(mb, v[i]);
+          }
+        }
+        mb = mb == -INFINITY ? -INFINITY : mb * c2;
+        const bool up = mb > mref + RESCALE2;
+        // the P slot is free once the product of the item two back completed
+        tc::mbar_wait(&p_empty[ps], ((n >> 1) & 1) ^ 1);
+        if (jj > 0 && __any_sync(0xffffffffu, up)) {
+          // O must be stable: the previous item's product has completed too
+          tc::mbar_wait(&p_empty[ps ^ 1], (((n - 1) >> 1) & 1));
+          tc::fence_after();
+          const float al = up ? ex2(mref - mb) : 1.f;
+          l *= al;
+#pragma unroll 1
+          for (int c0 = 0; c0 < DH; c0 += 16) {
+            float o[16];
+            uint32_t u[16];
+            tc::tmem_ld16(trow + T_O + c0, o);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) u[i] = __float_as_uint(o[i] * al);
+            tc::tmem_st16(trow + T_O + c0, u);
+          }
+          tc::fence_before();
+        }
+        if (up) mref = mb;
+        const float mr = mref == -INFINITY ? 0.f : mref;  // nothing visible yet: every P is exp2(-inf) = 0
+        uint32_t pk[32];
+#pragma unroll
+        for (int i = 0; i < 64; i += 2) {
+          const float a0 = ex2(fmaf(v[i], c2, -mr)), a1 = ex2(fmaf(v[i + 1], c2, -mr));
+          l += a0 + a1;
+          pk[i >> 1] = tc::pack_bf16(a0, a1);
+        }
+        uint8_t* blk = sP + ps * PH;
+        store_sw(blk, r, 0, pk);
+        store_sw(blk, r, 32, pk + 16);
+        tc::fence_async_smem();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&p_full[ps]);
+      }
+      tc::mbar_wait(o_full, t & 1);
+      tc::fence_after();
+      float o[64];
+      tc::tmem_ld32(trow + T_O, o);
+      tc::tmem_ld32(trow + T_O + 32, o + 32);
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(o_empty);
+      if (q < p.T) {
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+        uint4* dst = reinterpret_cast<uint4*>(O + (long long)q * p.ld_o);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          uint4 u;
+          u.x = tc::pack_bf16(o[8 * c + 0] * inv, o[8 * c + 1] * inv);
+          u.y = tc::pack_bf16(o[8 * c + 2] * inv, o[8 * c + 3] * inv);
+          u.z = tc::pack_bf16(o[8 * c + 4] * inv, o[8 * c + 5] * inv);
+          u.w = tc::pack_bf16(o[8 * c + 6] * inv, o[8 * c + 7] * inv);
+          dst[c] = u;
+        }
+        LSE[q] = l > 0.f ? (mref + __log2f(l)) * 0.6931471805599453f : INFINITY;
+      }
+      ++t;
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tmem, 256);
+}
+
+size_t fwd_smem_bytes() { return 1024 + TILE + FKR * 2 * HTILE + 2 * PH + (2 + 2 * FKR + 2 * FNS + 4 + 2) * 8 + 16; }
+
 }  // namespace v3
 
 bool map3(CUtensorMap* m, const void* ptr, long long inner, int T, int B, long long ld, long long bs,
@@ -2138,11 +2400,19 @@ int swa_fwd_tc(const SwaP& p, cudaStream_t s) {
     dim3 grid((p.T + TB - 1) / TB, p.H, p.B);
     launch_k(swa_fwd_tc_kernel, grid, NT, smem, s, tq, p);
   } else {
-    const size_t smem = v2::smem_bytes();
-    cudaFuncSetAttribute(v2::swa_fwd_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int W = p.B * p.H * ((p.T + TB - 1) / TB);
-    const int grid = std::min(W, tc_num_sms());
-    launch_k(v2::swa_fwd_tc2_kernel, grid, v2::NT2, smem, s, tq, p);
+    CUtensorMap tkv64;
+    if (!getenv("KL_SWA_FWD_V2") && map3(&tkv64, p.QKV, 3LL * p.H * DH, p.T, p.B, p.ld_qkv, p.bs_qkv, 64)) {
+      const size_t smem = v3::fwd_smem_bytes();
+      cudaFuncSetAttribute(v3::swa_fwd_tc3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      const int grid = std::min(W, 2 * tc_num_sms());
+      launch_k(v3::swa_fwd_tc3_kernel, grid, v3::NTF, smem, s, tq, tkv64, p);
+    } else {
+      const size_t smem = v2::smem_bytes();
+      cudaFuncSetAttribute(v2::swa_fwd_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      const int grid = std::min(W, tc_num_sms());
+      launch_k(v2::swa_fwd_tc2_kernel, grid, v2::NT2, smem, s, tq, p);
+    }
   }
   count_launch();
   return launch_check("swa_fwd_tc");
