@@ -459,10 +459,29 @@ def main():
     bwd_avg = (sum(swab_ms) / len(swab_ms)) if swab_ms else None
     roof = None
     if fwd_avg:
-        ach = swa_flops / (fwd_avg / 1e3) / 1e12
-        roof = {"bound": "tensor", "kernel": "kl_swa_fwd (banded flash attention core)", "achieved": ach,
-                "peak": burst, "unit": "TFLOP/s", "frac": ach / burst, "traffic": None,
-                "algorithmic_flops_per_launch": swa_flops, "avg_launch_ms": fwd_avg,
+        # The banded attention core reads Q, K, V (B*T*3*H*d_h bf16) and
+        # writes O (bf16) + LSE (fp32) once: at d_h = 64 its floor is HBM
+        # (bytes / 6.5 TB/s) above the tensor floor (executed flops / peak),
+        # so the roofline is the HBM one; the tensor numbers ride along.
+        H_ = cfg.heads
+        swa_bytes = float(sum(B * ev.T * (3 * cfg.d * 2 + cfg.d * 2 + H_ * 4) for ev in cfg.events))
+        ach_gbs = swa_bytes / (fwd_avg / 1e3) / 1e9
+        ach_tf = swa_flops / (fwd_avg / 1e3) / 1e12
+        traffic = None
+        try:  # dram__bytes_read.sum + dram__bytes_write.sum of the same kernel/shape (ncu --set full)
+            prof = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                                               "r1_swa3_ncu.json")))
+            k = prof["kernels"].get("swa_fwd_tc3_kernel")
+            if k and args.config == "c2" and B == 128:
+                traffic = k["dram_bytes_per_launch"]
+        except (OSError, ValueError, KeyError):
+            pass
+        roof = {"bound": "hbm", "kernel": "kl_swa_fwd (banded flash attention core, swa_fwd_tc3_kernel)",
+                "achieved": ach_gbs, "peak": hbm, "unit": "GB/s", "frac": ach_gbs / hbm, "traffic": traffic,
+                "algorithmic_bytes_per_launch": swa_bytes, "avg_launch_ms": fwd_avg,
+                "tensor": {"achieved_tflops": ach_tf, "peak": burst, "frac": ach_tf / burst,
+                           "algorithmic_flops_per_launch": swa_flops,
+                           "floor_ms": {"hbm": swa_bytes / hbm / 1e6, "tensor": swa_flops / burst / 1e9}},
                 "bwd_avg_launch_ms": bwd_avg, "launches_per_step": n_swa_layers,
                 "share_of_step": (fwd_avg + (bwd_avg or 0)) * n_swa_layers / ms}
     achieved_tf = fps * value / world / 1e12
