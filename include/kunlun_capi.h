@@ -287,8 +287,8 @@ int kl_gram_triu_bwd(int B, int n, int d, int dtype, const void* x, long long x_
 
 /* Gated residual of a Wukong expert: out = x + gd*deep + gt*dot, gates are
  * device fp32 scalars (shape (1,), interaction.py:97-98).  bwd: ddeep = g*gd,
- * ddot = g*gt, dx += g, dgate_{deep,dot} = sum(g*deep), sum(g*dot) (fp32,
- * written; fp64 accumulation; scratch >= 2*512 doubles).  All tensors
+ * ddot = g*gt, dx += g, dgate_{deep,dot} += sum(g*deep), sum(g*dot) (fp32,
+ * accumulated into the gate gradients; fp64 sums; scratch >= 2*512 doubles).  All tensors
  * (rows, d) contiguous with row strides given. */
 int kl_gated_sum_fwd(int rows, int d, int dtype, const void* x, long long x_rs, const void* deep,
                      const void* dot, const float* gd, const float* gt, void* out, long long o_rs,

@@ -466,9 +466,9 @@ __global__ void reduce_pairs_kernel(int nblk, const double* partial, float* o0, 
   }
   a = block_sum_d(a, sh);
   b = block_sum_d(b, sh);
-  if (threadIdx.x == 0) {
-    o0[0] = (float)a;
-    o1[0] = (float)b;
+  if (threadIdx.x == 0) {  // accumulate into the gate gradients
+    o0[0] += (float)a;
+    o1[0] += (float)b;
   }
 }
 

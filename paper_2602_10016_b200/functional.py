@@ -17,6 +17,8 @@ from __future__ import annotations
 
 import ctypes as C
 
+import os
+
 import torch
 
 from . import _capi
@@ -83,6 +85,46 @@ def _codes(acts):
 
 def _stream():
     return _capi._stream()
+
+
+_SIDE = {}
+BRANCH_STREAMS = os.environ.get("KL_BRANCH_STREAMS", "1") != "0"
+
+
+def side_stream(device):
+    """One cached side stream per device for independent branches."""
+    key = torch.device(device).index or 0
+    if key not in _SIDE:
+        _SIDE[key] = torch.cuda.Stream(device=device)
+    return _SIDE[key]
+
+
+def run_branches(fns, device, inputs=()):
+    """Run independent branches ``fns`` (callables) alternately on the current
+    and a side stream, joined before returning; inside a CUDA graph capture
+    this becomes a fork / join of parallel graph branches, so the branches'
+    small kernels overlap.  Autograd runs each branch's backward on the stream
+    its forward ran on, so the backward branches overlap the same way.
+    Tensors crossing streams are recorded on the consuming stream."""
+    if not BRANCH_STREAMS or len(fns) < 2 or not torch.cuda.is_available():
+        return [f() for f in fns]
+    main = torch.cuda.current_stream(device)
+    side = side_stream(device)
+    side.wait_stream(main)
+    for t in inputs:  # made on the current stream, read by the side branches
+        t.record_stream(side)
+    outs = []
+    for i, f in enumerate(fns):
+        st = main if i % 2 == 0 else side
+        with torch.cuda.stream(st):
+            outs.append(f())
+    main.wait_stream(side)
+    for i, o in enumerate(outs):
+        if i % 2 == 1:
+            for t in (o if isinstance(o, (list, tuple)) else (o,)):
+                if isinstance(t, torch.Tensor):
+                    t.record_stream(main)
+    return outs
 
 
 def _as4(t):
@@ -774,13 +816,10 @@ class _Gated(torch.autograd.Function):
         ddeep = torch.empty_like(deep)
         ddot = torch.empty_like(dot)
         scratch = torch.empty(2 * 512, device=g.device, dtype=torch.float64)
-        dgd = torch.empty(1, device=g.device, dtype=torch.float32)
-        dgt = torch.empty(1, device=g.device, dtype=torch.float32)
+        dgd, dgt = P.g(ctx.gdkey), P.g(ctx.gtkey)  # fp32 (1,) views of the flat gradient: the kernel accumulates
         _capi.call("kl_gated_sum_bwd", B * n, d, _capi.dt(g), g.data_ptr(), d, deep.data_ptr(), dot.data_ptr(),
                    P.w32(ctx.gdkey).data_ptr(), P.w32(ctx.gtkey).data_ptr(), ddeep.data_ptr(), ddot.data_ptr(),
                    dgd.data_ptr(), dgt.data_ptr(), scratch.data_ptr(), _stream())
-        P.g(ctx.gdkey).add_(dgd)
-        P.g(ctx.gtkey).add_(dgt)
         return g, ddeep, ddot, None, None, None, None
 
 
