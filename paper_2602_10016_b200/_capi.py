@@ -208,10 +208,13 @@ WS_BYTES = 64 << 20  # split-K scratch per device (GEMMs run stream-ordered, so 
 
 
 def _workspace(device) -> torch.Tensor:
-    ws = _WS.get(device)
+    """Split-K scratch, one per (device, stream): GEMMs of parallel stream /
+    graph branches run concurrently and must not share it."""
+    key = (device, torch.cuda.current_stream(device).cuda_stream)
+    ws = _WS.get(key)
     if ws is None:
         ws = torch.empty(WS_BYTES // 4, dtype=torch.float32, device=device)
-        _WS[device] = ws
+        _WS[key] = ws
     return ws
 
 

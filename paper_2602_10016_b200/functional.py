@@ -49,18 +49,37 @@ class GradSink:
     first consumer whose backward runs registers its dS; consumers that can
     accumulate in their own epilogue (HSP pooling, recent rows) add into it
     and return no gradient, so autograd does not materialise and add one
-    (B, T, d) gradient per consumer."""
+    (B, T, d) gradient per consumer.  The consumers may run on different
+    streams (parallel branches): ``take`` orders the accumulation after the
+    registering stream's write, ``release`` orders the registering stream's
+    later work (the autograd consumers of the buffer) after it."""
 
-    __slots__ = ("t",)
+    __slots__ = ("t", "stream")
 
     def __init__(self):
         self.t = None
+        self.stream = None
+
+    def put(self, t):
+        self.t = t
+        self.stream = torch.cuda.current_stream(t.device) if t.is_cuda else None
 
     def take(self, like):
         t = self.t
         if t is not None and t.shape == like.shape and t.dtype == like.dtype and t.is_contiguous():
+            if self.stream is not None:
+                cur = torch.cuda.current_stream(t.device)
+                if cur != self.stream:
+                    cur.wait_stream(self.stream)
+                    t.record_stream(cur)
             return t
         return None
+
+    def release(self):
+        if self.stream is not None:
+            cur = torch.cuda.current_stream(self.t.device)
+            if cur != self.stream:
+                self.stream.wait_stream(cur)
 
 
 class ResidualStash:
@@ -91,15 +110,16 @@ _SIDE = {}
 BRANCH_STREAMS = os.environ.get("KL_BRANCH_STREAMS", "1") != "0"
 
 
-def side_stream(device):
-    """One cached side stream per device for independent branches."""
-    key = torch.device(device).index or 0
+def side_stream(device, name="side"):
+    """Cached side streams per (device, name) for independent branches
+    (distinct names for nested branch sets)."""
+    key = (torch.device(device).index or 0, name)
     if key not in _SIDE:
         _SIDE[key] = torch.cuda.Stream(device=device)
     return _SIDE[key]
 
 
-def run_branches(fns, device, inputs=()):
+def run_branches(fns, device, inputs=(), name="side"):
     """Run independent branches ``fns`` (callables) alternately on the current
     and a side stream, joined before returning; inside a CUDA graph capture
     this becomes a fork / join of parallel graph branches, so the branches'
@@ -109,21 +129,28 @@ def run_branches(fns, device, inputs=()):
     if not BRANCH_STREAMS or len(fns) < 2 or not torch.cuda.is_available():
         return [f() for f in fns]
     main = torch.cuda.current_stream(device)
-    side = side_stream(device)
+    side = side_stream(device, name)
     side.wait_stream(main)
     for t in inputs:  # made on the current stream, read by the side branches
-        t.record_stream(side)
+        if isinstance(t, torch.Tensor):
+            t.record_stream(side)
     outs = []
     for i, f in enumerate(fns):
         st = main if i % 2 == 0 else side
         with torch.cuda.stream(st):
             outs.append(f())
     main.wait_stream(side)
+
+    def record(o):
+        if isinstance(o, torch.Tensor):
+            o.record_stream(main)
+        elif isinstance(o, (list, tuple)):
+            for x in o:
+                record(x)
+
     for i, o in enumerate(outs):
         if i % 2 == 1:
-            for t in (o if isinstance(o, (list, tuple)) else (o,)):
-                if isinstance(t, torch.Tensor):
-                    t.record_stream(main)
+            record(o)
     return outs
 
 
@@ -327,7 +354,7 @@ class _GdpaCore(torch.autograd.Function):
             a.dY, a.dS, a.dKt, a.dVt = g.data_ptr(), dS.data_ptr(), dKt.data_ptr(), dVt.data_ptr()
             _capi.call("kl_gdpa_bwd", C.byref(a), _stream())
             if ctx.sink is not None and ctx.sink.t is None:
-                ctx.sink.t = dS
+                ctx.sink.put(dS)
             return dS, dKt, dVt, None, None, None, None, None
         S, Kt, Vt, Z, A, lengths = ctx.saved_tensors
         dZ = torch.empty_like(Z)
@@ -337,7 +364,7 @@ class _GdpaCore(torch.autograd.Function):
         dKt = gemm(dZ.transpose(1, 2), S)
         dVt = gemm(A.transpose(1, 2), g)
         if ctx.sink is not None and ctx.sink.t is None:
-            ctx.sink.t = dS
+            ctx.sink.put(dS)
         return dS, dKt, dVt, None, None, None, None, None
 
 
@@ -473,8 +500,9 @@ class _HspPool(torch.autograd.Function):
         if dS is not None and ctx.sink is not None:
             if ctx.sink.t is dS:
                 dS = None  # accumulated into the sequence's shared gradient buffer
+                ctx.sink.release()
             elif ctx.sink.t is None:
-                ctx.sink.t = dS
+                ctx.sink.put(dS)
         return dS, dQ, None, None, None, None
 
 

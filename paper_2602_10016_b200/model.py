@@ -196,28 +196,40 @@ class KunlunModel:
         if self.layer_hook is not None:
             outs = _Boundary.apply(self.layer_hook, l, X, *S_list)
             X, S_list = outs[0], list(outs[1:])
-        xsum = summarize_nonseq(X, F.PRef(self.P, lp.pool)) if (not flags.skip_pffn and live_seq) else None
-        H_list = []
         # one shared dS buffer per event sequence: its consumers (the GDPA
         # branch, HSP pooling + recent rows) accumulate into it
         sinks = [F.GradSink() for _ in cfg.events]
-        for e in range(len(cfg.events)):
-            if flags.skip_hsp:
-                H_list.append(H_prev[e])
-            else:
-                qr = qrows.get((l, e)) if qrows else None
-                H_list.append(hsp_summarize(S_list[e], lp.summ[e], lengths[e], sink=sinks[e], q_rows=qr).rows())
-        Xn = global_interaction(X, H_list, lp.gi)
-        S_out = []
-        for e, ev in enumerate(cfg.events):
-            s = S_list[e]
-            if live_seq and not flags.skip_pffn:
-                k, v = generate_kv(xsum, lp.wg[e], cfg.gdpa_cfg(e))
-                kt, vt = fold_kv(k, v, lp.wg[e])
-                s = F.gdpa_core(s, kt, vt, lengths[e], cfg.gdpa_acts, cfg.n_kv, 1.0 / float(ev.T), sink=sinks[e])
-            if live_seq and not flags.skip_self_attention:
-                s = mha_window(s, lp.mha[e], WindowSpec(ev.w, ev.causal), lengths[e])
-            S_out.append(s)
+
+        def x_branch():  # HSP summaries -> global interaction
+            H_list = []
+            for e in range(len(cfg.events)):
+                if flags.skip_hsp:
+                    H_list.append(H_prev[e])
+                else:
+                    qr = qrows.get((l, e)) if qrows else None
+                    H_list.append(hsp_summarize(S_list[e], lp.summ[e], lengths[e], sink=sinks[e], q_rows=qr).rows())
+            return global_interaction(X, H_list, lp.gi), H_list
+
+        def s_branch():  # GDPA (weights generated from X) -> windowed self-attention
+            xsum = summarize_nonseq(X, F.PRef(self.P, lp.pool)) if (not flags.skip_pffn and live_seq) else None
+            S_out = []
+            for e, ev in enumerate(cfg.events):
+                s = S_list[e]
+                if live_seq and not flags.skip_pffn:
+                    k, v = generate_kv(xsum, lp.wg[e], cfg.gdpa_cfg(e))
+                    kt, vt = fold_kv(k, v, lp.wg[e])
+                    s = F.gdpa_core(s, kt, vt, lengths[e], cfg.gdpa_acts, cfg.n_kv, 1.0 / float(ev.T), sink=sinks[e])
+                if live_seq and not flags.skip_self_attention:
+                    s = mha_window(s, lp.mha[e], WindowSpec(ev.w, ev.causal), lengths[e])
+                S_out.append(s)
+            return S_out
+
+        # the two branches only share their inputs: the sequence branch runs on
+        # the current stream, the summary / interaction branch beside it
+        # (parallel CUDA-graph branches, forward and backward)
+        shared = [X] + list(S_list) + list(qrows.values() if qrows else []) + list(H_prev or [])
+        S_out, (Xn, H_list) = F.run_branches([s_branch, x_branch], X.device, inputs=shared, name="xbranch")
+        S_out = list(S_out)
         return Xn, S_out, H_list
 
     def seq_live(self) -> list:
