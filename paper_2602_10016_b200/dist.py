@@ -18,6 +18,8 @@ from __future__ import annotations
 import torch
 import torch.distributed as dist
 
+from . import functional as F
+
 
 class GradReducer:
     def __init__(self, model, group=None, min_bucket: int = 1 << 20, average: bool = True):
@@ -47,6 +49,11 @@ class GradReducer:
             ev.record()
             with torch.cuda.stream(self.stream):
                 self.stream.wait_event(ev)
+                # the layer's gradients are also written on the parallel
+                # branch and weight-gradient streams (functional.run_branches,
+                # DW_STREAM): everything they were given so far precedes this
+                for st in F.side_streams(buf.device):
+                    self.stream.wait_stream(st)
                 dist.all_reduce(buf, group=self.group)
                 if self.average:
                     buf.mul_(1.0 / self.world)

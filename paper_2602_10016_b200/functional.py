@@ -110,6 +110,12 @@ _SIDE = {}
 BRANCH_STREAMS = os.environ.get("KL_BRANCH_STREAMS", "1") != "0"
 
 
+def side_streams(device):
+    """Every side stream created so far on ``device``."""
+    idx = torch.device(device).index or 0
+    return [st for (i, _), st in _SIDE.items() if i == idx]
+
+
 def side_stream(device, name="side"):
     """Cached side streams per (device, name) for independent branches
     (distinct names for nested branch sets)."""
@@ -117,6 +123,47 @@ def side_stream(device, name="side"):
     if key not in _SIDE:
         _SIDE[key] = torch.cuda.Stream(device=device)
     return _SIDE[key]
+
+
+# Weight gradients on their own stream: while a training step runs
+# (optim.TrainStep sets DW_STREAM), every weight / bias gradient GEMM is issued
+# on a "dw" side stream (forked from the node's stream), so the long-K,
+# HBM-bound dW products overlap the activation-gradient chain; TrainStep joins
+# the stream before the optimizer.  Off by default: a bare loss.backward()
+# leaves every kernel on the caller's streams.
+DW_STREAM = False
+
+
+class _DwFork:
+    __slots__ = ("prev", "st", "on")
+
+    def __init__(self, tensors):
+        self.on = DW_STREAM and torch.cuda.is_available()
+        if self.on:
+            dev = next(t.device for t in tensors if isinstance(t, torch.Tensor))
+            cur = torch.cuda.current_stream(dev)
+            self.st = side_stream(dev, "dw")
+            self.st.wait_stream(cur)
+            for t in tensors:
+                if isinstance(t, torch.Tensor):
+                    t.record_stream(self.st)
+
+    def __enter__(self):
+        if self.on:
+            self.prev = torch.cuda.current_stream(self.st.device)
+            torch.cuda.set_stream(self.st)
+        return self
+
+    def __exit__(self, *exc):
+        if self.on:
+            torch.cuda.set_stream(self.prev)
+        return False
+
+
+def dw_join(device):
+    """Current stream waits for the weight-gradient stream (see DW_STREAM)."""
+    if torch.cuda.is_available():
+        torch.cuda.current_stream(device).wait_stream(side_stream(device, "dw"))
 
 
 def run_branches(fns, device, inputs=(), name="side"):
@@ -197,14 +244,16 @@ class _MM(torch.autograd.Function):
         if ctx.aref is not None or ctx.needs_input_grad[0]:
             red = _bcast_reduce(A4, g4)
             if ctx.aref is not None:
-                gemm(g4, B4.transpose(2, 3), _as4(ctx.aref.g()), alpha=ctx.alpha, beta=1.0, reduce=red)
+                with _DwFork((g, Bm)):
+                    gemm(g4, B4.transpose(2, 3), _as4(ctx.aref.g()), alpha=ctx.alpha, beta=1.0, reduce=red)
             else:
                 da = gemm(g4, B4.transpose(2, 3), alpha=ctx.alpha, reduce=red)
                 da = da.reshape(a_t.shape)
         if ctx.bref is not None or ctx.needs_input_grad[1]:
             red = _bcast_reduce(B4, g4)
             if ctx.bref is not None:
-                gemm(A4.transpose(2, 3), g4, _as4(ctx.bref.g()), alpha=ctx.alpha, beta=1.0, reduce=red)
+                with _DwFork((g, A)):
+                    gemm(A4.transpose(2, 3), g4, _as4(ctx.bref.g()), alpha=ctx.alpha, beta=1.0, reduce=red)
             else:
                 db = gemm(A4.transpose(2, 3), g4, alpha=ctx.alpha, reduce=red)
                 db = db.reshape(b_t.shape)
@@ -276,12 +325,13 @@ class _Linear(torch.autograd.Function):
             dx = dx.reshape(ctx.xshape)
         # dW = sum over rows (and batch dims) of gp^T x
         gp4, x44 = _as4(gp), _as4(x4)
-        gemm(gp4.transpose(2, 3), x44, P.g(ctx.wkey), beta=1.0, reduce=(True, True))
-        if ctx.bkey:
-            rows = gp.numel() // gp.shape[-1]
-            ones = _ones(rows, gp.dtype, gp.device)
-            gemm(ones.view(1, rows), gp.reshape(rows, gp.shape[-1]) if gp.is_contiguous() else gp.contiguous().view(rows, -1),
-                 P.g(ctx.bkey).view(1, -1), beta=1.0)
+        rows = gp.numel() // gp.shape[-1]
+        gpc = gp if gp.is_contiguous() else gp.contiguous()
+        ones = _ones(rows, gp.dtype, gp.device) if ctx.bkey else None
+        with _DwFork((gp, gpc, x4, ones)):
+            gemm(gp4.transpose(2, 3), x44, P.g(ctx.wkey), beta=1.0, reduce=(True, True))
+            if ctx.bkey:
+                gemm(ones.view(1, rows), gpc.view(rows, -1), P.g(ctx.bkey).view(1, -1), beta=1.0)
         dres = g.reshape(ctx.xshape[:-1] + (g.shape[-1],)) if ctx.has_res else None
         if dres is not None and ctx.stash_out is not None:
             ctx.stash_out.g = dres  # added by the earlier op's dX epilogue instead

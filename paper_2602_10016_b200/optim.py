@@ -38,10 +38,17 @@ class TrainStep:
         self.loss = None
 
     def eager(self):
+        from . import functional as F
+
         m = self.model
         m.P.zero_grad()
         loss, _ = m.loss(self.X, self.S, self.lengths, self.labels)
-        loss.backward()
+        F.DW_STREAM = F.BRANCH_STREAMS  # weight-gradient GEMMs beside the dX chain
+        try:
+            loss.backward()
+        finally:
+            F.DW_STREAM = False
+        F.dw_join(self.X.device)
         if self.reducer is not None:
             self.reducer.finish()
         self.opt.step()

@@ -21,11 +21,15 @@ def _run(model, batch, graph):
         torch.cuda.synchronize()
         return float(loss), logits.detach().float().clone(), model.P.gflat.detach().clone()
     opt = FlatAdam(model.P, lr=0.0)
-    st = TrainStep(model, opt, X, S, L, y).capture(warmup=1)
-    model.P.zero_grad()
-    st()
+    st = TrainStep(model, opt, X, S, L, y)
+    if graph == "eager-step":  # TrainStep without capture (weight-gradient stream on)
+        st.loss = st.eager()
+    else:
+        st.capture(warmup=1)
+        model.P.zero_grad()
+        st()
     torch.cuda.synchronize()
-    return float(st.loss), None, model.P.gflat.detach().clone()
+    return float(st.loss.detach()), None, model.P.gflat.detach().clone()
 
 
 @pytest.mark.parametrize("compskip", [False, True])
@@ -51,6 +55,7 @@ def test_branch_streams_match_serial(compskip):
         F.BRANCH_STREAMS = True
         l1, z1, g1 = _run(model, batch, graph=False)
         l2, _, g2 = _run(model, batch, graph=True)
+        l3, _, g3 = _run(model, batch, graph="eager-step")
     finally:
         F.BRANCH_STREAMS = old
     scale = float(g0.abs().max())
@@ -59,3 +64,5 @@ def test_branch_streams_match_serial(compskip):
     assert float((g1 - g0).abs().max()) <= 2e-2 * scale
     assert abs(l2 - l0) <= 1e-3 * max(1.0, abs(l0))
     assert float((g2 - g0).abs().max()) <= 2e-2 * scale
+    assert abs(l3 - l0) <= 1e-3 * max(1.0, abs(l0))
+    assert float((g3 - g0).abs().max()) <= 2e-2 * scale
