@@ -277,7 +277,9 @@ int kl_recent_rows_bwd(int B, int T, int d, int n_recent, int dtype, const void*
                        const int* lengths, void* dS, long long s_bs, void* stream);
 
 /* Wukong pairwise-dot block (interaction.py:63-76, 106-121):
- * tri[b, p] = x[b, r_p] . x[b, c_p] over np.triu_indices(n) order.
+ * tri[b, p] = x[b, r_p] . x[b, c_p] over np.triu_indices(n) order; columns
+ * n(n+1)/2 .. t_bs-1 of each row (the padding of a contiguous (B, t_bs) tri)
+ * are written as zeros.
  * bwd: dx[b] += (dG + dG^T) x[b] with dG scattered from dtri. */
 int kl_gram_triu_fwd(int B, int n, int d, int dtype, const void* x, long long x_rs, long long x_bs,
                      void* tri, long long t_bs, void* stream);
@@ -296,6 +298,11 @@ int kl_gated_sum_fwd(int rows, int d, int dtype, const void* x, long long x_rs, 
 int kl_gated_sum_bwd(int rows, int d, int dtype, const void* g, long long g_rs, const void* deep,
                      const void* dot, const float* gd, const float* gt, void* ddeep, void* ddot,
                      float* dgd, float* dgt, float* scratch, void* stream);
+
+/* out[r] = sum_k a[r, k] * b[r, k], fp32 accumulation (rows of length d,
+ * row strides a_rs / b_rs): the softmax-VJP row term rowsum(dO * O). */
+int kl_rowdot(int rows, int d, int dtype, const void* a, long long a_rs, const void* b, long long b_rs, float* out,
+              void* stream);
 
 /* Mean BCE with logits (tensor.py:535-549): loss[0] = mean(...), dz = (sig(z)-y)/n.
  * z, y, dz fp32 (n,). */

@@ -131,6 +131,8 @@ _SIGS = {
     "kl_gram_triu_fwd": ([C.c_int] * 4 + [C.c_void_p, C.c_longlong, C.c_longlong, C.c_void_p, C.c_longlong, C.c_void_p], C.c_int),
     "kl_gram_triu_bwd": ([C.c_int] * 4 + [C.c_void_p, C.c_longlong, C.c_longlong, C.c_void_p, C.c_longlong,
                                           C.c_void_p, C.c_longlong, C.c_longlong, C.c_void_p], C.c_int),
+    "kl_rowdot": ([C.c_int] * 3 + [C.c_void_p, C.c_longlong, C.c_void_p, C.c_longlong, C.c_void_p, C.c_void_p],
+                  C.c_int),
     "kl_gated_sum_fwd": ([C.c_int] * 3 + [C.c_void_p, C.c_longlong] + [C.c_void_p] * 5 + [C.c_longlong, C.c_void_p], C.c_int),
     "kl_gated_sum_bwd": ([C.c_int] * 3 + [C.c_void_p, C.c_longlong] + [C.c_void_p] * 10, C.c_int),
     "kl_bce_fwd_bwd": ([C.c_int] + [C.c_void_p] * 5, C.c_int),

@@ -363,6 +363,9 @@ __global__ void __launch_bounds__(256) gram_triu_fwd_kernel(int n, int d, const 
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (l == 0) stf(tri + (long long)b * t_bs + p, acc);
   }
+  // zero padding columns [np, t_bs) of a contiguous (B, t_bs) tri
+  if (blockIdx.y == 0)
+    for (int p = np_ + threadIdx.x; p < t_bs; p += blockDim.x) stf(tri + (long long)b * t_bs + p, 0.f);
 }
 
 // dx[b, r, k] += sum_j W[r][j] x[b, j, k], W symmetric from dtri (diagonal x2).
@@ -847,4 +850,53 @@ extern "C" int kl_adam_step(long long n, float lr, float beta1, float beta2, flo
   launch_k(adam_kernel, grid, 256, 0, s, n, lr, beta1, beta2, eps, step, step_dev, w, g, m, v, (bf16*)w_bf16);
   count_launch(step_dev ? 2 : 1);
   return launch_check("adam_step");
+}
+
+namespace kl {
+namespace {
+// out[r] = sum_k a[r, k] * b[r, k] (fp32 accumulation): one warp per row,
+// 16-byte loads when rows are 16-byte aligned (the softmax-VJP row term
+// rowsum(dO * O) of the pooling backward).
+template <typename T, bool VEC>
+__global__ void __launch_bounds__(256) rowdot_kernel(int rows, int d, const T* a, long long a_rs, const T* b,
+                                                     long long b_rs, float* out) {
+  KL_PDL_ENTRY();
+  const int r = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const T* ar = a + (long long)r * a_rs;
+  const T* br = b + (long long)r * b_rs;
+  float acc = 0.f;
+  if (VEC) {
+    for (int k = lane * 8; k < d; k += 256) {
+      float x[8], y[8];
+      ld8(ar + k, x);
+      ld8(br + k, y);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc = fmaf(x[i], y[i], acc);
+    }
+  } else {
+    for (int k = lane; k < d; k += 32) acc = fmaf(ldf(ar + k), ldf(br + k), acc);
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) out[r] = acc;
+}
+}  // namespace
+}  // namespace kl
+
+extern "C" int kl_rowdot(int rows, int d, int dtype, const void* a, long long a_rs, const void* b, long long b_rs,
+                         float* out, void* stream) {
+  using namespace kl;
+  if (rows <= 0) return KL_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const unsigned grid = (unsigned)((rows + 7) / 8);
+  const bool vec = vec8_ok(a, a_rs, d) && vec8_ok(b, b_rs, d);
+  if (dtype == KL_F32) {
+    if (vec) launch_k(rowdot_kernel<float, true>, grid, 256, 0, s, rows, d, (const float*)a, a_rs, (const float*)b, b_rs, out);
+    else launch_k(rowdot_kernel<float, false>, grid, 256, 0, s, rows, d, (const float*)a, a_rs, (const float*)b, b_rs, out);
+  } else {
+    if (vec) launch_k(rowdot_kernel<bf16, true>, grid, 256, 0, s, rows, d, (const bf16*)a, a_rs, (const bf16*)b, b_rs, out);
+    else launch_k(rowdot_kernel<bf16, false>, grid, 256, 0, s, rows, d, (const bf16*)a, a_rs, (const bf16*)b, b_rs, out);
+  }
+  count_launch();
+  return launch_check("rowdot");
 }

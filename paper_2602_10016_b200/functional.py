@@ -166,7 +166,7 @@ def dw_join(device):
         torch.cuda.current_stream(device).wait_stream(side_stream(device, "dw"))
 
 
-def run_branches(fns, device, inputs=(), name="side"):
+def run_branches(fns, device, inputs=(), name="side", side_first=False):
     """Run independent branches ``fns`` (callables) alternately on the current
     and a side stream, joined before returning; inside a CUDA graph capture
     this becomes a fork / join of parallel graph branches, so the branches'
@@ -182,8 +182,12 @@ def run_branches(fns, device, inputs=(), name="side"):
         if isinstance(t, torch.Tensor):
             t.record_stream(side)
     outs = []
+    # side_first: even-indexed branches go to the side stream.  The branch
+    # issued last creates the newest autograd nodes, whose backward runs
+    # first; callers use this to pick which branch's backward leads.
+    on_side = [(i % 2 == 0) == side_first for i in range(len(fns))]
     for i, f in enumerate(fns):
-        st = main if i % 2 == 0 else side
+        st = side if on_side[i] else main
         with torch.cuda.stream(st):
             outs.append(f())
     main.wait_stream(side)
@@ -196,7 +200,7 @@ def run_branches(fns, device, inputs=(), name="side"):
                 record(x)
 
     for i, o in enumerate(outs):
-        if i % 2 == 1:
+        if on_side[i]:
             record(o)
     return outs
 
@@ -627,7 +631,8 @@ def _hsp_fused_bwd(ctx, gs):
     gl = [torch.zeros_like(o) if g is None else g for g, o in zip(gs, outs)]
     dO = gl[0].contiguous() if len(gl) == 1 else torch.cat(gl, dim=1)
     O = outs[0] if len(outs) == 1 else torch.cat(outs, dim=1)
-    Dq = torch.linalg.vecdot(dO.float(), O.float())  # rowsum(dO * pooled): the softmax-VJP term
+    Dq = torch.empty(B, HQ, device=S.device, dtype=torch.float32)  # rowsum(dO * pooled): the softmax-VJP term
+    _capi.call("kl_rowdot", B * HQ, d, _capi.dt(dO), dO.data_ptr(), d, O.data_ptr(), d, Dq.data_ptr(), _stream())
     acc = ctx.sink.take(S) if ctx.sink is not None else None
     dS = acc if acc is not None else torch.empty_like(S)
     dZ = torch.empty(B, HQ, T, device=S.device, dtype=S.dtype)
@@ -846,7 +851,7 @@ class _GramTriu(torch.autograd.Function):
             raise ShapeError("gram_triu needs unit column stride")
         # pairs padded to a multiple of 8 (zeros) so the DotMap GEMM's rows are
         # 16-byte aligned for TMA; the padding multiplies zero weight columns
-        tri = torch.zeros(B, pad8(n * (n + 1) // 2), device=x.device, dtype=x.dtype)
+        tri = torch.empty(B, pad8(n * (n + 1) // 2), device=x.device, dtype=x.dtype)  # kernel zeroes the pad
         _capi.call("kl_gram_triu_fwd", B, n, d, _capi.dt(x), x.data_ptr(), x.stride(1), x.stride(0),
                    tri.data_ptr(), tri.stride(0), _stream())
         ctx.save_for_backward(x)

@@ -226,9 +226,12 @@ class KunlunModel:
 
         # the two branches only share their inputs: the sequence branch runs on
         # the current stream, the summary / interaction branch beside it
-        # (parallel CUDA-graph branches, forward and backward)
+        # (parallel CUDA-graph branches, forward and backward).  The sequence
+        # branch is issued last so its backward runs first: GDPA registers the
+        # shared dS and HSP pooling accumulates into it.
         shared = [X] + list(S_list) + list(qrows.values() if qrows else []) + list(H_prev or [])
-        S_out, (Xn, H_list) = F.run_branches([s_branch, x_branch], X.device, inputs=shared, name="xbranch")
+        (Xn, H_list), S_out = F.run_branches([x_branch, s_branch], X.device, inputs=shared, name="xbranch",
+                                             side_first=True)
         S_out = list(S_out)
         return Xn, S_out, H_list
 

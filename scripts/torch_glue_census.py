@@ -28,23 +28,28 @@ for _ in range(3):
 torch.cuda.synchronize()
 from torch.profiler import ProfilerActivity, profile  # noqa: E402
 
-with profile(activities=[ProfilerActivity.CPU], with_stack=True) as prof:
+with profile(activities=[ProfilerActivity.CPU], with_stack=True, record_shapes=True) as prof:
     st.eager()
     torch.cuda.synchronize()
 agg = collections.Counter()
+KEEP = ("aten::copy_", "aten::add_", "aten::fill_", "aten::cat", "aten::zero_", "aten::mul", "aten::sum",
+        "aten::linalg_vecdot", "aten::add", "aten::clone", "aten::_to_copy", "aten::ones_like", "aten::stack")
 for ev in prof.events():
-    name = ev.name
-    if not name.startswith("aten::") or name in ("aten::empty", "aten::empty_strided", "aten::view", "aten::as_strided",
-                                                  "aten::reshape", "aten::slice", "aten::select", "aten::t",
-                                                  "aten::transpose", "aten::permute", "aten::expand", "aten::detach",
-                                                  "aten::unsqueeze", "aten::squeeze", "aten::alias", "aten::lift_fresh",
-                                                  "aten::_reshape_alias", "aten::resize_", "aten::set_",
-                                                  "aten::result_type", "aten::is_nonzero", "aten::item",
-                                                  "aten::_local_scalar_dense", "aten::empty_like", "aten::split",
-                                                  "aten::narrow", "aten::unbind", "aten::chunk", "aten::_unsafe_view"):
+    if ev.name not in KEEP:
         continue
-    frames = [f for f in (ev.stack or []) if "paper_2602_10016_b200" in f]
-    site = frames[0].split("paper_2602_10016_b200/")[-1] if frames else "(autograd engine)"
-    agg[(name, site)] += 1
-for (name, site), c in agg.most_common(60):
-    print(f"{c:4d}  {name:28s} {site}")
+    # skip nested (e.g. copy_ inside clone): keep only events without a KEEP parent
+    par = ev.cpu_parent
+    nested = False
+    while par is not None:
+        if par.name in KEEP:
+            nested = True
+            break
+        par = par.cpu_parent
+    if nested:
+        continue
+    shapes = str(ev.input_shapes)[:90]
+    stack = [f for f in (ev.stack or []) if "paper_2602_10016_b200" in f or "/tests/" in f]
+    site = stack[0].split("/")[-1] if stack else ""
+    agg[(ev.name, shapes, site)] += 1
+for (name, shapes, site), c in agg.most_common(45):
+    print(f"{c:4d}  {name:22s} {shapes:92s} {site}")
