@@ -323,9 +323,13 @@ int kl_act_bwd(int rows, int cols, int dtype, const void* g, long long ldg, cons
 /* Fused Adam step over a flat fp32 parameter buffer (bias-corrected; the
  * SPEC.md trainer default), optionally refreshing a bf16 mirror in place.
  * With step_dev != NULL the step count lives on the device: it is incremented
- * first and read by the kernel (CUDA-graph replayable). */
+ * first and read by the kernel (CUDA-graph replayable); step == -1 with
+ * step_dev reads it without incrementing (one step's Adam split over several
+ * parameter ranges, kl_adam_tick issued once before them). */
 int kl_adam_step(long long n, float lr, float beta1, float beta2, float eps, int step, int* step_dev, float* w,
                  const float* g, float* m, float* v, void* w_bf16, void* stream);
+/* *step_dev += 1 (the device step count of a split Adam step). */
+int kl_adam_tick(int* step_dev, void* stream);
 
 /* Non-finite scan: atomically ORs 1 into *flag if any element of x is NaN/Inf
  * (NumericsError, tensor.py:21-27). */

@@ -141,6 +141,7 @@ _SIGS = {
                     C.c_void_p, C.c_void_p], C.c_int),
     "kl_act_bwd": ([C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_longlong, C.c_void_p, C.c_longlong, C.c_void_p,
                     C.c_longlong, C.c_int, C.c_int, C.c_void_p, C.c_void_p], C.c_int),
+    "kl_adam_tick": ([C.c_void_p, C.c_void_p], C.c_int),
     "kl_adam_step": ([C.c_longlong, C.c_float, C.c_float, C.c_float, C.c_float, C.c_int] + [C.c_void_p] * 7,
                      C.c_int),
     "kl_check_finite": ([C.c_longlong, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),

@@ -840,16 +840,24 @@ extern "C" int kl_adam_step(long long n, float lr, float beta1, float beta2, flo
                             float* w, const float* g, float* m, float* v, void* w_bf16, void* stream) {
   if (n == 0) return KL_OK;
   if (!step_dev && step < 1) { set_error("kl_adam_step: step must be >= 1"); return KL_EBADSHAPE; }
+  if (step_dev && step != 0 && step != -1) { set_error("kl_adam_step: step must be 0 or -1 with step_dev"); return KL_EBADSHAPE; }
   if (((uintptr_t)w | (uintptr_t)g | (uintptr_t)m | (uintptr_t)v) & 15) {
     set_error("kl_adam_step: buffers must be 16-byte aligned");
     return KL_EBADSHAPE;
   }
   cudaStream_t s = (cudaStream_t)stream;
-  if (step_dev) launch_k(tick_kernel, 1, 1, 0, s, step_dev);
+  const bool tick = step_dev && step != -1;
+  if (tick) launch_k(tick_kernel, 1, 1, 0, s, step_dev);
   unsigned grid = (unsigned)std::min<long long>((n / 4 + 255) / 256 + 1, 148 * 8);
   launch_k(adam_kernel, grid, 256, 0, s, n, lr, beta1, beta2, eps, step, step_dev, w, g, m, v, (bf16*)w_bf16);
-  count_launch(step_dev ? 2 : 1);
+  count_launch(tick ? 2 : 1);
   return launch_check("adam_step");
+}
+
+extern "C" int kl_adam_tick(int* step_dev, void* stream) {
+  launch_k(tick_kernel, 1, 1, 0, (cudaStream_t)stream, step_dev);
+  count_launch();
+  return launch_check("adam_tick");
 }
 
 namespace kl {

@@ -36,6 +36,7 @@ class GradReducer:
         self.stream = torch.cuda.Stream() if self.P.gflat.is_cuda else None
         self.pending = []
         self._carry = None
+        self._done = set()
         model.layer_hook = self.on_layer_done
 
     def _layer_start(self, l: int) -> int:
@@ -63,6 +64,7 @@ class GradReducer:
                 buf.mul_(1.0 / self.world)
 
     def on_layer_done(self, l: int):
+        self._done.add(l)
         lo, hi = self.ranges[l]
         if self._carry is not None:
             hi = self._carry[1]
@@ -76,5 +78,11 @@ class GradReducer:
         if self._carry is not None:
             self._launch(*self._carry)
             self._carry = None
+        # layers whose boundary never fired (layer 0 when its inputs are data
+        # that need no gradient): their buckets go now
+        for l in range(len(self.ranges)):
+            if l not in self._done:
+                self._launch(*self.ranges[l])
+        self._done = set()
         if self.stream is not None:
             torch.cuda.current_stream().wait_stream(self.stream)

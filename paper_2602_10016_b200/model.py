@@ -163,6 +163,27 @@ class KunlunModel:
         self.layer_hook = None  # set by dist.GradReducer
 
     # ------------------------------------------------------------------
+    def late_grad_blocks(self):
+        """Block keys whose gradients are written after every layer's
+        backward: the query-fold inputs (seeds, gains, query/key projections,
+        CLS queries), folded once per step before layer 0 (query_rows)."""
+        keys = []
+        for l in range(self.cfg.L):
+            if self.flags[l].skip_hsp:
+                continue
+            for s in self.layers[l].summ:
+                keys += [s.hsp.seeds, s.hsp.gain, s.hsp.attn.wqkv]
+                if s.cls_queries:
+                    keys += [s.cls_queries, s.cls_attn.wqkv]
+        return keys
+
+    def layer_param_ranges(self):
+        """Flat [lo, hi) parameter range of each layer (the head rides with
+        the last layer)."""
+        starts = [self.P.block_range(self.P.block_of(f"L{l}/pool")[0])[0] for l in range(self.cfg.L)]
+        ends = starts[1:] + [self.P.gflat.numel()]
+        return list(zip(starts, ends))
+
     def query_rows(self):
         """{(layer, event): (HQ, d) fp32 query rows} of every layer that runs
         HSP, folded for all those layers at once per event

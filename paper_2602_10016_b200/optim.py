@@ -24,6 +24,36 @@ class FlatAdam:
         _capi.call("kl_adam_step", P.flat.numel(), self.lr, self.b1, self.b2, self.eps, 0, self.t.data_ptr(),
                    P.flat.data_ptr(), P.gflat.data_ptr(), self.m.data_ptr(), self.v.data_ptr(), wc, _capi._stream())
 
+    # one step split over parameter ranges: tick() once, then step_range()
+    # over disjoint ranges covering the buffer (same arithmetic as step())
+    def tick(self):
+        _capi.call("kl_adam_tick", self.t.data_ptr(), _capi._stream())
+
+    def step_range(self, lo: int, hi: int):
+        P = self.P
+        if hi <= lo:
+            return
+        e32, e16 = 4, 2
+        wc = P.flat_c.data_ptr() + lo * e16 if P.flat_c is not None else None
+        _capi.call("kl_adam_step", hi - lo, self.lr, self.b1, self.b2, self.eps, -1, self.t.data_ptr(),
+                   P.flat.data_ptr() + lo * e32, P.gflat.data_ptr() + lo * e32, self.m.data_ptr() + lo * e32,
+                   self.v.data_ptr() + lo * e32, wc, _capi._stream())
+
+
+def _subtract(rng, holes):
+    """[lo, hi) minus the sorted disjoint ``holes``."""
+    lo, hi = rng
+    out = []
+    for a, b in holes:
+        if b <= lo or a >= hi:
+            continue
+        if a > lo:
+            out.append((lo, a))
+        lo = max(lo, b)
+    if lo < hi:
+        out.append((lo, hi))
+    return out
+
 
 class TrainStep:
     """One training step (zero grads, forward, BCE, backward, DP all-reduce,
@@ -36,22 +66,67 @@ class TrainStep:
         self.X, self.S, self.lengths, self.labels = X, S, lengths, labels
         self.graph = None
         self.loss = None
+        # Adam split by layer (single process): a layer's parameters are
+        # updated on a side stream as soon as its backward is done, beside the
+        # earlier layers' backward; the query-fold inputs (gradients written
+        # after layer 0) and the rest go last.  Data-parallel runs keep one
+        # Adam after the all-reduce.
+        self.segments = self.late = None
+        if reducer is None and hasattr(model, "layer_param_ranges"):
+            P = model.P
+            holes = sorted(P.block_range(k) for k in model.late_grad_blocks())
+            self.segments = [_subtract(r, holes) for r in model.layer_param_ranges()]
+            covered = [seg for segs in self.segments for seg in segs]
+            self.late = _subtract((0, P.gflat.numel()), sorted(covered))
+
+    def _adam_layer(self, l):
+        from . import functional as F
+
+        self._fired.add(l)
+        dev = self.X.device
+        st = F.side_stream(dev, "adam")
+        st.wait_stream(torch.cuda.current_stream(dev))
+        for o in F.side_streams(dev):
+            if o is not st:
+                st.wait_stream(o)
+        with torch.cuda.stream(st):
+            for lo, hi in self.segments[l]:
+                self.opt.step_range(lo, hi)
 
     def eager(self):
         from . import functional as F
 
         m = self.model
+        split = F.BRANCH_STREAMS and self.segments is not None
         m.P.zero_grad()
-        loss, _ = m.loss(self.X, self.S, self.lengths, self.labels)
-        F.DW_STREAM = F.BRANCH_STREAMS  # weight-gradient GEMMs beside the dX chain
+        if split:
+            self.opt.tick()
+            self._fired = set()
+            m.layer_hook = self._adam_layer
         try:
+            loss, _ = m.loss(self.X, self.S, self.lengths, self.labels)
+            F.DW_STREAM = F.BRANCH_STREAMS  # weight-gradient GEMMs beside the dX chain
             loss.backward()
         finally:
             F.DW_STREAM = False
+            if split:
+                m.layer_hook = None
         F.dw_join(self.X.device)
         if self.reducer is not None:
             self.reducer.finish()
-        self.opt.step()
+        if split:
+            dev = self.X.device
+            torch.cuda.current_stream(dev).wait_stream(F.side_stream(dev, "adam"))
+            # layers whose boundary never fired (layer 0: its inputs are data
+            # that need no gradient) and the late ranges
+            for l in range(len(self.segments)):
+                if l not in self._fired:
+                    for lo, hi in self.segments[l]:
+                        self.opt.step_range(lo, hi)
+            for lo, hi in self.late:
+                self.opt.step_range(lo, hi)
+        else:
+            self.opt.step()
         return loss
 
     def capture(self, warmup: int = 3):

@@ -45,7 +45,7 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, min_bucket, q):
+def _worker(rank, world, port, min_bucket, q, skip0=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -62,18 +62,20 @@ def _worker(rank, world, port, min_bucket, q):
     g = torch.arange(m.P.gflat.numel(), dtype=torch.float32) * (rank + 1)
     m.P.gflat.copy_(g)
     for l in reversed(range(L)):  # backward order
+        if skip0 and l == 0:
+            continue  # layer 0's boundary never fires when its inputs need no gradient
         m.layer_hook(l)
     red.finish()
     q.put((rank, m.P.gflat.numpy().copy()))
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("min_bucket", [1, 64])
-def test_grad_average_world2(min_bucket):
+@pytest.mark.parametrize("min_bucket,skip0", [(1, False), (64, False), (1, True), (64, True)])
+def test_grad_average_world2(min_bucket, skip0):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, min_bucket, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, min_bucket, q, skip0)) for r in range(2)]
     for p in procs:
         p.start()
     out = dict(q.get(timeout=120) for _ in procs)
