@@ -1,7 +1,8 @@
 """Summarise an `ncu --metrics gpu__time_duration.sum --csv` launch list of
 `bench.py --eager --steps K --warmup W`: per-kernel share of ONE training
-step, the launches between the last two fused-Adam launches (Adam closes
-every step).  usage: python summarize_launches.py launches.csv"""
+step: the launches between the last two Adam step-count ticks (one per
+step; older captures without a tick kernel use the fused-Adam launch, which
+then closed every step).  usage: python summarize_launches.py launches.csv"""
 import collections
 import csv
 import sys
@@ -16,8 +17,10 @@ for r in data:
         vals.append((int(r[ii]), r[ki][:100], float(r[vi].replace(",", ""))))
     except (ValueError, IndexError):
         pass
-adam = [i for i, (_, k, _) in enumerate(vals) if "adam_kernel" in k]
-last = vals[adam[-2] + 1:adam[-1] + 1] if len(adam) >= 2 else vals[int(len(vals) * 0.75):]
+marks = [i for i, (_, k, _) in enumerate(vals) if "tick_kernel" in k]
+if len(marks) < 2:
+    marks = [i for i, (_, k, _) in enumerate(vals) if "adam_kernel" in k]
+last = vals[marks[-2]:marks[-1]] if len(marks) >= 2 else vals[int(len(vals) * 0.75):]
 tot, cnt = collections.defaultdict(float), collections.Counter()
 for _, k, v in last:
     tot[k] += v
