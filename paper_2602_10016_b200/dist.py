@@ -33,6 +33,15 @@ class GradReducer:
         # element ranges of each layer's parameters (+ the head with the last layer)
         bounds = [self._layer_start(l) for l in range(L)] + [self.P.gflat.numel()]
         self.ranges = [(bounds[l], bounds[l + 1]) for l in range(L)]
+        # blocks whose gradients are written after every layer's backward
+        # (the query-fold inputs, model.late_grad_blocks) are reduced in
+        # finish(), not with their layer's bucket
+        from .optim import _subtract
+
+        holes = sorted(self.P.block_range(k) for k in model.late_grad_blocks()) \
+            if hasattr(model, "late_grad_blocks") else []
+        self.segments = [_subtract(r, holes) for r in self.ranges]
+        self.late = holes
         self.stream = torch.cuda.Stream() if self.P.gflat.is_cuda else None
         self.pending = []
         self._carry = None
@@ -65,24 +74,25 @@ class GradReducer:
 
     def on_layer_done(self, l: int):
         self._done.add(l)
-        lo, hi = self.ranges[l]
-        if self._carry is not None:
-            hi = self._carry[1]
-            self._carry = None
-        if hi - lo < self.min_bucket and l > 0:
-            self._carry = (lo, hi)
+        segs = (self._carry or []) + self.segments[l]
+        self._carry = None
+        if sum(b - a for a, b in segs) < self.min_bucket and l > 0:
+            self._carry = segs
             return
-        self._launch(lo, hi)
+        for lo, hi in segs:
+            self._launch(lo, hi)
 
     def finish(self):
-        if self._carry is not None:
-            self._launch(*self._carry)
-            self._carry = None
+        segs = self._carry or []
+        self._carry = None
         # layers whose boundary never fired (layer 0 when its inputs are data
-        # that need no gradient): their buckets go now
+        # that need no gradient), then the late blocks
         for l in range(len(self.ranges)):
             if l not in self._done:
-                self._launch(*self.ranges[l])
+                segs += self.segments[l]
+        segs += self.late
+        for lo, hi in segs:
+            self._launch(lo, hi)
         self._done = set()
         if self.stream is not None:
             torch.cuda.current_stream().wait_stream(self.stream)

@@ -132,6 +132,7 @@ def side_stream(device, name="side"):
 # the stream before the optimizer.  Off by default: a bare loss.backward()
 # leaves every kernel on the caller's streams.
 DW_STREAM = False
+DW_STREAM_FWD = False  # set by TrainStep around its forward (query folds on the summary-branch stream)
 
 
 class _DwFork:
@@ -161,9 +162,15 @@ class _DwFork:
 
 
 def dw_join(device):
-    """Current stream waits for the weight-gradient stream (see DW_STREAM)."""
+    """Current stream waits for every side stream (weight gradients, branch
+    work whose results autograd does not see, e.g. in-place parameter
+    gradients written on a branch stream)."""
     if torch.cuda.is_available():
-        torch.cuda.current_stream(device).wait_stream(side_stream(device, "dw"))
+        cur = torch.cuda.current_stream(device)
+        side_stream(device, "dw")
+        for st in side_streams(device):
+            if st != cur:
+                cur.wait_stream(st)
 
 
 def run_branches(fns, device, inputs=(), name="side", side_first=False):

@@ -269,7 +269,19 @@ class KunlunModel:
         live = self.seq_live() if prune_dead else [True] * self.cfg.L
         H = None
         outs = []
-        qrows = self.query_rows() if FOLD_ALL_LAYERS else None
+        qrows = None
+        if FOLD_ALL_LAYERS:
+            # the query folds (small fp32 products) only feed the summary
+            # branches: in a training step (which joins every side stream
+            # before the optimizer) issue them on that branch's stream, beside
+            # layer 0's sequence branch (their backward then overlaps it too)
+            if F.DW_STREAM_FWD and X.is_cuda:
+                side = F.side_stream(X.device, "xbranch")
+                side.wait_stream(torch.cuda.current_stream(X.device))
+                with torch.cuda.stream(side):
+                    qrows = self.query_rows()
+            else:
+                qrows = self.query_rows()
         for l in range(self.cfg.L):
             X, S_list, H = self.layer_forward(l, self.flags[l], X, S_list, lengths, H, live_seq=live[l], qrows=qrows)
             if keep_outputs:

@@ -104,11 +104,13 @@ class TrainStep:
             self._fired = set()
             m.layer_hook = self._adam_layer
         try:
+            F.DW_STREAM_FWD = F.BRANCH_STREAMS
             loss, _ = m.loss(self.X, self.S, self.lengths, self.labels)
+            F.DW_STREAM_FWD = False
             F.DW_STREAM = F.BRANCH_STREAMS  # weight-gradient GEMMs beside the dX chain
             loss.backward()
         finally:
-            F.DW_STREAM = False
+            F.DW_STREAM = F.DW_STREAM_FWD = False
             if split:
                 m.layer_hook = None
         F.dw_join(self.X.device)

@@ -23,9 +23,10 @@ class _FakeModel:
     """Just enough of KunlunModel for the reducer: cfg.L, P (flat params with
     L{l}/pool blocks), layer_hook."""
 
-    def __init__(self, L, sizes):
+    def __init__(self, L, sizes, late=()):
         from paper_2602_10016_b200.tensor import Params
 
+        self._late = list(late)
         P = Params()
         for l in range(L):
             P.add(f"L{l}/pool", np.zeros((2, 3)))
@@ -36,6 +37,9 @@ class _FakeModel:
         self.cfg = _FakeCfg(L)
         self.layer_hook = None
 
+    def late_grad_blocks(self):
+        return self._late
+
 
 def _port():
     s = socket.socket()
@@ -45,14 +49,14 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, min_bucket, q, skip0=False):
+def _worker(rank, world, port, min_bucket, q, skip0=False, late=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2602_10016_b200.dist import GradReducer
 
     L = 4
-    m = _FakeModel(L, [7, 1, 300, 2])
+    m = _FakeModel(L, [7, 1, 300, 2], late=["L2/w"] if late else [])
     red = GradReducer(m, min_bucket=min_bucket)
     # ranges tile [start of L0, end of buffer) without gaps
     assert red.ranges[0][0] == m.P.block_range("L0/pool")[0]
@@ -65,17 +69,21 @@ def _worker(rank, world, port, min_bucket, q, skip0=False):
         if skip0 and l == 0:
             continue  # layer 0's boundary never fires when its inputs need no gradient
         m.layer_hook(l)
+    if late:  # a late contribution (like the query folds' backward) after every boundary
+        lo, hi = m.P.block_range("L2/w")
+        m.P.gflat[lo:hi] += 1000.0 * (rank + 1)
     red.finish()
     q.put((rank, m.P.gflat.numpy().copy()))
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("min_bucket,skip0", [(1, False), (64, False), (1, True), (64, True)])
-def test_grad_average_world2(min_bucket, skip0):
+@pytest.mark.parametrize("min_bucket,skip0,late", [(1, False, False), (64, False, False), (1, True, False),
+                                                    (64, True, True), (1, False, True)])
+def test_grad_average_world2(min_bucket, skip0, late):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, min_bucket, q, skip0)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, min_bucket, q, skip0, late)) for r in range(2)]
     for p in procs:
         p.start()
     out = dict(q.get(timeout=120) for _ in procs)
@@ -84,6 +92,12 @@ def test_grad_average_world2(min_bucket, skip0):
         assert p.exitcode == 0
     n = out[0].size
     expect = np.arange(n, dtype=np.float32) * 1.5  # mean of (1x, 2x)
+    if late:
+        from paper_2602_10016_b200.tensor import Params  # noqa: F401
+
+        m = _FakeModel(4, [7, 1, 300, 2])
+        lo, hi = m.P.block_range("L2/w")
+        expect[lo:hi] += 1500.0
     start = 0
     for r in (0, 1):
         np.testing.assert_allclose(out[r][start:], expect[start:], rtol=0, atol=0)
