@@ -52,6 +52,7 @@ struct TcParams {
   float* ws;    // split-K partials [split][out batch][M][N] (fp32) or NULL (atomics)
   int c_has1, c_has2;  // MODE 2: C tensor-map batch dims present
   int reduce_c;        // MODE 2: TMA reduce-add into C (fp32 accumulate / split-K)
+  int x_tma;           // MODE 3, aux_mode 1: pre-activation stored by TMA (tmX, C's layout)
 };
 
 constexpr int SLD = 66;  // epilogue staging row stride (floats): 64 columns + pad, 8-byte aligned
@@ -359,27 +360,30 @@ __device__ __forceinline__ void st8_row(bf16* p, const float* v, bool live) {
 }
 
 template <typename TC, bool FULL>
-__device__ __forceinline__ void epi_tma(const TcParams& p, const Epi& e, const CUtensorMap* tmC, uint32_t tbase,
-                                        uint8_t* stg, float* bsm, int mb, int nb, int zc2, int zc1, int lane_base,
-                                        int lim, const uint8_t* Rs, int& nbox, TC* X) {
+__device__ __forceinline__ void epi_tma(const TcParams& p, const Epi& e, const CUtensorMap* tmC,
+                                        const CUtensorMap* tmX, uint32_t tbase, uint8_t* stg, float* bsm, int mb,
+                                        int nb, int zc2, int zc1, int lane_base, int lim, const uint8_t* Rs,
+                                        int& nbox, TC* X) {
+  // aux_mode 1 with a tensor map: the pre-activation is staged in the warp's
+  // second box and TMA-stored beside C (one box pair in flight)
+  const bool xtma = FULL && e.aux_mode == 1 && p.x_tma;
   const int lane = threadIdx.x & 31;
   constexpr int SPB = 128 / (int)sizeof(TC) / 32;  // 32-column slabs per 128-byte box row: 2 bf16, 1 fp32
   const int row = lane_base + lane;
   const bool live = mb * BM + row < lim;
-  if (FULL && e.bias) {  // this tile's bias -> the warp's smem row (read back as broadcasts)
-    for (int c = lane; c < p.BN; c += 32) {
-      const int n = nb * p.BN + c;
-      bsm[c] = n < p.N ? __ldg(&e.bias[n]) : 0.f;
-    }
-    __syncwarp();
-  }
+  // (FULL: the caller staged this tile's bias in bsm before the accumulator wait)
   uint8_t* buf = stg;
 #pragma unroll 1
   for (int c = 0; c < p.BN; c += 32) {
     const int hb = (c >> 5) % SPB;
     if (hb == 0) {
-      buf = stg + (nbox & 1) * 4096;
-      if (lane == 0) tc::bulk_wait_read1();
+      buf = xtma ? stg : stg + (nbox & 1) * 4096;
+      if (lane == 0) {
+        if (xtma)
+          tc::bulk_wait_read0();
+        else
+          tc::bulk_wait_read1();
+      }
       __syncwarp();
     }
     float v[32];
@@ -415,7 +419,31 @@ __device__ __forceinline__ void epi_tma(const TcParams& p, const Epi& e, const C
           v[4 * q + 3] += b4.w;
         }
       }
-      if (e.aux_mode == 1 && xrow) {  // forward: keep the pre-activation for the backward
+      if (xtma) {  // forward: pre-activation -> the aux staging box (same swizzle as C)
+        uint8_t* xr = stg + 4096 + lane * 128;
+        if constexpr (sizeof(TC) == 2) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int chunk = hb * 4 + q;
+            uint4 u = make_uint4(0u, 0u, 0u, 0u);
+            if (live) {
+              u.x = tc::pack_bf16(v[8 * q], v[8 * q + 1]);
+              u.y = tc::pack_bf16(v[8 * q + 2], v[8 * q + 3]);
+              u.z = tc::pack_bf16(v[8 * q + 4], v[8 * q + 5]);
+              u.w = tc::pack_bf16(v[8 * q + 6], v[8 * q + 7]);
+            }
+            *reinterpret_cast<uint4*>(xr + ((chunk ^ (lane & 7)) << 4)) = u;
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const uint4 u = live ? make_uint4(__float_as_uint(v[4 * q]), __float_as_uint(v[4 * q + 1]),
+                                              __float_as_uint(v[4 * q + 2]), __float_as_uint(v[4 * q + 3]))
+                                 : make_uint4(0u, 0u, 0u, 0u);
+            *reinterpret_cast<uint4*>(xr + ((q ^ (lane & 7)) << 4)) = u;
+          }
+        }
+      } else if (e.aux_mode == 1 && xrow) {  // forward: keep the pre-activation for the backward
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           if (n0 + 8 * q + 8 <= p.N) {
@@ -476,12 +504,13 @@ __device__ __forceinline__ void epi_tma(const TcParams& p, const Epi& e, const C
           tc::tma_reduce_add_4d(tmC, buf, gc, gr, zc2, zc1);
         else
           tc::tma_store_4d(tmC, buf, gc, gr, zc2, zc1);
+        if (xtma) tc::tma_store_4d(tmX, stg + 4096, gc, gr, zc2, zc1);
         tc::bulk_commit();
       }
       ++nbox;
     }
   }
-  if (FULL && e.bias) __syncwarp();  // bsm reused by the next tile
+  if (FULL && e.bias) __syncwarp();  // bsm rewritten for the next tile
 }
 
 // MODE 0: plain store, 1: generic epilogue (lane = column pair), 2/3: TMA-store
@@ -489,7 +518,8 @@ __device__ __forceinline__ void epi_tma(const TcParams& p, const Epi& e, const C
 template <typename TC, int MODE>
 __global__ void __launch_bounds__(NTHREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const __grid_constant__ CUtensorMap tmR, const __grid_constant__ CUtensorMap tmC, TcParams p,
+                   const __grid_constant__ CUtensorMap tmR, const __grid_constant__ CUtensorMap tmC,
+                   const __grid_constant__ CUtensorMap tmX, TcParams p,
                    Epi e) {
   constexpr bool PLAIN = MODE == 0;
   extern __shared__ uint8_t smem_raw[];
@@ -514,6 +544,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     tc::prefetch_tmap(&tmB);
     if (p.r_boxes) tc::prefetch_tmap(&tmR);
     if (MODE >= 2) tc::prefetch_tmap(&tmC);
+    if (MODE == 3 && p.x_tma) tc::prefetch_tmap(&tmX);
     for (int s = 0; s < p.stages; ++s) {
       tc::mbar_init(&full[s], 1);
       tc::mbar_init(&empty[s], 1);
@@ -647,6 +678,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const int lim = e.row_limit ? e.row_limit[zo] : 0x7fffffff;
       const int m0 = mb * BM + lane_base;
       float* stg = stage_s + (warp - 2) * (32 * SLD);
+      float* bsm = reinterpret_cast<float*>(rempty + 2 + 2) + (warp - 2) * 256;
+      if (MODE == 3 && e.bias) {
+        // this tile's bias -> the warp's smem row, while the tile's MMAs run
+        // (read back as broadcasts by epi_tma)
+        for (int c = lane; c < p.BN; c += 32) {
+          const int n = nb * p.BN + c;
+          bsm[c] = n < p.N ? __ldg(&e.bias[n]) : 0.f;
+        }
+        __syncwarp();
+      }
       tc::mbar_wait(&tfull[acc], acc_phase);
       tc::fence_after();
       const uint32_t tbase = tmem + acc * p.acc_stride + ((uint32_t)lane_base << 16);
@@ -657,8 +698,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           tc::mbar_wait(&rfull[t & 1], (t >> 1) & 1);
           Rs = sR + (t & 1) * p.r_boxes * 16384;
         }
-        epi_tma<TC, MODE == 3>(p, e, &tmC, tbase, reinterpret_cast<uint8_t*>(stage_s) + (warp - 2) * 8192,
-                               reinterpret_cast<float*>(rempty + 2 + 2) + (warp - 2) * 256, mb, nb,
+        epi_tma<TC, MODE == 3>(p, e, &tmC, &tmX, tbase, reinterpret_cast<uint8_t*>(stage_s) + (warp - 2) * 8192,
+                               bsm, mb, nb,
                     p.c_has2 ? z2o : 0, p.c_has1 ? z1o : 0, lane_base, lim, Rs, nbox, X);
       } else
       for (int c0 = 0; c0 < p.BN; c0 += 64) {
@@ -952,6 +993,14 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
     p.c_has1 = h1;
     p.reduce_c = accum_only0 ? 1 : 0;
   }
+  CUtensorMap tx_map;
+  p.x_tma = 0;
+  if (mode2 && e.aux_mode == 1 && g.aux && ((uintptr_t)g.aux & 15) == 0) {
+    int h2 = 0, h1 = 0;
+    const long long s1c = g.red1 ? 0 : g.c_s1, s2c = g.red2 ? 0 : g.c_s2;
+    p.x_tma = make_map(&tx_map, g.aux, g.N, g.M, g.c_rs, g.red2 ? 1 : g.nb2, s2c, g.red1 ? 1 : g.nb1, s1c,
+                       128 / esz_c, 32, &h2, &h1, true, esz_c) && h2 == p.c_has2 && h1 == p.c_has1;
+  }
   p.r_boxes = use_r ? (bn + 63) / 64 : 0;
   const uint32_t rbytes = 2u * p.r_boxes * 16384;
   // dynamic smem budget: 227 KB minus the 33 KB static epilogue staging
@@ -1019,7 +1068,8 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
   }
   auto launch = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    launch_k(kern, grid, NTHREADS, smem, s, ta, tb, use_r ? tr : ta, mode2 ? tc_map : ta, p, e);
+    launch_k(kern, grid, NTHREADS, smem, s, ta, tb, use_r ? tr : ta, mode2 ? tc_map : ta, p.x_tma ? tx_map : ta, p,
+             e);
   };
   if (mode2 && !p.ws) {
     const bool full = e.bias || e.n_act || e.aux_mode;
