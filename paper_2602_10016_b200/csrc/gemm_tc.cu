@@ -1107,8 +1107,16 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(GemmDesc g, Epi e, c
     const int zo = (int)(i / MN);
     const long long mn = i % MN;
     const int m = (int)(mn / g.N), n = (int)(mn % g.N);
-    float acc = 0.f;
-    for (int s = 0; s < splits; ++s) acc += ws[(long long)s * total + i];
+    // independent partial sums: the split loads are issued back to back
+    // instead of one dependent L2 round trip per split
+    float a4[4] = {0.f, 0.f, 0.f, 0.f};
+    int s = 0;
+    for (; s + 4 <= splits; s += 4) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) a4[u] += ws[(long long)(s + u) * total + i];
+    }
+    for (; s < splits; ++s) a4[0] += ws[(long long)s * total + i];
+    const float acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
     const int z1o = g.red1 ? 0 : zo / nb2o, z2o = g.red2 ? 0 : zo % nb2o;
     TC* C = (TC*)g.C + (long long)z1o * (g.red1 ? 0 : g.c_s1) + (long long)z2o * (g.red2 ? 0 : g.c_s2);
     const TC* R = g.R ? (const TC*)g.R + (long long)z1o * (g.red1 ? 0 : g.r_s1) + (long long)z2o * (g.red2 ? 0 : g.r_s2)

@@ -53,5 +53,6 @@ for a, b, s, n in kern:
     others = sum(1 for a2, b2, s2, n2 in kern if s2 != s and a2 < b and b2 > a)
     if others == 0:
         alone[n[:70]] += b - a
-for n, v in alone.most_common(15):
+print(f"kernels {len(kern)}, span {(t1 - t0) / 1e3:.3f} ms, alone total {sum(alone.values()) / 1e3:.3f} ms")
+for n, v in alone.most_common(25):
     print(f"alone {v / 1e3:7.3f} ms  {n}")
