@@ -18,6 +18,12 @@ namespace {
 
 constexpr int BN = 64, BK = 32;
 
+template <typename TC>
+__device__ __noinline__ void epilogue_store_ool(const Epi& e, TC* C, const TC* R, TC* X, long long off, long long roff,
+                                                int m, int n, int lim, float acc) {
+  epilogue_store(e, C, R, X, off, roff, m, n, lim, acc);
+}
+
 // Output tile BM x 64, k-tiles of 32 double-buffered in smem: the global loads
 // of k-tile i+1 are in flight (registers) while k-tile i is multiplied, so a
 // small-M / long-K product is not one global-latency round trip per k-step.
@@ -126,6 +132,10 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmDesc g, Epi e, int s
                 : nullptr;
   const int lim = e.row_limit ? e.row_limit[zo] : 0x7fffffff;
   const int nout = gridDim.z / splits;
+  // the common epilogue (alpha, bias, beta*C) inline; activations / aux /
+  // residual / row limit through one out-of-line call per element (16
+  // inlined copies of the generic epilogue blew the instruction cache)
+  const bool simple = e.n_act == 0 && !e.aux_mode && !R && !e.row_limit;
 #pragma unroll
   for (int i = 0; i < TM; ++i) {
     const int m = m0 + ty * TM + i;
@@ -135,12 +145,18 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(GemmDesc g, Epi e, int s
       const int n = n0 + tx * 4 + j;
       if (n >= g.N) continue;
       const long long off = (long long)m * g.c_rs + (long long)n * g.c_cs;
-      if (splits > 1 && g.ws)
+      if (splits > 1 && g.ws) {
         g.ws[((long long)sp * nout + zo) * g.M * g.N + (long long)m * g.N + n] = acc[i][j];
-      else if (splits > 1)
+      } else if (splits > 1) {
         atomicAdd((float*)C + off, e.alpha * acc[i][j]);
-      else
-        epilogue_store(e, C, R, X, off, (long long)m * g.r_rs + (long long)n * g.r_cs, m, n, lim, acc[i][j]);
+      } else if (simple) {
+        float v = e.alpha * acc[i][j];
+        if (e.bias) v += e.bias[n];
+        if (e.beta != 0.f) v += e.beta * ldf(C + off);
+        stf(C + off, v);
+      } else {
+        epilogue_store_ool(e, C, R, X, off, (long long)m * g.r_rs + (long long)n * g.r_cs, m, n, lim, acc[i][j]);
+      }
     }
   }
 }
