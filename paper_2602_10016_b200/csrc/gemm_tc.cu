@@ -295,38 +295,39 @@ __device__ __forceinline__ float rcp_apx(float x) {
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// The TMA-store epilogue instantiates only the activations the model's
+// GEMM epilogues use (identity, relu, silu, tanh; host-checked, others take
+// the generic epilogue): every case is a 32-wide unrolled loop, and each extra
+// case grows the epilogue warps' code (instruction-cache pressure).
 __device__ __forceinline__ void act32(int code, float* v) {
-  switch (code) {
-    case KL_ACT_RELU:
+  if (code == KL_ACT_RELU) {
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
-      break;
-    case KL_ACT_SILU:
+    for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
+  } else if (code == KL_ACT_SILU) {
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = v[i] * rcp_apx(1.f + __expf(-v[i]));
-      break;
-    case KL_ACT_TANH:
+    for (int i = 0; i < 32; ++i) v[i] = v[i] * rcp_apx(1.f + __expf(-v[i]));
+  } else if (code == KL_ACT_TANH) {
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = tanh_apx(v[i]);
-      break;
-    case KL_ACT_SIGMOID:
+    for (int i = 0; i < 32; ++i) v[i] = tanh_apx(v[i]);
+  }
+}
+// v *= act'(a) for the same four codes (x = pre-activation), fp32 accurate
+__device__ __forceinline__ void dact32(int code, float* v, const float* a) {
+  if (code == KL_ACT_RELU) {
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = rcp_apx(1.f + __expf(-v[i]));
-      break;
-    case KL_ACT_EXP:
+    for (int i = 0; i < 32; ++i) v[i] = a[i] > 0.f ? v[i] : 0.f;
+  } else if (code == KL_ACT_SILU) {
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = __expf(v[i]);
-      break;
-    case KL_ACT_SQRT:
+    for (int i = 0; i < 32; ++i) {
+      const float sg = 1.f / (1.f + expf(-a[i]));
+      v[i] *= sg * (1.f + a[i] * (1.f - sg));
+    }
+  } else if (code == KL_ACT_TANH) {
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = sqrtf(v[i]);
-      break;
-    case KL_ACT_LOG:
-#pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = __logf(v[i]);
-      break;
-    default:
-      break;
+    for (int i = 0; i < 32; ++i) {
+      const float y = tanhf(a[i]);
+      v[i] *= 1.f - y * y;
+    }
   }
 }
 
@@ -404,9 +405,7 @@ __device__ __forceinline__ void epi_tma(const TcParams& p, const Epi& e, const C
           for (int i = 0; i < 8; ++i) a[8 * q + i] = n0 + 8 * q + i < p.N ? ldf(xrow + 8 * q + i) : 0.f;
         }
       }
-      const int code = epi_code(e, n0);
-#pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] *= act_deriv(code, a[i]);
+      dact32(epi_code(e, n0), v, a);
     }
     if (FULL) {
       if (e.bias) {
@@ -975,6 +974,10 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
                (!e.aux_mode || (g.aux && ((uintptr_t)g.aux & 15) == 0)) && bn % 32 == 0 &&
                (g.c_dtype == KL_BF16 ? e.beta == 0.f : (e.beta == 0.f && !g.R) || accum_only0) &&
                (!g.R || use_r) && (e.n_act <= 1 || (e.act_group > 0 && e.act_group % 32 == 0));
+  for (int i = 0; i < e.n_act && mode2; ++i) {
+    const int c = e.act_codes[i];
+    mode2 = c == KL_ACT_IDENTITY || c == KL_ACT_RELU || c == KL_ACT_SILU || c == KL_ACT_TANH;
+  }
   if (use_r) {
     int h2 = 0, h1 = 0;
     use_r = ((uintptr_t)g.R & 15) == 0 &&
