@@ -131,38 +131,6 @@ __device__ __forceinline__ void act_run(int code, const float* z, const float* g
         if (BWD) dy[i] = g[i] * s * (1.f - t * t);
       }
       break;
-    case KL_ACT_SIGMOID:
-#pragma unroll
-      for (int i = 0; i < N; ++i) {
-        const float sg = sigm_fast(z[i] * s);
-        y[i] = sg;
-        if (BWD) dy[i] = g[i] * s * sg * (1.f - sg);
-      }
-      break;
-    case KL_ACT_EXP:
-#pragma unroll
-      for (int i = 0; i < N; ++i) {
-        const float e = __expf(z[i] * s);
-        y[i] = e;
-        if (BWD) dy[i] = g[i] * s * e;
-      }
-      break;
-    case KL_ACT_SQRT:
-#pragma unroll
-      for (int i = 0; i < N; ++i) {
-        const float q = sqrtf(z[i] * s);
-        y[i] = q;
-        if (BWD) dy[i] = g[i] * s * 0.5f / q;
-      }
-      break;
-    case KL_ACT_LOG:
-#pragma unroll
-      for (int i = 0; i < N; ++i) {
-        const float x = z[i] * s;
-        y[i] = __logf(x);
-        if (BWD) dy[i] = g[i] * s / x;
-      }
-      break;
     default:
 #pragma unroll
       for (int i = 0; i < N; ++i) {
@@ -172,18 +140,16 @@ __device__ __forceinline__ void act_run(int code, const float* z, const float* g
   }
 }
 
-// This thread's 32 Z columns [c0, c0+32): per-head runs of 16 when every
-// 16-column group has one code (n_kv % 16 == 0), else per column.
+// This thread's 32 Z columns [c0, c0+32): two per-head runs of 16 (every
+// 16-column group shares one code: n_kv % 16 == 0, host-checked).  The fused
+// kernels take the reference's default activation cycle (identity, relu,
+// silu, tanh; gdpa.py:31); other tags run the GEMM composition.  Each extra
+// unrolled case grows the kernels' code (instruction-cache pressure).
 template <bool BWD>
-__device__ __forceinline__ void act_cols32(const unsigned char* code, int c0, bool uniform16, const float* z,
-                                           const float* g, float s, float* y, float* dy) {
-  if (uniform16) {
-    act_run<16, BWD>(code[c0], z, g, s, y, dy);
-    act_run<16, BWD>(code[c0 + 16], z + 16, g + 16, s, y + 16, dy + 16);
-  } else {
-#pragma unroll
-    for (int i = 0; i < 32; ++i) act_run<1, BWD>(code[c0 + i], z + i, g + i, s, y + i, dy + i);
-  }
+__device__ __forceinline__ void act_cols32(const unsigned char* code, int c0, bool, const float* z, const float* g,
+                                           float s, float* y, float* dy) {
+  act_run<16, BWD>(code[c0], z, g, s, y, dy);
+  act_run<16, BWD>(code[c0 + 16], z + 16, g + 16, s, y + 16, dy + 16);
 }
 
 // In-place: tile(r, c0..c0+31) = bf16(acc[0..31] + tile(r, c0..c0+31)).
@@ -720,8 +686,18 @@ static int gdpa_prepare(const kl_gdpa_args* a, const char* who, gdpa::P& p, void
     p.code[j] = (unsigned char)(a->n_act ? a->act_codes[h % a->n_act] : KL_ACT_IDENTITY);
   }
   p.uniform16 = 1;
-  for (int j = 0; j < gdpa::HK; ++j)
+  for (int j = 0; j < gdpa::HK; ++j) {
     if (p.code[j] != p.code[j & ~15]) p.uniform16 = 0;
+    const int c = p.code[j];
+    if (c != KL_ACT_IDENTITY && c != KL_ACT_RELU && c != KL_ACT_SILU && c != KL_ACT_TANH) {
+      set_error("%s: fused path takes identity/relu/silu/tanh heads (got code %d)", who, c);
+      return KL_EUNSUPPORTED;
+    }
+  }
+  if (!p.uniform16) {
+    set_error("%s: fused path needs n_kv %% 16 == 0 (got %d)", who, a->n_kv);
+    return KL_EUNSUPPORTED;
+  }
   p.o_rs = a->s_rs;
   p.o_bs = a->s_bs;
   p.trace = (unsigned long long*)a->trace;

@@ -386,7 +386,7 @@ class _GdpaCore(torch.autograd.Function):
         B, T, d = S.shape
         HK = Kt.shape[1]
         ctx.codes, ctx.n_kv, ctx.inv_tau, ctx.sink = codes, n_kv, inv_tau, sink
-        ctx.fused = _gdpa_fused_ok(S, HK)
+        ctx.fused = _gdpa_fused_ok(S, HK, codes, n_kv)
         if ctx.fused:
             S = S.contiguous()
             Kt, Vt = Kt.contiguous(), Vt.contiguous()
@@ -432,8 +432,14 @@ class _GdpaCore(torch.autograd.Function):
 GDPA_FUSED = True  # tests flip this to A/B the fused kernels against the GEMM composition
 
 
-def _gdpa_fused_ok(S, HK) -> bool:
+_FUSED_ACTS = tuple(ACTIVATIONS[a] for a in ("identity", "relu", "silu", "tanh"))
+
+
+def _gdpa_fused_ok(S, HK, codes=(), n_kv=16) -> bool:
+    """The fused kernels: bf16, 64 generated rows, d in {128, 256}, n_kv a
+    multiple of 16, the default activation cycle (kl_gdpa_fwd's contract)."""
     return (GDPA_FUSED and S.dtype == torch.bfloat16 and HK == 64 and S.shape[-1] in (128, 256)
+            and n_kv % 16 == 0 and all(c in _FUSED_ACTS for c in codes)
             and bool(_capi.lib().kl_tcgen05_available()))
 
 
