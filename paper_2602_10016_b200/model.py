@@ -221,29 +221,39 @@ class KunlunModel:
         # branch, HSP pooling + recent rows) accumulate into it
         sinks = [F.GradSink() for _ in cfg.events]
 
-        def x_branch():  # HSP summaries -> global interaction
-            H_list = []
-            for e in range(len(cfg.events)):
-                if flags.skip_hsp:
-                    H_list.append(H_prev[e])
-                else:
+        events = range(len(cfg.events))
+
+        def x_branch():  # HSP summaries (per event, parallel branches) -> global interaction
+            def hsp(e):
+                def run():
                     qr = qrows.get((l, e)) if qrows else None
-                    H_list.append(hsp_summarize(S_list[e], lp.summ[e], lengths[e], sink=sinks[e], q_rows=qr).rows())
+                    return hsp_summarize(S_list[e], lp.summ[e], lengths[e], sink=sinks[e], q_rows=qr).rows()
+                return run
+            if flags.skip_hsp:
+                H_list = list(H_prev)
+            else:
+                H_list = F.run_branches([hsp(e) for e in events], X.device, name="ev_x")
             return global_interaction(X, H_list, lp.gi), H_list
 
-        def s_branch():  # GDPA (weights generated from X) -> windowed self-attention
+        def s_branch():  # GDPA (weights generated from X) -> windowed self-attention, per event
             xsum = summarize_nonseq(X, F.PRef(self.P, lp.pool)) if (not flags.skip_pffn and live_seq) else None
-            S_out = []
-            for e, ev in enumerate(cfg.events):
-                s = S_list[e]
-                if live_seq and not flags.skip_pffn:
-                    k, v = generate_kv(xsum, lp.wg[e], cfg.gdpa_cfg(e))
-                    kt, vt = fold_kv(k, v, lp.wg[e])
-                    s = F.gdpa_core(s, kt, vt, lengths[e], cfg.gdpa_acts, cfg.n_kv, 1.0 / float(ev.T), sink=sinks[e])
-                if live_seq and not flags.skip_self_attention:
-                    s = mha_window(s, lp.mha[e], WindowSpec(ev.w, ev.causal), lengths[e])
-                S_out.append(s)
-            return S_out
+
+            def seq(e):
+                def run():
+                    ev = cfg.events[e]
+                    s = S_list[e]
+                    if live_seq and not flags.skip_pffn:
+                        k, v = generate_kv(xsum, lp.wg[e], cfg.gdpa_cfg(e))
+                        kt, vt = fold_kv(k, v, lp.wg[e])
+                        s = F.gdpa_core(s, kt, vt, lengths[e], cfg.gdpa_acts, cfg.n_kv, 1.0 / float(ev.T),
+                                        sink=sinks[e])
+                    if live_seq and not flags.skip_self_attention:
+                        s = mha_window(s, lp.mha[e], WindowSpec(ev.w, ev.causal), lengths[e])
+                    return s
+                return run
+            # events are independent sequences: parallel branches
+            return F.run_branches([seq(e) for e in events], X.device, inputs=[xsum] if xsum is not None else (),
+                                  name="ev_s")
 
         # the two branches only share their inputs: the sequence branch runs on
         # the current stream, the summary / interaction branch beside it
