@@ -53,6 +53,7 @@ struct TcParams {
   int c_has1, c_has2;  // MODE 2: C tensor-map batch dims present
   int reduce_c;        // MODE 2: TMA reduce-add into C (fp32 accumulate / split-K)
   int x_tma;           // MODE 3, aux_mode 1: pre-activation stored by TMA (tmX, C's layout)
+  int r_bufs;          // residual tile buffers (2; 1 for 256-wide tiles with a long reduction)
 };
 
 constexpr int SLD = 66;  // epilogue staging row stride (floats): 64 columns + pad, 8-byte aligned
@@ -529,7 +530,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   // epilogue staging: MODE 0/1 transpose (one 32 x 64 fp32 slab per warp);
   // MODE 2 two 4 KB swizzled TMA boxes per warp
   __shared__ __align__(1024) float stage_s[4 * 32 * SLD];
-  uint64_t* full = (uint64_t*)(sR + (p.r_boxes ? 2 * p.r_boxes * 16384 : 0));
+  uint64_t* full = (uint64_t*)(sR + (p.r_boxes ? p.r_bufs * p.r_boxes * 16384 : 0));
   uint64_t* empty = full + p.stages;
   uint64_t* tfull = empty + p.stages;
   uint64_t* tempty = tfull + 2;
@@ -584,15 +585,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const int nb = (tile / p.tiles_m) % p.tiles_n;
         const int zo = tile / (p.tiles_m * p.tiles_n);
         const int z1o = p.red1 ? 0 : zo / nb2o, z2o = p.red2 ? 0 : zo % nb2o;
-        if (p.r_boxes) {
-          // residual tile for this output tile, double-buffered against the epilogue
-          const int rb = t & 1;
-          tc::mbar_wait(&rempty[rb], ((t >> 1) & 1) ^ 1);
+        // residual tile for this output tile: double-buffered against the
+        // epilogue and issued before the tile's operand loads; single-buffered
+        // (r_bufs == 1) it is issued after them, so waiting for the previous
+        // tile's epilogue never holds back this tile's mainloop
+        auto load_r = [&]() {
+          const int rb = t % p.r_bufs;
+          tc::mbar_wait(&rempty[rb], ((t / p.r_bufs) & 1) ^ 1);
           tc::mbar_arrive_expect_tx(&rfull[rb], p.r_boxes * 16384);
           for (int j = 0; j < p.r_boxes; ++j)
             tc::tma_load_4d(sR + (rb * p.r_boxes + j) * 16384, &tmR, &rfull[rb], nb * p.BN + j * 64, mb * BM,
                             p.r_has2 ? z2o : 0, p.r_has1 ? z1o : 0);
-        }
+        };
+        if (p.r_boxes && p.r_bufs == 2) load_r();
         for (int it = it0; it < it1; ++it) {
           const int r = it / p.kblocks, kb = it % p.kblocks;
           const int z1 = p.red1 ? r / r2n : z1o;
@@ -622,6 +627,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
           }
         }
+        if (p.r_boxes && p.r_bufs == 1) load_r();
       }
     }
   } else if (warp == 1) {
@@ -694,8 +700,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       if constexpr (MODE >= 2) {
         const uint8_t* Rs = nullptr;
         if (p.r_boxes) {
-          tc::mbar_wait(&rfull[t & 1], (t >> 1) & 1);
-          Rs = sR + (t & 1) * p.r_boxes * 16384;
+          tc::mbar_wait(&rfull[t % p.r_bufs], (t / p.r_bufs) & 1);
+          Rs = sR + (t % p.r_bufs) * p.r_boxes * 16384;
         }
         epi_tma<TC, MODE == 3>(p, e, &tmC, &tmX, tbase, reinterpret_cast<uint8_t*>(stage_s) + (warp - 2) * 8192,
                                bsm, mb, nb,
@@ -744,8 +750,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         } else {
           const bf16* Rs = nullptr;
           if (p.r_boxes) {
-            if (c0 == 0) tc::mbar_wait(&rfull[t & 1], (t >> 1) & 1);
-            Rs = reinterpret_cast<const bf16*>(sR + (t & 1) * p.r_boxes * 16384);
+            if (c0 == 0) tc::mbar_wait(&rfull[t % p.r_bufs], (t / p.r_bufs) & 1);
+            Rs = reinterpret_cast<const bf16*>(sR + (t % p.r_bufs) * p.r_boxes * 16384);
           }
           epi_generic(p, e, stg, C, R, X, m0, rows, n, ok0, ok1, lim, Rs, lane_base, cl);
         }
@@ -755,7 +761,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       __syncwarp();
       if (lane == 0) {
         tc::mbar_arrive(&tempty[acc]);
-        if (p.r_boxes) tc::mbar_arrive(&rempty[t & 1]);
+        if (p.r_boxes) tc::mbar_arrive(&rempty[t % p.r_bufs]);
       }
     }
     if (MODE >= 2 && lane == 0) tc::bulk_wait0();
@@ -877,7 +883,12 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
   // double-buffered residual fits next to the operand ring.
   CUtensorMap tr;
   bool use_r = g.R && g.c_dtype == KL_BF16 && g.r_cs == 1 && !g.red1 && !g.red2;
-  const int bn_max = use_r ? 128 : 256;
+  // residual tiles are double-buffered next to the operand ring with N tiles
+  // of <= 128; a long reduction (>= 8 k-blocks: the epilogue of one tile has
+  // a whole mainloop to finish before the next residual tile is needed) may
+  // take 256-wide tiles with a single residual buffer
+  const bool r_wide = use_r && (g.K + BK - 1) / BK >= 8;
+  const int bn_max = use_r && !r_wide ? 128 : 256;
   const int n_out0 = (g.red1 ? 1 : g.nb1) * (g.red2 ? 1 : g.nb2);
   const long long k_tot = (long long)((g.red1 ? g.nb1 : 1) * (g.red2 ? g.nb2 : 1)) * g.K;
   auto split_n = [&](int cap) {
@@ -1005,7 +1016,8 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
                        128 / esz_c, 32, &h2, &h1, true, esz_c) && h2 == p.c_has2 && h1 == p.c_has1;
   }
   p.r_boxes = use_r ? (bn + 63) / 64 : 0;
-  const uint32_t rbytes = 2u * p.r_boxes * 16384;
+  p.r_bufs = bn > 128 ? 1 : 2;
+  const uint32_t rbytes = (uint32_t)p.r_bufs * p.r_boxes * 16384;
   // dynamic smem budget: 227 KB minus the 33 KB static epilogue staging
   p.stages = std::min<int>(8, (int)((188 * 1024 - rbytes) / stage));
   if (p.stages < 2) return KL_EUNSUPPORTED;

@@ -193,3 +193,22 @@ def test_tc_tma_epilogue_aux(N, out_dtype):
     pz = pre.double()
     s = torch.sigmoid(pz)
     assert rel(d, (A.double() @ B.double()) * s * (1 + pz * (1 - s))) < tol
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("N", [256, 320])
+def test_tc_residual_long_k(N):
+    """Residual epilogue with a long reduction: 256-wide tiles with a single
+    TMA-staged residual buffer (issued after the tile's operand loads)."""
+    from paper_2602_10016_b200._capi import gemm
+
+    g = torch.Generator(device="cuda").manual_seed(N + 11)
+    A = operand((3, 333, 768), True, g)
+    B = operand((768, N), False, g)
+    R = torch.randn(3, 333, N, device="cuda", generator=g).to(torch.bfloat16)
+    out = gemm(A, B, residual=R)
+    ref = A.double() @ B.double() + R.double()
+    assert rel(out, ref) < 1e-2
+    C = R.clone()
+    gemm(A, B, C, beta=1.0)  # accumulate onto a bf16 output: the residual path with R = C
+    assert rel(C, ref) < 1e-2
