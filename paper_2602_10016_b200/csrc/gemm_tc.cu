@@ -835,6 +835,12 @@ static bool getenv_flag_epi1() {
   return v == 1;
 }
 
+static int r_wide_kb() {  // KL_GEMM_RWIDE_KB: min k-blocks for 256-wide residual tiles (A/B)
+  static int v = -1;
+  if (v < 0) v = getenv("KL_GEMM_RWIDE_KB") ? atoi(getenv("KL_GEMM_RWIDE_KB")) : 4;
+  return v;
+}
+
 int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
   if (g0.ab_dtype != KL_BF16) return KL_EUNSUPPORTED;
   if (!kl_tcgen05_available()) return KL_EUNSUPPORTED;
@@ -884,10 +890,11 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
   CUtensorMap tr;
   bool use_r = g.R && g.c_dtype == KL_BF16 && g.r_cs == 1 && !g.red1 && !g.red2;
   // residual tiles are double-buffered next to the operand ring with N tiles
-  // of <= 128; a long reduction (>= 8 k-blocks: the epilogue of one tile has
-  // a whole mainloop to finish before the next residual tile is needed) may
-  // take 256-wide tiles with a single residual buffer
-  const bool r_wide = use_r && (g.K + BK - 1) / BK >= 8;
+  // of <= 128; a reduction of >= 4 k-blocks (the epilogue of one tile has a
+  // mainloop to finish before the next residual tile is needed) may take
+  // 256-wide tiles with a single residual buffer (measured: out-projection
+  // 47 -> 40 us, QKV dX 105 -> 80 us at c2)
+  const bool r_wide = use_r && (g.K + BK - 1) / BK >= r_wide_kb();
   const int bn_max = use_r && !r_wide ? 128 : 256;
   const int n_out0 = (g.red1 ? 1 : g.nb1) * (g.red2 ? 1 : g.nb2);
   const long long k_tot = (long long)((g.red1 ? g.nb1 : 1) * (g.red2 ? g.nb2 : 1)) * g.K;
