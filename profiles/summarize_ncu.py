@@ -14,7 +14,7 @@ COLS = [
     ("DRAM MB", ("dram__bytes_read.sum", "dram__bytes_write.sum"), 1e-6),
     ("DRAM %", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", 1),
     ("tensor %", "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", 1),
-    ("tc-ops %", "sm__inst_executed_pipe_tc.avg.pct_of_peak_sustained_active", 1),
+    ("L2 hit %", "lts__t_sector_hit_rate.pct", 1),
     ("issue %", "sm__inst_issued.avg.pct_of_peak_sustained_active", 1),
     ("regs", "launch__registers_per_thread", 1),
 ]
