@@ -308,6 +308,13 @@ int kl_rowdot(int rows, int d, int dtype, const void* a, long long a_rs, const v
  * z, y, dz fp32 (n,). */
 int kl_bce_fwd_bwd(int n, const float* z, const float* y, float* loss, float* dz, void* stream);
 
+/* Normalized entropy (Eq. A1-A2; SPEC.md:553-561 normalized_entropy):
+ * kind 0: p holds probabilities (clipped to [1e-12, 1-1e-12]); kind 1: p holds logits.
+ * y labels in {0,1}; fp64 accumulation in one block.  out (device, 4 doubles) =
+ * {cross_entropy, background_entropy, ne, ctr}; ctr 0 or 1 -> ne = NaN (the
+ * host wrapper raises "degenerate background entropy"). */
+int kl_ne(int n, int kind, const float* p, const float* y, double* out, void* stream);
+
 /* dtype conversion copy (fp32 <-> bf16), n elements, contiguous. */
 int kl_cast(long long n, int dtype_in, const void* x, int dtype_out, void* y, void* stream);
 

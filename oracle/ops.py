@@ -131,6 +131,29 @@ def bce_with_logits(z: np.ndarray, y: np.ndarray):
     return loss, bwd
 
 
+def normalized_entropy(labels, preds, from_logits: bool = False) -> dict:
+    """NE = cross entropy / background entropy (PAPER.md:438-446 Eq. A1-A2;
+    SPEC.md:540-561 ``normalized_entropy`` / ``NeReport``), natural log, float64.
+    Probabilities are clipped to [1e-12, 1 - 1e-12]; logits use
+    the stable log-sigmoid.  All-zero / all-one labels raise."""
+    y = np.asarray(labels, dtype=np.float64).ravel()
+    p = np.asarray(preds, dtype=np.float64).ravel()
+    if y.size < 1 or y.size != p.size:
+        raise ValueError("normalized_entropy: need N >= 1 labels and predictions")
+    if from_logits:
+        lp = -np.log1p(np.exp(-np.abs(p))) + np.minimum(p, 0.0)
+        lq = -np.log1p(np.exp(-np.abs(p))) - np.maximum(p, 0.0)
+    else:
+        c = np.clip(p, 1e-12, 1.0 - 1e-12)
+        lp, lq = np.log(c), np.log1p(-c)
+    ce = float(-(y * lp + (1.0 - y) * lq).mean())
+    ctr = float(y.mean())
+    if not 0.0 < ctr < 1.0:
+        raise ValueError("degenerate background entropy")
+    h = float(-ctr * np.log(ctr) - (1.0 - ctr) * np.log1p(-ctr))
+    return {"cross_entropy": ce, "background_entropy": h, "ne": ce / h, "ctr": ctr, "n": int(y.size)}
+
+
 def mlp_rows(x: np.ndarray, ws, bs, acts):
     """Rowwise (linear, bias, act) stack; "identity" skips the act (mlp.py:47-54)."""
     caches = []

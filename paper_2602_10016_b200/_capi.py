@@ -136,6 +136,7 @@ _SIGS = {
     "kl_gated_sum_fwd": ([C.c_int] * 3 + [C.c_void_p, C.c_longlong] + [C.c_void_p] * 5 + [C.c_longlong, C.c_void_p], C.c_int),
     "kl_gated_sum_bwd": ([C.c_int] * 3 + [C.c_void_p, C.c_longlong] + [C.c_void_p] * 10, C.c_int),
     "kl_bce_fwd_bwd": ([C.c_int] + [C.c_void_p] * 5, C.c_int),
+    "kl_ne": ([C.c_int, C.c_int] + [C.c_void_p] * 4, C.c_int),
     "kl_cast": ([C.c_longlong, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p], C.c_int),
     "kl_act_fwd": ([C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_longlong, C.c_void_p, C.c_longlong, C.c_int, C.c_int,
                     C.c_void_p, C.c_void_p], C.c_int),

@@ -491,6 +491,40 @@ __global__ void bce_kernel(int n, const float* z, const float* y, float* loss, f
   if (threadIdx.x == 0) loss[0] = acc * inv;
 }
 
+// Normalized entropy (PAPER.md:438-446 Eq. A1-A2): one block,
+// fp64 accumulation.  kind 0: p = probabilities clipped to [1e-12, 1 - 1e-12];
+// kind 1: p = logits, log(sigmoid) evaluated stably.  out = {cross_entropy,
+// background_entropy, ne, ctr}; a degenerate background (ctr 0 or 1) gives ne = NaN.
+__global__ void ne_kernel(int n, int kind, const float* p, const float* y, double* out) {
+  KL_PDL_ENTRY();
+  __shared__ double sh[32];
+  double ce = 0.0, ys = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double yi = y[i], pi = p[i];
+    double lp, lq;  // log(p), log(1 - p)
+    if (kind == 1) {
+      lp = -log1p(exp(-fabs(pi))) + fmin(pi, 0.0);
+      lq = -log1p(exp(-fabs(pi))) - fmax(pi, 0.0);
+    } else {
+      const double c = fmin(fmax(pi, 1e-12), 1.0 - 1e-12);
+      lp = log(c);
+      lq = log1p(-c);
+    }
+    ce -= yi * lp + (1.0 - yi) * lq;
+    ys += yi;
+  }
+  ce = block_sum_d(ce, sh);
+  ys = block_sum_d(ys, sh);
+  if (threadIdx.x == 0) {
+    const double inv = 1.0 / (double)max(n, 1), ctr = ys * inv;
+    const double h = (ctr > 0.0 && ctr < 1.0) ? -ctr * log(ctr) - (1.0 - ctr) * log1p(-ctr) : 0.0;
+    out[0] = ce * inv;
+    out[1] = h;
+    out[2] = h > 0.0 ? ce * inv / h : nan("");
+    out[3] = ctr;
+  }
+}
+
 template <typename TI, typename TO>
 __global__ void cast_kernel(long long n, const TI* x, TO* y) {
   KL_PDL_ENTRY();
@@ -719,6 +753,15 @@ extern "C" int kl_gated_sum_bwd(int rows, int d, int dtype, const void* g, long 
   launch_k(reduce_pairs_kernel, 1, 256, 0, s, nb, (const double*)scratch, dgd, dgt);
   count_launch(2);
   return launch_check("gated_sum_bwd");
+}
+
+extern "C" int kl_ne(int n, int kind, const float* p, const float* y, double* out, void* stream) {
+  if (n < 1 || (kind != 0 && kind != 1)) {
+    set_error("kl_ne: needs n >= 1 and kind 0 (probabilities) or 1 (logits)");
+    return KL_EBADSHAPE;
+  }
+  launch_k(ne_kernel, 1, 256, 0, (cudaStream_t)stream, n, kind, p, y, out);
+  return launch_check("ne");
 }
 
 extern "C" int kl_bce_fwd_bwd(int n, const float* z, const float* y, float* loss, float* dz, void* stream) {

@@ -15,6 +15,9 @@ only, 1 MAC = 2 FLOPs, training = 3 x forward.  Two ledgers:
 
 from __future__ import annotations
 
+import ctypes as C
+from dataclasses import dataclass
+
 import numpy as np
 
 from .attention import band_support_sizes
@@ -89,3 +92,40 @@ def mfu(flops_per_sample: float, samples_per_s: float, peak_tflops: float) -> fl
     """MFU = achieved FLOP/s / peak: 1e9 FLOPs x 100/s on a
     1e12 peak -> 0.1."""
     return flops_per_sample * samples_per_s / (peak_tflops * 1e12)
+
+
+@dataclass(frozen=True)
+class NeReport:
+    """SPEC.md:540-543: ne = cross_entropy / background_entropy (nats/sample)."""
+    cross_entropy: float
+    background_entropy: float
+    ne: float
+    ctr: float
+    n: int
+
+
+def normalized_entropy(labels, preds, from_logits: bool = False) -> NeReport:
+    """Normalized entropy on the GPU (``kl_ne``; PAPER.md:438-446 Eq. A1-A2,
+    SPEC.md:553-561 ``normalized_entropy``).  ``labels`` / ``preds`` are CUDA
+    tensors of N values; ``preds`` are probabilities (clipped to
+    [1e-12, 1 - 1e-12]) or, with ``from_logits``, the model's logits.  fp64
+    accumulation in one block; the 4-double report is read back (one sync).
+    Raises ``ValueError("degenerate background entropy")`` for all-zero /
+    all-one labels, as the SPEC's error contract."""
+    import torch
+
+    from . import _capi
+
+    y = labels.detach().reshape(-1).float().contiguous()
+    p = preds.detach().reshape(-1).float().contiguous()
+    if not (y.is_cuda and p.is_cuda):
+        raise ValueError("normalized_entropy: labels and preds must be CUDA tensors (no CPU path)")
+    if y.numel() < 1 or y.numel() != p.numel():
+        raise ValueError("normalized_entropy: need N >= 1 labels and predictions")
+    out = torch.empty(4, device=y.device, dtype=torch.float64)
+    _capi.call("kl_ne", y.numel(), 1 if from_logits else 0, C.c_void_p(p.data_ptr()), C.c_void_p(y.data_ptr()),
+               C.c_void_p(out.data_ptr()), _capi._stream())
+    ce, h, ne, ctr = out.tolist()
+    if not h > 0.0:
+        raise ValueError("degenerate background entropy")
+    return NeReport(ce, h, ne, ctr, int(y.numel()))

@@ -413,3 +413,36 @@ def test_model_vs_oracle(dtype, compskip):
     for e in range(2):
         assert rel(S_t[e].grad, ref["dS"][e]) < tol
     check_grads(model.P.grad, ref["grads"], dtype)
+
+
+@pytest.mark.parametrize("n", [2, 4, 257, 4096, 100_000])
+@pytest.mark.parametrize("from_logits", [False, True])
+def test_normalized_entropy(n, from_logits):
+    """kl_ne vs the oracle, fp64 accumulation."""
+    from oracle import ops
+    from paper_2602_10016_b200.metrics import normalized_entropy
+
+    rng = np.random.default_rng(n)
+    z = (rng.normal(size=n) * 3).astype(np.float32)
+    y = (rng.random(n) < 0.3).astype(np.float32)
+    y[0], y[1] = 1.0, 0.0  # non-degenerate
+    p = z if from_logits else (1 / (1 + np.exp(-z.astype(np.float64)))).astype(np.float32)
+    got = normalized_entropy(torch.tensor(y, device="cuda"), torch.tensor(p, device="cuda"), from_logits=from_logits)
+    ref = ops.normalized_entropy(y, p, from_logits=from_logits)
+    for k in ("cross_entropy", "background_entropy", "ne", "ctr"):
+        assert abs(getattr(got, k) - ref[k]) <= 1e-10 * max(1.0, abs(ref[k])), k
+    assert got.n == n
+
+
+def test_normalized_entropy_spec_examples_and_errors():
+    from paper_2602_10016_b200.metrics import normalized_entropy
+
+    def ne(y, p):
+        return normalized_entropy(torch.tensor(y, device="cuda", dtype=torch.float32),
+                                  torch.tensor(p, device="cuda", dtype=torch.float32)).ne
+
+    assert abs(ne([1, 0, 1, 0], [0.5] * 4) - 1.0) < 1e-12
+    assert ne([1, 0], [1 - 1e-12, 1e-12]) < 1e-10
+    assert abs(ne([1, 0, 0, 0], [0.7, 0.1, 0.1, 0.1]) - 0.2991) < 5e-5
+    with pytest.raises(ValueError, match="degenerate background entropy"):
+        ne([0, 0, 0], [0.2, 0.3, 0.4])

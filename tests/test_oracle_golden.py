@@ -142,3 +142,23 @@ def test_compskip_spec_examples():
     assert OM.compskip_config(3, enabled=False) == [(False, False, False)] * 3
     with pytest.raises(ValueError):
         OM.compskip_config(0)
+
+
+def test_normalized_entropy_spec_examples():
+    """SPEC.md:559-561 examples and the SPEC.md:557 error contract."""
+    from oracle import ops
+
+    eps = 1e-12
+    assert abs(ops.normalized_entropy([1, 0, 1, 0], [0.5] * 4)["ne"] - 1.0) < 1e-12
+    assert ops.normalized_entropy([1, 0], [1 - eps, eps])["ne"] < 1e-10
+    r = ops.normalized_entropy([1, 0, 0, 0], [0.7, 0.1, 0.1, 0.1])
+    assert abs(r["ne"] - 0.2991) < 5e-5 and r["ctr"] == 0.25 and r["n"] == 4
+    assert abs(r["ne"] - r["cross_entropy"] / r["background_entropy"]) < 1e-15
+    z = np.random.default_rng(0).normal(size=64) * 4
+    y = (np.arange(64) % 3 == 0).astype(np.float64)
+    a = ops.normalized_entropy(y, z, from_logits=True)["ne"]
+    b = ops.normalized_entropy(y, 1 / (1 + np.exp(-z)))["ne"]
+    assert abs(a - b) < 1e-12
+    for bad in ([0, 0, 0], [1, 1]):
+        with pytest.raises(ValueError, match="degenerate background entropy"):
+            ops.normalized_entropy(bad, [0.5] * len(bad))
