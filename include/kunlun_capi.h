@@ -308,6 +308,32 @@ int kl_rowdot(int rows, int d, int dtype, const void* a, long long a_rs, const v
  * z, y, dz fp32 (n,). */
 int kl_bce_fwd_bwd(int n, const float* z, const float* y, float* loss, float* dz, void* stream);
 
+/* ROTE, the rotary temporal encoding of behaviour sequences (preproc.py:155-199
+ * rote_sequence / rote / gaps_from_timestamps; tensor.py:508-532 rotate_pairs).
+ * Row t < lengths[b] of sample b: each (even, odd) column pair i rotates by
+ *   angle = t * pos_freqs[i] + log1p(max(gap_t, 0) / tau_scale) * temp_freqs[i]
+ * with gap_t = ts[t] - ts[t-1] (ts[0]: 0; gap_mode 0, "previous") or
+ * ts[len-1] - ts[t] (gap_mode 1, "latest"); timestamps NULL -> tau = 0.
+ * Angles in fp64, reduced mod 2 pi, sin/cos in fp32.  inverse = 1 rotates by
+ * the negative angles (the VJP).  Rows >= lengths[b] are copied unchanged.
+ * x, y: (B, T, d) with row / batch strides in elements, d even; y != x. */
+typedef struct kl_rote_args {
+  int B, T, d, dtype;        /* dtype KL_F32 / KL_BF16 (x and y) */
+  const void* x;
+  long long x_rs, x_bs;
+  void* y;
+  long long y_rs, y_bs;
+  const int* lengths;        /* (B,) or NULL (= T) */
+  const double* timestamps;  /* (B, T) rows of ts_bs doubles, or NULL */
+  long long ts_bs;
+  const double* pos_freqs;   /* (d/2,) */
+  const double* temp_freqs;  /* (d/2,) */
+  double tau_scale;
+  int gap_mode;              /* 0 previous, 1 latest */
+  int inverse;
+} kl_rote_args;
+int kl_rote(const kl_rote_args* a, void* stream);
+
 /* Normalized entropy (Eq. A1-A2; SPEC.md:553-561 normalized_entropy):
  * kind 0: p holds probabilities (clipped to [1e-12, 1-1e-12]); kind 1: p holds logits.
  * y labels in {0,1}; fp64 accumulation in one block.  out (device, 4 doubles) =

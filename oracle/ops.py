@@ -154,6 +154,47 @@ def normalized_entropy(labels, preds, from_logits: bool = False) -> dict:
     return {"cross_entropy": ce, "background_entropy": h, "ne": ce / h, "ctr": ctr, "n": int(y.size)}
 
 
+def rote_angles(t_len: int, timestamps, pos_freqs, temp_freqs, tau_scale: float, gap_mode: str) -> np.ndarray:
+    """(T, d/2) rotation angles of rote_sequence (preproc.py:187-199): row
+    position t times pos_freqs plus tau = log1p(max(gap, 0) / tau_scale) times
+    temp_freqs; gaps to the previous event or below the newest
+    (gaps_from_timestamps, preproc.py:175-184); no timestamps -> tau = 0."""
+    pos = np.arange(t_len, dtype=np.float64)
+    if timestamps is None or t_len == 0:
+        taus = np.zeros(t_len)
+    else:
+        ts = np.asarray(timestamps, dtype=np.float64)
+        gaps = np.concatenate([[0.0], np.diff(ts)]) if gap_mode == "previous" else ts[-1] - ts
+        taus = np.log1p(np.maximum(gaps, 0.0) / tau_scale)
+    return pos[:, None] * np.asarray(pos_freqs)[None, :] + taus[:, None] * np.asarray(temp_freqs)[None, :]
+
+
+def rotate_pairs(x: np.ndarray, ang: np.ndarray):
+    """Per-plane rotation of (even, odd) pairs (tensor.py:508-532); the VJP
+    rotates the cotangent by the negative angles."""
+    x = np.asarray(x, dtype=np.float64)
+    c, s = np.cos(ang), np.sin(ang)
+    y = np.empty_like(x)
+    y[..., 0::2] = x[..., 0::2] * c - x[..., 1::2] * s
+    y[..., 1::2] = x[..., 0::2] * s + x[..., 1::2] * c
+
+    def bwd(g):
+        g = np.asarray(g, dtype=np.float64)
+        gx = np.empty_like(g)
+        gx[..., 0::2] = g[..., 0::2] * c + g[..., 1::2] * s
+        gx[..., 1::2] = -g[..., 0::2] * s + g[..., 1::2] * c
+        return gx
+
+    return y, bwd
+
+
+def rote_sequence(x: np.ndarray, timestamps, pos_freqs, temp_freqs, tau_scale: float = 60.0,
+                  gap_mode: str = "previous"):
+    """ROTE on a (T, d) sequence (preproc.py:187-199)."""
+    x = np.asarray(x, dtype=np.float64)
+    return rotate_pairs(x, rote_angles(x.shape[0], timestamps, pos_freqs, temp_freqs, tau_scale, gap_mode))
+
+
 def mlp_rows(x: np.ndarray, ws, bs, acts):
     """Rowwise (linear, bias, act) stack; "identity" skips the act (mlp.py:47-54)."""
     caches = []

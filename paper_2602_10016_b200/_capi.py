@@ -81,6 +81,18 @@ class GdpaArgs(C.Structure):
     ]
 
 
+class RoteArgs(C.Structure):
+    """kl_rote_args (include/kunlun_capi.h)."""
+    _fields_ = [
+        ("B", C.c_int), ("T", C.c_int), ("d", C.c_int), ("dtype", C.c_int),
+        ("x", C.c_void_p), ("x_rs", C.c_longlong), ("x_bs", C.c_longlong),
+        ("y", C.c_void_p), ("y_rs", C.c_longlong), ("y_bs", C.c_longlong),
+        ("lengths", C.c_void_p), ("timestamps", C.c_void_p), ("ts_bs", C.c_longlong),
+        ("pos_freqs", C.c_void_p), ("temp_freqs", C.c_void_p),
+        ("tau_scale", C.c_double), ("gap_mode", C.c_int), ("inverse", C.c_int),
+    ]
+
+
 class HspArgs(C.Structure):
     _fields_ = [
         ("B", C.c_int), ("T", C.c_int), ("HQ", C.c_int), ("d", C.c_int), ("n1", C.c_int),
@@ -137,6 +149,7 @@ _SIGS = {
     "kl_gated_sum_bwd": ([C.c_int] * 3 + [C.c_void_p, C.c_longlong] + [C.c_void_p] * 10, C.c_int),
     "kl_bce_fwd_bwd": ([C.c_int] + [C.c_void_p] * 5, C.c_int),
     "kl_ne": ([C.c_int, C.c_int] + [C.c_void_p] * 4, C.c_int),
+    "kl_rote": ([C.c_void_p, C.c_void_p], C.c_int),
     "kl_cast": ([C.c_longlong, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p], C.c_int),
     "kl_act_fwd": ([C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_longlong, C.c_void_p, C.c_longlong, C.c_int, C.c_int,
                     C.c_void_p, C.c_void_p], C.c_int),

@@ -525,6 +525,45 @@ __global__ void ne_kernel(int n, int kind, const float* p, const float* y, doubl
   }
 }
 
+// ROTE (preproc.py:187-199; rotate_pairs tensor.py:508-532): thread = one
+// (sample, row, column pair), grid-stride; angles in fp64 reduced mod 2 pi.
+template <typename T>
+__global__ void rote_kernel(kl_rote_args a) {
+  KL_PDL_ENTRY();
+  const int half = a.d >> 1;
+  const long long total = (long long)a.B * a.T * half;
+  const T* x = (const T*)a.x;
+  T* y = (T*)a.y;
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(idx % half);
+    const long long bt = idx / half;
+    const int t = (int)(bt % a.T), b = (int)(bt / a.T);
+    const T* xp = x + (long long)b * a.x_bs + (long long)t * a.x_rs + 2 * i;
+    T* yp = y + (long long)b * a.y_bs + (long long)t * a.y_rs + 2 * i;
+    const float x0 = ldf(xp), x1 = ldf(xp + 1);
+    const int len = a.lengths ? a.lengths[b] : a.T;
+    if (t >= len) {
+      stf(yp, x0);
+      stf(yp + 1, x1);
+      continue;
+    }
+    double ang = (double)t * a.pos_freqs[i];
+    if (a.timestamps) {
+      const double* ts = a.timestamps + (long long)b * a.ts_bs;
+      const double gap = a.gap_mode == 0 ? (t > 0 ? ts[t] - ts[t - 1] : 0.0) : ts[len - 1] - ts[t];
+      ang += log1p(fmax(gap, 0.0) / a.tau_scale) * a.temp_freqs[i];
+    }
+    const double two_pi = 6.283185307179586476925286766559;
+    ang -= two_pi * rint(ang / two_pi);
+    float sn, cs;
+    sincosf((float)ang, &sn, &cs);
+    if (a.inverse) sn = -sn;
+    stf(yp, x0 * cs - x1 * sn);
+    stf(yp + 1, x0 * sn + x1 * cs);
+  }
+}
+
 template <typename TI, typename TO>
 __global__ void cast_kernel(long long n, const TI* x, TO* y) {
   KL_PDL_ENTRY();
@@ -753,6 +792,23 @@ extern "C" int kl_gated_sum_bwd(int rows, int d, int dtype, const void* g, long 
   launch_k(reduce_pairs_kernel, 1, 256, 0, s, nb, (const double*)scratch, dgd, dgt);
   count_launch(2);
   return launch_check("gated_sum_bwd");
+}
+
+extern "C" int kl_rote(const kl_rote_args* a, void* stream) {
+  if (!a || a->B < 0 || a->T < 0 || a->d < 2 || (a->d & 1) || (a->dtype != KL_F32 && a->dtype != KL_BF16) ||
+      !a->pos_freqs || !a->temp_freqs || !(a->tau_scale > 0.0) || (a->gap_mode != 0 && a->gap_mode != 1) ||
+      (a->x == a->y && (long long)a->B * a->T > 0)) {
+    set_error("kl_rote: bad args (d even >= 2, tau_scale > 0, gap_mode 0/1, y != x)");
+    return KL_EBADSHAPE;
+  }
+  const long long total = (long long)a->B * a->T * (a->d / 2);
+  if (total == 0) return 0;
+  const int grid = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
+  if (a->dtype == KL_BF16)
+    launch_k(rote_kernel<bf16>, grid, 256, 0, (cudaStream_t)stream, *a);
+  else
+    launch_k(rote_kernel<float>, grid, 256, 0, (cudaStream_t)stream, *a);
+  return launch_check("rote");
 }
 
 extern "C" int kl_ne(int n, int kind, const float* p, const float* y, double* out, void* stream) {

@@ -32,6 +32,7 @@ from kunlun import attention as A  # noqa: E402
 from kunlun import gdpa as G  # noqa: E402
 from kunlun import interaction as I  # noqa: E402
 from kunlun import mlp as M  # noqa: E402
+from kunlun import preproc as PP  # noqa: E402
 from kunlun import seqsum as Q  # noqa: E402
 from kunlun import tensor as T  # noqa: E402
 
@@ -312,6 +313,38 @@ def case_index():
     _save("index.npz", **arrays)
 
 
+def case_rote():
+    """ROTE (preproc.py:155-199, tensor.py:508-532): rote_sequence on (T, d)
+    rows with and without timestamps, both gap modes, default and custom
+    frequency schedules; output and input gradient under a random cotangent."""
+    rng = np.random.default_rng(20261019)
+    out = {}
+    cases = [("prev", 8, 7, "previous", True, None), ("latest", 8, 7, "latest", True, None),
+             ("nots", 6, 5, "previous", False, None), ("custom", 4, 9, "latest", True, 17.0),
+             ("empty", 4, 0, "previous", True, None)]
+    for tag, d, t_len, mode, with_ts, tau_scale in cases:
+        if tau_scale is None:
+            cfg = PP.RoteConfig.default(d, gap_mode=mode)
+        else:
+            cfg = PP.RoteConfig(rng.uniform(0.01, 2.0, d // 2), rng.uniform(0.01, 2.0, d // 2), tau_scale, mode)
+        params = T.Params()
+        s = params.add("in/S", rng.normal(0, 1, (t_len, d)))
+        ts = np.cumsum(rng.exponential(120.0, t_len)) if with_ts else None
+        r = rng.normal(0, 1, (t_len, d))
+        with T.Tape(params) as tape:
+            y = PP.rote_sequence(s, ts, cfg)
+            loss = _dot(y, r)
+        if t_len:
+            g = _backward(tape, loss)["in/S"].data
+        else:
+            g = np.zeros((0, d))
+        out.update({f"{tag}:S": s.data, f"{tag}:ts": np.zeros(0) if ts is None else ts, f"{tag}:has_ts": np.array(int(with_ts)),
+                    f"{tag}:pos": cfg.pos_freqs, f"{tag}:temp": cfg.temp_freqs, f"{tag}:tau_scale": np.array(cfg.tau_scale),
+                    f"{tag}:mode": np.array(0 if mode == "previous" else 1), f"{tag}:Y": y.data, f"{tag}:cot": r,
+                    f"{tag}:dS": g})
+    _save("rote.npz", **out)
+
+
 def main():
     rng = np.random.default_rng(20260218)
     case_gdpa(rng, ("silu", "relu", "identity", "tanh"), "default")
@@ -330,4 +363,8 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["rote"]:
+        case_rote()
+    else:
+        main()
+        case_rote()

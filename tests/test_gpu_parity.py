@@ -446,3 +446,63 @@ def test_normalized_entropy_spec_examples_and_errors():
     assert abs(ne([1, 0, 0, 0], [0.7, 0.1, 0.1, 0.1]) - 0.2991) < 5e-5
     with pytest.raises(ValueError, match="degenerate background entropy"):
         ne([0, 0, 0], [0.2, 0.3, 0.4])
+
+
+@pytest.mark.parametrize("tag", ["prev", "latest", "nots", "custom", "empty"])
+def test_rote_golden(tag):
+    """kl_rote (fp32) vs the reference's own rote_sequence outputs / input gradients (tests/golden/rote.npz)."""
+    import os
+
+    from paper_2602_10016_b200.preproc import RoteConfig, rote_sequence
+
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "rote.npz"))
+    cfg = RoteConfig(z[f"{tag}:pos"], z[f"{tag}:temp"], float(z[f"{tag}:tau_scale"]),
+                     "previous" if int(z[f"{tag}:mode"]) == 0 else "latest")
+    s = torch.tensor(z[f"{tag}:S"], device="cuda", dtype=torch.float32, requires_grad=True)
+    ts = z[f"{tag}:ts"] if int(z[f"{tag}:has_ts"]) else None
+    y = rote_sequence(s, ts, cfg)
+    assert tuple(y.shape) == z[f"{tag}:Y"].shape
+    if y.numel():
+        y.backward(torch.tensor(z[f"{tag}:cot"], device="cuda", dtype=torch.float32))
+        assert rel(y, z[f"{tag}:Y"]) <= TOL[torch.float32]
+        assert rel(s.grad, z[f"{tag}:dS"]) <= TOL[torch.float32]
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("mode", ["previous", "latest"])
+@pytest.mark.parametrize("B,T,d", [(5, 33, 16), (2, 4096, 512)])
+def test_rote_batched(dtype, mode, B, T, d):
+    """Padded batch with per-sample lengths and timestamps vs the oracle per sample; padded rows pass through."""
+    from oracle import ops
+    from paper_2602_10016_b200.preproc import RoteConfig, rote_sequence
+
+    rng = np.random.default_rng(B * T + d)
+    cfg = RoteConfig.default(d, tau_scale=45.0, gap_mode=mode)
+    x = rng.normal(size=(B, T, d))
+    ts = np.cumsum(rng.exponential(300.0, (B, T)), axis=1)
+    lens = np.array([T, 0, 1] + list(rng.integers(1, T + 1, B)))[:B].astype(np.int32)
+    xt = torch.tensor(x, device="cuda", dtype=dtype, requires_grad=True)
+    xq = xt.detach().double().cpu().numpy()  # the inputs the kernel sees (bf16-rounded)
+    y = rote_sequence(xt, ts, cfg, lengths=torch.tensor(lens, device="cuda"))
+    g = rng.normal(size=(B, T, d))
+    y.backward(torch.tensor(g, device="cuda", dtype=dtype))
+    gq = torch.tensor(g, dtype=dtype).double().numpy()
+    for b in range(B):
+        n = int(lens[b])
+        yo, bwd = ops.rote_sequence(xq[b, :n], ts[b, :n], cfg.pos_freqs, cfg.temp_freqs, cfg.tau_scale, mode)
+        if n:
+            assert rel(y[b, :n], yo) <= TOL[dtype]
+            assert rel(xt.grad[b, :n], bwd(gq[b, :n])) <= TOL[dtype]
+        assert torch.equal(y[b, n:], xt.detach()[b, n:])
+
+
+def test_rote_errors():
+    from paper_2602_10016_b200.preproc import RoteConfig, rote_sequence
+    from paper_2602_10016_b200.tensor import ShapeError
+
+    with pytest.raises(ShapeError):
+        rote_sequence(torch.zeros(4, 6, device="cuda"), None, RoteConfig.default(8))
+    with pytest.raises(ValueError):
+        RoteConfig.default(7)
+    with pytest.raises(ValueError):
+        RoteConfig(np.ones(2), np.ones(3))

@@ -162,3 +162,17 @@ def test_normalized_entropy_spec_examples():
     for bad in ([0, 0, 0], [1, 1]):
         with pytest.raises(ValueError, match="degenerate background entropy"):
             ops.normalized_entropy(bad, [0.5] * len(bad))
+
+
+@pytest.mark.parametrize("tag", ["prev", "latest", "nots", "custom", "empty"])
+def test_rote(tag):
+    """oracle.ops.rote_sequence vs the reference's rote_sequence (preproc.py:187-199)."""
+    from oracle import ops
+
+    z = np.load(os.path.join(G, "rote.npz"))
+    ts = z[f"{tag}:ts"] if int(z[f"{tag}:has_ts"]) else None
+    y, bwd = ops.rote_sequence(z[f"{tag}:S"], ts, z[f"{tag}:pos"], z[f"{tag}:temp"], float(z[f"{tag}:tau_scale"]),
+                               "previous" if int(z[f"{tag}:mode"]) == 0 else "latest")
+    assert y.shape == z[f"{tag}:Y"].shape
+    assert rel(y, z[f"{tag}:Y"]) < 1e-12
+    assert rel(bwd(z[f"{tag}:cot"]), z[f"{tag}:dS"]) < 1e-12
