@@ -526,7 +526,8 @@ __global__ void ne_kernel(int n, int kind, const float* p, const float* y, doubl
 }
 
 // ROTE (preproc.py:187-199; rotate_pairs tensor.py:508-532): thread = one
-// (sample, row, column pair), grid-stride; angles in fp64 reduced mod 2 pi.
+// (sample, row, column pair), grid-stride; angles in fp64, reduced to
+// [-1/2, 1/2] turns, then fp32 sincospi (no Payne-Hanek path, no fp64 divide).
 template <typename T>
 __global__ void rote_kernel(kl_rote_args a) {
   KL_PDL_ENTRY();
@@ -554,13 +555,93 @@ __global__ void rote_kernel(kl_rote_args a) {
       const double gap = a.gap_mode == 0 ? (t > 0 ? ts[t] - ts[t - 1] : 0.0) : ts[len - 1] - ts[t];
       ang += log1p(fmax(gap, 0.0) / a.tau_scale) * a.temp_freqs[i];
     }
-    const double two_pi = 6.283185307179586476925286766559;
-    ang -= two_pi * rint(ang / two_pi);
+    double u = ang * 0.15915494309189533577;  // turns
+    u -= rint(u);
     float sn, cs;
-    sincosf((float)ang, &sn, &cs);
+    sincospif((float)(2.0 * u), &sn, &cs);
     if (a.inverse) sn = -sn;
     stf(yp, x0 * cs - x1 * sn);
     stf(yp + 1, x0 * sn + x1 * cs);
+  }
+}
+
+// Vector ROTE: thread = 4 consecutive column pairs (16 B of bf16, 32 B of
+// fp32) of one row, 32-bit indexing, one log1p per thread instead of one per
+// pair.  Per-pair angle math is the same as rote_kernel's (bit-equal outputs).
+// Needs d % 8 == 0, 8-element-aligned strides and 16 B-aligned bases.
+template <typename T>
+struct RoteVec;
+template <>
+struct RoteVec<bf16> {
+  static __device__ __forceinline__ void load(const bf16* p, float* v) {
+    const uint4 u = *reinterpret_cast<const uint4*>(p);
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 f = __bfloat1622float2(h[k]);
+      v[2 * k] = f.x;
+      v[2 * k + 1] = f.y;
+    }
+  }
+  static __device__ __forceinline__ void store(bf16* p, const float* v) {
+    uint4 u;
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) h[k] = __floats2bfloat162_rn(v[2 * k], v[2 * k + 1]);
+    *reinterpret_cast<uint4*>(p) = u;
+  }
+};
+template <>
+struct RoteVec<float> {
+  static __device__ __forceinline__ void load(const float* p, float* v) {
+    const float4 a = reinterpret_cast<const float4*>(p)[0], b = reinterpret_cast<const float4*>(p)[1];
+    v[0] = a.x, v[1] = a.y, v[2] = a.z, v[3] = a.w, v[4] = b.x, v[5] = b.y, v[6] = b.z, v[7] = b.w;
+  }
+  static __device__ __forceinline__ void store(float* p, const float* v) {
+    reinterpret_cast<float4*>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
+    reinterpret_cast<float4*>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
+  }
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) rote_vec_kernel(kl_rote_args a) {
+  KL_PDL_ENTRY();
+  const int cpr = a.d >> 3;  // 4-pair chunks per row
+  const unsigned total = (unsigned)a.B * (unsigned)a.T * (unsigned)cpr;
+  const T* x = (const T*)a.x;
+  T* y = (T*)a.y;
+  for (unsigned idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
+    const unsigned c = idx % (unsigned)cpr, bt = idx / (unsigned)cpr;
+    const int t = (int)(bt % (unsigned)a.T), b = (int)(bt / (unsigned)a.T);
+    const T* xp = x + (long long)b * a.x_bs + (long long)t * a.x_rs + 8 * c;
+    T* yp = y + (long long)b * a.y_bs + (long long)t * a.y_rs + 8 * c;
+    float v[8];
+    RoteVec<T>::load(xp, v);
+    const int len = a.lengths ? __ldg(a.lengths + b) : a.T;
+    if (t < len) {
+      double g = 0.0;
+      if (a.timestamps) {
+        const double* ts = a.timestamps + (long long)b * a.ts_bs;
+        const double gap = a.gap_mode == 0 ? (t > 0 ? __ldg(ts + t) - __ldg(ts + t - 1) : 0.0)
+                                           : __ldg(ts + len - 1) - __ldg(ts + t);
+        g = log1p(fmax(gap, 0.0) / a.tau_scale);
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int i = 4 * c + k;
+        double ang = (double)t * __ldg(a.pos_freqs + i);
+        if (a.timestamps) ang += g * __ldg(a.temp_freqs + i);
+        double u = ang * 0.15915494309189533577;  // turns
+        u -= rint(u);
+        float sn, cs;
+        sincospif((float)(2.0 * u), &sn, &cs);
+        if (a.inverse) sn = -sn;
+        const float x0 = v[2 * k], x1 = v[2 * k + 1];
+        v[2 * k] = x0 * cs - x1 * sn;
+        v[2 * k + 1] = x0 * sn + x1 * cs;
+      }
+    }
+    RoteVec<T>::store(yp, v);
   }
 }
 
@@ -803,6 +884,17 @@ extern "C" int kl_rote(const kl_rote_args* a, void* stream) {
   }
   const long long total = (long long)a->B * a->T * (a->d / 2);
   if (total == 0) return 0;
+  const auto al16 = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
+  const bool vec = a->d % 8 == 0 && a->x_rs % 8 == 0 && a->x_bs % 8 == 0 && a->y_rs % 8 == 0 &&
+                   a->y_bs % 8 == 0 && al16(a->x) && al16(a->y) && total / 4 < (1LL << 31);
+  if (vec) {
+    const int grid = (int)std::min<long long>((total / 4 + 255) / 256, 148LL * 64);
+    if (a->dtype == KL_BF16)
+      launch_k(rote_vec_kernel<bf16>, grid, 256, 0, (cudaStream_t)stream, *a);
+    else
+      launch_k(rote_vec_kernel<float>, grid, 256, 0, (cudaStream_t)stream, *a);
+    return launch_check("rote");
+  }
   const int grid = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
   if (a->dtype == KL_BF16)
     launch_k(rote_kernel<bf16>, grid, 256, 0, (cudaStream_t)stream, *a);
