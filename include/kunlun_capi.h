@@ -314,7 +314,8 @@ int kl_bce_fwd_bwd(int n, const float* z, const float* y, float* loss, float* dz
  *   angle = t * pos_freqs[i] + log1p(max(gap_t, 0) / tau_scale) * temp_freqs[i]
  * with gap_t = ts[t] - ts[t-1] (ts[0]: 0; gap_mode 0, "previous") or
  * ts[len-1] - ts[t] (gap_mode 1, "latest"); timestamps NULL -> tau = 0.
- * Angles in fp64, reduced mod 2 pi, sin/cos in fp32.  inverse = 1 rotates by
+ * Angles in fp64, reduced to [-1/2, 1/2] turns, sin/cos in fp32 (MUFU on the
+ * vector path: d % 8 == 0 with 16 B-aligned rows; |err| <= 2^-21).  inverse = 1 rotates by
  * the negative angles (the VJP).  Rows >= lengths[b] are copied unchanged.
  * x, y: (B, T, d) with row / batch strides in elements, d even; y != x. */
 typedef struct kl_rote_args {
