@@ -611,23 +611,28 @@ __global__ void __launch_bounds__(256, 4) rote_vec_kernel(kl_rote_args a) {
   const T* x = (const T*)a.x;
   T* y = (T*)a.y;
   const double inv_tau = 1.0 / a.tau_scale;
+  // The launcher makes the grid stride a multiple of cpr: each thread keeps one
+  // column chunk c (frequencies in registers) and walks rows (b, t) by a fixed
+  // step with no division in the loop.
+  const unsigned idx0 = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx0 >= total) return;
+  const unsigned c = idx0 % (unsigned)cpr, r0 = idx0 / (unsigned)cpr;
+  const unsigned rstep = gridDim.x * blockDim.x / (unsigned)cpr;
+  const int db = (int)(rstep / (unsigned)a.T), dt = (int)(rstep % (unsigned)a.T);
   double pf[4], tf[4];
-  unsigned cprev = ~0u;
-  for (unsigned idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
-    const unsigned c = idx % (unsigned)cpr, bt = idx / (unsigned)cpr;
-    const int t = (int)(bt % (unsigned)a.T), b = (int)(bt / (unsigned)a.T);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    pf[k] = __ldg(a.pos_freqs + 4 * c + k);
+    tf[k] = __ldg(a.temp_freqs + 4 * c + k);
+  }
+  int b = (int)(r0 / (unsigned)a.T), t = (int)(r0 % (unsigned)a.T);
+  for (; b < a.B; b += db, t += dt) {
+    if (t >= a.T) t -= a.T, ++b;
+    if (b >= a.B) break;
     const T* xp = x + (long long)b * a.x_bs + (long long)t * a.x_rs + 8 * c;
     T* yp = y + (long long)b * a.y_bs + (long long)t * a.y_rs + 8 * c;
     float v[8];
     RoteVec<T>::load(xp, v);
-    if (c != cprev) {  // the grid stride is a multiple of cpr: loaded once per thread
-      cprev = c;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        pf[k] = __ldg(a.pos_freqs + 4 * c + k);
-        tf[k] = __ldg(a.temp_freqs + 4 * c + k);
-      }
-    }
     const int len = a.lengths ? __ldg(a.lengths + b) : a.T;
     if (t < len) {
       double g = 0.0;
@@ -897,12 +902,15 @@ extern "C" int kl_rote(const kl_rote_args* a, void* stream) {
   const bool vec = a->d % 8 == 0 && a->x_rs % 8 == 0 && a->x_bs % 8 == 0 && a->y_rs % 8 == 0 &&
                    a->y_bs % 8 == 0 && al16(a->x) && al16(a->y) && total / 4 < (1LL << 31);
   if (vec) {
-    // grid * 256 a multiple of cpr (a power of two <= 256) keeps each thread on one column chunk
-    const int grid = (int)std::min<long long>((total / 4 + 255) / 256, 148LL * 8);
+    const long long cpr = a->d / 8;
+    // persistent: one wave of 4 blocks/SM; 148*4*256 = 2^11*74 threads divide
+    // any power-of-two cpr <= 2048, otherwise round the grid to a multiple of cpr
+    long long grid = std::min<long long>((total / 4 + 255) / 256, 148LL * 4);
+    if ((grid * 256) % cpr) grid = (grid + cpr - 1) / cpr * cpr;
     if (a->dtype == KL_BF16)
-      launch_k(rote_vec_kernel<bf16>, grid, 256, 0, (cudaStream_t)stream, *a);
+      launch_k(rote_vec_kernel<bf16>, (int)grid, 256, 0, (cudaStream_t)stream, *a);
     else
-      launch_k(rote_vec_kernel<float>, grid, 256, 0, (cudaStream_t)stream, *a);
+      launch_k(rote_vec_kernel<float>, (int)grid, 256, 0, (cudaStream_t)stream, *a);
     return launch_check("rote");
   }
   const int grid = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
