@@ -66,6 +66,27 @@ void kl_set_pdl(int on);
 /* Path the last kl_gemm call on this thread took: 1 tcgen05, 0 SIMT. */
 int kl_last_gemm_path(void);
 
+/* Kernel-path counters: how many launches each kernel family made since load
+ * (or the last kl_reset_path_hits).  Parity tests read them to assert which
+ * kernels a composed step actually ran (e.g. that the fused tcgen05 GDPA /
+ * HSP / SWA kernels, not a composition or SIMT fallback, were exercised). */
+#define KL_PATH_GEMM_TC 0       /* tcgen05 GEMM (kl_gemm, bf16)                */
+#define KL_PATH_GEMM_SIMT 1     /* FFMA GEMM (fp32 / unsupported bf16 shapes)  */
+#define KL_PATH_GDPA_FWD_TC 2   /* fused GDPA forward (kl_gdpa_fwd)            */
+#define KL_PATH_GDPA_BWD_TC 3   /* fused GDPA backward (kl_gdpa_bwd)           */
+#define KL_PATH_HSP_FWD_TC 4    /* fused HSP / PMA pooling forward             */
+#define KL_PATH_HSP_BWD_TC 5    /* fused HSP / PMA pooling backward            */
+#define KL_PATH_SWA_FWD_TC 6    /* banded flash attention forward, tcgen05     */
+#define KL_PATH_SWA_BWD_TC 7    /* banded flash attention backward, tcgen05    */
+#define KL_PATH_SWA_FWD_SIMT 8  /* banded attention forward, SIMT              */
+#define KL_PATH_SWA_BWD_SIMT 9  /* banded attention backward, SIMT             */
+#define KL_PATH_COLSOFTMAX 10   /* column softmax of the pooling composition   */
+#define KL_PATH_GDPA_FWD_TC512 11 /* fused GDPA forward, d = 512 variant       */
+#define KL_PATH_GDPA_BWD_TC512 12 /* fused GDPA backward, d = 512 variant      */
+#define KL_PATH_COUNT 16
+unsigned long long kl_path_hits(int path);
+void kl_reset_path_hits(void);
+
 /*
  * Strided, batched, optionally batch-reducing GEMM with a fused epilogue.
  * Replaces every matmul/matvec of the hot path and their VJPs
@@ -247,7 +268,9 @@ typedef struct kl_colsoftmax_args {
   void* dX_lo; /* optional: dX - round(dX) in dX's dtype (bf16 hi/lo split) */
   int dtype_dp; /* backward: dP's dtype (KL_F32 when zero-initialised) */
   /* backward, optional: precomputed Dcol (Bn, C) fp32 (= rowsum(dO * O) of the
-   * pooled output); NULL -> reduced over t here (two passes) */
+   * pooled output); NULL -> reduced over t here (two passes).
+   * backward, optional: X (fp32 scores, x_rs / x_bs) and LSE both set ->
+   * P = exp(X - LSE) is recomputed in fp32 instead of read from P. */
   const float* Dcol;
 } kl_colsoftmax_args;
 

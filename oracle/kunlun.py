@@ -82,12 +82,12 @@ def multi_head_attention(xq, xkv, p: dict, prefix: str, mask=None):
     if mask is None:
         mask = np.ones((n_q, n_k), dtype=bool)
     inv = 1.0 / np.sqrt(d_h)
-    q = np.einsum("nd,hcd->hnc", xq, Wq)
-    k = np.einsum("nd,hcd->hnc", xkv, Wk)
-    v = np.einsum("nd,hcd->hnc", xkv, Wv)
-    scores = np.einsum("hnc,hmc->hnm", q, k) * inv
+    q = xq @ Wq.transpose(0, 2, 1)  # (H, n, d_h); batched BLAS, same sums as the einsum
+    k = xkv @ Wk.transpose(0, 2, 1)
+    v = xkv @ Wv.transpose(0, 2, 1)
+    scores = (q @ k.transpose(0, 2, 1)) * inv
     attn, sm_bwd = masked_softmax(scores, mask[None])
-    o = np.einsum("hnm,hmc->hnc", attn, v)
+    o = attn @ v
     cat = o.transpose(1, 0, 2).reshape(n_q, H * d_h)
     out = cat @ Wo.T
 
@@ -96,20 +96,20 @@ def multi_head_attention(xq, xkv, p: dict, prefix: str, mask=None):
         grads[f"{prefix}/w_out"] = g.T @ cat
         dcat = g @ Wo
         do = dcat.reshape(n_q, H, d_h).transpose(1, 0, 2)
-        dattn = np.einsum("hnc,hmc->hnm", do, v)
-        dv = np.einsum("hnm,hnc->hmc", attn, do)
+        dattn = do @ v.transpose(0, 2, 1)
+        dv = attn.transpose(0, 2, 1) @ do
         dscores = sm_bwd(dattn) * inv
-        dq = np.einsum("hnm,hmc->hnc", dscores, k)
-        dk = np.einsum("hnm,hnc->hmc", dscores, q)
-        dWq = np.einsum("hnc,nd->hcd", dq, xq)
-        dWk = np.einsum("hmc,md->hcd", dk, xkv)
-        dWv = np.einsum("hmc,md->hcd", dv, xkv)
+        dq = dscores @ k
+        dk = dscores.transpose(0, 2, 1) @ q
+        dWq = dq.transpose(0, 2, 1) @ xq
+        dWk = dk.transpose(0, 2, 1) @ xkv
+        dWv = dv.transpose(0, 2, 1) @ xkv
         for h in range(H):
             grads[f"{prefix}/head{h}/w_q"] = dWq[h]
             grads[f"{prefix}/head{h}/w_k"] = dWk[h]
             grads[f"{prefix}/head{h}/w_v"] = dWv[h]
-        dxq = np.einsum("hnc,hcd->nd", dq, Wq)
-        dxkv = np.einsum("hmc,hcd->md", dk, Wk) + np.einsum("hmc,hcd->md", dv, Wv)
+        dxq = (dq @ Wq).sum(0)
+        dxkv = (dk @ Wk).sum(0) + (dv @ Wv).sum(0)
         return dxq, dxkv, grads
 
     return out, bwd

@@ -121,6 +121,8 @@ _SIGS = {
     "kl_set_gemm_path": ([C.c_int], None),
     "kl_set_pdl": ([C.c_int], None),
     "kl_last_gemm_path": ([], C.c_int),
+    "kl_path_hits": ([C.c_int], C.c_ulonglong),
+    "kl_reset_path_hits": ([], None),
     "kl_gemm": ([C.POINTER(GemmArgs), C.c_void_p], C.c_int),
     "kl_gdpa_fwd": ([C.POINTER(GdpaArgs), C.c_void_p], C.c_int),
     "kl_gdpa_bwd": ([C.POINTER(GdpaArgs), C.c_void_p], C.c_int),
@@ -410,3 +412,19 @@ def call(name: str, *args):
 
 def launch_count() -> int:
     return int(lib().kl_launch_count())
+
+
+# Kernel-path counters (include/kunlun_capi.h KL_PATH_*).
+PATHS = {"gemm_tc": 0, "gemm_simt": 1, "gdpa_fwd_tc": 2, "gdpa_bwd_tc": 3, "hsp_fwd_tc": 4, "hsp_bwd_tc": 5,
+         "swa_fwd_tc": 6, "swa_bwd_tc": 7, "swa_fwd_simt": 8, "swa_bwd_simt": 9, "colsoftmax": 10,
+         "gdpa_fwd_tc512": 11, "gdpa_bwd_tc512": 12}
+
+
+def path_hits() -> dict:
+    """{kernel family: launches since load / the last reset_path_hits()}."""
+    L = lib()
+    return {k: int(L.kl_path_hits(v)) for k, v in PATHS.items()}
+
+
+def reset_path_hits() -> None:
+    lib().kl_reset_path_hits()

@@ -38,6 +38,11 @@ int launch_check(const char* what) {
 
 void count_launch(unsigned n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+static std::atomic<unsigned long long> g_path_hits[KL_PATH_COUNT];
+void count_path(int path, unsigned n) {
+  if (path >= 0 && path < KL_PATH_COUNT) g_path_hits[path].fetch_add(n, std::memory_order_relaxed);
+}
+
 int gemm_path() { return g_gemm_path; }
 
 // Tensor-map encoding is a driver-API call that needs a current context.  The
@@ -86,6 +91,12 @@ extern "C" unsigned long long kl_launch_count(void) { return g_launches.load(); 
 extern "C" void kl_set_gemm_path(int path) { g_gemm_path = path; }
 extern "C" void kl_set_pdl(int on) { kl::g_pdl = on ? 1 : 0; }
 extern "C" int kl_last_gemm_path(void) { return kl::g_last_path; }
+extern "C" unsigned long long kl_path_hits(int path) {
+  return (path >= 0 && path < KL_PATH_COUNT) ? kl::g_path_hits[path].load() : 0ull;
+}
+extern "C" void kl_reset_path_hits(void) {
+  for (auto& h : kl::g_path_hits) h.store(0);
+}
 
 extern "C" int kl_tcgen05_available(void) {
   int dev = 0, major = 0, minor = 0;

@@ -18,6 +18,7 @@ typedef __nv_bfloat16 bf16;
 void set_error(const char* fmt, ...);
 int launch_check(const char* what);
 void count_launch(unsigned n = 1);
+void count_path(int path, unsigned n = 1);  // KL_PATH_* kernel-family counters
 bool pdl_enabled();
 void bind_device(cudaStream_t s);
 

@@ -725,6 +725,7 @@ static int gdpa_fwd_launch(const kl_gdpa_args* a, const gdpa::P& p, cudaStream_t
   q.out = (bf16*)a->Y;
   launch_k(gdpa::gdpa_fwd_kernel<D>, grid, gdpa::NT, smem, s, ts, tk, tv, ty, q);
   count_launch();
+  count_path(KL_PATH_GDPA_FWD_TC);
   return launch_check("gdpa_fwd_tc");
 }
 
@@ -749,6 +750,7 @@ static int gdpa_bwd_launch(const kl_gdpa_args* a, const gdpa::P& p, cudaStream_t
   q.out = (bf16*)a->dS;
   launch_k(gdpa::gdpa_bwd_kernel<D>, grid, gdpa::NT, smem, s, ts, tg, tk, tv, tds, q);
   count_launch();
+  count_path(KL_PATH_GDPA_BWD_TC);
   return launch_check("gdpa_bwd_tc");
 }
 

@@ -200,6 +200,7 @@ int launch(const GemmDesc& g, const Epi& e, cudaStream_t s) {
   else
     launch_k(gemm_simt_kernel<bf16, bf16, BM>, grid, 256, 0, s, gd, e, splits);
   count_launch();
+  count_path(KL_PATH_GEMM_SIMT);
   int rc = launch_check("gemm_simt");
   if (rc || !gd.ws) return rc;
   return splitk_reduce(g, e, gd.ws, splits, nout, s);

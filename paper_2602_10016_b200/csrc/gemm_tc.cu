@@ -1105,6 +1105,7 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
     else launch(gemm_tc_kernel<float, 1>);
   }
   count_launch();
+  count_path(KL_PATH_GEMM_TC);
   int rc = launch_check("gemm_tc");
   if (rc || !p.ws) return rc;
   return splitk_reduce(g, e, p.ws, p.splits, p.n_out, s);

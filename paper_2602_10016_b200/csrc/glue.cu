@@ -86,7 +86,9 @@ __global__ void __launch_bounds__(256) colsoftmax_fwd_kernel(kl_colsoftmax_args 
 }
 
 // dX = P * (dP - sum_t P dP)   (tensor.py:501-503); P in TP, dP in TG, dX in TO.
-template <typename TP, typename TG, typename TO>
+// RECOMP: P = exp(X - LSE[c]) recomputed in fp32 from the fp32 scores X and
+// the forward's log-sum-exp (no bf16 rounding of P in the score gradient).
+template <typename TP, typename TG, typename TO, bool RECOMP = false>
 __global__ void __launch_bounds__(256) colsoftmax_bwd_kernel(kl_colsoftmax_args a) {
   KL_PDL_ENTRY();
   __shared__ float red[8][33];
@@ -94,7 +96,10 @@ __global__ void __launch_bounds__(256) colsoftmax_bwd_kernel(kl_colsoftmax_args 
   const int cl = threadIdx.x & 31, rg = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + cl;
   const int len = a.lengths[b];
-  const TP* P = (const TP*)a.P + (long long)b * a.p_bs + c;
+  const TP* P = RECOMP ? (const TP*)a.X + (long long)b * a.x_bs + c : (const TP*)a.P + (long long)b * a.p_bs + c;
+  const long long p_rs = RECOMP ? a.x_rs : a.p_rs;
+  const float lse = (RECOMP && c < a.C && len > 0) ? a.LSE[(long long)b * a.C + c] : 0.f;
+  auto ldp = [&](long long t) { return RECOMP ? expf(ldf(P + t * p_rs) - lse) : ldf(P + t * p_rs); };
   const TG* G = (const TG*)a.dP + (long long)b * a.dp_bs + c;
   TO* D = (TO*)a.dX + (long long)b * a.dx_bs + c;
   TO* L = a.dX_lo ? (TO*)a.dX_lo + (long long)b * a.dx_bs + c : nullptr;
@@ -106,7 +111,7 @@ __global__ void __launch_bounds__(256) colsoftmax_bwd_kernel(kl_colsoftmax_args 
 #pragma unroll
       for (int u = 0; u < CS_U; ++u) {
         const int t = t0 + 8 * u;
-        if (t < len) acc[u] += ldf(P + (long long)t * a.p_rs) * ldf(G + (long long)t * a.dp_rs);
+        if (t < len) acc[u] += ldp(t) * ldf(G + (long long)t * a.dp_rs);
       }
     }
   float at = 0.f;
@@ -124,7 +129,7 @@ __global__ void __launch_bounds__(256) colsoftmax_bwd_kernel(kl_colsoftmax_args 
 #pragma unroll
     for (int u = 0; u < CS_U; ++u) {
       const int t = t0 + 8 * u;
-      pv[u] = t < len ? ldf(P + (long long)t * a.p_rs) : 0.f;
+      pv[u] = t < len ? ldp(t) : 0.f;
       gv[u] = t < len ? ldf(G + (long long)t * a.dp_rs) : 0.f;
     }
 #pragma unroll
@@ -721,6 +726,7 @@ extern "C" int kl_colsoftmax_fwd(const kl_colsoftmax_args* a, void* stream) {
   else if (a->dtype_out == KL_F32) launch_k(colsoftmax_fwd_kernel<bf16, float>, grid, 256, 0, s, *a);
   else launch_k(colsoftmax_fwd_kernel<bf16, bf16>, grid, 256, 0, s, *a);
   count_launch();
+  count_path(KL_PATH_COLSOFTMAX);
   return launch_check("colsoftmax_fwd");
 }
 
@@ -731,7 +737,11 @@ extern "C" int kl_colsoftmax_bwd(const kl_colsoftmax_args* a, void* stream) {
   dim3 grid((a->C + 31) / 32, a->Bn);
   // P in dtype_out, dP in dtype_dp, dX (and dX_lo) in dtype_in
   const int tp = a->dtype_out, tg = a->dtype_dp, to = a->dtype_in;
-  if (tp == KL_F32 && tg == KL_F32 && to == KL_F32) launch_k(colsoftmax_bwd_kernel<float, float, float>, grid, 256, 0, s, *a);
+  if (a->X && a->LSE) {  // P recomputed from fp32 scores + LSE
+    if (tg != KL_F32) { set_error("kl_colsoftmax_bwd: recompute mode needs fp32 dP"); return KL_EUNSUPPORTED; }
+    if (to == KL_F32) launch_k(colsoftmax_bwd_kernel<float, float, float, true>, grid, 256, 0, s, *a);
+    else launch_k(colsoftmax_bwd_kernel<float, float, bf16, true>, grid, 256, 0, s, *a);
+  } else if (tp == KL_F32 && tg == KL_F32 && to == KL_F32) launch_k(colsoftmax_bwd_kernel<float, float, float>, grid, 256, 0, s, *a);
   else if (tp == KL_F32 && tg == KL_F32) launch_k(colsoftmax_bwd_kernel<float, float, bf16>, grid, 256, 0, s, *a);
   else if (tp == KL_BF16 && tg == KL_F32 && to == KL_BF16) launch_k(colsoftmax_bwd_kernel<bf16, float, bf16>, grid, 256, 0, s, *a);
   else if (tp == KL_BF16 && tg == KL_F32) launch_k(colsoftmax_bwd_kernel<bf16, float, float>, grid, 256, 0, s, *a);

@@ -736,6 +736,7 @@ extern "C" int kl_hsp_fwd(const kl_hsp_args* a, void* stream) {
     launch_k(hsp::hsp_fwd_kernel<128>, grid, hsp::NT, smem, s, tS, tQ, p);
   }
   count_launch();
+  count_path(KL_PATH_HSP_FWD_TC);
   return launch_check("hsp_fwd");
 }
 
@@ -794,5 +795,6 @@ extern "C" int kl_hsp_bwd(const kl_hsp_args* a, void* stream) {
     launch_k(hsp::hsp_bwd_kernel<128>, grid, hsp::NT, smem, s, tS, tQ, tG, p);
   }
   count_launch();
+  count_path(KL_PATH_HSP_BWD_TC);
   return launch_check("hsp_bwd");
 }

@@ -301,6 +301,7 @@ int launch_fwd(const SwaP& p, cudaStream_t s) {
   dim3 grid((p.T + TQ - 1) / TQ, p.H, p.B);
   launch_k(swa_fwd_kernel<T, DH>, grid, 256, smem, s, p);
   count_launch();
+  count_path(KL_PATH_SWA_FWD_SIMT);
   return launch_check("swa_fwd_simt");
 }
 
@@ -316,6 +317,7 @@ int launch_bwd(const SwaP& p, cudaStream_t s) {
   cudaFuncSetAttribute(swa_bwd_dq_kernel<T, DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
   launch_k(swa_bwd_dq_kernel<T, DH>, grid, 256, smem2, s, p);
   count_launch(3);
+  count_path(KL_PATH_SWA_BWD_SIMT);
   return launch_check("swa_bwd_simt");
 }
 

@@ -2415,6 +2415,7 @@ int swa_fwd_tc(const SwaP& p, cudaStream_t s) {
     }
   }
   count_launch();
+  count_path(KL_PATH_SWA_FWD_TC);
   return launch_check("swa_fwd_tc");
 }
 
@@ -2452,6 +2453,7 @@ int swa_bwd_tc(const SwaP& p, cudaStream_t s) {
       launch_k(v2::swa_bwd_dq_tc2_kernel, grid, v2::NT2, s2, s, tq, tdo, p);
     }
     count_launch(2);
+    count_path(KL_PATH_SWA_BWD_TC);
     return launch_check("swa_bwd_tc2");
   }
   dim3 grid((p.T + TB - 1) / TB, p.H, p.B);
@@ -2462,6 +2464,7 @@ int swa_bwd_tc(const SwaP& p, cudaStream_t s) {
   cudaFuncSetAttribute(swa_bwd_dq_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
   launch_k(swa_bwd_dq_tc_kernel, grid, NT, smem2, s, tq, tdo, p);
   count_launch(2);
+  count_path(KL_PATH_SWA_BWD_TC);
   return launch_check("swa_bwd_tc");
 }
 

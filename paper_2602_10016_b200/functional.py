@@ -45,14 +45,24 @@ class PRef:
 
 class GradSink:
     """One gradient buffer shared by the consumers of a (B, T, d) sequence
-    tensor (HSP pooling, recent rows, the GDPA / attention branch).  The
-    first consumer whose backward runs registers its dS; consumers that can
-    accumulate in their own epilogue (HSP pooling, recent rows) add into it
-    and return no gradient, so autograd does not materialise and add one
-    (B, T, d) gradient per consumer.  The consumers may run on different
-    streams (parallel branches): ``take`` orders the accumulation after the
-    registering stream's write, ``release`` orders the registering stream's
-    later work (the autograd consumers of the buffer) after it."""
+    tensor inside a layer (HSP pooling + recent rows, the GDPA / attention
+    branch), delivered to autograd by ONE ``_SeqJoin`` node.
+
+    The layer applies ``seq_join(S, sink)`` once and hands its output to the
+    consumers.  The first consumer whose backward runs registers its dS
+    (``put``); later consumers accumulate into it — the fused HSP kernel in
+    its own epilogue (``take`` + accumulate_ds), others with one add — and
+    every participating consumer returns *no* gradient for S.  The join's
+    backward then returns the buffer: autograd never materialises one
+    (B, T, d) gradient per consumer and never adds them.  Consumers outside
+    the layer (a caller reading the layer output) see S itself, not the
+    join's output, so autograd sums their gradients with the join's buffer —
+    correct for any graph, not just the model's own.
+
+    The consumers may run on different streams (parallel branches): ``take``
+    orders the accumulation after the registering stream's write,
+    ``release`` orders the registering stream's later work after it, and the
+    join waits for the registering stream."""
 
     __slots__ = ("t", "stream")
 
@@ -80,6 +90,51 @@ class GradSink:
             cur = torch.cuda.current_stream(self.t.device)
             if cur != self.stream:
                 self.stream.wait_stream(cur)
+
+    def deliver(self, dS):
+        """A consumer's backward hands over its full dS: registered if it is
+        the first, else added into the registered buffer.  Returns the
+        gradient the consumer must return to autograd (always None)."""
+        if self.t is None:
+            self.put(dS)
+        else:
+            acc = self.take(dS)
+            if acc is None:
+                raise ShapeError("shared sequence gradient: shape / dtype mismatch")
+            acc.add_(dS)
+            self.release()
+        return None
+
+
+class _SeqJoin(torch.autograd.Function):
+    """Identity whose output feeds a layer's sequence consumers; its
+    backward returns the GradSink buffer they filled (plus, if some
+    consumer returned an ordinary gradient, that gradient)."""
+
+    @staticmethod
+    def forward(ctx, S, sink):
+        ctx.sink = sink
+        ctx.set_materialize_grads(False)
+        return S.view_as(S)
+
+    @staticmethod
+    def backward(ctx, g):
+        sink = ctx.sink
+        t = sink.t
+        sink.t = None
+        if t is None:
+            return g, None
+        if sink.stream is not None:
+            cur = torch.cuda.current_stream(t.device)
+            if cur != sink.stream:
+                cur.wait_stream(sink.stream)
+                t.record_stream(cur)
+        return (t if g is None else t + g), None
+
+
+def seq_join(S, sink):
+    """S for a layer's sequence consumers that share ``sink`` (GradSink)."""
+    return _SeqJoin.apply(S, sink)
 
 
 class ResidualStash:
@@ -414,8 +469,8 @@ class _GdpaCore(torch.autograd.Function):
             a = _gdpa_args(S, Kt, Vt, lengths, ctx.codes, ctx.n_kv, ctx.inv_tau)
             a.dY, a.dS, a.dKt, a.dVt = g.data_ptr(), dS.data_ptr(), dKt.data_ptr(), dVt.data_ptr()
             _capi.call("kl_gdpa_bwd", C.byref(a), _stream())
-            if ctx.sink is not None and ctx.sink.t is None:
-                ctx.sink.put(dS)
+            if ctx.sink is not None:
+                dS = ctx.sink.deliver(dS)
             return dS, dKt, dVt, None, None, None, None, None
         S, Kt, Vt, Z, A, lengths = ctx.saved_tensors
         dZ = torch.empty_like(Z)
@@ -424,8 +479,8 @@ class _GdpaCore(torch.autograd.Function):
         dS = gemm(dZ, Kt, residual=g)
         dKt = gemm(dZ.transpose(1, 2), S)
         dVt = gemm(A.transpose(1, 2), g)
-        if ctx.sink is not None and ctx.sink.t is None:
-            ctx.sink.put(dS)
+        if ctx.sink is not None:
+            dS = ctx.sink.deliver(dS)
         return dS, dKt, dVt, None, None, None, None, None
 
 
@@ -544,13 +599,16 @@ class _HspPool(torch.autograd.Function):
             return tuple(outs) + ((rec,) if rec is not None else ())
         sc = gemm(S, Q.t(), out_dtype=torch.float32)  # (B, T, HQ)
         Pm = torch.empty(B, T, HQ, device=S.device, dtype=S.dtype)
-        a = _colsm_args(sc, Pm, lengths)
+        lse = torch.empty(B, HQ, device=S.device, dtype=torch.float32)
+        a = _colsm_args(sc, Pm, lengths, lse)
         _capi.call("kl_colsoftmax_fwd", C.byref(a), _stream())
         outs, c0 = [], 0
         for n in splits:
             outs.append(gemm(Pm[:, :, c0:c0 + n].transpose(1, 2), S))  # (B, n, d)
             c0 += n
-        ctx.save_for_backward(S, Q, lengths, Pm, *outs)
+        # the backward recomputes P in fp32 from the scores + LSE (a bf16 P
+        # would feed its rounding into the cancellation-heavy dQ reduction)
+        ctx.save_for_backward(S, Q, lengths, Pm, sc, lse, *outs)
         return tuple(outs) + ((rec,) if rec is not None else ())
 
     @staticmethod
@@ -566,16 +624,16 @@ class _HspPool(torch.autograd.Function):
             _recent_bwd_into(dS, g_rec, ctx.saved_tensors[2])
         if dS is not None and ctx.sink is not None:
             if ctx.sink.t is dS:
-                dS = None  # accumulated into the sequence's shared gradient buffer
+                dS = None  # accumulated into the sequence's shared gradient buffer (kernel epilogue)
                 ctx.sink.release()
-            elif ctx.sink.t is None:
-                ctx.sink.put(dS)
+            else:
+                dS = ctx.sink.deliver(dS)
         return dS, dQ, None, None, None, None
 
 
 def _hsp_gemm_bwd(ctx, gs):
     """GEMM composition of the pooling VJP (fp32 parity path)."""
-    S, Q, lengths, Pm, *outs = ctx.saved_tensors
+    S, Q, lengths, Pm, sc, lse, *outs = ctx.saved_tensors
     B, T, d = S.shape
     HQ = Q.shape[0]
     dP = torch.empty(B, T, HQ, device=S.device, dtype=torch.float32)
@@ -596,6 +654,8 @@ def _hsp_gemm_bwd(ctx, gs):
     dsc = torch.empty_like(Pm)
     lo = torch.empty_like(Pm) if Pm.dtype != torch.float32 else None
     a = _colsm_args(dsc, Pm, lengths)  # dtype_in = dsc dtype, dtype_out = P dtype
+    a.X, a.x_rs, a.x_bs = sc.data_ptr(), sc.stride(1), sc.stride(0)  # recompute mode: P = exp(sc - LSE)
+    a.LSE = lse.data_ptr()
     a.dP, a.dp_rs, a.dp_bs = dP.data_ptr(), dP.stride(1), dP.stride(0)
     a.dX, a.dx_rs, a.dx_bs = dsc.data_ptr(), dsc.stride(1), dsc.stride(0)
     a.dX_lo = lo.data_ptr() if lo is not None else None

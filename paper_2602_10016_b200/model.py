@@ -220,6 +220,7 @@ class KunlunModel:
         # one shared dS buffer per event sequence: its consumers (the GDPA
         # branch, HSP pooling + recent rows) accumulate into it
         sinks = [F.GradSink() for _ in cfg.events]
+        S_list = [F.seq_join(s, k) for s, k in zip(S_list, sinks)]
 
         events = range(len(cfg.events))
 

@@ -2,7 +2,7 @@
 timeout 300 python -m pytest tests/test_gpu_gemm_tc.py -q -x 2>&1 | tail -2
 for w in qkv dx res bias mlp_noaux; do for ns in 0 1; do
 if [ $ns = 1 ]; then export KL_GEMM_NO_ESPLIT=1; else unset KL_GEMM_NO_ESPLIT; fi
-echo -n "$w nosplit=$ns "; timeout 120 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:gemm_tc python tests/gemm_one.py $w 2>&1 | grep -E "duration" | tail -1
+echo -n "$w nosplit=$ns "; timeout 120 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:gemm_tc python scripts/probes/gemm_one.py $w 2>&1 | grep -E "duration" | tail -1
 done; done
 unset KL_GEMM_NO_ESPLIT
 timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2

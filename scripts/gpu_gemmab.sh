@@ -1,7 +1,7 @@
 timeout 300 python -m pytest tests/test_gpu_gemm_tc.py -q -x 2>&1 | tail -2
 for w in qkv bias res dx; do for nb in 0 1; do
 if [ $nb = 1 ]; then export KL_GEMM_NO_BRES=1; else unset KL_GEMM_NO_BRES; fi
-echo "$w nobres=$nb"; timeout 120 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:gemm_tc python tests/gemm_one.py $w 2>&1 | grep -E "duration" | tail -1
+echo "$w nobres=$nb"; timeout 120 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:gemm_tc python scripts/probes/gemm_one.py $w 2>&1 | grep -E "duration" | tail -1
 done; done
 unset KL_GEMM_NO_BRES
 timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2

@@ -1,4 +1,4 @@
-for w in mlp mlp_noaux mlp_bias mlp_plain; do echo $w; timeout 120 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:gemm_tc python tests/gemm_one.py $w 2>&1 | grep -E "duration" | tail -1; done
+for w in mlp mlp_noaux mlp_bias mlp_plain; do echo $w; timeout 120 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:gemm_tc python scripts/probes/gemm_one.py $w 2>&1 | grep -E "duration" | tail -1; done
 timeout 300 python -m pytest tests/test_gpu_gemm_tc.py -q -x 2>&1 | tail -1
 timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -1
 timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench rc $?

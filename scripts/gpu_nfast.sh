@@ -2,7 +2,7 @@
 timeout 300 python -m pytest tests/test_gpu_gemm_tc.py -q -x 2>&1 | tail -2
 for w in qkv bias mlp_noaux; do for mf in 0 1; do
 if [ $mf = 1 ]; then export KL_GEMM_M_FAST=1; else unset KL_GEMM_M_FAST; fi
-echo -n "$w mfast=$mf "; timeout 120 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum --clock-control none -k regex:gemm_tc python tests/gemm_one.py $w 2>&1 | grep -E "duration|dram" | tail -2 | tr '\n' ' '; echo
+echo -n "$w mfast=$mf "; timeout 120 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum --clock-control none -k regex:gemm_tc python scripts/probes/gemm_one.py $w 2>&1 | grep -E "duration|dram" | tail -2 | tr '\n' ' '; echo
 done; done
 unset KL_GEMM_M_FAST
 timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2

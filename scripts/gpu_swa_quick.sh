@@ -1,5 +1,5 @@
 timeout 300 python -m pytest tests/test_gpu_parity.py -q -x -k "swa or model" 2>&1 | tail -1
-timeout 300 python tests/swa_tc_probe.py bwd_only 128 1024 4 128 0 full > /dev/null 2>&1
+timeout 300 python scripts/probes/swa_tc_probe.py bwd_only 128 1024 4 128 0 full > /dev/null 2>&1
 timeout 300 python - <<'PY'
 import sys, torch
 sys.path.insert(0, ".")

@@ -1,6 +1,6 @@
 """Standalone timing probe of the fused GDPA kernels (kl_gdpa_fwd/bwd) at a
 given shape (run on the GPU box; also the ncu target):
-    python tests/gdpa_probe.py [B T d] [iters]
+    python scripts/probes/gdpa_probe.py [B T d] [iters]
 Prints average device time per launch and the achieved algorithmic HBM
 bandwidth (fwd: read S + write Y; bwd: read S, dY + write dS)."""
 import ctypes as C

@@ -1,5 +1,5 @@
 """Time model-shaped kl_gemm calls (CUDA events, L2-resident or not):
-    python tests/gemm_bench.py  -> one line per shape: us, TF/s, GB/s."""
+    python scripts/probes/gemm_bench.py  -> one line per shape: us, TF/s, GB/s."""
 import sys
 
 import torch

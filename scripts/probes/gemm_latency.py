@@ -1,5 +1,5 @@
 """Per-call device time of small kl_gemm shapes, back to back (eager) and
-replayed from a CUDA graph:  python tests/gemm_latency.py"""
+replayed from a CUDA graph:  python scripts/probes/gemm_latency.py"""
 import sys
 
 import torch

@@ -1,5 +1,5 @@
 """GEMM timing probe on the B200: kl_gemm on model shapes, CUDA-event timed.
-usage: python tests/gemm_probe.py [reps]"""
+usage: python scripts/probes/gemm_probe.py [reps]"""
 import sys
 
 import torch

@@ -1,5 +1,5 @@
 """A/B the tcgen05 (operand-swapped) and SIMT paths on the model's batched
-small products (graph-replayed per-call device time):  python tests/gemm_small_ab.py"""
+small products (graph-replayed per-call device time):  python scripts/probes/gemm_small_ab.py"""
 import sys
 
 import torch

@@ -1,5 +1,5 @@
 """Probe of the fused HSP pooling kernels vs a torch fp32 reference:
-    python tests/hsp_probe.py [B T d HQ n1]"""
+    python scripts/probes/hsp_probe.py [B T d HQ n1]"""
 import ctypes as C
 import sys
 

@@ -1,5 +1,5 @@
 """Timing probe of kl_rote (the ROTE kernel) at a c4-sized batch:
-    python tests/rote_probe.py [B T d] [iters]
+    python scripts/probes/rote_probe.py [B T d] [iters]
 Prints device time per launch (CUDA events, inputs >> L2 rotate through 4
 buffers) and achieved algorithmic HBM bandwidth: read x + write y (bf16) +
 read the fp64 timestamps."""
