@@ -112,27 +112,41 @@ def _cpu_worker(args):
 _CPU_STATE = {}
 
 
-def oracle_spec(cfg):
+def oracle_spec(cfg, L=None):
     from oracle import model as OM
 
-    return OM.ModelSpec(L=cfg.L, d=cfg.d, heads=cfg.heads, n_ctx=cfg.n_ctx, n_sum=cfg.n_sum, n_kv=cfg.n_kv,
+    return OM.ModelSpec(L=L or cfg.L, d=cfg.d, heads=cfg.heads, n_ctx=cfg.n_ctx, n_sum=cfg.n_sum, n_kv=cfg.n_kv,
                         experts=cfg.experts, compskip=cfg.compskip, gdpa_acts=tuple(cfg.gdpa_acts),
                         expert_hidden=cfg.expert_hidden, head_hidden=cfg.head_hidden,
                         events=[OM.EventSpec(T=e.T, w=e.w, budget=e.budget, n_seeds=e.n_seeds, rank=e.rank,
                                              causal=e.causal) for e in cfg.events])
 
 
+def reference_layers(cfg):
+    """Layers the CPU reference runs per sample: the whole model when that is
+    cheap, else a layer sample (1 layer, or one even + one odd layer under
+    CompSkip, whose layers alternate) scaled to cfg.L ("time
+    per-layer on >= P samples and state the L-scaling explicitly")."""
+    work = cfg.L * sum(e.T for e in cfg.events) * cfg.d * cfg.d
+    if work <= 4 * 1024 * 256 * 256:  # c1, c2: the full model
+        return cfg.L
+    return min(cfg.L, 2 if cfg.compskip else 1)
+
+
 def cpu_reference(cfg, workers: int, samples_per_worker: int = 1, rounds: int = 1, warm: int = 0):
     """Times the float64 oracle fwd+bwd (the reference algorithm restated,
     oracle/model.py) with ``workers`` forked single-thread processes, each on
-    ``samples_per_worker`` samples per round.  Returns per-round samples/s."""
+    ``samples_per_worker`` samples per round.  Returns (per-round samples/s
+    of the FULL model, layers run per sample); with a layer sample the rate is
+    scaled by layers_run / cfg.L."""
     import multiprocessing as mp
 
     from oracle import model as OM
 
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
     os.environ["OMP_NUM_THREADS"] = "1"
-    spec = oracle_spec(cfg)
+    Lr = reference_layers(cfg)
+    spec = oracle_spec(cfg, Lr)
     _CPU_STATE["spec"] = (spec, OM.init_params(spec, seed=0))
     ctx = mp.get_context("fork")
     rates = []
@@ -142,8 +156,19 @@ def cpu_reference(cfg, workers: int, samples_per_worker: int = 1, rounds: int = 
             done = sum(pool.map(_cpu_worker, [("spec", samples_per_worker, 1000 * r + i) for i in range(workers)]))
             dt = time.perf_counter() - t0
             if r >= warm:
-                rates.append(done / dt)
-    return rates
+                rates.append(done / dt * Lr / cfg.L)
+    return rates, Lr
+
+
+def cpu_model_name():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def host_cores():
@@ -161,15 +186,17 @@ def run_reference(args, cfg, B, rank, world):
     if rank != 0:
         return
     workers = max(1, min(host_cores(), args.cpu_workers))
-    rates = cpu_reference(cfg, workers, 1, rounds=args.steps, warm=args.warmup)
+    rates, Lr = cpu_reference(cfg, workers, 1, rounds=args.steps, warm=args.warmup)
     v = statistics.median(rates)
+    sample = (f"{workers} samples/step (1 per forked single-thread worker), oracle float64 fwd+bwd of "
+              + ("the full model" if Lr == cfg.L else f"{Lr} of {cfg.L} layers, rate scaled by {Lr}/{cfg.L}")
+              + f"; host CPU {cpu_model_name()}")
     line = {
         "impl": "reference", "metric": "kunlun_fwd_bwd_samples_per_s", "value": v, "unit": "samples/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * workers / v,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": workload(args, cfg, B, world),
-        "cpu_baseline": {"value": v, "unit": "samples/s", "cores": workers, "kind": "port",
-                         "sample": f"{workers} samples/step (1 per worker process), oracle float64 fwd+bwd"},
+        "cpu_baseline": {"value": v, "unit": "samples/s", "cores": workers, "kind": "port", "sample": sample},
         "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -223,6 +250,111 @@ def graph_census(log, step, use_graph):
         print(f"{v / 1e3:8.3f} ms {100 * v / tot:5.1f}% {cnt[k]:4d}k  {k[0]:18s} {k[1]:24s} {k[2]}", file=sys.stderr)
 
 
+NCU_KERNELS = {  # roofline family -> kernel-name substrings (CUPTI / ncu names)
+    "gemm": ("gemm_tc_kernel", "gemm_simt_kernel", "splitk_reduce"),
+    "swa_fwd": ("swa_fwd_tc", "swa_fwd_kernel"), "swa_bwd": ("swa_bwd_", "swa_rowdot"),
+    "gdpa_fwd": ("gdpa_fwd_kernel",), "gdpa_bwd": ("gdpa_bwd_kernel",), "hsp_fwd": ("hsp_fwd_kernel",),
+    "hsp_bwd": ("hsp_bwd_kernel",), "colsoftmax_fwd": ("colsoftmax_fwd_kernel",),
+    "colsoftmax_bwd": ("colsoftmax_bwd_kernel",), "adam": ("adam_kernel",),
+}
+
+
+def family_of(kernel_name):
+    for f, subs in NCU_KERNELS.items():
+        if any(x in kernel_name for x in subs):
+            return f
+    return None
+
+
+def kernel_records(step):
+    """[(kernel name, device us)] of one replay of ``step`` (CUPTI)."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        step()
+        torch.cuda.synchronize()
+    return [(e.name, e.time_range.end - e.time_range.start) for e in prof.events()
+            if e.device_type.name == "CUDA"]
+
+
+def _ncu_traffic(config, B):
+    """{family: {"dram_bytes_per_launch", "tensor_pipe_pct", ...}} from the
+    committed ncu --set full summary of this config (profiles/ncu_<config>_B<B>.json,
+    written by profiles/summarize_ncu.py), or {}."""
+    try:
+        with open(os.path.join(ROOT, "profiles", f"ncu_{config}_B{B}.json")) as f:
+            return json.load(f).get("families", {})
+    except (OSError, ValueError):
+        return {}
+
+
+def roofline_table(work, kernels, ms_step, burst, sustained, hbm, peak_kind, config, B):
+    """Per kernel family of one step: launches and summed device time (CUPTI
+    records of a replay of the captured step), the algorithmic flops / bytes
+    the step's C-ABI calls declare (_capi._work_of), the bound (tensor when
+    flops/bytes >= the ridge of the measured peaks), the achieved rate against
+    the measured peak (sustained bf16: these kernels run inside a long step),
+    and the ncu DRAM traffic where a capture exists.  ``share_of_step`` is the
+    family's summed kernel time over the step time (branches overlap, so
+    shares can sum past 1).  The headline ``roofline`` is the family with the
+    most device time."""
+    ridge = sustained * 1e12 / (hbm * 1e9)
+    fam = {}
+    for f, flops, nbytes, _, _ in work:
+        d = fam.setdefault(f, {"launches": 0, "ms": 0.0, "flops": 0.0, "bytes": 0.0, "calls": 0, "tflops": 0.0})
+        d["calls"] += 1
+        d["flops"] += flops
+        d["bytes"] += nbytes
+        if flops >= ridge * nbytes:
+            d["tflops"] += flops  # flops of calls that are tensor-bound on their own
+    other = 0.0
+    for name, us in kernels:
+        f = family_of(name)
+        if f is None or f not in fam:
+            other += us / 1e3
+            continue
+        fam[f]["launches"] += 1
+        fam[f]["ms"] += us / 1e3
+    ncu = _ncu_traffic(config, B)
+    table = {}
+    for f, d in fam.items():
+        if not d["launches"]:
+            continue
+        sec = d["ms"] / 1e3
+        # a family is tensor-bound when most of its flops come from calls whose
+        # own flops/bytes sit above the ridge (the GEMM family mixes K = d
+        # projections with small per-sample products)
+        tensor = d["flops"] > 0 and d["tflops"] >= 0.5 * d["flops"]
+        gbs, tfs = d["bytes"] / sec / 1e9, d["flops"] / sec / 1e12
+        ach, peak, unit = (tfs, sustained, "TFLOP/s") if tensor else (gbs, hbm, "GB/s")
+        n = d["launches"]
+        table[f] = {"bound": "tensor" if tensor else "hbm", "achieved": ach, "peak": peak, "unit": unit,
+                    "frac": ach / peak, "launches": n, "calls": d["calls"], "avg_launch_ms": d["ms"] / n,
+                    "ms_per_step": d["ms"], "share_of_step": d["ms"] / ms_step,
+                    "algorithmic_flops_per_launch": d["flops"] / n, "algorithmic_bytes_per_launch": d["bytes"] / n,
+                    "achieved_gbs": gbs, "achieved_tflops": tfs, "tensor_bound_flop_share": d["tflops"] / max(d["flops"], 1.0),
+                    "traffic": None}
+        nc = ncu.get(f)
+        if nc:
+            table[f]["traffic"] = nc.get("dram_bytes_per_launch")
+            table[f]["ncu"] = nc
+    if not table:
+        return table, None
+    table["_other_kernels"] = {"ms_per_step": other, "share_of_step": other / ms_step}
+    top = max((k for k in table if not k.startswith("_")), key=lambda k: table[k]["ms_per_step"])
+    t = table[top]
+    roof = {"bound": t["bound"], "kernel": top, "achieved": t["achieved"], "peak": t["peak"], "unit": t["unit"],
+            "frac": t["frac"], "traffic": t["traffic"],
+            "peak_kind": f"{peak_kind} " + ("bf16 sustained" if t["bound"] == "tensor" else "HBM copy"),
+            "algorithmic_per_launch": t["algorithmic_flops_per_launch" if t["bound"] == "tensor"
+                                        else "algorithmic_bytes_per_launch"],
+            "avg_launch_ms": t["avg_launch_ms"], "launches_per_step": t["launches"],
+            "share_of_step": t["share_of_step"]}
+    return table, roof
+
+
 def workload(args, cfg, B, world):
     ev = cfg.events[0]
     return {"workload": f"kunlun_{args.config}_train_step", "model": "kunlun", "layers": cfg.L, "d": cfg.d,
@@ -238,7 +370,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c4", help="BASELINE.json configs: c4 (the 1/2/4/8-GPU DP config, default), "
+                    "c1, c2, c3")
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-workers", type=int, default=32)
@@ -251,7 +384,18 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # --gpus N without a launcher: one process per GPU via torchrun (NCCL)
+        import random
+
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={random.randint(20000, 40000)}",
+               os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
+
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.gpus > 1 and world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
 
@@ -340,17 +484,21 @@ def main():
     # The SWA kernels are timed with CUDA events recorded on their launching
     # stream; in graph mode the event records are nodes of the captured step,
     # so the durations come from the timed replays themselves.
-    timed_ops = {"kl_swa_fwd": [], "kl_swa_bwd": []}
+    # Per-launch work accounting (roofline table): every accounted launch of
+    # one step is bracketed by external CUDA events recorded on its launching
+    # stream; in graph mode they are nodes of the captured step, so the
+    # durations come from the timed replays themselves.
     n_step = _capi.launch_count()
-    steps_[0].eager()
+    work = []  # (family, algorithmic flops, bytes) of every accounted launch of one step
+    _capi.WORK, _capi.WORK_EVENTS = work, False
+    try:
+        steps_[0].eager()
+    finally:
+        _capi.WORK, _capi.WORK_EVENTS = None, True
     launches_per_step = _capi.launch_count() - n_step
     use_graph = not args.eager
     if use_graph:
-        try:
-            _capi.TIMED, _capi.TIMED_EXTERNAL = timed_ops, True
-            steps_[0].capture(warmup=0)
-        finally:
-            _capi.TIMED, _capi.TIMED_EXTERNAL = None, False
+        steps_[0].capture(warmup=0)
         for st in steps_[1:]:
             st.capture(warmup=0)
         for _ in range(args.warmup):
@@ -361,33 +509,25 @@ def main():
         graph_census(census_log, steps_[0], use_graph)
 
     # ---- device-timed region: inputs resident in HBM ----------------------
-    if not use_graph:
-        _capi.TIMED = timed_ops
     clocks = ClockSampler(torch.cuda.current_device())
     clocks.start()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     h0 = time.perf_counter()
-    for _ in range(args.steps):
+    for i in range(args.steps):
         steps_[0]()
     host_ms = (time.perf_counter() - h0) * 1e3 / args.steps
     e1.record()
     barrier()
     launches = launches_per_step * args.steps
     clk = clocks.stop()
-    _capi.TIMED = None
     ms = e0.elapsed_time(e1) / args.steps
     t = torch.tensor([ms], device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     value = world * B / (ms / 1e3)
-
-    # ---- roofline of the dominant kernel: SWA (fwd + bwd) ------------------
-    nsw = sum(1 for l in range(cfg.L) if model.seq_live()[l] and not model.flags[l].skip_self_attention)
-    swa_ms = [s.elapsed_time(e) for (s, e) in timed_ops["kl_swa_fwd"][-nsw:]] if nsw else []
-    swab_ms = [s.elapsed_time(e) for (s, e) in timed_ops["kl_swa_bwd"][-nsw:]] if nsw else []
 
     flags, live = model.flags, model.seq_live()
     fps = metrics.train_flops_per_sample(cfg, flags, live)
@@ -444,46 +584,26 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu:
         workers = max(1, min(host_cores(), args.cpu_workers))
         try:
-            rates = cpu_reference(cfg, workers, 1, rounds=1)
+            rates, Lr = cpu_reference(cfg, workers, 1, rounds=1)
             cpu = {"value": rates[0], "unit": "samples/s", "cores": workers, "kind": "port",
                    "sample": f"{workers} samples (1 per forked single-thread worker), oracle float64 fwd+bwd "
-                             f"of the same config (oracle/model.py; dense masked T x T attention as the reference)"}
+                             f"of the same config (oracle/model.py: the reference's masked attention, block-banded "
+                             f"above T=1024)" + ("" if Lr == cfg.L else f", {Lr} of {cfg.L} layers, rate scaled by "
+                                                                      f"{Lr}/{cfg.L}")
+                             + f"; host CPU {cpu_model_name()}"}
         except Exception as exc:  # pragma: no cover
             cpu = {"value": None, "unit": "samples/s", "cores": workers, "kind": "port", "sample": f"failed: {exc}"}
 
     if rank != 0:
         return
-    swa_flops = 4.0 * sum(metrics._support(ev.T, ev.w, ev.causal) for ev in cfg.events) * cfg.d * B
-    n_swa_layers = sum(1 for l in range(cfg.L) if live[l] and not flags[l].skip_self_attention)
-    fwd_avg = (sum(swa_ms) / len(swa_ms)) if swa_ms else None
-    bwd_avg = (sum(swab_ms) / len(swab_ms)) if swab_ms else None
-    roof = None
-    if fwd_avg:
-        # The banded attention core reads Q, K, V (B*T*3*H*d_h bf16) and
-        # writes O (bf16) + LSE (fp32) once: at d_h = 64 its floor is HBM
-        # (bytes / 6.5 TB/s) above the tensor floor (executed flops / peak),
-        # so the roofline is the HBM one; the tensor numbers ride along.
-        H_ = cfg.heads
-        swa_bytes = float(sum(B * ev.T * (3 * cfg.d * 2 + cfg.d * 2 + H_ * 4) for ev in cfg.events))
-        ach_gbs = swa_bytes / (fwd_avg / 1e3) / 1e9
-        ach_tf = swa_flops / (fwd_avg / 1e3) / 1e12
-        traffic = None
-        try:  # dram__bytes_read.sum + dram__bytes_write.sum of the same kernel/shape (ncu --set full)
-            prof = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
-                                               "r1_swa3_ncu.json")))
-            k = prof["kernels"].get("swa_fwd_tc3_kernel")
-            if k and args.config == "c2" and B == 128:
-                traffic = k["dram_bytes_per_launch"]
-        except (OSError, ValueError, KeyError):
-            pass
-        roof = {"bound": "hbm", "kernel": "kl_swa_fwd (banded flash attention core, swa_fwd_tc3_kernel)",
-                "achieved": ach_gbs, "peak": hbm, "unit": "GB/s", "frac": ach_gbs / hbm, "traffic": traffic,
-                "algorithmic_bytes_per_launch": swa_bytes, "avg_launch_ms": fwd_avg,
-                "tensor": {"achieved_tflops": ach_tf, "peak": burst, "frac": ach_tf / burst,
-                           "algorithmic_flops_per_launch": swa_flops,
-                           "floor_ms": {"hbm": swa_bytes / hbm / 1e6, "tensor": swa_flops / burst / 1e9}},
-                "bwd_avg_launch_ms": bwd_avg, "launches_per_step": n_swa_layers,
-                "share_of_step": (fwd_avg + (bwd_avg or 0)) * n_swa_layers / ms}
+    # ---- per-kernel-family roofline table (after, and outside, the timed
+    # regions): CUPTI kernel records of one more replay of the same captured
+    # step (torch.profiler), grouped by kernel family, against the
+    # algorithmic work the C-ABI calls of one step declare.
+    table, roof = None, None
+    if rank == 0:
+        table, roof = roofline_table(work, kernel_records(steps_[0]), ms, burst, sustained, hbm, peak_kind,
+                                     args.config, B)
     achieved_tf = fps * value / world / 1e12
     line = {
         "metric": "kunlun_fwd_bwd_samples_per_s", "value": value, "unit": "samples/s", "n_gpus": world,
@@ -495,7 +615,7 @@ def main():
                 "achieved_tflops_per_gpu": achieved_tf, "train_flops_per_sample": fps,
                 "ledger": "executed matmul MACs x2 x3 (metrics.py), liveness-pruned, reassociated forms",
                 "reference_formulation_flops_per_sample": fps_ref, "fwd_macs_by_part": macs},
-        "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+        "roofline": roof, "roofline_table": table, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
         "clocks": clk, "host_issue_ms_per_step": host_ms, "cuda_graph": use_graph,
     }
     print(json.dumps(line), flush=True)

@@ -115,12 +115,80 @@ def multi_head_attention(xq, xkv, p: dict, prefix: str, mask=None):
     return out, bwd
 
 
-def mha_window(s, p: dict, prefix: str, w: int, causal: bool = False, length=None):
-    """S + MHA(S, S, band & valid) (attention.py:124-129)."""
+BAND_MIN_T = 1024  # mha_window evaluates block-banded above this length (same sums, no T x T arrays)
+BAND_BLOCK = 128
+
+
+def _banded_self_attention(x, p: dict, prefix: str, w: int, causal: bool, valid):
+    """multi_head_attention(x, x, p, prefix, band & valid) evaluated per
+    128-query block over the key rows that block can see ([q0 - w, q0 + 127 +
+    w]): every score outside that range is masked in the reference
+    (attention.py:69-93 with band_mask, attention.py:96-104), so it contributes
+    an exact zero to the masked softmax (tensor.py:485-505) and to every
+    product — the result equals the dense evaluation up to float64 summation
+    order (tests/test_oracle_golden.py checks them against each other)."""
+    H = heads_of(p, prefix)
+    Wq = np.stack([p[f"{prefix}/head{h}/w_q"] for h in range(H)])
+    Wk = np.stack([p[f"{prefix}/head{h}/w_k"] for h in range(H)])
+    Wv = np.stack([p[f"{prefix}/head{h}/w_v"] for h in range(H)])
+    Wo = p[f"{prefix}/w_out"]
+    T = x.shape[0]
+    d_h = Wq.shape[1]
+    inv = 1.0 / np.sqrt(d_h)
+    q = x @ Wq.transpose(0, 2, 1)
+    k = x @ Wk.transpose(0, 2, 1)
+    v = x @ Wv.transpose(0, 2, 1)
+    o = np.zeros((H, T, d_h))
+    blocks = []
+    for q0 in range(0, T, BAND_BLOCK):
+        q1 = min(T, q0 + BAND_BLOCK)
+        k0, k1 = max(0, q0 - w), min(T, q1 + w)
+        qi = np.arange(q0, q1)[:, None]
+        kj = np.arange(k0, k1)[None, :]
+        m = (np.abs(qi - kj) <= w) & valid[q0:q1, None] & valid[None, k0:k1]
+        if causal:
+            m &= kj <= qi
+        sc = (q[:, q0:q1] @ k[:, k0:k1].transpose(0, 2, 1)) * inv
+        attn, sm_bwd = masked_softmax(sc, m[None])
+        o[:, q0:q1] = attn @ v[:, k0:k1]
+        blocks.append((q0, q1, k0, k1, attn, sm_bwd))
+    cat = o.transpose(1, 0, 2).reshape(T, H * d_h)
+    out = cat @ Wo.T
+
+    def bwd(g):
+        grads = {f"{prefix}/w_out": g.T @ cat}
+        do = (g @ Wo).reshape(T, H, d_h).transpose(1, 0, 2)
+        dq, dk, dv = np.zeros_like(q), np.zeros_like(k), np.zeros_like(v)
+        for q0, q1, k0, k1, attn, sm_bwd in blocks:
+            dattn = do[:, q0:q1] @ v[:, k0:k1].transpose(0, 2, 1)
+            dv[:, k0:k1] += attn.transpose(0, 2, 1) @ do[:, q0:q1]
+            dsc = sm_bwd(dattn) * inv
+            dq[:, q0:q1] += dsc @ k[:, k0:k1]
+            dk[:, k0:k1] += dsc.transpose(0, 2, 1) @ q[:, q0:q1]
+        dWq, dWk, dWv = dq.transpose(0, 2, 1) @ x, dk.transpose(0, 2, 1) @ x, dv.transpose(0, 2, 1) @ x
+        for h in range(H):
+            grads[f"{prefix}/head{h}/w_q"] = dWq[h]
+            grads[f"{prefix}/head{h}/w_k"] = dWk[h]
+            grads[f"{prefix}/head{h}/w_v"] = dWv[h]
+        dx = (dq @ Wq).sum(0) + (dk @ Wk).sum(0) + (dv @ Wv).sum(0)
+        return dx, np.zeros_like(x), grads
+
+    return out, bwd
+
+
+def mha_window(s, p: dict, prefix: str, w: int, causal: bool = False, length=None, banded=None):
+    """S + MHA(S, S, band & valid) (attention.py:124-129).  ``banded``
+    (default: T > BAND_MIN_T) evaluates the same masked attention per query
+    block over its visible key range (_banded_self_attention)."""
     t_len = s.shape[0]
     valid = length_mask(t_len, length)
-    mask = band_mask(t_len, w, causal) & valid[None, :] & valid[:, None]
-    a, a_bwd = multi_head_attention(s, s, p, prefix, mask)
+    if banded is None:
+        banded = t_len > BAND_MIN_T
+    if banded:
+        a, a_bwd = _banded_self_attention(s, p, prefix, w, causal, valid)
+    else:
+        mask = band_mask(t_len, w, causal) & valid[None, :] & valid[:, None]
+        a, a_bwd = multi_head_attention(s, s, p, prefix, mask)
 
     def bwd(g):
         dxq, dxkv, grads = a_bwd(g)

@@ -329,6 +329,16 @@ def gemm(A: torch.Tensor, B: torch.Tensor, out: torch.Tensor | None = None, *, o
     a.workspace, a.workspace_bytes = ws.data_ptr(), ws.numel() * 4
     if OP_LOG is not None:
         _logged("kl_gemm", f"{M}x{N}x{K} b{nb1}x{nb2} r{int(red1)}{int(red2)}", lib().kl_gemm, C.byref(a), _stream())
+    elif WORK is not None:
+        ea, ec = A.element_size(), out.element_size()
+        nA = (A4.shape[0] * A4.shape[1]) * M * K
+        nB = (B4.shape[0] * B4.shape[1]) * K * N
+        nC = oshape[0] * oshape[1] * M * N
+        nbytes = (nA + nB) * ea + nC * ec * (2 if beta != 0.0 else 1) + (nC * ec if residual is not None else 0) \
+            + (nC * ec if aux is not None else 0)
+        fam = "gemm"
+        _check(_record_work(fam, 2.0 * M * N * K * nb1 * nb2, float(nbytes), lib().kl_gemm, C.byref(a), _stream()),
+               "kl_gemm")
     else:
         _check(lib().kl_gemm(C.byref(a), _stream()), "kl_gemm")
     if GEMM_LOG is not None:
@@ -394,7 +404,73 @@ def _logged(name, shape, fn, *args):
     _check(rc, name)
 
 
+# Per-launch work accounting for bench.py's roofline table: while WORK is a
+# list, every accounted entry point records (family, algorithmic flops,
+# algorithmic bytes, start event, end event) around its launch on the
+# launching stream (external events survive CUDA-graph capture, so a captured
+# step's replays refresh the durations).
+WORK = None
+
+
+def _support_total(T, w, causal):
+    import numpy as np
+
+    i = np.arange(T)
+    hi = np.minimum(i + w, T - 1) if not causal else i
+    return int((hi - np.maximum(i - w, 0) + 1).sum())
+
+
+def _work_of(name, args):
+    """(family, flops, bytes) of one launch from its C-ABI arguments (the
+    algorithmic work: operands read once, results written once)."""
+    a = args[0]._obj if args and hasattr(args[0], "_obj") else None
+    if name in ("kl_swa_fwd", "kl_swa_bwd") and a is not None:
+        HD = a.H * a.d_h
+        sup = _support_total(a.T, a.w, bool(a.causal))
+        if name == "kl_swa_fwd":
+            return "swa_fwd", 4.0 * sup * HD * a.B, float(a.B) * a.T * (3 * HD * 2 + HD * 2 + a.H * 4)
+        return "swa_bwd", 10.0 * sup * HD * a.B, float(a.B) * a.T * (3 * HD * 2 * 2 + HD * 2 * 2 + a.H * 4 * 2)
+    if name in ("kl_gdpa_fwd", "kl_gdpa_bwd") and a is not None:
+        mm = 2.0 * a.B * a.T * a.HK * a.d
+        kv = 2.0 * a.B * a.HK * a.d * 2
+        if name == "kl_gdpa_fwd":
+            return "gdpa_fwd", 2 * mm, 2.0 * a.B * a.T * a.d * 2 + kv
+        return "gdpa_bwd", 5 * mm, 3.0 * a.B * a.T * a.d * 2 + 2 * kv
+    if name in ("kl_hsp_fwd", "kl_hsp_bwd") and a is not None:
+        mm = 2.0 * a.B * a.T * a.HQ * a.d
+        if name == "kl_hsp_fwd":
+            return "hsp_fwd", 2 * mm, float(a.B) * a.T * a.d * 2
+        return "hsp_bwd", 4 * mm, 2.0 * a.B * a.T * a.d * 2 + 2.0 * a.B * a.HQ * a.T * 2 * 2
+    if name in ("kl_colsoftmax_fwd", "kl_colsoftmax_bwd") and a is not None:
+        n = float(a.Bn) * a.T * a.C
+        return ("colsoftmax_fwd", 0.0, n * 6) if name == "kl_colsoftmax_fwd" else ("colsoftmax_bwd", 0.0, n * 12)
+    if name == "kl_adam_step":
+        return "adam", 0.0, float(args[0]) * 30  # fp32 p, g, m, v read; p, m, v + bf16 mirror written
+    return None
+
+
+WORK_EVENTS = True  # False: log the work only (durations come from a profiler pass)
+
+
+def _record_work(fam, flops, nbytes, fn, *args):
+    if not WORK_EVENTS:
+        WORK.append((fam, flops, nbytes, None, None))
+        return fn(*args)
+    s = torch.cuda.Event(enable_timing=True, external=True)
+    e = torch.cuda.Event(enable_timing=True, external=True)
+    s.record()
+    rc = fn(*args)
+    e.record()
+    WORK.append((fam, flops, nbytes, s, e))
+    return rc
+
+
 def call(name: str, *args):
+    if WORK is not None:
+        w = _work_of(name, args)
+        if w is not None:
+            _check(_record_work(w[0], w[1], w[2], getattr(lib(), name), *args), name)
+            return
     if OP_LOG is not None:
         _logged(name, "", getattr(lib(), name), *args)
         return

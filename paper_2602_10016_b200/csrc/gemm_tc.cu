@@ -300,35 +300,58 @@ __device__ __forceinline__ float rcp_apx(float x) {
 // GEMM epilogues use (identity, relu, silu, tanh; host-checked, others take
 // the generic epilogue): every case is a 32-wide unrolled loop, and each extra
 // case grows the epilogue warps' code (instruction-cache pressure).
-__device__ __forceinline__ void act32(int code, float* v) {
+template <int N>
+__device__ __forceinline__ void act_n(int code, float* v) {
   if (code == KL_ACT_RELU) {
 #pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
+    for (int i = 0; i < N; ++i) v[i] = fmaxf(v[i], 0.f);
   } else if (code == KL_ACT_SILU) {
 #pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = v[i] * rcp_apx(1.f + __expf(-v[i]));
+    for (int i = 0; i < N; ++i) v[i] = v[i] * rcp_apx(1.f + __expf(-v[i]));
   } else if (code == KL_ACT_TANH) {
 #pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = tanh_apx(v[i]);
+    for (int i = 0; i < N; ++i) v[i] = tanh_apx(v[i]);
   }
 }
 // v *= act'(a) for the same four codes (x = pre-activation), fp32 accurate
-__device__ __forceinline__ void dact32(int code, float* v, const float* a) {
+template <int N>
+__device__ __forceinline__ void dact_n(int code, float* v, const float* a) {
   if (code == KL_ACT_RELU) {
 #pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = a[i] > 0.f ? v[i] : 0.f;
+    for (int i = 0; i < N; ++i) v[i] = a[i] > 0.f ? v[i] : 0.f;
   } else if (code == KL_ACT_SILU) {
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
+    for (int i = 0; i < N; ++i) {
       const float sg = 1.f / (1.f + expf(-a[i]));
       v[i] *= sg * (1.f + a[i] * (1.f - sg));
     }
   } else if (code == KL_ACT_TANH) {
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
+    for (int i = 0; i < N; ++i) {
       const float y = tanhf(a[i]);
       v[i] *= 1.f - y * y;
     }
+  }
+}
+// A 32-column slab: activation groups are multiples of 16 columns (host-
+// checked), so each 16-column half has one code (e.g. GDPA's per-head runs
+// of n_kv = 16 generated rows).
+__device__ __forceinline__ void act32(const Epi& e, int n0, float* v) {
+  const int c0 = epi_code(e, n0), c1 = epi_code(e, n0 + 16);
+  if (c0 == c1) {
+    act_n<32>(c0, v);
+  } else {
+    act_n<16>(c0, v);
+    act_n<16>(c1, v + 16);
+  }
+}
+__device__ __forceinline__ void dact32(const Epi& e, int n0, float* v, const float* a) {
+  const int c0 = epi_code(e, n0), c1 = epi_code(e, n0 + 16);
+  if (c0 == c1) {
+    dact_n<32>(c0, v, a);
+  } else {
+    dact_n<16>(c0, v, a);
+    dact_n<16>(c1, v + 16, a + 16);
   }
 }
 
@@ -406,7 +429,7 @@ __device__ __forceinline__ void epi_tma(const TcParams& p, const Epi& e, const C
           for (int i = 0; i < 8; ++i) a[8 * q + i] = n0 + 8 * q + i < p.N ? ldf(xrow + 8 * q + i) : 0.f;
         }
       }
-      dact32(epi_code(e, n0), v, a);
+      dact32(e, n0, v, a);
     }
     if (FULL) {
       if (e.bias) {
@@ -455,7 +478,7 @@ __device__ __forceinline__ void epi_tma(const TcParams& p, const Epi& e, const C
           }
         }
       }
-      if (e.n_act && e.aux_mode != 2) act32(epi_code(e, nb * p.BN + c), v);  // slab-uniform (host-checked)
+      if (e.n_act && e.aux_mode != 2) act32(e, nb * p.BN + c, v);  // 16-column-uniform (host-checked)
     }
     if (Rs) {
 #pragma unroll
@@ -991,7 +1014,7 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
                (g.c_s1 * esz_c) % 16 == 0 && (g.c_s2 * esz_c) % 16 == 0 &&
                (!e.aux_mode || (g.aux && ((uintptr_t)g.aux & 15) == 0)) && bn % 32 == 0 &&
                (g.c_dtype == KL_BF16 ? e.beta == 0.f : (e.beta == 0.f && !g.R) || accum_only0) &&
-               (!g.R || use_r) && (e.n_act <= 1 || (e.act_group > 0 && e.act_group % 32 == 0));
+               (!g.R || use_r) && (e.n_act <= 1 || (e.act_group > 0 && e.act_group % 16 == 0));
   for (int i = 0; i < e.n_act && mode2; ++i) {
     const int c = e.act_codes[i];
     mode2 = c == KL_ACT_IDENTITY || c == KL_ACT_RELU || c == KL_ACT_SILU || c == KL_ACT_TANH;

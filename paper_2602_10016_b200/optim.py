@@ -113,7 +113,8 @@ class TrainStep:
             F.DW_STREAM = F.DW_STREAM_FWD = False
             if split:
                 m.layer_hook = None
-        F.dw_join(self.X.device)
+        if F.BRANCH_STREAMS:  # (single-stream steps issued nothing on the side streams)
+            F.dw_join(self.X.device)
         if self.reducer is not None:
             self.reducer.finish()
         if split:

@@ -176,3 +176,27 @@ def test_rote(tag):
     assert y.shape == z[f"{tag}:Y"].shape
     assert rel(y, z[f"{tag}:Y"]) < 1e-12
     assert rel(bwd(z[f"{tag}:cot"]), z[f"{tag}:dS"]) < 1e-12
+
+
+@pytest.mark.parametrize("T,w,causal,length", [(300, 17, False, 300), (300, 128, True, 257), (129, 0, False, 1),
+                                               (260, 200, False, 0)])
+def test_banded_mha_equals_dense(T, w, causal, length):
+    """The oracle's block-banded mha_window (used above T = 1024) is the dense
+    masked evaluation (the reference's own, attention.py:69-129) with the
+    exactly-masked entries skipped: outputs and VJPs agree to float64
+    rounding."""
+    from oracle import kunlun as K
+    from oracle import model as OM
+
+    spec = OM.ModelSpec(L=1, d=32, heads=4, n_ctx=2, events=[OM.EventSpec(T=T, w=w, budget=4, n_seeds=4, rank=1)])
+    p = OM.init_params(spec, seed=3)
+    rng = np.random.default_rng(T + w)
+    s = rng.normal(0, 1, (T, 32))
+    g = rng.normal(0, 1, (T, 32))
+    yd, bd = K.mha_window(s, p, "L0/ev0/mha", w, causal, length, banded=False)
+    yb, bb = K.mha_window(s, p, "L0/ev0/mha", w, causal, length, banded=True)
+    assert np.abs(yd - yb).max() <= 1e-12 * max(1.0, np.abs(yd).max())
+    (dd, gd), (db, gb) = bd(g), bb(g)
+    assert np.abs(dd - db).max() <= 1e-12 * max(1.0, np.abs(dd).max())
+    for k in gd:
+        assert np.abs(gd[k] - gb[k]).max() <= 1e-12 * max(1.0, np.abs(gd[k]).max()), k
