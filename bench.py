@@ -253,8 +253,8 @@ def graph_census(log, step, use_graph):
 NCU_KERNELS = {  # roofline family -> kernel-name substrings (CUPTI / ncu names)
     "gemm": ("gemm_tc_kernel", "gemm_simt_kernel", "splitk_reduce"),
     "swa_fwd": ("swa_fwd_tc", "swa_fwd_kernel"), "swa_bwd": ("swa_bwd_", "swa_rowdot"),
-    "gdpa_fwd": ("gdpa_fwd_kernel",), "gdpa_bwd": ("gdpa_bwd_kernel",), "hsp_fwd": ("hsp_fwd_kernel",),
-    "hsp_bwd": ("hsp_bwd_kernel",), "colsoftmax_fwd": ("colsoftmax_fwd_kernel",),
+    "gdpa_fwd": ("gdpa_fwd",), "gdpa_bwd": ("gdpa_bwd",), "hsp_fwd": ("hsp_fwd",),
+    "hsp_bwd": ("hsp_bwd",), "colsoftmax_fwd": ("colsoftmax_fwd_kernel",),
     "colsoftmax_bwd": ("colsoftmax_bwd_kernel",), "adam": ("adam_kernel",),
 }
 

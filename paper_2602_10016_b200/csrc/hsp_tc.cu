@@ -661,6 +661,469 @@ __global__ void __launch_bounds__(NT, 1)
   if (warp == 1) tc::tmem_dealloc(tmem, 512);
 }
 
+// ---------------------------------------------------------------------------
+// d = 512 (the c4 shape).  A 128 x 512 fp32 pooled accumulator alone fills
+// the 512 TMEM columns and a resident 128 x 512 query tile plus one S block
+// alone fill the shared memory, so the d = 512 kernels stream their operands
+// in 64-column atoms:
+//
+// Forward, persistent CTAs over (sample, query tile) items (sample-major, so
+// the query tiles of one sample run on neighbouring CTAs and share its S
+// blocks through L2), each item in two passes h over the 256-column halves of
+// the pooled output (Z recomputed per pass; the online softmax sees the same
+// Z both times, so both halves use identical P):
+//   warp 0     TMA: per S block, 8 (Qt atom, S atom) stages into a 4-slot
+//              ring (Z operands), then the block's half-h S atoms (the O
+//              operand) into one slot
+//   warp 1     MMA: Z_j = sum_a Qt_a S_a^T into a double-buffered TMEM Z
+//              (2 x 128 columns); O_h += P_j S_j[:, h] (N = 256, TMEM [256, 512))
+//   warps 2-5  softmax as the d <= 256 kernel; pass epilogue O_h / l -> bf16
+//              columns [256 h, 256 h + 256) of the pooled rows, LSE.
+constexpr int ZST = 4;                   // Z operand ring stages
+constexpr uint32_t ZSTAGE = 2 * ATOM;    // Qt atom + S atom
+
+__global__ void __launch_bounds__(NT, 1)
+    hsp_fwd512_kernel(const __grid_constant__ CUtensorMap tmS, const __grid_constant__ CUtensorMap tmQ, FwdP p) {
+  constexpr int D = 512, NA = 8, DH = 256;
+  constexpr uint32_t IDESC_Z = tc::idesc_bf16(TB, TB, 0, 0);
+  constexpr uint32_t IDESC_O = tc::idesc_bf16(TB, DH, 0, 1);
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sZ = sm;                       // ZST x (Qt atom | S atom)
+  uint8_t* sO = sZ + ZST * ZSTAGE;        // 4 S atoms (half h of block j)
+  uint8_t* sP = sO + 4 * ATOM;            // 128 x 128 bf16
+  uint64_t* bar = (uint64_t*)(sP + 2 * ATOM);
+  uint64_t* zs_full = bar;                // [ZST]
+  uint64_t* zs_empty = bar + ZST;         // [ZST]
+  uint64_t* os_full = bar + 2 * ZST;
+  uint64_t* os_empty = os_full + 1;
+  uint64_t* z_full = os_full + 2;         // [2]
+  uint64_t* z_empty = os_full + 4;        // [2]
+  uint64_t* p_full = os_full + 6;
+  uint64_t* p_empty = os_full + 7;
+  uint64_t* o_full = os_full + 8;
+  uint64_t* o_empty = os_full + 9;
+  uint32_t* tslot = (uint32_t*)(os_full + 10);
+
+  const int W = p.B * p.qtiles;
+  const int i0 = (int)((long long)W * blockIdx.x / gridDim.x);
+  const int i1 = (int)((long long)W * (blockIdx.x + 1) / gridDim.x);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    tc::prefetch_tmap(&tmS);
+    tc::prefetch_tmap(&tmQ);
+    for (int i = 0; i < ZST; ++i) {
+      tc::mbar_init(&zs_full[i], 1);
+      tc::mbar_init(&zs_empty[i], 1);
+    }
+    tc::mbar_init(os_full, 1);
+    tc::mbar_init(os_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&z_full[i], 1);
+      tc::mbar_init(&z_empty[i], 4);
+    }
+    tc::mbar_init(p_full, 4);
+    tc::mbar_init(p_empty, 1);
+    tc::mbar_init(o_full, 1);
+    tc::mbar_init(o_empty, 4);
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tslot, 512);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tslot;
+  KL_PDL_ENTRY();
+  const uint32_t T_O = 256;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int zc = 0, oc = 0;
+      for (int idx = i0; idx < i1; ++idx) {
+        const int b = idx / p.qtiles, qt = idx % p.qtiles;
+        const int nb = nblocks(p.lengths, b);
+        for (int h = 0; h < 2 && nb > 0; ++h) {
+          for (int j = 0; j < nb; ++j) {
+#pragma unroll 1
+            for (int a = 0; a < NA; ++a, ++zc) {
+              const int st = zc % ZST;
+              tc::mbar_wait(&zs_empty[st], ((zc / ZST) & 1) ^ 1);
+              tc::mbar_arrive_expect_tx(&zs_full[st], ZSTAGE);
+              tc::tma_load_3d(sZ + st * ZSTAGE, &tmQ, &zs_full[st], a * 64, qt * TB, 0);
+              tc::tma_load_3d(sZ + st * ZSTAGE + ATOM, &tmS, &zs_full[st], a * 64, j * TB, b);
+            }
+            tc::mbar_wait(os_empty, (oc & 1) ^ 1);
+            tc::mbar_arrive_expect_tx(os_full, 4 * ATOM);
+#pragma unroll
+            for (int a = 0; a < 4; ++a) tc::tma_load_3d(sO + a * ATOM, &tmS, os_full, (4 * h + a) * 64, j * TB, b);
+            ++oc;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int zc = 0, zb = 0, oc = 0, pc = 0, t = 0;
+      const uint32_t z0 = tc::smem_u32(sZ), oa = tc::smem_u32(sO), pa = tc::smem_u32(sP);
+      auto mma_z = [&]() {  // the next Z block into buffer zb & 1
+        const int z = zb & 1;
+        tc::mbar_wait(&z_empty[z], ((zb >> 1) & 1) ^ 1);
+        tc::fence_after();
+#pragma unroll 1
+        for (int a = 0; a < NA; ++a, ++zc) {
+          const int st = zc % ZST;
+          tc::mbar_wait(&zs_full[st], (zc / ZST) & 1);
+          tc::fence_after();
+          const uint32_t qa = z0 + st * ZSTAGE, sa = qa + ATOM;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            tc::mma_bf16(tmem + z * TB, dk(qa, kk), dk(sa, kk), IDESC_Z, (a | kk) > 0 ? 1u : 0u);
+          tc::mma_commit(&zs_empty[st]);
+        }
+        tc::mma_commit(&z_full[z]);
+        ++zb;
+      };
+      for (int idx = i0; idx < i1; ++idx) {
+        const int b = idx / p.qtiles;
+        const int nb = nblocks(p.lengths, b);
+        for (int h = 0; h < 2 && nb > 0; ++h) {
+          mma_z();
+          for (int j = 0; j < nb; ++j) {
+            if (j + 1 < nb) mma_z();
+            tc::mbar_wait(p_full, pc & 1);
+            if (j == 0) tc::mbar_wait(o_empty, (t & 1) ^ 1);  // the epilogue has read the previous O half
+            tc::mbar_wait(os_full, oc & 1);
+            tc::fence_after();
+#pragma unroll
+            for (int kk = 0; kk < TB / 16; ++kk)
+              tc::mma_bf16(tmem + T_O, dk(pa, kk), dmn(oa, kk), IDESC_O, (j | kk) > 0 ? 1u : 0u);
+            tc::mma_commit(p_empty);
+            tc::mma_commit(os_empty);
+            ++pc;
+            ++oc;
+          }
+          tc::mma_commit(o_full);
+          ++t;
+        }
+      }
+    }
+  } else {
+    const int qtr = warp & 3;
+    const int r = qtr * 32 + lane;
+    const uint32_t trow = tmem + ((uint32_t)(qtr * 32) << 16);
+    int zc = 0, pc = 0, t = 0;
+    for (int idx = i0; idx < i1; ++idx) {
+      const int b = idx / p.qtiles, qt = idx % p.qtiles;
+      const int len = p.lengths[b];
+      const int nb = nblocks(p.lengths, b);
+      const int q = qt * TB + r;
+      bf16* orow = nullptr;
+      if (q < p.HQ)
+        orow = q < p.n1 ? p.O1 + (long long)b * p.o1_bs + (long long)q * D
+                        : p.O2 + (long long)b * p.o2_bs + (long long)(q - p.n1) * D;
+      if (nb == 0) {  // empty sequence: pooled rows are zeros (seqsum.py:32-33, 99-100)
+        if (orow) {
+          const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll 4
+          for (int c = 0; c < D; c += 8) *reinterpret_cast<uint4*>(orow + c) = z4;
+          p.LSE[(long long)b * p.HQ + q] = INFINITY;
+        }
+        continue;
+      }
+      for (int h = 0; h < 2; ++h) {
+        float mref = -INFINITY, l = 0.f;
+        for (int j = 0; j < nb; ++j, ++zc, ++pc) {
+          const int z = zc & 1;
+          const uint32_t tz = trow + z * TB;
+          const int tv = len - j * TB;
+          tc::mbar_wait(&z_full[z], (zc >> 1) & 1);
+          tc::fence_after();
+          float mb = -INFINITY;
+#pragma unroll
+          for (int c0 = 0; c0 < TB; c0 += 32) {
+            float v[32];
+            tc::tmem_ld32(tz + c0, v);
+            if (c0 + 32 <= tv) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) mb = fmaxf(mb, v[i]);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; ++i)
+                if (c0 + i < tv) mb = fmaxf(mb, v[i]);
+            }
+          }
+          mb *= LOG2E;
+          tc::mbar_wait(p_empty, (pc & 1) ^ 1);
+          tc::fence_after();
+          const bool up = mb > mref + RESCALE;
+          if (j > 0 && __any_sync(0xffffffffu, up)) {
+            const float al = up ? ex2(mref - mb) : 1.f;
+            l *= al;
+#pragma unroll 1
+            for (int c0 = 0; c0 < DH; c0 += 16) {
+              float v[16];
+              uint32_t u[16];
+              tc::tmem_ld16(trow + T_O + c0, v);
+#pragma unroll
+              for (int i = 0; i < 16; ++i) u[i] = __float_as_uint(v[i] * al);
+              tc::tmem_st16(trow + T_O + c0, u);
+            }
+          }
+          if (up) mref = mb;
+#pragma unroll
+          for (int c0 = 0; c0 < TB; c0 += 32) {
+            float v[32];
+            uint32_t pk[16];
+            tc::tmem_ld32(tz + c0, v);
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) {
+              const float a = c0 + i < tv ? ex2(fmaf(v[i], LOG2E, -mref)) : 0.f;
+              const float bq = c0 + i + 1 < tv ? ex2(fmaf(v[i + 1], LOG2E, -mref)) : 0.f;
+              l += a + bq;
+              pk[i >> 1] = tc::pack_bf16(a, bq);
+            }
+            store_sw(sP, r, c0, pk);
+          }
+          tc::fence_async_smem();
+          tc::fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            tc::mbar_arrive(&z_empty[z]);
+            tc::mbar_arrive(p_full);
+          }
+        }
+        tc::mbar_wait(o_full, t & 1);
+        tc::fence_after();
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+#pragma unroll 1
+        for (int c0 = 0; c0 < DH; c0 += 32) {
+          float v[32];
+          tc::tmem_ld32(trow + T_O + c0, v);
+          if (orow) {
+            uint4* o = reinterpret_cast<uint4*>(orow + h * DH + c0);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              uint4 u;
+              u.x = tc::pack_bf16(v[8 * c + 0] * inv, v[8 * c + 1] * inv);
+              u.y = tc::pack_bf16(v[8 * c + 2] * inv, v[8 * c + 3] * inv);
+              u.z = tc::pack_bf16(v[8 * c + 4] * inv, v[8 * c + 5] * inv);
+              u.w = tc::pack_bf16(v[8 * c + 6] * inv, v[8 * c + 7] * inv);
+              o[c] = u;
+            }
+          }
+        }
+        if (orow && h == 1) p.LSE[(long long)b * p.HQ + q] = (mref + __log2f(l)) * 0.6931471805599453f;
+        tc::fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(o_empty);
+        ++t;
+      }
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tmem, 512);
+}
+
+size_t fwd512_smem() { return 1024 + ZST * ZSTAGE + 4 * ATOM + 2 * ATOM + (2 * ZST + 10) * 8 + 16; }
+
+// Backward (d = 512), persistent CTAs over (sample, 128-row S block) items,
+// looping over the query tiles; the S block stays resident (8 atoms) and the
+// query-tile operands stream through a 3-slot ring of (Qt atom, dO atom):
+//   MMA   Z = sum_a Qt_a S_a^T, dP = sum_a dO_a S_a^T   (TMEM 2 x (128 | 128))
+//   warps P = exp(Z - LSE) (t < len), dZ = P (dP - Dq): P and dZ (bf16) to the
+//         rows [0, HQ) and [HQ, 2 HQ) of PZ (B, 2 HQ, T), dZ's bf16 residual
+//         to dZ_lo (B, HQ, T).
+// The T-length products that need the whole pooled width — dS = P^T dO +
+// dZ^T Qt and dQ = sum_b dZ S — run as tcgen05 GEMMs on PZ (host).
+constexpr int GST = 3;
+constexpr uint32_t GSTAGE = 2 * ATOM;  // Qt atom + dO atom
+
+__global__ void __launch_bounds__(NT, 1)
+    hsp_bwd512_kernel(const __grid_constant__ CUtensorMap tmS, const __grid_constant__ CUtensorMap tmQ,
+                      const __grid_constant__ CUtensorMap tmG, BwdP p) {
+  constexpr int NA = 8;
+  constexpr uint32_t IDESC_Z = tc::idesc_bf16(TB, TB, 0, 0);
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sS = sm;                    // 8 atoms: the S block
+  uint8_t* sG = sS + NA * ATOM;        // GST x (Qt atom | dO atom)
+  uint64_t* bar = (uint64_t*)(sG + GST * GSTAGE);
+  uint64_t* s_full = bar;
+  uint64_t* s_empty = bar + 1;
+  uint64_t* gs_full = bar + 2;         // [GST]
+  uint64_t* gs_empty = gs_full + GST;  // [GST]
+  uint64_t* zd_full = gs_empty + GST;  // [2]
+  uint64_t* zd_empty = zd_full + 2;    // [2]
+  uint32_t* tslot = (uint32_t*)(zd_empty + 2);
+
+  const int W = p.B * p.tblocks;
+  const int i0 = (int)((long long)W * blockIdx.x / gridDim.x);
+  const int i1 = (int)((long long)W * (blockIdx.x + 1) / gridDim.x);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    tc::prefetch_tmap(&tmS);
+    tc::prefetch_tmap(&tmQ);
+    tc::prefetch_tmap(&tmG);
+    tc::mbar_init(s_full, 1);
+    tc::mbar_init(s_empty, 1);
+    for (int i = 0; i < GST; ++i) {
+      tc::mbar_init(&gs_full[i], 1);
+      tc::mbar_init(&gs_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&zd_full[i], 1);
+      tc::mbar_init(&zd_empty[i], 4);
+    }
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tslot, 512);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tslot;
+  KL_PDL_ENTRY();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int n = 0, gc = 0;
+      for (int idx = i0; idx < i1; ++idx) {
+        const int b = idx / p.tblocks, j = idx % p.tblocks;
+        if (j >= nblocks(p.lengths, b)) continue;
+        tc::mbar_wait(s_empty, (n & 1) ^ 1);
+        tc::mbar_arrive_expect_tx(s_full, NA * ATOM);
+#pragma unroll
+        for (int a = 0; a < NA; ++a) tc::tma_load_3d(sS + a * ATOM, &tmS, s_full, a * 64, j * TB, b);
+        ++n;
+        for (int qt = 0; qt < p.qtiles; ++qt) {
+#pragma unroll 1
+          for (int a = 0; a < NA; ++a, ++gc) {
+            const int st = gc % GST;
+            tc::mbar_wait(&gs_empty[st], ((gc / GST) & 1) ^ 1);
+            tc::mbar_arrive_expect_tx(&gs_full[st], GSTAGE);
+            tc::tma_load_3d(sG + st * GSTAGE, &tmQ, &gs_full[st], a * 64, qt * TB, 0);
+            tc::tma_load_3d(sG + st * GSTAGE + ATOM, &tmG, &gs_full[st], a * 64, qt * TB, b);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int n = 0, gc = 0, zc = 0;
+      const uint32_t sa0 = tc::smem_u32(sS), g0 = tc::smem_u32(sG);
+      for (int idx = i0; idx < i1; ++idx) {
+        const int b = idx / p.tblocks, j = idx % p.tblocks;
+        if (j >= nblocks(p.lengths, b)) continue;
+        tc::mbar_wait(s_full, n & 1);
+        for (int qt = 0; qt < p.qtiles; ++qt, ++zc) {
+          const int z = zc & 1;
+          tc::mbar_wait(&zd_empty[z], ((zc >> 1) & 1) ^ 1);
+          tc::fence_after();
+#pragma unroll 1
+          for (int a = 0; a < NA; ++a, ++gc) {
+            const int st = gc % GST;
+            tc::mbar_wait(&gs_full[st], (gc / GST) & 1);
+            tc::fence_after();
+            const uint32_t qa = g0 + st * GSTAGE, ga = qa + ATOM, sa = sa0 + a * ATOM;
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              const uint32_t acc = (a | kk) > 0 ? 1u : 0u;
+              tc::mma_bf16(tmem + z * 256, dk(qa, kk), dk(sa, kk), IDESC_Z, acc);
+              tc::mma_bf16(tmem + z * 256 + TB, dk(ga, kk), dk(sa, kk), IDESC_Z, acc);
+            }
+            tc::mma_commit(&gs_empty[st]);
+          }
+          tc::mma_commit(&zd_full[z]);
+        }
+        tc::mma_commit(s_empty);
+        ++n;
+      }
+    }
+  } else {
+    const int qtr = warp & 3;
+    const int r = qtr * 32 + lane;
+    const uint32_t trow = tmem + ((uint32_t)(qtr * 32) << 16);
+    const bool vec = (p.T & 7) == 0;
+    int zc = 0;
+    for (int idx = i0; idx < i1; ++idx) {
+      const int b = idx / p.tblocks, j = idx % p.tblocks;
+      const int len = p.lengths[b];
+      const int tv = len - j * TB;
+      const int t0 = j * TB;
+      const bool live_blk = j < nblocks(p.lengths, b);
+      for (int qt = 0; qt < p.qtiles; ++qt) {
+        const int q = qt * TB + r;
+        const bool qv = q < p.HQ;
+        bf16* pr = qv ? p.dZ + ((long long)b * 2 * p.HQ + q) * p.T + t0 : nullptr;            // P row
+        bf16* zr = qv ? p.dZ + ((long long)b * 2 * p.HQ + p.HQ + q) * p.T + t0 : nullptr;     // dZ row
+        bf16* lr = qv ? p.dZlo + ((long long)b * p.HQ + q) * p.T + t0 : nullptr;
+        const int cols = min(TB, p.T - t0);
+        if (!live_blk) {  // past the sequence: zero rows (the GEMMs read them)
+          if (qv) {
+            for (int c = 0; c < cols; ++c) pr[c] = zr[c] = lr[c] = __float2bfloat16(0.f);
+          }
+          continue;
+        }
+        const int z = zc & 1;
+        const float lse2 = qv ? p.LSE[(long long)b * p.HQ + q] * LOG2E : INFINITY;
+        const float dq = qv ? p.Dq[(long long)b * p.HQ + q] : 0.f;
+        tc::mbar_wait(&zd_full[z], (zc >> 1) & 1);
+        tc::fence_after();
+#pragma unroll 1
+        for (int c0 = 0; c0 < TB; c0 += 32) {
+          float v[32], g[32];
+          uint32_t pp[16], pk[16], lo[16];
+          tc::tmem_ld32(trow + z * 256 + c0, v);
+          tc::tmem_ld32(trow + z * 256 + TB + c0, g);
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            float pv[2], z2[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              pv[u] = c0 + i + u < tv ? ex2(fmaf(v[i + u], LOG2E, -lse2)) : 0.f;
+              z2[u] = pv[u] * (g[i + u] - dq);
+            }
+            pp[i >> 1] = tc::pack_bf16(pv[0], pv[1]);
+            pk[i >> 1] = tc::pack_bf16(z2[0], z2[1]);
+            const float2 hf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&pk[i >> 1]));
+            lo[i >> 1] = tc::pack_bf16(z2[0] - hf.x, z2[1] - hf.y);
+          }
+          if (qv && c0 < cols) {
+            if (vec && c0 + 32 <= cols) {
+#pragma unroll
+              for (int c = 0; c < 4; ++c) {
+                *reinterpret_cast<uint4*>(pr + c0 + 8 * c) = make_uint4(pp[4 * c], pp[4 * c + 1], pp[4 * c + 2], pp[4 * c + 3]);
+                *reinterpret_cast<uint4*>(zr + c0 + 8 * c) = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+                *reinterpret_cast<uint4*>(lr + c0 + 8 * c) = make_uint4(lo[4 * c], lo[4 * c + 1], lo[4 * c + 2], lo[4 * c + 3]);
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                if (c0 + i >= cols) continue;
+                const int sh = (i & 1) * 16;
+                reinterpret_cast<unsigned short*>(pr)[c0 + i] = (unsigned short)(pp[i >> 1] >> sh);
+                reinterpret_cast<unsigned short*>(zr)[c0 + i] = (unsigned short)(pk[i >> 1] >> sh);
+                reinterpret_cast<unsigned short*>(lr)[c0 + i] = (unsigned short)(lo[i >> 1] >> sh);
+              }
+            }
+          }
+        }
+        tc::fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&zd_empty[z]);
+        ++zc;
+      }
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tmem, 512);
+}
+
+size_t bwd512_smem() { return 1024 + 8 * ATOM + GST * GSTAGE + (2 + 2 * GST + 4) * 8 + 16; }
+
 template <int D>
 size_t bwd_smem() {
   return 1024 + 3 * (size_t)(D / 64) * ATOM + 2 * ATOM + 12 * 8;  // S, Qt, dO tiles, P/dZ, barriers
@@ -696,8 +1159,8 @@ extern "C" int kl_hsp_fwd(const kl_hsp_args* a, void* stream) {
     set_error("kl_hsp_fwd: bad extents");
     return KL_EBADSHAPE;
   }
-  if (a->dtype != KL_BF16 || (a->d != 128 && a->d != 256) || !kl_tcgen05_available()) {
-    set_error("kl_hsp_fwd: needs bf16, d in {128, 256} and an sm_100a device");
+  if (a->dtype != KL_BF16 || (a->d != 128 && a->d != 256 && a->d != 512) || !kl_tcgen05_available()) {
+    set_error("kl_hsp_fwd: needs bf16, d in {128, 256, 512} and an sm_100a device");
     return KL_EUNSUPPORTED;
   }
   if (a->B == 0) return KL_OK;
@@ -726,7 +1189,11 @@ extern "C" int kl_hsp_fwd(const kl_hsp_args* a, void* stream) {
   const int items = p.B * p.qtiles;
   int grid = std::min(items, tc_num_sms());
   if (const char* g = getenv("KL_HSP_GRID")) grid = std::max(1, std::min(grid, atoi(g)));  // testing
-  if (a->d == 256) {
+  if (a->d == 512) {
+    const size_t smem = hsp::fwd512_smem();
+    cudaFuncSetAttribute(hsp::hsp_fwd512_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    launch_k(hsp::hsp_fwd512_kernel, grid, hsp::NT, smem, s, tS, tQ, p);
+  } else if (a->d == 256) {
     const size_t smem = hsp::fwd_smem<256>();
     cudaFuncSetAttribute(hsp::hsp_fwd_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     launch_k(hsp::hsp_fwd_kernel<256>, grid, hsp::NT, smem, s, tS, tQ, p);
@@ -745,8 +1212,8 @@ extern "C" int kl_hsp_bwd(const kl_hsp_args* a, void* stream) {
     set_error("kl_hsp_bwd: bad extents");
     return KL_EBADSHAPE;
   }
-  if (a->dtype != KL_BF16 || (a->d != 128 && a->d != 256) || !kl_tcgen05_available()) {
-    set_error("kl_hsp_bwd: needs bf16, d in {128, 256} and an sm_100a device");
+  if (a->dtype != KL_BF16 || (a->d != 128 && a->d != 256 && a->d != 512) || !kl_tcgen05_available()) {
+    set_error("kl_hsp_bwd: needs bf16, d in {128, 256, 512} and an sm_100a device");
     return KL_EUNSUPPORTED;
   }
   if (!a->dO1 || !a->dS || !a->dZ || !a->dZ_lo || !a->LSE || !a->Dq) {
@@ -785,7 +1252,11 @@ extern "C" int kl_hsp_bwd(const kl_hsp_args* a, void* stream) {
   const int items = p.B * p.tblocks;
   int grid = std::min(items, tc_num_sms());
   if (const char* g = getenv("KL_HSP_GRID")) grid = std::max(1, std::min(grid, atoi(g)));  // testing
-  if (a->d == 256) {
+  if (a->d == 512) {  // P / dZ to dZ (B, 2 HQ, T), dZ's residual to dZ_lo; dS by the caller's GEMMs
+    const size_t smem = hsp::bwd512_smem();
+    cudaFuncSetAttribute(hsp::hsp_bwd512_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    launch_k(hsp::hsp_bwd512_kernel, grid, hsp::NT, smem, s, tS, tQ, tG, p);
+  } else if (a->d == 256) {
     const size_t smem = hsp::bwd_smem<256>();
     cudaFuncSetAttribute(hsp::hsp_bwd_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     launch_k(hsp::hsp_bwd_kernel<256>, grid, hsp::NT, smem, s, tS, tQ, tG, p);

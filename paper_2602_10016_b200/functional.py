@@ -677,7 +677,7 @@ HSP_FUSED = True  # tests flip this to A/B the fused tcgen05 pooling against the
 
 
 def _hsp_fused_ok(S, HQ, n_splits) -> bool:
-    return (HSP_FUSED and S.dtype == torch.bfloat16 and S.shape[-1] in (128, 256) and n_splits <= 2
+    return (HSP_FUSED and S.dtype == torch.bfloat16 and S.shape[-1] in (128, 256, 512) and n_splits <= 2
             and bool(_capi.lib().kl_tcgen05_available()))
 
 
@@ -707,6 +707,8 @@ def _hsp_fused_bwd(ctx, gs):
     Dq = torch.empty(B, HQ, device=S.device, dtype=torch.float32)  # rowsum(dO * pooled): the softmax-VJP term
     _capi.call("kl_rowdot", B * HQ, d, _capi.dt(dO), dO.data_ptr(), d, O.data_ptr(), d, Dq.data_ptr(), _stream())
     acc = ctx.sink.take(S) if ctx.sink is not None else None
+    if d == 512:
+        return _hsp_bwd512(S, Q, lengths, LSE, dO, Dq, acc, ctx)
     dS = acc if acc is not None else torch.empty_like(S)
     dZ = torch.empty(B, HQ, T, device=S.device, dtype=S.dtype)
     dZlo = torch.empty_like(dZ)
@@ -718,6 +720,34 @@ def _hsp_fused_bwd(ctx, gs):
     _capi.call("kl_hsp_bwd", C.byref(a), _stream())
     dQ = torch.zeros(1, 1, HQ, d, device=S.device, dtype=torch.float32)
     gemm(dZ.unsqueeze(0), S.unsqueeze(0), dQ, beta=1.0, reduce=(False, True))
+    gemm(dZlo.unsqueeze(0), S.unsqueeze(0), dQ, beta=1.0, reduce=(False, True))
+    return dS, dQ.reshape(Q.shape)
+
+
+def _hsp_bwd512(S, Q, lengths, LSE, dO, Dq, acc, ctx):
+    """d = 512: kl_hsp_bwd writes P and dZ (one pass over S, the score
+    products streamed through the kernel, hsp_bwd512_kernel) into PZ
+    (B, 2 HQ, T) and dZ's bf16 residual into dZ_lo; the whole-width T-length
+    products are tcgen05 GEMMs:
+        dS  = [P; dZ]^T [dO; Qt]            (one GEMM, K = 2 HQ; accumulates
+                                             into the shared sequence gradient)
+        dQ  = sum_b (dZ + dZ_lo) S          (batch-reduced, hi + lo)."""
+    B, T, d = S.shape
+    HQ = Q.shape[0]
+    PZ = torch.empty(B, 2 * HQ, T, device=S.device, dtype=S.dtype)
+    dZlo = torch.empty(B, HQ, T, device=S.device, dtype=S.dtype)
+    a = _hsp_args(S, Q, lengths, HQ, dO, dO, LSE)
+    a.dO1 = dO.data_ptr()
+    a.dS, a.ds_rs, a.ds_bs = S.data_ptr(), S.stride(1), S.stride(0)  # unused at d = 512
+    a.dZ, a.dZ_lo, a.Dq = PZ.data_ptr(), dZlo.data_ptr(), Dq.data_ptr()
+    _capi.call("kl_hsp_bwd", C.byref(a), _stream())
+    GQ = torch.cat([dO, Q.unsqueeze(0).expand(B, HQ, d)], dim=1)  # (B, 2 HQ, d)
+    if acc is not None:
+        dS = gemm(PZ.transpose(1, 2), GQ, acc, residual=acc)
+    else:
+        dS = gemm(PZ.transpose(1, 2), GQ)
+    dQ = torch.zeros(1, 1, HQ, d, device=S.device, dtype=torch.float32)
+    gemm(PZ[:, HQ:].unsqueeze(0), S.unsqueeze(0), dQ, beta=1.0, reduce=(False, True))
     gemm(dZlo.unsqueeze(0), S.unsqueeze(0), dQ, beta=1.0, reduce=(False, True))
     return dS, dQ.reshape(Q.shape)
 

@@ -39,8 +39,11 @@ def _lib():
     _capi.lib()
 
 
-def _spec(compskip, L=3):
-    return OM.ModelSpec(L=L, d=256, heads=4, n_ctx=16, n_sum=4, n_kv=16, experts=2, compskip=compskip,
+def _spec(compskip, shape="d256"):
+    if shape == "d512":  # the c4 widths (d = 512, H = 8, H*n_kv = 128), shorter sequences
+        return OM.ModelSpec(L=2, d=512, heads=8, n_ctx=16, n_sum=4, n_kv=16, experts=2, compskip=compskip,
+                            events=[OM.EventSpec(T=640, w=128, budget=32, n_seeds=32, rank=8)])
+    return OM.ModelSpec(L=3, d=256, heads=4, n_ctx=16, n_sum=4, n_kv=16, experts=2, compskip=compskip,
                         events=[OM.EventSpec(T=1024, w=128, budget=32, n_seeds=32, rank=8),
                                 OM.EventSpec(T=384, w=128, budget=8, n_seeds=8, rank=2)])
 
@@ -59,18 +62,19 @@ def _bf16(x):
     return torch.tensor(np.asarray(x)).to(torch.bfloat16).double().numpy()
 
 
-@pytest.mark.parametrize("compskip", [False, True])
-def test_model_bf16_tcgen05_path_vs_oracle(compskip):
+@pytest.mark.parametrize("compskip,shape", [(False, "d256"), (True, "d256"), (False, "d512")])
+def test_model_bf16_tcgen05_path_vs_oracle(compskip, shape):
     from paper_2602_10016_b200 import _capi
     from paper_2602_10016_b200 import functional as F
 
-    spec = _spec(compskip)
+    spec = _spec(compskip, shape)
     pnp = OM.init_params(spec, seed=21)
     model = _gpu_model(spec)
     model.P.load(pnp)
     rng = np.random.default_rng(7)
     B = 5
-    lengths = [np.array([1024, 1023, 129, 1, 0]), np.array([384, 0, 383, 129, 1])]
+    lengths = [np.array([ev.T, ev.T - 1, 129, 1, 0])[np.r_[0:5] if e == 0 else [0, 4, 1, 2, 3]]
+               for e, ev in enumerate(spec.events)]
     d = spec.d
     # the oracle sees exactly the bf16 inputs the device reads
     X = _bf16(rng.normal(0, 1 / np.sqrt(d), (B, spec.n_ctx, d)))
@@ -99,7 +103,10 @@ def test_model_bf16_tcgen05_path_vs_oracle(compskip):
     hits = _capi.path_hits()
 
     # --- the benchmarked kernels ran (and no fallback did)
-    for k in ("gdpa_fwd_tc", "gdpa_bwd_tc", "hsp_fwd_tc", "hsp_bwd_tc", "swa_fwd_tc", "swa_bwd_tc", "gemm_tc"):
+    fused = ("hsp_fwd_tc", "hsp_bwd_tc", "swa_fwd_tc", "swa_bwd_tc", "gemm_tc")
+    if spec.d <= 256:
+        fused += ("gdpa_fwd_tc", "gdpa_bwd_tc")
+    for k in fused:
         assert hits[k] > 0, (k, hits)
     for k in ("swa_fwd_simt", "swa_bwd_simt", "colsoftmax"):
         assert hits[k] == 0, (k, hits)

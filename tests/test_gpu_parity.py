@@ -406,11 +406,13 @@ def test_swa_tc_mask_bitexact_via_lse(T, w, causal):
 
 @pytest.mark.parametrize("dtype", DTYPES)
 @pytest.mark.parametrize("T,d,H,n_seeds", [(37, 32, 2, 6), (1, 32, 2, 6), (300, 128, 2, 40), (257, 256, 4, 32),
-                                           (130, 256, 4, 12)])
+                                           (130, 256, 4, 12), (300, 512, 8, 32), (1000, 512, 8, 12)])
 def test_hsp_vs_oracle(dtype, T, d, H, n_seeds):
-    """HSP + CLS pooling vs the oracle; d in {128, 256} in bf16 runs the fused
-    tcgen05 pooling kernels (kl_hsp_fwd / kl_hsp_bwd), with query tiles that
-    straddle the seed / CLS boundary and a partial second tile."""
+    """HSP + CLS pooling vs the oracle; d in {128, 256, 512} in bf16 runs the
+    fused tcgen05 pooling kernels (kl_hsp_fwd / kl_hsp_bwd; d = 512 streams
+    its operands and forms dS / dQ with GEMMs), with query tiles that straddle
+    the seed / CLS boundary and a partial second tile — asserted through the
+    kernel-path counters."""
     from paper_2602_10016_b200 import functional as F
     from paper_2602_10016_b200 import seqsum as Q
     from paper_2602_10016_b200.tensor import Params
@@ -428,9 +430,15 @@ def test_hsp_vs_oracle(dtype, T, d, H, n_seeds):
     if dtype == torch.bfloat16:
         S = _round(S, dtype)
     S_t = dev(S, grad=True)
+    from paper_2602_10016_b200 import _capi
+
+    _capi.reset_path_hits()
     rows = Q.hsp_summarize(F.cast(S_t, dtype), sp, lengths).rows()
     P.zero_grad()
     (F.cast(rows, torch.float32) * dev(R)).sum().backward()
+    hits = _capi.path_hits()
+    fused = dtype == torch.bfloat16 and d in (128, 256, 512)
+    assert (hits["hsp_fwd_tc"] > 0 and hits["hsp_bwd_tc"] > 0 and hits["colsoftmax"] == 0) == fused, hits
     tol = TOL[dtype]
     grads = {}
     for b in range(B):
