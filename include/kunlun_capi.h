@@ -163,8 +163,15 @@ typedef struct kl_gdpa_args {
   void* dVt;
   /* debug: if non-NULL, 32 x 16 clock64 stamps of CTA 0's pipeline stages */
   unsigned long long* trace;
+  /* d = 512 (HK = 128) backward: the kernel writes dZ and A = Act(Z) as
+   * (B, T, HK) bf16 here (rows >= length zero) and the caller forms
+   * dKt = dZ^T S, dVt = A^T dY with GEMMs; dKt / dVt are not written. */
+  void* dZ_out;
+  void* A_out;
 } kl_gdpa_args;
 
+/* bf16; (HK = 64, d in {128, 256}) or (HK = 128, d = 512); per-16-column
+ * activation codes from {identity, relu, silu, tanh}. */
 int kl_gdpa_fwd(const kl_gdpa_args* args, void* stream);
 int kl_gdpa_bwd(const kl_gdpa_args* args, void* stream);
 

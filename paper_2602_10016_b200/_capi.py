@@ -78,6 +78,7 @@ class GdpaArgs(C.Structure):
         ("Kt", C.c_void_p), ("Vt", C.c_void_p), ("Y", C.c_void_p),
         ("dY", C.c_void_p), ("dS", C.c_void_p), ("dKt", C.c_void_p), ("dVt", C.c_void_p),
         ("trace", C.c_void_p),
+        ("dZ_out", C.c_void_p), ("A_out", C.c_void_p),
     ]
 
 

@@ -32,6 +32,8 @@
 // Traffic per row: read S, dY; write dS (6*d bytes) + 2*HK*d*2 per sample.
 #include <cudaTypedefs.h>
 
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "common.cuh"
@@ -629,6 +631,448 @@ __global__ void __launch_bounds__(NT, 1)
   if (warp == 1) tc::tmem_dealloc(tmem, 512);
 }
 
+// ---------------------------------------------------------------------------
+// d = 512 (the c4 shape, H*n_kv = HK2 = 128).  A resident 128 x 512 S tile
+// plus the 128 x 512 Kt / Vt of a sample would need ~384 KB of shared
+// memory, and a 128 x 512 fp32 output accumulator fills TMEM, so these
+// kernels stream the K = d contractions in 64-column atoms and produce the
+// d-wide results in two 256-column halves:
+//
+// Forward, persistent CTAs over (sample, 128-row tile) items:
+//   warp 0     TMA: 8 (S atom, Kt atom) stages per tile into a 4-slot ring,
+//              then each half of Vt (4 atoms, MN-major B operand) into a slot
+//   warp 1     MMA: Z = sum_a S_a Kt_a^T (double-buffered, 2 x 128 TMEM
+//              columns), Y_h = A Vt[:, h] (N = 256, TMEM [256, 512))
+//   warps 2-9  Z -> Act (per 16-column head group) -> bf16 A tile in smem;
+//              Y_h + S[:, h] (residual read from global / L2) -> bf16 rows.
+// Backward, persistent CTAs over the same items:
+//   MMA   dA = sum_a dY_a Vt_a^T, Z = sum_a S_a Kt_a^T (one 2-slot ring of
+//         (dY, Vt, S, Kt) atoms); dS_h = dZ Kt[:, h] (N = 256)
+//   warps dZ = dA Act'(Z) / tau, A = Act(Z): both to HBM (the caller's
+//         dKt = dZ^T S and dVt = A^T dY GEMMs), dZ also to smem; dS_h + dY
+//         -> bf16 rows.
+constexpr int HK2 = 128;
+constexpr int NT5 = 320;                       // warp 0 TMA, 1 MMA, 2-9 epilogue
+constexpr int RST = 4;                         // forward ring stages
+constexpr uint32_t FSTAGE = 2 * ATOM_S;        // S atom | Kt atom (128 rows x 64)
+constexpr uint32_t BSTAGE = 4 * ATOM_S;        // dY | Vt | S | Kt atoms
+
+struct P5 {
+  int B, T;
+  bf16* out;            // Y (fwd) or dS (bwd): (B, T, 512), rows o_rs apart
+  long long o_rs, o_bs;
+  const bf16* res;      // residual: S (fwd) or dY (bwd), same layout
+  long long r_rs, r_bs;
+  float inv_tau;
+  const int* lengths;
+  unsigned char code[HK2];
+  bf16* dZ;             // bwd: (B, T, HK2)
+  bf16* A;
+};
+
+// Act over this thread's 64 Z columns [c0, c0 + 64): four 16-column head groups.
+template <bool BWD>
+__device__ __forceinline__ void act_cols64(const unsigned char* code, int c0, const float* z, const float* g,
+                                           float s, float* y, float* dy) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    act_run<16, BWD>(code[c0 + 16 * q], z + 16 * q, BWD ? g + 16 * q : nullptr, s, y + 16 * q,
+                     BWD ? dy + 16 * q : nullptr);
+}
+
+// 32 fp32 accumulator columns + 32 bf16 residual columns -> 32 bf16 outputs of row `row`.
+__device__ __forceinline__ void add_res_store32(const float* v, const bf16* res, bf16* out) {
+  const uint4* rp = reinterpret_cast<const uint4*>(res);
+  uint4* op = reinterpret_cast<uint4*>(out);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const uint4 u = rp[c];
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[i]));
+      o[i] = tc::pack_bf16(v[8 * c + 2 * i] + f.x, v[8 * c + 2 * i + 1] + f.y);
+    }
+    op[c] = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+__global__ void __launch_bounds__(NT5, 1)
+    gdpa_fwd512_kernel(const __grid_constant__ CUtensorMap ts, const __grid_constant__ CUtensorMap tk,
+                       const __grid_constant__ CUtensorMap tv, const P5 p) {
+  constexpr uint32_t IDESC_Z = tc::idesc_bf16(TB, HK2, 0, 0);
+  constexpr uint32_t IDESC_Y = tc::idesc_bf16(TB, 256, 0, 1);
+  constexpr uint32_t T_Y = 256;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sR = align1k(smem_raw);          // RST x (S atom | Kt atom)
+  uint8_t* sV = sR + RST * FSTAGE;          // Vt half: 4 atoms
+  uint8_t* sA = sV + 4 * ATOM_S;            // 128 x 128 bf16 (2 atoms)
+  uint64_t* bar = (uint64_t*)(sA + 2 * ATOM_S);
+  uint64_t* rs_full = bar;                  // [RST]
+  uint64_t* rs_empty = bar + RST;           // [RST]
+  uint64_t* vs_full = bar + 2 * RST;
+  uint64_t* vs_empty = vs_full + 1;
+  uint64_t* z_full = vs_full + 2;           // [2]
+  uint64_t* z_empty = vs_full + 4;          // [2]
+  uint64_t* a_full = vs_full + 6;
+  uint64_t* a_empty = vs_full + 7;
+  uint64_t* y_full = vs_full + 8;
+  uint64_t* y_empty = vs_full + 9;
+  uint32_t* tslot = (uint32_t*)(vs_full + 10);
+
+  const int nT = (p.T + TB - 1) / TB;
+  const int W = p.B * nT;
+  const int i0 = (int)((long long)W * blockIdx.x / gridDim.x);
+  const int i1 = (int)((long long)W * (blockIdx.x + 1) / gridDim.x);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __shared__ unsigned char code[HK2];
+  if (threadIdx.x < HK2) code[threadIdx.x] = p.code[threadIdx.x];
+
+  if (warp == 0 && lane == 0) {
+    tc::prefetch_tmap(&ts);
+    tc::prefetch_tmap(&tk);
+    tc::prefetch_tmap(&tv);
+    for (int i = 0; i < RST; ++i) {
+      tc::mbar_init(&rs_full[i], 1);
+      tc::mbar_init(&rs_empty[i], 1);
+    }
+    tc::mbar_init(vs_full, 1);
+    tc::mbar_init(vs_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&z_full[i], 1);
+      tc::mbar_init(&z_empty[i], 8);
+    }
+    tc::mbar_init(a_full, 8);
+    tc::mbar_init(a_empty, 1);
+    tc::mbar_init(y_full, 1);
+    tc::mbar_init(y_empty, 8);
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tslot, 512);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tslot;
+  KL_PDL_ENTRY();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // Load order (matches the MMA issue order, which computes the next
+      // tile's Z before this tile's Y halves): Z stages of the first tile;
+      // then per tile k: Vt half 0 of k, Z stages of k + 1, Vt half 1 of k.
+      int rc = 0, vc = 0;
+      auto load_z = [&](int k) {
+        const int b = k / nT, q0 = (k % nT) * TB;
+#pragma unroll 1
+        for (int a = 0; a < 8; ++a, ++rc) {
+          const int st = rc % RST;
+          tc::mbar_wait(&rs_empty[st], ((rc / RST) & 1) ^ 1);
+          tc::mbar_arrive_expect_tx(&rs_full[st], FSTAGE);
+          tc::tma_load_3d(sR + st * FSTAGE, &ts, &rs_full[st], a * 64, q0, b);
+          tc::tma_load_3d(sR + st * FSTAGE + ATOM_S, &tk, &rs_full[st], a * 64, 0, b);
+        }
+      };
+      auto load_v = [&](int k, int h) {
+        const int b = k / nT;
+        tc::mbar_wait(vs_empty, (vc & 1) ^ 1);
+        tc::mbar_arrive_expect_tx(vs_full, 4 * ATOM_S);
+#pragma unroll
+        for (int a = 0; a < 4; ++a) tc::tma_load_3d(sV + a * ATOM_S, &tv, vs_full, (4 * h + a) * 64, 0, b);
+        ++vc;
+      };
+      if (i0 < i1) load_z(i0);
+      for (int k = i0; k < i1; ++k) {
+        load_v(k, 0);
+        if (k + 1 < i1) load_z(k + 1);
+        load_v(k, 1);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int rc = 0, zc = 0, vc = 0, yc = 0, ac = 0;
+      const uint32_t r0 = tc::smem_u32(sR), va = tc::smem_u32(sV), aa = tc::smem_u32(sA);
+      auto mma_z = [&]() {
+        const int z = zc & 1;
+        tc::mbar_wait(&z_empty[z], ((zc >> 1) & 1) ^ 1);
+        tc::fence_after();
+#pragma unroll 1
+        for (int a = 0; a < 8; ++a, ++rc) {
+          const int st = rc % RST;
+          tc::mbar_wait(&rs_full[st], (rc / RST) & 1);
+          tc::fence_after();
+          const uint32_t sa = r0 + st * FSTAGE, ka = sa + ATOM_S;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            tc::mma_bf16(tmem + z * HK2, dk(sa, kk, ATOM_S), dk(ka, kk, ATOM_S), IDESC_Z, (a | kk) > 0 ? 1u : 0u);
+          tc::mma_commit(&rs_empty[st]);
+        }
+        tc::mma_commit(&z_full[z]);
+        ++zc;
+      };
+      if (i0 < i1) mma_z();
+      for (int k = i0; k < i1; ++k) {
+        if (k + 1 < i1) mma_z();  // the next tile's Z runs while this tile's Y drains
+        tc::mbar_wait(a_full, ac & 1);
+        for (int h = 0; h < 2; ++h, ++yc, ++vc) {
+          tc::mbar_wait(y_empty, (yc & 1) ^ 1);
+          tc::mbar_wait(vs_full, vc & 1);
+          tc::fence_after();
+#pragma unroll
+          for (int kk = 0; kk < HK2 / 16; ++kk)
+            tc::mma_bf16(tmem + T_Y, dk(aa, kk, ATOM_S), dmn(va, kk, ATOM_S), IDESC_Y, kk > 0 ? 1u : 0u);
+          tc::mma_commit(y_full);
+          tc::mma_commit(vs_empty);
+        }
+        tc::mma_commit(a_empty);
+        ++ac;
+      }
+    }
+  } else {
+    const int qtr = warp & 3, hf = (warp - 2) >> 2;
+    const int r = qtr * 32 + lane;
+    const uint32_t trow = tmem + ((uint32_t)(qtr * 32) << 16);
+    int zc = 0, yc = 0, ac = 0;
+    for (int k = i0; k < i1; ++k) {
+      const int b = k / nT, q0 = (k % nT) * TB;
+      int len = __ldg(&p.lengths[b]);
+      asm volatile("" : "+r"(len));
+      const bool live = q0 + r < len, inb = q0 + r < p.T;
+      const int z = zc & 1;
+      tc::mbar_wait(&z_full[z], (zc >> 1) & 1);
+      tc::fence_after();
+      float v[64];
+      tc::tmem_ld32(trow + z * HK2 + hf * 64, v);
+      tc::tmem_ld32(trow + z * HK2 + hf * 64 + 32, v + 32);
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&z_empty[z]);
+      ++zc;
+      uint32_t pk[32];
+      {
+        float y[64];
+        act_cols64<false>(code, hf * 64, v, nullptr, p.inv_tau, y, nullptr);
+#pragma unroll
+        for (int i = 0; i < 64; i += 2) pk[i >> 1] = live ? tc::pack_bf16(y[i], y[i + 1]) : 0u;
+      }
+      tc::mbar_wait(a_empty, (ac & 1) ^ 1);
+#pragma unroll
+      for (int g = 0; g < 4; ++g) store_sw16(sA, r, hf * 64 + 16 * g, pk + 8 * g);
+      tc::fence_async_smem();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(a_full);
+      ++ac;
+      const bf16* rrow = p.res + (long long)b * p.r_bs + (long long)(q0 + r) * p.r_rs;
+      bf16* orow = p.out + (long long)b * p.o_bs + (long long)(q0 + r) * p.o_rs;
+      for (int h = 0; h < 2; ++h, ++yc) {
+        tc::mbar_wait(y_full, yc & 1);
+        tc::fence_after();
+#pragma unroll 1
+        for (int cc = 0; cc < 128; cc += 32) {
+          float acc[32];
+          tc::tmem_ld32(trow + T_Y + hf * 128 + cc, acc);
+          const int col = h * 256 + hf * 128 + cc;
+          if (inb) add_res_store32(acc, rrow + col, orow + col);
+        }
+        tc::fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(y_empty);
+      }
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tmem, 512);
+}
+
+size_t fwd512_smem() { return 1024 + RST * FSTAGE + 4 * ATOM_S + 2 * ATOM_S + (2 * RST + 10) * 8 + 16; }
+
+__global__ void __launch_bounds__(NT5, 1)
+    gdpa_bwd512_kernel(const __grid_constant__ CUtensorMap ts, const __grid_constant__ CUtensorMap tg,
+                       const __grid_constant__ CUtensorMap tk, const __grid_constant__ CUtensorMap tv,
+                       const P5 p) {
+  constexpr uint32_t IDESC_Z = tc::idesc_bf16(TB, HK2, 0, 0);
+  constexpr uint32_t IDESC_DS = tc::idesc_bf16(TB, 256, 0, 1);
+  constexpr uint32_t T_DA = 0, T_Z = 128, T_DS = 256;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sR = align1k(smem_raw);          // 2 x (dY | Vt | S | Kt atoms)
+  uint8_t* sK = sR + 2 * BSTAGE;            // Kt half: 4 atoms (MN-major B of dS = dZ Kt)
+  uint8_t* sD = sK + 4 * ATOM_S;            // dZ tile 128 x 128 bf16
+  uint64_t* bar = (uint64_t*)(sD + 2 * ATOM_S);
+  uint64_t* rs_full = bar;                  // [2]
+  uint64_t* rs_empty = bar + 2;             // [2]
+  uint64_t* ks_full = bar + 4;
+  uint64_t* ks_empty = bar + 5;
+  uint64_t* zz_full = bar + 6;
+  uint64_t* zz_empty = bar + 7;
+  uint64_t* d_full = bar + 8;
+  uint64_t* d_empty = bar + 9;
+  uint64_t* s_full = bar + 10;
+  uint64_t* s_empty = bar + 11;
+  uint32_t* tslot = (uint32_t*)(bar + 12);
+
+  const int nT = (p.T + TB - 1) / TB;
+  const int W = p.B * nT;
+  const int i0 = (int)((long long)W * blockIdx.x / gridDim.x);
+  const int i1 = (int)((long long)W * (blockIdx.x + 1) / gridDim.x);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __shared__ unsigned char code[HK2];
+  if (threadIdx.x < HK2) code[threadIdx.x] = p.code[threadIdx.x];
+
+  if (warp == 0 && lane == 0) {
+    tc::prefetch_tmap(&ts);
+    tc::prefetch_tmap(&tg);
+    tc::prefetch_tmap(&tk);
+    tc::prefetch_tmap(&tv);
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&rs_full[i], 1);
+      tc::mbar_init(&rs_empty[i], 1);
+    }
+    tc::mbar_init(ks_full, 1);
+    tc::mbar_init(ks_empty, 1);
+    tc::mbar_init(zz_full, 1);
+    tc::mbar_init(zz_empty, 8);
+    tc::mbar_init(d_full, 8);
+    tc::mbar_init(d_empty, 1);
+    tc::mbar_init(s_full, 1);
+    tc::mbar_init(s_empty, 8);
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tslot, 512);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tslot;
+  KL_PDL_ENTRY();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int rc = 0, kc = 0;
+      for (int k = i0; k < i1; ++k) {
+        const int b = k / nT, q0 = (k % nT) * TB;
+#pragma unroll 1
+        for (int a = 0; a < 8; ++a, ++rc) {
+          const int st = rc & 1;
+          uint8_t* d = sR + st * BSTAGE;
+          tc::mbar_wait(&rs_empty[st], ((rc >> 1) & 1) ^ 1);
+          tc::mbar_arrive_expect_tx(&rs_full[st], BSTAGE);
+          tc::tma_load_3d(d, &tg, &rs_full[st], a * 64, q0, b);
+          tc::tma_load_3d(d + ATOM_S, &tv, &rs_full[st], a * 64, 0, b);
+          tc::tma_load_3d(d + 2 * ATOM_S, &ts, &rs_full[st], a * 64, q0, b);
+          tc::tma_load_3d(d + 3 * ATOM_S, &tk, &rs_full[st], a * 64, 0, b);
+        }
+        for (int h = 0; h < 2; ++h, ++kc) {
+          tc::mbar_wait(ks_empty, (kc & 1) ^ 1);
+          tc::mbar_arrive_expect_tx(ks_full, 4 * ATOM_S);
+#pragma unroll
+          for (int a = 0; a < 4; ++a) tc::tma_load_3d(sK + a * ATOM_S, &tk, ks_full, (4 * h + a) * 64, 0, b);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int rc = 0, kc = 0, sc = 0, c = 0;
+      const uint32_t r0 = tc::smem_u32(sR), ka0 = tc::smem_u32(sK), da = tc::smem_u32(sD);
+      for (int k = i0; k < i1; ++k, ++c) {
+        tc::mbar_wait(zz_empty, (c & 1) ^ 1);
+        tc::fence_after();
+#pragma unroll 1
+        for (int a = 0; a < 8; ++a, ++rc) {
+          const int st = rc & 1;
+          tc::mbar_wait(&rs_full[st], (rc >> 1) & 1);
+          tc::fence_after();
+          const uint32_t ga = r0 + st * BSTAGE, vva = ga + ATOM_S, sa = ga + 2 * ATOM_S, kta = ga + 3 * ATOM_S;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint32_t acc = (a | kk) > 0 ? 1u : 0u;
+            tc::mma_bf16(tmem + T_DA, dk(ga, kk, ATOM_S), dk(vva, kk, ATOM_S), IDESC_Z, acc);
+            tc::mma_bf16(tmem + T_Z, dk(sa, kk, ATOM_S), dk(kta, kk, ATOM_S), IDESC_Z, acc);
+          }
+          tc::mma_commit(&rs_empty[st]);
+        }
+        tc::mma_commit(zz_full);
+        tc::mbar_wait(d_full, c & 1);
+        for (int h = 0; h < 2; ++h, ++sc, ++kc) {
+          tc::mbar_wait(s_empty, (sc & 1) ^ 1);
+          tc::mbar_wait(ks_full, kc & 1);
+          tc::fence_after();
+#pragma unroll
+          for (int kk = 0; kk < HK2 / 16; ++kk)
+            tc::mma_bf16(tmem + T_DS, dk(da, kk, ATOM_S), dmn(ka0, kk, ATOM_S), IDESC_DS, kk > 0 ? 1u : 0u);
+          tc::mma_commit(s_full);
+          tc::mma_commit(ks_empty);
+        }
+        tc::mma_commit(d_empty);
+      }
+    }
+  } else {
+    const int qtr = warp & 3, hf = (warp - 2) >> 2;
+    const int r = qtr * 32 + lane;
+    const uint32_t trow = tmem + ((uint32_t)(qtr * 32) << 16);
+    int c = 0, sc = 0;
+    for (int k = i0; k < i1; ++k, ++c) {
+      const int b = k / nT, q0 = (k % nT) * TB;
+      int len = __ldg(&p.lengths[b]);
+      asm volatile("" : "+r"(len));
+      const bool live = q0 + r < len, inb = q0 + r < p.T;
+      tc::mbar_wait(zz_full, c & 1);
+      tc::fence_after();
+      uint32_t pdz[32], pa[32];
+#pragma unroll
+      for (int hc = 0; hc < 2; ++hc) {  // two 32-column chunks (two head groups each)
+        float da[32], z[32], y[32], dy[32];
+        tc::tmem_ld32(trow + T_DA + hf * 64 + 32 * hc, da);
+        tc::tmem_ld32(trow + T_Z + hf * 64 + 32 * hc, z);
+        act_cols32<true>(code, hf * 64 + 32 * hc, true, z, da, p.inv_tau, y, dy);
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          pdz[16 * hc + (i >> 1)] = live ? tc::pack_bf16(dy[i], dy[i + 1]) : 0u;
+          pa[16 * hc + (i >> 1)] = live ? tc::pack_bf16(y[i], y[i + 1]) : 0u;
+        }
+      }
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(zz_empty);
+      if (inb) {  // dZ and A rows -> HBM (the dKt / dVt GEMMs' operands)
+        uint4* zo = reinterpret_cast<uint4*>(p.dZ + ((long long)b * p.T + q0 + r) * HK2 + hf * 64);
+        uint4* ao = reinterpret_cast<uint4*>(p.A + ((long long)b * p.T + q0 + r) * HK2 + hf * 64);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          zo[q] = make_uint4(pdz[4 * q], pdz[4 * q + 1], pdz[4 * q + 2], pdz[4 * q + 3]);
+          ao[q] = make_uint4(pa[4 * q], pa[4 * q + 1], pa[4 * q + 2], pa[4 * q + 3]);
+        }
+      }
+      tc::mbar_wait(d_empty, (c & 1) ^ 1);
+#pragma unroll
+      for (int g = 0; g < 4; ++g) store_sw16(sD, r, hf * 64 + 16 * g, pdz + 8 * g);
+      tc::fence_async_smem();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(d_full);
+      const bf16* rrow = p.res + (long long)b * p.r_bs + (long long)(q0 + r) * p.r_rs;
+      bf16* orow = p.out + (long long)b * p.o_bs + (long long)(q0 + r) * p.o_rs;
+      for (int h = 0; h < 2; ++h, ++sc) {
+        tc::mbar_wait(s_full, sc & 1);
+        tc::fence_after();
+#pragma unroll 1
+        for (int cc = 0; cc < 128; cc += 32) {
+          float acc[32];
+          tc::tmem_ld32(trow + T_DS + hf * 128 + cc, acc);
+          const int col = h * 256 + hf * 128 + cc;
+          if (inb) add_res_store32(acc, rrow + col, orow + col);
+        }
+        tc::fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(s_empty);
+      }
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tmem, 512);
+}
+
+size_t bwd512_smem() { return 1024 + 2 * BSTAGE + 4 * ATOM_S + 2 * ATOM_S + 12 * 8 + 16; }
+
 static int last_rc = 0;
 bool map3(CUtensorMap* m, const void* ptr, long long inner, long long rows, long long B, long long ld, long long bs,
           int box_rows) {
@@ -668,9 +1112,10 @@ static int gdpa_prepare(const kl_gdpa_args* a, const char* who, gdpa::P& p, void
     set_error("%s: lengths, S, Kt and Vt are required", who);
     return KL_EBADSHAPE;
   }
-  if (a->dtype != KL_BF16 || a->HK != gdpa::HK || (a->d != 128 && a->d != 256) || !kl_tcgen05_available()) {
-    set_error("%s: fused path takes bf16, HK=%d, d in {128,256} on sm_100 (got dtype=%d HK=%d d=%d)", who,
-              gdpa::HK, a->dtype, a->HK, a->d);
+  const bool shape_ok = (a->HK == gdpa::HK && (a->d == 128 || a->d == 256)) || (a->HK == gdpa::HK2 && a->d == 512);
+  if (a->dtype != KL_BF16 || !shape_ok || !kl_tcgen05_available()) {
+    set_error("%s: fused path takes bf16 with (HK=64, d in {128,256}) or (HK=128, d=512) on sm_100 "
+              "(got dtype=%d HK=%d d=%d)", who, a->dtype, a->HK, a->d);
     return KL_EUNSUPPORTED;
   }
   if (a->n_act < 0 || a->n_act > KL_MAX_ACT_GROUPS) {
@@ -681,14 +1126,16 @@ static int gdpa_prepare(const kl_gdpa_args* a, const char* who, gdpa::P& p, void
   p.T = a->T;
   p.inv_tau = a->inv_tau;
   p.lengths = a->lengths;
-  for (int j = 0; j < gdpa::HK; ++j) {
+  unsigned char codes[gdpa::HK2];
+  for (int j = 0; j < a->HK; ++j) {
     const int h = j / a->n_kv;
-    p.code[j] = (unsigned char)(a->n_act ? a->act_codes[h % a->n_act] : KL_ACT_IDENTITY);
+    codes[j] = (unsigned char)(a->n_act ? a->act_codes[h % a->n_act] : KL_ACT_IDENTITY);
+    if (j < gdpa::HK) p.code[j] = codes[j];
   }
   p.uniform16 = 1;
-  for (int j = 0; j < gdpa::HK; ++j) {
-    if (p.code[j] != p.code[j & ~15]) p.uniform16 = 0;
-    const int c = p.code[j];
+  for (int j = 0; j < a->HK; ++j) {
+    if (codes[j] != codes[j & ~15]) p.uniform16 = 0;
+    const int c = codes[j];
     if (c != KL_ACT_IDENTITY && c != KL_ACT_RELU && c != KL_ACT_SILU && c != KL_ACT_TANH) {
       set_error("%s: fused path takes identity/relu/silu/tanh heads (got code %d)", who, c);
       return KL_EUNSUPPORTED;
@@ -754,6 +1201,83 @@ static int gdpa_bwd_launch(const kl_gdpa_args* a, const gdpa::P& p, cudaStream_t
   return launch_check("gdpa_bwd_tc");
 }
 
+static gdpa::P5 p5_of(const kl_gdpa_args* a, const gdpa::P& p) {
+  gdpa::P5 q{};
+  q.B = a->B;
+  q.T = a->T;
+  q.inv_tau = a->inv_tau;
+  q.lengths = a->lengths;
+  for (int j = 0; j < gdpa::HK2; ++j) {
+    const int h = j / a->n_kv;
+    q.code[j] = (unsigned char)(a->n_act ? a->act_codes[h % a->n_act] : KL_ACT_IDENTITY);
+  }
+  q.o_rs = q.r_rs = a->s_rs;
+  q.o_bs = q.r_bs = a->s_bs;
+  return q;
+}
+
+static int gdpa_fwd512_launch(const kl_gdpa_args* a, const gdpa::P& p, cudaStream_t s) {
+  CUtensorMap ts, tk, tv;
+  const long long kvbs = (long long)gdpa::HK2 * 512;
+  if (!gdpa::map3(&ts, a->S, 512, a->T, a->B, a->s_rs, a->s_bs, gdpa::TB) ||
+      !gdpa::map3(&tk, a->Kt, 512, gdpa::HK2, a->B, 512, kvbs, gdpa::HK2) ||
+      !gdpa::map3(&tv, a->Vt, 512, gdpa::HK2, a->B, 512, kvbs, gdpa::HK2)) {
+    set_error("kl_gdpa_fwd: tensor map encode failed (alignment?)");
+    return KL_EUNSUPPORTED;
+  }
+  if ((a->s_rs % 8) || (a->s_bs % 8) || ((uintptr_t)a->S & 15) || ((uintptr_t)a->Y & 15)) {
+    set_error("kl_gdpa_fwd: S / Y rows must be 16-byte aligned");
+    return KL_EUNSUPPORTED;
+  }
+  gdpa::P5 q = p5_of(a, p);
+  q.out = (bf16*)a->Y;
+  q.res = (const bf16*)a->S;
+  const size_t smem = gdpa::fwd512_smem();
+  cudaFuncSetAttribute(gdpa::gdpa_fwd512_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int W = a->B * ((a->T + gdpa::TB - 1) / gdpa::TB);
+  int grid = std::min(W, tc_num_sms());
+  if (const char* g = getenv("KL_GDPA_GRID")) grid = std::max(1, std::min(grid, atoi(g)));  // testing: multi-tile CTAs
+  launch_k(gdpa::gdpa_fwd512_kernel, grid, gdpa::NT5, smem, s, ts, tk, tv, q);
+  count_launch();
+  count_path(KL_PATH_GDPA_FWD_TC512);
+  return launch_check("gdpa_fwd512_tc");
+}
+
+static int gdpa_bwd512_launch(const kl_gdpa_args* a, const gdpa::P& p, cudaStream_t s) {
+  if (!a->dZ_out || !a->A_out) {
+    set_error("kl_gdpa_bwd: d = 512 needs dZ_out and A_out (B, T, 128) scratch");
+    return KL_EBADSHAPE;
+  }
+  CUtensorMap ts, tg, tk, tv;
+  const long long kvbs = (long long)gdpa::HK2 * 512;
+  if (!gdpa::map3(&ts, a->S, 512, a->T, a->B, a->s_rs, a->s_bs, gdpa::TB) ||
+      !gdpa::map3(&tg, a->dY, 512, a->T, a->B, a->s_rs, a->s_bs, gdpa::TB) ||
+      !gdpa::map3(&tk, a->Kt, 512, gdpa::HK2, a->B, 512, kvbs, gdpa::HK2) ||
+      !gdpa::map3(&tv, a->Vt, 512, gdpa::HK2, a->B, 512, kvbs, gdpa::HK2)) {
+    set_error("kl_gdpa_bwd: tensor map encode failed (alignment?)");
+    return KL_EUNSUPPORTED;
+  }
+  if ((a->s_rs % 8) || (a->s_bs % 8) || ((uintptr_t)a->dY & 15) || ((uintptr_t)a->dS & 15) ||
+      ((uintptr_t)a->dZ_out & 15) || ((uintptr_t)a->A_out & 15)) {
+    set_error("kl_gdpa_bwd: dY / dS / dZ / A rows must be 16-byte aligned");
+    return KL_EUNSUPPORTED;
+  }
+  gdpa::P5 q = p5_of(a, p);
+  q.out = (bf16*)a->dS;
+  q.res = (const bf16*)a->dY;
+  q.dZ = (bf16*)a->dZ_out;
+  q.A = (bf16*)a->A_out;
+  const size_t smem = gdpa::bwd512_smem();
+  cudaFuncSetAttribute(gdpa::gdpa_bwd512_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int W = a->B * ((a->T + gdpa::TB - 1) / gdpa::TB);
+  int grid = std::min(W, tc_num_sms());
+  if (const char* g = getenv("KL_GDPA_GRID")) grid = std::max(1, std::min(grid, atoi(g)));  // testing: multi-tile CTAs
+  launch_k(gdpa::gdpa_bwd512_kernel, grid, gdpa::NT5, smem, s, ts, tg, tk, tv, q);
+  count_launch();
+  count_path(KL_PATH_GDPA_BWD_TC512);
+  return launch_check("gdpa_bwd512_tc");
+}
+
 extern "C" int kl_gdpa_fwd(const kl_gdpa_args* a, void* stream) {
   gdpa::P p;
   int rc = gdpa_prepare(a, "kl_gdpa_fwd", p, stream);
@@ -764,6 +1288,7 @@ extern "C" int kl_gdpa_fwd(const kl_gdpa_args* a, void* stream) {
   }
   if (a->B == 0 || a->T == 0) return KL_OK;
   cudaStream_t s = (cudaStream_t)stream;
+  if (a->d == 512) return gdpa_fwd512_launch(a, p, s);
   return a->d == 256 ? gdpa_fwd_launch<256>(a, p, s) : gdpa_fwd_launch<128>(a, p, s);
 }
 
@@ -771,12 +1296,13 @@ extern "C" int kl_gdpa_bwd(const kl_gdpa_args* a, void* stream) {
   gdpa::P p;
   int rc = gdpa_prepare(a, "kl_gdpa_bwd", p, stream);
   if (rc) return rc;
-  if (!a->dY || !a->dS || !a->dKt || !a->dVt) {
-    set_error("kl_gdpa_bwd: dY, dS, dKt and dVt are required");
+  if (!a->dY || !a->dS || (a->d != 512 && (!a->dKt || !a->dVt))) {
+    set_error("kl_gdpa_bwd: dY, dS and (d < 512) dKt, dVt are required");
     return KL_EBADSHAPE;
   }
   if (a->B == 0) return KL_OK;
   cudaStream_t s = (cudaStream_t)stream;
+  if (a->d == 512) return a->T == 0 ? KL_OK : gdpa_bwd512_launch(a, p, s);
   if (a->T == 0) {
     cudaMemsetAsync(a->dKt, 0, (size_t)a->B * a->HK * a->d * 2, s);
     cudaMemsetAsync(a->dVt, 0, (size_t)a->B * a->HK * a->d * 2, s);

@@ -465,10 +465,21 @@ class _GdpaCore(torch.autograd.Function):
         if ctx.fused:
             S, Kt, Vt, lengths = ctx.saved_tensors
             dS = torch.empty_like(S)
-            dKt, dVt = torch.empty_like(Kt), torch.empty_like(Vt)
             a = _gdpa_args(S, Kt, Vt, lengths, ctx.codes, ctx.n_kv, ctx.inv_tau)
-            a.dY, a.dS, a.dKt, a.dVt = g.data_ptr(), dS.data_ptr(), dKt.data_ptr(), dVt.data_ptr()
-            _capi.call("kl_gdpa_bwd", C.byref(a), _stream())
+            if S.shape[-1] == 512:
+                # d = 512: the kernel forms dS and writes dZ, A (B, T, HK); the
+                # sample-wide reductions dKt = dZ^T S, dVt = A^T dY are GEMMs
+                B, T, _ = S.shape
+                dZ = torch.empty(B, T, Kt.shape[1], device=S.device, dtype=S.dtype)
+                A = torch.empty_like(dZ)
+                a.dY, a.dS, a.dZ_out, a.A_out = g.data_ptr(), dS.data_ptr(), dZ.data_ptr(), A.data_ptr()
+                _capi.call("kl_gdpa_bwd", C.byref(a), _stream())
+                dKt = gemm(dZ.transpose(1, 2), S)
+                dVt = gemm(A.transpose(1, 2), g)
+            else:
+                dKt, dVt = torch.empty_like(Kt), torch.empty_like(Vt)
+                a.dY, a.dS, a.dKt, a.dVt = g.data_ptr(), dS.data_ptr(), dKt.data_ptr(), dVt.data_ptr()
+                _capi.call("kl_gdpa_bwd", C.byref(a), _stream())
             if ctx.sink is not None:
                 dS = ctx.sink.deliver(dS)
             return dS, dKt, dVt, None, None, None, None, None
@@ -491,9 +502,11 @@ _FUSED_ACTS = tuple(ACTIVATIONS[a] for a in ("identity", "relu", "silu", "tanh")
 
 
 def _gdpa_fused_ok(S, HK, codes=(), n_kv=16) -> bool:
-    """The fused kernels: bf16, 64 generated rows, d in {128, 256}, n_kv a
-    multiple of 16, the default activation cycle (kl_gdpa_fwd's contract)."""
-    return (GDPA_FUSED and S.dtype == torch.bfloat16 and HK == 64 and S.shape[-1] in (128, 256)
+    """The fused kernels: bf16, (64 generated rows, d in {128, 256}) or
+    (128 generated rows, d = 512), n_kv a multiple of 16, the default
+    activation cycle (kl_gdpa_fwd's contract)."""
+    d = S.shape[-1]
+    return (GDPA_FUSED and S.dtype == torch.bfloat16 and ((HK == 64 and d in (128, 256)) or (HK == 128 and d == 512))
             and n_kv % 16 == 0 and all(c in _FUSED_ACTS for c in codes)
             and bool(_capi.lib().kl_tcgen05_available()))
 

@@ -104,8 +104,7 @@ def test_model_bf16_tcgen05_path_vs_oracle(compskip, shape):
 
     # --- the benchmarked kernels ran (and no fallback did)
     fused = ("hsp_fwd_tc", "hsp_bwd_tc", "swa_fwd_tc", "swa_bwd_tc", "gemm_tc")
-    if spec.d <= 256:
-        fused += ("gdpa_fwd_tc", "gdpa_bwd_tc")
+    fused += ("gdpa_fwd_tc", "gdpa_bwd_tc") if spec.d <= 256 else ("gdpa_fwd_tc512", "gdpa_bwd_tc512")
     for k in fused:
         assert hits[k] > 0, (k, hits)
     for k in ("swa_fwd_simt", "swa_bwd_simt", "colsoftmax"):

@@ -141,7 +141,8 @@ def _params_gdpa(dtype, H=4, d=32, n_kv=4, n_sum=2, n_ctx=5, T=20, seed=0, acts=
                                              (4, 128, 16, 300, ("silu", "relu", "identity", "tanh")),
                                              (4, 256, 16, 1024, ("silu", "relu", "identity", "tanh")),
                                              (4, 256, 16, 257, ("tanh", "silu", "sigmoid", "identity")),
-                                             (2, 256, 32, 128, ("silu", "relu"))])
+                                             (2, 256, 32, 128, ("silu", "relu")),
+                                             (8, 512, 16, 700, ("silu", "relu", "identity", "tanh") * 2)])
 def test_gdpa_vs_oracle(dtype, H, d, n_kv, T, acts):
     """GDPA (weight generation + folded core) vs the oracle, per tensor.
 
@@ -175,9 +176,10 @@ def test_gdpa_vs_oracle(dtype, H, d, n_kv, T, acts):
     P.zero_grad()
     (F.cast(y, torch.float32) * dev(R)).sum().backward()
     hits = _capi.path_hits()
-    fused = (dtype == torch.bfloat16 and d in (128, 256) and H * n_kv == 64
+    fused = (dtype == torch.bfloat16 and ((d in (128, 256) and H * n_kv == 64) or (d == 512 and H * n_kv == 128))
              and all(a in ("identity", "relu", "silu", "tanh") for a in cfg.activations))
-    assert (hits["gdpa_fwd_tc"] > 0 and hits["gdpa_bwd_tc"] > 0) == fused, hits
+    sfx = "512" if d == 512 else ""
+    assert (hits["gdpa_fwd_tc" + sfx] > 0 and hits["gdpa_bwd_tc" + sfx] > 0) == fused, hits
     from oracle.parity import KINK_TOL, grad_errors, relu_kink, violations
 
     relu = dtype == torch.bfloat16 and "relu" in cfg.activations
@@ -647,3 +649,72 @@ def test_rote_errors():
         RoteConfig.default(7)
     with pytest.raises(ValueError):
         RoteConfig(np.ones(2), np.ones(3))
+
+
+@pytest.mark.parametrize("grid", [None, "3"])
+def test_gdpa512_fused_vs_gemm_composition(grid, monkeypatch):
+    """d = 512 fused kernels (streamed operands, two 256-column halves) vs the
+    kl_gemm composition, including CTAs that walk several tiles (grid
+    capped through KL_GDPA_GRID) and jagged lengths."""
+    from paper_2602_10016_b200 import _capi
+    from paper_2602_10016_b200 import functional as F
+
+    if grid:
+        monkeypatch.setenv("KL_GDPA_GRID", grid)
+    torch.manual_seed(5)
+    B, T, d, HK, n_kv = 5, 1000, 512, 128, 16
+    acts = ("silu", "relu", "identity", "tanh") * 2
+    S = (torch.randn(B, T, d, device="cuda") / d ** 0.5).bfloat16().requires_grad_()
+    Kt = (torch.randn(B, HK, d, device="cuda") / 2).bfloat16().requires_grad_()
+    Vt = (torch.randn(B, HK, d, device="cuda") / 8).bfloat16().requires_grad_()
+    lengths = torch.tensor([T, T - 1, 0, 1, 129], dtype=torch.int32, device="cuda")
+    G = torch.randn(B, T, d, device="cuda").bfloat16()
+    outs = []
+    for fused in (True, False):
+        F.GDPA_FUSED = fused
+        try:
+            S.grad = Kt.grad = Vt.grad = None
+            _capi.reset_path_hits()
+            y = F.gdpa_core(S, Kt, Vt, lengths, acts, n_kv, 1.0 / 3.0)
+            y.backward(G)
+            torch.cuda.synchronize()
+            hits = _capi.path_hits()
+            assert (hits["gdpa_fwd_tc512"] > 0 and hits["gdpa_bwd_tc512"] > 0) == fused, hits
+            outs.append([y.detach().float(), S.grad.float(), Kt.grad.float(), Vt.grad.float()])
+        finally:
+            F.GDPA_FUSED = True
+    for name, a, b in zip(("Y", "dS", "dKt", "dVt"), outs[0], outs[1]):
+        err = ((a - b).norm() / b.norm().clamp_min(1e-30)).item()
+        assert err < 1e-2, (name, err)
+    assert torch.equal(outs[0][0][2], S.detach()[2].float())  # length-0 sample passes through
+    assert torch.equal(outs[0][1][2], G[2].float())
+
+
+@pytest.mark.parametrize("grid", [None, "5"])
+def test_hsp512_fused_vs_composition(grid, monkeypatch):
+    """d = 512 fused pooling vs the GEMM + column-softmax composition, with
+    CTAs walking several items (KL_HSP_GRID) and jagged lengths."""
+    from paper_2602_10016_b200 import functional as F
+
+    if grid:
+        monkeypatch.setenv("KL_HSP_GRID", grid)
+    torch.manual_seed(6)
+    B, T, d, HQ = 5, 900, 512, 320
+    S = (torch.randn(B, T, d, device="cuda") * 4 / d ** 0.5).bfloat16().requires_grad_()
+    Q = (torch.randn(HQ, d, device="cuda") / d ** 0.5).requires_grad_()
+    lengths = torch.tensor([T, 0, 257, 1, T - 3], dtype=torch.int32, device="cuda")
+    outs = []
+    for fused in (True, False):
+        F.HSP_FUSED = fused
+        try:
+            S.grad = Q.grad = None
+            o1, o2 = F.hsp_pool(S, Q, lengths, splits=(256, 64))
+            g1 = torch.randn_like(o1.float(), generator=torch.Generator(device="cuda").manual_seed(1)).bfloat16()
+            g2 = torch.randn_like(o2.float(), generator=torch.Generator(device="cuda").manual_seed(2)).bfloat16()
+            torch.autograd.backward([o1, o2], [g1, g2])
+            outs.append([o1.detach().float(), o2.detach().float(), S.grad.float(), Q.grad.float()])
+        finally:
+            F.HSP_FUSED = True
+    for name, a, b in zip(("O1", "O2", "dS", "dQ"), outs[0], outs[1]):
+        err = ((a - b).norm() / b.norm().clamp_min(1e-30)).item()
+        assert err < 1e-2, (name, err)
