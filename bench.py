@@ -522,6 +522,7 @@ def main():
     barrier()
     launches = launches_per_step * args.steps
     clk = clocks.stop()
+    steps_[0].check_numerics()  # NumericsError if any timed step produced a NaN / Inf logit or loss
     ms = e0.elapsed_time(e1) / args.steps
     t = torch.tensor([ms], device=dev)
     if world > 1:

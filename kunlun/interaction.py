@@ -1,0 +1,5 @@
+"""``kunlun.interaction`` — the reference module name (/root/reference/pkg/src/kunlun/interaction.py)
+backed by the B200 implementation in ``paper_2602_10016_b200.interaction`` (same
+names, dataclasses, validation and registry names; batched CUDA tensors)."""
+
+from paper_2602_10016_b200.interaction import *  # noqa: F401,F403

@@ -1,0 +1,5 @@
+"""``kunlun.mlp`` — the reference module name (/root/reference/pkg/src/kunlun/mlp.py)
+backed by the B200 implementation in ``paper_2602_10016_b200.mlp`` (same
+names, dataclasses, validation and registry names; batched CUDA tensors)."""
+
+from paper_2602_10016_b200.mlp import *  # noqa: F401,F403

@@ -19,7 +19,7 @@ import torch
 
 from . import _capi
 from . import functional as F
-from .tensor import Params, ShapeError
+from .tensor import Params, ShapeError, flag_nonfinite, numerics_check_mode
 
 
 @dataclass
@@ -129,6 +129,8 @@ def _self_attention(s, p: MhaParams, w: int, causal: bool, lengths):
     qkv = F.linear(s, p.P, p.wqkv, stash_in=stash)
     o = F.swa_core(qkv, lens, p.heads, p.head_dim, w, causal)
     y = F.linear(o, p.P, p.wout, residual=s, stash_out=stash)
+    if numerics_check_mode() == "eager":
+        flag_nonfinite(y, "self-attention")
     return y.squeeze(0) if squeeze else y
 
 
@@ -182,6 +184,8 @@ def multi_head_attention(queries, keys_values, p: MhaParams, mask=None, lengths=
     (pooled,) = F.hsp_pool(kv, q_rows, lens)
     o = F.head_proj(pooled.view(kv.shape[0], n_q, H, p.dim), p.ref(2))
     out = F.linear(o, p.P, p.wout)
+    if numerics_check_mode() == "eager":
+        flag_nonfinite(out, "multi_head_attention")
     return out.squeeze(0) if squeeze else out
 
 

@@ -22,7 +22,7 @@ import torch
 
 from . import functional as F
 from .jagged import JaggedBatch
-from .tensor import ACTIVATIONS, Params, ShapeError
+from .tensor import ACTIVATIONS, Params, ShapeError, flag_nonfinite, numerics_check_mode
 
 DEFAULT_ACTIVATION_CYCLE = ("silu", "relu", "identity", "tanh")  # gdpa.py:31
 
@@ -160,6 +160,8 @@ def gdpa_forward(s: torch.Tensor, x_sum: torch.Tensor, cfg: GdpaConfig, p: Weigh
         kv = generate_kv(x_sum, p, cfg)
     kt, vt = fold_kv(kv[0], kv[1], p)
     y = F.gdpa_core(s, kt, vt, _lengths(s, lengths), cfg.activations, cfg.n_kv, 1.0 / cfg.tau)
+    if numerics_check_mode() == "eager":
+        flag_nonfinite(y, "gdpa_forward")
     return y.squeeze(0) if squeeze else y
 
 

@@ -21,7 +21,7 @@ from .gdpa import GdpaConfig, WeightGenParams, fold_kv, generate_kv, summarize_n
 from .interaction import ExpertPartition, InteractionParams, global_interaction
 from .mlp import Mlp
 from .seqsum import SummarizerParams, SummarySplit, hsp_summarize
-from .tensor import Params, ShapeError
+from .tensor import Params, ShapeError, _flag, flag_nonfinite
 
 DEFAULT_ACTIVATION_CYCLE = ("silu", "relu", "identity", "tanh")
 FOLD_ALL_LAYERS = True  # fold every layer's HSP/CLS queries in one batched pass (tests A/B it)
@@ -159,6 +159,8 @@ class KunlunModel:
             self.layers.append(LayerParams(pool, wg, mh, sm, gi))
         self.head = Mlp.create(P, "head", [cfg.n_ctx * d, cfg.head_hidden, 1], ["silu", "identity"], rng)
         P.finalize(device, dtype)
+        if torch.device(device).type == "cuda":
+            _flag(device)  # the non-finite flag exists before any CUDA-graph capture
         self.flags = compskip_config(cfg.L, cfg.compskip)
         self.layer_hook = None  # set by dist.GradReducer
 
@@ -300,11 +302,14 @@ class KunlunModel:
         B = X.shape[0]
         z = self.head.apply_rows(X.reshape(B, -1))
         logits = F.cast(z, torch.float32).reshape(B)
+        flag_nonfinite(logits, "logits")  # deferred: read by raise_if_nonfinite / TrainStep.check_numerics
         return (logits, outs) if keep_outputs else logits
 
     def loss(self, X, S_list, lengths, labels, prune_dead=True):
         logits = self.forward(X, S_list, lengths, prune_dead=prune_dead)
-        return F.bce_with_logits(logits, labels), logits
+        loss = F.bce_with_logits(logits, labels)
+        flag_nonfinite(loss, "loss")
+        return loss, logits
 
     def count_params(self) -> int:
         return self.P.count()

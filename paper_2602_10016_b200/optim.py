@@ -150,3 +150,10 @@ class TrainStep:
             return self.eager()
         self.graph.replay()
         return self.loss
+
+    def check_numerics(self):
+        """NumericsError if any step since the last check produced a NaN / Inf
+        logit or loss (the device flag of tensor.flag_nonfinite; one sync)."""
+        from .tensor import raise_if_nonfinite
+
+        raise_if_nonfinite(self.X.device, "training step")

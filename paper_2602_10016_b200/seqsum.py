@@ -22,7 +22,7 @@ import torch
 
 from . import functional as F
 from .attention import MhaParams, multi_head_attention, shared_queries, _lengths
-from .tensor import Params, ShapeError
+from .tensor import Params, ShapeError, flag_nonfinite, numerics_check_mode
 
 
 def pma(s, queries, p: MhaParams, lengths=None):
@@ -246,6 +246,9 @@ def hsp_summarize(s, p: SummarizerParams, lengths=None, sink=None, q_rows=None) 
         cls_tok = S.new_zeros(B, 0, d)
     rec = outs[len(splits)] if n_rec > 0 else S.new_zeros(B, 0, d)
     bundle = SummaryBundle(cls_tok, hsp_tok, rec)
+    if numerics_check_mode() == "eager":
+        for t in (cls_tok, hsp_tok, rec):
+            flag_nonfinite(t, "hsp_summarize")
     if squeeze:
         bundle = SummaryBundle(cls_tok[0], hsp_tok[0], rec[0])
     assert bundle.total_rows == p.split.total

@@ -213,3 +213,67 @@ class Params:
 
 def inv_sqrt(x: float) -> float:
     return 1.0 / math.sqrt(x)
+
+
+# ---------------------------------------------------------------------------
+# Non-finite detection (the reference's _ensure_finite, tensor.py:21-27,
+# called from every op at tensor.py:245-549).
+#
+# The device path cannot raise inside a kernel, so a scan kernel
+# (kl_check_finite) ORs a per-device flag and the host raises NumericsError
+# when it reads it.  Modes (set_numerics_check):
+#   "eager"     every public op (gdpa_forward, mha_window / mha_full,
+#               multi_head_attention, hsp_summarize, pma, global_interaction,
+#               Mlp, the model's logits / loss) scans its output and raises
+#               at once — the reference's semantics, one host sync per op;
+#   "deferred"  (default) only the model's logits and loss are scanned (a NaN
+#               / Inf anywhere upstream reaches them), with no sync; the flag
+#               is read by raise_if_nonfinite() — TrainStep.check_numerics()
+#               and bench.py call it once after the steps;
+#   "off"       no scans.
+_NUMERICS = {"mode": "deferred"}
+_FLAGS: dict = {}
+
+
+def set_numerics_check(mode: str) -> None:
+    if mode not in ("eager", "deferred", "off"):
+        raise ValueError(f"numerics check mode must be eager, deferred or off, got {mode!r}")
+    _NUMERICS["mode"] = mode
+
+
+def numerics_check_mode() -> str:
+    return _NUMERICS["mode"]
+
+
+def _flag(device) -> torch.Tensor:
+    key = torch.device(device).index or 0
+    f = _FLAGS.get(key)
+    if f is None:
+        f = torch.zeros(1, dtype=torch.int32, device=device)
+        _FLAGS[key] = f
+    return f
+
+
+def flag_nonfinite(t: torch.Tensor, what: str = "") -> None:
+    """Scan ``t`` on its stream and OR the device's non-finite flag; in
+    eager mode raise NumericsError now if it is set."""
+    mode = _NUMERICS["mode"]
+    if mode == "off" or t is None or not t.is_cuda or t.numel() == 0:
+        return
+    from . import _capi
+
+    x = t.detach()
+    if not x.is_contiguous():
+        x = x.contiguous()
+    f = _flag(x.device)
+    _capi.call("kl_check_finite", x.numel(), _capi.dt(x), x.data_ptr(), f.data_ptr(), _capi._stream())
+    if mode == "eager":
+        raise_if_nonfinite(x.device, what)
+
+
+def raise_if_nonfinite(device="cuda", what: str = "") -> None:
+    """Read (and clear) the device's non-finite flag; NumericsError if set."""
+    f = _flag(device)
+    if int(f.item()):
+        f.zero_()
+        raise NumericsError(f"non-finite values{' in ' + what if what else ''} (NaN/Inf; tensor.py:21-27)")

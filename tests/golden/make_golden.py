@@ -25,8 +25,11 @@ import numpy as np
 
 REF = "/root/reference/pkg/src"
 HERE = os.path.dirname(os.path.abspath(__file__))
-sys.path.insert(0, REF)
+# the repo root first (for ``oracle``), then the reference in front of it, so
+# ``import kunlun`` resolves to the unmodified reference, not the repo's
+# B200 drop-in package of the same name
 sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+sys.path.insert(0, REF)
 
 from kunlun import attention as A  # noqa: E402
 from kunlun import gdpa as G  # noqa: E402

@@ -718,3 +718,63 @@ def test_hsp512_fused_vs_composition(grid, monkeypatch):
     for name, a, b in zip(("O1", "O2", "dS", "dQ"), outs[0], outs[1]):
         err = ((a - b).norm() / b.norm().clamp_min(1e-30)).item()
         assert err < 1e-2, (name, err)
+
+
+def _gdpa_setup(acts, scale=1.0, d=128, T=200):
+    from paper_2602_10016_b200 import functional as F
+    from paper_2602_10016_b200 import gdpa as G
+
+    P, cfg, wg, named = _params_gdpa(torch.bfloat16, 4, d, 16, 2, 5, T, acts=acts)
+    rng = np.random.default_rng(3)
+    S = torch.tensor(rng.normal(0, scale, (2, T, d)), device="cuda").bfloat16()
+    X = torch.tensor(rng.normal(0, 1, (2, 5, d)), device="cuda").bfloat16()
+    xs = G.summarize_nonseq(X, F.PRef(P, "pool"))
+    return G, cfg, wg, S, xs
+
+
+@pytest.mark.parametrize("tag", ["exp", "log", "sqrt"])
+def test_numerics_error_eager(tag):
+    """exp / log / sqrt GDPA heads on ordinary score ranges give Inf / NaN:
+    in eager mode the op raises NumericsError (tensor.py:21-27), as the
+    reference's _ensure_finite does."""
+    from paper_2602_10016_b200.tensor import NumericsError, numerics_check_mode, set_numerics_check
+
+    G, cfg, wg, S, xs = _gdpa_setup((tag, "silu", "relu", tag), scale=40.0 if tag == "exp" else 1.0)
+    cfg.tau = 1e-3 if tag == "exp" else cfg.tau  # large scores: exp overflows
+    old = numerics_check_mode()
+    set_numerics_check("eager")
+    try:
+        with pytest.raises(NumericsError):
+            G.gdpa_forward(S, xs, cfg, wg)
+        # finite inputs with smooth heads pass
+        cfg2 = G.GdpaConfig(cfg.dim, cfg.heads, cfg.n_kv, 200.0, ("silu", "relu", "identity", "tanh"))
+        G.gdpa_forward(S / 40.0 if tag == "exp" else S, xs, cfg2, wg)
+    finally:
+        set_numerics_check(old)
+
+
+def test_numerics_error_deferred_training_step():
+    """Deferred mode: a NaN input leaves the training step running (no sync)
+    and raise_if_nonfinite / TrainStep.check_numerics raise afterwards."""
+    from paper_2602_10016_b200.configs import c1
+    from paper_2602_10016_b200.model import KunlunModel
+    from paper_2602_10016_b200.optim import FlatAdam, TrainStep
+    from paper_2602_10016_b200.synth import ctr_batch
+    from paper_2602_10016_b200.tensor import NumericsError
+
+    cfg, _ = c1()
+    B = 4
+    model = KunlunModel(cfg, "cuda", torch.bfloat16, seed=0)
+    Xn, Sn, Ln, yn = ctr_batch(cfg, B, seed=3)
+    X = torch.tensor(Xn, device="cuda").bfloat16()
+    S = [torch.tensor(s, device="cuda").bfloat16() for s in Sn]
+    lens = [torch.tensor(l, device="cuda") for l in Ln]
+    y = torch.tensor(yn, device="cuda")
+    step = TrainStep(model, FlatAdam(model.P), X, S, lens, y, None)
+    step.eager()
+    step.check_numerics()  # clean
+    S[0][1, 3, 5] = float("nan")
+    step.eager()
+    with pytest.raises(NumericsError):
+        step.check_numerics()
+    step.check_numerics()  # the flag was cleared
