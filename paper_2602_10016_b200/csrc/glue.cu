@@ -8,6 +8,8 @@
 
 namespace kl {
 
+int tc_num_sms();  // cached cudaDevAttrMultiProcessorCount (gemm_tc.cu)
+
 namespace {
 
 // ---------------------------------------------------------------------------
@@ -548,7 +550,7 @@ __global__ void rote_kernel(kl_rote_args a) {
     const T* xp = x + (long long)b * a.x_bs + (long long)t * a.x_rs + 2 * i;
     T* yp = y + (long long)b * a.y_bs + (long long)t * a.y_rs + 2 * i;
     const float x0 = ldf(xp), x1 = ldf(xp + 1);
-    const int len = a.lengths ? a.lengths[b] : a.T;
+    const int len = a.lengths ? min(max(a.lengths[b], 0), a.T) : a.T;  // clamped: never read past the sample
     if (t >= len) {
       stf(yp, x0);
       stf(yp + 1, x1);
@@ -638,7 +640,7 @@ __global__ void __launch_bounds__(256, 4) rote_vec_kernel(kl_rote_args a) {
     T* yp = y + (long long)b * a.y_bs + (long long)t * a.y_rs + 8 * c;
     float v[8];
     RoteVec<T>::load(xp, v);
-    const int len = a.lengths ? __ldg(a.lengths + b) : a.T;
+    const int len = a.lengths ? min(max(__ldg(a.lengths + b), 0), a.T) : a.T;  // clamped: never read past the sample
     if (t < len) {
       double g = 0.0;
       if (a.timestamps) {
@@ -913,9 +915,10 @@ extern "C" int kl_rote(const kl_rote_args* a, void* stream) {
                    a->y_bs % 8 == 0 && al16(a->x) && al16(a->y) && total / 4 < (1LL << 31);
   if (vec) {
     const long long cpr = a->d / 8;
-    // persistent: one wave of 4 blocks/SM; 148*4*256 = 2^11*74 threads divide
-    // any power-of-two cpr <= 2048, otherwise round the grid to a multiple of cpr
-    long long grid = std::min<long long>((total / 4 + 255) / 256, 148LL * 4);
+    // persistent: one wave of 4 blocks/SM (148*4*256 = 2^11*74 threads on a
+    // B200 divide any power-of-two cpr <= 2048); otherwise the grid is rounded
+    // to a multiple of cpr
+    long long grid = std::min<long long>((total / 4 + 255) / 256, (long long)tc_num_sms() * 4);
     if ((grid * 256) % cpr) grid = (grid + cpr - 1) / cpr * cpr;
     if (a->dtype == KL_BF16)
       launch_k(rote_vec_kernel<bf16>, (int)grid, 256, 0, (cudaStream_t)stream, *a);
@@ -923,7 +926,7 @@ extern "C" int kl_rote(const kl_rote_args* a, void* stream) {
       launch_k(rote_vec_kernel<float>, (int)grid, 256, 0, (cudaStream_t)stream, *a);
     return launch_check("rote");
   }
-  const int grid = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
+  const int grid = (int)std::min<long long>((total + 255) / 256, (long long)tc_num_sms() * 16);
   if (a->dtype == KL_BF16)
     launch_k(rote_kernel<bf16>, grid, 256, 0, (cudaStream_t)stream, *a);
   else
@@ -949,7 +952,7 @@ extern "C" int kl_bce_fwd_bwd(int n, const float* z, const float* y, float* loss
 extern "C" int kl_cast(long long n, int dtype_in, const void* x, int dtype_out, void* y, void* stream) {
   if (n == 0) return KL_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  unsigned g = (unsigned)std::min<long long>((n + 255) / 256, 148 * 16);
+  unsigned g = (unsigned)std::min<long long>((n + 255) / 256, (long long)tc_num_sms() * 16);
   if (dtype_in == KL_F32 && dtype_out == KL_BF16) launch_k(cast_kernel<float, bf16>, g, 256, 0, s, n, (const float*)x, (bf16*)y);
   else if (dtype_in == KL_BF16 && dtype_out == KL_F32) launch_k(cast_kernel<bf16, float>, g, 256, 0, s, n, (const bf16*)x, (float*)y);
   else if (dtype_in == KL_F32) launch_k(cast_kernel<float, float>, g, 256, 0, s, n, (const float*)x, (float*)y);
@@ -993,7 +996,7 @@ extern "C" int kl_act_bwd(int rows, int cols, int dtype, const void* g, long lon
 extern "C" int kl_check_finite(long long n, int dtype, const void* x, unsigned int* flag, void* stream) {
   if (n == 0) return KL_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  unsigned g = (unsigned)std::min<long long>((n + 255) / 256, 148 * 8);
+  unsigned g = (unsigned)std::min<long long>((n + 255) / 256, (long long)tc_num_sms() * 8);
   if (dtype == KL_F32) launch_k(finite_kernel<float>, g, 256, 0, s, n, (const float*)x, flag);
   else launch_k(finite_kernel<bf16>, g, 256, 0, s, n, (const bf16*)x, flag);
   count_launch();
@@ -1067,7 +1070,7 @@ extern "C" int kl_adam_step(long long n, float lr, float beta1, float beta2, flo
   cudaStream_t s = (cudaStream_t)stream;
   const bool tick = step_dev && step != -1;
   if (tick) launch_k(tick_kernel, 1, 1, 0, s, step_dev);
-  unsigned grid = (unsigned)std::min<long long>((n / 4 + 255) / 256 + 1, 148 * 8);
+  unsigned grid = (unsigned)std::min<long long>((n / 4 + 255) / 256 + 1, (long long)tc_num_sms() * 8);
   launch_k(adam_kernel, grid, 256, 0, s, n, lr, beta1, beta2, eps, step, step_dev, w, g, m, v, (bf16*)w_bf16);
   count_launch(tick ? 2 : 1);
   return launch_check("adam_step");

@@ -41,10 +41,14 @@ class FlatAdam:
 
 
 def _subtract(rng, holes):
-    """[lo, hi) minus the sorted disjoint ``holes``."""
+    """[lo, hi) minus the sorted disjoint ``holes``.  A hole's end is rounded
+    up to the 8-element block alignment of Params (the gap is block padding,
+    never a parameter), so every returned segment starts 16-byte aligned as
+    kl_adam_step requires, whatever the hole's element count."""
     lo, hi = rng
     out = []
     for a, b in holes:
+        b = min((b + 7) // 8 * 8, hi) if b < hi else b
         if b <= lo or a >= hi:
             continue
         if a > lo:

@@ -56,8 +56,12 @@ class RoteConfig:
         return self.pos_freqs.size
 
     def device_freqs(self, device) -> tuple[torch.Tensor, torch.Tensor]:
-        """fp64 copies of the schedules on ``device`` (uploaded once)."""
-        key = str(device)
+        """fp64 copies of the schedules on ``device``, uploaded once per
+        (device, schedule values): reassigning pos_freqs / temp_freqs
+        re-uploads.  Call it (or run one eager step) before capturing a CUDA
+        graph — the upload is a host copy."""
+        key = (str(device), id(self.pos_freqs), id(self.temp_freqs), self.pos_freqs.tobytes().__hash__(),
+               self.temp_freqs.tobytes().__hash__())
         if key not in self._dev:
             self._dev[key] = (torch.tensor(self.pos_freqs, device=device, dtype=torch.float64),
                               torch.tensor(self.temp_freqs, device=device, dtype=torch.float64))
@@ -120,6 +124,12 @@ def rote_sequence(s: torch.Tensor, timestamps, cfg: RoteConfig, lengths: torch.T
     ln = None
     if lengths is not None:
         ln = torch.as_tensor(lengths, device=x.device).to(torch.int32).contiguous()
+        if ln.numel() != x.shape[0]:
+            raise ShapeError(f"need one length per sample ({x.shape[0]}), got {ln.numel()}")
+        if not torch.cuda.is_current_stream_capturing():  # (the kernels also clamp to [0, T])
+            lo, hi = int(ln.min()), int(ln.max())
+            if lo < 0 or hi > x.shape[1]:
+                raise ValueError(f"lengths must lie in [0, {x.shape[1]}], got [{lo}, {hi}]")
     if x.numel() == 0:  # T = 0: the reference returns the (empty) input
         return s
     y = _Rote.apply(x, ln, ts, cfg)
