@@ -40,15 +40,15 @@ class FlatAdam:
                    self.v.data_ptr() + lo * e32, wc, _capi._stream())
 
 
-def _subtract(rng, holes):
-    """[lo, hi) minus the sorted disjoint ``holes``.  A hole's end is rounded
-    up to the 8-element block alignment of Params (the gap is block padding,
-    never a parameter), so every returned segment starts 16-byte aligned as
-    kl_adam_step requires, whatever the hole's element count."""
+def _subtract(rng, holes, align: int = 1):
+    """[lo, hi) minus the sorted disjoint ``holes``.  With ``align`` = 8 a
+    hole's end is rounded up to the 8-element block alignment of Params (the
+    gap is block padding, never a parameter), so every returned segment starts
+    16-byte aligned as kl_adam_step requires, whatever the hole's size."""
     lo, hi = rng
     out = []
     for a, b in holes:
-        b = min((b + 7) // 8 * 8, hi) if b < hi else b
+        b = min((b + align - 1) // align * align, hi) if b < hi else b
         if b <= lo or a >= hi:
             continue
         if a > lo:
@@ -79,7 +79,7 @@ class TrainStep:
         if reducer is None and hasattr(model, "layer_param_ranges"):
             P = model.P
             holes = sorted(P.block_range(k) for k in model.late_grad_blocks())
-            self.segments = [_subtract(r, holes) for r in model.layer_param_ranges()]
+            self.segments = [_subtract(r, holes, align=8) for r in model.layer_param_ranges()]
             covered = [seg for segs in self.segments for seg in segs]
             self.late = _subtract((0, P.gflat.numel()), sorted(covered))
 
