@@ -13,6 +13,14 @@ float64 oracle restatement, oracle/) on the host cores instead.
 
 from __future__ import annotations
 
+import os
+
+# The CPU reference legs fork single-thread numpy workers: OpenBLAS must be
+# single-threaded before numpy (imported by torch / the package) first loads
+# it, or every forked worker spins a full-width BLAS pool (oversubscription).
+for _v in ("OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+    os.environ.setdefault(_v, "1")
+
 import argparse
 import json
 import os
@@ -96,7 +104,12 @@ def _cpu_worker(args):
     spec_name, n, seed = args
     import numpy as np
 
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    try:  # in case BLAS was initialised multi-threaded before the env was set
+        from threadpoolctl import threadpool_limits
+
+        threadpool_limits(1)
+    except Exception:
+        pass
     from oracle import model as OM
 
     spec, p = _CPU_STATE[spec_name]

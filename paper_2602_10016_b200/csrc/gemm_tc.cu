@@ -921,11 +921,15 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
   const int bn_max = use_r && !r_wide ? 128 : 256;
   const int n_out0 = (g.red1 ? 1 : g.nb1) * (g.red2 ? 1 : g.nb2);
   const long long k_tot = (long long)((g.red1 ? g.nb1 : 1) * (g.red2 ? g.nb2 : 1)) * g.K;
+  // N tiles are whole TMA-store boxes: 128-byte rows, i.e. 64 bf16 or 32 fp32
+  // columns.  (A 96-column bf16 tile would store its last half-filled
+  // 64-column box over the neighbouring tile's first 32 columns.)
+  const int box_cols = g.c_dtype == KL_BF16 ? 64 : 32;
   auto split_n = [&](int cap) {
     int tn = (g.N + cap - 1) / cap;
     int b = (g.N + tn - 1) / tn;
-    b = (b + 31) / 32 * 32;  // 32-column slabs (TMA-store epilogue)
-    return b;
+    b = (b + box_cols - 1) / box_cols * box_cols;
+    return std::min(b, std::max(cap, box_cols));
   };
   int bn = split_n(bn_max);
   // Split-K plan for a tile count: weight-gradient shapes (few output tiles,
@@ -986,7 +990,7 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
       const char* v = getenv("KL_GEMM_BN");
       force = v ? atoi(v) : 0;
     }
-    if (force >= 16) bn = std::min(split_n(bn_max), (force + 15) / 16 * 16);
+    if (force >= 16) bn = std::min(split_n(bn_max), (force + box_cols - 1) / box_cols * box_cols);
   }
   p.BN = bn;
   p.tiles_n = (g.N + bn - 1) / bn;

@@ -21,7 +21,7 @@ from .gdpa import GdpaConfig, WeightGenParams, fold_kv, generate_kv, summarize_n
 from .interaction import ExpertPartition, InteractionParams, global_interaction
 from .mlp import Mlp
 from .seqsum import SummarizerParams, SummarySplit, hsp_summarize
-from .tensor import Params, ShapeError, _flag, flag_nonfinite
+from .tensor import Params, ShapeError, _flag, flag_nonfinite, numerics_check_mode
 
 DEFAULT_ACTIVATION_CYCLE = ("silu", "relu", "identity", "tanh")
 FOLD_ALL_LAYERS = True  # fold every layer's HSP/CLS queries in one batched pass (tests A/B it)
@@ -250,6 +250,8 @@ class KunlunModel:
                         kt, vt = fold_kv(k, v, lp.wg[e])
                         s = F.gdpa_core(s, kt, vt, lengths[e], cfg.gdpa_acts, cfg.n_kv, 1.0 / float(ev.T),
                                         sink=sinks[e])
+                        if numerics_check_mode() == "eager":
+                            flag_nonfinite(s, f"layer {l} event {e} GDPA")
                     if live_seq and not flags.skip_self_attention:
                         s = mha_window(s, lp.mha[e], WindowSpec(ev.w, ev.causal), lengths[e])
                     return s
