@@ -54,6 +54,7 @@ struct TcParams {
   int reduce_c;        // MODE 2: TMA reduce-add into C (fp32 accumulate / split-K)
   int x_tma;           // MODE 3, aux_mode 1: pre-activation stored by TMA (tmX, C's layout)
   int r_bufs;          // residual tile buffers (2; 1 for 256-wide tiles with a long reduction)
+  int n_fast;          // tile order: N tiles of one M block adjacent (A read once from HBM)
 };
 
 constexpr int SLD = 66;  // epilogue staging row stride (floats): 64 columns + pad, 8-byte aligned
@@ -538,7 +539,13 @@ __device__ __forceinline__ void epi_tma(const TcParams& p, const Epi& e, const C
 
 // MODE 0: plain store, 1: generic epilogue (lane = column pair), 2/3: TMA-store
 // epilogue (thread = row; see epi_tma) without / with bias and activations.
-template <typename TC, int MODE>
+// PAIR: a CTA pair (cluster of 2, cta_group::2) computes a 256 x BN tile —
+// each CTA loads its 128 A rows and half of the tile's B columns, the leader
+// issues M = 256 MMAs over both CTAs' shared memory, each CTA's TMEM holds its
+// 128 rows.  Half the B operand bytes per CTA and half the MMA instructions
+// per output (the single-CTA kernel is bound by L2 -> SM operand traffic at
+// ~10 TB/s: ncu, c4 projections).
+template <typename TC, int MODE, bool PAIR = false>
 __global__ void __launch_bounds__(NTHREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmR, const __grid_constant__ CUtensorMap tmC,
@@ -562,6 +569,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint32_t* tmem_slot = (uint32_t*)(rempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = PAIR ? tc::cluster_ctarank() : 0u;
+  const int unit0 = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int ustep = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
   if (warp == 0 && lane == 0) {
     tc::prefetch_tmap(&tmA);
     tc::prefetch_tmap(&tmB);
@@ -574,15 +584,21 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&tfull[i], 1);
-      tc::mbar_init(&tempty[i], 4);
+      tc::mbar_init(&tempty[i], PAIR ? 8 : 4);  // pair: both CTAs' epilogue warps drain the leader's MMAs
       tc::mbar_init(&rfull[i], 1);
       tc::mbar_init(&rempty[i], 4);
     }
     tc::fence_barrier_init();
   }
-  if (warp == 1) tc::tmem_alloc(tmem_slot, p.tmem_cols);
+  if (warp == 1) {
+    if (PAIR)
+      tc::tmem_alloc_pair(tmem_slot, p.tmem_cols);
+    else
+      tc::tmem_alloc(tmem_slot, p.tmem_cols);
+  }
   tc::fence_before();
   __syncthreads();
+  if (PAIR) tc::cluster_sync();  // the peer's barriers exist before any remote arrive / TMA signal
   tc::fence_after();
   const uint32_t tmem = *tmem_slot;
   // PDL: the prologue above (barrier init, TMEM alloc, tensor-map prefetch)
@@ -601,11 +617,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       uint32_t phase = 0;
       const uint32_t tx = p.a_stage_bytes + p.b_stage_bytes;
       int t = 0;
-      for (int unit = blockIdx.x; unit < total; unit += gridDim.x, ++t) {
+      for (int unit = unit0; unit < total; unit += ustep, ++t) {
         const int tile = unit / p.splits, sp = unit % p.splits;
         const int it0 = (int)((long long)iters * sp / p.splits), it1 = (int)((long long)iters * (sp + 1) / p.splits);
-        const int mb = tile % p.tiles_m;
-        const int nb = (tile / p.tiles_m) % p.tiles_n;
+        const int mbt = p.n_fast ? (tile / p.tiles_n) % p.tiles_m : tile % p.tiles_m;
+        const int mb = PAIR ? 2 * mbt + (int)rank : mbt;  // this CTA's 128-row block
+        const int nb = p.n_fast ? tile % p.tiles_n : (tile / p.tiles_m) % p.tiles_n;
         const int zo = tile / (p.tiles_m * p.tiles_n);
         const int z1o = p.red1 ? 0 : zo / nb2o, z2o = p.red2 ? 0 : zo % nb2o;
         // residual tile for this output tile: double-buffered against the
@@ -629,9 +646,27 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           const int b1 = p.b_has1 ? z1 : 0, b2 = p.b_has2 ? z2 : 0;
           {
             tc::mbar_wait(&empty[stage], phase ^ 1);
-            tc::mbar_arrive_expect_tx(&full[stage], tx);
             uint8_t* da = sA + stage * p.a_stage_bytes;
             uint8_t* db = sB + stage * p.b_stage_bytes;
+            if constexpr (PAIR) {
+              // both CTAs' operand halves complete on the leader's full barrier
+              if (rank == 0) tc::mbar_arrive_expect_tx(&full[stage], 2 * tx);
+              const uint32_t fb = tc::mapa(&full[stage], 0);
+              const int n0 = nb * p.BN + (int)rank * (p.BN / 2);
+              if (!p.a_mn) {
+                tc::tma_load_4d_pair(da, &tmA, fb, kb * BK, mb * BM, a2, a1);
+              } else {
+                tc::tma_load_4d_pair(da, &tmA, fb, mb * BM, kb * BK, a2, a1);
+                tc::tma_load_4d_pair(da + 8192, &tmA, fb, mb * BM + 64, kb * BK, a2, a1);
+              }
+              if (!p.b_mn) {
+                tc::tma_load_4d_pair(db, &tmB, fb, kb * BK, n0, b2, b1);
+              } else {
+                for (int j = 0; j < p.b_boxes; ++j)
+                  tc::tma_load_4d_pair(db + j * 8192, &tmB, fb, n0 + j * 64, kb * BK, b2, b1);
+              }
+            } else {
+            tc::mbar_arrive_expect_tx(&full[stage], tx);
             if (!p.a_mn) {
               tc::tma_load_4d(da, &tmA, &full[stage], kb * BK, mb * BM, a2, a1);
             } else {
@@ -644,6 +679,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               for (int j = 0; j < p.b_boxes; ++j)
                 tc::tma_load_4d(db + j * 8192, &tmB, &full[stage], nb * p.BN + j * 64, kb * BK, b2, b1);
             }
+            }
             if (++stage == p.stages) {
               stage = 0;
               phase ^= 1;
@@ -654,12 +690,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      const uint32_t idesc = tc::idesc_bf16(BM, p.BN, p.a_mn, p.b_mn);
+    if (lane == 0 && rank == 0) {  // (pair: the leader issues for both CTAs)
+      const uint32_t idesc = tc::idesc_bf16(PAIR ? 2 * BM : BM, p.BN, p.a_mn, p.b_mn);
       int stage = 0;
       uint32_t phase = 0;
       int t = 0;
-      for (int unit = blockIdx.x; unit < total; unit += gridDim.x, ++t) {
+      for (int unit = unit0; unit < total; unit += ustep, ++t) {
         const int sp = unit % p.splits;
         const int it0 = (int)((long long)iters * sp / p.splits), it1 = (int)((long long)iters * (sp + 1) / p.splits);
         const int acc = t & 1;
@@ -676,26 +712,36 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           for (int k = 0; k < BK / 16; ++k) {
             const uint64_t ad = p.a_mn ? tc::sdesc(a0 + k * 2048, 8192, 1024) : tc::sdesc(a0 + k * 32, 16, 1024);
             const uint64_t bd = p.b_mn ? tc::sdesc(b0 + k * 2048, 8192, 1024) : tc::sdesc(b0 + k * 32, 16, 1024);
-            tc::mma_bf16(d, ad, bd, idesc, (it > it0 || k > 0) ? 1u : 0u);
+            if constexpr (PAIR)
+              tc::mma_bf16_pair(d, ad, bd, idesc, (it > it0 || k > 0) ? 1u : 0u);
+            else
+              tc::mma_bf16(d, ad, bd, idesc, (it > it0 || k > 0) ? 1u : 0u);
           }
-          tc::mma_commit(&empty[stage]);
+          if constexpr (PAIR)
+            tc::mma_commit_pair(&empty[stage], 3);  // frees the stage in both CTAs
+          else
+            tc::mma_commit(&empty[stage]);
           if (++stage == p.stages) {
             stage = 0;
             phase ^= 1;
           }
         }
-        tc::mma_commit(&tfull[acc]);
+        if constexpr (PAIR)
+          tc::mma_commit_pair(&tfull[acc], 3);
+        else
+          tc::mma_commit(&tfull[acc]);
       }
     }
   } else {
     const int lane_base = (warp & 3) * 32;
     int t = 0, nbox = 0;
-    for (int unit = blockIdx.x; unit < total; unit += gridDim.x, ++t) {
+    for (int unit = unit0; unit < total; unit += ustep, ++t) {
       const int tile = unit / p.splits;
       const int acc = t & 1;
       const uint32_t acc_phase = (t >> 1) & 1;
-      const int mb = tile % p.tiles_m;
-      const int nb = (tile / p.tiles_m) % p.tiles_n;
+      const int mbt = p.n_fast ? (tile / p.tiles_n) % p.tiles_m : tile % p.tiles_m;
+      const int mb = PAIR ? 2 * mbt + (int)rank : mbt;
+      const int nb = p.n_fast ? tile % p.tiles_n : (tile / p.tiles_m) % p.tiles_n;
       const int zo = tile / (p.tiles_m * p.tiles_n);
       const int z1o = p.red1 ? 0 : zo / nb2o, z2o = p.red2 ? 0 : zo % nb2o;
       TC* C = (TC*)p.C + (long long)z1o * (p.red1 ? 0 : p.c_s1) + (long long)z2o * (p.red2 ? 0 : p.c_s2);
@@ -783,14 +829,22 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       tc::fence_before();
       __syncwarp();
       if (lane == 0) {
-        tc::mbar_arrive(&tempty[acc]);
+        if (PAIR)
+          tc::mbar_arrive_cluster(tc::mapa(&tempty[acc], 0));  // the leader's accumulator barrier
+        else
+          tc::mbar_arrive(&tempty[acc]);
         if (p.r_boxes) tc::mbar_arrive(&rempty[t % p.r_bufs]);
       }
     }
     if (MODE >= 2 && lane == 0) tc::bulk_wait0();
   }
   __syncthreads();
-  if (warp == 1) tc::tmem_dealloc(tmem, p.tmem_cols);
+  if (PAIR) {
+    tc::cluster_sync();  // no remote arrive / operand read of the peer is still in flight
+    if (warp == 1) tc::tmem_dealloc_pair(tmem, p.tmem_cols);
+  } else if (warp == 1) {
+    tc::tmem_dealloc(tmem, p.tmem_cols);
+  }
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -851,6 +905,15 @@ int num_sms() {
 
 int gemm_path();
 
+// KL_GEMM_PAIR=0 keeps every GEMM on single CTAs (A/B testing).
+static bool getenv_flag_nopair() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("KL_GEMM_PAIR");
+    v = (e && e[0] == '0') ? 1 : 0;
+  }
+  return v == 1;
+}
 // KL_GEMM_EPI1=1 forces the MODE 0/1 epilogues (A/B testing).
 static bool getenv_flag_epi1() {
   static int v = -1;
@@ -995,6 +1058,18 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
   p.BN = bn;
   p.tiles_n = (g.N + bn - 1) / bn;
   p.tiles_m = (g.M + BM - 1) / BM;
+  // Tile order.  M-adjacent (default): the CTAs of one wave share an N tile,
+  // so B is read once and A streams.  When A (M x K per output batch) is
+  // larger than the L2 can keep across the N passes and the larger operand,
+  // M-adjacent re-reads A from HBM once per N tile (ncu, c4 QKV projection:
+  // 803 MB DRAM reads for a 134 MB A); N-adjacent makes the tiles_n CTAs that
+  // share an A block run in the same wave.
+  {
+    const long long a_bytes = (long long)g.M * g.K * 2, b_bytes = (long long)g.N * g.K * 2;
+    int nf = p.tiles_n > 1 && a_bytes > b_bytes && a_bytes > (48LL << 20) ? 1 : 0;
+    if (const char* v = getenv("KL_GEMM_NFAST")) nf = atoi(v);  // A/B testing
+    p.n_fast = nf;
+  }
   p.nb1 = g.nb1;
   p.nb2 = g.nb2;
   p.red1 = g.red1;
@@ -1049,11 +1124,32 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
     p.x_tma = make_map(&tx_map, g.aux, g.N, g.M, g.c_rs, g.red2 ? 1 : g.nb2, s2c, g.red1 ? 1 : g.nb1, s1c,
                        128 / esz_c, 32, &h2, &h1, true, esz_c) && h2 == p.c_has2 && h1 == p.c_has1;
   }
+  // CTA pairs (cta_group::2) for the TMA-store epilogues on N tiles of 128 /
+  // 256 with at least two 128-row blocks; the workspace split-K path and the
+  // MODE 0/1 epilogues stay single-CTA.
+  // Only for long mainloops (K >= 512) over at least two waves of tiles: a
+  // pair needs both SMs of a TPC free at once, which costs overlap with the
+  // concurrent graph branches on short GEMMs (measured: c2, K = 256, step
+  // 6.20 -> 6.37 ms with pairs everywhere; c4 29.9 -> 29.4 ms).
+  const long long tiles128 = (long long)((g.M + BM - 1) / BM) * ((g.N + bn - 1) / bn) * n_out0;
+  bool pair = mode2 && bn % 128 == 0 && (g.M + BM - 1) / BM >= 2 && k_tot >= 512 && tiles128 >= 2LL * num_sms() &&
+              !getenv_flag_nopair();
+  if (pair) {  // the split plan the launch below makes for the pair tile count must not use the workspace
+    bool wsp = false;
+    const long long tiles2 = (long long)((g.M + 2 * BM - 1) / (2 * BM)) * p.tiles_n * p.n_out;
+    if (plan_splits(tiles2, &wsp) > 1 && wsp) pair = false;
+  }
+  if (pair) {
+    p.tiles_m = (g.M + 2 * BM - 1) / (2 * BM);
+    p.b_boxes = b_n ? (bn / 2 + 63) / 64 : 1;
+    p.b_stage_bytes = b_n ? p.b_boxes * 64 * BK * 2 : (bn / 2) * BK * 2;
+  }
+  const uint32_t stage_p = p.a_stage_bytes + p.b_stage_bytes;
   p.r_boxes = use_r ? (bn + 63) / 64 : 0;
   p.r_bufs = bn > 128 ? 1 : 2;
   const uint32_t rbytes = (uint32_t)p.r_bufs * p.r_boxes * 16384;
   // dynamic smem budget: 227 KB minus the 33 KB static epilogue staging
-  p.stages = std::min<int>(8, (int)((188 * 1024 - rbytes) / stage));
+  p.stages = std::min<int>(8, (int)((188 * 1024 - rbytes) / stage_p));
   if (p.stages < 2) return KL_EUNSUPPORTED;
   p.acc_stride = bn > 128 ? 256 : (bn > 64 ? 128 : (bn > 32 ? 64 : 32));
   p.tmem_cols = 2 * p.acc_stride;
@@ -1068,7 +1164,8 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
       return KL_EUNSUPPORTED;
   }
   if (b_k) {
-    if (!make_map(&tb, g.B, g.K, g.N, g.b_cs, g.nb2, g.b_s2, g.nb1, g.b_s1, BK, bn, &p.b_has2, &p.b_has1))
+    if (!make_map(&tb, g.B, g.K, g.N, g.b_cs, g.nb2, g.b_s2, g.nb1, g.b_s1, BK, pair ? bn / 2 : bn, &p.b_has2,
+                  &p.b_has1))
       return KL_EUNSUPPORTED;
   } else {
     if (!make_map(&tb, g.B, g.N, g.K, g.b_rs, g.nb2, g.b_s2, g.nb1, g.b_s1, 64, BK, &p.b_has2, &p.b_has1))
@@ -1093,7 +1190,7 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
     p.vec_r = g.R && g.r_cs == 1 && g.r_rs % 2 == 0 && (g.r_s1 % 2 == 0) && (g.r_s2 % 2 == 0) && al(g.R);
   }
 
-  const size_t smem = 1024 + (size_t)p.stages * stage + rbytes + (2 * p.stages + 8) * 8 + 16 + 4 * 256 * 4;
+  const size_t smem = 1024 + (size_t)p.stages * stage_p + rbytes + (2 * p.stages + 8) * 8 + 16 + 4 * 256 * 4;
   const int tiles = p.tiles_m * p.tiles_n * p.n_out;
   const int iters = ((g.red1 ? g.nb1 : 1) * (g.red2 ? g.nb2 : 1)) * p.kblocks;
   p.ws = nullptr;
@@ -1103,7 +1200,7 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
     if (wsp) p.ws = g.ws;
   }
   const int total = tiles * p.splits;
-  const int grid = std::min(total, num_sms());
+  const int grid = pair ? 2 * std::min(total, num_sms() / 2) : std::min(total, num_sms());
   const bool plain = e.alpha == 1.f && e.beta == 0.f && !e.bias && !e.row_limit && !e.aux_mode && e.n_act == 0 &&
                      !g.R;
   {
@@ -1111,16 +1208,42 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
     if (trace < 0) trace = getenv("KL_GEMM_TRACE") ? 1 : 0;
     if (trace)
       fprintf(stderr, "gemm_tc M=%d N=%d K=%d nb=%dx%d red=%d%d c=%s beta=%g bias=%d aux=%d act=%d/%d R=%d lim=%d "
-              "mode2=%d bn=%d splits=%d ws=%d\n", g.M, g.N, g.K, g.nb1, g.nb2, g.red1, g.red2,
+              "mode2=%d bn=%d splits=%d ws=%d pair=%d stages=%d\n", g.M, g.N, g.K, g.nb1, g.nb2, g.red1, g.red2,
               g.c_dtype == KL_BF16 ? "bf16" : "f32", e.beta, e.bias != nullptr, e.aux_mode, e.n_act, e.act_group,
-              g.R != nullptr, e.row_limit != nullptr, (int)mode2, bn, p.splits, p.ws != nullptr);
+              g.R != nullptr, e.row_limit != nullptr, (int)mode2, bn, p.splits, p.ws != nullptr, (int)(pair && !p.ws),
+              p.stages);
   }
   auto launch = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     launch_k(kern, grid, NTHREADS, smem, s, ta, tb, use_r ? tr : ta, mode2 ? tc_map : ta, p.x_tma ? tx_map : ta, p,
              e);
   };
-  if (mode2 && !p.ws) {
+  auto launch_pair = [&](auto kern) {  // clusters of 2 CTAs (a TPC's two SMs)
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(NTHREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    cudaLaunchKernelEx(&cfg, kern, ta, tb, use_r ? tr : ta, mode2 ? tc_map : ta, p.x_tma ? tx_map : ta, p, e);
+  };
+  if (pair && !p.ws) {
+    const bool full = e.bias || e.n_act || e.aux_mode;
+    if (g.c_dtype == KL_BF16)
+      full ? launch_pair(gemm_tc_kernel<bf16, 3, true>) : launch_pair(gemm_tc_kernel<bf16, 2, true>);
+    else
+      full ? launch_pair(gemm_tc_kernel<float, 3, true>) : launch_pair(gemm_tc_kernel<float, 2, true>);
+  } else if (mode2 && !p.ws) {
     const bool full = e.bias || e.n_act || e.aux_mode;
     if (g.c_dtype == KL_BF16) full ? launch(gemm_tc_kernel<bf16, 3>) : launch(gemm_tc_kernel<bf16, 2>);
     else full ? launch(gemm_tc_kernel<float, 3>) : launch(gemm_tc_kernel<float, 2>);

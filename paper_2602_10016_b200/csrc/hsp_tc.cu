@@ -667,11 +667,11 @@ __global__ void __launch_bounds__(NT, 1)
 // alone fill the shared memory, so the d = 512 kernels stream their operands
 // in 64-column atoms:
 //
-// Forward, persistent CTAs over (sample, query tile) items (sample-major, so
-// the query tiles of one sample run on neighbouring CTAs and share its S
-// blocks through L2), each item in two passes h over the 256-column halves of
-// the pooled output (Z recomputed per pass; the online softmax sees the same
-// Z both times, so both halves use identical P):
+// Forward, persistent CTAs over (sample, query tile, output half h) items
+// (sample-major, so the query tiles and halves of one sample run on
+// neighbouring CTAs and share its S blocks through L2); each item computes
+// the 256-column half h of the pooled output, recomputing Z (the online
+// softmax sees the same Z in both halves, so both use identical P):
 //   warp 0     TMA: per S block, 8 (Qt atom, S atom) stages into a 4-slot
 //              ring (Z operands), then the block's half-h S atoms (the O
 //              operand) into one slot
@@ -705,7 +705,7 @@ __global__ void __launch_bounds__(NT, 1)
   uint64_t* o_empty = os_full + 9;
   uint32_t* tslot = (uint32_t*)(os_full + 10);
 
-  const int W = p.B * p.qtiles;
+  const int W = p.B * p.qtiles * 2;  // (sample, query tile, output half) items
   const int i0 = (int)((long long)W * blockIdx.x / gridDim.x);
   const int i1 = (int)((long long)W * (blockIdx.x + 1) / gridDim.x);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -741,9 +741,9 @@ __global__ void __launch_bounds__(NT, 1)
     if (lane == 0) {
       int zc = 0, oc = 0;
       for (int idx = i0; idx < i1; ++idx) {
-        const int b = idx / p.qtiles, qt = idx % p.qtiles;
+        const int b = idx / (2 * p.qtiles), qt = (idx >> 1) % p.qtiles, h = idx & 1;
         const int nb = nblocks(p.lengths, b);
-        for (int h = 0; h < 2 && nb > 0; ++h) {
+        {
           for (int j = 0; j < nb; ++j) {
 #pragma unroll 1
             for (int a = 0; a < NA; ++a, ++zc) {
@@ -785,9 +785,9 @@ __global__ void __launch_bounds__(NT, 1)
         ++zb;
       };
       for (int idx = i0; idx < i1; ++idx) {
-        const int b = idx / p.qtiles;
+        const int b = idx / (2 * p.qtiles);
         const int nb = nblocks(p.lengths, b);
-        for (int h = 0; h < 2 && nb > 0; ++h) {
+        if (nb > 0) {
           mma_z();
           for (int j = 0; j < nb; ++j) {
             if (j + 1 < nb) mma_z();
@@ -814,7 +814,7 @@ __global__ void __launch_bounds__(NT, 1)
     const uint32_t trow = tmem + ((uint32_t)(qtr * 32) << 16);
     int zc = 0, pc = 0, t = 0;
     for (int idx = i0; idx < i1; ++idx) {
-      const int b = idx / p.qtiles, qt = idx % p.qtiles;
+      const int b = idx / (2 * p.qtiles), qt = (idx >> 1) % p.qtiles, h = idx & 1;
       const int len = p.lengths[b];
       const int nb = nblocks(p.lengths, b);
       const int q = qt * TB + r;
@@ -826,12 +826,12 @@ __global__ void __launch_bounds__(NT, 1)
         if (orow) {
           const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll 4
-          for (int c = 0; c < D; c += 8) *reinterpret_cast<uint4*>(orow + c) = z4;
-          p.LSE[(long long)b * p.HQ + q] = INFINITY;
+          for (int c = 0; c < DH; c += 8) *reinterpret_cast<uint4*>(orow + h * DH + c) = z4;
+          if (h == 1) p.LSE[(long long)b * p.HQ + q] = INFINITY;
         }
         continue;
       }
-      for (int h = 0; h < 2; ++h) {
+      {
         float mref = -INFINITY, l = 0.f;
         for (int j = 0; j < nb; ++j, ++zc, ++pc) {
           const int z = zc & 1;
@@ -1186,7 +1186,7 @@ extern "C" int kl_hsp_fwd(const kl_hsp_args* a, void* stream) {
     return KL_EUNSUPPORTED;
   }
   cudaStream_t s = (cudaStream_t)stream;
-  const int items = p.B * p.qtiles;
+  const int items = p.B * p.qtiles * (a->d == 512 ? 2 : 1);
   int grid = std::min(items, tc_num_sms());
   if (const char* g = getenv("KL_HSP_GRID")) grid = std::max(1, std::min(grid, atoi(g)));  // testing
   if (a->d == 512) {
