@@ -370,7 +370,8 @@ def roofline_table(work, kernels, ms_step, burst, sustained, hbm, peak_kind, con
 
 def workload(args, cfg, B, world):
     ev = cfg.events[0]
-    return {"workload": f"kunlun_{args.config}_train_step", "model": "kunlun", "layers": cfg.L, "d": cfg.d,
+    abl = f"_ablation_{args.ablation.replace(',', '+')}" if args.ablation else ""
+    return {"workload": f"kunlun_{args.config}{abl}_train_step", "model": "kunlun", "layers": cfg.L, "d": cfg.d,
             "heads": cfg.heads, "seq_len": ev.T, "window": ev.w, "events": len(cfg.events),
             "n_seeds": ev.n_seeds, "budget": ev.budget, "kron_rank": ev.rank, "n_ctx": cfg.n_ctx,
             "n_kv": cfg.n_kv, "n_sum": cfg.n_sum, "experts": cfg.experts, "compskip": cfg.compskip,
@@ -386,6 +387,8 @@ def main():
     ap.add_argument("--config", default="c4", help="BASELINE.json configs: c4 (the 1/2/4/8-GPU DP config, default), "
                     "c1, c2, c3")
     ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--ablation", default="", help="PAPER.md Table 2 switch: pffn (pffn_original instead of GDPA), "
+                    "pma (PMA summaries instead of HSP), full (full attention instead of SWA); comma-separated")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--cpu-workers", type=int, default=32)
     ap.add_argument("--no-cpu", action="store_true")
@@ -417,6 +420,11 @@ def main():
     cfg, B = CONFIGS[args.config]()
     if args.batch:
         B = args.batch
+    for a in filter(None, args.ablation.split(",")):
+        if a not in ("pffn", "pma", "full"):
+            raise SystemExit(f"unknown ablation {a!r}")
+        setattr(cfg, {"pffn": "pffn", "pma": "summarizer", "full": "attention"}[a],
+                {"pffn": "original", "pma": "pma", "full": "full"}[a])
 
     if args.impl == "reference":
         run_reference(args, cfg, B, rank, world)

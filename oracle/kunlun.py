@@ -504,3 +504,80 @@ def merge_grads(dst: dict, src: dict) -> None:
 
 def zero_like_grads(p: dict) -> dict:
     return defaultdict(float)
+
+
+# ---------------------------------------------------------------------------
+# Ablation baselines (Table 2)
+# ---------------------------------------------------------------------------
+
+
+def pffn_original(x_sum, s, p: dict, prefix: str, hidden_act: str = "silu"):
+    """Original PFFN: a per-sample (d, d) transform f = reshape(W2 act(W1
+    flat(X_sum) + b1) + b2, (d, d)) applied rowwise, Y = S f^T, no residual
+    (gdpa.py:227-257).  Returns (Y, bwd) with bwd(g) -> (dS, dX_sum, grads)."""
+    from .ops import act_dfn, act_fwd
+
+    w1, b1 = p[f"{prefix}/w1"], p[f"{prefix}/b1"]
+    w2, b2 = p[f"{prefix}/w2"], p[f"{prefix}/b2"]
+    d = s.shape[1]
+    flat = x_sum.reshape(-1)
+    pre = w1 @ flat + b1
+    h = act_fwd(hidden_act, pre)
+    f = (w2 @ h + b2).reshape(d, d)
+    y = s @ f.T
+
+    def bwd(g):
+        df = g.T @ s                      # (d, d): dY = S f^T -> df = g^T S
+        ds = g @ f
+        dfv = df.reshape(-1)
+        grads = {f"{prefix}/w2": np.outer(dfv, h), f"{prefix}/b2": dfv.copy()}
+        dh = w2.T @ dfv
+        dpre = dh * act_dfn(hidden_act, pre, h)
+        grads[f"{prefix}/w1"] = np.outer(dpre, flat)
+        grads[f"{prefix}/b1"] = dpre
+        dflat = w1.T @ dpre
+        return ds, dflat.reshape(x_sum.shape), grads
+
+    return y, bwd
+
+
+def pma_summarize(s, p: dict, prefix: str, budget: int):
+    """The "w/o HSP (use PMA)" summary of PAPER.md Table 2: [CLS | PMA tokens |
+    recent], the middle n_tok rows pooled by learnable queries
+    (pma = MHA(Q_learn, S, S), seqsum.py:26-34) instead of
+    seed attention + SumKronLinear.  Empty sequences give zeros."""
+    n_cls, n_tok, n_rec = split_for_budget(budget)
+    d = s.shape[1]
+    parts, bwds = [], []
+    for key, n in (("cls", n_cls), ("pma", n_tok)):
+        if n == 0:
+            continue
+        if s.shape[0] == 0:
+            parts.append(np.zeros((n, d)))
+            bwds.append(None)
+            continue
+        q = p[f"{prefix}/{key}_queries"]
+        o, ob = multi_head_attention(q, s, p, f"{prefix}/{key}_attn")
+        parts.append(o)
+        bwds.append((key, n, ob))
+    rec, r_bwd = recent_rows(s, n_rec)
+    parts.append(rec)
+    rows = np.concatenate(parts, axis=0)
+
+    def bwd(g):
+        grads = {}
+        ds = np.zeros_like(s)
+        off = 0
+        for entry, part in zip(bwds, parts[:len(bwds)]):
+            n = part.shape[0]
+            if entry is not None:
+                key, _, ob = entry
+                dq, dkv, gr = ob(g[off:off + n])
+                merge_grads(grads, gr)
+                _acc(grads, f"{prefix}/{key}_queries", dq)
+                ds = ds + dkv
+            off += n
+        ds = ds + r_bwd(g[off:])
+        return ds, grads
+
+    return rows, bwd

@@ -44,6 +44,10 @@ class ModelSpec:
     gdpa_acts: tuple = ()
     expert_hidden: int = 0     # default 2d
     head_hidden: int = 0       # default 4d
+    pffn: str = "gdpa"         # Table 2 ablations: "original" (gdpa.py:227-257)
+    summarizer: str = "hsp"    # "pma": learnable-query PMA summaries
+    attention: str = "window"  # "full": mha_full (attention.py:115-121)
+    pffn_hidden: int = 0       # default 2d
 
     def __post_init__(self):
         if not self.gdpa_acts:
@@ -53,6 +57,8 @@ class ModelSpec:
             self.expert_hidden = 2 * self.d
         if not self.head_hidden:
             self.head_hidden = 4 * self.d
+        if not self.pffn_hidden:
+            self.pffn_hidden = 2 * self.d
 
     @property
     def n_tot(self) -> int:
@@ -95,16 +101,31 @@ def init_params(spec: ModelSpec, seed: int = 0) -> dict:
     for l in range(spec.L):
         p[f"L{l}/pool"] = rng.normal(0.0, 1.0 / np.sqrt(spec.n_ctx), (spec.n_sum, spec.n_ctx))
         for e, ev in enumerate(spec.events):
-            pre = f"L{l}/ev{e}/gdpa"
             fan = spec.n_sum * d
-            for h in range(H):
-                p[f"{pre}/head{h}/w_q"] = rng.normal(0.0, 1.0 / np.sqrt(d), (d_h, d))
-                p[f"{pre}/head{h}/w_kgen"] = rng.normal(0.0, 1.0 / np.sqrt(fan), (spec.n_kv * d_h, fan))
-                p[f"{pre}/head{h}/w_vgen"] = rng.normal(0.0, 1.0 / np.sqrt(fan), (spec.n_kv * d_h, fan))
-            p[f"{pre}/w_out"] = rng.normal(0.0, 0.5 / np.sqrt(d), (d, d))
+            if spec.pffn == "original":  # gdpa.py:235-245
+                pre = f"L{l}/ev{e}/pffn"
+                hid = spec.pffn_hidden
+                p[f"{pre}/w1"] = rng.normal(0.0, 1.0 / np.sqrt(fan), (hid, fan))
+                p[f"{pre}/b1"] = np.zeros(hid)
+                p[f"{pre}/w2"] = rng.normal(0.0, 0.1 / np.sqrt(hid), (d * d, hid))
+                p[f"{pre}/b2"] = np.zeros(d * d)
+            else:
+                pre = f"L{l}/ev{e}/gdpa"
+                for h in range(H):
+                    p[f"{pre}/head{h}/w_q"] = rng.normal(0.0, 1.0 / np.sqrt(d), (d_h, d))
+                    p[f"{pre}/head{h}/w_kgen"] = rng.normal(0.0, 1.0 / np.sqrt(fan), (spec.n_kv * d_h, fan))
+                    p[f"{pre}/head{h}/w_vgen"] = rng.normal(0.0, 1.0 / np.sqrt(fan), (spec.n_kv * d_h, fan))
+                p[f"{pre}/w_out"] = rng.normal(0.0, 0.5 / np.sqrt(d), (d, d))
             mha(f"L{l}/ev{e}/mha")
             n_cls, n_tok, _ = K.split_for_budget(ev.budget)
             sp = f"L{l}/ev{e}/summ"
+            if spec.summarizer == "pma":
+                if n_cls > 0:
+                    p[f"{sp}/cls_queries"] = rng.normal(0.0, 1.0 / np.sqrt(d), (n_cls, d))
+                    mha(f"{sp}/cls_attn")
+                p[f"{sp}/pma_queries"] = rng.normal(0.0, 1.0 / np.sqrt(d), (n_tok, d))
+                mha(f"{sp}/pma_attn")
+                continue
             p[f"{sp}/hsp/seeds"] = rng.normal(0.0, 1.0 / np.sqrt(d), (ev.n_seeds, d))
             p[f"{sp}/hsp/norm_gain"] = np.ones(d)
             mha(f"{sp}/hsp/attn")
@@ -145,7 +166,7 @@ def layer_forward(spec: ModelSpec, p: dict, l: int, flags, X, S_list, H_prev):
     kv, kv_bwd = [], []
     H_list, h_bwd = [], []
     for e, ev in enumerate(spec.events):
-        if skip_pffn:
+        if skip_pffn or spec.pffn == "original":
             kv.append(None)
             kv_bwd.append(None)
         else:
@@ -156,7 +177,8 @@ def layer_forward(spec: ModelSpec, p: dict, l: int, flags, X, S_list, H_prev):
             H_list.append(H_prev[e])
             h_bwd.append(None)
         else:
-            rows, rb = K.hsp_summarize(S_list[e], p, f"L{l}/ev{e}/summ", ev.budget)
+            summ = K.pma_summarize if spec.summarizer == "pma" else K.hsp_summarize
+            rows, rb = summ(S_list[e], p, f"L{l}/ev{e}/summ", ev.budget)
             H_list.append(rows)
             h_bwd.append(rb)
     Xn, gi_bwd = K.global_interaction(X, H_list, p, f"L{l}/gi", spec.experts)
@@ -165,10 +187,15 @@ def layer_forward(spec: ModelSpec, p: dict, l: int, flags, X, S_list, H_prev):
         s = S_list[e]
         if skip_pffn:
             st, gb = s, None
+        elif spec.pffn == "original":
+            st, pb = K.pffn_original(xsum, s, p, f"L{l}/ev{e}/pffn")
+            gb = ("original", pb)
         else:
             st, gb = K.gdpa_forward(s, kv[e], p, f"L{l}/ev{e}/gdpa", float(ev.T), spec.gdpa_acts)
         if skip_attn:
             so, ab = st, None
+        elif spec.attention == "full":
+            so, ab = K.mha_full(st, p, f"L{l}/ev{e}/mha")
         else:
             so, ab = K.mha_window(st, p, f"L{l}/ev{e}/mha", ev.w, ev.causal)
         S_out.append(so)
@@ -186,7 +213,11 @@ def layer_forward(spec: ModelSpec, p: dict, l: int, flags, X, S_list, H_prev):
             if ab is not None:
                 g, gr = ab(g)
                 K.merge_grads(grads, gr)
-            if gb is not None:
+            if isinstance(gb, tuple):  # pffn_original: dS and dX_sum directly
+                g, dxs, gr = gb[1](g)
+                K.merge_grads(grads, gr)
+                dxsum = dxsum + dxs
+            elif gb is not None:
                 g, dkvs, gr = gb(g)
                 K.merge_grads(grads, gr)
                 dxs, gr = kv_bwd[e](dkvs)

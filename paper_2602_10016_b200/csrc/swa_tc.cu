@@ -2382,6 +2382,9 @@ bool map3(CUtensorMap* m, const void* ptr, long long inner, int T, int B, long l
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// The tile walks hold a band of at most three 128-blocks (the dK / dV kernel
+// stages the LSE / D of <= 6 64-query half-blocks per tile): w <= 128.  Wider
+// windows (mha_full) run the SIMT kernels.
 bool supported(const SwaP& p) {
   return p.dtype == KL_BF16 && p.d_h == DH && p.w <= TB && kl_tcgen05_available();
 }

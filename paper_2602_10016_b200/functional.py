@@ -1108,3 +1108,25 @@ class _HeadProj(torch.autograd.Function):
 def head_proj(X, wref):
     """X (B, n, H, d) -> (B, n, H*d_h)."""
     return _HeadProj.apply(X, wref.P.flat, wref)
+
+
+class _RowsSelect(torch.autograd.Function):
+    """out[b, t] = a[b, t] for t < lengths[b], else b_[b, t] (ablation paths:
+    pass-through padding rows of an op without a residual)."""
+
+    @staticmethod
+    def forward(ctx, a, b_, lengths):
+        T = a.shape[1]
+        mask = (torch.arange(T, device=a.device)[None, :] < lengths[:, None].long())[..., None]
+        ctx.save_for_backward(mask)
+        return torch.where(mask, a, b_)
+
+    @staticmethod
+    def backward(ctx, g):
+        (mask,) = ctx.saved_tensors
+        z = torch.zeros((), device=g.device, dtype=g.dtype)
+        return torch.where(mask, g, z), torch.where(mask, z, g), None
+
+
+def rows_select(a, b_, lengths):
+    return _RowsSelect.apply(a, b_, lengths)

@@ -193,3 +193,70 @@ def gdpa_forward_jagged(batch: JaggedBatch, x_sums, cfg: GdpaConfig, p: WeightGe
     values = np.concatenate([out[i, : lengths[i]] for i in range(batch.batch_size)], axis=0)
     ts = None if batch.timestamps is None else batch.timestamps.copy()
     return JaggedBatch(values, batch.offsets.copy(), ts)
+
+
+# ---------------------------------------------------------------------------
+# "w/o GDPA" ablation baseline (Table 2): the original PFFN
+
+
+@dataclass
+class PffnParams:
+    """Two-layer MLP emitting a (d, d) rowwise transform from the summary
+    (gdpa.py:227-245): registry names ``{prefix}/w1, b1, w2, b2``, the
+    reference's init distributions and draw order."""
+
+    P: Params
+    prefix: str
+    dim: int
+    hidden: int
+    hidden_act: str = "silu"
+
+    @property
+    def w1(self):
+        return f"{self.prefix}/w1"
+
+    @property
+    def b1(self):
+        return f"{self.prefix}/b1"
+
+    @property
+    def w2(self):
+        return f"{self.prefix}/w2"
+
+    @property
+    def b2(self):
+        return f"{self.prefix}/b2"
+
+    @classmethod
+    def create(cls, params: Params, prefix: str, dim: int, n_sum: int, ctx_dim: int, hidden: int,
+               rng: np.random.Generator | None = None) -> "PffnParams":
+        rng = rng if rng is not None else np.random.default_rng(0)
+        fan = n_sum * ctx_dim
+        p = cls(params, prefix, dim, hidden)
+        params.add(p.w1, rng.normal(0.0, 1.0 / np.sqrt(fan), (hidden, fan)))
+        params.add(p.b1, np.zeros(hidden))
+        params.add(p.w2, rng.normal(0.0, 0.1 / np.sqrt(hidden), (dim * dim, hidden)))
+        params.add(p.b2, np.zeros(dim * dim))
+        return p
+
+
+def pffn_original(x_sum: torch.Tensor, s: torch.Tensor, p: PffnParams, lengths=None) -> torch.Tensor:
+    """Original formulation (gdpa.py:247-257): per sample f = reshape(W2
+    act(W1 flat(X_sum) + b1) + b2, (d, d)), Y = S f^T — no residual (the
+    non-stackable baseline kept for ablation).  Batched: two bias / activation
+    GEMM epilogues for f, one batched GEMM for Y."""
+    squeeze = s.dim() == 2
+    if squeeze:
+        s, x_sum = s.unsqueeze(0), x_sum.unsqueeze(0)
+    B, d = s.shape[0], s.shape[-1]
+    if d != p.dim:
+        raise ShapeError(f"sequence width {d} does not match the PFFN dim {p.dim}")
+    flat = x_sum.reshape(B, -1)
+    h = F.linear(flat, p.P, p.w1, p.b1, act=p.hidden_act)
+    f = F.linear(h, p.P, p.w2, p.b2).view(B, d, d)
+    y = F.mm(s, f.transpose(1, 2))
+    if lengths is not None:  # padding rows pass through (the reference sees only the valid rows)
+        y = F.rows_select(y, s, _lengths(s, lengths))
+    if numerics_check_mode() == "eager":
+        flag_nonfinite(y, "pffn_original")
+    return y.squeeze(0) if squeeze else y

@@ -39,16 +39,29 @@ def layer_macs(cfg, flags, live_seq: bool = True, formulation: str = "executed",
         T = ev.T if lengths is None else int(lengths[e])
         split = SummarySplit.for_budget(ev.budget)
         n_s, n_cls, n_tok = ev.n_seeds, split.n_cls, split.n_tokens
-        if live_seq and not flags.skip_pffn:
+        pffn = getattr(cfg, "pffn", "gdpa")
+        if live_seq and not flags.skip_pffn and pffn == "original":
+            # pffn_original (gdpa.py:247-257): f = W2 act(W1 flat + b1) + b2, Y = S f^T
+            hid = getattr(cfg, "pffn_hidden", 2 * d)
+            out["wgen"] += cfg.n_sum * cfg.n_ctx * d + hid * cfg.n_sum * d + d * d * hid
+            out["gdpa"] += T * d * d
+        elif live_seq and not flags.skip_pffn:
             out["wgen"] += cfg.n_sum * cfg.n_ctx * d + 2 * cfg.n_kv * d_h * H * cfg.n_sum * d
             if formulation == "executed":
                 out["gdpa"] += 2 * cfg.n_kv * d * d + 2 * T * d * H * cfg.n_kv
             else:
                 out["gdpa"] += 2 * T * d * d + 2 * T * cfg.n_kv * d
         if live_seq and not flags.skip_self_attention:
+            w = max(ev.T - 1, 0) if getattr(cfg, "attention", "window") == "full" else ev.w
             out["swa_proj"] += 4 * T * d * d
-            out["swa_core"] += 2 * _support(ev.T, ev.w, ev.causal, T) * d
-        if not flags.skip_hsp:
+            out["swa_core"] += 2 * _support(ev.T, w, ev.causal and w == ev.w, T) * d
+        if not flags.skip_hsp and getattr(cfg, "summarizer", "hsp") == "pma":
+            n_q = n_tok + n_cls  # learnable-query PMA pooling (folded, like the CLS set), no SumKron
+            if formulation == "executed":
+                out["hsp"] += 2 * T * d * H * n_q + 2 * n_q * d * d
+            else:
+                out["hsp"] += n_q * (2 * d * d + 2 * T * d) + 2 * T * d * d
+        elif not flags.skip_hsp:
             n_q = n_s + n_cls
             if formulation == "executed":
                 # scores S Qt^T and pooling P^T S over all H*n_q queries, then

@@ -16,8 +16,8 @@ import numpy as np
 import torch
 
 from . import functional as F
-from .attention import MhaParams, WindowSpec, mha_window
-from .gdpa import GdpaConfig, WeightGenParams, fold_kv, generate_kv, summarize_nonseq
+from .attention import MhaParams, WindowSpec, mha_full, mha_window
+from .gdpa import GdpaConfig, PffnParams, WeightGenParams, fold_kv, generate_kv, pffn_original, summarize_nonseq
 from .interaction import ExpertPartition, InteractionParams, global_interaction
 from .mlp import Mlp
 from .seqsum import SummarizerParams, SummarySplit, hsp_summarize
@@ -85,6 +85,13 @@ class ModelConfig:
     gdpa_acts: tuple = ()
     expert_hidden: int = 0
     head_hidden: int = 0
+    # PAPER.md Table 2 ablations (lines 355-381): "original" = the pffn_original
+    # baseline instead of GDPA (gdpa.py:227-257); "pma" = learnable-query PMA
+    # summaries instead of HSP; "full" = full self-attention instead of SWA
+    pffn: str = "gdpa"
+    summarizer: str = "hsp"
+    attention: str = "window"
+    pffn_hidden: int = 0
 
     def __post_init__(self):
         if self.d % self.heads:
@@ -94,6 +101,10 @@ class ModelConfig:
             self.gdpa_acts = tuple(c[h % len(c)] for h in range(self.heads))
         self.expert_hidden = self.expert_hidden or 2 * self.d
         self.head_hidden = self.head_hidden or 4 * self.d
+        self.pffn_hidden = self.pffn_hidden or 2 * self.d
+        if self.pffn not in ("gdpa", "original") or self.summarizer not in ("hsp", "pma") or \
+                self.attention not in ("window", "full"):
+            raise ValueError("ablation switches: pffn gdpa|original, summarizer hsp|pma, attention window|full")
         ExpertPartition.contiguous(self.n_tot, self.experts)
 
     @property
@@ -151,10 +162,13 @@ class KunlunModel:
             pool = P.add(f"L{l}/pool", rng.normal(0.0, 1.0 / np.sqrt(cfg.n_ctx), (cfg.n_sum, cfg.n_ctx)))
             wg, mh, sm = [], [], []
             for e, ev in enumerate(cfg.events):
-                wg.append(WeightGenParams.create(P, f"L{l}/ev{e}/gdpa", cfg.gdpa_cfg(e), cfg.n_sum, d, rng))
+                if cfg.pffn == "original":
+                    wg.append(PffnParams.create(P, f"L{l}/ev{e}/pffn", d, cfg.n_sum, d, cfg.pffn_hidden, rng))
+                else:
+                    wg.append(WeightGenParams.create(P, f"L{l}/ev{e}/gdpa", cfg.gdpa_cfg(e), cfg.n_sum, d, rng))
                 mh.append(MhaParams.create(P, f"L{l}/ev{e}/mha", d, H, rng))
                 sm.append(SummarizerParams.create(P, f"L{l}/ev{e}/summ", d, SummarySplit.for_budget(ev.budget),
-                                                  ev.n_seeds, ev.rank, H, rng))
+                                                  ev.n_seeds, ev.rank, H, rng, mode=cfg.summarizer))
             gi = InteractionParams.create(P, f"L{l}/gi", part, cfg.n_ctx, d, cfg.expert_hidden, rng)
             self.layers.append(LayerParams(pool, wg, mh, sm, gi))
         self.head = Mlp.create(P, "head", [cfg.n_ctx * d, cfg.head_hidden, 1], ["silu", "identity"], rng)
@@ -171,7 +185,7 @@ class KunlunModel:
         CLS queries), folded once per step before layer 0 (query_rows)."""
         keys = []
         for l in range(self.cfg.L):
-            if self.flags[l].skip_hsp:
+            if self.flags[l].skip_hsp or self.cfg.summarizer != "hsp":
                 continue
             for s in self.layers[l].summ:
                 keys += [s.hsp.seeds, s.hsp.gain, s.hsp.attn.wqkv]
@@ -193,7 +207,7 @@ class KunlunModel:
         cfg = self.cfg
         out = {}
         layers = [l for l in range(cfg.L) if not self.flags[l].skip_hsp]
-        if not layers:
+        if not layers or cfg.summarizer != "hsp":
             return out
         for e in range(len(cfg.events)):
             sp = [self.layers[l].summ[e] for l in layers]
@@ -245,14 +259,18 @@ class KunlunModel:
                 def run():
                     ev = cfg.events[e]
                     s = S_list[e]
-                    if live_seq and not flags.skip_pffn:
+                    if live_seq and not flags.skip_pffn and cfg.pffn == "original":
+                        s = pffn_original(xsum, s, lp.wg[e], lengths[e])  # Table 2 "w/o GDPA" (no residual)
+                    elif live_seq and not flags.skip_pffn:
                         k, v = generate_kv(xsum, lp.wg[e], cfg.gdpa_cfg(e))
                         kt, vt = fold_kv(k, v, lp.wg[e])
                         s = F.gdpa_core(s, kt, vt, lengths[e], cfg.gdpa_acts, cfg.n_kv, 1.0 / float(ev.T),
                                         sink=sinks[e])
                         if numerics_check_mode() == "eager":
                             flag_nonfinite(s, f"layer {l} event {e} GDPA")
-                    if live_seq and not flags.skip_self_attention:
+                    if live_seq and not flags.skip_self_attention and cfg.attention == "full":
+                        s = mha_full(s, lp.mha[e], lengths[e])  # Table 2 "w/o SWA"
+                    elif live_seq and not flags.skip_self_attention:
                         s = mha_window(s, lp.mha[e], WindowSpec(ev.w, ev.causal), lengths[e])
                     return s
                 return run

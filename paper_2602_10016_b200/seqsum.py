@@ -182,23 +182,44 @@ class SummaryBundle:
 
 @dataclass
 class SummarizerParams:
-    """Everything for one event type's SummaryBundle (seqsum.py:165-183)."""
+    """Everything for one event type's SummaryBundle (seqsum.py:165-183).
 
-    hsp: HspParams
+    ``mode="pma"`` is the "w/o HSP (use PMA)" ablation of PAPER.md Table 2
+    (lines 355-381; PMA = MHA(Q_learnable, S, S)): the
+    n_tokens middle rows are pooled by learnable queries
+    (``{prefix}/pma_queries`` with ``{prefix}/pma_attn``) instead of seed
+    attention + SumKronLinear."""
+
+    hsp: HspParams | None
     cls_queries: str | None
     cls_attn: MhaParams | None
     split: SummarySplit
+    mode: str = "hsp"
+    pma_queries: str | None = None
+    pma_attn: MhaParams | None = None
+
+    @property
+    def P(self) -> Params:
+        return self.hsp.P if self.hsp is not None else self.pma_attn.P
 
     @classmethod
     def create(cls, params: Params, prefix: str, dim: int, split: SummarySplit, n_seeds: int, rank: int,
-               heads: int, rng: np.random.Generator | None = None) -> "SummarizerParams":
+               heads: int, rng: np.random.Generator | None = None, mode: str = "hsp") -> "SummarizerParams":
         rng = rng if rng is not None else np.random.default_rng(0)
-        hsp = HspParams.create(params, f"{prefix}/hsp", dim, n_seeds, split.n_tokens, rank, heads, rng)
+        if mode not in ("hsp", "pma"):
+            raise ValueError(f"summarizer mode must be 'hsp' or 'pma', got {mode!r}")
+        hsp = None
+        if mode == "hsp":
+            hsp = HspParams.create(params, f"{prefix}/hsp", dim, n_seeds, split.n_tokens, rank, heads, rng)
         queries = attn = None
         if split.n_cls > 0:
             queries = params.add(f"{prefix}/cls_queries", rng.normal(0.0, 1.0 / np.sqrt(dim), (split.n_cls, dim)))
             attn = MhaParams.create(params, f"{prefix}/cls_attn", dim, heads, rng)
-        return cls(hsp, queries, attn, split)
+        pq = pa = None
+        if mode == "pma":
+            pq = params.add(f"{prefix}/pma_queries", rng.normal(0.0, 1.0 / np.sqrt(dim), (split.n_tokens, dim)))
+            pa = MhaParams.create(params, f"{prefix}/pma_attn", dim, heads, rng)
+        return cls(hsp, queries, attn, split, mode, pq, pa)
 
 
 def recent_rows(s, n_recent: int, lengths=None):
@@ -219,6 +240,8 @@ def hsp_summarize(s, p: SummarizerParams, lengths=None, sink=None, q_rows=None) 
     S = s.unsqueeze(0) if squeeze else s
     B, T, d = S.shape
     lens = _lengths(S, lengths)
+    if p.mode == "pma":
+        return _pma_summarize(S, p, lens, squeeze)
     hp = p.hsp
     H = hp.attn.heads
     n_s = hp.n_seeds
@@ -253,3 +276,19 @@ def hsp_summarize(s, p: SummarizerParams, lengths=None, sink=None, q_rows=None) 
         bundle = SummaryBundle(cls_tok[0], hsp_tok[0], rec[0])
     assert bundle.total_rows == p.split.total
     return bundle
+
+
+def _pma_summarize(S, p: SummarizerParams, lens, squeeze) -> SummaryBundle:
+    """[CLS | PMA(Q_learnable) | recent] (the Table 2 PMA ablation): both query
+    sets pool through the batch-shared-query path (fused tcgen05 pooling)."""
+    B, T, d = S.shape
+    P = p.P
+    cls_tok = pma(S, F.PRef(P, p.cls_queries), p.cls_attn, lens) if p.split.n_cls > 0 else S.new_zeros(B, 0, d)
+    tok = pma(S, F.PRef(P, p.pma_queries), p.pma_attn, lens)
+    rec = recent_rows(S, p.split.n_recent, lens) if p.split.n_recent > 0 else S.new_zeros(B, 0, d)
+    if numerics_check_mode() == "eager":
+        for t in (cls_tok, tok, rec):
+            flag_nonfinite(t, "pma summary")
+    if squeeze:
+        return SummaryBundle(cls_tok[0], tok[0], rec[0])
+    return SummaryBundle(cls_tok, tok, rec)

@@ -30,6 +30,14 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 # B200 drop-in package of the same name
 sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
 sys.path.insert(0, REF)
+# the reference's kunlun is a namespace package: a regular package of the same
+# name anywhere on sys.path (the repo's B200 drop-in kunlun/) would win, so
+# bind the name to the reference's directory explicitly
+import types  # noqa: E402
+
+_ref_pkg = types.ModuleType("kunlun")
+_ref_pkg.__path__ = [os.path.join(REF, "kunlun")]
+sys.modules["kunlun"] = _ref_pkg
 
 from kunlun import attention as A  # noqa: E402
 from kunlun import gdpa as G  # noqa: E402
@@ -348,6 +356,46 @@ def case_rote():
     _save("rote.npz", **out)
 
 
+def case_ablation():
+    """Table 2 ablation baselines from the reference's own building blocks:
+    gdpa.pffn_original (gdpa.py:227-257) and a PMA-only summary
+    [CLS | pma(Q_learn, S) | recent] (seqsum.py:26-34, 186-196)."""
+    rng = np.random.default_rng(20261019)
+    d, n_sum, n_ctx, t_len, hidden = 8, 2, 5, 9, 12
+    params = T.Params()
+    pp = G.PffnParams.create(params, "pf", d, n_sum, d, hidden, rng)
+    s = params.add("in/S", rng.normal(0, 1 / np.sqrt(d), (t_len, d)))
+    xsum = params.add("in/Xsum", rng.normal(0, 1, (n_sum, d)))
+    r = rng.normal(0, 1, (t_len, d))
+    with T.Tape(params) as tape:
+        y = G.pffn_original(xsum, s, pp)
+        loss = _dot(y, r)
+    grads = _backward(tape, loss)
+    _save("pffn_original.npz", **_pack("param", {k: v.data for k, v in params.items()}),
+          **_pack("grad", {k: v.data for k, v in grads.items()}), out_Y=y.data, cot_Y=r,
+          meta=np.array([d, n_sum, n_ctx, t_len, hidden]))
+    for t_len, tag in ((10, "t10"), (0, "t0")):
+        d, H, budget = 16, 2, 8
+        n_cls, n_tok, n_rec = 2, 4, 2
+        params = T.Params()
+        cq = params.add("s/cls_queries", rng.normal(0, 1 / np.sqrt(d), (n_cls, d)))
+        ca = A.MhaParams.create(params, "s/cls_attn", d, H, rng)
+        pq = params.add("s/pma_queries", rng.normal(0, 1 / np.sqrt(d), (n_tok, d)))
+        pa = A.MhaParams.create(params, "s/pma_attn", d, H, rng)
+        s = params.add("in/S", rng.normal(0, 1, (t_len, d)))
+        r = rng.normal(0, 1, (budget, d))
+        with T.Tape(params) as tape:
+            if t_len:
+                rows = T.concat([Q.pma(s, cq, ca), Q.pma(s, pq, pa), Q.recent_rows(s, n_rec)], axis=0)
+            else:
+                rows = T.constant(np.zeros((budget, d)))
+            loss = _dot(rows, r)
+        grads = _backward(tape, loss) if t_len else {k: T.Tensor(np.zeros_like(v.data)) for k, v in params.items()}
+        _save(f"pma_summary_{tag}.npz", **_pack("param", {k: v.data for k, v in params.items()}),
+              **_pack("grad", {k: v.data for k, v in grads.items()}), out_rows=rows.data, cot=r,
+              meta=np.array([d, H, budget, t_len]))
+
+
 def main():
     rng = np.random.default_rng(20260218)
     case_gdpa(rng, ("silu", "relu", "identity", "tanh"), "default")
@@ -368,6 +416,9 @@ def main():
 if __name__ == "__main__":
     if sys.argv[1:] == ["rote"]:
         case_rote()
+    elif sys.argv[1:] == ["ablation"]:
+        case_ablation()
     else:
         main()
         case_rote()
+        case_ablation()

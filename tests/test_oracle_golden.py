@@ -200,3 +200,37 @@ def test_banded_mha_equals_dense(T, w, causal, length):
     assert np.abs(dd - db).max() <= 1e-12 * max(1.0, np.abs(dd).max())
     for k in gd:
         assert np.abs(gd[k] - gb[k]).max() <= 1e-12 * max(1.0, np.abs(gd[k]).max()), k
+
+
+def test_pffn_original_golden():
+    """oracle.kunlun.pffn_original vs the reference's gdpa.pffn_original (Table 2 'w/o GDPA')."""
+    from oracle import kunlun as K
+
+    z = np.load(os.path.join(G, "pffn_original.npz"))
+    p = {k[len("param:"):]: z[k] for k in z.files if k.startswith("param:")}
+    g = {k[len("grad:"):]: z[k] for k in z.files if k.startswith("grad:")}
+    y, bwd = K.pffn_original(p["in/Xsum"], p["in/S"], p, "pf")
+    assert np.abs(y - z["out_Y"]).max() < 1e-10
+    ds, dx, gr = bwd(z["cot_Y"])
+    assert np.abs(ds - g["in/S"]).max() < 1e-10
+    assert np.abs(dx - g["in/Xsum"]).max() < 1e-10
+    for k, v in gr.items():
+        assert np.abs(v - g[k]).max() < 1e-10, k
+
+
+@pytest.mark.parametrize("tag", ["t10", "t0"])
+def test_pma_summary_golden(tag):
+    """oracle.kunlun.pma_summarize vs [pma(CLS) | pma(Q_learn) | recent] run on the reference (Table 2 'w/o HSP')."""
+    from oracle import kunlun as K
+
+    z = np.load(os.path.join(G, f"pma_summary_{tag}.npz"))
+    p = {k[len("param:"):]: z[k] for k in z.files if k.startswith("param:")}
+    g = {k[len("grad:"):]: z[k] for k in z.files if k.startswith("grad:")}
+    d, H, budget, t_len = (int(v) for v in z["meta"])
+    rows, bwd = K.pma_summarize(p["in/S"], p, "s", budget)
+    assert np.abs(rows - z["out_rows"]).max() < 1e-10
+    ds, gr = bwd(z["cot"])
+    if t_len:
+        assert np.abs(ds - g["in/S"]).max() < 1e-10
+        for k, v in gr.items():
+            assert np.abs(v - g[k]).max() < 1e-10, k
