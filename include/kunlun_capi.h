@@ -365,6 +365,22 @@ typedef struct kl_rote_args {
 } kl_rote_args;
 int kl_rote(const kl_rote_args* a, void* stream);
 
+/* Non-sequence embedding, fused (preproc.py:103-136: embed_dense,
+ * embed_sparse, assemble_nonseq): out (B, n_sparse + 1, d) in dtype with
+ *   out[b, 0]     = proj (d, m) @ x_dense[b]          (x_dense (B, m) fp32)
+ *   out[b, 1 + i] = table[offsets[i] + ids[b, i]]     (table (vocab_tot, d):
+ *                   the per-feature tables stacked; ids (B, n_sparse) int64)
+ * The caller validates 0 <= ids[b, i] < vocab_i (IndexError, preproc.py:121);
+ * the kernel clamps to the stacked table for memory safety.
+ * Backward: dtable[offsets[i] + ids[b, i]] += dout[b, 1 + i] (fp32 atomics)
+ * and dproj += dout[:, 0]^T x_dense (fp32, accumulated). */
+int kl_embed_nonseq_fwd(int B, int n_sparse, int d, int m, int dtype, const float* x_dense, const void* proj,
+                        const void* table, const long long* offsets, const long long* ids, long long vocab_tot,
+                        void* out, void* stream);
+int kl_embed_nonseq_bwd(int B, int n_sparse, int d, int m, int dtype, const float* x_dense, const void* dout,
+                        const long long* offsets, const long long* ids, long long vocab_tot, float* dtable,
+                        float* dproj, void* stream);
+
 /* Normalized entropy (Eq. A1-A2; SPEC.md:553-561 normalized_entropy):
  * kind 0: p holds probabilities (clipped to [1e-12, 1-1e-12]); kind 1: p holds logits.
  * y labels in {0,1}; fp64 accumulation in one block.  out (device, 4 doubles) =

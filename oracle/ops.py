@@ -217,3 +217,50 @@ def mlp_rows(x: np.ndarray, ws, bs, acts):
         return g, dws, dbs
 
     return h, bwd
+
+
+# ---------------------------------------------------------------------------
+# preproc.py:103-152 — raw features to embeddings
+
+
+def embed_nonseq(x_dense, ids, proj, tables):
+    """[proj x | table_0[id_0] | ...] (embed_dense preproc.py:103-108 as a
+    matvec, embed_sparse 111-116 as a row lookup, assemble_nonseq 119-127).
+    Returns (out (n+1, d), bwd(g) -> (dproj, [dtable_i]))."""
+    rows = [proj @ x_dense] + [t[int(i)] for t, i in zip(tables, ids)]
+    out = np.stack(rows)
+
+    def bwd(g):
+        dproj = np.outer(g[0], x_dense)
+        dts = []
+        for k, (t, i) in enumerate(zip(tables, ids)):
+            dt = np.zeros_like(t)
+            dt[int(i)] += g[1 + k]
+            dts.append(dt)
+        return dproj, dts
+
+    return out, bwd
+
+
+def align_right(seqs, target_len: int):
+    """preproc.py:146-152."""
+    out = []
+    for s in seqs:
+        pad = target_len - s.shape[0]
+        if pad < 0:
+            raise ValueError(f"sequence of length {s.shape[0]} exceeds target {target_len}")
+        out.append(np.concatenate([np.zeros((pad, s.shape[1])), s], axis=0) if pad else s)
+    return out
+
+
+def fuse_sequences(seqs, ws, bs, acts):
+    """Rowwise MLP over the (T, K*d) concatenation (preproc.py:130-143)."""
+    cat = np.concatenate(seqs, axis=1)
+    y, mbwd = mlp_rows(cat, ws, bs, acts)
+
+    def bwd(g):
+        dcat, dws, dbs = mbwd(g)
+        widths = np.cumsum([0] + [s.shape[1] for s in seqs])
+        return [dcat[:, a:b] for a, b in zip(widths[:-1], widths[1:])], dws, dbs
+
+    return y, bwd

@@ -123,6 +123,10 @@ _SIGS = {
     "kl_set_pdl": ([C.c_int], None),
     "kl_last_gemm_path": ([], C.c_int),
     "kl_path_hits": ([C.c_int], C.c_ulonglong),
+    "kl_embed_nonseq_fwd": ([C.c_int, C.c_int, C.c_int, C.c_int, C.c_int] + [C.c_void_p] * 5 + [C.c_longlong, C.c_void_p,
+                             C.c_void_p], C.c_int),
+    "kl_embed_nonseq_bwd": ([C.c_int, C.c_int, C.c_int, C.c_int, C.c_int] + [C.c_void_p] * 4 + [C.c_longlong] +
+                            [C.c_void_p] * 3, C.c_int),
     "kl_reset_path_hits": ([], None),
     "kl_gemm": ([C.POINTER(GemmArgs), C.c_void_p], C.c_int),
     "kl_gdpa_fwd": ([C.POINTER(GdpaArgs), C.c_void_p], C.c_int),

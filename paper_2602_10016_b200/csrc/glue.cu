@@ -1130,3 +1130,96 @@ extern "C" int kl_rowdot(int rows, int d, int dtype, const void* a, long long a_
   count_launch();
   return launch_check("rowdot");
 }
+
+// ---------------------------------------------------------------------------
+// Non-sequence embedding (preproc.py:103-136: embed_dense, embed_sparse,
+// assemble_nonseq) fused into one pass: out[b, 0] = proj x_dense[b] (m small:
+// per-thread dot products), out[b, 1 + i] = table[offset_i + ids[b, i]] (row
+// gathers of the stacked per-feature tables).  One block per sample row
+// (b, i), threads over d.  HBM-bound: one read of each gathered row, one write.
+namespace kl {
+namespace emb {
+template <typename T>
+__global__ void __launch_bounds__(128) embed_fwd_kernel(int n_sparse, int d, int m, const float* xd, const T* proj,
+                                                        const T* table, const long long* offsets,
+                                                        const long long* ids, long long vocab_tot, T* out) {
+  KL_PDL_ENTRY();
+  const int b = blockIdx.y, i = blockIdx.x;  // i = 0: dense row, i >= 1: sparse feature i - 1
+  T* o = out + ((long long)b * (n_sparse + 1) + i) * d;
+  if (i == 0) {
+    const float* x = xd + (long long)b * m;
+    for (int c = threadIdx.x; c < d; c += blockDim.x) {
+      float acc = 0.f;
+      for (int k = 0; k < m; ++k) acc = fmaf(ldf(proj + (long long)c * m + k), __ldg(x + k), acc);
+      stf(o + c, acc);
+    }
+    return;
+  }
+  long long row = offsets[i - 1] + ids[(long long)b * n_sparse + (i - 1)];
+  row = row < 0 ? 0 : (row >= vocab_tot ? vocab_tot - 1 : row);  // host-validated; clamped for memory safety
+  const T* src = table + row * d;
+  for (int c = threadIdx.x; c < d; c += blockDim.x) o[c] = src[c];
+}
+
+// VJP: dtable[row] += dout[b, 1 + i] (fp32 atomics: several samples can pick
+// one id), dproj[c, k] += sum_b dout[b, 0, c] x_dense[b, k].
+template <typename T>
+__global__ void __launch_bounds__(128) embed_bwd_kernel(int B, int n_sparse, int d, int m, const float* xd,
+                                                        const T* dout, const long long* offsets, const long long* ids,
+                                                        long long vocab_tot, float* dtable, float* dproj) {
+  KL_PDL_ENTRY();
+  const int i = blockIdx.x;
+  if (i == 0) {  // dense projection gradient: block per (c chunk); loops over the batch
+    for (int c = threadIdx.x + blockIdx.y * blockDim.x; c < d; c += blockDim.x * gridDim.y)
+      for (int k = 0; k < m; ++k) {
+        float acc = 0.f;
+        for (int b = 0; b < B; ++b)
+          acc = fmaf(ldf(dout + (long long)b * (n_sparse + 1) * d + c), __ldg(xd + (long long)b * m + k), acc);
+        dproj[(long long)c * m + k] += acc;
+      }
+    return;
+  }
+  for (int b = blockIdx.y; b < B; b += gridDim.y) {
+    long long row = offsets[i - 1] + ids[(long long)b * n_sparse + (i - 1)];
+    if (row < 0 || row >= vocab_tot) continue;
+    const T* g = dout + ((long long)b * (n_sparse + 1) + i) * d;
+    float* dst = dtable + row * d;
+    for (int c = threadIdx.x; c < d; c += blockDim.x) atomicAdd(dst + c, ldf(g + c));
+  }
+}
+}  // namespace emb
+}  // namespace kl
+
+extern "C" int kl_embed_nonseq_fwd(int B, int n_sparse, int d, int m, int dtype, const float* x_dense,
+                                   const void* proj, const void* table, const long long* offsets,
+                                   const long long* ids, long long vocab_tot, void* out, void* stream) {
+  if (B < 0 || n_sparse < 0 || d < 1 || m < 0) { set_error("kl_embed_nonseq_fwd: bad extents"); return KL_EBADSHAPE; }
+  if (B == 0) return KL_OK;
+  dim3 grid(n_sparse + 1, B);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == KL_F32)
+    launch_k(kl::emb::embed_fwd_kernel<float>, grid, 128, 0, s, n_sparse, d, m, x_dense, (const float*)proj,
+             (const float*)table, offsets, ids, vocab_tot, (float*)out);
+  else
+    launch_k(kl::emb::embed_fwd_kernel<bf16>, grid, 128, 0, s, n_sparse, d, m, x_dense, (const bf16*)proj, (const bf16*)table,
+             offsets, ids, vocab_tot, (bf16*)out);
+  count_launch();
+  return launch_check("embed_nonseq_fwd");
+}
+
+extern "C" int kl_embed_nonseq_bwd(int B, int n_sparse, int d, int m, int dtype, const float* x_dense,
+                                   const void* dout, const long long* offsets, const long long* ids,
+                                   long long vocab_tot, float* dtable, float* dproj, void* stream) {
+  if (B < 0 || n_sparse < 0 || d < 1 || m < 0) { set_error("kl_embed_nonseq_bwd: bad extents"); return KL_EBADSHAPE; }
+  if (B == 0) return KL_OK;
+  dim3 grid(n_sparse + 1, std::min(B, 64));
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == KL_F32)
+    launch_k(kl::emb::embed_bwd_kernel<float>, grid, 128, 0, s, B, n_sparse, d, m, x_dense, (const float*)dout, offsets, ids,
+             vocab_tot, dtable, dproj);
+  else
+    launch_k(kl::emb::embed_bwd_kernel<bf16>, grid, 128, 0, s, B, n_sparse, d, m, x_dense, (const bf16*)dout, offsets, ids,
+             vocab_tot, dtable, dproj);
+  count_launch();
+  return launch_check("embed_nonseq_bwd");
+}

@@ -396,6 +396,39 @@ def case_ablation():
               meta=np.array([d, H, budget, t_len]))
 
 
+def case_preproc():
+    """preproc.embed_dense / embed_sparse / assemble_nonseq / fuse_sequences /
+    align_right of the reference (preproc.py:103-152)."""
+    rng = np.random.default_rng(20261020)
+    d, m, vocabs = 8, 3, [5, 7, 2]
+    params = T.Params()
+    proj = params.add("emb/dense_proj", rng.normal(0, 1 / np.sqrt(m), (d, m)))
+    tabs = [params.add(f"emb/sparse{i}", rng.normal(0, 1 / np.sqrt(d), (v, d))) for i, v in enumerate(vocabs)]
+    x = rng.normal(0, 1, m)
+    ids = np.array([4, 0, 1])
+    r = rng.normal(0, 1, (len(vocabs) + 1, d))
+    with T.Tape(params) as tape:
+        out = PP.assemble_nonseq(PP.embed_dense(x, proj), [PP.embed_sparse(i, t) for i, t in zip(ids, tabs)])
+        loss = _dot(out, r)
+    grads = _backward(tape, loss)
+    # fusion of K = 2 right-aligned sequences
+    K_, t_len = 2, 6
+    fusion = M.Mlp.create(params, "fus", [K_ * d, 12, d], ["silu", "identity"], rng)
+    raw = [rng.normal(0, 1, (4, d)), rng.normal(0, 1, (6, d))]
+    al = PP.align_right(raw, t_len)
+    seqs = [params.add(f"in/seq{k}", a) for k, a in enumerate(al)]
+    rf = rng.normal(0, 1, (t_len, d))
+    with T.Tape(params) as tape:
+        fo = PP.fuse_sequences(seqs, fusion)
+        loss = _dot(fo, rf)
+    fgrads = _backward(tape, loss)
+    _save("preproc.npz", **_pack("param", {k: v.data for k, v in params.items()}),
+          **_pack("grad", {k: v.data for k, v in grads.items()}),
+          **_pack("fgrad", {k: v.data for k, v in fgrads.items()}),
+          x=x, ids=ids, out=out.data, cot=r, fused=fo.data, fcot=rf, raw0=raw[0], raw1=raw[1],
+          meta=np.array([d, m, t_len] + vocabs))
+
+
 def main():
     rng = np.random.default_rng(20260218)
     case_gdpa(rng, ("silu", "relu", "identity", "tanh"), "default")
@@ -418,7 +451,10 @@ if __name__ == "__main__":
         case_rote()
     elif sys.argv[1:] == ["ablation"]:
         case_ablation()
+    elif sys.argv[1:] == ["preproc"]:
+        case_preproc()
     else:
         main()
         case_rote()
         case_ablation()
+        case_preproc()

@@ -234,3 +234,35 @@ def test_pma_summary_golden(tag):
         assert np.abs(ds - g["in/S"]).max() < 1e-10
         for k, v in gr.items():
             assert np.abs(v - g[k]).max() < 1e-10, k
+
+
+def test_preproc_golden():
+    """oracle.ops embed_nonseq / fuse_sequences / align_right vs the
+    reference's embed_dense + embed_sparse + assemble_nonseq, fuse_sequences
+    and align_right (preproc.py:103-152)."""
+    from oracle import ops
+
+    z = np.load(os.path.join(G, "preproc.npz"))
+    p = {k[len("param:"):]: z[k] for k in z.files if k.startswith("param:")}
+    g = {k[len("grad:"):]: z[k] for k in z.files if k.startswith("grad:")}
+    fg = {k[len("fgrad:"):]: z[k] for k in z.files if k.startswith("fgrad:")}
+    d, m, t_len = (int(v) for v in z["meta"][:3])
+    vocabs = [int(v) for v in z["meta"][3:]]
+    tabs = [p[f"emb/sparse{i}"] for i in range(len(vocabs))]
+    out, bwd = ops.embed_nonseq(z["x"], z["ids"], p["emb/dense_proj"], tabs)
+    assert np.abs(out - z["out"]).max() < 1e-12
+    dproj, dts = bwd(z["cot"])
+    assert np.abs(dproj - g["emb/dense_proj"]).max() < 1e-12
+    for i, dt in enumerate(dts):
+        assert np.abs(dt - g[f"emb/sparse{i}"]).max() < 1e-12
+    al = ops.align_right([z["raw0"], z["raw1"]], t_len)
+    assert np.array_equal(al[0], p["in/seq0"]) and np.array_equal(al[1], p["in/seq1"])
+    ws, bs = [p["fus/w0"], p["fus/w1"]], [p["fus/b0"], p["fus/b1"]]
+    fo, fb = ops.fuse_sequences(al, ws, bs, ["silu", "identity"])
+    assert np.abs(fo - z["fused"]).max() < 1e-10
+    dseqs, dws, dbs = fb(z["fcot"])
+    for k in range(2):
+        assert np.abs(dseqs[k] - fg[f"in/seq{k}"]).max() < 1e-10
+    for i in range(2):
+        assert np.abs(dws[i] - fg[f"fus/w{i}"]).max() < 1e-10
+        assert np.abs(dbs[i] - fg[f"fus/b{i}"]).max() < 1e-10
