@@ -28,6 +28,9 @@ class EventSpec:
     n_seeds: int
     rank: int
     causal: bool = False
+    d: int = 0        # event width / heads / depth (0 = the model's): event-level
+    heads: int = 0    # personalization
+    layers: int = 0
 
 
 @dataclass
@@ -64,6 +67,21 @@ class ModelSpec:
     def n_tot(self) -> int:
         return self.n_ctx + sum(e.budget for e in self.events)
 
+    def ev_d(self, e: int) -> int:
+        return self.events[e].d or self.d
+
+    def ev_heads(self, e: int) -> int:
+        return self.events[e].heads or self.heads
+
+    def ev_layers(self, e: int) -> int:
+        return self.events[e].layers or self.L
+
+    def ev_acts(self, e: int) -> tuple:
+        H = self.ev_heads(e)
+        if H == self.heads:
+            return tuple(self.gdpa_acts)
+        return tuple(DEFAULT_ACTIVATION_CYCLE[h % len(DEFAULT_ACTIVATION_CYCLE)] for h in range(H))
+
 
 def compskip_config(L: int, enabled: bool = True):
     """Alg. 4: even l -> (skip_attn=T,
@@ -84,13 +102,13 @@ def init_params(spec: ModelSpec, seed: int = 0) -> dict:
     d_h = d // H
     p = {}
 
-    def mha(prefix):
-        sig = 1.0 / np.sqrt(d)
-        for h in range(H):
-            p[f"{prefix}/head{h}/w_q"] = rng.normal(0.0, sig, (d_h, d))
-            p[f"{prefix}/head{h}/w_k"] = rng.normal(0.0, sig, (d_h, d))
-            p[f"{prefix}/head{h}/w_v"] = rng.normal(0.0, sig, (d_h, d))
-        p[f"{prefix}/w_out"] = rng.normal(0.0, 0.5 * sig, (d, d))
+    def mha(prefix, dd=d, HH=H):
+        sig = 1.0 / np.sqrt(dd)
+        for h in range(HH):
+            p[f"{prefix}/head{h}/w_q"] = rng.normal(0.0, sig, (dd // HH, dd))
+            p[f"{prefix}/head{h}/w_k"] = rng.normal(0.0, sig, (dd // HH, dd))
+            p[f"{prefix}/head{h}/w_v"] = rng.normal(0.0, sig, (dd // HH, dd))
+        p[f"{prefix}/w_out"] = rng.normal(0.0, 0.5 * sig, (dd, dd))
 
     def mlp(prefix, widths):
         for i, (fi, fo) in enumerate(zip(widths[:-1], widths[1:])):
@@ -101,34 +119,40 @@ def init_params(spec: ModelSpec, seed: int = 0) -> dict:
     for l in range(spec.L):
         p[f"L{l}/pool"] = rng.normal(0.0, 1.0 / np.sqrt(spec.n_ctx), (spec.n_sum, spec.n_ctx))
         for e, ev in enumerate(spec.events):
+            if l >= spec.ev_layers(e):  # the event's stack ended (hold-last)
+                continue
+            dd, HH = spec.ev_d(e), spec.ev_heads(e)
+            dh = dd // HH
             fan = spec.n_sum * d
             if spec.pffn == "original":  # gdpa.py:235-245
                 pre = f"L{l}/ev{e}/pffn"
                 hid = spec.pffn_hidden
                 p[f"{pre}/w1"] = rng.normal(0.0, 1.0 / np.sqrt(fan), (hid, fan))
                 p[f"{pre}/b1"] = np.zeros(hid)
-                p[f"{pre}/w2"] = rng.normal(0.0, 0.1 / np.sqrt(hid), (d * d, hid))
-                p[f"{pre}/b2"] = np.zeros(d * d)
+                p[f"{pre}/w2"] = rng.normal(0.0, 0.1 / np.sqrt(hid), (dd * dd, hid))
+                p[f"{pre}/b2"] = np.zeros(dd * dd)
             else:
                 pre = f"L{l}/ev{e}/gdpa"
-                for h in range(H):
-                    p[f"{pre}/head{h}/w_q"] = rng.normal(0.0, 1.0 / np.sqrt(d), (d_h, d))
-                    p[f"{pre}/head{h}/w_kgen"] = rng.normal(0.0, 1.0 / np.sqrt(fan), (spec.n_kv * d_h, fan))
-                    p[f"{pre}/head{h}/w_vgen"] = rng.normal(0.0, 1.0 / np.sqrt(fan), (spec.n_kv * d_h, fan))
-                p[f"{pre}/w_out"] = rng.normal(0.0, 0.5 / np.sqrt(d), (d, d))
-            mha(f"L{l}/ev{e}/mha")
+                for h in range(HH):
+                    p[f"{pre}/head{h}/w_q"] = rng.normal(0.0, 1.0 / np.sqrt(dd), (dh, dd))
+                    p[f"{pre}/head{h}/w_kgen"] = rng.normal(0.0, 1.0 / np.sqrt(fan), (spec.n_kv * dh, fan))
+                    p[f"{pre}/head{h}/w_vgen"] = rng.normal(0.0, 1.0 / np.sqrt(fan), (spec.n_kv * dh, fan))
+                p[f"{pre}/w_out"] = rng.normal(0.0, 0.5 / np.sqrt(dd), (dd, dd))
+            mha(f"L{l}/ev{e}/mha", dd, HH)
+            if dd != d:  # learnable linear adapter of the summaries
+                p[f"L{l}/ev{e}/adapter"] = rng.normal(0.0, 1.0 / np.sqrt(dd), (d, dd))
             n_cls, n_tok, _ = K.split_for_budget(ev.budget)
             sp = f"L{l}/ev{e}/summ"
             if spec.summarizer == "pma":
                 if n_cls > 0:
-                    p[f"{sp}/cls_queries"] = rng.normal(0.0, 1.0 / np.sqrt(d), (n_cls, d))
-                    mha(f"{sp}/cls_attn")
-                p[f"{sp}/pma_queries"] = rng.normal(0.0, 1.0 / np.sqrt(d), (n_tok, d))
-                mha(f"{sp}/pma_attn")
+                    p[f"{sp}/cls_queries"] = rng.normal(0.0, 1.0 / np.sqrt(dd), (n_cls, dd))
+                    mha(f"{sp}/cls_attn", dd, HH)
+                p[f"{sp}/pma_queries"] = rng.normal(0.0, 1.0 / np.sqrt(dd), (n_tok, dd))
+                mha(f"{sp}/pma_attn", dd, HH)
                 continue
-            p[f"{sp}/hsp/seeds"] = rng.normal(0.0, 1.0 / np.sqrt(d), (ev.n_seeds, d))
-            p[f"{sp}/hsp/norm_gain"] = np.ones(d)
-            mha(f"{sp}/hsp/attn")
+            p[f"{sp}/hsp/seeds"] = rng.normal(0.0, 1.0 / np.sqrt(dd), (ev.n_seeds, dd))
+            p[f"{sp}/hsp/norm_gain"] = np.ones(dd)
+            mha(f"{sp}/hsp/attn", dd, HH)
             base = np.zeros((ev.n_seeds, n_tok))
             bounds = K.hsp_init_bounds(ev.n_seeds, n_tok)
             for j in range(n_tok):
@@ -136,10 +160,10 @@ def init_params(spec: ModelSpec, seed: int = 0) -> dict:
                 base[lo:hi, j] = 1.0 / (hi - lo)
             for i in range(ev.rank):
                 p[f"{sp}/hsp/kron{i}/seq_map"] = base / ev.rank + rng.normal(0.0, 0.02, (ev.n_seeds, n_tok))
-                p[f"{sp}/hsp/kron{i}/emb_map"] = np.eye(d) + rng.normal(0.0, 0.02, (d, d))
+                p[f"{sp}/hsp/kron{i}/emb_map"] = np.eye(dd) + rng.normal(0.0, 0.02, (dd, dd))
             if n_cls > 0:
-                p[f"{sp}/cls_queries"] = rng.normal(0.0, 1.0 / np.sqrt(d), (n_cls, d))
-                mha(f"{sp}/cls_attn")
+                p[f"{sp}/cls_queries"] = rng.normal(0.0, 1.0 / np.sqrt(dd), (n_cls, dd))
+                mha(f"{sp}/cls_attn", dd, HH)
         gp = f"L{l}/gi"
         for i, (a, b) in enumerate(ranges):
             n_i = b - a
@@ -165,33 +189,48 @@ def layer_forward(spec: ModelSpec, p: dict, l: int, flags, X, S_list, H_prev):
     xsum, xs_bwd = K.summarize_nonseq(X, p[f"L{l}/pool"])
     kv, kv_bwd = [], []
     H_list, h_bwd = [], []
+    ended = [l >= spec.ev_layers(e) for e in range(len(spec.events))]  # hold-last events
     for e, ev in enumerate(spec.events):
-        if skip_pffn or spec.pffn == "original":
+        if skip_pffn or spec.pffn == "original" or ended[e]:
             kv.append(None)
             kv_bwd.append(None)
         else:
             a, b = K.generate_kv(xsum, p, f"L{l}/ev{e}/gdpa", spec.n_kv)
             kv.append(a)
             kv_bwd.append(b)
-        if skip_hsp:
+        if skip_hsp or ended[e]:
             H_list.append(H_prev[e])
             h_bwd.append(None)
         else:
             summ = K.pma_summarize if spec.summarizer == "pma" else K.hsp_summarize
             rows, rb = summ(S_list[e], p, f"L{l}/ev{e}/summ", ev.budget)
+            akey = f"L{l}/ev{e}/adapter"
+            if akey in p:  # d_e -> d linear adapter
+                A = p[akey]
+                rows_e = rows
+                rows = rows_e @ A.T
+
+                def rb(g, rb=rb, rows_e=rows_e, A=A, akey=akey):
+                    ds, gr = rb(g @ A)
+                    K._acc(gr, akey, g.T @ rows_e)
+                    return ds, gr
             H_list.append(rows)
             h_bwd.append(rb)
     Xn, gi_bwd = K.global_interaction(X, H_list, p, f"L{l}/gi", spec.experts)
     S_out, s_bwd = [], []
     for e, ev in enumerate(spec.events):
         s = S_list[e]
+        if ended[e]:  # the event's sequence passes through
+            S_out.append(s)
+            s_bwd.append((None, None))
+            continue
         if skip_pffn:
             st, gb = s, None
         elif spec.pffn == "original":
             st, pb = K.pffn_original(xsum, s, p, f"L{l}/ev{e}/pffn")
             gb = ("original", pb)
         else:
-            st, gb = K.gdpa_forward(s, kv[e], p, f"L{l}/ev{e}/gdpa", float(ev.T), spec.gdpa_acts)
+            st, gb = K.gdpa_forward(s, kv[e], p, f"L{l}/ev{e}/gdpa", float(ev.T), spec.ev_acts(e))
         if skip_attn:
             so, ab = st, None
         elif spec.attention == "full":
@@ -293,7 +332,7 @@ def model_forward_backward(spec: ModelSpec, p: dict, X, S, lengths, labels, cot=
             K._acc(grads, f"head/w{i}", dws[i])
             K._acc(grads, f"head/b{i}", dbs[i])
         dx = dflat.reshape(spec.n_ctx, spec.d)
-        ds = [np.zeros((lengths[e][b], spec.d)) for e in range(len(spec.events))]
+        ds = [np.zeros((lengths[e][b], spec.ev_d(e))) for e in range(len(spec.events))]
         dh = [None] * len(spec.events)
         for l in reversed(range(spec.L)):
             if cot is not None:

@@ -765,7 +765,11 @@ def _hsp_bwd512(S, Q, lengths, LSE, dO, Dq, acc, ctx):
     return dS, dQ.reshape(Q.shape)
 
 
-HSP_DCOL = True  # softmax-VJP column term from the pooled output (tests A/B it against the t-reduction)
+# softmax-VJP column term of the composition path: False = the t-reduction
+# sum_t P dP inside kl_colsoftmax_bwd, consistent with the fp32 P it
+# recomputes (the bf16-rounded pooled output would put its rounding into the
+# cancellation-heavy query gradient); True = rowdot(dO, pooled)
+HSP_DCOL = False
 
 
 def hsp_pool(S, Q, lengths, splits=None, n_recent=0, sink=None):

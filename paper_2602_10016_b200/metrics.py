@@ -30,12 +30,18 @@ def _support(T: int, w: int, causal: bool, length: int | None = None) -> int:
     return int(band_support_sizes(L, w, causal).sum()) if L > 0 else 0
 
 
-def layer_macs(cfg, flags, live_seq: bool = True, formulation: str = "executed", lengths=None) -> dict:
-    """Per-sample forward MACs of one layer, by component."""
-    d, H = cfg.d, cfg.heads
-    d_h = d // H
+def layer_macs(cfg, flags, live_seq: bool = True, formulation: str = "executed", lengths=None, layer=None) -> dict:
+    """Per-sample forward MACs of one layer, by component (per-event widths,
+    heads and depths: an event whose stack ended before ``layer`` costs
+    nothing; summary adapters count under "hsp")."""
+    D = cfg.d
     out = {"wgen": 0, "gdpa": 0, "swa_proj": 0, "swa_core": 0, "hsp": 0, "sumkron": 0, "gi": 0}
     for e, ev in enumerate(cfg.events):
+        if layer is not None and hasattr(cfg, "ev_layers") and layer >= cfg.ev_layers(e):
+            continue
+        d = cfg.ev_d(e) if hasattr(cfg, "ev_d") else D
+        H = cfg.ev_heads(e) if hasattr(cfg, "ev_heads") else cfg.heads
+        d_h = d // H
         T = ev.T if lengths is None else int(lengths[e])
         split = SummarySplit.for_budget(ev.budget)
         n_s, n_cls, n_tok = ev.n_seeds, split.n_cls, split.n_tokens
@@ -43,10 +49,10 @@ def layer_macs(cfg, flags, live_seq: bool = True, formulation: str = "executed",
         if live_seq and not flags.skip_pffn and pffn == "original":
             # pffn_original (gdpa.py:247-257): f = W2 act(W1 flat + b1) + b2, Y = S f^T
             hid = getattr(cfg, "pffn_hidden", 2 * d)
-            out["wgen"] += cfg.n_sum * cfg.n_ctx * d + hid * cfg.n_sum * d + d * d * hid
+            out["wgen"] += cfg.n_sum * cfg.n_ctx * D + hid * cfg.n_sum * D + d * d * hid
             out["gdpa"] += T * d * d
         elif live_seq and not flags.skip_pffn:
-            out["wgen"] += cfg.n_sum * cfg.n_ctx * d + 2 * cfg.n_kv * d_h * H * cfg.n_sum * d
+            out["wgen"] += cfg.n_sum * cfg.n_ctx * D + 2 * cfg.n_kv * d_h * H * cfg.n_sum * D
             if formulation == "executed":
                 out["gdpa"] += 2 * cfg.n_kv * d * d + 2 * T * d * H * cfg.n_kv
             else:
@@ -75,6 +81,9 @@ def layer_macs(cfg, flags, live_seq: bool = True, formulation: str = "executed",
                 if n_cls:
                     out["hsp"] += (n_cls * d * d + 2 * T * d * d + 2 * n_cls * T * d + n_cls * d * d)
                 out["sumkron"] += ev.rank * (n_tok * n_s * d + n_tok * d * d)
+        if not flags.skip_hsp and d != D:
+            out["hsp"] += ev.budget * d * D  # summary adapter d_e -> d
+    d = D
     part = ExpertPartition.contiguous(cfg.n_tot, cfg.experts)
     for a, b in part.ranges:
         n_i = b - a
@@ -89,7 +98,7 @@ def model_macs(cfg, flags, live, formulation: str = "executed", lengths=None) ->
     """Per-sample forward MACs of the whole model (layers + head)."""
     tot = {}
     for l in range(cfg.L):
-        for k, v in layer_macs(cfg, flags[l], live[l], formulation, lengths).items():
+        for k, v in layer_macs(cfg, flags[l], live[l], formulation, lengths, layer=l).items():
             tot[k] = tot.get(k, 0) + v
     tot["head"] = cfg.n_ctx * cfg.d * cfg.head_hidden + cfg.head_hidden
     tot["total"] = sum(tot.values())

@@ -30,7 +30,11 @@ FOLD_ALL_LAYERS = True  # fold every layer's HSP/CLS queries in one batched pass
 @dataclass
 class EventConfig:
     """Per-event sequence knobs: padded length T, window
-    half-width w, summary token budget, HSP seeds and SumKron rank."""
+    half-width w, summary token budget, HSP seeds and SumKron rank, and the
+    event's own width ``d``, heads and depth ``layers`` (0 = the model's;
+    event-level personalization: an event with fewer layers
+    holds its last summaries for the deeper global layers, and a learnable
+    linear adapter maps its summaries to the model width when d != d_model)."""
 
     T: int
     w: int
@@ -39,10 +43,15 @@ class EventConfig:
     rank: int
     causal: bool = False
     name: str = ""
+    d: int = 0
+    heads: int = 0
+    layers: int = 0
 
     def __post_init__(self):
         if min(self.T, self.budget, self.n_seeds, self.rank) < 1 or self.w < 0:
             raise ValueError("event config values must be positive")
+        if min(self.d, self.heads, self.layers) < 0:
+            raise ValueError("event width / heads / layers must be >= 0 (0 = the model's)")
 
 
 @dataclass
@@ -105,15 +114,36 @@ class ModelConfig:
         if self.pffn not in ("gdpa", "original") or self.summarizer not in ("hsp", "pma") or \
                 self.attention not in ("window", "full"):
             raise ValueError("ablation switches: pffn gdpa|original, summarizer hsp|pma, attention window|full")
+        for e in range(len(self.events)):
+            if self.ev_d(e) % self.ev_heads(e):
+                raise ValueError(f"event {e}: dim {self.ev_d(e)} not divisible by {self.ev_heads(e)} heads")
+            if self.ev_layers(e) > self.L:
+                raise ValueError(f"event {e}: {self.ev_layers(e)} layers > the model's {self.L}")
         ExpertPartition.contiguous(self.n_tot, self.experts)
 
     @property
     def n_tot(self) -> int:
         return self.n_ctx + sum(e.budget for e in self.events)
 
+    def ev_d(self, e: int) -> int:
+        return self.events[e].d or self.d
+
+    def ev_heads(self, e: int) -> int:
+        return self.events[e].heads or self.heads
+
+    def ev_layers(self, e: int) -> int:
+        return self.events[e].layers or self.L
+
+    def ev_acts(self, e: int) -> tuple:
+        H = self.ev_heads(e)
+        if H == self.heads:
+            return tuple(self.gdpa_acts)
+        c = DEFAULT_ACTIVATION_CYCLE
+        return tuple(c[h % len(c)] for h in range(H))
+
     def gdpa_cfg(self, e: int) -> GdpaConfig:
         # tau = the event's padded max length
-        return GdpaConfig(self.d, self.heads, self.n_kv, float(self.events[e].T), tuple(self.gdpa_acts))
+        return GdpaConfig(self.ev_d(e), self.ev_heads(e), self.n_kv, float(self.events[e].T), self.ev_acts(e))
 
 
 @dataclass
@@ -123,6 +153,7 @@ class LayerParams:
     mha: list
     summ: list
     gi: InteractionParams
+    adapters: list = field(default_factory=list)  # per event: (d, d_e) block key or None
 
 
 class _Boundary(torch.autograd.Function):
@@ -160,17 +191,23 @@ class KunlunModel:
         self.layers = []
         for l in range(cfg.L):
             pool = P.add(f"L{l}/pool", rng.normal(0.0, 1.0 / np.sqrt(cfg.n_ctx), (cfg.n_sum, cfg.n_ctx)))
-            wg, mh, sm = [], [], []
+            wg, mh, sm, ad = [], [], [], []
             for e, ev in enumerate(cfg.events):
+                if l >= cfg.ev_layers(e):  # the event's stack ended: its summaries are held (hold-last)
+                    wg.append(None), mh.append(None), sm.append(None), ad.append(None)
+                    continue
+                de, He = cfg.ev_d(e), cfg.ev_heads(e)
                 if cfg.pffn == "original":
-                    wg.append(PffnParams.create(P, f"L{l}/ev{e}/pffn", d, cfg.n_sum, d, cfg.pffn_hidden, rng))
+                    wg.append(PffnParams.create(P, f"L{l}/ev{e}/pffn", de, cfg.n_sum, d, cfg.pffn_hidden, rng))
                 else:
                     wg.append(WeightGenParams.create(P, f"L{l}/ev{e}/gdpa", cfg.gdpa_cfg(e), cfg.n_sum, d, rng))
-                mh.append(MhaParams.create(P, f"L{l}/ev{e}/mha", d, H, rng))
-                sm.append(SummarizerParams.create(P, f"L{l}/ev{e}/summ", d, SummarySplit.for_budget(ev.budget),
-                                                  ev.n_seeds, ev.rank, H, rng, mode=cfg.summarizer))
+                mh.append(MhaParams.create(P, f"L{l}/ev{e}/mha", de, He, rng))
+                sm.append(SummarizerParams.create(P, f"L{l}/ev{e}/summ", de, SummarySplit.for_budget(ev.budget),
+                                                  ev.n_seeds, ev.rank, He, rng, mode=cfg.summarizer))
+                ad.append(P.add(f"L{l}/ev{e}/adapter", rng.normal(0.0, 1.0 / np.sqrt(de), (d, de)))
+                          if de != d else None)
             gi = InteractionParams.create(P, f"L{l}/gi", part, cfg.n_ctx, d, cfg.expert_hidden, rng)
-            self.layers.append(LayerParams(pool, wg, mh, sm, gi))
+            self.layers.append(LayerParams(pool, wg, mh, sm, gi, ad))
         self.head = Mlp.create(P, "head", [cfg.n_ctx * d, cfg.head_hidden, 1], ["silu", "identity"], rng)
         P.finalize(device, dtype)
         if torch.device(device).type == "cuda":
@@ -188,6 +225,8 @@ class KunlunModel:
             if self.flags[l].skip_hsp or self.cfg.summarizer != "hsp":
                 continue
             for s in self.layers[l].summ:
+                if s is None:
+                    continue
                 keys += [s.hsp.seeds, s.hsp.gain, s.hsp.attn.wqkv]
                 if s.cls_queries:
                     keys += [s.cls_queries, s.cls_attn.wqkv]
@@ -210,14 +249,17 @@ class KunlunModel:
         if not layers or cfg.summarizer != "hsp":
             return out
         for e in range(len(cfg.events)):
-            sp = [self.layers[l].summ[e] for l in layers]
+            lay_e = [l for l in layers if l < cfg.ev_layers(e)]
+            if not lay_e:
+                continue
+            sp = [self.layers[l].summ[e] for l in lay_e]
             keys = ([s.hsp.seeds for s in sp], [s.hsp.gain for s in sp], [s.hsp.attn.wqkv for s in sp],
                     [s.cls_queries for s in sp] if sp[0].cls_queries else [],
                     [s.cls_attn.wqkv for s in sp] if sp[0].cls_queries else [])
-            qs = F.query_folds(self.P, keys, cfg.heads, cfg.d // cfg.heads)
+            qs = F.query_folds(self.P, keys, cfg.ev_heads(e), cfg.ev_d(e) // cfg.ev_heads(e))
             if qs is None:
                 return {}
-            for l, q in zip(layers, qs):
+            for l, q in zip(lay_e, qs):
                 out[(l, e)] = q
         return out
 
@@ -238,18 +280,27 @@ class KunlunModel:
         sinks = [F.GradSink() for _ in cfg.events]
         S_list = [F.seq_join(s, k) for s, k in zip(S_list, sinks)]
 
-        events = range(len(cfg.events))
+        events = [e for e in range(len(cfg.events)) if l < cfg.ev_layers(e)]  # events whose stack reaches l
+        held = [e for e in range(len(cfg.events)) if l >= cfg.ev_layers(e)]
+        if held and H_prev is None:
+            raise ValueError("an event's stack ended before the first layer")
 
         def x_branch():  # HSP summaries (per event, parallel branches) -> global interaction
             def hsp(e):
                 def run():
                     qr = qrows.get((l, e)) if qrows else None
-                    return hsp_summarize(S_list[e], lp.summ[e], lengths[e], sink=sinks[e], q_rows=qr).rows()
+                    rows = hsp_summarize(S_list[e], lp.summ[e], lengths[e], sink=sinks[e], q_rows=qr).rows()
+                    if lp.adapters and lp.adapters[e] is not None:  # d_e -> d (learnable linear adapter)
+                        rows = F.linear(rows, self.P, lp.adapters[e])
+                    return rows
                 return run
-            if flags.skip_hsp:
+            if flags.skip_hsp or not events:
                 H_list = list(H_prev)
             else:
-                H_list = F.run_branches([hsp(e) for e in events], X.device, name="ev_x")
+                fresh = F.run_branches([hsp(e) for e in events], X.device, name="ev_x")
+                H_list = list(H_prev) if H_prev is not None else [None] * len(cfg.events)
+                for e, h in zip(events, fresh):
+                    H_list[e] = h  # events whose stack ended keep their last summaries
             return global_interaction(X, H_list, lp.gi), H_list
 
         def s_branch():  # GDPA (weights generated from X) -> windowed self-attention, per event
@@ -264,7 +315,7 @@ class KunlunModel:
                     elif live_seq and not flags.skip_pffn:
                         k, v = generate_kv(xsum, lp.wg[e], cfg.gdpa_cfg(e))
                         kt, vt = fold_kv(k, v, lp.wg[e])
-                        s = F.gdpa_core(s, kt, vt, lengths[e], cfg.gdpa_acts, cfg.n_kv, 1.0 / float(ev.T),
+                        s = F.gdpa_core(s, kt, vt, lengths[e], cfg.ev_acts(e), cfg.n_kv, 1.0 / float(ev.T),
                                         sink=sinks[e])
                         if numerics_check_mode() == "eager":
                             flag_nonfinite(s, f"layer {l} event {e} GDPA")
@@ -274,9 +325,14 @@ class KunlunModel:
                         s = mha_window(s, lp.mha[e], WindowSpec(ev.w, ev.causal), lengths[e])
                     return s
                 return run
-            # events are independent sequences: parallel branches
-            return F.run_branches([seq(e) for e in events], X.device, inputs=[xsum] if xsum is not None else (),
+            # events are independent sequences: parallel branches; the sequence
+            # of an event whose stack ended passes through unchanged
+            outs = F.run_branches([seq(e) for e in events], X.device, inputs=[xsum] if xsum is not None else (),
                                   name="ev_s")
+            S_new = list(S_list)
+            for e, s in zip(events, outs):
+                S_new[e] = s
+            return S_new
 
         # the two branches only share their inputs: the sequence branch runs on
         # the current stream, the summary / interaction branch beside it

@@ -129,3 +129,64 @@ def test_model_bf16_tcgen05_path_vs_oracle(compskip, shape):
                      pools=[f"L{l}/pool" for l in range(spec.L)])  # exception 1 of oracle/parity.py
     bad = violations({**errs, **gerr}, False, kink)
     assert not bad, bad[:8]
+
+
+@pytest.mark.parametrize("dtype", [torch.float32])
+def test_model_heterogeneous_events_vs_oracle(dtype):
+    """Event-level personalization:
+    events with their own width / heads / depth — a d=16, 2-head, 2-layer
+    event beside a full-depth d=32 event in a 3-layer d=32 model — with the
+    summary adapters (d_e -> d) and hold-last summaries for the layers past
+    an event's depth, against the oracle's composition.  FP32 (1e-5): the
+    composition is exact; its bf16 kernels are the ones the bf16 model tests
+    above check (at these toy widths a 3-sample batch's bf16 activation
+    rounding moves single small gradients past 2e-2 — conditioning, not
+    semantics)."""
+    from paper_2602_10016_b200 import functional as F
+    from paper_2602_10016_b200.model import EventConfig, KunlunModel, ModelConfig
+
+    D, de, T0, T1, ns1 = 32, 16, 12, 9, 3
+    evs = [dict(T=T0, w=3, budget=8, n_seeds=6, rank=2), dict(T=T1, w=2, budget=4, n_seeds=ns1, rank=1, d=de, heads=2,
+                                                              layers=2)]
+    spec = OM.ModelSpec(L=3, d=D, heads=4, n_ctx=5, n_sum=2, n_kv=4, experts=2, events=[OM.EventSpec(**e) for e in evs])
+    cfg = ModelConfig(L=3, d=D, heads=4, n_ctx=5, n_sum=2, n_kv=4, experts=2, events=[EventConfig(**e) for e in evs])
+    pnp = OM.init_params(spec, seed=5)
+    model = KunlunModel(cfg, "cuda", dtype)
+    assert set(model.P.names()) == set(pnp)
+    model.P.load(pnp)
+    rng = np.random.default_rng(3)
+    B = 3
+    lengths = [np.array([T0, 5, 0]), np.array([T1, 1, 4])]
+    rnd = lambda shape: torch.tensor(rng.normal(0, 0.2, shape)).to(dtype).double().numpy()
+    X = rnd((B, 5, D))
+    S = [rnd((B, T0, D)), rnd((B, T1, de))]
+    labels = np.array([1.0, 0.0, 1.0])
+    cot = [{"X": rng.normal(0, 0.1, X.shape), "S": [rng.normal(0, 0.1, s.shape) for s in S],
+            "H": [rng.normal(0, 0.1, (B, ev["budget"], D)) for ev in evs]} for _ in range(3)]
+    ref = OM.model_forward_backward(spec, pnp, X, S, lengths, labels, cot)
+    dv = lambda x, g=False: torch.tensor(np.asarray(x), dtype=torch.float32, device="cuda").requires_grad_(g)
+    X_t, S_t = dv(X, True), [dv(s, True) for s in S]
+    logits, outs = model.forward(F.cast(X_t, dtype), [F.cast(s, dtype) for s in S_t],
+                                 [torch.tensor(L, dtype=torch.int32, device="cuda") for L in lengths],
+                                 keep_outputs=True, prune_dead=False)
+    loss = F.bce_with_logits(logits, dv(labels))
+    for l, (xo, so, ho) in enumerate(outs):
+        loss = loss + (F.cast(xo, torch.float32) * dv(cot[l]["X"])).sum()
+        for e in range(2):
+            loss = loss + (F.cast(so[e], torch.float32) * dv(cot[l]["S"][e])).sum()
+            loss = loss + (F.cast(ho[e], torch.float32) * dv(cot[l]["H"][e])).sum()
+    model.P.zero_grad()
+    loss.backward()
+    fp32 = dtype == torch.float32
+    err = rel if fp32 else relf
+    errs = {"logits": rel(logits.detach().double().cpu().numpy(), ref["logits"]),
+            "dX": err(X_t.grad.double().cpu().numpy(), ref["dX"])}
+    for e in range(2):
+        errs[f"dS{e}"] = err(S_t[e].grad.double().cpu().numpy(), ref["dS"][e])
+        for l in range(3):
+            errs[f"L{l}/H{e}"] = rel(outs[l][2][e].detach().double().cpu().numpy(), ref["outs"][l]["H"][e])
+    gerr = grad_errors({k: model.P.grad(k).double().cpu().numpy() for k in ref["grads"]}, ref["grads"], fp32)
+    kink = set() if fp32 else relu_kink(gerr, lambda prefix: spec.gdpa_acts if prefix.endswith("/gdpa") else None,
+                                        pools=[f"L{l}/pool" for l in range(3)])
+    bad = violations({**errs, **gerr}, fp32, kink)
+    assert not bad, bad[:6]
