@@ -284,6 +284,15 @@ typedef struct kl_colsoftmax_args {
 int kl_colsoftmax_fwd(const kl_colsoftmax_args* args, void* stream);
 int kl_colsoftmax_bwd(const kl_colsoftmax_args* args, void* stream);
 
+/* masked_softmax_lastdim (tensor.py:485-505) over rows of n fp32 scores with a
+ * boolean (uint8) mask of mask_rows x n rows, row r using mask row
+ * r % mask_rows (one (n_q, n_k) mask for every batch / head); fully-masked
+ * rows give 0.  Backward dx = y * (g - sum(g * y)).  The arbitrary-mask path
+ * of multi_head_attention (attention.py:69-93). */
+int kl_masked_softmax_fwd(long long rows, int n, const float* x, const unsigned char* mask, long long mask_rows,
+                          float* y, void* stream);
+int kl_masked_softmax_bwd(long long rows, int n, const float* y, const float* g, float* dx, void* stream);
+
 /* RMSNorm over the last axis, eps inside the sqrt (tensor.py:552-556).
  * x (rows, d) fp32; y = x / sqrt(mean(x^2)+eps) * gain.  bwd writes dx and
  * dgain (fp32, dgain fully written). */

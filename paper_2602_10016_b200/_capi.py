@@ -123,6 +123,9 @@ _SIGS = {
     "kl_set_pdl": ([C.c_int], None),
     "kl_last_gemm_path": ([], C.c_int),
     "kl_path_hits": ([C.c_int], C.c_ulonglong),
+    "kl_masked_softmax_fwd": ([C.c_longlong, C.c_int, C.c_void_p, C.c_void_p, C.c_longlong, C.c_void_p, C.c_void_p],
+                              C.c_int),
+    "kl_masked_softmax_bwd": ([C.c_longlong, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p], C.c_int),
     "kl_embed_nonseq_fwd": ([C.c_int, C.c_int, C.c_int, C.c_int, C.c_int] + [C.c_void_p] * 5 + [C.c_longlong, C.c_void_p,
                              C.c_void_p], C.c_int),
     "kl_embed_nonseq_bwd": ([C.c_int, C.c_int, C.c_int, C.c_int, C.c_int] + [C.c_void_p] * 4 + [C.c_longlong] +

@@ -168,13 +168,17 @@ def multi_head_attention(queries, keys_values, p: MhaParams, mask=None, lengths=
         ``(B, T, d)`` with per-sample ``lengths`` (mask=None) — PMA / HSP;
       * self-attention (``queries is keys_values``) with a band mask given as
         a ``WindowSpec``.
-    Arbitrary dense masks are not a hot-path shape and raise ValueError."""
+      * any other query / key rows with an explicit boolean ``mask``
+        (n_q, n_k) or (B, n_q, n_k) — the reference's general form: fp32
+        per-head score GEMMs, the masked row softmax kernel
+        (kl_masked_softmax_*, fully-masked rows -> 0), fp32 P V, then the
+        output projection in the compute dtype."""
     if isinstance(mask, WindowSpec):
         if queries is not keys_values:
             raise ValueError("windowed attention needs queries is keys_values")
         return _self_attention(keys_values, p, mask.w, mask.causal, lengths) - keys_values
     if mask is not None:
-        raise ValueError("arbitrary dense masks are not supported on the B200 path")
+        return _masked_attention(queries, keys_values, p, mask)
     squeeze = keys_values.dim() == 2
     kv = keys_values.unsqueeze(0) if squeeze else keys_values
     qt = shared_queries(queries, p)  # (H, n_q, d)
@@ -202,3 +206,60 @@ def swa_support(lengths, t_len: int, w: int, causal: bool = False, heads: int = 
     sup = torch.zeros(B * max(t_len, 1), dtype=torch.int32, device="cuda")
     _capi.call("kl_swa_debug_support", C.byref(a), sup.data_ptr(), _capi._stream())
     return sup.view(B, -1)[:, :t_len].cpu().numpy()
+
+
+class _MaskedSoftmax(torch.autograd.Function):
+    """masked_softmax_lastdim (tensor.py:485-505) of fp32 scores (B, H, n_q,
+    n_k) under a uint8 mask (n_q, n_k) or (B, H, n_q, n_k)."""
+
+    @staticmethod
+    def forward(ctx, x, mask):
+        x = x.contiguous()
+        y = torch.empty_like(x)
+        n = x.shape[-1]
+        rows = x.numel() // max(n, 1)
+        _capi.call("kl_masked_softmax_fwd", rows, n, x.data_ptr(), mask.data_ptr(), mask.numel() // max(n, 1),
+                   y.data_ptr(), _capi._stream())
+        ctx.save_for_backward(y)
+        return y
+
+    @staticmethod
+    def backward(ctx, g):
+        (y,) = ctx.saved_tensors
+        g = g.contiguous().float()
+        dx = torch.empty_like(y)
+        n = y.shape[-1]
+        _capi.call("kl_masked_softmax_bwd", y.numel() // max(n, 1), n, y.data_ptr(), g.data_ptr(), dx.data_ptr(),
+                   _capi._stream())
+        return dx, None
+
+
+def _masked_attention(queries, keys_values, p: MhaParams, mask):
+    """multi_head_attention (attention.py:69-93) with an arbitrary boolean mask."""
+    squeeze = keys_values.dim() == 2
+    xkv = keys_values.unsqueeze(0) if squeeze else keys_values
+    xq = queries.unsqueeze(0) if queries.dim() == 2 else queries
+    if xq.shape[0] == 1 and xkv.shape[0] > 1:
+        xq = xq.expand(xkv.shape[0], -1, -1)
+    B, n_q, n_k = xkv.shape[0], xq.shape[1], xkv.shape[1]
+    H, d_h, d = p.heads, p.head_dim, p.dim
+    m = torch.as_tensor(np.asarray(mask) if not isinstance(mask, torch.Tensor) else mask, device=xkv.device)
+    m = m.to(torch.uint8)
+    if m.shape == (n_q, n_k):
+        m = m.contiguous()
+    elif m.shape == (B, n_q, n_k):
+        m = m[:, None].expand(B, H, n_q, n_k).contiguous()
+    else:
+        raise ShapeError(f"mask must be ({n_q}, {n_k}) or ({B}, {n_q}, {n_k}), got {tuple(m.shape)}")
+    proj = lambda x, j: F.mm(x, F.PRef(p.P, p.wqkv, lambda w, j=j: w[j * H * d_h:(j + 1) * H * d_h].t()))
+    q = F.cast(proj(xq, 0), torch.float32).view(B, n_q, H, d_h).permute(0, 2, 1, 3)
+    k = F.cast(proj(xkv, 1), torch.float32).view(B, n_k, H, d_h).permute(0, 2, 1, 3)
+    v = F.cast(proj(xkv, 2), torch.float32).view(B, n_k, H, d_h).permute(0, 2, 1, 3)
+    scores = F.mm(q, k.transpose(2, 3), alpha=1.0 / float(np.sqrt(d_h)))  # (B, H, n_q, n_k), fp32
+    attn = _MaskedSoftmax.apply(scores, m)
+    o = F.mm(attn, v)  # (B, H, n_q, d_h)
+    cat = F.cast(o.permute(0, 2, 1, 3).reshape(B, n_q, H * d_h), xkv.dtype)
+    out = F.linear(cat, p.P, p.wout)
+    if numerics_check_mode() == "eager":
+        flag_nonfinite(out, "multi_head_attention")
+    return out.squeeze(0) if squeeze else out

@@ -1223,3 +1223,65 @@ extern "C" int kl_embed_nonseq_bwd(int B, int n_sparse, int d, int m, int dtype,
   count_launch();
   return launch_check("embed_nonseq_bwd");
 }
+
+// ---------------------------------------------------------------------------
+// masked_softmax_lastdim (tensor.py:485-505) with an explicit boolean mask:
+// one warp per row of n columns; fully-masked rows give 0.  The mask is
+// (rows / mask_div) x n, so one (n_q, n_k) mask serves every (batch, head).
+namespace kl {
+namespace msm {
+__global__ void __launch_bounds__(256) masked_softmax_fwd_kernel(long long rows, int n, const float* x,
+                                                                 const unsigned char* mask, long long mask_div,
+                                                                 float* y) {
+  KL_PDL_ENTRY();
+  const long long row = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const float* xr = x + row * n;
+  const unsigned char* mr = mask + (row % mask_div) * n;
+  float mx = -INFINITY;
+  for (int c = lane; c < n; c += 32)
+    if (mr[c]) mx = fmaxf(mx, xr[c]);
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  float s = 0.f;
+  for (int c = lane; c < n; c += 32)
+    if (mr[c]) s += expf(xr[c] - mx);
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const float inv = s > 0.f ? 1.f / s : 0.f;
+  for (int c = lane; c < n; c += 32) y[row * n + c] = mr[c] ? expf(xr[c] - mx) * inv : 0.f;
+}
+// dx = y * (g - sum(g * y))   (tensor.py:501-503)
+__global__ void __launch_bounds__(256) masked_softmax_bwd_kernel(long long rows, int n, const float* y, const float* g,
+                                                                 float* dx) {
+  KL_PDL_ENTRY();
+  const long long row = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const float* yr = y + row * n;
+  const float* gr = g + row * n;
+  float acc = 0.f;
+  for (int c = lane; c < n; c += 32) acc = fmaf(yr[c], gr[c], acc);
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  for (int c = lane; c < n; c += 32) dx[row * n + c] = yr[c] * (gr[c] - acc);
+}
+}  // namespace msm
+}  // namespace kl
+
+extern "C" int kl_masked_softmax_fwd(long long rows, int n, const float* x, const unsigned char* mask,
+                                     long long mask_rows, float* y, void* stream) {
+  if (rows < 0 || n < 0 || mask_rows < 1) { set_error("kl_masked_softmax_fwd: bad extents"); return KL_EBADSHAPE; }
+  if (rows == 0 || n == 0) return KL_OK;
+  launch_k(kl::msm::masked_softmax_fwd_kernel, (unsigned)((rows + 7) / 8), 256, 0, (cudaStream_t)stream, rows, n, x,
+           mask, mask_rows, y);
+  count_launch();
+  return launch_check("masked_softmax_fwd");
+}
+
+extern "C" int kl_masked_softmax_bwd(long long rows, int n, const float* y, const float* g, float* dx, void* stream) {
+  if (rows < 0 || n < 0) { set_error("kl_masked_softmax_bwd: bad extents"); return KL_EBADSHAPE; }
+  if (rows == 0 || n == 0) return KL_OK;
+  launch_k(kl::msm::masked_softmax_bwd_kernel, (unsigned)((rows + 7) / 8), 256, 0, (cudaStream_t)stream, rows, n, y,
+           g, dx);
+  count_launch();
+  return launch_check("masked_softmax_bwd");
+}

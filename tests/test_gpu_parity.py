@@ -778,3 +778,67 @@ def test_numerics_error_deferred_training_step():
     with pytest.raises(NumericsError):
         step.check_numerics()
     step.check_numerics()  # the flag was cleared
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_gdpa_forward_jagged_vs_oracle(dtype):
+    """gdpa_forward_jagged (gdpa.py:209-224): one batched launch over the
+    padded layout of a JaggedBatch (lengths 0, 1, T and between), per-sample
+    context summaries; forward only, zero-length samples pass through."""
+    from paper_2602_10016_b200 import gdpa as G
+    from paper_2602_10016_b200.jagged import JaggedBatch
+
+    d, H, n_kv, n_sum = 32, 4, 4, 2
+    P, cfg, wg, named = _params_gdpa(dtype, H, d, n_kv, n_sum, 5, 40)
+    rng = np.random.default_rng(4)
+    lens = [40, 0, 1, 17, 40]
+    vals = [rng.normal(0, 1 / np.sqrt(d), (n, d)) for n in lens]
+    if dtype == torch.bfloat16:
+        vals = [_round(v, dtype) for v in vals]
+    batch = JaggedBatch(np.concatenate(vals, axis=0), np.concatenate([[0], np.cumsum(lens)]))
+    xs = [_round(rng.normal(0, 1, (n_sum, d)), dtype) if dtype == torch.bfloat16 else rng.normal(0, 1, (n_sum, d))
+          for _ in lens]
+    out = G.gdpa_forward_jagged(batch, xs, cfg, wg)
+    assert isinstance(out, JaggedBatch) and np.array_equal(out.offsets, batch.offsets)
+    for b, n in enumerate(lens):
+        got = out.values[out.offsets[b]:out.offsets[b + 1]]
+        if n == 0:
+            assert got.shape == (0, d)
+            continue
+        kv, _ = K.generate_kv(xs[b], named, "g", n_kv)
+        yo, _ = K.gdpa_forward(vals[b], kv, named, "g", float(cfg.tau), cfg.activations)
+        assert (rel if dtype == torch.float32 else relf)(got, yo) < TOL[dtype]
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_multi_head_attention_arbitrary_mask_vs_oracle(dtype):
+    """multi_head_attention with a dense boolean mask (attention.py:69-93):
+    cross-attention of query rows over key rows, a random mask with one
+    fully-masked query row (-> 0, tensor.py:494-498)."""
+    from paper_2602_10016_b200 import attention as A
+    from paper_2602_10016_b200 import functional as F
+    from paper_2602_10016_b200.tensor import Params
+
+    d, H, n_q, n_k = 32, 4, 7, 11
+    rng = np.random.default_rng(12)
+    P = Params()
+    mp = A.MhaParams.create(P, "m", d, H, rng)
+    P.finalize("cuda", dtype)
+    named = {n: P[n].double().cpu().numpy() for n in P.names()}
+    xq = _round(rng.normal(0, 1, (n_q, d)), dtype) if dtype == torch.bfloat16 else rng.normal(0, 1, (n_q, d))
+    xkv = _round(rng.normal(0, 1, (n_k, d)), dtype) if dtype == torch.bfloat16 else rng.normal(0, 1, (n_k, d))
+    mask = rng.random((n_q, n_k)) < 0.6
+    mask[3] = False
+    R = rng.normal(0, 1, (n_q, d))
+    q_t, kv_t = dev(xq, grad=True), dev(xkv, grad=True)
+    y = A.multi_head_attention(F.cast(q_t, dtype), F.cast(kv_t, dtype), mp, mask=mask)
+    P.zero_grad()
+    (F.cast(y, torch.float32) * dev(R)).sum().backward()
+    yo, bwd = K.multi_head_attention(xq, xkv, named, "m", mask)
+    assert rel(y.float(), yo) < TOL[dtype]
+    assert np.abs(y[3].detach().float().cpu().numpy()).max() == 0.0  # fully-masked row
+    dxq, dxkv, gr = bwd(R)
+    err = rel if dtype == torch.float32 else relf
+    assert err(q_t.grad, dxq) < TOL[dtype]
+    assert err(kv_t.grad, dxkv) < TOL[dtype]
+    check_grads(P.grad, gr, dtype)
