@@ -680,9 +680,9 @@ __device__ __forceinline__ void act_cols64(const unsigned char* code, int c0, co
                      BWD ? dy + 16 * q : nullptr);
 }
 
-// 32 fp32 accumulator columns + 32 bf16 residual columns -> 32 bf16 outputs of row `row`.
-__device__ __forceinline__ void add_res_store32(const float* v, const bf16* res, bf16* out) {
-  const uint4* rp = reinterpret_cast<const uint4*>(res);
+// 32 fp32 accumulator columns + 32 bf16 residual columns (4 prefetched
+// 16-byte chunks) -> 32 bf16 outputs.
+__device__ __forceinline__ void add_res_store32(const float* v, const uint4* rp, bf16* out) {
   uint4* op = reinterpret_cast<uint4*>(out);
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
@@ -696,6 +696,14 @@ __device__ __forceinline__ void add_res_store32(const float* v, const bf16* res,
     }
     op[c] = make_uint4(o[0], o[1], o[2], o[3]);
   }
+}
+
+// This thread's 128 residual columns of one output half, loaded before the
+// accumulator wait (the global / L2 latency hides behind the MMAs).
+__device__ __forceinline__ void prefetch_res128(const bf16* src, bool ok, uint4* r) {
+  const uint4* p = reinterpret_cast<const uint4*>(src);
+#pragma unroll
+  for (int c = 0; c < 16; ++c) r[c] = ok ? __ldg(p + c) : make_uint4(0u, 0u, 0u, 0u);
 }
 
 __global__ void __launch_bounds__(NT5, 1)
@@ -865,14 +873,16 @@ __global__ void __launch_bounds__(NT5, 1)
       const bf16* rrow = p.res + (long long)b * p.r_bs + (long long)(q0 + r) * p.r_rs;
       bf16* orow = p.out + (long long)b * p.o_bs + (long long)(q0 + r) * p.o_rs;
       for (int h = 0; h < 2; ++h, ++yc) {
+        uint4 res[16];
+        prefetch_res128(rrow + h * 256 + hf * 128, inb, res);
         tc::mbar_wait(y_full, yc & 1);
         tc::fence_after();
-#pragma unroll 1
-        for (int cc = 0; cc < 128; cc += 32) {
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
           float acc[32];
-          tc::tmem_ld32(trow + T_Y + hf * 128 + cc, acc);
-          const int col = h * 256 + hf * 128 + cc;
-          if (inb) add_res_store32(acc, rrow + col, orow + col);
+          tc::tmem_ld32(trow + T_Y + hf * 128 + 32 * cc, acc);
+          const int col = h * 256 + hf * 128 + 32 * cc;
+          if (inb) add_res_store32(acc, res + 4 * cc, orow + col);
         }
         tc::fence_before();
         __syncwarp();
@@ -1051,14 +1061,16 @@ __global__ void __launch_bounds__(NT5, 1)
       const bf16* rrow = p.res + (long long)b * p.r_bs + (long long)(q0 + r) * p.r_rs;
       bf16* orow = p.out + (long long)b * p.o_bs + (long long)(q0 + r) * p.o_rs;
       for (int h = 0; h < 2; ++h, ++sc) {
+        uint4 res[16];
+        prefetch_res128(rrow + h * 256 + hf * 128, inb, res);
         tc::mbar_wait(s_full, sc & 1);
         tc::fence_after();
-#pragma unroll 1
-        for (int cc = 0; cc < 128; cc += 32) {
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
           float acc[32];
-          tc::tmem_ld32(trow + T_DS + hf * 128 + cc, acc);
-          const int col = h * 256 + hf * 128 + cc;
-          if (inb) add_res_store32(acc, rrow + col, orow + col);
+          tc::tmem_ld32(trow + T_DS + hf * 128 + 32 * cc, acc);
+          const int col = h * 256 + hf * 128 + 32 * cc;
+          if (inb) add_res_store32(acc, res + 4 * cc, orow + col);
         }
         tc::fence_before();
         __syncwarp();
