@@ -181,7 +181,7 @@ int kl_gdpa_bwd(const kl_gdpa_args* args, void* stream);
  * folded into the queries (Q = q W_q^T W_k / sqrt(d_h), rows ordered
  * (query, head)):  pooled[b] = softmax_t<len(Q S[b]^T) S[b].
  *   S:  (B, T, d) bf16, rows s_rs apart, samples s_bs apart.
- *   Q:  (HQ, d) bf16 contiguous.
+ *   Q:  (HQ, d) bf16 contiguous (or one set per sample group, q_group).
  *   O1: query rows [0, n1) -> (B, n1, d) (batch stride o1_bs); O2: rows
  *       [n1, HQ) -> (B, HQ - n1, d).  Empty samples give zero rows.
  *   LSE: (B, HQ) fp32 natural-log normaliser (+inf for empty samples).
@@ -213,6 +213,10 @@ typedef struct kl_hsp_args {
   void* dZ;
   void* dZ_lo;
   const float* Dq;
+  /* grouped event types: Q holds B / q_group query sets, (B / q_group, HQ, d)
+   * contiguous, and sample b pools with set b / q_group; 0 = one set shared
+   * by every sample (the reference's batch-shared queries). */
+  int q_group;
 } kl_hsp_args;
 
 int kl_hsp_fwd(const kl_hsp_args* args, void* stream);

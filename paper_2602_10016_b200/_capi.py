@@ -109,6 +109,7 @@ class HspArgs(C.Structure):
         ("accumulate_ds", C.c_int),
         ("dZ", C.c_void_p), ("dZ_lo", C.c_void_p),
         ("Dq", C.c_void_p),
+        ("q_group", C.c_int),
     ]
 
 

@@ -48,6 +48,7 @@ constexpr float RESCALE = 8.f;         // lazy-rescale threshold (log2 units)
 
 struct FwdP {
   int B, T, HQ, n1, qtiles;
+  int qg;  // samples per query set: sample b pools with query set b / qg (grouped event types)
   const int* lengths;
   bf16* O1;  // query rows [0, n1): (B, n1, D), batch stride o1_bs
   long long o1_bs;
@@ -151,26 +152,27 @@ __global__ void __launch_bounds__(NT, 1)
   KL_PDL_ENTRY();
   const uint32_t T_O = 256;
 
-  // the query tile of the next item with work (-1: none) -> release Q after this item?
+  // the (query tile, query set) of the next item with work (-1: none) -> release Q after this item?
   auto next_qt = [&](int idx) {
     for (int k = idx + 1; k < i1; ++k)
-      if (nblocks(p.lengths, k % p.B) > 0) return k / p.B;
+      if (nblocks(p.lengths, k % p.B) > 0) return (k / p.B) * p.B + (k % p.B) / p.qg;
     return -1;
   };
 
   if (warp == 0) {
     if (lane == 0) {
-      int cur_qt = -1, nq = 0, sc = 0;
+      int cur_q = -1, nq = 0, sc = 0;
       for (int idx = i0; idx < i1; ++idx) {
         const int qt = idx / p.B, b = idx % p.B;
         const int nb = nblocks(p.lengths, b);
         if (nb == 0) continue;
-        if (qt != cur_qt) {
+        const int qkey = qt * p.B + b / p.qg;  // (query tile, query set)
+        if (qkey != cur_q) {
           if (nq > 0) tc::mbar_wait(q_empty, (nq - 1) & 1);
           tc::mbar_arrive_expect_tx(q_full, BLK);
 #pragma unroll
-          for (int a = 0; a < NA; ++a) tc::tma_load_3d(sQ + a * ATOM, &tmQ, q_full, a * 64, qt * TB, 0);
-          cur_qt = qt;
+          for (int a = 0; a < NA; ++a) tc::tma_load_3d(sQ + a * ATOM, &tmQ, q_full, a * 64, qt * TB, b / p.qg);
+          cur_q = qkey;
           ++nq;
         }
         for (int j = 0; j < nb; ++j, ++sc) {
@@ -186,16 +188,17 @@ __global__ void __launch_bounds__(NT, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      int cur_qt = -1, nq = 0, sc = 0, zc = 0, pc = 0, t = 0;
+      int cur_q = -1, nq = 0, sc = 0, zc = 0, pc = 0, t = 0;
       const uint32_t qa = tc::smem_u32(sQ), pa = tc::smem_u32(sP);
       for (int idx = i0; idx < i1; ++idx) {
         const int qt = idx / p.B, b = idx % p.B;
         const int nb = nblocks(p.lengths, b);
         if (nb == 0) continue;
-        if (qt != cur_qt) {
+        const int qkey = qt * p.B + b / p.qg;
+        if (qkey != cur_q) {
           tc::mbar_wait(q_full, nq & 1);
           ++nq;
-          cur_qt = qt;
+          cur_q = qkey;
         }
         auto mma_z = [&](int j) {  // S block sc0 + j, Z buffer zc0 + j
           const int s = (sc + j) & 1, z = (zc + j) & 1;
@@ -227,7 +230,7 @@ __global__ void __launch_bounds__(NT, 1)
           ++pc;
         }
         tc::mma_commit(o_full);
-        if (next_qt(idx) != qt) tc::mma_commit(q_empty);
+        if (next_qt(idx) != qkey) tc::mma_commit(q_empty);
         sc += nb;
         zc += nb;
         ++t;
@@ -376,6 +379,7 @@ __global__ void __launch_bounds__(NT, 1)
 // length only zero their dZ / dS rows.
 struct BwdP {
   int B, T, HQ, qtiles, tblocks;
+  int qg;  // samples per query set (see FwdP)
   const int* lengths;
   const float* LSE;  // (B, HQ)
   const float* Dq;   // (B, HQ)
@@ -460,7 +464,7 @@ __global__ void __launch_bounds__(NT, 1)
           tc::mbar_arrive_expect_tx(qg_full, 2 * BLK);
 #pragma unroll
           for (int a = 0; a < NA; ++a) {
-            tc::tma_load_3d(sQ + a * ATOM, &tmQ, qg_full, a * 64, qt * TB, 0);
+            tc::tma_load_3d(sQ + a * ATOM, &tmQ, qg_full, a * 64, qt * TB, b / p.qg);
             tc::tma_load_3d(sG + a * ATOM, &tmG, qg_full, a * 64, qt * TB, b);
           }
         }
@@ -750,7 +754,7 @@ __global__ void __launch_bounds__(NT, 1)
               const int st = zc % ZST;
               tc::mbar_wait(&zs_empty[st], ((zc / ZST) & 1) ^ 1);
               tc::mbar_arrive_expect_tx(&zs_full[st], ZSTAGE);
-              tc::tma_load_3d(sZ + st * ZSTAGE, &tmQ, &zs_full[st], a * 64, qt * TB, 0);
+              tc::tma_load_3d(sZ + st * ZSTAGE, &tmQ, &zs_full[st], a * 64, qt * TB, b / p.qg);
               tc::tma_load_3d(sZ + st * ZSTAGE + ATOM, &tmS, &zs_full[st], a * 64, j * TB, b);
             }
             tc::mbar_wait(os_empty, (oc & 1) ^ 1);
@@ -1003,7 +1007,7 @@ __global__ void __launch_bounds__(NT, 1)
             const int st = gc % GST;
             tc::mbar_wait(&gs_empty[st], ((gc / GST) & 1) ^ 1);
             tc::mbar_arrive_expect_tx(&gs_full[st], GSTAGE);
-            tc::tma_load_3d(sG + st * GSTAGE, &tmQ, &gs_full[st], a * 64, qt * TB, 0);
+            tc::tma_load_3d(sG + st * GSTAGE, &tmQ, &gs_full[st], a * 64, qt * TB, b / p.qg);
             tc::tma_load_3d(sG + st * GSTAGE + ATOM, &tmG, &gs_full[st], a * 64, qt * TB, b);
           }
         }
@@ -1171,6 +1175,12 @@ extern "C" int kl_hsp_fwd(const kl_hsp_args* a, void* stream) {
   p.HQ = a->HQ;
   p.n1 = a->n1;
   p.qtiles = (a->HQ + hsp::TB - 1) / hsp::TB;
+  const int qg = a->q_group > 0 ? a->q_group : a->B;
+  if (a->B % qg) {
+    set_error("kl_hsp_fwd: q_group %d does not divide B = %d", a->q_group, a->B);
+    return KL_EBADSHAPE;
+  }
+  p.qg = qg;
   p.lengths = a->lengths;
   p.O1 = (bf16*)a->O1;
   p.o1_bs = a->o1_bs;
@@ -1181,7 +1191,7 @@ extern "C" int kl_hsp_fwd(const kl_hsp_args* a, void* stream) {
   if (const char* tv = getenv("KL_HSP_TRACE")) p.trace = (unsigned*)strtoull(tv, nullptr, 0);  // testing
   CUtensorMap tS, tQ;
   if (!hsp::map3(&tS, a->S, a->d, a->T, a->s_rs, a->B, a->s_bs) ||
-      !hsp::map3(&tQ, a->Q, a->d, a->HQ, a->d, 1, (long long)a->d * a->HQ)) {
+      !hsp::map3(&tQ, a->Q, a->d, a->HQ, a->d, a->B / qg, (long long)a->d * a->HQ)) {
     set_error("kl_hsp_fwd: tensor map encode failed (alignment?)");
     return KL_EUNSUPPORTED;
   }
@@ -1228,6 +1238,12 @@ extern "C" int kl_hsp_bwd(const kl_hsp_args* a, void* stream) {
   p.HQ = a->HQ;
   p.qtiles = (a->HQ + hsp::TB - 1) / hsp::TB;
   p.tblocks = (a->T + hsp::TB - 1) / hsp::TB;
+  const int qg = a->q_group > 0 ? a->q_group : a->B;
+  if (a->B % qg) {
+    set_error("kl_hsp_bwd: q_group %d does not divide B = %d", a->q_group, a->B);
+    return KL_EBADSHAPE;
+  }
+  p.qg = qg;
   p.lengths = a->lengths;
   p.LSE = a->LSE;
   p.Dq = a->Dq;
@@ -1243,7 +1259,7 @@ extern "C" int kl_hsp_bwd(const kl_hsp_args* a, void* stream) {
   }
   CUtensorMap tS, tQ, tG;
   if (!hsp::map3(&tS, a->S, a->d, a->T, a->s_rs, a->B, a->s_bs) ||
-      !hsp::map3(&tQ, a->Q, a->d, a->HQ, a->d, 1, (long long)a->d * a->HQ) ||
+      !hsp::map3(&tQ, a->Q, a->d, a->HQ, a->d, a->B / qg, (long long)a->d * a->HQ) ||
       !hsp::map3(&tG, a->dO1, a->d, a->HQ, a->d, a->B, a->o1_bs)) {
     set_error("kl_hsp_bwd: tensor map encode failed (alignment?)");
     return KL_EUNSUPPORTED;

@@ -43,6 +43,26 @@ class PRef:
         return self.fn(v) if self.fn else v
 
 
+class SRef(PRef):
+    """A stacked parameter operand: blocks ``keys`` (one per grouped event
+    type, equally shaped and uniformly spaced in the flat buffers) seen as one
+    (G, ...) tensor through ``fn`` (Params.stacked)."""
+
+    __slots__ = ("keys",)
+
+    def __init__(self, P, keys, fn=None, fp32=False):
+        super().__init__(P, keys[0], fn, fp32)
+        self.keys = tuple(keys)
+
+    def w(self):
+        v = self.P.stacked(self.keys, "w32" if self.fp32 else "w")
+        return self.fn(v) if self.fn else v
+
+    def g(self):
+        v = self.P.stacked(self.keys, "g")
+        return self.fn(v) if self.fn else v
+
+
 class GradSink:
     """One gradient buffer shared by the consumers of a (B, T, d) sequence
     tensor inside a layer (HSP pooling + recent rows, the GDPA / attention
@@ -345,15 +365,15 @@ class _Linear(torch.autograd.Function):
 
     @staticmethod
     def forward(ctx, x, flat, P, wkey, bkey, act, residual, out_dtype=None, stash_out=None, stash_in=None):
-        W = P.w(wkey)
-        N = W.shape[0]
+        W = _pw(P, wkey)
+        N = W.shape[-2]
         codes = _codes(act) if act and act != "identity" else []
         pre = None
         bias = P.w32(bkey) if bkey else None
         x4 = x if x.dim() >= 2 else x.unsqueeze(0)
         if codes:
             pre = torch.empty(x4.shape[:-1] + (N,), device=x.device, dtype=x.dtype)
-        y = gemm(x4, W.t(), bias=bias, acts=codes or None, aux=pre, aux_mode=1 if codes else 0,
+        y = gemm(x4, W.transpose(-1, -2), bias=bias, acts=codes or None, aux=pre, aux_mode=1 if codes else 0,
                  residual=residual, out_dtype=out_dtype)
         ctx.P, ctx.wkey, ctx.bkey, ctx.codes = P, wkey, bkey, codes
         ctx.has_res = residual is not None
@@ -366,7 +386,7 @@ class _Linear(torch.autograd.Function):
     def backward(ctx, g):
         x4, pre = ctx.saved_tensors
         P = ctx.P
-        W = P.w(ctx.wkey)
+        W = _pw(P, ctx.wkey)
         g = g.contiguous()
         if g.dtype != W.dtype:  # fp32-output linear (weight generation)
             g = cast(g, W.dtype)
@@ -394,8 +414,10 @@ class _Linear(torch.autograd.Function):
         rows = gp.numel() // gp.shape[-1]
         gpc = gp if gp.is_contiguous() else gp.contiguous()
         ones = _ones(rows, gp.dtype, gp.device) if ctx.bkey else None
+        grouped = not isinstance(ctx.wkey, str)  # one weight per group (leading batch dim): no reduction over it
         with _DwFork((gp, gpc, x4, ones)):
-            gemm(gp4.transpose(2, 3), x44, P.g(ctx.wkey), beta=1.0, reduce=(True, True))
+            gemm(gp4.transpose(2, 3), x44, _as4(_pg(P, ctx.wkey)) if grouped else P.g(ctx.wkey), beta=1.0,
+                 reduce=(True, not grouped))
             if ctx.bkey:
                 gemm(ones.view(1, rows), gpc.view(rows, -1), P.g(ctx.bkey).view(1, -1), beta=1.0)
         dres = g.reshape(ctx.xshape[:-1] + (g.shape[-1],)) if ctx.has_res else None
@@ -417,9 +439,23 @@ def _ones(n, dtype, device):
     return t[:n]
 
 
+def _pw(P, key):
+    """A weight block, or (a tuple of keys) the (G, ...) stack of equally
+    shaped, uniformly spaced blocks (grouped event types; Params.stacked)."""
+    return P.w(key) if isinstance(key, str) else P.stacked(key, "w")
+
+
+def _pg(P, key):
+    return P.g(key) if isinstance(key, str) else P.stacked(key, "g")
+
+
 def linear(x, P, wkey, bkey=None, act=None, residual=None, out_dtype=None, stash_out=None, stash_in=None):
     """y = act(x W^T + b) + residual.  ``stash_out`` / ``stash_in``: a
-    ResidualStash shared with an earlier linear on the same input."""
+    ResidualStash shared with an earlier linear on the same input.  A tuple
+    ``wkey`` is a grouped linear: x (G, M, K) with one stacked weight per
+    group (Params.stacked), no bias."""
+    if not isinstance(wkey, str) and bkey is not None:
+        raise ValueError("grouped linear takes no bias")
     return _Linear.apply(x, P.flat, P, wkey, bkey, act, residual, out_dtype, stash_out, stash_in)
 
 
@@ -590,7 +626,10 @@ class _HspPool(torch.autograd.Function):
         # Q arrives in fp32 (the batch-shared query path is computed in fp32);
         # the T-length work runs in S's dtype and dQ is returned in fp32.
         B, T, d = S.shape
-        HQ = Q32.shape[0]
+        HQ = Q32.shape[-2]
+        G = Q32.shape[0] if Q32.dim() == 3 else 1  # grouped event types: one query set per B / G samples
+        if B % G:
+            raise ShapeError(f"{G} query sets do not divide the batch of {B}")
         if sum(splits) != HQ:
             raise ShapeError(f"query splits {splits} do not cover {HQ} rows")
         Q = Q32
@@ -610,7 +649,8 @@ class _HspPool(torch.autograd.Function):
             _capi.call("kl_hsp_fwd", C.byref(a), _stream())
             ctx.save_for_backward(S, Q, lengths, LSE, *outs)
             return tuple(outs) + ((rec,) if rec is not None else ())
-        sc = gemm(S, Q.t(), out_dtype=torch.float32)  # (B, T, HQ)
+        sc = gemm(S.view(G, B // G, T, d), Q.view(G, 1, HQ, d).transpose(2, 3), out_dtype=torch.float32)
+        sc = sc.view(B, T, HQ)
         Pm = torch.empty(B, T, HQ, device=S.device, dtype=S.dtype)
         lse = torch.empty(B, HQ, device=S.device, dtype=torch.float32)
         a = _colsm_args(sc, Pm, lengths, lse)
@@ -648,7 +688,8 @@ def _hsp_gemm_bwd(ctx, gs):
     """GEMM composition of the pooling VJP (fp32 parity path)."""
     S, Q, lengths, Pm, sc, lse, *outs = ctx.saved_tensors
     B, T, d = S.shape
-    HQ = Q.shape[0]
+    HQ = Q.shape[-2]
+    G = Q.shape[0] if Q.dim() == 3 else 1
     dP = torch.empty(B, T, HQ, device=S.device, dtype=torch.float32)
     # D[b, c] = sum_t P dP = dO[c] . pooled[c]: the softmax-VJP column term
     # from the (B, HQ, d) pooled output instead of a pass over T
@@ -675,13 +716,15 @@ def _hsp_gemm_bwd(ctx, gs):
     a.dtype_dp = _capi.dt(dP)
     a.Dcol = Dcol.data_ptr() if HSP_DCOL else None
     _capi.call("kl_colsoftmax_bwd", C.byref(a), _stream())
-    gemm(dsc, Q.unsqueeze(0).expand(S.shape[0], -1, -1), dS, beta=1.0)
-    # dQ = sum_b dsc^T S: softmax-VJP rows sum to zero over t, so this
-    # reduction cancels; bf16 runs it on the hi + lo split of dsc.
-    dQ = torch.zeros(1, 1, Q.shape[0], Q.shape[1], device=S.device, dtype=torch.float32)
-    gemm(dsc.transpose(1, 2).unsqueeze(0), S.unsqueeze(0), dQ, beta=1.0, reduce=(False, True))
+    Bg = B // G
+    gemm(dsc.view(G, Bg, T, HQ), Q.view(G, 1, HQ, d).expand(G, Bg, HQ, d), dS.view(G, Bg, T, d), beta=1.0)
+    # dQ = sum_b dsc^T S (over each query set's samples): softmax-VJP rows sum
+    # to zero over t, so this reduction cancels; bf16 runs it on the hi + lo
+    # split of dsc.
+    dQ = torch.zeros(G, 1, HQ, d, device=S.device, dtype=torch.float32)
+    gemm(dsc.view(G, Bg, T, HQ).transpose(2, 3), S.view(G, Bg, T, d), dQ, beta=1.0, reduce=(False, True))
     if lo is not None:
-        gemm(lo.transpose(1, 2).unsqueeze(0), S.unsqueeze(0), dQ, beta=1.0, reduce=(False, True))
+        gemm(lo.view(G, Bg, T, HQ).transpose(2, 3), S.view(G, Bg, T, d), dQ, beta=1.0, reduce=(False, True))
     dQ = dQ.reshape(Q.shape)
     return dS, dQ
 
@@ -697,7 +740,8 @@ def _hsp_fused_ok(S, HQ, n_splits) -> bool:
 def _hsp_args(S, Q, lengths, n1, O1, O2, LSE):
     a = _capi.HspArgs()
     a.B, a.T, a.d = S.shape
-    a.HQ, a.n1 = Q.shape[0], n1
+    a.HQ, a.n1 = Q.shape[-2], n1
+    a.q_group = a.B // Q.shape[0] if Q.dim() == 3 else 0
     a.dtype = _capi.dt(S)
     a.lengths = lengths.data_ptr()
     a.S, a.s_rs, a.s_bs = S.data_ptr(), S.stride(1), S.stride(0)
@@ -713,7 +757,8 @@ def _hsp_fused_bwd(ctx, gs):
     the batch-shared query gradient dQ = sum_b dZ S (hi + lo) as GEMMs."""
     S, Q, lengths, LSE, *outs = ctx.saved_tensors
     B, T, d = S.shape
-    HQ = Q.shape[0]
+    HQ = Q.shape[-2]
+    G = Q.shape[0] if Q.dim() == 3 else 1
     gl = [torch.zeros_like(o) if g is None else g for g, o in zip(gs, outs)]
     dO = gl[0].contiguous() if len(gl) == 1 else torch.cat(gl, dim=1)
     O = outs[0] if len(outs) == 1 else torch.cat(outs, dim=1)
@@ -731,9 +776,10 @@ def _hsp_fused_bwd(ctx, gs):
     a.accumulate_ds = 1 if acc is not None else 0
     a.dZ, a.dZ_lo, a.Dq = dZ.data_ptr(), dZlo.data_ptr(), Dq.data_ptr()
     _capi.call("kl_hsp_bwd", C.byref(a), _stream())
-    dQ = torch.zeros(1, 1, HQ, d, device=S.device, dtype=torch.float32)
-    gemm(dZ.unsqueeze(0), S.unsqueeze(0), dQ, beta=1.0, reduce=(False, True))
-    gemm(dZlo.unsqueeze(0), S.unsqueeze(0), dQ, beta=1.0, reduce=(False, True))
+    Bg = B // G
+    dQ = torch.zeros(G, 1, HQ, d, device=S.device, dtype=torch.float32)
+    gemm(dZ.view(G, Bg, HQ, T), S.view(G, Bg, T, d), dQ, beta=1.0, reduce=(False, True))
+    gemm(dZlo.view(G, Bg, HQ, T), S.view(G, Bg, T, d), dQ, beta=1.0, reduce=(False, True))
     return dS, dQ.reshape(Q.shape)
 
 
@@ -746,7 +792,9 @@ def _hsp_bwd512(S, Q, lengths, LSE, dO, Dq, acc, ctx):
                                              into the shared sequence gradient)
         dQ  = sum_b (dZ + dZ_lo) S          (batch-reduced, hi + lo)."""
     B, T, d = S.shape
-    HQ = Q.shape[0]
+    HQ = Q.shape[-2]
+    G = Q.shape[0] if Q.dim() == 3 else 1
+    Bg = B // G
     PZ = torch.empty(B, 2 * HQ, T, device=S.device, dtype=S.dtype)
     dZlo = torch.empty(B, HQ, T, device=S.device, dtype=S.dtype)
     a = _hsp_args(S, Q, lengths, HQ, dO, dO, LSE)
@@ -754,14 +802,14 @@ def _hsp_bwd512(S, Q, lengths, LSE, dO, Dq, acc, ctx):
     a.dS, a.ds_rs, a.ds_bs = S.data_ptr(), S.stride(1), S.stride(0)  # unused at d = 512
     a.dZ, a.dZ_lo, a.Dq = PZ.data_ptr(), dZlo.data_ptr(), Dq.data_ptr()
     _capi.call("kl_hsp_bwd", C.byref(a), _stream())
-    GQ = torch.cat([dO, Q.unsqueeze(0).expand(B, HQ, d)], dim=1)  # (B, 2 HQ, d)
+    GQ = torch.cat([dO, Q.view(G, 1, HQ, d).expand(G, Bg, HQ, d).reshape(B, HQ, d)], dim=1)  # (B, 2 HQ, d)
     if acc is not None:
         dS = gemm(PZ.transpose(1, 2), GQ, acc, residual=acc)
     else:
         dS = gemm(PZ.transpose(1, 2), GQ)
-    dQ = torch.zeros(1, 1, HQ, d, device=S.device, dtype=torch.float32)
-    gemm(PZ[:, HQ:].unsqueeze(0), S.unsqueeze(0), dQ, beta=1.0, reduce=(False, True))
-    gemm(dZlo.unsqueeze(0), S.unsqueeze(0), dQ, beta=1.0, reduce=(False, True))
+    dQ = torch.zeros(G, 1, HQ, d, device=S.device, dtype=torch.float32)
+    gemm(PZ.view(G, Bg, 2 * HQ, T)[:, :, HQ:], S.view(G, Bg, T, d), dQ, beta=1.0, reduce=(False, True))
+    gemm(dZlo.view(G, Bg, HQ, T), S.view(G, Bg, T, d), dQ, beta=1.0, reduce=(False, True))
     return dS, dQ.reshape(Q.shape)
 
 
@@ -775,8 +823,10 @@ HSP_DCOL = False
 def hsp_pool(S, Q, lengths, splits=None, n_recent=0, sink=None):
     """Pooled outputs, one (B, n, d) tensor per entry of ``splits`` (default:
     all HQ rows in one), then, if ``n_recent``, the recent rows (seqsum.py:
-    186-196) — one op, so the sequence gets one gradient buffer."""
-    return _HspPool.apply(S, Q, lengths, tuple(splits) if splits else (Q.shape[0],), int(n_recent), sink)
+    186-196) — one op, so the sequence gets one gradient buffer.  ``Q`` is
+    (HQ, d), or (G, HQ, d) for G grouped event types whose samples are
+    stacked along S's batch (sample b pools with set b // (B / G))."""
+    return _HspPool.apply(S, Q, lengths, tuple(splits) if splits else (Q.shape[-2],), int(n_recent), sink)
 
 
 def _recent_fwd(S, lengths, n):
@@ -1087,11 +1137,14 @@ class _HeadProj(torch.autograd.Function):
     @staticmethod
     def forward(ctx, X, flat, wref):
         B, n, H, d = X.shape
-        W = wref.w()  # (H, d_h, d)
-        d_h = W.shape[1]
+        W = wref.w()  # (H, d_h, d), or (G, H, d_h, d) for G grouped event types (samples stacked by group)
+        G = W.shape[0] if W.dim() == 4 else 1
+        W4 = W.view(G, *W.shape[-3:])
+        d_h = W.shape[-2]
         X = X.contiguous()
+        M = B // G * n
         out = torch.empty(B * n, H, d_h, device=X.device, dtype=X.dtype)
-        gemm(X.view(B * n, H, d).permute(1, 0, 2), W.transpose(1, 2), out.permute(1, 0, 2))
+        gemm(X.view(G, M, H, d).permute(0, 2, 1, 3), W4.transpose(2, 3), out.view(G, M, H, d_h).permute(0, 2, 1, 3))
         ctx.save_for_backward(X)
         ctx.wref = wref
         return out.view(B, n, H * d_h)
@@ -1101,11 +1154,16 @@ class _HeadProj(torch.autograd.Function):
         (X,) = ctx.saved_tensors
         B, n, H, d = X.shape
         W = ctx.wref.w()
-        d_h = W.shape[1]
-        gv = g.contiguous().view(B * n, H, d_h).permute(1, 0, 2)  # (H, B*n, d_h)
+        G = W.shape[0] if W.dim() == 4 else 1
+        W4 = W.view(G, *W.shape[-3:])
+        d_h = W.shape[-2]
+        M = B // G * n
+        gv = g.contiguous().view(G, M, H, d_h).permute(0, 2, 1, 3)  # (G, H, M, d_h)
+        Xv = X.view(G, M, H, d).permute(0, 2, 1, 3)
         dX = torch.empty_like(X)
-        gemm(gv, W, dX.view(B * n, H, d).permute(1, 0, 2))
-        gemm(gv.transpose(1, 2), X.view(B * n, H, d).permute(1, 0, 2), ctx.wref.g(), beta=1.0)
+        gemm(gv, W4, dX.view(G, M, H, d).permute(0, 2, 1, 3))
+        Wg = ctx.wref.g()
+        gemm(gv.transpose(2, 3), Xv, Wg.view(G, *Wg.shape[-3:]), beta=1.0)
         return dX, None, None
 
 

@@ -16,11 +16,12 @@ import numpy as np
 import torch
 
 from . import functional as F
+from . import grouped
 from .attention import MhaParams, WindowSpec, mha_full, mha_window
 from .gdpa import GdpaConfig, PffnParams, WeightGenParams, fold_kv, generate_kv, pffn_original, summarize_nonseq
 from .interaction import ExpertPartition, InteractionParams, global_interaction
 from .mlp import Mlp
-from .seqsum import SummarizerParams, SummarySplit, hsp_summarize
+from .seqsum import SummarizerParams, SummarySplit, hsp_summarize, summary_queries
 from .tensor import Params, ShapeError, _flag, flag_nonfinite, numerics_check_mode
 
 DEFAULT_ACTIVATION_CYCLE = ("silu", "relu", "identity", "tanh")
@@ -101,6 +102,9 @@ class ModelConfig:
     summarizer: str = "hsp"
     attention: str = "window"
     pffn_hidden: int = 0
+    # event types of one shape run grouped (grouped.py): stacked along the
+    # batch, one launch per operator over all of them
+    group_events: bool = True
 
     def __post_init__(self):
         if self.d % self.heads:
@@ -210,6 +214,11 @@ class KunlunModel:
             self.layers.append(LayerParams(pool, wg, mh, sm, gi, ad))
         self.head = Mlp.create(P, "head", [cfg.n_ctx * d, cfg.head_hidden, 1], ["silu", "identity"], rng)
         P.finalize(device, dtype)
+        self.groups = None
+        if cfg.group_events and grouped.uniform_events(cfg):
+            gs = [grouped.EventGroup(P, lp) for lp in self.layers]
+            if all(g.ok() for g in gs):
+                self.groups = gs
         if torch.device(device).type == "cuda":
             _flag(device)  # the non-finite flag exists before any CUDA-graph capture
         self.flags = compskip_config(cfg.L, cfg.compskip)
@@ -345,6 +354,52 @@ class KunlunModel:
         S_out = list(S_out)
         return Xn, S_out, H_list
 
+    def _group_queries(self, l, qrows):
+        """(E, HQ, d) fp32: every event type's folded query rows of layer l."""
+        E = len(self.cfg.events)
+        if qrows:
+            return torch.stack([qrows[(l, e)] for e in range(E)])
+        return torch.stack([summary_queries(self.layers[l].summ[e]) for e in range(E)])
+
+    def layer_forward_grouped(self, l: int, flags: LayerSkipFlags, X, S, lens, H_prev, live_seq=True, qrows=None):
+        """layer_forward with the event types grouped (grouped.py): S is the
+        (E*B, T, d) stack of every event's sequence, ``lens`` its (E*B,)
+        lengths; H_prev / the returned H are per-event (B, budget, d) lists."""
+        cfg = self.cfg
+        lp, grp = self.layers[l], self.groups[l]
+        E, B = grp.E, X.shape[0]
+        ev = cfg.events[0]
+        if flags.skip_hsp and H_prev is None:
+            raise ValueError("skip_hsp on a layer without H_prev")
+        if self.layer_hook is not None:
+            X, S = _Boundary.apply(self.layer_hook, l, X, S)
+        sink = F.GradSink()  # the stacked sequences' one shared gradient buffer
+        S = F.seq_join(S, sink)
+
+        def x_branch():
+            if flags.skip_hsp:
+                H_list = list(H_prev)
+            else:
+                rows = grouped.summarize(S, grp, lens, self._group_queries(l, qrows), sink=sink)
+                H_list = list(rows.view(E, B, *rows.shape[1:]).unbind(0))
+            return global_interaction(X, H_list, lp.gi), H_list
+
+        def s_branch():
+            s = S
+            if live_seq and not flags.skip_pffn:
+                kt, vt = grouped.generate_fold(summarize_nonseq(X, F.PRef(self.P, lp.pool)), grp)
+                s = F.gdpa_core(s, kt, vt, lens, cfg.ev_acts(0), cfg.n_kv, 1.0 / float(ev.T), sink=sink)
+                if numerics_check_mode() == "eager":
+                    flag_nonfinite(s, f"layer {l} GDPA (grouped events)")
+            if live_seq and not flags.skip_self_attention:
+                s = grouped.window_attention(s, grp, lens, ev.w, ev.causal)
+            return s
+
+        shared = [X, S] + list(qrows.values() if qrows else []) + list(H_prev or [])
+        (Xn, H_list), S_out = F.run_branches([x_branch, s_branch], X.device, inputs=shared, name="xbranch",
+                                             side_first=True)
+        return Xn, S_out, H_list
+
     def seq_live(self) -> list:
         """Layers whose sequence output can still reach a later HSP (and so
         the loss): l is live iff some l' > l does not skip HSP."""
@@ -371,10 +426,20 @@ class KunlunModel:
                     qrows = self.query_rows()
             else:
                 qrows = self.query_rows()
-        for l in range(self.cfg.L):
-            X, S_list, H = self.layer_forward(l, self.flags[l], X, S_list, lengths, H, live_seq=live[l], qrows=qrows)
-            if keep_outputs:
-                outs.append((X, list(S_list), list(H)))
+        if self.groups is not None:  # event types stacked along the batch (grouped.py)
+            E = len(S_list)
+            S = grouped.stack_inputs(S_list)
+            lens = grouped.stack_inputs([torch.as_tensor(t, dtype=torch.int32, device=S.device) for t in lengths])
+            for l in range(self.cfg.L):
+                X, S, H = self.layer_forward_grouped(l, self.flags[l], X, S, lens, H, live_seq=live[l], qrows=qrows)
+                if keep_outputs:
+                    outs.append((X, list(S.view(E, -1, *S.shape[1:]).unbind(0)), list(H)))
+        else:
+            for l in range(self.cfg.L):
+                X, S_list, H = self.layer_forward(l, self.flags[l], X, S_list, lengths, H, live_seq=live[l],
+                                                  qrows=qrows)
+                if keep_outputs:
+                    outs.append((X, list(S_list), list(H)))
         B = X.shape[0]
         z = self.head.apply_rows(X.reshape(B, -1))
         logits = F.cast(z, torch.float32).reshape(B)

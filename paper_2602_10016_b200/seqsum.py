@@ -230,6 +230,19 @@ def recent_rows(s, n_recent: int, lengths=None):
     return out.squeeze(0) if squeeze else out
 
 
+def summary_queries(p: SummarizerParams) -> torch.Tensor:
+    """The folded seed + CLS query rows ((n_seeds + n_cls) * H, d) fp32 that
+    pool over S in hsp_summarize, rows ordered (query, head): each pooled set
+    is (B, n, H, d) and its projections run on B*n flattened rows."""
+    hp = p.hsp
+    H, d = hp.attn.heads, hp.dim
+    qs = hsp_queries(hp)  # (H, n_s, d)
+    if p.split.n_cls > 0:
+        qc = shared_queries(F.PRef(hp.P, p.cls_queries), p.cls_attn)  # (H, n_cls, d)
+        qs = torch.cat([qs, qc], dim=1)
+    return qs.transpose(0, 1).reshape(qs.shape[1] * H, d)
+
+
 def hsp_summarize(s, p: SummarizerParams, lengths=None, sink=None, q_rows=None) -> SummaryBundle:
     """Full three-part summary [CLS | compressed seeds | recent]
     (seqsum.py:199-210).  The seed and CLS query sets pool over S in a single
@@ -246,17 +259,8 @@ def hsp_summarize(s, p: SummarizerParams, lengths=None, sink=None, q_rows=None) 
     H = hp.attn.heads
     n_s = hp.n_seeds
     n_cls = p.split.n_cls
-    n_q = n_s + n_cls
     if q_rows is None:  # (the model folds every layer's queries at once: functional.query_folds)
-        qs = hsp_queries(hp)  # (H, n_s, d)
-        if n_cls > 0:
-            qc = shared_queries(F.PRef(hp.P, p.cls_queries), p.cls_attn)  # (H, n_cls, d)
-            q_all = torch.cat([qs, qc], dim=1)
-        else:
-            q_all = qs
-        # query rows ordered (query, head): each pooled set is (B, n, H, d) and
-        # its projections run on B*n flattened rows
-        q_rows = q_all.transpose(0, 1).reshape(n_q * H, d)
+        q_rows = summary_queries(p)
     splits = (n_s * H, n_cls * H) if n_cls > 0 else (n_s * H,)
     n_rec = p.split.n_recent
     outs = F.hsp_pool(S, q_rows, lens, splits, n_recent=n_rec, sink=sink)

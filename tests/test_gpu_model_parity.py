@@ -40,6 +40,9 @@ def _lib():
 
 
 def _spec(compskip, shape="d256"):
+    if shape == "grouped":  # three event types of one shape: the grouped-events path (grouped.py)
+        return OM.ModelSpec(L=2, d=256, heads=4, n_ctx=16, n_sum=4, n_kv=16, experts=2, compskip=compskip,
+                            events=[OM.EventSpec(T=384, w=128, budget=8, n_seeds=8, rank=2) for _ in range(3)])
     if shape == "d512":  # the c4 widths (d = 512, H = 8, H*n_kv = 128), shorter sequences
         return OM.ModelSpec(L=2, d=512, heads=8, n_ctx=16, n_sum=4, n_kv=16, experts=2, compskip=compskip,
                             events=[OM.EventSpec(T=640, w=128, budget=32, n_seeds=32, rank=8)])
@@ -62,7 +65,8 @@ def _bf16(x):
     return torch.tensor(np.asarray(x)).to(torch.bfloat16).double().numpy()
 
 
-@pytest.mark.parametrize("compskip,shape", [(False, "d256"), (True, "d256"), (False, "d512")])
+@pytest.mark.parametrize("compskip,shape", [(False, "d256"), (True, "d256"), (False, "d512"), (False, "grouped"),
+                                            (True, "grouped")])
 def test_model_bf16_tcgen05_path_vs_oracle(compskip, shape):
     from paper_2602_10016_b200 import _capi
     from paper_2602_10016_b200 import functional as F
@@ -70,11 +74,12 @@ def test_model_bf16_tcgen05_path_vs_oracle(compskip, shape):
     spec = _spec(compskip, shape)
     pnp = OM.init_params(spec, seed=21)
     model = _gpu_model(spec)
+    assert (model.groups is not None) == (shape == "grouped")
     model.P.load(pnp)
     rng = np.random.default_rng(7)
     B = 5
-    lengths = [np.array([ev.T, ev.T - 1, 129, 1, 0])[np.r_[0:5] if e == 0 else [0, 4, 1, 2, 3]]
-               for e, ev in enumerate(spec.events)]
+    perms = [np.r_[0:5], [0, 4, 1, 2, 3], [3, 1, 4, 0, 2]]
+    lengths = [np.array([ev.T, ev.T - 1, 129, 1, 0])[perms[e]] for e, ev in enumerate(spec.events)]
     d = spec.d
     # the oracle sees exactly the bf16 inputs the device reads
     X = _bf16(rng.normal(0, 1 / np.sqrt(d), (B, spec.n_ctx, d)))
