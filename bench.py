@@ -459,12 +459,18 @@ def main():
     S = [torch.tensor(s, device=dev).to(dtype) for s in Sn]
     lens = [torch.tensor(l, device=dev) for l in Ln]
     y = torch.tensor(yn, device=dev)
+    if model.groups is not None:  # grouped event types: the sequences as adjacent slices of one batch
+        from paper_2602_10016_b200.grouped import stage
+
+        S, lens = stage(S), stage(lens)
 
     from paper_2602_10016_b200.optim import TrainStep
 
     bufs = [(X, S, y)]
     if not args.no_e2e:  # a second static input set: the e2e loop double-buffers host->device copies
-        bufs.append((torch.empty_like(X), [torch.empty_like(s) for s in S], torch.empty_like(y)))
+        bufs.append((torch.empty_like(X), list(torch.empty((len(S),) + tuple(S[0].shape), device=dev, dtype=dtype)
+                                               .unbind(0)) if model.groups is not None
+                     else [torch.empty_like(s) for s in S], torch.empty_like(y)))
     steps_ = [TrainStep(model, opt, xb, sb, lens, yb, reducer) for (xb, sb, yb) in bufs]
 
     def barrier():

@@ -67,10 +67,6 @@ class TrainStep:
 
     def __init__(self, model, opt, X, S, lengths, labels, reducer=None):
         self.model, self.opt, self.reducer = model, opt, reducer
-        if getattr(model, "groups", None) is not None:  # grouped event types read one stacked batch
-            from . import grouped
-
-            S, lengths = grouped.stage(S), grouped.stage(lengths)
         self.X, self.S, self.lengths, self.labels = X, S, lengths, labels
         self.graph = None
         self.loss = None

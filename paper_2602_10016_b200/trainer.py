@@ -78,6 +78,10 @@ def train(model: KunlunModel, steps: int, batch: int, *, lr: float = 1e-3, seed:
     eval_ids = [i for i in range(10 * eval_batches) if i % 10 == 9][:eval_batches]
     eval_set = [_device_batch(cfg, batch, seed * 1_000_003 + i, dev, dt) for i in eval_ids]
     X, S, L, y = _device_batch(cfg, batch, seed * 1_000_003 + train_ids[0], dev, dt)
+    if model.groups is not None:  # grouped event types read the sequences as one stacked batch
+        from .grouped import stage
+
+        S, L = stage(S), stage(L)
     step = TrainStep(model, opt, X, S, L, y)
     if graph:
         step.eager()  # warm-up before capture (also the first training update)
