@@ -859,7 +859,7 @@ class _QueryFolds(torch.autograd.Function):
     parameter gradients straight into the gradient buffer."""
 
     @staticmethod
-    def forward(ctx, flat, P, keys, H, d_h, eps):
+    def forward(ctx, flat, P, keys, H, d_h, eps, stacked=False):
         seeds_k, gain_k, wqkv_k, cls_k, cw_k = keys
         E = P.stacked(seeds_k, "w32")
         G = P.stacked(gain_k, "w32")
@@ -886,7 +886,8 @@ class _QueryFolds(torch.autograd.Function):
         ctx.P, ctx.keys, ctx.H, ctx.d_h, ctx.eps = P, keys, H, d_h, eps
         ctx.save_for_backward(xs, qh_s, qh_c)
         Qr = Q.view(L, n_q * H, d)
-        return tuple(Qr[l] for l in range(L))
+        ctx.stacked = stacked
+        return Qr if stacked else tuple(Qr[l] for l in range(L))
 
     @staticmethod
     def backward(ctx, *gs):
@@ -896,8 +897,12 @@ class _QueryFolds(torch.autograd.Function):
         L, n_s, d = xs.shape
         Hd = H * d_h
         scale = 1.0 / float(d_h) ** 0.5
-        n_q = gs[0].shape[0] // H if gs[0] is not None else n_s + (P.shape(cls_k[0])[0] if cls_k else 0)
-        dQ = torch.stack([torch.zeros(n_q * H, d, device=xs.device) if g is None else g for g in gs]).view(L, n_q, H, d)
+        n_q = n_s + (P.shape(cls_k[0])[0] if cls_k else 0)
+        if ctx.stacked:
+            dQ = gs[0].contiguous().view(L, n_q, H, d)
+        else:
+            dQ = torch.stack([torch.zeros(n_q * H, d, device=xs.device) if g is None else g for g in gs])
+            dQ = dQ.view(L, n_q, H, d)
 
         def fold_bwd(dQs, qh, n, W, gW):
             """dQs (L, H, n, d), qh (L, n, H*d_h): dW_k += scale qh^T dQ; returns
@@ -928,17 +933,18 @@ class _QueryFolds(torch.autograd.Function):
             dqc = fold_bwd(dQ[:, n_s:].permute(0, 2, 1, 3), qh_c, n_cls, CW, gCW)
             gemm(dqc.transpose(1, 2), Cq, gCW[:, :Hd], beta=1.0)
             gemm(dqc, CW[:, :Hd], P.stacked(cls_k, "g"), beta=1.0)
-        return None, None, None, None, None, None
+        return None, None, None, None, None, None, None
 
 
-def query_folds(P, keys, H, d_h, eps=1e-6):
-    """Per-layer (HQ, d) fp32 query rows of every layer in ``keys`` (lists of
-    per-layer registry block keys), see _QueryFolds; None if the blocks are
-    not uniformly spaced."""
+def query_folds(P, keys, H, d_h, eps=1e-6, stacked=False):
+    """Per-entry (HQ, d) fp32 query rows of every entry in ``keys`` (lists of
+    per-layer — or, for grouped event types, per-event — registry block
+    keys), see _QueryFolds; one (n, HQ, d) tensor if ``stacked``; None if
+    the blocks are not uniformly spaced."""
     for ks in keys:
         if ks and P.stacked(ks, "w32") is None:
             return None
-    return _QueryFolds.apply(P.flat, P, keys, int(H), int(d_h), float(eps))
+    return _QueryFolds.apply(P.flat, P, keys, int(H), int(d_h), float(eps), bool(stacked))
 
 
 # ---------------------------------------------------------------------------

@@ -257,6 +257,17 @@ class KunlunModel:
         layers = [l for l in range(cfg.L) if not self.flags[l].skip_hsp]
         if not layers or cfg.summarizer != "hsp":
             return out
+        if self.groups is not None:  # grouped event types: per layer, every event's queries in one pass
+            for l in layers:
+                sp = self.layers[l].summ
+                keys = ([s.hsp.seeds for s in sp], [s.hsp.gain for s in sp], [s.hsp.attn.wqkv for s in sp],
+                        [s.cls_queries for s in sp] if sp[0].cls_queries else [],
+                        [s.cls_attn.wqkv for s in sp] if sp[0].cls_queries else [])
+                q = F.query_folds(self.P, keys, cfg.heads, cfg.d // cfg.heads, stacked=True)
+                if q is None:
+                    return {}
+                out[l] = q  # (E, HQ, d)
+            return out
         for e in range(len(cfg.events)):
             lay_e = [l for l in layers if l < cfg.ev_layers(e)]
             if not lay_e:
@@ -358,7 +369,7 @@ class KunlunModel:
         """(E, HQ, d) fp32: every event type's folded query rows of layer l."""
         E = len(self.cfg.events)
         if qrows:
-            return torch.stack([qrows[(l, e)] for e in range(E)])
+            return qrows[l]
         return torch.stack([summary_queries(self.layers[l].summ[e]) for e in range(E)])
 
     def layer_forward_grouped(self, l: int, flags: LayerSkipFlags, X, S, lens, H_prev, live_seq=True, qrows=None):
