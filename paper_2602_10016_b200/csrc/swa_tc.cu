@@ -1412,12 +1412,20 @@ struct Walk {
   int seg_bh, seg_base, seg_first, ld_end;
   Tile tl;
   bool done;
+  // the length of sample lb: a sequence's tiles are consecutive, so the
+  // walkers read lengths[] once per sequence instead of a dependent global
+  // load on every tile
+  int lb = -1, lv = 0;
 };
 
 template <bool QM = false>
 __device__ __forceinline__ void walk_fill(const SwaP& p, Walk& w) {
   w.tl.k0 = w.kt * TB;
-  w.tl.len = p.lengths[w.tl.b];
+  if (w.tl.b != w.lb) {
+    w.lb = w.tl.b;
+    w.lv = p.lengths[w.tl.b];
+  }
+  w.tl.len = w.lv;
   band_of<QM>(p, w.tl);
 }
 __device__ __forceinline__ void walk_adv(const SwaP& p, Walk& w) {
