@@ -44,18 +44,27 @@ def uniform_events(cfg) -> bool:
     return all(key(e) == k0 for e in range(1, len(evs))) and cfg.ev_d(0) == cfg.d and cfg.ev_layers(0) == cfg.L
 
 
-class EventGroup:
-    """Stacked parameter keys of one layer's grouped event types."""
+class FoldSpec:
+    """The weight-generation blocks (kgv, wq, wout) of E event types of one
+    shape (E = 1: a single event's GDPA)."""
 
-    def __init__(self, P, lp):
-        wg, mh, sm = lp.wg, lp.mha, lp.summ
+    def __init__(self, P, wg):
         self.P = P
         self.E = len(wg)
-        g0, m0, s0 = wg[0], mh[0], sm[0]
+        g0 = wg[0]
         self.H, self.n_kv, self.d_h, self.d = g0.heads, g0.n_kv, g0.head_dim, g0.dim
         self.kgv = tuple(g.kgv for g in wg)
         self.wq = tuple(g.wq for g in wg)
         self.gwout = tuple(g.wout for g in wg)
+
+
+class EventGroup(FoldSpec):
+    """Stacked parameter keys of one layer's grouped event types."""
+
+    def __init__(self, P, lp):
+        wg, mh, sm = lp.wg, lp.mha, lp.summ
+        super().__init__(P, wg)
+        m0, s0 = mh[0], sm[0]
         self.wqkv = tuple(m.wqkv for m in mh)
         self.mwout = tuple(m.wout for m in mh)
         hs = [s.hsp for s in sm]
@@ -129,9 +138,11 @@ class _GroupFold(torch.autograd.Function):
         return dkv, None, None
 
 
-def generate_fold(xsum, grp: EventGroup):
+def generate_fold(xsum, grp: FoldSpec):
     """All event types' generated weights (one GEMM: the flattened summary
-    broadcast against the stacked kgv blocks), folded per event."""
+    broadcast against the stacked kgv blocks), folded per event into the
+    (E*B, H*n_kv, d) Kt / Vt of the fused GDPA kernels (generate_kv + fold_kv,
+    gdpa.py:103-138, without the per-head K / V slices' gradient copies)."""
     B = xsum.shape[0]
     flat = xsum.reshape(B, -1)
     kv = F.mm(flat, F.SRef(grp.P, grp.kgv, lambda w: w.transpose(1, 2)))  # (E, B, 2 H n_kv d_h)

@@ -18,7 +18,7 @@ import torch
 from . import functional as F
 from . import grouped
 from .attention import MhaParams, WindowSpec, mha_full, mha_window
-from .gdpa import GdpaConfig, PffnParams, WeightGenParams, fold_kv, generate_kv, pffn_original, summarize_nonseq
+from .gdpa import GdpaConfig, PffnParams, WeightGenParams, pffn_original, summarize_nonseq
 from .interaction import ExpertPartition, InteractionParams, global_interaction
 from .mlp import Mlp
 from .seqsum import SummarizerParams, SummarySplit, hsp_summarize, summary_queries
@@ -333,8 +333,7 @@ class KunlunModel:
                     if live_seq and not flags.skip_pffn and cfg.pffn == "original":
                         s = pffn_original(xsum, s, lp.wg[e], lengths[e])  # Table 2 "w/o GDPA" (no residual)
                     elif live_seq and not flags.skip_pffn:
-                        k, v = generate_kv(xsum, lp.wg[e], cfg.gdpa_cfg(e))
-                        kt, vt = fold_kv(k, v, lp.wg[e])
+                        kt, vt = grouped.generate_fold(xsum, grouped.FoldSpec(self.P, [lp.wg[e]]))
                         s = F.gdpa_core(s, kt, vt, lengths[e], cfg.ev_acts(e), cfg.n_kv, 1.0 / float(ev.T),
                                         sink=sinks[e])
                         if numerics_check_mode() == "eager":

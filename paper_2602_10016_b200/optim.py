@@ -102,7 +102,17 @@ class TrainStep:
 
         m = self.model
         split = F.BRANCH_STREAMS and self.segments is not None
-        m.P.zero_grad()
+        # the gradient buffer is cleared beside the forward (nothing writes it
+        # before the backward, which waits for the clear)
+        dev = self.X.device
+        zs = None
+        if self.X.is_cuda:
+            zs = F.side_stream(dev, "zero_grad")
+            zs.wait_stream(torch.cuda.current_stream(dev))
+            with torch.cuda.stream(zs):
+                m.P.zero_grad()
+        else:
+            m.P.zero_grad()
         if split:
             self.opt.tick()
             self._fired = set()
@@ -112,6 +122,8 @@ class TrainStep:
             loss, _ = m.loss(self.X, self.S, self.lengths, self.labels)
             F.DW_STREAM_FWD = False
             F.DW_STREAM = F.BRANCH_STREAMS  # weight-gradient GEMMs beside the dX chain
+            if zs is not None:
+                torch.cuda.current_stream(dev).wait_stream(zs)
             loss.backward()
         finally:
             F.DW_STREAM = F.DW_STREAM_FWD = False
