@@ -347,6 +347,37 @@ int kl_gated_sum_bwd(int rows, int d, int dtype, const void* g, long long g_rs, 
 int kl_rowdot(int rows, int d, int dtype, const void* a, long long a_rs, const void* b, long long b_rs, float* out,
               void* stream);
 
+/* out[b * out_bs + i] = sum_k a[b, i, k] * b[b, i, k], i < n: rowdot over a
+ * (B, n, d) pair of strided row sets (one pooled part of the HSP backward). */
+int kl_rowdot3(int B, int n, int d, int dtype, const void* a, long long a_bs, long long a_rs, const void* b,
+               long long b_bs, long long b_rs, float* out, long long out_bs, void* stream);
+
+/*
+ * Row regrouping along a token axis in ONE launch: the concatenations /
+ * splits of row blocks the layer composes (SummaryBundle rows [CLS | seeds |
+ * recent], seqsum.py:148-162; the expert slices of [X | summaries] and their
+ * re-concatenation, interaction.py:144-157).  Segment s copies `rows` rows of
+ * every sample b: dst + b*dst_bs + i*dst_rs <- src + b*src_bs + i*src_rs
+ * (elements; rows of d contiguous elements; src NULL writes zeros).  The
+ * destination rows of the segments are enumerated in order.
+ */
+#define KL_MAX_SEGS 16
+typedef struct kl_regroup_seg {
+  const void* src;
+  long long src_bs, src_rs;
+  void* dst;
+  long long dst_bs, dst_rs;
+  int rows;
+} kl_regroup_seg;
+typedef struct kl_regroup_args {
+  int B, d, dtype, n_seg;
+  kl_regroup_seg seg[KL_MAX_SEGS];
+} kl_regroup_args;
+int kl_regroup(const kl_regroup_args* args, void* stream);
+
+/* Zero `bytes` bytes of device memory (a memset node in a captured graph). */
+int kl_memset(void* p, long long bytes, void* stream);
+
 /* Mean BCE with logits (tensor.py:535-549): loss[0] = mean(...), dz = (sig(z)-y)/n.
  * z, y, dz fp32 (n,). */
 int kl_bce_fwd_bwd(int n, const float* z, const float* y, float* loss, float* dz, void* stream);

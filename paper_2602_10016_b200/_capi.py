@@ -15,6 +15,8 @@ import torch
 from .tensor import NumericsError, ShapeError
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libkunlun_sm100a.so")
+if os.environ.get("KL_LIB_PATH"):  # A/B timing of two builds in one GPU session (scripts/r2/)
+    LIB_PATH = os.environ["KL_LIB_PATH"]
 
 KL_OK, KL_EBADSHAPE, KL_EUNSUPPORTED, KL_ELAUNCH = 0, 1, 2, 3
 KL_F32, KL_BF16 = 0, 1
@@ -94,6 +96,19 @@ class RoteArgs(C.Structure):
     ]
 
 
+MAX_SEGS = 16
+
+
+class RegroupSeg(C.Structure):
+    _fields_ = [("src", C.c_void_p), ("src_bs", C.c_longlong), ("src_rs", C.c_longlong),
+                ("dst", C.c_void_p), ("dst_bs", C.c_longlong), ("dst_rs", C.c_longlong), ("rows", C.c_int)]
+
+
+class RegroupArgs(C.Structure):
+    _fields_ = [("B", C.c_int), ("d", C.c_int), ("dtype", C.c_int), ("n_seg", C.c_int),
+                ("seg", RegroupSeg * MAX_SEGS)]
+
+
 class HspArgs(C.Structure):
     _fields_ = [
         ("B", C.c_int), ("T", C.c_int), ("HQ", C.c_int), ("d", C.c_int), ("n1", C.c_int),
@@ -154,6 +169,10 @@ _SIGS = {
     "kl_gram_triu_fwd": ([C.c_int] * 4 + [C.c_void_p, C.c_longlong, C.c_longlong, C.c_void_p, C.c_longlong, C.c_void_p], C.c_int),
     "kl_gram_triu_bwd": ([C.c_int] * 4 + [C.c_void_p, C.c_longlong, C.c_longlong, C.c_void_p, C.c_longlong,
                                           C.c_void_p, C.c_longlong, C.c_longlong, C.c_void_p], C.c_int),
+    "kl_rowdot3": ([C.c_int] * 4 + [C.c_void_p, C.c_longlong, C.c_longlong, C.c_void_p, C.c_longlong, C.c_longlong,
+                                   C.c_void_p, C.c_longlong, C.c_void_p], C.c_int),
+    "kl_regroup": ([C.c_void_p, C.c_void_p], C.c_int),
+    "kl_memset": ([C.c_void_p, C.c_longlong, C.c_void_p], C.c_int),
     "kl_rowdot": ([C.c_int] * 3 + [C.c_void_p, C.c_longlong, C.c_void_p, C.c_longlong, C.c_void_p, C.c_void_p],
                   C.c_int),
     "kl_gated_sum_fwd": ([C.c_int] * 3 + [C.c_void_p, C.c_longlong] + [C.c_void_p] * 5 + [C.c_longlong, C.c_void_p], C.c_int),

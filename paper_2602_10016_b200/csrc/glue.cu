@@ -1285,3 +1285,128 @@ extern "C" int kl_masked_softmax_bwd(long long rows, int n, const float* y, cons
   count_launch();
   return launch_check("masked_softmax_bwd");
 }
+
+// ---------------------------------------------------------------------------
+// Row regrouping (the token-axis concatenations / splits of the layer:
+// SummaryBundle [CLS | seeds | recent] rows (seqsum.py:148-162), the expert
+// slices of [X | summaries] and their re-concatenation (interaction.py:
+// 144-157), the pooled-row gradients of the HSP backward): every destination
+// row is one source row (or zeros), all segments of all samples in ONE launch.
+// HBM-bound: one read and one write of each row, 16-byte vectors when the
+// rows allow.  A block per (destination row, sample).
+namespace kl {
+namespace rg {
+struct Segs {
+  int n_seg, d, esz;
+  int row0[KL_MAX_SEGS + 1];  // destination-row prefix of the segments
+  kl_regroup_seg seg[KL_MAX_SEGS];
+};
+
+template <int VB>  // bytes per vector access (16 or the element size)
+__global__ void __launch_bounds__(128) regroup_kernel(Segs sg) {
+  KL_PDL_ENTRY();
+  const int r = blockIdx.x, b = blockIdx.y;
+  int s = 0;
+  while (s + 1 < sg.n_seg && r >= sg.row0[s + 1]) ++s;
+  const kl_regroup_seg& g = sg.seg[s];
+  const int i = r - sg.row0[s];
+  const long long rb = (long long)sg.d * sg.esz;  // row bytes
+  char* dst = (char*)g.dst + ((long long)b * g.dst_bs + (long long)i * g.dst_rs) * sg.esz;
+  if (g.src == nullptr) {
+    for (long long o = (long long)threadIdx.x * VB; o < rb; o += 128 * VB) {
+      if (VB == 16) *reinterpret_cast<uint4*>(dst + o) = make_uint4(0u, 0u, 0u, 0u);
+      else if (VB == 4) *reinterpret_cast<uint32_t*>(dst + o) = 0u;
+      else *reinterpret_cast<uint16_t*>(dst + o) = 0;
+    }
+    return;
+  }
+  const char* src = (const char*)g.src + ((long long)b * g.src_bs + (long long)i * g.src_rs) * sg.esz;
+  for (long long o = (long long)threadIdx.x * VB; o < rb; o += 128 * VB) {
+    if (VB == 16) *reinterpret_cast<uint4*>(dst + o) = *reinterpret_cast<const uint4*>(src + o);
+    else if (VB == 4) *reinterpret_cast<uint32_t*>(dst + o) = *reinterpret_cast<const uint32_t*>(src + o);
+    else *reinterpret_cast<uint16_t*>(dst + o) = *reinterpret_cast<const uint16_t*>(src + o);
+  }
+}
+
+// out[b * out_bs + i] = sum_k a[b, i, k] * b[b, i, k] for i < n (rows of a
+// (B, n, d) strided tensor pair): the softmax-VJP row term of one pooled part.
+template <typename T>
+__global__ void __launch_bounds__(256) rowdot3_kernel(int B, int n, int d, const T* a, long long a_bs,
+                                                      long long a_rs, const T* b, long long b_bs, long long b_rs,
+                                                      float* out, long long out_bs) {
+  KL_PDL_ENTRY();
+  const long long r = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= (long long)B * n) return;
+  const int bb = (int)(r / n), i = (int)(r % n);
+  const T* ar = a + bb * a_bs + i * a_rs;
+  const T* br = b + bb * b_bs + i * b_rs;
+  float acc = 0.f;
+  for (int k = lane; k < d; k += 32) acc = fmaf(ldf(ar + k), ldf(br + k), acc);
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) out[bb * out_bs + i] = acc;
+}
+}  // namespace rg
+}  // namespace kl
+
+extern "C" int kl_regroup(const kl_regroup_args* a, void* stream) {
+  using namespace kl;
+  if (!a || a->B < 0 || a->d < 1 || a->n_seg < 1 || a->n_seg > KL_MAX_SEGS ||
+      (a->dtype != KL_BF16 && a->dtype != KL_F32)) {
+    set_error("kl_regroup: bad extents (B >= 0, d >= 1, 1..%d segments, bf16 / fp32)", KL_MAX_SEGS);
+    return KL_EBADSHAPE;
+  }
+  rg::Segs sg{};
+  sg.n_seg = a->n_seg;
+  sg.d = a->d;
+  sg.esz = a->dtype == KL_F32 ? 4 : 2;
+  bool vec = (a->d * sg.esz) % 16 == 0;
+  int rows = 0;
+  for (int s = 0; s < a->n_seg; ++s) {
+    const kl_regroup_seg& g = a->seg[s];
+    if (g.rows < 0 || !g.dst) {
+      set_error("kl_regroup: segment %d has no destination or negative rows", s);
+      return KL_EBADSHAPE;
+    }
+    sg.row0[s] = rows;
+    sg.seg[s] = g;
+    rows += g.rows;
+    auto al = [&](const void* p, long long bs, long long rs) {
+      return ((uintptr_t)p & 15) == 0 && (bs * sg.esz) % 16 == 0 && (rs * sg.esz) % 16 == 0;
+    };
+    vec = vec && al(g.dst, g.dst_bs, g.dst_rs) && (!g.src || al(g.src, g.src_bs, g.src_rs));
+  }
+  sg.row0[a->n_seg] = rows;
+  if (rows == 0 || a->B == 0) return KL_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  dim3 grid((unsigned)rows, (unsigned)a->B);
+  if (vec) launch_k(rg::regroup_kernel<16>, grid, 128, 0, s, sg);
+  else if (sg.esz == 4) launch_k(rg::regroup_kernel<4>, grid, 128, 0, s, sg);
+  else launch_k(rg::regroup_kernel<2>, grid, 128, 0, s, sg);
+  count_launch();
+  return launch_check("regroup");
+}
+
+extern "C" int kl_rowdot3(int B, int n, int d, int dtype, const void* a, long long a_bs, long long a_rs, const void* b,
+                          long long b_bs, long long b_rs, float* out, long long out_bs, void* stream) {
+  using namespace kl;
+  if (B < 0 || n < 0 || d < 1) { set_error("kl_rowdot3: bad extents"); return KL_EBADSHAPE; }
+  if ((long long)B * n == 0) return KL_OK;
+  const unsigned grid = (unsigned)(((long long)B * n + 7) / 8);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == KL_F32)
+    launch_k(rg::rowdot3_kernel<float>, grid, 256, 0, s, B, n, d, (const float*)a, a_bs, a_rs, (const float*)b, b_bs,
+             b_rs, out, out_bs);
+  else
+    launch_k(rg::rowdot3_kernel<bf16>, grid, 256, 0, s, B, n, d, (const bf16*)a, a_bs, a_rs, (const bf16*)b, b_bs,
+             b_rs, out, out_bs);
+  count_launch();
+  return launch_check("rowdot3");
+}
+
+extern "C" int kl_memset(void* p, long long bytes, void* stream) {
+  if (bytes < 0 || (bytes > 0 && !p)) { kl::set_error("kl_memset: bad buffer"); return KL_EBADSHAPE; }
+  if (bytes == 0) return KL_OK;
+  cudaMemsetAsync(p, 0, (size_t)bytes, (cudaStream_t)stream);
+  return kl::launch_check("memset");
+}

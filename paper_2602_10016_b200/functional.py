@@ -759,14 +759,30 @@ def _hsp_fused_bwd(ctx, gs):
     B, T, d = S.shape
     HQ = Q.shape[-2]
     G = Q.shape[0] if Q.dim() == 3 else 1
-    gl = [torch.zeros_like(o) if g is None else g for g, o in zip(gs, outs)]
-    dO = gl[0].contiguous() if len(gl) == 1 else torch.cat(gl, dim=1)
-    O = outs[0] if len(outs) == 1 else torch.cat(outs, dim=1)
-    Dq = torch.empty(B, HQ, device=S.device, dtype=torch.float32)  # rowsum(dO * pooled): the softmax-VJP term
-    _capi.call("kl_rowdot", B * HQ, d, _capi.dt(dO), dO.data_ptr(), d, O.data_ptr(), d, Dq.data_ptr(), _stream())
+    # the pooled parts' gradients as one (B, HQ, d) row set (one kl_regroup;
+    # missing gradients are zero rows); at d = 512 directly into the rows
+    # [0, HQ) of the dS GEMM's K operand [dO; Qt] (B, 2 HQ, d)
+    ns = [o.shape[1] for o in outs]
+    wide = d == 512 and G == 1
+    GQ = torch.empty(B, (2 if wide else 1) * HQ, d, device=S.device, dtype=S.dtype)
+    segs, r0 = [], 0
+    for g, n in zip(gs, ns):
+        segs.append((None if g is None else (g if g.stride(2) == 1 else g.contiguous()), 0, GQ, r0, n))
+        r0 += n
+    if wide:
+        segs.append((Q.unsqueeze(0).expand(B, HQ, d), 0, GQ, HQ, HQ))
+    copy_rows(segs, B, d, S.dtype)
+    dO = GQ[:, :HQ]
+    # rowsum(dO * pooled) per part (the softmax-VJP term), no concatenated copy of the pooled rows
+    Dq = torch.empty(B, HQ, device=S.device, dtype=torch.float32)
+    r0 = 0
+    for o, n in zip(outs, ns):
+        _capi.call("kl_rowdot3", B, n, d, _capi.dt(o), dO[:, r0:].data_ptr(), dO.stride(0), dO.stride(1),
+                   o.data_ptr(), o.stride(0), o.stride(1), Dq[:, r0:].data_ptr(), HQ, _stream())
+        r0 += n
     acc = ctx.sink.take(S) if ctx.sink is not None else None
     if d == 512:
-        return _hsp_bwd512(S, Q, lengths, LSE, dO, Dq, acc, ctx)
+        return _hsp_bwd512(S, Q, lengths, LSE, dO, Dq, acc, ctx, GQ if wide else None)
     dS = acc if acc is not None else torch.empty_like(S)
     dZ = torch.empty(B, HQ, T, device=S.device, dtype=S.dtype)
     dZlo = torch.empty_like(dZ)
@@ -777,13 +793,13 @@ def _hsp_fused_bwd(ctx, gs):
     a.dZ, a.dZ_lo, a.Dq = dZ.data_ptr(), dZlo.data_ptr(), Dq.data_ptr()
     _capi.call("kl_hsp_bwd", C.byref(a), _stream())
     Bg = B // G
-    dQ = torch.zeros(G, 1, HQ, d, device=S.device, dtype=torch.float32)
+    dQ = zeros((G, 1, HQ, d), S.device)  # split-K partials add into it (fp32 reduce-add epilogue)
     gemm(dZ.view(G, Bg, HQ, T), S.view(G, Bg, T, d), dQ, beta=1.0, reduce=(False, True))
     gemm(dZlo.view(G, Bg, HQ, T), S.view(G, Bg, T, d), dQ, beta=1.0, reduce=(False, True))
     return dS, dQ.reshape(Q.shape)
 
 
-def _hsp_bwd512(S, Q, lengths, LSE, dO, Dq, acc, ctx):
+def _hsp_bwd512(S, Q, lengths, LSE, dO, Dq, acc, ctx, GQ=None):
     """d = 512: kl_hsp_bwd writes P and dZ (one pass over S, the score
     products streamed through the kernel, hsp_bwd512_kernel) into PZ
     (B, 2 HQ, T) and dZ's bf16 residual into dZ_lo; the whole-width T-length
@@ -802,12 +818,13 @@ def _hsp_bwd512(S, Q, lengths, LSE, dO, Dq, acc, ctx):
     a.dS, a.ds_rs, a.ds_bs = S.data_ptr(), S.stride(1), S.stride(0)  # unused at d = 512
     a.dZ, a.dZ_lo, a.Dq = PZ.data_ptr(), dZlo.data_ptr(), Dq.data_ptr()
     _capi.call("kl_hsp_bwd", C.byref(a), _stream())
-    GQ = torch.cat([dO, Q.view(G, 1, HQ, d).expand(G, Bg, HQ, d).reshape(B, HQ, d)], dim=1)  # (B, 2 HQ, d)
+    if GQ is None:  # (grouped query sets: one per sample group)
+        GQ = torch.cat([dO, Q.view(G, 1, HQ, d).expand(G, Bg, HQ, d).reshape(B, HQ, d)], dim=1)  # (B, 2 HQ, d)
     if acc is not None:
         dS = gemm(PZ.transpose(1, 2), GQ, acc, residual=acc)
     else:
         dS = gemm(PZ.transpose(1, 2), GQ)
-    dQ = torch.zeros(G, 1, HQ, d, device=S.device, dtype=torch.float32)
+    dQ = zeros((G, 1, HQ, d), S.device)
     gemm(PZ.view(G, Bg, 2 * HQ, T)[:, :, HQ:], S.view(G, Bg, T, d), dQ, beta=1.0, reduce=(False, True))
     gemm(dZlo.view(G, Bg, HQ, T), S.view(G, Bg, T, d), dQ, beta=1.0, reduce=(False, True))
     return dS, dQ.reshape(Q.shape)
@@ -845,6 +862,98 @@ def _recent_bwd_into(dS, g, lengths):
     g = g.contiguous()
     _capi.call("kl_recent_rows_bwd", B, T, d, g.shape[1], _capi.dt(g), g.data_ptr(), g.stride(0),
                lengths.data_ptr(), dS.data_ptr(), dS.stride(0), _stream())
+
+
+# ---------------------------------------------------------------------------
+def zeros(shape, device, dtype=torch.float32):
+    """A zero-filled buffer as a memset (kl_memset: a memset node in the
+    captured step, not an elementwise fill kernel)."""
+    t = torch.empty(shape, device=device, dtype=dtype)
+    if t.is_cuda:
+        _capi.call("kl_memset", t.data_ptr(), t.numel() * t.element_size(), _stream())
+    else:
+        t.zero_()
+    return t
+
+
+def copy_rows(segs, B, d, dtype):
+    """kl_regroup: segments (src tensor or None, src row, dst tensor, dst row,
+    rows) over (B, n, d) row sets with unit column stride, all in one launch
+    (chunks of MAX_SEGS segments)."""
+    esz = 4 if dtype == torch.float32 else 2
+    for c0 in range(0, len(segs), _capi.MAX_SEGS):
+        chunk = [g for g in segs[c0:c0 + _capi.MAX_SEGS] if g[4] > 0]
+        if not chunk:
+            continue
+        a = _capi.RegroupArgs()
+        a.B, a.d, a.dtype, a.n_seg = B, d, _capi.dt(chunk[0][2]), len(chunk)
+        for k, (src, r0, dst, q0, rows) in enumerate(chunk):
+            g = a.seg[k]
+            if src is not None:
+                g.src = src.data_ptr() + r0 * src.stride(1) * esz
+                g.src_bs, g.src_rs = src.stride(0), src.stride(1)
+            g.dst = dst.data_ptr() + q0 * dst.stride(1) * esz
+            g.dst_bs, g.dst_rs = dst.stride(0), dst.stride(1)
+            g.rows = rows
+        _capi.call("kl_regroup", C.byref(a), _stream())
+
+
+def _plan(n_in, n_out):
+    """Overlaps of two partitions of one token axis: (i, row in i, j, row in j, rows)."""
+    out, i, j, ri, rj = [], 0, 0, 0, 0
+    while i < len(n_in) and j < len(n_out):
+        k = min(n_in[i] - ri, n_out[j] - rj)
+        if k > 0:
+            out.append((i, ri, j, rj, k))
+        ri += k
+        rj += k
+        if ri == n_in[i]:
+            i, ri = i + 1, 0
+        if rj == n_out[j]:
+            j, rj = j + 1, 0
+    return out
+
+
+class _Regroup(torch.autograd.Function):
+    """Re-partition the token axis of (B, n_i, d) row sets into contiguous
+    (B, m_j, d) tensors (sum n_i = sum m_j): torch.cat / slicing along dim 1
+    without ATen copies, zero-fills or gradient accumulation — every row has
+    exactly one source, so the VJP is the inverse regrouping (missing output
+    gradients are zero rows).  One kl_regroup launch per direction."""
+
+    @staticmethod
+    def forward(ctx, sizes, *pieces):
+        p0 = pieces[0]
+        B, d = p0.shape[0], p0.shape[2]
+        n_in = [t.shape[1] for t in pieces]
+        outs = [torch.empty(B, m, d, device=p0.device, dtype=p0.dtype) for m in sizes]
+        copy_rows([(pieces[i], ri, outs[j], rj, k) for i, ri, j, rj, k in _plan(n_in, sizes)], B, d, p0.dtype)
+        ctx.n_in, ctx.sizes = n_in, tuple(sizes)
+        return tuple(outs)
+
+    @staticmethod
+    def backward(ctx, *gs):
+        ref = next(g for g in gs if g is not None)
+        B, d = ref.shape[0], ref.shape[2]
+        gin = [torch.empty(B, n, d, device=ref.device, dtype=ref.dtype) for n in ctx.n_in]
+        gs = [g if g is None or g.stride(2) == 1 else g.contiguous() for g in gs]
+        copy_rows([(gs[j], rj, gin[i], ri, k) for i, ri, j, rj, k in _plan(ctx.n_in, ctx.sizes)], B, d, ref.dtype)
+        return (None,) + tuple(gin)
+
+
+def regroup(pieces, sizes):
+    """(B, n_i, d) row sets -> contiguous (B, m_j, d) tensors over the same
+    concatenated token axis (see _Regroup)."""
+    if sum(t.shape[1] for t in pieces) != sum(sizes):
+        raise ShapeError(f"regroup: {sum(t.shape[1] for t in pieces)} rows into {sum(sizes)}")
+    return _Regroup.apply(tuple(int(m) for m in sizes), *pieces)
+
+
+def cat_rows(pieces):
+    """torch.cat(pieces, dim=1) of (B, n_i, d) row sets, one launch each way."""
+    if len(pieces) == 1:
+        return pieces[0]
+    return regroup(pieces, [sum(t.shape[1] for t in pieces)])[0]
 
 
 # ---------------------------------------------------------------------------

@@ -185,7 +185,7 @@ def summarize(S, grp: EventGroup, lens, q_rows, sink=None):
     parts.append(hsp_tok.view(EB, n_tok, d))
     if n_rec > 0:
         parts.append(outs[len(splits)])
-    rows = parts[0] if len(parts) == 1 else torch.cat(parts, dim=1)
+    rows = F.cat_rows(parts)
     if numerics_check_mode() == "eager":
         flag_nonfinite(rows, "hsp_summarize (grouped)")
     return rows

@@ -173,7 +173,11 @@ class SummaryBundle:
 
     def rows(self) -> torch.Tensor:
         parts = [t for t in (self.cls_tokens, self.hsp_tokens, self.recent_tokens) if t.shape[-2] > 0]
-        return parts[0] if len(parts) == 1 else torch.cat(parts, dim=-2)
+        if len(parts) == 1:
+            return parts[0]
+        if parts[0].dim() == 3 and parts[0].is_cuda:
+            return F.cat_rows(parts)  # one kl_regroup launch each way
+        return torch.cat(parts, dim=-2)
 
     @property
     def total_rows(self) -> int:

@@ -155,7 +155,13 @@ class Params:
         return base.as_strided((len(keys),) + tuple(shape), (st,) + tuple(inner), offs[0])
 
     def zero_grad(self) -> None:
-        self.gflat.zero_()
+        if self.gflat.is_cuda:  # a memset (node), not an elementwise fill kernel
+            from . import _capi
+
+            _capi.call("kl_memset", self.gflat.data_ptr(), self.gflat.numel() * 4,
+                       torch.cuda.current_stream(self.gflat.device).cuda_stream)
+        else:
+            self.gflat.zero_()
 
     # -- reference-registry views --------------------------------------------
     def __getitem__(self, name: str) -> torch.Tensor:
