@@ -1330,7 +1330,7 @@ __global__ void __launch_bounds__(128) regroup_kernel(Segs sg) {
 
 // out[b * out_bs + i] = sum_k a[b, i, k] * b[b, i, k] for i < n (rows of a
 // (B, n, d) strided tensor pair): the softmax-VJP row term of one pooled part.
-template <typename T>
+template <typename T, bool VEC>
 __global__ void __launch_bounds__(256) rowdot3_kernel(int B, int n, int d, const T* a, long long a_bs,
                                                       long long a_rs, const T* b, long long b_bs, long long b_rs,
                                                       float* out, long long out_bs) {
@@ -1342,7 +1342,17 @@ __global__ void __launch_bounds__(256) rowdot3_kernel(int B, int n, int d, const
   const T* ar = a + bb * a_bs + i * a_rs;
   const T* br = b + bb * b_bs + i * b_rs;
   float acc = 0.f;
-  for (int k = lane; k < d; k += 32) acc = fmaf(ldf(ar + k), ldf(br + k), acc);
+  if (VEC) {
+    for (int k = lane * 8; k < d; k += 256) {
+      float x[8], y[8];
+      ld8(ar + k, x);
+      ld8(br + k, y);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc = fmaf(x[u], y[u], acc);
+    }
+  } else {
+    for (int k = lane; k < d; k += 32) acc = fmaf(ldf(ar + k), ldf(br + k), acc);
+  }
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   if (lane == 0) out[bb * out_bs + i] = acc;
 }
@@ -1394,12 +1404,22 @@ extern "C" int kl_rowdot3(int B, int n, int d, int dtype, const void* a, long lo
   if ((long long)B * n == 0) return KL_OK;
   const unsigned grid = (unsigned)(((long long)B * n + 7) / 8);
   cudaStream_t s = (cudaStream_t)stream;
-  if (dtype == KL_F32)
-    launch_k(rg::rowdot3_kernel<float>, grid, 256, 0, s, B, n, d, (const float*)a, a_bs, a_rs, (const float*)b, b_bs,
-             b_rs, out, out_bs);
-  else
-    launch_k(rg::rowdot3_kernel<bf16>, grid, 256, 0, s, B, n, d, (const bf16*)a, a_bs, a_rs, (const bf16*)b, b_bs,
-             b_rs, out, out_bs);
+  const bool vec = vec8_ok(a, a_rs, d) && vec8_ok(b, b_rs, d) && a_bs % 8 == 0 && b_bs % 8 == 0;
+  if (dtype == KL_F32) {
+    if (vec)
+      launch_k(rg::rowdot3_kernel<float, true>, grid, 256, 0, s, B, n, d, (const float*)a, a_bs, a_rs,
+               (const float*)b, b_bs, b_rs, out, out_bs);
+    else
+      launch_k(rg::rowdot3_kernel<float, false>, grid, 256, 0, s, B, n, d, (const float*)a, a_bs, a_rs,
+               (const float*)b, b_bs, b_rs, out, out_bs);
+  } else {
+    if (vec)
+      launch_k(rg::rowdot3_kernel<bf16, true>, grid, 256, 0, s, B, n, d, (const bf16*)a, a_bs, a_rs, (const bf16*)b,
+               b_bs, b_rs, out, out_bs);
+    else
+      launch_k(rg::rowdot3_kernel<bf16, false>, grid, 256, 0, s, B, n, d, (const bf16*)a, a_bs, a_rs,
+               (const bf16*)b, b_bs, b_rs, out, out_bs);
+  }
   count_launch();
   return launch_check("rowdot3");
 }

@@ -941,6 +941,52 @@ class _Regroup(torch.autograd.Function):
         return (None,) + tuple(gin)
 
 
+class _GatherRows(torch.autograd.Function):
+    """Rows [a, b) of the token-axis concatenation of (B, n_i, d) pieces as one
+    contiguous (B, b - a, d) tensor (one kl_regroup launch).  VJP: each
+    touched piece's gradient in one launch — written whole where the range
+    covers the piece, zero-filled (memset) around its rows otherwise."""
+
+    @staticmethod
+    def forward(ctx, a, b, *pieces):
+        p0 = pieces[0]
+        B, d = p0.shape[0], p0.shape[2]
+        out = torch.empty(B, b - a, d, device=p0.device, dtype=p0.dtype)
+        segs, lo = [], 0
+        ctx.parts = []  # (piece index, row in piece, row in out, rows, covers the whole piece)
+        for i, t in enumerate(pieces):
+            n = t.shape[1]
+            s0, s1 = max(a, lo), min(b, lo + n)
+            if s0 < s1:
+                segs.append((t if t.stride(2) == 1 else t.contiguous(), s0 - lo, out, s0 - a, s1 - s0))
+                ctx.parts.append((i, s0 - lo, s0 - a, s1 - s0, s1 - s0 == n))
+            lo += n
+        copy_rows(segs, B, d, p0.dtype)
+        ctx.shapes = [t.shape for t in pieces]
+        return out
+
+    @staticmethod
+    def backward(ctx, g):
+        g = g if g.stride(2) == 1 else g.contiguous()
+        B, d = g.shape[0], g.shape[2]
+        grads = [None] * len(ctx.shapes)
+        segs = []
+        for i, r_in, r_out, n, whole in ctx.parts:
+            shape = tuple(ctx.shapes[i])
+            gi = torch.empty(shape, device=g.device, dtype=g.dtype) if whole else zeros(shape, g.device, g.dtype)
+            grads[i] = gi
+            segs.append((g, r_out, gi, r_in, n))
+        copy_rows(segs, B, d, g.dtype)
+        return (None, None) + tuple(grads)
+
+
+def gather_rows(pieces, a, b):
+    """Rows [a, b) of torch.cat(pieces, dim=1) (see _GatherRows)."""
+    if pieces[0].is_cuda:
+        return _GatherRows.apply(int(a), int(b), *pieces)
+    return torch.cat(pieces, dim=1)[:, a:b].contiguous()
+
+
 def regroup(pieces, sizes):
     """(B, n_i, d) row sets -> contiguous (B, m_j, d) tensors over the same
     concatenated token axis (see _Regroup)."""

@@ -1,0 +1,4 @@
+for i in 1 2; do
+for v in NONE KL_AB_ZERO KL_AB_GI KL_AB_ROWS KL_AB_ZS; do
+env $v=1 timeout 600 python bench.py --config c2 --no-cpu --no-e2e 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$v', d['ms_per_step'])"
+done; done

@@ -1,0 +1,6 @@
+for i in 1 2; do
+for v in NONE KL_AB_GIOLD; do
+env $v=1 timeout 600 python bench.py --config c2 --no-cpu --no-e2e 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$v', d['ms_per_step'])"
+done
+env KL_AB_GIOLD=1 KL_AB_HSPDO=1 KL_AB_DQZ=1 KL_AB_ROWS=1 KL_AB_ZERO=1 timeout 600 python bench.py --config c2 --no-cpu --no-e2e 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('ALLOLD', d['ms_per_step'])"
+done
