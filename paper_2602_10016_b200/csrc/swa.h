@@ -17,6 +17,7 @@ struct SwaP {
   const void* dO;
   void* dQKV;
   float* Dbuf;
+  unsigned long long* trace = nullptr;  // debug: CTA 0's pipeline clock stamps (KL_SWA_TRACE), dK / dV kernel
 };
 
 int swa_fwd_simt(const SwaP& p, cudaStream_t s);

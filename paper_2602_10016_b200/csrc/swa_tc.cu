@@ -1374,6 +1374,18 @@ constexpr int MAXQ = 6 * HB;            // queries of a tile's band
 constexpr uint32_t IDESC_S64 = tc::idesc_bf16(128, 64, 0, 0);
 
 constexpr int NT3 = 352;  // warp 0 TMA, warp 1 S^T/dP^T MMAs, warps 2..9 gradients, warp 10 dV/dK MMAs
+constexpr int SDR = 2;
+// pipeline clock stamps of CTA 0 (scripts/r2/swa_trace.py); compiled in only with -DKL_SWA_TRACE_BUILD
+#ifdef KL_SWA_TRACE_BUILD
+#define SWT(ev, idx)                                                                          \
+  do {                                                                                        \
+    if (p.trace && blockIdx.x == 0 && (idx) < 1024) p.trace[(ev) * 1024 + (idx)] = clock64(); \
+  } while (0)
+#else
+#define SWT(ev, idx) \
+  do {               \
+  } while (0)
+#endif    // dK / dV kernel: S^T | dP^T TMEM slots (the other 256 columns: two dV | dK accumulators)
 
 struct Tile {
   int b, h, k0, len, lo, n;  // lo, n: 64-query half-blocks that see keys [k0, k0 + 128)
@@ -1500,13 +1512,13 @@ __global__ void __launch_bounds__(NT3, 1)
   uint64_t* kv_empty = bar + 2;            // [2]
   uint64_t* qg_full = bar + 4;             // [QR]
   uint64_t* qg_empty = qg_full + QR;       // [QR]
-  uint64_t* sd_full = qg_empty + QR;       // [3]
-  uint64_t* sd_empty = sd_full + 3;        // [3]
-  uint64_t* pd_full = sd_empty + 3;        // [2]
+  uint64_t* sd_full = qg_empty + QR;       // [SDR]
+  uint64_t* sd_empty = sd_full + SDR;      // [SDR]
+  uint64_t* pd_full = sd_empty + SDR;      // [2]
   uint64_t* pd_empty = pd_full + 2;        // [2]
-  uint64_t* acc_full = pd_empty + 2;
-  uint64_t* acc_empty = acc_full + 1;
-  uint32_t* tslot = (uint32_t*)(acc_empty + 1);
+  uint64_t* acc_full = pd_empty + 2;      // [2]: dV / dK accumulators double-buffered by tile parity
+  uint64_t* acc_empty = acc_full + 2;     // [2]
+  uint32_t* tslot = (uint32_t*)(acc_empty + 2);
 
   const int nT = (p.T + TB - 1) / TB;
   const int W = p.B * p.H * nT;
@@ -1527,7 +1539,7 @@ __global__ void __launch_bounds__(NT3, 1)
       tc::mbar_init(&qg_full[i], 1);
       tc::mbar_init(&qg_empty[i], 1);
     }
-    for (int i = 0; i < 3; ++i) {
+    for (int i = 0; i < SDR; ++i) {
       tc::mbar_init(&sd_full[i], 1);
       tc::mbar_init(&sd_empty[i], 4);
     }
@@ -1535,8 +1547,10 @@ __global__ void __launch_bounds__(NT3, 1)
       tc::mbar_init(&pd_full[i], 4);
       tc::mbar_init(&pd_empty[i], 1);
     }
-    tc::mbar_init(acc_full, 1);
-    tc::mbar_init(acc_empty, 4);
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&acc_full[i], 1);
+      tc::mbar_init(&acc_empty[i], 4);
+    }
     tc::fence_barrier_init();
   }
   if (warp == 1) tc::tmem_alloc(tslot, 512);
@@ -1545,7 +1559,8 @@ __global__ void __launch_bounds__(NT3, 1)
   tc::fence_after();
   const uint32_t tmem = *tslot;
   KL_PDL_ENTRY();
-  const uint32_t T_DV = 384, T_DK = 448;
+  // TMEM: SDR x (S^T | dP^T) 128-column slots, then two (dV | dK) 128-column accumulators
+  const uint32_t T_ACC = SDR * 128;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -1555,6 +1570,7 @@ __global__ void __launch_bounds__(NT3, 1)
       while (!w.done) {
         const Tile& tl = w.tl;
         const int kb = w.t & 1;
+        SWT(10, w.t);
         tc::mbar_wait(&kv_empty[kb], ((w.t >> 1) & 1) ^ 1);
         tc::mbar_arrive_expect_tx(&kv_full[kb], 2 * TILE);
         tc::tma_load_3d(sKV + kb * 2 * TILE, &tkv, &kv_full[kb], HD + tl.h * DH, tl.k0, tl.b);
@@ -1581,14 +1597,17 @@ __global__ void __launch_bounds__(NT3, 1)
       const uint32_t kv0 = tc::smem_u32(sKV), qg0 = tc::smem_u32(sQG);
       while (!a.done) {
         const int kb = a.t & 1;
+        SWT(0, n);
         if (a.j == a.tl.lo) tc::mbar_wait(&kv_full[kb], (a.t >> 1) & 1);
         const int li = load_index(a, a.j);
         if (li >= waited) {
           tc::mbar_wait(&qg_full[li % QR], (li / QR) & 1);
           waited = li + 1;
         }
-        const int ss = n % 3;
-        tc::mbar_wait(&sd_empty[ss], ((n / 3) & 1) ^ 1);
+        const int ss = n % SDR;
+        SWT(1, n);
+        tc::mbar_wait(&sd_empty[ss], ((n / SDR) & 1) ^ 1);
+        SWT(2, n);
         tc::fence_after();
         const uint32_t ka = kv0 + kb * 2 * TILE, va = ka + TILE;
         const uint32_t qa = qg0 + (li % QR) * 2 * HTILE, ga = qa + HTILE;
@@ -1614,7 +1633,7 @@ __global__ void __launch_bounds__(NT3, 1)
       while (!b.done) {
         const bool first = b.j == b.tl.lo, last = b.j == b.tl.lo + b.tl.n - 1;
         if (first) {
-          tc::mbar_wait(acc_empty, (b.t & 1) ^ 1);
+          tc::mbar_wait(&acc_empty[b.t & 1], ((b.t >> 1) & 1) ^ 1);
           // half-blocks below `keep` are not seen by the next key block of
           // this sequence: their ring slots are released after their products
           keep = b.tl.lo + b.tl.n;
@@ -1627,20 +1646,24 @@ __global__ void __launch_bounds__(NT3, 1)
           }
         }
         const int ps = n & 1;
+        SWT(3, n);
         tc::mbar_wait(&pd_full[ps], (n >> 1) & 1);
+        SWT(4, n);
         tc::fence_after();
         const int li = load_index(b, b.j);
         const uint32_t qa = qg0 + (li % QR) * 2 * HTILE, ga = qa + HTILE;
         const uint32_t pt = pd0 + ps * 2 * PH, dt = pt + PH;
 #pragma unroll
         for (int kk = 0; kk < HB / 16; ++kk)
-          tc::mma_bf16(tmem + T_DV, d_kmaj64(pt, kk), d_mn(ga, kk), IDESC_PV, (!first || kk > 0) ? 1u : 0u);
+          tc::mma_bf16(tmem + T_ACC + (b.t & 1) * 128, d_kmaj64(pt, kk), d_mn(ga, kk), IDESC_PV,
+                       (!first || kk > 0) ? 1u : 0u);
 #pragma unroll
         for (int kk = 0; kk < HB / 16; ++kk)
-          tc::mma_bf16(tmem + T_DK, d_kmaj64(dt, kk), d_mn(qa, kk), IDESC_PV, (!first || kk > 0) ? 1u : 0u);
+          tc::mma_bf16(tmem + T_ACC + (b.t & 1) * 128 + 64, d_kmaj64(dt, kk), d_mn(qa, kk), IDESC_PV,
+                       (!first || kk > 0) ? 1u : 0u);
         tc::mma_commit(&pd_empty[ps]);
         if (b.j < keep) tc::mma_commit(&qg_empty[li % QR]);
-        if (last) tc::mma_commit(acc_full);
+        if (last) tc::mma_commit(&acc_full[b.t & 1]);
         ++n;
         walk_step(p, b);
       }
@@ -1662,16 +1685,18 @@ __global__ void __launch_bounds__(NT3, 1)
     struct LD3 {
       float l[3], d[3];
     };
+    // raw loads only (in-range addresses; masked and scaled when staged): an
+    // instruction that consumed the loaded values here would stall the warp
+    // for the full DRAM latency at every tile
     auto fetch = [](const SwaP& pp, const Tile& tl, int tid) {
       LD3 v;
       const float* LSE = pp.LSE + ((long long)tl.b * pp.H + tl.h) * pp.T;
       const float* D = pp.Dbuf + ((long long)tl.b * pp.H + tl.h) * pp.T;
 #pragma unroll
       for (int u = 0; u < 3; ++u) {
-        const int i = tid + u * 128, q = tl.lo * HB + i;
-        const bool in = i < tl.n * HB && q < tl.len;
-        v.l[u] = in ? LSE[q] * 1.4426950408889634f : INFINITY;
-        v.d[u] = in ? D[q] : 0.f;
+        const int q = min(tl.lo * HB + tid + u * 128, pp.T - 1);
+        v.l[u] = LSE[q];
+        v.d[u] = D[q];
       }
       return v;
     };
@@ -1689,8 +1714,7 @@ __global__ void __launch_bounds__(NT3, 1)
       walk_adv(p, pw);
       if (pw.idx < i1) walk_fill(p, pw);
     }
-    LD3 nx = {};
-    if (pw.idx < i1) nx = fetch(p, pw.tl, wtid);
+    LD3 nx = fetch(p, pw.idx < i1 ? pw.tl : w.tl, wtid);
     for (; w.idx < i1; walk_adv(p, w)) {
       walk_fill(p, w);
       const Tile tl = w.tl;
@@ -1701,28 +1725,36 @@ __global__ void __launch_bounds__(NT3, 1)
       }
       float* ls = sLD[wg][t & 1][0];
       float* dd = sLD[wg][t & 1][1];
+      if (wtid == 0) SWT(11 + wg, t);
 #pragma unroll
       for (int u = 0; u < 3; ++u) {
-        ls[wtid + u * 128] = nx.l[u];
-        dd[wtid + u * 128] = nx.d[u];
+        const int i = wtid + u * 128, q = tl.lo * HB + i;
+        const bool in = i < tl.n * HB && q < tl.len;
+        ls[i] = in ? nx.l[u] * 1.4426950408889634f : INFINITY;
+        dd[i] = in ? nx.d[u] : 0.f;
       }
+      if (wtid == 0) SWT(13 + wg, t);
       named_bar(1 + wg, 128);
+      if (wtid == 0) SWT(15 + wg, t);
       pw = w;
       do {
         walk_adv(p, pw);
         if (pw.idx < i1) walk_fill(p, pw);
       } while (pw.idx < i1 && !pw.tl.real);
-      if (pw.idx < i1) nx = fetch(p, pw.tl, wtid);
+      nx = fetch(p, pw.idx < i1 ? pw.tl : tl, wtid);
       const int key = tl.k0 + r;
       int qlo = max(0, key - p.w), qhi = min(tl.len - 1, key + p.w);
       if (p.causal) qlo = max(qlo, key);
       if (key >= tl.len) qhi = -1;
       const int last_item = n_item + tl.n - 1;
+      if (wtid == 0) SWT(17 + wg, t);
       for (int jj = 0; jj < tl.n; ++jj, ++n_item) {
         if ((n_item & 1) != wg) continue;
-        const int ss = n_item % 3;
+        const int ss = n_item % SDR;
         uint8_t* blk = sPD + wg * 2 * PH;
-        tc::mbar_wait(&sd_full[ss], (n_item / 3) & 1);
+        if (wtid == 0) SWT(5, n_item);
+        tc::mbar_wait(&sd_full[ss], (n_item / SDR) & 1);
+        if (wtid == 0) SWT(6, n_item);
         tc::fence_after();
 #pragma unroll 1
         for (int ch = 0; ch < 2; ++ch) {
@@ -1774,11 +1806,14 @@ __global__ void __launch_bounds__(NT3, 1)
         }
         tc::fence_async_smem();
         __syncwarp();
+        if (wtid == 0) SWT(7, n_item);
         if (lane == 0) tc::mbar_arrive(&pd_full[wg]);
       }
       // the warpgroup that took the tile's last half-block writes dK / dV
       if ((last_item & 1) == wg) {
-        tc::mbar_wait(acc_full, t & 1);
+        if (wtid == 0) SWT(8, t);
+        tc::mbar_wait(&acc_full[t & 1], (t >> 1) & 1);
+        if (wtid == 0) SWT(9, t);
         tc::fence_after();
 #pragma unroll 1
         for (int which = 0; which < 2; ++which) {  // 0: dK (scaled), 1: dV
@@ -1786,11 +1821,11 @@ __global__ void __launch_bounds__(NT3, 1)
 #pragma unroll 1
           for (int ch = 0; ch < 2; ++ch) {
             float v[32];
-            tc::tmem_ld32(trow + (which ? T_DV : T_DK) + ch * 32, v);
+            tc::tmem_ld32(trow + T_ACC + (t & 1) * 128 + (which ? 0 : 64) + ch * 32, v);
             if (which == 1 && ch == 1) {
               tc::fence_before();
               __syncwarp();
-              if (lane == 0) tc::mbar_arrive(acc_empty);
+              if (lane == 0) tc::mbar_arrive(&acc_empty[t & 1]);
             }
             if (key < p.T) {
               uint4* o = reinterpret_cast<uint4*>(out + (long long)key * p.ld_qkv + (1 + which) * HD + ch * 32);
@@ -1806,6 +1841,7 @@ __global__ void __launch_bounds__(NT3, 1)
             }
           }
         }
+        if (wtid == 0) SWT(19, t);
       }
       ++t;
     }
@@ -1815,7 +1851,7 @@ __global__ void __launch_bounds__(NT3, 1)
   if (warp == 1) tc::tmem_dealloc(tmem, 512);
 }
 
-size_t dkv_smem_bytes() { return 1024 + 2 * 2 * TILE + QR * 2 * HTILE + 2 * 2 * PH + (4 + 2 * QR + 6 + 4 + 2) * 8 + 16; }
+size_t dkv_smem_bytes() { return 1024 + 2 * 2 * TILE + QR * 2 * HTILE + 2 * 2 * PH + (4 + 2 * QR + 2 * SDR + 4 + 4) * 8 + 16; }
 
 // ---------------------------------------------------------------------------
 // dQ v3: the query-block-major mirror of dK / dV v3.  A tile is a 128-query
@@ -1999,11 +2035,12 @@ __global__ void __launch_bounds__(NT3, 1)
     w.tl.b = w.bh % p.B;
     w.tl.h = w.bh / p.B;
     // this row's LSE (log2 units) / D of the next real tile, prefetched
+    // raw loads (masked / scaled at the tile that uses them, see dK / dV)
     auto fetch = [&](const Tile& tl, float& l2, float& dr) {
-      const int q = tl.k0 + r;
+      const int q = min(tl.k0 + r, p.T - 1);
       const long long off = ((long long)tl.b * p.H + tl.h) * p.T + q;
-      l2 = q < tl.len ? p.LSE[off] * 1.4426950408889634f : 0.f;
-      dr = q < tl.len ? p.Dbuf[off] : 0.f;
+      l2 = p.LSE[off];
+      dr = p.Dbuf[off];
     };
     Walk pw = w;
     walk_fill<true>(p, pw);
@@ -2012,7 +2049,7 @@ __global__ void __launch_bounds__(NT3, 1)
       if (pw.idx < i1) walk_fill<true>(p, pw);
     }
     float nl = 0.f, nd = 0.f;
-    if (pw.idx < i1) fetch(pw.tl, nl, nd);
+    fetch(pw.idx < i1 ? pw.tl : w.tl, nl, nd);
     for (; w.idx < i1; walk_adv(p, w)) {
       walk_fill<true>(p, w);
       const Tile tl = w.tl;
@@ -2021,13 +2058,14 @@ __global__ void __launch_bounds__(NT3, 1)
         zero_rows(out, p.ld_qkv, tl.k0, TB, p.T, wg * 128 + wtid, 256);
         continue;
       }
-      const float lse2 = nl, dr = nd;
+      const bool qin = tl.k0 + r < tl.len;
+      const float lse2 = qin ? nl * 1.4426950408889634f : 0.f, dr = qin ? nd : 0.f;
       pw = w;
       do {
         walk_adv(p, pw);
         if (pw.idx < i1) walk_fill<true>(p, pw);
       } while (pw.idx < i1 && !pw.tl.real);
-      if (pw.idx < i1) fetch(pw.tl, nl, nd);
+      fetch(pw.idx < i1 ? pw.tl : tl, nl, nd);
       const int q = tl.k0 + r;
       int klo = max(0, q - p.w), khi = min(tl.len - 1, q + p.w);
       if (p.causal) khi = min(khi, q);
@@ -2437,6 +2475,8 @@ int swa_bwd_tc(const SwaP& p, cudaStream_t s) {
   if (!map3(&tdo, p.dO, (long long)p.H * DH, p.T, p.B, p.ld_o, p.bs_o)) return KL_EUNSUPPORTED;
   int rc = swa_rowdot(p, s);
   if (rc) return rc;
+  SwaP pt = p;
+  if (const char* tv = getenv("KL_SWA_TRACE")) pt.trace = (unsigned long long*)strtoull(tv, nullptr, 0);  // testing
   if (!getenv("KL_SWA_BWD_V1")) {
     const int W = p.B * p.H * ((p.T + TB - 1) / TB);
     const int grid = std::min(W, tc_num_sms());
@@ -2448,7 +2488,7 @@ int swa_bwd_tc(const SwaP& p, cudaStream_t s) {
         map3(&tdo64, p.dO, (long long)p.H * DH, p.T, p.B, p.ld_o, p.bs_o, 64)) {
       const size_t s1 = v3::dkv_smem_bytes();
       cudaFuncSetAttribute(v3::swa_bwd_dkv_tc3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1);
-      launch_k(v3::swa_bwd_dkv_tc3_kernel, grid, v3::NT3, s1, s, tq, tq64, tdo64, p);
+      launch_k(v3::swa_bwd_dkv_tc3_kernel, grid, v3::NT3, s1, s, tq, tq64, tdo64, pt);
     } else {
       const size_t s1 = v2::dkv_smem_bytes();
       cudaFuncSetAttribute(v2::swa_bwd_dkv_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1);

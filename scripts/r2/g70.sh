@@ -1,0 +1,3 @@
+timeout 300 python scripts/r2/swa_trace.py | tail -20
+KL_LIB_PATH=$PWD/paper_2602_10016_b200/lib/ab_new.so timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -k "swa or window or mha" 2>&1 | tail -2
+bash scripts/r2/ab.sh scripts/r2/swa_time.py
