@@ -2230,6 +2230,7 @@ __global__ void __launch_bounds__(NTF, 2)
       int n = 0;
       while (!w.done) {
         const Tile& tl = w.tl;
+        SWT(10, w.t);
         tc::mbar_wait(q_empty, (w.t & 1) ^ 1);
         tc::mbar_arrive_expect_tx(q_full, TILE);
         tc::tma_load_3d(sQ, &tq, q_full, tl.h * DH, tl.k0, tl.b);
@@ -2250,10 +2251,13 @@ __global__ void __launch_bounds__(NTF, 2)
       int n = 0;
       const uint32_t qa = tc::smem_u32(sQ), kv0 = tc::smem_u32(sKV);
       while (!a.done) {
+        SWT(0, n);
         if (a.j == a.tl.lo) tc::mbar_wait(q_full, a.t & 1);
         const int s = n % FKR, ss = n % FNS;
         tc::mbar_wait(&kv_full[s], (n / FKR) & 1);
+        SWT(1, n);
         tc::mbar_wait(&s_empty[ss], ((n / FNS) & 1) ^ 1);
+        SWT(2, n);
         tc::fence_after();
         const uint32_t ka = kv0 + s * 2 * HTILE;
 #pragma unroll
@@ -2275,7 +2279,9 @@ __global__ void __launch_bounds__(NTF, 2)
         const bool first = b.j == b.tl.lo, last = b.j == b.tl.lo + b.tl.n - 1;
         if (first) tc::mbar_wait(o_empty, (b.t & 1) ^ 1);
         const int ps = n & 1, s = n % FKR;
+        SWT(3, n);
         tc::mbar_wait(&p_full[ps], (n >> 1) & 1);
+        SWT(4, n);
         tc::fence_after();
         const uint32_t va = kv0 + s * 2 * HTILE + HTILE, pa = p0 + ps * PH;
 #pragma unroll
@@ -2323,7 +2329,9 @@ __global__ void __launch_bounds__(NTF, 2)
         const int ss = n % FNS, ps = n & 1;
         const int k0 = (tl.lo + jj) * HB;
         float v[64];
+        if (ctid == 0) SWT(5, n);
         tc::mbar_wait(&s_full[ss], (n / FNS) & 1);
+        if (ctid == 0) SWT(6, n);
         tc::fence_after();
         tc::tmem_ld32(trow + ss * 64, v);
         tc::tmem_ld32(trow + ss * 64 + 32, v + 32);
@@ -2346,7 +2354,9 @@ __global__ void __launch_bounds__(NTF, 2)
         mb = mb == -INFINITY ? -INFINITY : mb * c2;
         const bool up = mb > mref + RESCALE2;
         // the P slot is free once the product of the item two back completed
+        if (ctid == 0) SWT(7, n);
         tc::mbar_wait(&p_empty[ps], ((n >> 1) & 1) ^ 1);
+        if (ctid == 0) SWT(8, n);
         if (jj > 0 && __any_sync(0xffffffffu, up)) {
           // O must be stable: the previous item's product has completed too
           tc::mbar_wait(&p_empty[ps ^ 1], (((n - 1) >> 1) & 1));
@@ -2378,9 +2388,12 @@ __global__ void __launch_bounds__(NTF, 2)
         store_sw(blk, r, 32, pk + 16);
         tc::fence_async_smem();
         __syncwarp();
+        if (ctid == 0) SWT(9, n);
         if (lane == 0) tc::mbar_arrive(&p_full[ps]);
       }
+      if (ctid == 0) SWT(11, t);
       tc::mbar_wait(o_full, t & 1);
+      if (ctid == 0) SWT(12, t);
       tc::fence_after();
       float o[64];
       tc::tmem_ld32(trow + T_O, o);
@@ -2402,6 +2415,7 @@ __global__ void __launch_bounds__(NTF, 2)
         }
         LSE[q] = l > 0.f ? (mref + __log2f(l)) * 0.6931471805599453f : INFINITY;
       }
+      if (ctid == 0) SWT(13, t);
       ++t;
     }
   }
@@ -2439,8 +2453,10 @@ bool supported(const SwaP& p) {
 
 int swa_rowdot(const SwaP& p, cudaStream_t s);
 
-int swa_fwd_tc(const SwaP& p, cudaStream_t s) {
-  if (!supported(p)) return KL_EUNSUPPORTED;
+int swa_fwd_tc(const SwaP& p0, cudaStream_t s) {
+  if (!supported(p0)) return KL_EUNSUPPORTED;
+  SwaP p = p0;
+  if (const char* tv = getenv("KL_SWA_TRACE_FWD")) p.trace = (unsigned long long*)strtoull(tv, nullptr, 0);  // testing
   CUtensorMap tq;
   if (!map3(&tq, p.QKV, 3LL * p.H * DH, p.T, p.B, p.ld_qkv, p.bs_qkv)) return KL_EUNSUPPORTED;
   if (getenv("KL_SWA_FWD_V1")) {
