@@ -83,6 +83,7 @@ int kl_last_gemm_path(void);
 #define KL_PATH_COLSOFTMAX 10   /* column softmax of the pooling composition   */
 #define KL_PATH_GDPA_FWD_TC512 11 /* fused GDPA forward, d = 512 variant       */
 #define KL_PATH_GDPA_BWD_TC512 12 /* fused GDPA backward, d = 512 variant      */
+#define KL_PATH_HSP_FWD_SPLIT 13 /* HSP forward d = 512, split form          */
 #define KL_PATH_COUNT 16
 unsigned long long kl_path_hits(int path);
 void kl_reset_path_hits(void);
@@ -217,9 +218,16 @@ typedef struct kl_hsp_args {
    * contiguous, and sample b pools with set b / q_group; 0 = one set shared
    * by every sample (the reference's batch-shared queries). */
   int q_group;
+  /* d = 512 forward: scratch for the split form (per-part partial pooled rows
+   * + arrival counters), at least kl_hsp_fwd_workspace_bytes(args) bytes,
+   * 16-byte aligned, not shared with a concurrent launch; NULL selects the
+   * unsplit kernel. */
+  void* workspace;
+  long long workspace_bytes;
 } kl_hsp_args;
 
 int kl_hsp_fwd(const kl_hsp_args* args, void* stream);
+long long kl_hsp_fwd_workspace_bytes(const kl_hsp_args* args);
 int kl_hsp_bwd(const kl_hsp_args* args, void* stream);
 
 /*

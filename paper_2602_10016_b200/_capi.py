@@ -125,6 +125,7 @@ class HspArgs(C.Structure):
         ("dZ", C.c_void_p), ("dZ_lo", C.c_void_p),
         ("Dq", C.c_void_p),
         ("q_group", C.c_int),
+        ("workspace", C.c_void_p), ("workspace_bytes", C.c_longlong),
     ]
 
 
@@ -151,6 +152,7 @@ _SIGS = {
     "kl_gdpa_fwd": ([C.POINTER(GdpaArgs), C.c_void_p], C.c_int),
     "kl_gdpa_bwd": ([C.POINTER(GdpaArgs), C.c_void_p], C.c_int),
     "kl_hsp_fwd": ([C.POINTER(HspArgs), C.c_void_p], C.c_int),
+    "kl_hsp_fwd_workspace_bytes": ([C.POINTER(HspArgs)], C.c_longlong),
     "kl_hsp_bwd": ([C.POINTER(HspArgs), C.c_void_p], C.c_int),
     "kl_swa_fwd": ([C.POINTER(SwaArgs), C.c_void_p], C.c_int),
     "kl_swa_bwd": ([C.POINTER(SwaArgs), C.c_void_p], C.c_int),
@@ -521,7 +523,7 @@ def launch_count() -> int:
 # Kernel-path counters (include/kunlun_capi.h KL_PATH_*).
 PATHS = {"gemm_tc": 0, "gemm_simt": 1, "gdpa_fwd_tc": 2, "gdpa_bwd_tc": 3, "hsp_fwd_tc": 4, "hsp_bwd_tc": 5,
          "swa_fwd_tc": 6, "swa_bwd_tc": 7, "swa_fwd_simt": 8, "swa_bwd_simt": 9, "colsoftmax": 10,
-         "gdpa_fwd_tc512": 11, "gdpa_bwd_tc512": 12}
+         "gdpa_fwd_tc512": 11, "gdpa_bwd_tc512": 12, "hsp_fwd_split": 13}
 
 
 def path_hits() -> dict:

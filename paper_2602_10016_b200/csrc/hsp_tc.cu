@@ -932,6 +932,366 @@ __global__ void __launch_bounds__(NT, 1)
 
 size_t fwd512_smem() { return 1024 + ZST * ZSTAGE + 4 * ATOM + 2 * ATOM + (2 * ZST + 10) * 8 + 16; }
 
+// ---------------------------------------------------------------------------
+// d = 512 forward, balanced form.  The kernel above runs one (sample, query
+// tile, half) item per CTA: 192 items on 148 SMs leave the SMs active ~60 %
+// of the kernel (ncu, c4).  Here a CTA serves one lane (query set g, query
+// tile qt, output half h) and an even share of that lane's 128-key blocks
+// (all samples of the group, flattened), with the data path of the kernel
+// above.  A sample cut by a share boundary leaves its per-part partial
+// (unnormalised O half, running max, sum) in the workspace; the last part to
+// arrive (per-(lane, sample) counter) merges them.  (A variant that kept the
+// lane's 128 x 512 query tile resident and streamed S once in 64-key blocks
+// was slower: its N = 64 score products run at 2/3 rate and the shared
+// memory left for the S stream holds one block, so TMA latency paced it.)
+constexpr int PARTF = 256 * 128 + 2 * 128;  // partial: O [col][row] fp32, max (log2), sum
+
+struct SplitP {
+  int B, T, HQ, n1, qtiles, qg, cpl, lanes;
+  const int* lengths;
+  bf16* O1;
+  long long o1_bs;
+  bf16* O2;
+  long long o2_bs;
+  float* LSE;
+  float* ws;       // [grid][2][PARTF]
+  unsigned* cnt;   // [lanes][qg] arrival counters, zero on entry, re-zeroed by the merging CTA
+};
+
+__device__ __forceinline__ int part_start(long long NB, int p, int cpl) { return (int)(NB * p / cpl); }
+
+// The part containing flattened block x.
+__device__ __forceinline__ int part_of(long long NB, int x, int cpl) {
+  int p = (int)(((long long)x * cpl) / (NB > 0 ? NB : 1));
+  while (p + 1 < cpl && part_start(NB, p + 1, cpl) <= x) ++p;
+  while (p > 0 && part_start(NB, p, cpl) > x) --p;
+  return p;
+}
+
+// Walks the (sample, block range) segments of this CTA's part: calls
+// f(b, j0, j1, whole, first, Fb) for every sample with blocks in [P0, P1)
+// (first: the segment opens the part; Fb: the sample's first flattened block).
+template <typename F>
+__device__ __forceinline__ void walk_segments(const SplitP& p, int g, int P0, int P1, F&& f) {
+  int F0 = 0;
+  for (int bi = 0; bi < p.qg && F0 < P1; ++bi) {
+    const int b = g * p.qg + bi;
+    const int nb = nblocks(p.lengths, b);
+    const int s0 = max(F0, P0), s1 = min(F0 + nb, P1);
+    if (s0 < s1) f(b, s0 - F0, s1 - F0, s0 == F0 && s1 == F0 + nb, s0 == P0, F0);
+    F0 += nb;
+  }
+}
+
+__global__ void __launch_bounds__(NT, 1)
+    hsp_fwd512b_kernel(const __grid_constant__ CUtensorMap tmS, const __grid_constant__ CUtensorMap tmQ, SplitP p) {
+  constexpr int D = 512, NA = 8, DH = 256;
+  constexpr uint32_t IDESC_Z = tc::idesc_bf16(TB, TB, 0, 0);
+  constexpr uint32_t IDESC_O = tc::idesc_bf16(TB, DH, 0, 1);
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sZ = sm;                       // ZST x (Qt atom | S atom)
+  uint8_t* sO = sZ + ZST * ZSTAGE;        // 4 S atoms (half h of block j)
+  uint8_t* sP = sO + 4 * ATOM;            // 128 x 128 bf16
+  uint64_t* bar = (uint64_t*)(sP + 2 * ATOM);
+  uint64_t* zs_full = bar;                // [ZST]
+  uint64_t* zs_empty = bar + ZST;         // [ZST]
+  uint64_t* os_full = bar + 2 * ZST;
+  uint64_t* os_empty = os_full + 1;
+  uint64_t* z_full = os_full + 2;         // [2]
+  uint64_t* z_empty = os_full + 4;        // [2]
+  uint64_t* p_full = os_full + 6;
+  uint64_t* p_empty = os_full + 7;
+  uint64_t* o_full = os_full + 8;
+  uint64_t* o_empty = os_full + 9;
+  uint32_t* tslot = (uint32_t*)(os_full + 10);
+  volatile int* flag = (volatile int*)(tslot + 1);
+
+  const int lane_id = blockIdx.x / p.cpl, part = blockIdx.x % p.cpl;
+  const int g = lane_id / (2 * p.qtiles), qt = (lane_id >> 1) % p.qtiles, h = lane_id & 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    tc::prefetch_tmap(&tmS);
+    tc::prefetch_tmap(&tmQ);
+    for (int i = 0; i < ZST; ++i) {
+      tc::mbar_init(&zs_full[i], 1);
+      tc::mbar_init(&zs_empty[i], 1);
+    }
+    tc::mbar_init(os_full, 1);
+    tc::mbar_init(os_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&z_full[i], 1);
+      tc::mbar_init(&z_empty[i], 4);
+    }
+    tc::mbar_init(p_full, 4);
+    tc::mbar_init(p_empty, 1);
+    tc::mbar_init(o_full, 1);
+    tc::mbar_init(o_empty, 4);
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tslot, 512);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tslot;
+  KL_PDL_ENTRY();
+  const uint32_t T_O = 256;
+
+  long long NBl = 0;  // the lane's flattened 128-key blocks
+  for (int bi = 0; bi < p.qg; ++bi) NBl += nblocks(p.lengths, g * p.qg + bi);
+  const int P0 = part_start(NBl, part, p.cpl), P1 = part_start(NBl, part + 1, p.cpl);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int zc = 0, oc = 0;
+      walk_segments(p, g, P0, P1, [&](int b, int j0, int j1, bool, bool, int) {
+        for (int j = j0; j < j1; ++j) {
+#pragma unroll 1
+          for (int a = 0; a < NA; ++a, ++zc) {
+            const int st = zc % ZST;
+            tc::mbar_wait(&zs_empty[st], ((zc / ZST) & 1) ^ 1);
+            tc::mbar_arrive_expect_tx(&zs_full[st], ZSTAGE);
+            tc::tma_load_3d(sZ + st * ZSTAGE, &tmQ, &zs_full[st], a * 64, qt * TB, g);
+            tc::tma_load_3d(sZ + st * ZSTAGE + ATOM, &tmS, &zs_full[st], a * 64, j * TB, b);
+          }
+          tc::mbar_wait(os_empty, (oc & 1) ^ 1);
+          tc::mbar_arrive_expect_tx(os_full, 4 * ATOM);
+#pragma unroll
+          for (int a = 0; a < 4; ++a) tc::tma_load_3d(sO + a * ATOM, &tmS, os_full, (4 * h + a) * 64, j * TB, b);
+          ++oc;
+        }
+      });
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && P0 < P1) {
+      int zc = 0, zb = 0, oc = 0, pc = 0, t = 0;
+      const uint32_t z0 = tc::smem_u32(sZ), oa = tc::smem_u32(sO), pa = tc::smem_u32(sP);
+      auto mma_z = [&]() {  // the next Z block into buffer zb & 1
+        const int z = zb & 1;
+        tc::mbar_wait(&z_empty[z], ((zb >> 1) & 1) ^ 1);
+        tc::fence_after();
+#pragma unroll 1
+        for (int a = 0; a < NA; ++a, ++zc) {
+          const int st = zc % ZST;
+          tc::mbar_wait(&zs_full[st], (zc / ZST) & 1);
+          tc::fence_after();
+          const uint32_t qa = z0 + st * ZSTAGE, sa = qa + ATOM;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            tc::mma_bf16(tmem + z * TB, dk(qa, kk), dk(sa, kk), IDESC_Z, (a | kk) > 0 ? 1u : 0u);
+          tc::mma_commit(&zs_empty[st]);
+        }
+        tc::mma_commit(&z_full[z]);
+        ++zb;
+      };
+      const int total = P1 - P0;
+      mma_z();
+      walk_segments(p, g, P0, P1, [&](int, int j0, int j1, bool, bool, int) {
+        for (int j = j0; j < j1; ++j) {
+          if (zb < total) mma_z();  // Z of the next block (possibly the next segment's) ahead of this block's O
+          tc::mbar_wait(p_full, pc & 1);
+          if (j == j0) tc::mbar_wait(o_empty, (t & 1) ^ 1);  // the epilogue has read the previous segment's O
+          tc::mbar_wait(os_full, oc & 1);
+          tc::fence_after();
+#pragma unroll
+          for (int kk = 0; kk < TB / 16; ++kk)
+            tc::mma_bf16(tmem + T_O, dk(pa, kk), dmn(oa, kk), IDESC_O, (j > j0 || kk > 0) ? 1u : 0u);
+          tc::mma_commit(p_empty);
+          tc::mma_commit(os_empty);
+          ++pc;
+          ++oc;
+        }
+        tc::mma_commit(o_full);
+        ++t;
+      });
+    }
+  } else {
+    const int qtr = warp & 3;
+    const int r = qtr * 32 + lane;
+    const uint32_t trow = tmem + ((uint32_t)(qtr * 32) << 16);
+    const int q = qt * TB + r;
+    const bool qok = q < p.HQ;
+    auto out_row = [&](int b) -> bf16* {
+      return q < p.n1 ? p.O1 + (long long)b * p.o1_bs + (long long)q * D
+                      : p.O2 + (long long)b * p.o2_bs + (long long)(q - p.n1) * D;
+    };
+    // empty samples of the group: zero rows, LSE = +inf (seqsum.py:32-33, 99-100)
+    for (int bi = part; bi < p.qg; bi += p.cpl) {
+      const int b = g * p.qg + bi;
+      if (p.lengths[b] > 0 || !qok) continue;
+      const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
+      bf16* o = out_row(b) + h * DH;
+#pragma unroll 4
+      for (int c = 0; c < DH; c += 8) *reinterpret_cast<uint4*>(o + c) = z4;
+      if (h == 1) p.LSE[(long long)b * p.HQ + q] = INFINITY;
+    }
+    int zc = 0, pc = 0, t = 0;
+    walk_segments(p, g, P0, P1, [&](int b, int j0, int j1, bool whole, bool first_seg, int Fb) {
+      const int len = p.lengths[b];
+      float mref = -INFINITY, l = 0.f;
+      for (int j = j0; j < j1; ++j, ++zc, ++pc) {
+        const int z = zc & 1;
+        const uint32_t tz = trow + z * TB;
+        const int tv = len - j * TB;
+        tc::mbar_wait(&z_full[z], (zc >> 1) & 1);
+        tc::fence_after();
+        float mb = -INFINITY;
+#pragma unroll
+        for (int c0 = 0; c0 < TB; c0 += 32) {
+          float v[32];
+          tc::tmem_ld32(tz + c0, v);
+          if (c0 + 32 <= tv) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) mb = fmaxf(mb, v[i]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (c0 + i < tv) mb = fmaxf(mb, v[i]);
+          }
+        }
+        mb *= LOG2E;
+        tc::mbar_wait(p_empty, (pc & 1) ^ 1);  // O of the previous block is complete (and P is free)
+        tc::fence_after();
+        const bool up = mb > mref + RESCALE;
+        if (j > j0 && __any_sync(0xffffffffu, up)) {
+          const float al = up ? ex2(mref - mb) : 1.f;
+          l *= al;
+#pragma unroll 1
+          for (int c0 = 0; c0 < DH; c0 += 16) {
+            float v[16];
+            uint32_t u[16];
+            tc::tmem_ld16(trow + T_O + c0, v);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) u[i] = __float_as_uint(v[i] * al);
+            tc::tmem_st16(trow + T_O + c0, u);
+          }
+        }
+        if (up) mref = mb;
+#pragma unroll
+        for (int c0 = 0; c0 < TB; c0 += 32) {
+          float v[32];
+          uint32_t pk[16];
+          tc::tmem_ld32(tz + c0, v);
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            const float a = c0 + i < tv ? ex2(fmaf(v[i], LOG2E, -mref)) : 0.f;
+            const float bq = c0 + i + 1 < tv ? ex2(fmaf(v[i + 1], LOG2E, -mref)) : 0.f;
+            l += a + bq;
+            pk[i >> 1] = tc::pack_bf16(a, bq);
+          }
+          store_sw(sP, r, c0, pk);
+        }
+        tc::fence_async_smem();
+        tc::fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          tc::mbar_arrive(&z_empty[z]);
+          tc::mbar_arrive(p_full);
+        }
+      }
+      // segment epilogue
+      tc::mbar_wait(o_full, t & 1);
+      tc::fence_after();
+      if (whole) {
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+#pragma unroll 1
+        for (int c0 = 0; c0 < DH; c0 += 32) {
+          float v[32];
+          tc::tmem_ld32(trow + T_O + c0, v);
+          if (qok) {
+            uint4* o = reinterpret_cast<uint4*>(out_row(b) + h * DH + c0);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              uint4 w;
+              w.x = tc::pack_bf16(v[8 * c + 0] * inv, v[8 * c + 1] * inv);
+              w.y = tc::pack_bf16(v[8 * c + 2] * inv, v[8 * c + 3] * inv);
+              w.z = tc::pack_bf16(v[8 * c + 4] * inv, v[8 * c + 5] * inv);
+              w.w = tc::pack_bf16(v[8 * c + 6] * inv, v[8 * c + 7] * inv);
+              o[c] = w;
+            }
+          }
+        }
+        if (qok && h == 1) p.LSE[(long long)b * p.HQ + q] = (mref + __log2f(l)) * 0.6931471805599453f;
+        tc::fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(o_empty);
+      } else {
+        // a cut sample is its part's first segment (slot 0) or last one (slot 1):
+        // unnormalised O half ([col][row]: coalesced per warp), max, sum -> workspace
+        float* pw_own = p.ws + ((long long)blockIdx.x * 2 + (first_seg ? 0 : 1)) * PARTF;
+#pragma unroll 1
+        for (int c0 = 0; c0 < DH; c0 += 32) {
+          float v[32];
+          tc::tmem_ld32(trow + T_O + c0, v);
+#pragma unroll
+          for (int c = 0; c < 32; ++c) __stcg(pw_own + (c0 + c) * TB + r, v[c]);
+        }
+        __stcg(pw_own + DH * TB + r, mref);
+        __stcg(pw_own + DH * TB + TB + r, l);
+        tc::fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(o_empty);
+        __threadfence();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        // parts holding blocks of sample b (parts own no blocks when the lane has
+        // fewer blocks than parts; those never arrive)
+        const int plo = part_of(NBl, Fb, p.cpl), phi = part_of(NBl, Fb + nblocks(p.lengths, b) - 1, p.cpl);
+        auto owns = [&](int pq) { return part_start(NBl, pq + 1, p.cpl) > part_start(NBl, pq, p.cpl); };
+        int nparts = 0;
+        for (int pq = plo; pq <= phi; ++pq) nparts += owns(pq);
+        unsigned* cn = p.cnt + (long long)lane_id * p.qg + (b - g * p.qg);
+        if (threadIdx.x == 64) *flag = (atomicAdd(cn, 1u) == (unsigned)(nparts - 1)) ? 1 : 0;
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (*flag) {  // the last part of this sample to finish merges the partials
+          __threadfence();
+          auto part_ws = [&](int pq) {
+            const int sl = (pq == plo && part_start(NBl, plo, p.cpl) < Fb) ? 1 : 0;
+            return p.ws + ((long long)(lane_id * p.cpl + pq) * 2 + sl) * PARTF;
+          };
+          float M = -INFINITY;
+          for (int pq = plo; pq <= phi; ++pq)
+            if (owns(pq)) M = fmaxf(M, __ldcg(part_ws(pq) + DH * TB + r));
+          float L = 0.f;
+          for (int pq = plo; pq <= phi; ++pq) {
+            if (!owns(pq)) continue;
+            const float* pw = part_ws(pq);
+            L += __ldcg(pw + DH * TB + TB + r) * ex2(__ldcg(pw + DH * TB + r) - M);
+          }
+          const float inv = L > 0.f ? 1.f / L : 0.f;
+#pragma unroll 1
+          for (int c0 = 0; c0 < DH; c0 += 8) {
+            float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            for (int pq = plo; pq <= phi; ++pq) {
+              if (!owns(pq)) continue;
+              const float* pw = part_ws(pq);
+              const float wgt = ex2(__ldcg(pw + DH * TB + r) - M);
+#pragma unroll
+              for (int c = 0; c < 8; ++c) acc[c] += wgt * __ldcg(pw + (c0 + c) * TB + r);
+            }
+            if (qok) {
+              uint4 w;
+              w.x = tc::pack_bf16(acc[0] * inv, acc[1] * inv);
+              w.y = tc::pack_bf16(acc[2] * inv, acc[3] * inv);
+              w.z = tc::pack_bf16(acc[4] * inv, acc[5] * inv);
+              w.w = tc::pack_bf16(acc[6] * inv, acc[7] * inv);
+              *reinterpret_cast<uint4*>(out_row(b) + h * DH + c0) = w;
+            }
+          }
+          if (qok && h == 1) p.LSE[(long long)b * p.HQ + q] = (M + __log2f(L)) * 0.6931471805599453f;
+          if (threadIdx.x == 64) *cn = 0u;  // re-armed for the next launch
+        }
+      }
+      ++t;
+    });
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tmem, 512);
+}
+
+size_t fwd512b_smem() { return fwd512_smem() + 16; }
+
 // Backward (d = 512), persistent CTAs over (sample, 128-row S block) items,
 // looping over the query tiles; the S block stays resident (8 atoms) and the
 // query-tile operands stream through a 3-slot ring of (Qt atom, dO atom):
@@ -1140,13 +1500,13 @@ size_t fwd_smem() {
 
 // 3-D bf16 tensor map (inner, rows, batch), 64 x 128 boxes, SWIZZLE_128B.
 bool map3(CUtensorMap* m, const void* ptr, long long inner, long long rows, long long rs, long long nb,
-          long long bs) {
+          long long bs, int box_rows = TB) {
   auto fn = tc_encode_fn();
   if (!fn) return false;
   if ((rs * 2) % 16 || (bs * 2) % 16 || ((uintptr_t)ptr & 15)) return false;
   cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)rows, (cuuint64_t)nb};
   cuuint64_t strides[2] = {(cuuint64_t)(rs * 2), (cuuint64_t)std::max<long long>(bs * 2, rs * 2 * rows)};
-  cuuint32_t box[3] = {64, (cuuint32_t)TB, 1};
+  cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -1157,6 +1517,21 @@ bool map3(CUtensorMap* m, const void* ptr, long long inner, long long rows, long
 }  // namespace kl
 
 using namespace kl;
+
+static long long hsp_cnt_bytes(int lanes, int qg) { return ((long long)lanes * qg * 4 + 255) / 256 * 256; }
+static long long hsp_split_ws_bytes(int lanes, int cpl, int qg) {
+  return hsp_cnt_bytes(lanes, qg) + (long long)lanes * cpl * 2 * hsp::PARTF * 4;
+}
+
+extern "C" long long kl_hsp_fwd_workspace_bytes(const kl_hsp_args* a) {
+  if (!a || a->d != 512 || a->B < 1 || a->HQ < 1) return 0;
+  const int qg = a->q_group > 0 ? a->q_group : a->B;
+  if (a->B % qg) return 0;
+  const int lanes = (a->B / qg) * ((a->HQ + hsp::TB - 1) / hsp::TB) * 2;
+  int cpl = std::max(1, tc_num_sms() / lanes);
+  if (const char* c = getenv("KL_HSP_CPL")) cpl = std::max(1, atoi(c));
+  return hsp_split_ws_bytes(lanes, cpl, qg);
+}
 
 extern "C" int kl_hsp_fwd(const kl_hsp_args* a, void* stream) {
   if (!a || a->B < 0 || a->T < 0 || a->HQ < 1 || a->d < 1 || a->n1 < 0 || a->n1 > a->HQ) {
@@ -1196,6 +1571,40 @@ extern "C" int kl_hsp_fwd(const kl_hsp_args* a, void* stream) {
     return KL_EUNSUPPORTED;
   }
   cudaStream_t s = (cudaStream_t)stream;
+  if (a->d == 512 && a->workspace) {  // balanced form: each lane's key blocks split evenly over the SMs
+    hsp::SplitP q{};
+    q.B = p.B;
+    q.T = p.T;
+    q.HQ = p.HQ;
+    q.n1 = p.n1;
+    q.qtiles = p.qtiles;
+    q.qg = qg;
+    q.lanes = (p.B / qg) * p.qtiles * 2;
+    q.cpl = std::max(1, tc_num_sms() / q.lanes);
+    if (const char* c = getenv("KL_HSP_CPL")) q.cpl = std::max(1, atoi(c));  // testing
+    const long long need = hsp_split_ws_bytes(q.lanes, q.cpl, qg);
+    if (a->workspace_bytes < need) {
+      set_error("kl_hsp_fwd: workspace of %lld bytes, %lld needed (kl_hsp_fwd_workspace_bytes)", a->workspace_bytes,
+                need);
+      return KL_EBADSHAPE;
+    }
+    q.lengths = p.lengths;
+    q.O1 = p.O1;
+    q.o1_bs = p.o1_bs;
+    q.O2 = p.O2;
+    q.o2_bs = p.o2_bs;
+    q.LSE = p.LSE;
+    q.cnt = (unsigned*)a->workspace;
+    q.ws = (float*)((char*)a->workspace + hsp_cnt_bytes(q.lanes, qg));
+    cudaMemsetAsync(q.cnt, 0, (size_t)q.lanes * qg * sizeof(unsigned), s);
+    const size_t smem = hsp::fwd512b_smem();
+    cudaFuncSetAttribute(hsp::hsp_fwd512b_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    launch_k(hsp::hsp_fwd512b_kernel, q.lanes * q.cpl, hsp::NT, smem, s, tS, tQ, q);
+    count_launch();
+    count_path(KL_PATH_HSP_FWD_TC);
+    count_path(KL_PATH_HSP_FWD_SPLIT);
+    return launch_check("hsp_fwd");
+  }
   const int items = p.B * p.qtiles * (a->d == 512 ? 2 : 1);
   int grid = std::min(items, tc_num_sms());
   if (const char* g = getenv("KL_HSP_GRID")) grid = std::max(1, std::min(grid, atoi(g)));  // testing

@@ -646,7 +646,13 @@ class _HspPool(torch.autograd.Function):
             outs = [torch.empty(B, n, d, device=S.device, dtype=S.dtype) for n in splits]
             LSE = torch.empty(B, HQ, device=S.device, dtype=torch.float32)
             a = _hsp_args(S, Q, lengths, splits[0], outs[0], outs[-1], LSE)
+            ws = None
+            if d == 512 and HSP_BALANCED:  # key blocks split over the SMs: per-part partials + arrival counters
+                nb = int(_capi.lib().kl_hsp_fwd_workspace_bytes(C.byref(a)))
+                ws = torch.empty(nb, device=S.device, dtype=torch.uint8)
+                a.workspace, a.workspace_bytes = ws.data_ptr(), nb
             _capi.call("kl_hsp_fwd", C.byref(a), _stream())
+            del ws
             ctx.save_for_backward(S, Q, lengths, LSE, *outs)
             return tuple(outs) + ((rec,) if rec is not None else ())
         sc = gemm(S.view(G, B // G, T, d), Q.view(G, 1, HQ, d).transpose(2, 3), out_dtype=torch.float32)
@@ -730,6 +736,7 @@ def _hsp_gemm_bwd(ctx, gs):
 
 
 HSP_FUSED = True  # tests flip this to A/B the fused tcgen05 pooling against the GEMM composition
+HSP_BALANCED = True  # d = 512 forward: the balanced (split key range) kernel; False = one CTA per item
 
 
 def _hsp_fused_ok(S, HQ, n_splits) -> bool:

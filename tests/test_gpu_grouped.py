@@ -123,10 +123,15 @@ def test_grouped_fp32_vs_oracle():
 
 
 @pytest.mark.parametrize("d", [256, 512])
-def test_hsp_q_group_equals_separate_launches(d):
+def test_hsp_q_group_equals_separate_launches(d, monkeypatch):
     """kl_hsp_fwd / kl_hsp_bwd with q_group (one query set per group of
-    samples) == one launch per group with its own set (bf16, fused kernels)."""
+    samples) == one launch per group with its own set (bf16, fused kernels).
+    d = 512: one CTA per (group, query tile, half) lane (KL_HSP_CPL=1), so
+    both launches pool every sample whole and agree bitwise (the balanced
+    split is checked against the composition in test_gpu_parity)."""
     from paper_2602_10016_b200 import functional as F
+
+    monkeypatch.setenv("KL_HSP_CPL", "1")
 
     torch.manual_seed(0)
     G, Bg, T, HQ = 3, 4, 300, 40

@@ -690,14 +690,22 @@ def test_gdpa512_fused_vs_gemm_composition(grid, monkeypatch):
     assert torch.equal(outs[0][1][2], G[2].float())
 
 
-@pytest.mark.parametrize("grid", [None, "5"])
-def test_hsp512_fused_vs_composition(grid, monkeypatch):
+@pytest.mark.parametrize("env", [None, ("KL_HSP_GRID", "5"), ("KL_HSP_CPL", "1"), ("KL_HSP_CPL", "3"),
+                                 ("KL_HSP_CPL", "7")])
+def test_hsp512_fused_vs_composition(env, monkeypatch):
     """d = 512 fused pooling vs the GEMM + column-softmax composition, with
-    CTAs walking several items (KL_HSP_GRID) and jagged lengths."""
+    jagged lengths: the balanced forward (key blocks of each (query tile,
+    half) lane split over 1 / 3 / 7 / the default number of CTAs — samples cut
+    between CTAs merge their partials) and the one-CTA-per-item forward with
+    CTAs walking several items (KL_HSP_GRID)."""
+    from paper_2602_10016_b200 import _capi
     from paper_2602_10016_b200 import functional as F
 
-    if grid:
-        monkeypatch.setenv("KL_HSP_GRID", grid)
+    if env:
+        monkeypatch.setenv(*env)
+    balanced = not (env and env[0] == "KL_HSP_GRID")
+    monkeypatch.setattr(F, "HSP_BALANCED", balanced)
+    _capi.reset_path_hits()
     torch.manual_seed(6)
     B, T, d, HQ = 5, 900, 512, 320
     S = (torch.randn(B, T, d, device="cuda") * 4 / d ** 0.5).bfloat16().requires_grad_()
@@ -713,6 +721,8 @@ def test_hsp512_fused_vs_composition(grid, monkeypatch):
             g2 = torch.randn_like(o2.float(), generator=torch.Generator(device="cuda").manual_seed(2)).bfloat16()
             torch.autograd.backward([o1, o2], [g1, g2])
             outs.append([o1.detach().float(), o2.detach().float(), S.grad.float(), Q.grad.float()])
+            if fused:
+                assert (_capi.path_hits()["hsp_fwd_split"] > 0) == balanced
         finally:
             F.HSP_FUSED = True
     for name, a, b in zip(("O1", "O2", "dS", "dQ"), outs[0], outs[1]):
