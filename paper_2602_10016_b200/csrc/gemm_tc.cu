@@ -55,6 +55,8 @@ struct TcParams {
   int x_tma;           // MODE 3, aux_mode 1: pre-activation stored by TMA (tmX, C's layout)
   int r_bufs;          // residual tile buffers (2; 1 for 256-wide tiles with a long reduction)
   int n_fast;          // tile order: N tiles of one M block adjacent (A read once from HBM)
+  int wide;            // PAIR: 256 x 512 tiles — two N = 256 products per k step into one 512-column
+                       // accumulator (no double buffer); each CTA stages 2 x 128 B columns
 };
 
 constexpr int SLD = 66;  // epilogue staging row stride (floats): 64 columns + pad, 8-byte aligned
@@ -659,7 +661,18 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 tc::tma_load_4d_pair(da, &tmA, fb, mb * BM, kb * BK, a2, a1);
                 tc::tma_load_4d_pair(da + 8192, &tmA, fb, mb * BM + 64, kb * BK, a2, a1);
               }
-              if (!p.b_mn) {
+              if (p.wide) {  // columns [256 h + 128 rank, +128) of each 256-column product h
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                  const int nh = nb * p.BN + h * 256 + (int)rank * 128;
+                  if (!p.b_mn) {
+                    tc::tma_load_4d_pair(db + h * 16384, &tmB, fb, kb * BK, nh, b2, b1);
+                  } else {
+                    tc::tma_load_4d_pair(db + h * 16384, &tmB, fb, nh, kb * BK, b2, b1);
+                    tc::tma_load_4d_pair(db + h * 16384 + 8192, &tmB, fb, nh + 64, kb * BK, b2, b1);
+                  }
+                }
+              } else if (!p.b_mn) {
                 tc::tma_load_4d_pair(db, &tmB, fb, kb * BK, n0, b2, b1);
               } else {
                 for (int j = 0; j < p.b_boxes; ++j)
@@ -691,15 +704,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {  // (pair: the leader issues for both CTAs)
-      const uint32_t idesc = tc::idesc_bf16(PAIR ? 2 * BM : BM, p.BN, p.a_mn, p.b_mn);
+      const uint32_t idesc = tc::idesc_bf16(PAIR ? 2 * BM : BM, p.wide ? 256 : p.BN, p.a_mn, p.b_mn);
       int stage = 0;
       uint32_t phase = 0;
       int t = 0;
       for (int unit = unit0; unit < total; unit += ustep, ++t) {
         const int sp = unit % p.splits;
         const int it0 = (int)((long long)iters * sp / p.splits), it1 = (int)((long long)iters * (sp + 1) / p.splits);
-        const int acc = t & 1;
-        const uint32_t acc_phase = (t >> 1) & 1;
+        const int acc = p.wide ? 0 : t & 1;
+        const uint32_t acc_phase = p.wide ? t & 1 : (t >> 1) & 1;
         tc::mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc::fence_after();
         const uint32_t d = tmem + acc * p.acc_stride;
@@ -712,9 +725,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           for (int k = 0; k < BK / 16; ++k) {
             const uint64_t ad = p.a_mn ? tc::sdesc(a0 + k * 2048, 8192, 1024) : tc::sdesc(a0 + k * 32, 16, 1024);
             const uint64_t bd = p.b_mn ? tc::sdesc(b0 + k * 2048, 8192, 1024) : tc::sdesc(b0 + k * 32, 16, 1024);
-            if constexpr (PAIR)
+            if constexpr (PAIR) {
               tc::mma_bf16_pair(d, ad, bd, idesc, (it > it0 || k > 0) ? 1u : 0u);
-            else
+              if (p.wide)
+                tc::mma_bf16_pair(d + 256, ad, bd + (16384 >> 4), idesc, (it > it0 || k > 0) ? 1u : 0u);
+            } else
               tc::mma_bf16(d, ad, bd, idesc, (it > it0 || k > 0) ? 1u : 0u);
           }
           if constexpr (PAIR)
@@ -737,8 +752,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     int t = 0, nbox = 0;
     for (int unit = unit0; unit < total; unit += ustep, ++t) {
       const int tile = unit / p.splits;
-      const int acc = t & 1;
-      const uint32_t acc_phase = (t >> 1) & 1;
+      const int acc = p.wide ? 0 : t & 1;
+      const uint32_t acc_phase = p.wide ? t & 1 : (t >> 1) & 1;
       const int mbt = p.n_fast ? (tile / p.tiles_n) % p.tiles_m : tile % p.tiles_m;
       const int mb = PAIR ? 2 * mbt + (int)rank : mbt;
       const int nb = p.n_fast ? tile % p.tiles_n : (tile / p.tiles_m) % p.tiles_n;
@@ -1139,10 +1154,26 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
     const long long tiles2 = (long long)((g.M + 2 * BM - 1) / (2 * BM)) * p.tiles_n * p.n_out;
     if (plan_splits(tiles2, &wsp) > 1 && wsp) pair = false;
   }
+  // Wide CTA pairs for the weight-gradient shapes (fp32 accumulate-only, a
+  // long reduction split over the SMs, N a multiple of 512): 256 x 512 tiles
+  // stage 48 KB of operands per 2 x 128 x 256 x 64 MACs per CTA (47 B/clk at
+  // the MMA rate) where single-CTA 128 x 256 tiles need 94 B/clk — above the
+  // ~60 B/clk/SM the TMA delivers with every SM loading (measured,
+  // scripts/r2/micro/tma_lat.cu).  One 512-column accumulator: the epilogue
+  // (once per long split) is not overlapped.
+  const bool wide = mode2 && accum_only0 && !use_r && !pair && g.N % 512 == 0 && (g.M + BM - 1) / BM >= 2 &&
+                    k_tot >= 8192 && !getenv_flag_nopair() && !getenv("KL_GEMM_NOWIDE");
+  if (wide) {
+    pair = true;
+    bn = 512;
+    p.BN = 512;
+    p.tiles_n = g.N / 512;
+  }
+  p.wide = wide ? 1 : 0;
   if (pair) {
     p.tiles_m = (g.M + 2 * BM - 1) / (2 * BM);
-    p.b_boxes = b_n ? (bn / 2 + 63) / 64 : 1;
-    p.b_stage_bytes = b_n ? p.b_boxes * 64 * BK * 2 : (bn / 2) * BK * 2;
+    p.b_boxes = wide ? 4 : (b_n ? (bn / 2 + 63) / 64 : 1);
+    p.b_stage_bytes = wide ? 2 * 128 * BK * 2 : (b_n ? p.b_boxes * 64 * BK * 2 : (bn / 2) * BK * 2);
   }
   const uint32_t stage_p = p.a_stage_bytes + p.b_stage_bytes;
   p.r_boxes = use_r ? (bn + 63) / 64 : 0;
@@ -1153,6 +1184,10 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
   if (p.stages < 2) return KL_EUNSUPPORTED;
   p.acc_stride = bn > 128 ? 256 : (bn > 64 ? 128 : (bn > 32 ? 64 : 32));
   p.tmem_cols = 2 * p.acc_stride;
+  if (wide) {
+    p.acc_stride = 0;
+    p.tmem_cols = 512;
+  }
   if (p.tmem_cols < 32) p.tmem_cols = 32;
 
   CUtensorMap ta, tb;
@@ -1164,8 +1199,8 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
       return KL_EUNSUPPORTED;
   }
   if (b_k) {
-    if (!make_map(&tb, g.B, g.K, g.N, g.b_cs, g.nb2, g.b_s2, g.nb1, g.b_s1, BK, pair ? bn / 2 : bn, &p.b_has2,
-                  &p.b_has1))
+    if (!make_map(&tb, g.B, g.K, g.N, g.b_cs, g.nb2, g.b_s2, g.nb1, g.b_s1, BK, wide ? 128 : (pair ? bn / 2 : bn),
+                  &p.b_has2, &p.b_has1))
       return KL_EUNSUPPORTED;
   } else {
     if (!make_map(&tb, g.B, g.N, g.K, g.b_rs, g.nb2, g.b_s2, g.nb1, g.b_s1, 64, BK, &p.b_has2, &p.b_has1))
@@ -1198,6 +1233,8 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
     bool wsp = false;
     p.splits = plan_splits(tiles, &wsp);
     if (wsp) p.ws = g.ws;
+    if (wide)  // units are CTA pairs: one wave of num_sms / 2 pairs
+      p.splits = std::max(1, std::min(num_sms() / 2 / std::max(tiles, 1), iters / 4));
   }
   const int total = tiles * p.splits;
   const int grid = pair ? 2 * std::min(total, num_sms() / 2) : std::min(total, num_sms());
@@ -1208,10 +1245,10 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
     if (trace < 0) trace = getenv("KL_GEMM_TRACE") ? 1 : 0;
     if (trace)
       fprintf(stderr, "gemm_tc M=%d N=%d K=%d nb=%dx%d red=%d%d c=%s beta=%g bias=%d aux=%d act=%d/%d R=%d lim=%d "
-              "mode2=%d bn=%d splits=%d ws=%d pair=%d stages=%d\n", g.M, g.N, g.K, g.nb1, g.nb2, g.red1, g.red2,
+              "mode2=%d bn=%d splits=%d ws=%d pair=%d wide=%d stages=%d\n", g.M, g.N, g.K, g.nb1, g.nb2, g.red1, g.red2,
               g.c_dtype == KL_BF16 ? "bf16" : "f32", e.beta, e.bias != nullptr, e.aux_mode, e.n_act, e.act_group,
               g.R != nullptr, e.row_limit != nullptr, (int)mode2, bn, p.splits, p.ws != nullptr, (int)(pair && !p.ws),
-              p.stages);
+              p.wide, p.stages);
   }
   auto launch = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
