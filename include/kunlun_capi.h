@@ -83,7 +83,8 @@ int kl_last_gemm_path(void);
 #define KL_PATH_COLSOFTMAX 10   /* column softmax of the pooling composition   */
 #define KL_PATH_GDPA_FWD_TC512 11 /* fused GDPA forward, d = 512 variant       */
 #define KL_PATH_GDPA_BWD_TC512 12 /* fused GDPA backward, d = 512 variant      */
-#define KL_PATH_HSP_FWD_SPLIT 13 /* HSP forward d = 512, split form          */
+#define KL_PATH_HSP_FWD_SPLIT 13 /* HSP forward d = 512, balanced form       */
+#define KL_PATH_GEMM_WIDE 14    /* tcgen05 GEMM, wide CTA pairs (256 x 512)  */
 #define KL_PATH_COUNT 16
 unsigned long long kl_path_hits(int path);
 void kl_reset_path_hits(void);

@@ -523,7 +523,7 @@ def launch_count() -> int:
 # Kernel-path counters (include/kunlun_capi.h KL_PATH_*).
 PATHS = {"gemm_tc": 0, "gemm_simt": 1, "gdpa_fwd_tc": 2, "gdpa_bwd_tc": 3, "hsp_fwd_tc": 4, "hsp_bwd_tc": 5,
          "swa_fwd_tc": 6, "swa_bwd_tc": 7, "swa_fwd_simt": 8, "swa_bwd_simt": 9, "colsoftmax": 10,
-         "gdpa_fwd_tc512": 11, "gdpa_bwd_tc512": 12, "hsp_fwd_split": 13}
+         "gdpa_fwd_tc512": 11, "gdpa_bwd_tc512": 12, "hsp_fwd_split": 13, "gemm_wide": 14}
 
 
 def path_hits() -> dict:

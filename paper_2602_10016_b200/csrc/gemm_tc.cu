@@ -767,7 +767,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const int lim = e.row_limit ? e.row_limit[zo] : 0x7fffffff;
       const int m0 = mb * BM + lane_base;
       float* stg = stage_s + (warp - 2) * (32 * SLD);
-      float* bsm = reinterpret_cast<float*>(rempty + 2 + 2) + (warp - 2) * 256;
+      float* bsm = reinterpret_cast<float*>(rempty + 2 + 2) + (warp - 2) * 512;
       if (MODE == 3 && e.bias) {
         // this tile's bias -> the warp's smem row, while the tile's MMAs run
         // (read back as broadcasts by epi_tma)
@@ -1161,8 +1161,15 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
   // ~60 B/clk/SM the TMA delivers with every SM loading (measured,
   // scripts/r2/micro/tma_lat.cu).  One 512-column accumulator: the epilogue
   // (once per long split) is not overlapped.
-  const bool wide = mode2 && accum_only0 && !use_r && !pair && g.N % 512 == 0 && (g.M + BM - 1) / BM >= 2 &&
-                    k_tot >= 8192 && !getenv_flag_nopair() && !getenv("KL_GEMM_NOWIDE");
+  // Stored outputs (bf16 / plain fp32) take wide pairs only for long
+  // reductions: the un-overlapped 512-column epilogue costs a K = 512 tile
+  // more than the operand bytes save (measured: QKV projection, K = 512,
+  // 199 -> 219 us; QKV dX, K = 1536, 188 -> 166 us; 8192^3 936 -> 702 us).
+  const bool wide = mode2 && !use_r && g.N % 512 == 0 && (g.M + BM - 1) / BM >= 2 && !getenv_flag_nopair() &&
+                    !getenv("KL_GEMM_NOWIDE") &&
+                    ((accum_only0 && !pair && k_tot >= 8192) ||
+                     (!accum_only0 && k_tot >= 1536 &&
+                      (long long)((g.M + 2 * BM - 1) / (2 * BM)) * (g.N / 512) * n_out0 >= num_sms() / 2));
   if (wide) {
     pair = true;
     bn = 512;
@@ -1225,7 +1232,7 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
     p.vec_r = g.R && g.r_cs == 1 && g.r_rs % 2 == 0 && (g.r_s1 % 2 == 0) && (g.r_s2 % 2 == 0) && al(g.R);
   }
 
-  const size_t smem = 1024 + (size_t)p.stages * stage_p + rbytes + (2 * p.stages + 8) * 8 + 16 + 4 * 256 * 4;
+  const size_t smem = 1024 + (size_t)p.stages * stage_p + rbytes + (2 * p.stages + 8) * 8 + 16 + 4 * 512 * 4;
   const int tiles = p.tiles_m * p.tiles_n * p.n_out;
   const int iters = ((g.red1 ? g.nb1 : 1) * (g.red2 ? g.nb2 : 1)) * p.kblocks;
   p.ws = nullptr;
@@ -1233,8 +1240,10 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
     bool wsp = false;
     p.splits = plan_splits(tiles, &wsp);
     if (wsp) p.ws = g.ws;
-    if (wide)  // units are CTA pairs: one wave of num_sms / 2 pairs
-      p.splits = std::max(1, std::min(num_sms() / 2 / std::max(tiles, 1), iters / 4));
+    if (wide) {  // units are CTA pairs: one wave of num_sms / 2 pairs; stored outputs are not split
+      p.ws = nullptr;
+      p.splits = accum_only0 ? std::max(1, std::min(num_sms() / 2 / std::max(tiles, 1), iters / 4)) : 1;
+    }
   }
   const int total = tiles * p.splits;
   const int grid = pair ? 2 * std::min(total, num_sms() / 2) : std::min(total, num_sms());
@@ -1293,6 +1302,7 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
   }
   count_launch();
   count_path(KL_PATH_GEMM_TC);
+  if (wide) count_path(KL_PATH_GEMM_WIDE);
   int rc = launch_check("gemm_tc");
   if (rc || !p.ws) return rc;
   return splitk_reduce(g, e, p.ws, p.splits, p.n_out, s);

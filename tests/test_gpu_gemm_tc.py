@@ -235,3 +235,42 @@ def test_gemm_partial_n_tiles_many_m_tiles(N, out_dtype):
         assert torch.isfinite(c).all()
         err = ((c.double() - ref).abs().max() / ref.abs().max()).item()
         assert err < 1e-2, err
+
+
+@pytest.mark.parametrize("a_k,b_n", [(True, False), (False, True), (True, True)])
+def test_tc_wide_pairs(a_k, b_n):
+    """Wide CTA pairs (256 x 512 tiles, two N = 256 products per k step into
+    one 512-column accumulator): a long-K bf16 GEMM with bias + 16-column
+    activation groups + aux pre-activation + row limit, batched, M and N
+    tails of the pair tile; and the fp32 accumulate weight-gradient form
+    (batch-reduced, split over the SMs)."""
+    from paper_2602_10016_b200 import _capi
+    from paper_2602_10016_b200._capi import gemm
+
+    g = torch.Generator(device="cuda").manual_seed(11)
+    M, N, K = 9000, 1024, 1600  # 2 x 18 x 2 = 72 pair tiles (>= one wave of pairs), M tail of 40 rows
+    A = operand((2, M, K), a_k, g) * 0.05
+    B = operand((K, N), not b_n, g) * 0.05
+    bias = torch.randn(N, device="cuda", generator=g)
+    lim = torch.tensor([M, 4321], device="cuda", dtype=torch.int32)
+    out = torch.empty(2, M, N, device="cuda", dtype=torch.bfloat16)
+    pre = torch.empty(2, M, N, device="cuda", dtype=torch.bfloat16)
+    _capi.reset_path_hits()
+    gemm(A, B, out, bias=bias, acts=["silu", "relu"], act_group=16, aux=pre, aux_mode=1, row_limit=lim)
+    assert _capi.path_hits()["gemm_wide"] == 1
+    z = A.double() @ B.double() + bias.double()
+    keep = torch.arange(M, device="cuda")[None, :, None] < lim.view(2, 1, 1)
+    cols = torch.arange(N, device="cuda") // 16 % 2
+    act = torch.where(cols == 0, torch.nn.functional.silu(z), torch.relu(z))
+    assert rel(pre, torch.where(keep, z, 0)) < 1e-2
+    assert rel(out, torch.where(keep, act, 0)) < 1e-2
+    # weight-gradient form: C (fp32) += sum_b A_b^T D_b
+    D = operand((6, 4096, 512), True, g)
+    X = operand((6, 4096, 1536), a_k, g)
+    C0 = torch.randn(1536, 512, device="cuda", generator=g)
+    C = C0.clone()
+    _capi.reset_path_hits()
+    gemm(X.transpose(1, 2), D, C, beta=1.0, reduce=(False, True))
+    assert _capi.path_hits()["gemm_wide"] == 1
+    ref = C0.double() + (X.double().transpose(1, 2) @ D.double()).sum(0)
+    assert rel(C, ref) < 1e-5
