@@ -653,7 +653,7 @@ __global__ void __launch_bounds__(NT, 1)
 //         -> bf16 rows.
 constexpr int HK2 = 128;
 constexpr int NT5 = 320;                       // warp 0 TMA, 1 MMA, 2-9 epilogue
-constexpr int RST = 4;                         // forward ring stages
+constexpr int RST = 3;                         // forward ring stages (+ 16 KB epilogue staging)
 constexpr uint32_t FSTAGE = 2 * ATOM_S;        // S atom | Kt atom (128 rows x 64)
 constexpr uint32_t BSTAGE = 4 * ATOM_S;        // dY | Vt | S | Kt atoms
 
@@ -668,7 +668,12 @@ struct P5 {
   unsigned char code[HK2];
   bf16* dZ;             // bwd: (B, T, HK2)
   bf16* A;
+  unsigned long long* trace;  // debug: per-tile clock64 stamps of CTA 0 ([tile < 32][event < 16]), or NULL
 };
+#define T5(c, slot)                                                                          \
+  do {                                                                                       \
+    if (p.trace && blockIdx.x == 0 && (c) < 32) p.trace[(c) * 16 + (slot)] = clock64();      \
+  } while (0)
 
 // Act over this thread's 64 Z columns [c0, c0 + 64): four 16-column head groups.
 template <bool BWD>
@@ -706,6 +711,63 @@ __device__ __forceinline__ void prefetch_res128(const bf16* src, bool ok, uint4*
   for (int c = 0; c < 16; ++c) r[c] = ok ? __ldg(p + c) : make_uint4(0u, 0u, 0u, 0u);
 }
 
+// Coalesced epilogue I/O of one warp's 32 rows x 32 bf16 columns.  With
+// thread = row (the TMEM lane layout) a 16-byte access per thread touches 32
+// different 128-byte lines per warp instruction; going through a 2 KB
+// per-warp staging tile, every warp instruction covers 8 rows x 64 B (4x
+// fewer L1 wavefronts: clock-stamp trace of the d = 512 GDPA forward, one
+// 128 x 256 output half took 6-8 k clk in its row-per-thread stores and
+// residual loads).  Staging row R, 16-byte chunk c lives at R*64 + (c ^ (R>>1 & 3))*16
+// (conflict-free for both the row-per-thread and the lane-per-chunk pattern).
+__device__ __forceinline__ uint32_t stg_off(int R, int c) { return R * 64 + ((c ^ ((R >> 1) & 3)) << 4); }
+
+// lane's 4 coalesced 16-byte residual chunks: rows row0 + (lane >> 2) + 8 i, chunk lane & 3
+__device__ __forceinline__ void res_load_co(const bf16* base, long long rs, int row0, int nvalid, int col0,
+                                            uint4* r4) {
+  const int lane = threadIdx.x & 31, c = lane & 3;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int R = (lane >> 2) + 8 * i;
+    r4[i] = R < nvalid ? __ldg(reinterpret_cast<const uint4*>(base + (long long)(row0 + R) * rs + col0 + 8 * c))
+                       : make_uint4(0u, 0u, 0u, 0u);
+  }
+}
+
+// out[row0 + lane, col0 .. col0 + 32) = acc (this thread's row) + residual
+// (r4: res_load_co chunks), stored coalesced; stg: the warp's 2 KB staging tile.
+__device__ __forceinline__ void res_add_store_co(uint8_t* stg, const uint4* r4, const float* acc, bf16* obase,
+                                                 long long os, int row0, int nvalid, int col0) {
+  const int lane = threadIdx.x & 31, c = lane & 3;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) *reinterpret_cast<uint4*>(stg + stg_off((lane >> 2) + 8 * i, c)) = r4[i];
+  __syncwarp();
+  uint4 o[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint4 u = *reinterpret_cast<const uint4*>(stg + stg_off(lane, q));
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+    uint32_t v[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[i]));
+      v[i] = tc::pack_bf16(acc[8 * q + 2 * i] + f.x, acc[8 * q + 2 * i + 1] + f.y);
+    }
+    o[q] = make_uint4(v[0], v[1], v[2], v[3]);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int q = 0; q < 4; ++q) *reinterpret_cast<uint4*>(stg + stg_off(lane, q)) = o[q];
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int R = (lane >> 2) + 8 * i;
+    if (R < nvalid)
+      *reinterpret_cast<uint4*>(obase + (long long)(row0 + R) * os + col0 + 8 * c) =
+          *reinterpret_cast<const uint4*>(stg + stg_off(R, c));
+  }
+  __syncwarp();
+}
+
 __global__ void __launch_bounds__(NT5, 1)
     gdpa_fwd512_kernel(const __grid_constant__ CUtensorMap ts, const __grid_constant__ CUtensorMap tk,
                        const __grid_constant__ CUtensorMap tv, const P5 p) {
@@ -716,7 +778,8 @@ __global__ void __launch_bounds__(NT5, 1)
   uint8_t* sR = align1k(smem_raw);          // RST x (S atom | Kt atom)
   uint8_t* sV = sR + RST * FSTAGE;          // Vt half: 4 atoms
   uint8_t* sA = sV + 4 * ATOM_S;            // 128 x 128 bf16 (2 atoms)
-  uint64_t* bar = (uint64_t*)(sA + 2 * ATOM_S);
+  uint8_t* sStg = sA + 2 * ATOM_S;          // 8 x 2 KB per-warp epilogue staging
+  uint64_t* bar = (uint64_t*)(sStg + 8 * 2048);
   uint64_t* rs_full = bar;                  // [RST]
   uint64_t* rs_empty = bar + RST;           // [RST]
   uint64_t* vs_full = bar + 2 * RST;
@@ -791,9 +854,13 @@ __global__ void __launch_bounds__(NT5, 1)
       };
       if (i0 < i1) load_z(i0);
       for (int k = i0; k < i1; ++k) {
+        T5(k - i0, 0);
         load_v(k, 0);
+        T5(k - i0, 1);
         if (k + 1 < i1) load_z(k + 1);
+        T5(k - i0, 2);
         load_v(k, 1);
+        T5(k - i0, 3);
       }
     }
   } else if (warp == 1) {
@@ -820,11 +887,15 @@ __global__ void __launch_bounds__(NT5, 1)
       };
       if (i0 < i1) mma_z();
       for (int k = i0; k < i1; ++k) {
+        T5(k - i0, 4);
         if (k + 1 < i1) mma_z();  // the next tile's Z runs while this tile's Y drains
+        T5(k - i0, 5);
         tc::mbar_wait(a_full, ac & 1);
+        T5(k - i0, 6);
         for (int h = 0; h < 2; ++h, ++yc, ++vc) {
           tc::mbar_wait(y_empty, (yc & 1) ^ 1);
           tc::mbar_wait(vs_full, vc & 1);
+          T5(k - i0, 7 + h);
           tc::fence_after();
 #pragma unroll
           for (int kk = 0; kk < HK2 / 16; ++kk)
@@ -848,6 +919,7 @@ __global__ void __launch_bounds__(NT5, 1)
       const bool live = q0 + r < len, inb = q0 + r < p.T;
       const int z = zc & 1;
       tc::mbar_wait(&z_full[z], (zc >> 1) & 1);
+      if (threadIdx.x == 64) T5(k - i0, 9);
       tc::fence_after();
       float v[64];
       tc::tmem_ld32(trow + z * HK2 + hf * 64, v);
@@ -869,24 +941,31 @@ __global__ void __launch_bounds__(NT5, 1)
       tc::fence_async_smem();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(a_full);
+      if (threadIdx.x == 64) T5(k - i0, 10);
       ++ac;
-      const bf16* rrow = p.res + (long long)b * p.r_bs + (long long)(q0 + r) * p.r_rs;
-      bf16* orow = p.out + (long long)b * p.o_bs + (long long)(q0 + r) * p.o_rs;
+      const bf16* rbase = p.res + (long long)b * p.r_bs;
+      bf16* obase = p.out + (long long)b * p.o_bs;
+      const int row0 = q0 + qtr * 32, nvalid = min(32, p.T - row0);
+      uint8_t* stg = sStg + (warp - 2) * 2048;
+      (void)inb;
       for (int h = 0; h < 2; ++h, ++yc) {
-        uint4 res[16];
-        prefetch_res128(rrow + h * 256 + hf * 128, inb, res);
+        uint4 res[16];  // the 4 chunks' residual, coalesced, loaded before the accumulator wait
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc)
+          res_load_co(rbase, p.r_rs, row0, nvalid, h * 256 + hf * 128 + 32 * cc, res + 4 * cc);
         tc::mbar_wait(y_full, yc & 1);
+        if (threadIdx.x == 64) T5(k - i0, 11 + 2 * h);
         tc::fence_after();
 #pragma unroll
         for (int cc = 0; cc < 4; ++cc) {
           float acc[32];
           tc::tmem_ld32(trow + T_Y + hf * 128 + 32 * cc, acc);
-          const int col = h * 256 + hf * 128 + 32 * cc;
-          if (inb) add_res_store32(acc, res + 4 * cc, orow + col);
+          res_add_store_co(stg, res + 4 * cc, acc, obase, p.o_rs, row0, nvalid, h * 256 + hf * 128 + 32 * cc);
         }
         tc::fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(y_empty);
+        if (threadIdx.x == 64) T5(k - i0, 12 + 2 * h);
       }
     }
   }
@@ -895,7 +974,7 @@ __global__ void __launch_bounds__(NT5, 1)
   if (warp == 1) tc::tmem_dealloc(tmem, 512);
 }
 
-size_t fwd512_smem() { return 1024 + RST * FSTAGE + 4 * ATOM_S + 2 * ATOM_S + (2 * RST + 10) * 8 + 16; }
+size_t fwd512_smem() { return 1024 + RST * FSTAGE + 4 * ATOM_S + 2 * ATOM_S + 8 * 2048 + (2 * RST + 10) * 8 + 16; }
 
 __global__ void __launch_bounds__(NT5, 1)
     gdpa_bwd512_kernel(const __grid_constant__ CUtensorMap ts, const __grid_constant__ CUtensorMap tg,
@@ -1242,6 +1321,7 @@ static int gdpa_fwd512_launch(const kl_gdpa_args* a, const gdpa::P& p, cudaStrea
     return KL_EUNSUPPORTED;
   }
   gdpa::P5 q = p5_of(a, p);
+  q.trace = (unsigned long long*)a->trace;
   q.out = (bf16*)a->Y;
   q.res = (const bf16*)a->S;
   const size_t smem = gdpa::fwd512_smem();

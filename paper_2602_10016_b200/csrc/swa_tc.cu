@@ -1761,8 +1761,7 @@ __global__ void __launch_bounds__(NT3, 1)
           const int q0c = (tl.lo + jj) * HB + ch * 32;
           const int lb = jj * HB + ch * 32;  // staged band index of column 0
           float s[32], g[32];
-          tc::tmem_ld32(trow + ss * 128 + ch * 32, s);
-          tc::tmem_ld32(trow + ss * 128 + 64 + ch * 32, g);
+          tc::tmem_ld32x2(trow + ss * 128 + ch * 32, s, trow + ss * 128 + 64 + ch * 32, g);
           if (ch == 1) {
             tc::fence_before();
             __syncwarp();
@@ -2081,8 +2080,7 @@ __global__ void __launch_bounds__(NT3, 1)
         for (int ch = 0; ch < 2; ++ch) {
           const int k0c = (tl.lo + jj) * HB + ch * 32;
           float sv[32], g[32];
-          tc::tmem_ld32(trow + ss * 128 + ch * 32, sv);
-          tc::tmem_ld32(trow + ss * 128 + 64 + ch * 32, g);
+          tc::tmem_ld32x2(trow + ss * 128 + ch * 32, sv, trow + ss * 128 + 64 + ch * 32, g);
           if (ch == 1) {
             tc::fence_before();
             __syncwarp();
@@ -2333,8 +2331,7 @@ __global__ void __launch_bounds__(NTF, 2)
         tc::mbar_wait(&s_full[ss], (n / FNS) & 1);
         if (ctid == 0) SWT(6, n);
         tc::fence_after();
-        tc::tmem_ld32(trow + ss * 64, v);
-        tc::tmem_ld32(trow + ss * 64 + 32, v + 32);
+        tc::tmem_ld32x2(trow + ss * 64, v, trow + ss * 64 + 32, v + 32);
         tc::fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&s_empty[ss]);

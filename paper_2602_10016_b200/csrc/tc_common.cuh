@@ -171,6 +171,20 @@ __device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t* r) {
       : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// Two 32-column loads in flight together, one wait (the per-load latency is
+// ~140 clk and a warp's TMEM reads are latency-bound: 28 B/clk per warp,
+// scripts/r2/micro/tmem_bw.cu).
+__device__ __forceinline__ void tmem_ld32x2(uint32_t a0, float* v0, uint32_t a1, float* v1) {
+  uint32_t r0[32], r1[32];
+  tmem_ld32_nowait(a0, r0);
+  tmem_ld32_nowait(a1, r1);
+  tmem_wait_ld();
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    v0[i] = __uint_as_float(r0[i]);
+    v1[i] = __uint_as_float(r1[i]);
+  }
+}
 // Pin n registers of split-phase loads after tmem_wait_ld(): no use of them can
 // be scheduled above the wait.
 template <int N>
