@@ -770,7 +770,8 @@ __device__ __forceinline__ void res_add_store_co(uint8_t* stg, const uint4* r4, 
 
 __global__ void __launch_bounds__(NT5, 1)
     gdpa_fwd512_kernel(const __grid_constant__ CUtensorMap ts, const __grid_constant__ CUtensorMap tk,
-                       const __grid_constant__ CUtensorMap tv, const P5 p) {
+                       const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tr32,
+                       const __grid_constant__ CUtensorMap to32, const P5 p) {
   constexpr uint32_t IDESC_Z = tc::idesc_bf16(TB, HK2, 0, 0);
   constexpr uint32_t IDESC_Y = tc::idesc_bf16(TB, 256, 0, 1);
   constexpr uint32_t T_Y = 256;
@@ -778,8 +779,8 @@ __global__ void __launch_bounds__(NT5, 1)
   uint8_t* sR = align1k(smem_raw);          // RST x (S atom | Kt atom)
   uint8_t* sV = sR + RST * FSTAGE;          // Vt half: 4 atoms
   uint8_t* sA = sV + 4 * ATOM_S;            // 128 x 128 bf16 (2 atoms)
-  uint8_t* sStg = sA + 2 * ATOM_S;          // 8 x 2 KB per-warp epilogue staging
-  uint64_t* bar = (uint64_t*)(sStg + 8 * 2048);
+  uint8_t* sStg = sA + 2 * ATOM_S;          // 8 x 4 KB per-warp epilogue tiles (32 rows x 64 cols, SW128)
+  uint64_t* bar = (uint64_t*)(sStg + 8 * 4096);
   uint64_t* rs_full = bar;                  // [RST]
   uint64_t* rs_empty = bar + RST;           // [RST]
   uint64_t* vs_full = bar + 2 * RST;
@@ -790,7 +791,8 @@ __global__ void __launch_bounds__(NT5, 1)
   uint64_t* a_empty = vs_full + 7;
   uint64_t* y_full = vs_full + 8;
   uint64_t* y_empty = vs_full + 9;
-  uint32_t* tslot = (uint32_t*)(vs_full + 10);
+  uint64_t* rbar = vs_full + 10;            // [8] per-warp residual tile landed
+  uint32_t* tslot = (uint32_t*)(vs_full + 18);
 
   const int nT = (p.T + TB - 1) / TB;
   const int W = p.B * nT;
@@ -818,6 +820,9 @@ __global__ void __launch_bounds__(NT5, 1)
     tc::mbar_init(a_empty, 1);
     tc::mbar_init(y_full, 1);
     tc::mbar_init(y_empty, 8);
+    for (int i = 0; i < 8; ++i) tc::mbar_init(&rbar[i], 1);
+    tc::prefetch_tmap(&tr32);
+    tc::prefetch_tmap(&to32);
     tc::fence_barrier_init();
   }
   if (warp == 1) tc::tmem_alloc(tslot, 512);
@@ -835,6 +840,7 @@ __global__ void __launch_bounds__(NT5, 1)
       int rc = 0, vc = 0;
       auto load_z = [&](int k) {
         const int b = k / nT, q0 = (k % nT) * TB;
+
 #pragma unroll 1
         for (int a = 0; a < 8; ++a, ++rc) {
           const int st = rc % RST;
@@ -865,53 +871,71 @@ __global__ void __launch_bounds__(NT5, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {
+      // Polling issue loop: the Y halves of tile k (latency-critical: the
+      // epilogue waits on them) go out as soon as A(k), the accumulator and
+      // the Vt half are ready, the next tile's Z atoms whenever a ring stage
+      // has landed — neither waits behind the other in program order (the
+      // in-order form issued Y0(k) only after all of Z(k+1)'s operand stream:
+      // clock-stamp trace, ~10 k clk per tile).
       int rc = 0, zc = 0, vc = 0, yc = 0, ac = 0;
+      int zt = i0, za = 0, yt = i0, yh = 0;
+      bool zbuf = false, a_ok = false;
       const uint32_t r0 = tc::smem_u32(sR), va = tc::smem_u32(sV), aa = tc::smem_u32(sA);
-      auto mma_z = [&]() {
-        const int z = zc & 1;
-        tc::mbar_wait(&z_empty[z], ((zc >> 1) & 1) ^ 1);
-        tc::fence_after();
-#pragma unroll 1
-        for (int a = 0; a < 8; ++a, ++rc) {
+      while (yt < i1) {
+        if (yt < zt) {  // Z(yt) is issued: its Y halves
+          if (!a_ok) a_ok = tc::mbar_try(a_full, ac & 1);
+          if (a_ok && tc::mbar_try(y_empty, (yc & 1) ^ 1) && tc::mbar_try(vs_full, vc & 1)) {
+            if (yh == 0) T5(yt - i0, 6);
+            T5(yt - i0, 7 + yh);
+            tc::fence_after();
+#pragma unroll
+            for (int kk = 0; kk < HK2 / 16; ++kk)
+              tc::mma_bf16(tmem + T_Y, dk(aa, kk, ATOM_S), dmn(va, kk, ATOM_S), IDESC_Y, kk > 0 ? 1u : 0u);
+            tc::mma_commit(y_full);
+            tc::mma_commit(vs_empty);
+            ++yc;
+            ++vc;
+            if (++yh == 2) {
+              tc::mma_commit(a_empty);
+              ++ac;
+              a_ok = false;
+              yh = 0;
+              ++yt;
+            }
+          }
+        }
+        if (zt < i1 && zt <= yt + 1) {  // Z at most one tile ahead of Y
+          const int z = zc & 1;
+          if (!zbuf) {
+            zbuf = tc::mbar_try(&z_empty[z], ((zc >> 1) & 1) ^ 1);
+            if (zbuf) T5(zt - i0, 4);
+          }
           const int st = rc % RST;
-          tc::mbar_wait(&rs_full[st], (rc / RST) & 1);
-          tc::fence_after();
-          const uint32_t sa = r0 + st * FSTAGE, ka = sa + ATOM_S;
+          if (zbuf && tc::mbar_try(&rs_full[st], (rc / RST) & 1)) {
+            tc::fence_after();
+            const uint32_t sa = r0 + st * FSTAGE, ka = sa + ATOM_S;
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            tc::mma_bf16(tmem + z * HK2, dk(sa, kk, ATOM_S), dk(ka, kk, ATOM_S), IDESC_Z, (a | kk) > 0 ? 1u : 0u);
-          tc::mma_commit(&rs_empty[st]);
+            for (int kk = 0; kk < 4; ++kk)
+              tc::mma_bf16(tmem + z * HK2, dk(sa, kk, ATOM_S), dk(ka, kk, ATOM_S), IDESC_Z, (za | kk) > 0 ? 1u : 0u);
+            tc::mma_commit(&rs_empty[st]);
+            ++rc;
+            if (++za == 8) {
+              tc::mma_commit(&z_full[z]);
+              T5(zt - i0, 5);
+              ++zc;
+              ++zt;
+              za = 0;
+              zbuf = false;
+            }
+          }
         }
-        tc::mma_commit(&z_full[z]);
-        ++zc;
-      };
-      if (i0 < i1) mma_z();
-      for (int k = i0; k < i1; ++k) {
-        T5(k - i0, 4);
-        if (k + 1 < i1) mma_z();  // the next tile's Z runs while this tile's Y drains
-        T5(k - i0, 5);
-        tc::mbar_wait(a_full, ac & 1);
-        T5(k - i0, 6);
-        for (int h = 0; h < 2; ++h, ++yc, ++vc) {
-          tc::mbar_wait(y_empty, (yc & 1) ^ 1);
-          tc::mbar_wait(vs_full, vc & 1);
-          T5(k - i0, 7 + h);
-          tc::fence_after();
-#pragma unroll
-          for (int kk = 0; kk < HK2 / 16; ++kk)
-            tc::mma_bf16(tmem + T_Y, dk(aa, kk, ATOM_S), dmn(va, kk, ATOM_S), IDESC_Y, kk > 0 ? 1u : 0u);
-          tc::mma_commit(y_full);
-          tc::mma_commit(vs_empty);
-        }
-        tc::mma_commit(a_empty);
-        ++ac;
       }
     }
   } else {
     const int qtr = warp & 3, hf = (warp - 2) >> 2;
     const int r = qtr * 32 + lane;
     const uint32_t trow = tmem + ((uint32_t)(qtr * 32) << 16);
-    int zc = 0, yc = 0, ac = 0;
+    int zc = 0, yc = 0, ac = 0, rph = 0;
     for (int k = i0; k < i1; ++k) {
       const int b = k / nT, q0 = (k % nT) * TB;
       int len = __ldg(&p.lengths[b]);
@@ -943,38 +967,72 @@ __global__ void __launch_bounds__(NT5, 1)
       if (lane == 0) tc::mbar_arrive(a_full);
       if (threadIdx.x == 64) T5(k - i0, 10);
       ++ac;
-      const bf16* rbase = p.res + (long long)b * p.r_bs;
-      bf16* obase = p.out + (long long)b * p.o_bs;
-      const int row0 = q0 + qtr * 32, nvalid = min(32, p.T - row0);
-      uint8_t* stg = sStg + (warp - 2) * 2048;
+      // Y_h + S[:, h] -> Y: per warp two 32-row x 64-column tiles per half, the
+      // residual TMA-loaded into the warp's SW128 staging tile, the sum written
+      // back in place by the row threads and TMA-stored (no per-thread global
+      // accesses: a row-per-thread 16-byte store touches 32 lines per warp
+      // instruction — clock-stamp trace, ~5 k clk per output half)
+      const int row0 = q0 + qtr * 32;
+      uint8_t* stg = sStg + (warp - 2) * 4096;
+      uint64_t* rb = &rbar[warp - 2];
       (void)inb;
+      auto res_issue = [&](int col0) {
+        if (lane == 0) {
+          tc::bulk_wait_read0();  // the previous tile's TMA store has read the staging tile
+          tc::mbar_arrive_expect_tx(rb, 4096);
+          tc::tma_load_3d(stg, &tr32, rb, col0, row0, b);
+        }
+      };
       for (int h = 0; h < 2; ++h, ++yc) {
-        uint4 res[16];  // the 4 chunks' residual, coalesced, loaded before the accumulator wait
-#pragma unroll
-        for (int cc = 0; cc < 4; ++cc)
-          res_load_co(rbase, p.r_rs, row0, nvalid, h * 256 + hf * 128 + 32 * cc, res + 4 * cc);
+        res_issue(h * 256 + hf * 128);  // lands while the Y half's MMAs run
         tc::mbar_wait(y_full, yc & 1);
         if (threadIdx.x == 64) T5(k - i0, 11 + 2 * h);
         tc::fence_after();
+#pragma unroll 1
+        for (int cc = 0; cc < 2; ++cc) {
+          const int col0 = h * 256 + hf * 128 + cc * 64;
+          float acc[64];
+          tc::tmem_ld32x2(trow + T_Y + hf * 128 + 64 * cc, acc, trow + T_Y + hf * 128 + 64 * cc + 32, acc + 32);
+          if (cc == 1) {
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(y_empty);
+            res_issue(col0);
+          }
+          tc::mbar_wait(rb, rph & 1);
+          ++rph;
+          uint8_t* rowp = stg + lane * 128;
 #pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {
-          float acc[32];
-          tc::tmem_ld32(trow + T_Y + hf * 128 + 32 * cc, acc);
-          res_add_store_co(stg, res + 4 * cc, acc, obase, p.o_rs, row0, nvalid, h * 256 + hf * 128 + 32 * cc);
+          for (int q = 0; q < 8; ++q) {
+            uint4* cp = reinterpret_cast<uint4*>(rowp + ((q ^ (lane & 7)) << 4));
+            const uint4 u = *cp;
+            const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+            uint32_t o[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[i]));
+              o[i] = tc::pack_bf16(acc[8 * q + 2 * i] + f.x, acc[8 * q + 2 * i + 1] + f.y);
+            }
+            *cp = make_uint4(o[0], o[1], o[2], o[3]);
+          }
+          tc::fence_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tc::tma_store_3d(&to32, stg, col0, row0, b);
+            tc::bulk_commit();
+          }
         }
-        tc::fence_before();
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(y_empty);
         if (threadIdx.x == 64) T5(k - i0, 12 + 2 * h);
       }
     }
+    if (lane == 0) tc::bulk_wait0();
   }
   tc::fence_before();
   __syncthreads();
   if (warp == 1) tc::tmem_dealloc(tmem, 512);
 }
 
-size_t fwd512_smem() { return 1024 + RST * FSTAGE + 4 * ATOM_S + 2 * ATOM_S + 8 * 2048 + (2 * RST + 10) * 8 + 16; }
+size_t fwd512_smem() { return 1024 + RST * FSTAGE + 4 * ATOM_S + 2 * ATOM_S + 8 * 4096 + (2 * RST + 18) * 8 + 16; }
 
 __global__ void __launch_bounds__(NT5, 1)
     gdpa_bwd512_kernel(const __grid_constant__ CUtensorMap ts, const __grid_constant__ CUtensorMap tg,
@@ -1320,6 +1378,12 @@ static int gdpa_fwd512_launch(const kl_gdpa_args* a, const gdpa::P& p, cudaStrea
     set_error("kl_gdpa_fwd: S / Y rows must be 16-byte aligned");
     return KL_EUNSUPPORTED;
   }
+  CUtensorMap tr32, to32;  // 32-row residual / output tiles of the epilogue
+  if (!gdpa::map3(&tr32, a->S, 512, a->T, a->B, a->s_rs, a->s_bs, 32) ||
+      !gdpa::map3(&to32, a->Y, 512, a->T, a->B, a->s_rs, a->s_bs, 32)) {
+    set_error("kl_gdpa_fwd: tensor map encode failed (alignment?)");
+    return KL_EUNSUPPORTED;
+  }
   gdpa::P5 q = p5_of(a, p);
   q.trace = (unsigned long long*)a->trace;
   q.out = (bf16*)a->Y;
@@ -1329,7 +1393,7 @@ static int gdpa_fwd512_launch(const kl_gdpa_args* a, const gdpa::P& p, cudaStrea
   const int W = a->B * ((a->T + gdpa::TB - 1) / gdpa::TB);
   int grid = std::min(W, tc_num_sms());
   if (const char* g = getenv("KL_GDPA_GRID")) grid = std::max(1, std::min(grid, atoi(g)));  // testing: multi-tile CTAs
-  launch_k(gdpa::gdpa_fwd512_kernel, grid, gdpa::NT5, smem, s, ts, tk, tv, q);
+  launch_k(gdpa::gdpa_fwd512_kernel, grid, gdpa::NT5, smem, s, ts, tk, tv, tr32, to32, q);
   count_launch();
   count_path(KL_PATH_GDPA_FWD_TC512);
   return launch_check("gdpa_fwd512_tc");
