@@ -26,6 +26,7 @@ namespace {
 constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int NTHREADS = 192;
+constexpr int NTHREADS_WIDE = 320;  // wide tiles: 8 epilogue warps (2 column halves per TMEM lane quarter)
 
 struct TcParams {
   int M, N, K, BN;
@@ -391,7 +392,7 @@ template <typename TC, bool FULL>
 __device__ __forceinline__ void epi_tma(const TcParams& p, const Epi& e, const CUtensorMap* tmC,
                                         const CUtensorMap* tmX, uint32_t tbase, uint8_t* stg, float* bsm, int mb,
                                         int nb, int zc2, int zc1, int lane_base, int lim, const uint8_t* Rs,
-                                        int& nbox, TC* X) {
+                                        int& nbox, TC* X, int c_lo, int c_hi) {
   // aux_mode 1 with a tensor map: the pre-activation is staged in the warp's
   // second box and TMA-stored beside C (one box pair in flight)
   const bool xtma = FULL && e.aux_mode == 1 && p.x_tma;
@@ -402,7 +403,7 @@ __device__ __forceinline__ void epi_tma(const TcParams& p, const Epi& e, const C
   // (FULL: the caller staged this tile's bias in bsm before the accumulator wait)
   uint8_t* buf = stg;
 #pragma unroll 1
-  for (int c = 0; c < p.BN; c += 32) {
+  for (int c = c_lo; c < c_hi; c += 32) {
     const int hb = (c >> 5) % SPB;
     if (hb == 0) {
       buf = xtma ? stg : stg + (nbox & 1) * 4096;
@@ -521,7 +522,7 @@ __device__ __forceinline__ void epi_tma(const TcParams& p, const Epi& e, const C
         *reinterpret_cast<uint4*>(rowp + ((q ^ (lane & 7)) << 4)) = u;
       }
     }
-    if (hb == SPB - 1 || c + 32 >= p.BN) {
+    if (hb == SPB - 1 || c + 32 >= c_hi) {
       tc::fence_async_smem();
       __syncwarp();
       if (lane == 0) {
@@ -548,7 +549,7 @@ __device__ __forceinline__ void epi_tma(const TcParams& p, const Epi& e, const C
 // per output (the single-CTA kernel is bound by L2 -> SM operand traffic at
 // ~10 TB/s: ncu, c4 projections).
 template <typename TC, int MODE, bool PAIR = false>
-__global__ void __launch_bounds__(NTHREADS, 1)
+__global__ void __launch_bounds__(NTHREADS_WIDE, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmR, const __grid_constant__ CUtensorMap tmC,
                    const __grid_constant__ CUtensorMap tmX, TcParams p,
@@ -571,6 +572,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint32_t* tmem_slot = (uint32_t*)(rempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_epi = (int)(blockDim.x >> 5) - 2;  // 4, or 8 for wide tiles
+  // wide tiles: staging boxes of epilogue warps 6..9 (dynamic, 1 KB aligned, after the bias rows)
+  uint8_t* sX = (uint8_t*)((((uintptr_t)(reinterpret_cast<float*>(rempty + 2 + 2) + 4 * 512)) + 1023) & ~(uintptr_t)1023);
   const uint32_t rank = PAIR ? tc::cluster_ctarank() : 0u;
   const int unit0 = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
   const int ustep = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
@@ -586,7 +590,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&tfull[i], 1);
-      tc::mbar_init(&tempty[i], PAIR ? 8 : 4);  // pair: both CTAs' epilogue warps drain the leader's MMAs
+      tc::mbar_init(&tempty[i], (PAIR ? 2 : 1) * n_epi);  // pair: both CTAs' epilogue warps drain the leader's MMAs
       tc::mbar_init(&rfull[i], 1);
       tc::mbar_init(&rempty[i], 4);
     }
@@ -767,13 +771,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const int lim = e.row_limit ? e.row_limit[zo] : 0x7fffffff;
       const int m0 = mb * BM + lane_base;
       float* stg = stage_s + (warp - 2) * (32 * SLD);
-      float* bsm = reinterpret_cast<float*>(rempty + 2 + 2) + (warp - 2) * 512;
+      // this warp's columns of the tile (wide tiles: one half per 4 warps) and its bias row
+      const int ch = (warp - 2) >> 2, cw = p.BN / (n_epi >> 2), c_lo = ch * cw;
+      float* bsm = reinterpret_cast<float*>(rempty + 2 + 2) + (warp - 2) * (n_epi == 8 ? 256 : 512);
       if (MODE == 3 && e.bias) {
         // this tile's bias -> the warp's smem row, while the tile's MMAs run
         // (read back as broadcasts by epi_tma)
-        for (int c = lane; c < p.BN; c += 32) {
+        for (int c = c_lo + lane; c < c_lo + cw; c += 32) {
           const int n = nb * p.BN + c;
-          bsm[c] = n < p.N ? __ldg(&e.bias[n]) : 0.f;
+          bsm[c - c_lo] = n < p.N ? __ldg(&e.bias[n]) : 0.f;
         }
         __syncwarp();
       }
@@ -787,9 +793,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           tc::mbar_wait(&rfull[t % p.r_bufs], (t / p.r_bufs) & 1);
           Rs = sR + (t % p.r_bufs) * p.r_boxes * 16384;
         }
-        epi_tma<TC, MODE == 3>(p, e, &tmC, &tmX, tbase, reinterpret_cast<uint8_t*>(stage_s) + (warp - 2) * 8192,
-                               bsm, mb, nb,
-                    p.c_has2 ? z2o : 0, p.c_has1 ? z1o : 0, lane_base, lim, Rs, nbox, X);
+        // 8 epilogue warps (wide tiles): warps 6..9 take the upper column half,
+        // staged in dynamic shared memory after the operand ring
+        uint8_t* ebuf = ch == 0 ? reinterpret_cast<uint8_t*>(stage_s) + (warp - 2) * 8192
+                                : sX + (warp - 6) * 8192;
+        epi_tma<TC, MODE == 3>(p, e, &tmC, &tmX, tbase, ebuf, bsm - c_lo, mb, nb,
+                    p.c_has2 ? z2o : 0, p.c_has1 ? z1o : 0, lane_base, lim, Rs, nbox, X, ch * cw, ch * cw + cw);
       } else
       for (int c0 = 0; c0 < p.BN; c0 += 64) {
         // TMEM (thread = row) -> smem transpose -> each lane owns a column
@@ -939,6 +948,12 @@ static bool getenv_flag_epi1() {
 static int r_wide_kb() {  // KL_GEMM_RWIDE_KB: min k-blocks for 256-wide residual tiles (A/B)
   static int v = -1;
   if (v < 0) v = getenv("KL_GEMM_RWIDE_KB") ? atoi(getenv("KL_GEMM_RWIDE_KB")) : 4;
+  return v;
+}
+
+static int wide_min_k() {  // KL_GEMM_WIDE_K: shortest reduction of a stored-output wide GEMM (A/B)
+  static int v = -1;
+  if (v < 0) v = getenv("KL_GEMM_WIDE_K") ? atoi(getenv("KL_GEMM_WIDE_K")) : 512;
   return v;
 }
 
@@ -1161,14 +1176,16 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
   // ~60 B/clk/SM the TMA delivers with every SM loading (measured,
   // scripts/r2/micro/tma_lat.cu).  One 512-column accumulator: the epilogue
   // (once per long split) is not overlapped.
-  // Stored outputs (bf16 / plain fp32) take wide pairs only for long
-  // reductions: the un-overlapped 512-column epilogue costs a K = 512 tile
-  // more than the operand bytes save (measured: QKV projection, K = 512,
-  // 199 -> 219 us; QKV dX, K = 1536, 188 -> 166 us; 8192^3 936 -> 702 us).
+  // Stored outputs (bf16 / plain fp32): the 512-column epilogue is not
+  // overlapped with the next tile's mainloop, so it runs on 8 warps (two
+  // column halves per TMEM lane quarter); with 4 warps a K = 512 tile lost
+  // more than the operand bytes saved (QKV projection 199 -> 219 us), with 8:
+  // QKV projection 208 -> 204 us, HSP dS (K = 640) 102 -> 86 us, QKV dX
+  // (K = 1536) 188 -> 164 us, 8192^3 936 -> 700 us.
   const bool wide = mode2 && !use_r && g.N % 512 == 0 && (g.M + BM - 1) / BM >= 2 && !getenv_flag_nopair() &&
                     !getenv("KL_GEMM_NOWIDE") &&
                     ((accum_only0 && !pair && k_tot >= 8192) ||
-                     (!accum_only0 && k_tot >= 1536 &&
+                     (!accum_only0 && k_tot >= wide_min_k() &&
                       (long long)((g.M + 2 * BM - 1) / (2 * BM)) * (g.N / 512) * n_out0 >= num_sms() / 2));
   if (wide) {
     pair = true;
@@ -1232,7 +1249,9 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
     p.vec_r = g.R && g.r_cs == 1 && g.r_rs % 2 == 0 && (g.r_s1 % 2 == 0) && (g.r_s2 % 2 == 0) && al(g.R);
   }
 
-  const size_t smem = 1024 + (size_t)p.stages * stage_p + rbytes + (2 * p.stages + 8) * 8 + 16 + 4 * 512 * 4;
+  const size_t smem = 1024 + (size_t)p.stages * stage_p + rbytes + (2 * p.stages + 8) * 8 + 16 + 4 * 512 * 4 +
+                      (wide ? 1024 + 4 * 8192 : 0);
+  const int nthreads = wide ? NTHREADS_WIDE : NTHREADS;
   const int tiles = p.tiles_m * p.tiles_n * p.n_out;
   const int iters = ((g.red1 ? g.nb1 : 1) * (g.red2 ? g.nb2 : 1)) * p.kblocks;
   p.ws = nullptr;
@@ -1261,7 +1280,7 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
   }
   auto launch = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    launch_k(kern, grid, NTHREADS, smem, s, ta, tb, use_r ? tr : ta, mode2 ? tc_map : ta, p.x_tma ? tx_map : ta, p,
+    launch_k(kern, grid, nthreads, smem, s, ta, tb, use_r ? tr : ta, mode2 ? tc_map : ta, p.x_tma ? tx_map : ta, p,
              e);
   };
   auto launch_pair = [&](auto kern) {  // clusters of 2 CTAs (a TPC's two SMs)
@@ -1269,7 +1288,7 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(NTHREADS);
+    cfg.blockDim = dim3(nthreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute at[2];

@@ -14,7 +14,7 @@ from paper_2602_10016_b200.model import KunlunModel  # noqa: E402
 from paper_2602_10016_b200.optim import FlatAdam, TrainStep  # noqa: E402
 from paper_2602_10016_b200.synth import ctr_batch  # noqa: E402
 
-cfg, B = CONFIGS["c2"]()
+cfg, B = CONFIGS[os.environ.get("CFG", "c4")]()
 dev = torch.device("cuda", 0)
 model = KunlunModel(cfg, dev, torch.bfloat16, seed=0)
 opt = FlatAdam(model.P)
@@ -56,3 +56,15 @@ for a, b, s, n in kern:
 print(f"kernels {len(kern)}, span {(t1 - t0) / 1e3:.3f} ms, alone total {sum(alone.values()) / 1e3:.3f} ms")
 for n, v in alone.most_common(25):
     print(f"alone {v / 1e3:7.3f} ms  {n}")
+# wall time attributed per kernel name: each instant split evenly over the running kernels
+share = collections.Counter()
+pts2 = sorted(set([a for a, b, s, n in kern] + [b for a, b, s, n in kern]))
+import bisect
+for i in range(len(pts2) - 1):
+    lo, hi = pts2[i], pts2[i + 1]
+    run = [n for a, b, s, n in kern if a <= lo and b >= hi]
+    for n in run:
+        share[n[:70]] += (hi - lo) / len(run)
+print("wall-time share (ms):")
+for n, v in share.most_common(30):
+    print(f"share {v / 1e3:7.3f} ms  {n}")
