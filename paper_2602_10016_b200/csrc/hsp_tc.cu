@@ -81,6 +81,10 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+// 32 x 32 bf16 staging tile: row R, 16-byte chunk c at R*64 + (c ^ (R>>1 & 3))*16 (conflict-free
+// for row-per-thread writes and 8-rows-per-instruction reads)
+__device__ __forceinline__ uint32_t stg_off(int R, int c) { return R * 64 + ((c ^ ((R >> 1) & 3)) << 4); }
+
 __device__ __forceinline__ int nblocks(const int* lengths, int b) {
   const int len = lengths[b];
   return len > 0 ? (len + TB - 1) / TB : 0;
@@ -1301,8 +1305,9 @@ size_t fwd512b_smem() { return fwd512_smem() + 16; }
 //         to dZ_lo (B, HQ, T).
 // The T-length products that need the whole pooled width — dS = P^T dO +
 // dZ^T Qt and dQ = sum_b dZ S — run as tcgen05 GEMMs on PZ (host).
-constexpr int GST = 3;
+constexpr int GST = 2;
 constexpr uint32_t GSTAGE = 2 * ATOM;  // Qt atom + dO atom
+constexpr uint32_t BSTG = 3 * 2048;    // per softmax warp: P | dZ | dZ_lo 32 x 32 bf16 staging tiles
 
 __global__ void __launch_bounds__(NT, 1)
     hsp_bwd512_kernel(const __grid_constant__ CUtensorMap tmS, const __grid_constant__ CUtensorMap tmQ,
@@ -1313,7 +1318,8 @@ __global__ void __launch_bounds__(NT, 1)
   uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sS = sm;                    // 8 atoms: the S block
   uint8_t* sG = sS + NA * ATOM;        // GST x (Qt atom | dO atom)
-  uint64_t* bar = (uint64_t*)(sG + GST * GSTAGE);
+  uint8_t* sT = sG + GST * GSTAGE;     // 4 x BSTG output staging
+  uint64_t* bar = (uint64_t*)(sT + 4 * BSTG);
   uint64_t* s_full = bar;
   uint64_t* s_empty = bar + 1;
   uint64_t* gs_full = bar + 2;         // [GST]
@@ -1454,15 +1460,37 @@ __global__ void __launch_bounds__(NT, 1)
             const float2 hf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&pk[i >> 1]));
             lo[i >> 1] = tc::pack_bf16(z2[0] - hf.x, z2[1] - hf.y);
           }
-          if (qv && c0 < cols) {
-            if (vec && c0 + 32 <= cols) {
+          if (vec && c0 + 32 <= cols) {
+            // coalesced: the warp's 32 rows x 32 columns of P / dZ / dZ_lo go
+            // through staging tiles so each store instruction covers 8 rows x
+            // 64 B (row-per-thread 16-byte stores touch 32 lines per instruction)
+            uint8_t* st0 = sT + (warp - 2) * BSTG;
 #pragma unroll
-              for (int c = 0; c < 4; ++c) {
-                *reinterpret_cast<uint4*>(pr + c0 + 8 * c) = make_uint4(pp[4 * c], pp[4 * c + 1], pp[4 * c + 2], pp[4 * c + 3]);
-                *reinterpret_cast<uint4*>(zr + c0 + 8 * c) = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
-                *reinterpret_cast<uint4*>(lr + c0 + 8 * c) = make_uint4(lo[4 * c], lo[4 * c + 1], lo[4 * c + 2], lo[4 * c + 3]);
+            for (int c = 0; c < 4; ++c) {
+              const uint32_t o = stg_off(lane, c);
+              *reinterpret_cast<uint4*>(st0 + o) = make_uint4(pp[4 * c], pp[4 * c + 1], pp[4 * c + 2], pp[4 * c + 3]);
+              *reinterpret_cast<uint4*>(st0 + 2048 + o) = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+              *reinterpret_cast<uint4*>(st0 + 4096 + o) = make_uint4(lo[4 * c], lo[4 * c + 1], lo[4 * c + 2], lo[4 * c + 3]);
+            }
+            __syncwarp();
+            const int cc = lane & 3;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int R = (lane >> 2) + 8 * i, qq = qt * TB + qtr * 32 + R;
+              if (qq < p.HQ) {
+                const uint32_t o = stg_off(R, cc);
+                const long long col = t0 + c0 + 8 * cc;
+                *reinterpret_cast<uint4*>(p.dZ + ((long long)b * 2 * p.HQ + qq) * p.T + col) =
+                    *reinterpret_cast<const uint4*>(st0 + o);
+                *reinterpret_cast<uint4*>(p.dZ + ((long long)b * 2 * p.HQ + p.HQ + qq) * p.T + col) =
+                    *reinterpret_cast<const uint4*>(st0 + 2048 + o);
+                *reinterpret_cast<uint4*>(p.dZlo + ((long long)b * p.HQ + qq) * p.T + col) =
+                    *reinterpret_cast<const uint4*>(st0 + 4096 + o);
               }
-            } else {
+            }
+            __syncwarp();
+          } else if (qv && c0 < cols) {
+            {
 #pragma unroll
               for (int i = 0; i < 32; ++i) {
                 if (c0 + i >= cols) continue;
@@ -1486,7 +1514,7 @@ __global__ void __launch_bounds__(NT, 1)
   if (warp == 1) tc::tmem_dealloc(tmem, 512);
 }
 
-size_t bwd512_smem() { return 1024 + 8 * ATOM + GST * GSTAGE + (2 + 2 * GST + 4) * 8 + 16; }
+size_t bwd512_smem() { return 1024 + 8 * ATOM + GST * GSTAGE + 4 * BSTG + (2 + 2 * GST + 4) * 8 + 16; }
 
 template <int D>
 size_t bwd_smem() {
