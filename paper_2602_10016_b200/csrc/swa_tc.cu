@@ -96,6 +96,30 @@ __device__ __forceinline__ void store_row64(bf16* dst, uint32_t taddr, float sca
   }
 }
 
+
+// Coalesced store of one warp's 32 rows x 64 bf16 columns (thread = row; pk =
+// the row's 32 packed pairs) through a 4 KB staging region: each store
+// instruction covers 4 rows x 128 B, where a row-per-thread 16-byte store
+// touches 32 lines per warp instruction (4-8x the L1 wavefronts).
+__device__ __forceinline__ void store_rows64_co(uint8_t* stg, const uint32_t* pk, bf16* base, long long ld, int row0,
+                                                int nvalid) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    *reinterpret_cast<uint4*>(stg + lane * 128 + ((c ^ (lane & 7)) << 4)) =
+        make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+  __syncwarp();
+  const int c = lane & 7;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int R = (lane >> 3) + 4 * i;
+    if (R < nvalid)
+      *reinterpret_cast<uint4*>(base + (long long)(row0 + R) * ld + 8 * c) =
+          *reinterpret_cast<const uint4*>(stg + R * 128 + ((c ^ (R & 7)) << 4));
+  }
+  __syncwarp();
+}
+
 // Write 32 bf16 (one tcgen05.ld.x32 worth) of row r, columns [c0, c0+32), into
 // a K-major SWIZZLE_128B 128 x 128 block.
 __device__ __forceinline__ void store_sw(uint8_t* blk, int r, int c0, const uint32_t* pk) {
@@ -1814,32 +1838,27 @@ __global__ void __launch_bounds__(NT3, 1)
         tc::mbar_wait(&acc_full[t & 1], (t >> 1) & 1);
         if (wtid == 0) SWT(9, t);
         tc::fence_after();
+        // staged in this warpgroup's P^T | dS^T slot: acc_full says every
+        // product of the tile (those reading the slot included) has completed
+        uint8_t* stg = sPD + wg * 2 * PH + qtr * 4096;
+        const int row0 = tl.k0 + qtr * 32, nvalid = max(0, min(32, p.T - row0));
 #pragma unroll 1
         for (int which = 0; which < 2; ++which) {  // 0: dK (scaled), 1: dV
           const float sc = which ? 1.f : p.scale;
-#pragma unroll 1
-          for (int ch = 0; ch < 2; ++ch) {
-            float v[32];
-            tc::tmem_ld32(trow + T_ACC + (t & 1) * 128 + (which ? 0 : 64) + ch * 32, v);
-            if (which == 1 && ch == 1) {
-              tc::fence_before();
-              __syncwarp();
-              if (lane == 0) tc::mbar_arrive(&acc_empty[t & 1]);
-            }
-            if (key < p.T) {
-              uint4* o = reinterpret_cast<uint4*>(out + (long long)key * p.ld_qkv + (1 + which) * HD + ch * 32);
-#pragma unroll
-              for (int c = 0; c < 4; ++c) {
-                uint4 u;
-                u.x = tc::pack_bf16(v[8 * c + 0] * sc, v[8 * c + 1] * sc);
-                u.y = tc::pack_bf16(v[8 * c + 2] * sc, v[8 * c + 3] * sc);
-                u.z = tc::pack_bf16(v[8 * c + 4] * sc, v[8 * c + 5] * sc);
-                u.w = tc::pack_bf16(v[8 * c + 6] * sc, v[8 * c + 7] * sc);
-                o[c] = u;
-              }
-            }
+          float v[64];
+          const uint32_t ta = trow + T_ACC + (t & 1) * 128 + (which ? 0 : 64);
+          tc::tmem_ld32x2(ta, v, ta + 32, v + 32);
+          if (which == 1) {
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&acc_empty[t & 1]);
           }
+          uint32_t pk[32];
+#pragma unroll
+          for (int c = 0; c < 32; ++c) pk[c] = tc::pack_bf16(v[2 * c] * sc, v[2 * c + 1] * sc);
+          store_rows64_co(stg, pk, out + (1 + which) * HD, p.ld_qkv, row0, nvalid);
         }
+        (void)key;
         if (wtid == 0) SWT(19, t);
       }
       ++t;
@@ -2116,27 +2135,18 @@ __global__ void __launch_bounds__(NT3, 1)
       if ((last_item & 1) == wg) {
         tc::mbar_wait(acc_full, t & 1);
         tc::fence_after();
-#pragma unroll 1
-        for (int ch = 0; ch < 2; ++ch) {
-          float v[32];
-          tc::tmem_ld32(trow + T_DQ + ch * 32, v);
-          if (ch == 1) {
-            tc::fence_before();
-            __syncwarp();
-            if (lane == 0) tc::mbar_arrive(acc_empty);
-          }
-          if (q < p.T) {
-            uint4* o = reinterpret_cast<uint4*>(out + (long long)q * p.ld_qkv + ch * 32);
+        {
+          // staged in this warpgroup's dS slot (every dQ product has completed)
+          float v[64];
+          tc::tmem_ld32x2(trow + T_DQ, v, trow + T_DQ + 32, v + 32);
+          tc::fence_before();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(acc_empty);
+          uint32_t pk[32];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              uint4 u;
-              u.x = tc::pack_bf16(v[8 * c + 0] * p.scale, v[8 * c + 1] * p.scale);
-              u.y = tc::pack_bf16(v[8 * c + 2] * p.scale, v[8 * c + 3] * p.scale);
-              u.z = tc::pack_bf16(v[8 * c + 4] * p.scale, v[8 * c + 5] * p.scale);
-              u.w = tc::pack_bf16(v[8 * c + 6] * p.scale, v[8 * c + 7] * p.scale);
-              o[c] = u;
-            }
-          }
+          for (int c = 0; c < 32; ++c) pk[c] = tc::pack_bf16(v[2 * c] * p.scale, v[2 * c + 1] * p.scale);
+          const int row0 = tl.k0 + qtr * 32;
+          store_rows64_co(sDS + wg * PH + qtr * 4096, pk, out, p.ld_qkv, row0, max(0, min(32, p.T - row0)));
         }
       }
       ++t;
@@ -2398,19 +2408,16 @@ __global__ void __launch_bounds__(NTF, 2)
       tc::fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(o_empty);
-      if (q < p.T) {
+      {
+        // staged in P slot 0 (this warp's 32 rows of it): o_full says the
+        // tile's P V products, the last readers of P, have completed
         const float inv = l > 0.f ? 1.f / l : 0.f;
-        uint4* dst = reinterpret_cast<uint4*>(O + (long long)q * p.ld_o);
+        uint32_t pk[32];
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          uint4 u;
-          u.x = tc::pack_bf16(o[8 * c + 0] * inv, o[8 * c + 1] * inv);
-          u.y = tc::pack_bf16(o[8 * c + 2] * inv, o[8 * c + 3] * inv);
-          u.z = tc::pack_bf16(o[8 * c + 4] * inv, o[8 * c + 5] * inv);
-          u.w = tc::pack_bf16(o[8 * c + 6] * inv, o[8 * c + 7] * inv);
-          dst[c] = u;
-        }
-        LSE[q] = l > 0.f ? (mref + __log2f(l)) * 0.6931471805599453f : INFINITY;
+        for (int c = 0; c < 32; ++c) pk[c] = tc::pack_bf16(o[2 * c] * inv, o[2 * c + 1] * inv);
+        const int row0 = q - lane;
+        store_rows64_co(sP + qtr * 4096, pk, O, p.ld_o, row0, max(0, min(32, p.T - row0)));
+        if (q < p.T) LSE[q] = l > 0.f ? (mref + __log2f(l)) * 0.6931471805599453f : INFINITY;
       }
       if (ctid == 0) SWT(13, t);
       ++t;
