@@ -1034,18 +1034,34 @@ __global__ void __launch_bounds__(NT5, 1)
 
 size_t fwd512_smem() { return 1024 + RST * FSTAGE + 4 * ATOM_S + 2 * ATOM_S + 8 * 4096 + (2 * RST + 18) * 8 + 16; }
 
+// Backward (d = 512), persistent CTAs over (sample, 128-row tile) items:
+//   warp 0     TMA: per tile 8 (dY | Vt | S | Kt) atom stages (2-slot ring),
+//              then the 4 Kt column quarters (128 x 128, MN-major B of dS)
+//   warp 1     MMA: dA = sum_a dY_a Vt_a^T, Z = sum_a S_a Kt_a^T;
+//              dS_q = dZ Kt[:, q] (N = 128) into a double-buffered TMEM pair
+//   warps 2-9  dZ = dA Act'(Z) / tau, A = Act(Z) -> dZ to smem (the dS
+//              products' A operand) and, with A, to HBM by TMA store (the
+//              caller's dKt / dVt GEMMs); dS_q + dY -> dS: per warp a 32-row x
+//              64-column tile, residual TMA-loaded into and the sum TMA-stored
+//              from its staging tile.  (Row-per-thread 16-byte global accesses
+//              touch 32 lines per warp instruction; quarter-width dS products
+//              free the shared memory for the staging tiles and let the next
+//              quarter's product overlap this quarter's epilogue.)
 __global__ void __launch_bounds__(NT5, 1)
     gdpa_bwd512_kernel(const __grid_constant__ CUtensorMap ts, const __grid_constant__ CUtensorMap tg,
                        const __grid_constant__ CUtensorMap tk, const __grid_constant__ CUtensorMap tv,
-                       const P5 p) {
+                       const __grid_constant__ CUtensorMap tkq, const __grid_constant__ CUtensorMap tg32,
+                       const __grid_constant__ CUtensorMap to32, const __grid_constant__ CUtensorMap tz32,
+                       const __grid_constant__ CUtensorMap ta32, const P5 p) {
   constexpr uint32_t IDESC_Z = tc::idesc_bf16(TB, HK2, 0, 0);
-  constexpr uint32_t IDESC_DS = tc::idesc_bf16(TB, 256, 0, 1);
-  constexpr uint32_t T_DA = 0, T_Z = 128, T_DS = 256;
+  constexpr uint32_t IDESC_DS = tc::idesc_bf16(TB, 128, 0, 1);
+  constexpr uint32_t T_DA = 0, T_Z = 128, T_DS = 256;  // dS: 2 x 128 columns
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sR = align1k(smem_raw);          // 2 x (dY | Vt | S | Kt atoms)
-  uint8_t* sK = sR + 2 * BSTAGE;            // Kt half: 4 atoms (MN-major B of dS = dZ Kt)
-  uint8_t* sD = sK + 4 * ATOM_S;            // dZ tile 128 x 128 bf16
-  uint64_t* bar = (uint64_t*)(sD + 2 * ATOM_S);
+  uint8_t* sK = sR + 2 * BSTAGE;            // Kt quarter: 2 atoms (128 x 128, MN-major B of dS_q)
+  uint8_t* sD = sK + 2 * ATOM_S;            // dZ tile 128 x 128 bf16
+  uint8_t* sStg = sD + 2 * ATOM_S;          // 8 x 4 KB per-warp epilogue tiles
+  uint64_t* bar = (uint64_t*)(sStg + 8 * 4096);
   uint64_t* rs_full = bar;                  // [2]
   uint64_t* rs_empty = bar + 2;             // [2]
   uint64_t* ks_full = bar + 4;
@@ -1054,9 +1070,10 @@ __global__ void __launch_bounds__(NT5, 1)
   uint64_t* zz_empty = bar + 7;
   uint64_t* d_full = bar + 8;
   uint64_t* d_empty = bar + 9;
-  uint64_t* s_full = bar + 10;
-  uint64_t* s_empty = bar + 11;
-  uint32_t* tslot = (uint32_t*)(bar + 12);
+  uint64_t* s_full = bar + 10;              // [2]
+  uint64_t* s_empty = bar + 12;             // [2]
+  uint64_t* rbar = bar + 14;                // [8]
+  uint32_t* tslot = (uint32_t*)(bar + 22);
 
   const int nT = (p.T + TB - 1) / TB;
   const int W = p.B * nT;
@@ -1071,9 +1088,16 @@ __global__ void __launch_bounds__(NT5, 1)
     tc::prefetch_tmap(&tg);
     tc::prefetch_tmap(&tk);
     tc::prefetch_tmap(&tv);
+    tc::prefetch_tmap(&tkq);
+    tc::prefetch_tmap(&tg32);
+    tc::prefetch_tmap(&to32);
+    tc::prefetch_tmap(&tz32);
+    tc::prefetch_tmap(&ta32);
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&rs_full[i], 1);
       tc::mbar_init(&rs_empty[i], 1);
+      tc::mbar_init(&s_full[i], 1);
+      tc::mbar_init(&s_empty[i], 8);
     }
     tc::mbar_init(ks_full, 1);
     tc::mbar_init(ks_empty, 1);
@@ -1081,8 +1105,7 @@ __global__ void __launch_bounds__(NT5, 1)
     tc::mbar_init(zz_empty, 8);
     tc::mbar_init(d_full, 8);
     tc::mbar_init(d_empty, 1);
-    tc::mbar_init(s_full, 1);
-    tc::mbar_init(s_empty, 8);
+    for (int i = 0; i < 8; ++i) tc::mbar_init(&rbar[i], 1);
     tc::fence_barrier_init();
   }
   if (warp == 1) tc::tmem_alloc(tslot, 512);
@@ -1100,19 +1123,19 @@ __global__ void __launch_bounds__(NT5, 1)
 #pragma unroll 1
         for (int a = 0; a < 8; ++a, ++rc) {
           const int st = rc & 1;
-          uint8_t* d = sR + st * BSTAGE;
           tc::mbar_wait(&rs_empty[st], ((rc >> 1) & 1) ^ 1);
+          uint8_t* d = sR + st * BSTAGE;
           tc::mbar_arrive_expect_tx(&rs_full[st], BSTAGE);
           tc::tma_load_3d(d, &tg, &rs_full[st], a * 64, q0, b);
           tc::tma_load_3d(d + ATOM_S, &tv, &rs_full[st], a * 64, 0, b);
           tc::tma_load_3d(d + 2 * ATOM_S, &ts, &rs_full[st], a * 64, q0, b);
           tc::tma_load_3d(d + 3 * ATOM_S, &tk, &rs_full[st], a * 64, 0, b);
         }
-        for (int h = 0; h < 2; ++h, ++kc) {
+        for (int q = 0; q < 4; ++q, ++kc) {
           tc::mbar_wait(ks_empty, (kc & 1) ^ 1);
-          tc::mbar_arrive_expect_tx(ks_full, 4 * ATOM_S);
+          tc::mbar_arrive_expect_tx(ks_full, 2 * ATOM_S);
 #pragma unroll
-          for (int a = 0; a < 4; ++a) tc::tma_load_3d(sK + a * ATOM_S, &tk, ks_full, (4 * h + a) * 64, 0, b);
+          for (int a = 0; a < 2; ++a) tc::tma_load_3d(sK + a * ATOM_S, &tkq, ks_full, (2 * q + a) * 64, 0, b);
         }
       }
     }
@@ -1139,14 +1162,16 @@ __global__ void __launch_bounds__(NT5, 1)
         }
         tc::mma_commit(zz_full);
         tc::mbar_wait(d_full, c & 1);
-        for (int h = 0; h < 2; ++h, ++sc, ++kc) {
-          tc::mbar_wait(s_empty, (sc & 1) ^ 1);
+        for (int q = 0; q < 4; ++q, ++sc, ++kc) {
+          const int sb = sc & 1;
+          tc::mbar_wait(&s_empty[sb], ((sc >> 1) & 1) ^ 1);
           tc::mbar_wait(ks_full, kc & 1);
           tc::fence_after();
 #pragma unroll
           for (int kk = 0; kk < HK2 / 16; ++kk)
-            tc::mma_bf16(tmem + T_DS, dk(da, kk, ATOM_S), dmn(ka0, kk, ATOM_S), IDESC_DS, kk > 0 ? 1u : 0u);
-          tc::mma_commit(s_full);
+            tc::mma_bf16(tmem + T_DS + sb * 128, dk(da, kk, ATOM_S), dmn(ka0, kk, ATOM_S), IDESC_DS,
+                         kk > 0 ? 1u : 0u);
+          tc::mma_commit(&s_full[sb]);
           tc::mma_commit(ks_empty);
         }
         tc::mma_commit(d_empty);
@@ -1156,20 +1181,23 @@ __global__ void __launch_bounds__(NT5, 1)
     const int qtr = warp & 3, hf = (warp - 2) >> 2;
     const int r = qtr * 32 + lane;
     const uint32_t trow = tmem + ((uint32_t)(qtr * 32) << 16);
-    int c = 0, sc = 0;
+    uint8_t* stg = sStg + (warp - 2) * 4096;
+    uint64_t* rb = &rbar[warp - 2];
+    int c = 0, sc = 0, rph = 0;
     for (int k = i0; k < i1; ++k, ++c) {
       const int b = k / nT, q0 = (k % nT) * TB;
       int len = __ldg(&p.lengths[b]);
       asm volatile("" : "+r"(len));
-      const bool live = q0 + r < len, inb = q0 + r < p.T;
+      const bool live = q0 + r < len;
+      const int row0 = q0 + qtr * 32;
+      const long long zrow0 = (long long)b * p.T + row0;  // row of the flat (B*T, 128) dZ / A
       tc::mbar_wait(zz_full, c & 1);
       tc::fence_after();
       uint32_t pdz[32], pa[32];
 #pragma unroll
       for (int hc = 0; hc < 2; ++hc) {  // two 32-column chunks (two head groups each)
         float da[32], z[32], y[32], dy[32];
-        tc::tmem_ld32(trow + T_DA + hf * 64 + 32 * hc, da);
-        tc::tmem_ld32(trow + T_Z + hf * 64 + 32 * hc, z);
+        tc::tmem_ld32x2(trow + T_DA + hf * 64 + 32 * hc, da, trow + T_Z + hf * 64 + 32 * hc, z);
         act_cols32<true>(code, hf * 64 + 32 * hc, true, z, da, p.inv_tau, y, dy);
 #pragma unroll
         for (int i = 0; i < 32; i += 2) {
@@ -1180,47 +1208,89 @@ __global__ void __launch_bounds__(NT5, 1)
       tc::fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(zz_empty);
-      if (inb) {  // dZ and A rows -> HBM (the dKt / dVt GEMMs' operands)
-        uint4* zo = reinterpret_cast<uint4*>(p.dZ + ((long long)b * p.T + q0 + r) * HK2 + hf * 64);
-        uint4* ao = reinterpret_cast<uint4*>(p.A + ((long long)b * p.T + q0 + r) * HK2 + hf * 64);
+      // A -> this warp's staging tile (SW128, 32 rows x 64 columns) -> HBM
+      if (lane == 0) tc::bulk_wait_read0();  // the previous TMA store has read the tile
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        *reinterpret_cast<uint4*>(stg + lane * 128 + ((q ^ (lane & 7)) << 4)) =
+            make_uint4(pa[4 * q], pa[4 * q + 1], pa[4 * q + 2], pa[4 * q + 3]);
+      tc::mbar_wait(d_empty, (c & 1) ^ 1);
+#pragma unroll
+      for (int g = 0; g < 4; ++g) store_sw16(sD, r, hf * 64 + 16 * g, pdz + 8 * g);
+      tc::fence_async_smem();
+      __syncwarp();
+      const bool full_box = row0 + 32 <= p.T;  // the flat (B*T, 128) rows past T belong to the next sample
+      if (lane == 0) {
+        tc::mbar_arrive(d_full);
+        if (full_box) {
+          // dZ rows straight from the operand tile (atom hf, rows [32 qtr, +32): a SW128 box), A from staging
+          tc::tma_store_3d(&tz32, sD + hf * ATOM_S + qtr * 4096, hf * 64, (int)zrow0, 0);
+          tc::tma_store_3d(&ta32, stg, hf * 64, (int)zrow0, 0);
+        }
+        tc::bulk_commit();
+      }
+      if (!full_box && q0 + r < p.T) {  // sequence tail: this thread's row
+        uint4* zo = reinterpret_cast<uint4*>(p.dZ + (zrow0 + lane) * HK2 + hf * 64);
+        uint4* ao = reinterpret_cast<uint4*>(p.A + (zrow0 + lane) * HK2 + hf * 64);
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           zo[q] = make_uint4(pdz[4 * q], pdz[4 * q + 1], pdz[4 * q + 2], pdz[4 * q + 3]);
           ao[q] = make_uint4(pa[4 * q], pa[4 * q + 1], pa[4 * q + 2], pa[4 * q + 3]);
         }
       }
-      tc::mbar_wait(d_empty, (c & 1) ^ 1);
-#pragma unroll
-      for (int g = 0; g < 4; ++g) store_sw16(sD, r, hf * 64 + 16 * g, pdz + 8 * g);
-      tc::fence_async_smem();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(d_full);
-      const bf16* rrow = p.res + (long long)b * p.r_bs + (long long)(q0 + r) * p.r_rs;
-      bf16* orow = p.out + (long long)b * p.o_bs + (long long)(q0 + r) * p.o_rs;
-      for (int h = 0; h < 2; ++h, ++sc) {
-        uint4 res[16];
-        prefetch_res128(rrow + h * 256 + hf * 128, inb, res);
-        tc::mbar_wait(s_full, sc & 1);
-        tc::fence_after();
-#pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {
-          float acc[32];
-          tc::tmem_ld32(trow + T_DS + hf * 128 + 32 * cc, acc);
-          const int col = h * 256 + hf * 128 + 32 * cc;
-          if (inb) add_res_store32(acc, res + 4 * cc, orow + col);
+      // dS_q + dY -> dS, quarter q: this warp's 32 rows x columns [128 q + 64 hf, +64)
+      auto res_issue = [&](int col0) {
+        if (lane == 0) {
+          tc::bulk_wait_read0();
+          tc::mbar_arrive_expect_tx(rb, 4096);
+          tc::tma_load_3d(stg, &tg32, rb, col0, row0, b);
         }
+      };
+      res_issue(hf * 64);
+      for (int q = 0; q < 4; ++q, ++sc) {
+        const int sb = sc & 1;
+        const int col0 = q * 128 + hf * 64;
+        tc::mbar_wait(&s_full[sb], (sc >> 1) & 1);
+        tc::fence_after();
+        float acc[64];
+        tc::tmem_ld32x2(trow + T_DS + sb * 128 + hf * 64, acc, trow + T_DS + sb * 128 + hf * 64 + 32, acc + 32);
         tc::fence_before();
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive(s_empty);
+        if (lane == 0) tc::mbar_arrive(&s_empty[sb]);
+        tc::mbar_wait(rb, rph & 1);
+        ++rph;
+        uint8_t* rowp = stg + lane * 128;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          uint4* cp = reinterpret_cast<uint4*>(rowp + ((u ^ (lane & 7)) << 4));
+          const uint4 v4 = *cp;
+          const uint32_t w[4] = {v4.x, v4.y, v4.z, v4.w};
+          uint32_t o[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[i]));
+            o[i] = tc::pack_bf16(acc[8 * u + 2 * i] + f.x, acc[8 * u + 2 * i + 1] + f.y);
+          }
+          *cp = make_uint4(o[0], o[1], o[2], o[3]);
+        }
+        tc::fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tc::tma_store_3d(&to32, stg, col0, row0, b);
+          tc::bulk_commit();
+        }
+        if (q + 1 < 4) res_issue(col0 + 128);
       }
     }
+    if (lane == 0) tc::bulk_wait0();
   }
   tc::fence_before();
   __syncthreads();
   if (warp == 1) tc::tmem_dealloc(tmem, 512);
 }
 
-size_t bwd512_smem() { return 1024 + 2 * BSTAGE + 4 * ATOM_S + 2 * ATOM_S + 12 * 8 + 16; }
+size_t bwd512_smem() { return 1024 + 2 * BSTAGE + 2 * ATOM_S + 2 * ATOM_S + 8 * 4096 + 22 * 8 + 16; }
 
 static int last_rc = 0;
 bool map3(CUtensorMap* m, const void* ptr, long long inner, long long rows, long long B, long long ld, long long bs,
@@ -1418,6 +1488,19 @@ static int gdpa_bwd512_launch(const kl_gdpa_args* a, const gdpa::P& p, cudaStrea
     set_error("kl_gdpa_bwd: dY / dS / dZ / A rows must be 16-byte aligned");
     return KL_EUNSUPPORTED;
   }
+  // Kt column quarters (128 rows x 2 boxes) and the epilogue's 32-row tiles:
+  // dY residual, dS output, dZ / A rows of the flat (B*T, 128) buffers
+  CUtensorMap tkq, tg32, to32, tz32, ta32;
+  if (!gdpa::map3(&tkq, a->Kt, 512, gdpa::HK2, a->B, 512, kvbs, gdpa::HK2) ||
+      !gdpa::map3(&tg32, a->dY, 512, a->T, a->B, a->s_rs, a->s_bs, 32) ||
+      !gdpa::map3(&to32, a->dS, 512, a->T, a->B, a->s_rs, a->s_bs, 32) ||
+      !gdpa::map3(&tz32, a->dZ_out, gdpa::HK2, (long long)a->B * a->T, 1, gdpa::HK2,
+                  (long long)a->B * a->T * gdpa::HK2, 32) ||
+      !gdpa::map3(&ta32, a->A_out, gdpa::HK2, (long long)a->B * a->T, 1, gdpa::HK2,
+                  (long long)a->B * a->T * gdpa::HK2, 32)) {
+    set_error("kl_gdpa_bwd: tensor map encode failed (alignment?)");
+    return KL_EUNSUPPORTED;
+  }
   gdpa::P5 q = p5_of(a, p);
   q.out = (bf16*)a->dS;
   q.res = (const bf16*)a->dY;
@@ -1428,7 +1511,7 @@ static int gdpa_bwd512_launch(const kl_gdpa_args* a, const gdpa::P& p, cudaStrea
   const int W = a->B * ((a->T + gdpa::TB - 1) / gdpa::TB);
   int grid = std::min(W, tc_num_sms());
   if (const char* g = getenv("KL_GDPA_GRID")) grid = std::max(1, std::min(grid, atoi(g)));  // testing: multi-tile CTAs
-  launch_k(gdpa::gdpa_bwd512_kernel, grid, gdpa::NT5, smem, s, ts, tg, tk, tv, q);
+  launch_k(gdpa::gdpa_bwd512_kernel, grid, gdpa::NT5, smem, s, ts, tg, tk, tv, tkq, tg32, to32, tz32, ta32, q);
   count_launch();
   count_path(KL_PATH_GDPA_BWD_TC512);
   return launch_check("gdpa_bwd512_tc");
