@@ -23,7 +23,7 @@ import torch
 
 from . import _capi
 from ._capi import gemm
-from .tensor import ACTIVATIONS, ShapeError
+from .tensor import ACTIVATIONS, ShapeError, flag_nonfinite, numerics_check_mode
 
 
 class PRef:
@@ -1246,6 +1246,73 @@ class _Gated(torch.autograd.Function):
 
 def gated_sum(x, deep, dot, P, gdkey, gtkey):
     return _Gated.apply(x, deep, dot, P.flat, P, gdkey, gtkey)
+
+
+class _WukongExpert(torch.autograd.Function):
+    """One Wukong expert (interaction.py:106-121) as one autograd node:
+        out = x + g_deep * (silu(x W1^T + b1) W2^T + b2) + g_dot * (triu(x x^T) W_dot^T)
+    with the forward's kernels of gram_triu / the two linears / gated_sum.
+    Its VJP accumulates the three input-gradient paths into one buffer — the
+    deep path's dX GEMM takes the identity path (the incoming gradient) as its
+    residual and the gram VJP adds in place — so autograd sees one consumer
+    of x (no zero fills, clones or gradient additions between kernels)."""
+
+    @staticmethod
+    def forward(ctx, x, flat, P, dm, w1, b1, w2, b2, gd, gt):
+        B, n, d = x.shape
+        if x.stride(2) != 1 or x.stride(0) != n * x.stride(1) or x.stride(1) != d:
+            x = x.contiguous()
+        tri = torch.empty(B, pad8(n * (n + 1) // 2), device=x.device, dtype=x.dtype)  # kernel zeroes the pad
+        _capi.call("kl_gram_triu_fwd", B, n, d, _capi.dt(x), x.data_ptr(), x.stride(1), x.stride(0),
+                   tri.data_ptr(), tri.stride(0), _stream())
+        dot = gemm(tri, P.w(dm).transpose(0, 1))  # (B, n*d)
+        rows = x.view(B * n, d)
+        H = P.w(w1).shape[0]
+        pre = torch.empty(B * n, H, device=x.device, dtype=x.dtype)
+        h1 = gemm(rows, P.w(w1).transpose(0, 1), bias=P.w32(b1), acts=_codes(["silu"]), aux=pre, aux_mode=1)
+        deep = gemm(h1, P.w(w2).transpose(0, 1), bias=P.w32(b2))
+        if numerics_check_mode() == "eager":
+            flag_nonfinite(deep, "Mlp")
+        out = torch.empty(B, n, d, device=x.device, dtype=x.dtype)
+        _capi.call("kl_gated_sum_fwd", B * n, d, _capi.dt(x), x.data_ptr(), d, deep.data_ptr(), dot.data_ptr(),
+                   P.w32(gd).data_ptr(), P.w32(gt).data_ptr(), out.data_ptr(), d, _stream())
+        ctx.P, ctx.keys = P, (dm, w1, b1, w2, b2, gd, gt)
+        ctx.save_for_backward(x, tri, pre, h1, deep, dot)
+        return out
+
+    @staticmethod
+    def backward(ctx, g):
+        x, tri, pre, h1, deep, dot = ctx.saved_tensors
+        P = ctx.P
+        dm, w1, b1, w2, b2, gd, gt = ctx.keys
+        B, n, d = x.shape
+        rows = B * n
+        g = g.contiguous()
+        ddeep = torch.empty_like(deep)
+        ddot = torch.empty_like(dot)
+        scratch = torch.empty(2 * 512, device=g.device, dtype=torch.float64)
+        _capi.call("kl_gated_sum_bwd", rows, d, _capi.dt(g), g.data_ptr(), d, deep.data_ptr(), dot.data_ptr(),
+                   P.w32(gd).data_ptr(), P.w32(gt).data_ptr(), ddeep.data_ptr(), ddot.data_ptr(),
+                   P.g(gd).data_ptr(), P.g(gt).data_ptr(), scratch.data_ptr(), _stream())
+        # deep path: dh1 = (ddeep W2) * silu'(pre); dx = dh1 W1 + g (the identity path)
+        dh1 = gemm(ddeep, P.w(w2), acts=_codes(["silu"]), aux=pre, aux_mode=2)
+        dx = gemm(dh1, P.w(w1), residual=g.view(rows, d))
+        dtri = gemm(ddot, P.w(dm))  # dot path: d(triu) = ddot W_dot
+        ones = _ones(rows, g.dtype, g.device)
+        with _DwFork((ddeep, dh1, x, h1, ddot, tri, ones)):
+            gemm(ddeep.t(), h1, P.g(w2), beta=1.0)
+            gemm(ones.view(1, rows), ddeep, P.g(b2).view(1, -1), beta=1.0)
+            gemm(dh1.t(), x.view(rows, d), P.g(w1), beta=1.0)
+            gemm(ones.view(1, rows), dh1, P.g(b1).view(1, -1), beta=1.0)
+            gemm(ddot.t(), tri, P.g(dm), beta=1.0)
+        dx = dx.view(B, n, d)
+        _capi.call("kl_gram_triu_bwd", B, n, d, _capi.dt(x), x.data_ptr(), x.stride(1), x.stride(0),
+                   dtri.data_ptr(), dtri.stride(0), dx.data_ptr(), dx.stride(1), dx.stride(0), _stream())
+        return dx, None, None, None, None, None, None, None, None, None
+
+
+def wukong_expert_fused(x, P, dm, w1, b1, w2, b2, gd, gt):
+    return _WukongExpert.apply(x, P.flat, P, dm, w1, b1, w2, b2, gd, gt)
 
 
 class _BCE(torch.autograd.Function):
