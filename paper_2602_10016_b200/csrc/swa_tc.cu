@@ -1792,33 +1792,33 @@ __global__ void __launch_bounds__(NT3, 1)
             if (lane == 0) tc::mbar_arrive(&sd_empty[ss]);
           }
           uint32_t pp[16], pd[16];
-          if (q0c > qhi || q0c + 31 < qlo) {
+          // warp-uniform paths (a row-dependent band edge would otherwise split
+          // the warp between the full and the per-element path): all rows
+          // outside the band -> zeros; all rows fully inside -> no masking;
+          // else every lane runs the full math with a per-element select
+          const bool none = q0c > qhi || q0c + 31 < qlo, full = q0c >= qlo && q0c + 31 <= qhi;
+          if (__all_sync(0xffffffffu, none)) {
 #pragma unroll
             for (int i = 0; i < 16; ++i) pp[i] = pd[i] = 0u;
-          } else if (q0c >= qlo && q0c + 31 <= qhi) {
+          } else {
+            const bool all_full = __all_sync(0xffffffffu, full);
 #pragma unroll
             for (int i = 0; i < 32; i += 4) {
               const float4 l4 = *reinterpret_cast<const float4*>(&ls[lb + i]);
               const float4 d4 = *reinterpret_cast<const float4*>(&dd[lb + i]);
-              const float p0 = ex2(fmaf(s[i], c2, -l4.x)), p1 = ex2(fmaf(s[i + 1], c2, -l4.y));
-              const float p2 = ex2(fmaf(s[i + 2], c2, -l4.z)), p3 = ex2(fmaf(s[i + 3], c2, -l4.w));
+              float p0 = ex2(fmaf(s[i], c2, -l4.x)), p1 = ex2(fmaf(s[i + 1], c2, -l4.y));
+              float p2 = ex2(fmaf(s[i + 2], c2, -l4.z)), p3 = ex2(fmaf(s[i + 3], c2, -l4.w));
+              if (!all_full) {
+                const int qi = q0c + i;
+                p0 = (qi >= qlo && qi <= qhi) ? p0 : 0.f;
+                p1 = (qi + 1 >= qlo && qi + 1 <= qhi) ? p1 : 0.f;
+                p2 = (qi + 2 >= qlo && qi + 2 <= qhi) ? p2 : 0.f;
+                p3 = (qi + 3 >= qlo && qi + 3 <= qhi) ? p3 : 0.f;
+              }
               pp[i >> 1] = tc::pack_bf16(p0, p1);
               pp[(i >> 1) + 1] = tc::pack_bf16(p2, p3);
               pd[i >> 1] = tc::pack_bf16(p0 * (g[i] - d4.x), p1 * (g[i + 1] - d4.y));
               pd[(i >> 1) + 1] = tc::pack_bf16(p2 * (g[i + 2] - d4.z), p3 * (g[i + 3] - d4.w));
-            }
-          } else {
-#pragma unroll
-            for (int i = 0; i < 32; i += 2) {
-              float pr[2], dsv[2];
-#pragma unroll
-              for (int u = 0; u < 2; ++u) {
-                const int qi = q0c + i + u;
-                pr[u] = (qi >= qlo && qi <= qhi) ? ex2(fmaf(s[i + u], c2, -ls[lb + i + u])) : 0.f;
-                dsv[u] = pr[u] * (g[i + u] - dd[lb + i + u]);
-              }
-              pp[i >> 1] = tc::pack_bf16(pr[0], pr[1]);
-              pd[i >> 1] = tc::pack_bf16(dsv[0], dsv[1]);
             }
           }
           // this warpgroup's P^T / dS^T slot is free once the products of
@@ -2106,10 +2106,12 @@ __global__ void __launch_bounds__(NT3, 1)
             if (lane == 0) tc::mbar_arrive(&sd_empty[ss]);
           }
           uint32_t pk[16];
-          if (k0c > khi || k0c + 31 < klo) {
+          // warp-uniform paths (see the dK / dV kernel)
+          const bool none = k0c > khi || k0c + 31 < klo, full = k0c >= klo && k0c + 31 <= khi;
+          if (__all_sync(0xffffffffu, none)) {
 #pragma unroll
             for (int i = 0; i < 16; ++i) pk[i] = 0u;
-          } else if (k0c >= klo && k0c + 31 <= khi) {
+          } else if (__all_sync(0xffffffffu, full)) {
 #pragma unroll
             for (int i = 0; i < 32; i += 2) {
               const float a0 = ex2(fmaf(sv[i], c2, -lse2)) * (g[i] - dr);
@@ -2120,9 +2122,9 @@ __global__ void __launch_bounds__(NT3, 1)
 #pragma unroll
             for (int i = 0; i < 32; i += 2) {
               const bool ok0 = k0c + i >= klo && k0c + i <= khi, ok1 = k0c + i + 1 >= klo && k0c + i + 1 <= khi;
-              const float a0 = ok0 ? ex2(fmaf(sv[i], c2, -lse2)) * (g[i] - dr) : 0.f;
-              const float a1 = ok1 ? ex2(fmaf(sv[i + 1], c2, -lse2)) * (g[i + 1] - dr) : 0.f;
-              pk[i >> 1] = tc::pack_bf16(a0, a1);
+              const float e0 = ex2(fmaf(sv[i], c2, -lse2)) * (g[i] - dr);
+              const float e1 = ex2(fmaf(sv[i + 1], c2, -lse2)) * (g[i + 1] - dr);
+              pk[i >> 1] = tc::pack_bf16(ok0 ? e0 : 0.f, ok1 ? e1 : 0.f);
             }
           }
           if (ch == 0) tc::mbar_wait(&ds_empty[wg], ((n_item >> 1) & 1) ^ 1);
@@ -2347,7 +2349,7 @@ __global__ void __launch_bounds__(NTF, 2)
         if (lane == 0) tc::mbar_arrive(&s_empty[ss]);
         // mask to -inf outside [klo, khi]; block max in log2 units
         float mb = -INFINITY;
-        if (k0 >= klo && k0 + 63 <= khi) {
+        if (__all_sync(0xffffffffu, k0 >= klo && k0 + 63 <= khi)) {  // warp-uniform (band edges cross warps)
 #pragma unroll
           for (int i = 0; i < 64; ++i) mb = fmaxf(mb, v[i]);
         } else {
