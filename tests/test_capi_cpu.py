@@ -17,7 +17,7 @@ G = os.path.join(ROOT, "tests", "golden")
 
 def declared():
     src = open(HDR).read()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*|unsigned long long|void)\s+(kl_\w+)\s*\(", src, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|const char\*|unsigned long long|long long|void)\s+(kl_\w+)\s*\(", src, re.M)))
 
 
 def test_header_declares_entry_points():
