@@ -613,7 +613,7 @@ def test_rote_golden(tag):
 
 @pytest.mark.parametrize("dtype", DTYPES)
 @pytest.mark.parametrize("mode", ["previous", "latest"])
-@pytest.mark.parametrize("B,T,d", [(5, 33, 16), (2, 4096, 512)])
+@pytest.mark.parametrize("B,T,d", [(5, 33, 16), (2, 4096, 512), (3, 37, 24), (4, 29, 12)])
 def test_rote_batched(dtype, mode, B, T, d):
     """Padded batch with per-sample lengths and timestamps vs the oracle per sample; padded rows pass through."""
     from oracle import ops
