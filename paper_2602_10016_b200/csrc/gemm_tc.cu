@@ -58,6 +58,8 @@ struct TcParams {
   int n_fast;          // tile order: N tiles of one M block adjacent (A read once from HBM)
   int wide;            // PAIR: 256 x 512 tiles — two N = 256 products per k step into one 512-column
                        // accumulator (no double buffer); each CTA stages 2 x 128 B columns
+  int r_glob;          // wide tiles with a residual: the epilogue warps read it from global memory,
+                       // coalesced, into their staging boxes (no producer-staged residual tiles)
 };
 
 constexpr int SLD = 66;  // epilogue staging row stride (floats): 64 columns + pad, 8-byte aligned
@@ -392,7 +394,7 @@ template <typename TC, bool FULL>
 __device__ __forceinline__ void epi_tma(const TcParams& p, const Epi& e, const CUtensorMap* tmC,
                                         const CUtensorMap* tmX, uint32_t tbase, uint8_t* stg, float* bsm, int mb,
                                         int nb, int zc2, int zc1, int lane_base, int lim, const uint8_t* Rs,
-                                        int& nbox, TC* X, int c_lo, int c_hi) {
+                                        int& nbox, TC* X, int c_lo, int c_hi, const TC* Rg) {
   // aux_mode 1 with a tensor map: the pre-activation is staged in the warp's
   // second box and TMA-stored beside C (one box pair in flight)
   const bool xtma = FULL && e.aux_mode == 1 && p.x_tma;
@@ -402,6 +404,23 @@ __device__ __forceinline__ void epi_tma(const TcParams& p, const Epi& e, const C
   const bool live = mb * BM + row < lim;
   // (FULL: the caller staged this tile's bias in bsm before the accumulator wait)
   uint8_t* buf = stg;
+  // Rg (bf16 C only): the residual of each 64-column box, loaded coalesced
+  // (8 rows x 128 B per warp instruction) one box ahead into registers, then
+  // put into the box's staging buffer, where each row thread adds it before
+  // writing its result over it
+  uint4 rnext[8];
+  auto r_load = [&](int cb) {
+    const int cc = lane & 7;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int R = (lane >> 3) + 4 * i, row = mb * BM + lane_base + R;
+      rnext[i] = row < p.M ? __ldg(reinterpret_cast<const uint4*>(Rg + (long long)row * p.r_rs + nb * p.BN + cb + 8 * cc))
+                           : make_uint4(0u, 0u, 0u, 0u);
+    }
+  };
+  if constexpr (sizeof(TC) == 2) {
+    if (Rg) r_load(c_lo);
+  }
 #pragma unroll 1
   for (int c = c_lo; c < c_hi; c += 32) {
     const int hb = (c >> 5) % SPB;
@@ -414,6 +433,17 @@ __device__ __forceinline__ void epi_tma(const TcParams& p, const Epi& e, const C
           tc::bulk_wait_read1();
       }
       __syncwarp();
+      if constexpr (sizeof(TC) == 2) {
+        if (Rg) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int R = (lane >> 3) + 4 * i, cc = lane & 7;
+            *reinterpret_cast<uint4*>(buf + R * 128 + ((cc ^ (R & 7)) << 4)) = rnext[i];
+          }
+          __syncwarp();
+          if (c + 64 < c_hi) r_load(c + 64);
+        }
+      }
     }
     float v[32];
     tc::tmem_ld32(tbase + c, v);
@@ -498,11 +528,26 @@ __device__ __forceinline__ void epi_tma(const TcParams& p, const Epi& e, const C
         }
       }
     }
+    uint8_t* rowp = buf + lane * 128;
+    if constexpr (sizeof(TC) == 2) {
+      if (Rg) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint4 u = *reinterpret_cast<const uint4*>(rowp + (((hb * 4 + q) ^ (lane & 7)) << 4));
+          const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[k]));
+            v[8 * q + 2 * k] += f.x;
+            v[8 * q + 2 * k + 1] += f.y;
+          }
+        }
+      }
+    }
     if (!live) {
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] = 0.f;
     }
-    uint8_t* rowp = buf + lane * 128;
     if constexpr (sizeof(TC) == 2) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -798,7 +843,8 @@ __global__ void __launch_bounds__(NTHREADS_WIDE, 1)
         uint8_t* ebuf = ch == 0 ? reinterpret_cast<uint8_t*>(stage_s) + (warp - 2) * 8192
                                 : sX + (warp - 6) * 8192;
         epi_tma<TC, MODE == 3>(p, e, &tmC, &tmX, tbase, ebuf, bsm - c_lo, mb, nb,
-                    p.c_has2 ? z2o : 0, p.c_has1 ? z1o : 0, lane_base, lim, Rs, nbox, X, ch * cw, ch * cw + cw);
+                    p.c_has2 ? z2o : 0, p.c_has1 ? z1o : 0, lane_base, lim, Rs, nbox, X, ch * cw, ch * cw + cw,
+                    p.r_glob ? R : nullptr);
       } else
       for (int c0 = 0; c0 < p.BN; c0 += 64) {
         // TMEM (thread = row) -> smem transpose -> each lane owns a column
@@ -1182,7 +1228,13 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
   // more than the operand bytes saved (QKV projection 199 -> 219 us), with 8:
   // QKV projection 208 -> 204 us, HSP dS (K = 640) 102 -> 86 us, QKV dX
   // (K = 1536) 188 -> 164 us, 8192^3 936 -> 700 us.
-  const bool wide = mode2 && !use_r && g.N % 512 == 0 && (g.M + BM - 1) / BM >= 2 && !getenv_flag_nopair() &&
+  // a residual (bf16 C, unit column stride, 16-byte rows: what use_r checked) is read by the wide
+  // epilogue itself (TcParams::r_glob) instead of producer-staged 128 KB tiles
+  // (the extra residual reads of the un-overlapped epilogue pay off only for long reductions:
+  // QKV dX, K = 1536, 211 -> 191 us; K = 512 / 640: 102 -> 116 / 112 -> 125 us)
+  const bool r_ok = !use_r || (g.r_cs == 1 && (g.r_rs % 8) == 0 && ((uintptr_t)g.R & 15) == 0 && k_tot >= 1536 &&
+                               !getenv("KL_GEMM_NOWIDE_R"));
+  const bool wide = mode2 && r_ok && g.N % 512 == 0 && (g.M + BM - 1) / BM >= 2 && !getenv_flag_nopair() &&
                     !getenv("KL_GEMM_NOWIDE") &&
                     ((accum_only0 && !pair && k_tot >= 8192) ||
                      (!accum_only0 && k_tot >= wide_min_k() &&
@@ -1192,6 +1244,10 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
     bn = 512;
     p.BN = 512;
     p.tiles_n = g.N / 512;
+    if (use_r) {
+      p.r_glob = 1;
+      use_r = false;
+    }
   }
   p.wide = wide ? 1 : 0;
   if (pair) {

@@ -12,7 +12,7 @@ def t(fn, n=10):
     e1.record(); torch.cuda.synchronize()
     return e0.elapsed_time(e1) / n
 torch.manual_seed(0)
-for (M, N, Kb, nb) in ((1536, 512, 4096, 32), (512, 512, 4096, 32), (1024, 1024, 4096, 8), (768, 512, 1000, 7)):
+for (M, N, Kb, nb) in ((1536, 512, 4096, 32), (512, 512, 4096, 32), (768, 256, 1024, 128), (256, 256, 1024, 128), (1024, 1024, 4096, 8), (768, 512, 1000, 7)):
     K = Kb * nb
     A3 = torch.randn(nb, Kb, M, device="cuda").bfloat16()   # dY rows -> A = dY^T (MN-major), batch-reduced
     B3 = torch.randn(nb, Kb, N, device="cuda").bfloat16()

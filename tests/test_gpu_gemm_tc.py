@@ -264,6 +264,17 @@ def test_tc_wide_pairs(a_k, b_n):
     act = torch.where(cols == 0, torch.nn.functional.silu(z), torch.relu(z))
     assert rel(pre, torch.where(keep, z, 0)) < 1e-2
     assert rel(out, torch.where(keep, act, 0)) < 1e-2
+    # residual (C = A B + R, bf16): read by the wide epilogue from global memory
+    R = torch.randn(2, M, N, device="cuda", generator=g).to(torch.bfloat16)
+    _capi.reset_path_hits()
+    outr = gemm(A, B, residual=R)
+    assert _capi.path_hits()["gemm_wide"] == 1
+    assert rel(outr, A.double() @ B.double() + R.double()) < 1e-2
+    # accumulate into a bf16 C (the dX form: C += A B)
+    C0 = torch.randn(2, M, N, device="cuda", generator=g).to(torch.bfloat16)
+    C = C0.clone()
+    gemm(A, B, C, beta=1.0)
+    assert rel(C, A.double() @ B.double() + C0.double()) < 1e-2
     # weight-gradient form: C (fp32) += sum_b A_b^T D_b
     D = operand((6, 4096, 512), True, g)
     X = operand((6, 4096, 1536), a_k, g)
