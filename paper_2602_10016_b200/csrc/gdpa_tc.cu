@@ -653,6 +653,7 @@ __global__ void __launch_bounds__(NT, 1)
 //         -> bf16 rows.
 constexpr int HK2 = 128;
 constexpr int NT5 = 320;                       // warp 0 TMA, 1 MMA, 2-9 epilogue
+constexpr int NT6 = 352;                       // + warp 10: the second operand loader (d = 512)
 constexpr int RST = 3;                         // forward ring stages (+ 16 KB epilogue staging)
 constexpr uint32_t FSTAGE = 2 * ATOM_S;        // S atom | Kt atom (128 rows x 64)
 constexpr uint32_t BSTAGE = 4 * ATOM_S;        // dY | Vt | S | Kt atoms
@@ -768,7 +769,7 @@ __device__ __forceinline__ void res_add_store_co(uint8_t* stg, const uint4* r4, 
   __syncwarp();
 }
 
-__global__ void __launch_bounds__(NT5, 1)
+__global__ void __launch_bounds__(NT6, 1)
     gdpa_fwd512_kernel(const __grid_constant__ CUtensorMap ts, const __grid_constant__ CUtensorMap tk,
                        const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tr32,
                        const __grid_constant__ CUtensorMap to32, const P5 p) {
@@ -858,16 +859,26 @@ __global__ void __launch_bounds__(NT5, 1)
         for (int a = 0; a < 4; ++a) tc::tma_load_3d(sV + a * ATOM_S, &tv, vs_full, (4 * h + a) * 64, 0, b);
         ++vc;
       };
-      if (i0 < i1) load_z(i0);
+      // Z stages only; the Vt halves come from warp 10, so the Z stream
+      // never waits behind the single Vt buffer's release by a Y product
+      (void)load_v;
       for (int k = i0; k < i1; ++k) {
         T5(k - i0, 0);
-        load_v(k, 0);
-        T5(k - i0, 1);
-        if (k + 1 < i1) load_z(k + 1);
+        load_z(k);
         T5(k - i0, 2);
-        load_v(k, 1);
-        T5(k - i0, 3);
       }
+    }
+  } else if (warp == 10) {
+    if (lane == 0) {
+      int vc = 0;
+      for (int k = i0; k < i1; ++k)
+        for (int h = 0; h < 2; ++h, ++vc) {
+          const int b = k / nT;
+          tc::mbar_wait(vs_empty, (vc & 1) ^ 1);
+          tc::mbar_arrive_expect_tx(vs_full, 4 * ATOM_S);
+#pragma unroll
+          for (int a = 0; a < 4; ++a) tc::tma_load_3d(sV + a * ATOM_S, &tv, vs_full, (4 * h + a) * 64, 0, b);
+        }
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -1047,7 +1058,7 @@ size_t fwd512_smem() { return 1024 + RST * FSTAGE + 4 * ATOM_S + 2 * ATOM_S + 8 
 //              touch 32 lines per warp instruction; quarter-width dS products
 //              free the shared memory for the staging tiles and let the next
 //              quarter's product overlap this quarter's epilogue.)
-__global__ void __launch_bounds__(NT5, 1)
+__global__ void __launch_bounds__(NT6, 1)
     gdpa_bwd512_kernel(const __grid_constant__ CUtensorMap ts, const __grid_constant__ CUtensorMap tg,
                        const __grid_constant__ CUtensorMap tk, const __grid_constant__ CUtensorMap tv,
                        const __grid_constant__ CUtensorMap tkq, const __grid_constant__ CUtensorMap tg32,
@@ -1131,6 +1142,16 @@ __global__ void __launch_bounds__(NT5, 1)
           tc::tma_load_3d(d + 2 * ATOM_S, &ts, &rs_full[st], a * 64, q0, b);
           tc::tma_load_3d(d + 3 * ATOM_S, &tk, &rs_full[st], a * 64, 0, b);
         }
+        (void)kc;
+      }
+    }
+  } else if (warp == 10) {
+    // the Kt column quarters (dS products' B operand): their own loader, so
+    // the next tile's (dY | Vt | S | Kt) stages never wait behind them
+    if (lane == 0) {
+      int kc = 0;
+      for (int k = i0; k < i1; ++k) {
+        const int b = k / nT;
         for (int q = 0; q < 4; ++q, ++kc) {
           tc::mbar_wait(ks_empty, (kc & 1) ^ 1);
           tc::mbar_arrive_expect_tx(ks_full, 2 * ATOM_S);
@@ -1463,7 +1484,7 @@ static int gdpa_fwd512_launch(const kl_gdpa_args* a, const gdpa::P& p, cudaStrea
   const int W = a->B * ((a->T + gdpa::TB - 1) / gdpa::TB);
   int grid = std::min(W, tc_num_sms());
   if (const char* g = getenv("KL_GDPA_GRID")) grid = std::max(1, std::min(grid, atoi(g)));  // testing: multi-tile CTAs
-  launch_k(gdpa::gdpa_fwd512_kernel, grid, gdpa::NT5, smem, s, ts, tk, tv, tr32, to32, q);
+  launch_k(gdpa::gdpa_fwd512_kernel, grid, gdpa::NT6, smem, s, ts, tk, tv, tr32, to32, q);
   count_launch();
   count_path(KL_PATH_GDPA_FWD_TC512);
   return launch_check("gdpa_fwd512_tc");
@@ -1511,7 +1532,7 @@ static int gdpa_bwd512_launch(const kl_gdpa_args* a, const gdpa::P& p, cudaStrea
   const int W = a->B * ((a->T + gdpa::TB - 1) / gdpa::TB);
   int grid = std::min(W, tc_num_sms());
   if (const char* g = getenv("KL_GDPA_GRID")) grid = std::max(1, std::min(grid, atoi(g)));  // testing: multi-tile CTAs
-  launch_k(gdpa::gdpa_bwd512_kernel, grid, gdpa::NT5, smem, s, ts, tg, tk, tv, tkq, tg32, to32, tz32, ta32, q);
+  launch_k(gdpa::gdpa_bwd512_kernel, grid, gdpa::NT6, smem, s, ts, tg, tk, tv, tkq, tg32, to32, tz32, ta32, q);
   count_launch();
   count_path(KL_PATH_GDPA_BWD_TC512);
   return launch_check("gdpa_bwd512_tc");
