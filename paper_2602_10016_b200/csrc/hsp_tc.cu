@@ -949,7 +949,6 @@ size_t fwd512_smem() { return 1024 + ZST * ZSTAGE + 4 * ATOM + 2 * ATOM + (2 * Z
 // was slower: its N = 64 score products run at 2/3 rate and the shared
 // memory left for the S stream holds one block, so TMA latency paced it.)
 constexpr int PARTF = 256 * 128 + 2 * 128;  // partial: O [col][row] fp32, max (log2), sum
-constexpr int ZSTB = 5;                     // balanced kernel: (Qt atom | S atom) ring stages
 constexpr int NTB = 224;                    // balanced kernel: + warp 6, the O operand loader
 
 struct SplitP {
@@ -996,15 +995,13 @@ __global__ void __launch_bounds__(NTB, 1)
   constexpr uint32_t IDESC_O = tc::idesc_bf16(TB, DH, 0, 1);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  // P stays in TMEM (bf16 pairs written over its own Z buffer, the A operand
-  // of the O product): the 32 KB of shared memory a P tile took is a fifth
-  // (Qt atom | S atom) ring stage
-  uint8_t* sZ = sm;                       // ZSTB x (Qt atom | S atom)
-  uint8_t* sO = sZ + ZSTB * ZSTAGE;       // 4 S atoms (half h of block j)
-  uint64_t* bar = (uint64_t*)(sO + 4 * ATOM);
-  uint64_t* zs_full = bar;                // [ZSTB]
-  uint64_t* zs_empty = bar + ZSTB;        // [ZSTB]
-  uint64_t* os_full = bar + 2 * ZSTB;
+  uint8_t* sZ = sm;                       // ZST x (Qt atom | S atom)
+  uint8_t* sO = sZ + ZST * ZSTAGE;        // 4 S atoms (half h of block j)
+  uint8_t* sP = sO + 4 * ATOM;            // 128 x 128 bf16
+  uint64_t* bar = (uint64_t*)(sP + 2 * ATOM);
+  uint64_t* zs_full = bar;                // [ZST]
+  uint64_t* zs_empty = bar + ZST;         // [ZST]
+  uint64_t* os_full = bar + 2 * ZST;
   uint64_t* os_empty = os_full + 1;
   uint64_t* z_full = os_full + 2;         // [2]
   uint64_t* z_empty = os_full + 4;        // [2]
@@ -1022,7 +1019,7 @@ __global__ void __launch_bounds__(NTB, 1)
   if (warp == 0 && lane == 0) {
     tc::prefetch_tmap(&tmS);
     tc::prefetch_tmap(&tmQ);
-    for (int i = 0; i < ZSTB; ++i) {
+    for (int i = 0; i < ZST; ++i) {
       tc::mbar_init(&zs_full[i], 1);
       tc::mbar_init(&zs_empty[i], 1);
     }
@@ -1053,15 +1050,15 @@ __global__ void __launch_bounds__(NTB, 1)
   if (warp == 0) {
     // Z operand stages only: the O operand (half h of each S block) has its own
     // loader (warp 6), so the Z stream never waits for the single O buffer to
-    // be released by the previous block's O product
+    // be released by the previous block's O product (264 -> 220 us at c4)
     if (lane == 0) {
       int zc = 0;
       walk_segments(p, g, P0, P1, [&](int b, int j0, int j1, bool, bool, int) {
         for (int j = j0; j < j1; ++j) {
 #pragma unroll 1
           for (int a = 0; a < NA; ++a, ++zc) {
-            const int st = zc % ZSTB;
-            tc::mbar_wait(&zs_empty[st], ((zc / ZSTB) & 1) ^ 1);
+            const int st = zc % ZST;
+            tc::mbar_wait(&zs_empty[st], ((zc / ZST) & 1) ^ 1);
             tc::mbar_arrive_expect_tx(&zs_full[st], ZSTAGE);
             tc::tma_load_3d(sZ + st * ZSTAGE, &tmQ, &zs_full[st], a * 64, qt * TB, g);
             tc::tma_load_3d(sZ + st * ZSTAGE + ATOM, &tmS, &zs_full[st], a * 64, j * TB, b);
@@ -1084,15 +1081,15 @@ __global__ void __launch_bounds__(NTB, 1)
   } else if (warp == 1) {
     if (lane == 0 && P0 < P1) {
       int zc = 0, zb = 0, oc = 0, pc = 0, t = 0;
-      const uint32_t z0 = tc::smem_u32(sZ), oa = tc::smem_u32(sO);
+      const uint32_t z0 = tc::smem_u32(sZ), oa = tc::smem_u32(sO), pa = tc::smem_u32(sP);
       auto mma_z = [&]() {  // the next Z block into buffer zb & 1
         const int z = zb & 1;
         tc::mbar_wait(&z_empty[z], ((zb >> 1) & 1) ^ 1);
         tc::fence_after();
 #pragma unroll 1
         for (int a = 0; a < NA; ++a, ++zc) {
-          const int st = zc % ZSTB;
-          tc::mbar_wait(&zs_full[st], (zc / ZSTB) & 1);
+          const int st = zc % ZST;
+          tc::mbar_wait(&zs_full[st], (zc / ZST) & 1);
           tc::fence_after();
           const uint32_t qa = z0 + st * ZSTAGE, sa = qa + ATOM;
 #pragma unroll
@@ -1114,8 +1111,7 @@ __global__ void __launch_bounds__(NTB, 1)
           tc::fence_after();
 #pragma unroll
           for (int kk = 0; kk < TB / 16; ++kk)
-            tc::mma_bf16_ts(tmem + T_O, tmem + (pc & 1) * TB + kk * 8, dmn(oa, kk), IDESC_O,
-                            (j > j0 || kk > 0) ? 1u : 0u);
+            tc::mma_bf16(tmem + T_O, dk(pa, kk), dmn(oa, kk), IDESC_O, (j > j0 || kk > 0) ? 1u : 0u);
           tc::mma_commit(p_empty);
           tc::mma_commit(os_empty);
           ++pc;
@@ -1170,14 +1166,10 @@ __global__ void __launch_bounds__(NTB, 1)
           }
         }
         mb *= LOG2E;
+        tc::mbar_wait(p_empty, (pc & 1) ^ 1);  // O of the previous block is complete (and P is free)
+        tc::fence_after();
         const bool up = mb > mref + RESCALE;
         if (j > j0 && __any_sync(0xffffffffu, up)) {
-          // O must be stable: wait for the previous block's O product (O of the
-          // block before it completed before this block's Z did — in-order
-          // tensor pipe — so the parity wait is unambiguous).  Without a
-          // rescale nothing waits: P goes to this block's own TMEM buffer.
-          tc::mbar_wait(p_empty, (pc & 1) ^ 1);
-          tc::fence_after();
           const float al = up ? ex2(mref - mb) : 1.f;
           l *= al;
 #pragma unroll 1
@@ -1203,7 +1195,7 @@ __global__ void __launch_bounds__(NTB, 1)
             l += a + bq;
             pk[i >> 1] = tc::pack_bf16(a, bq);
           }
-          tc::tmem_st16(tz + (c0 >> 1), pk);  // over Z columns this pass has already read
+          store_sw(sP, r, c0, pk);
         }
         tc::fence_async_smem();
         tc::fence_before();
@@ -1313,7 +1305,7 @@ __global__ void __launch_bounds__(NTB, 1)
   if (warp == 1) tc::tmem_dealloc(tmem, 512);
 }
 
-size_t fwd512b_smem() { return 1024 + ZSTB * ZSTAGE + 4 * ATOM + (2 * ZSTB + 10) * 8 + 32; }
+size_t fwd512b_smem() { return fwd512_smem() + 16; }
 
 // Backward (d = 512), persistent CTAs over (sample, 128-row S block) items,
 // looping over the query tiles; the S block stays resident (8 atoms) and the

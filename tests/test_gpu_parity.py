@@ -852,3 +852,33 @@ def test_multi_head_attention_arbitrary_mask_vs_oracle(dtype):
     assert err(q_t.grad, dxq) < TOL[dtype]
     assert err(kv_t.grad, dxkv) < TOL[dtype]
     check_grads(P.grad, gr, dtype)
+
+
+def test_hsp512_long_sequence_repeat():
+    """The balanced d = 512 pooling forward at a bench-length sequence (T = 4096,
+    32 key blocks per sample, every query tile / half lane split over many
+    CTAs), three launches, against a torch fp32 evaluation: a pipeline race
+    in a variant that kept P in TMEM only showed up here (and as NaN in the
+    bench's training steps), not at the short parity shapes."""
+    from paper_2602_10016_b200 import _capi
+    from paper_2602_10016_b200 import functional as F
+
+    torch.manual_seed(3)
+    B, T, d, HQ = 6, 4096, 512, 320
+    # score magnitudes growing along the sequence: the running max moves on
+    # most key blocks, so the online-softmax rescale path runs constantly
+    ramp = (1.0 + torch.arange(T, device="cuda") / 512.0)[None, :, None]
+    S = (torch.randn(B, T, d, device="cuda") / d ** 0.5 * ramp).bfloat16()
+    Q = torch.randn(HQ, d, device="cuda") * 2.0
+    lengths = torch.tensor([T, T, 3000, 1, 0, T - 77], dtype=torch.int32, device="cuda")
+    Z = torch.einsum("qd,btd->bqt", Q.bfloat16().float(), S.float())
+    mask = torch.arange(T, device="cuda")[None, None, :] < lengths[:, None, None].long()
+    P = torch.softmax(Z.masked_fill(~mask, float("-inf")), dim=-1).nan_to_num(0.0)
+    ref = torch.einsum("bqt,btd->bqd", P, S.float())
+    for _ in range(3):
+        _capi.reset_path_hits()
+        o1, o2 = F.hsp_pool(S, Q, lengths, splits=(256, 64))
+        assert _capi.path_hits()["hsp_fwd_split"] > 0
+        out = torch.cat([o1.float(), o2.float()], dim=1)
+        assert torch.isfinite(out).all()
+        assert ((out - ref).abs().max() / ref.abs().max()).item() < 2e-2
