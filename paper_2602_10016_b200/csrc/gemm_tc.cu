@@ -997,6 +997,12 @@ static int r_wide_kb() {  // KL_GEMM_RWIDE_KB: min k-blocks for 256-wide residua
   return v;
 }
 
+static double ws_penalty() {  // KL_GEMM_WS_PENALTY: cost (clk) of the split-K reduce pass's extra launch (A/B)
+  static double v = -1.0;
+  if (v < 0) v = getenv("KL_GEMM_WS_PENALTY") ? atof(getenv("KL_GEMM_WS_PENALTY")) : 2000.0;
+  return v;
+}
+
 static int wide_min_k() {  // KL_GEMM_WIDE_K: shortest reduction of a stored-output wide GEMM (A/B)
   static int v = -1;
   if (v < 0) v = getenv("KL_GEMM_WIDE_K") ? atoi(getenv("KL_GEMM_WIDE_K")) : 512;
@@ -1118,7 +1124,7 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
       const long long waves = (tiles * sp + num_sms() - 1) / num_sms();
       const double per_k = std::max(128.0 * b / 2780.0, (128.0 + b) * 2.0 / 64.0);
       double cost = (double)waves * ((double)k_tot / sp * per_k + 500.0 + 4.0 * b);
-      if (wsp) cost += (double)n_out0 * g.M * g.N * 4.0 * (sp + 1) / 3100.0 + 2000.0;
+      if (wsp) cost += (double)n_out0 * g.M * g.N * 4.0 * (sp + 1) / 3100.0 + ws_penalty();
       if (best < 0 || cost < best * 0.97) {  // ties -> the wider tile
         best = cost;
         bn = b;
