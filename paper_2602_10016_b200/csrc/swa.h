@@ -18,6 +18,7 @@ struct SwaP {
   void* dQKV;
   float* Dbuf;
   unsigned long long* trace = nullptr;  // debug: CTA 0's pipeline clock stamps (KL_SWA_TRACE), dK / dV kernel
+  int dq_rowdot = 0;  // dQ v3 kernel: form D = rowsum(dO * O) itself (O tiles by TMA) and write Dbuf
 };
 
 int swa_fwd_simt(const SwaP& p, cudaStream_t s);

@@ -1885,13 +1885,16 @@ constexpr float RESCALE2 = 8.f;  // lazy-rescale threshold (log2 units)
 
 __global__ void __launch_bounds__(NT3, 1)
     swa_bwd_dq_tc3_kernel(const __grid_constant__ CUtensorMap tqg, const __grid_constant__ CUtensorMap tdo,
-                          const __grid_constant__ CUtensorMap tkv64, SwaP p) {
+                          const __grid_constant__ CUtensorMap tkv64, const __grid_constant__ CUtensorMap to, SwaP p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sQG = sm;                    // 2 x (Q 16 KB | dO 16 KB)
   uint8_t* sKV = sQG + 2 * 2 * TILE;    // KR x (K 8 KB | V 8 KB)
   uint8_t* sDS = sKV + KR * 2 * HTILE;  // 2 x dS 16 KB (one per warpgroup)
-  uint64_t* bar = (uint64_t*)(sDS + 2 * PH);
+  // p.dq_rowdot: 2 x O 16 KB (the tile's O rows: D = rowsum(dO * O) is formed
+  // here, replacing the separate row-dot pass over O and dO)
+  uint8_t* sO = sDS + 2 * PH;
+  uint64_t* bar = (uint64_t*)(sO + (p.dq_rowdot ? 2 * TILE : 0));
   uint64_t* qg_full = bar;                 // [2]
   uint64_t* qg_empty = bar + 2;            // [2]
   uint64_t* kv_full = bar + 4;             // [KR]
@@ -1902,7 +1905,8 @@ __global__ void __launch_bounds__(NT3, 1)
   uint64_t* ds_empty = ds_full + 2;        // [2]
   uint64_t* acc_full = ds_empty + 2;
   uint64_t* acc_empty = acc_full + 1;
-  uint32_t* tslot = (uint32_t*)(acc_empty + 1);
+  uint64_t* o_empty = acc_empty + 1;       // [2] (p.dq_rowdot)
+  uint32_t* tslot = (uint32_t*)(o_empty + 2);
 
   const int nT = (p.T + TB - 1) / TB;
   const int W = p.B * p.H * nT;
@@ -1915,11 +1919,13 @@ __global__ void __launch_bounds__(NT3, 1)
     tc::prefetch_tmap(&tqg);
     tc::prefetch_tmap(&tdo);
     tc::prefetch_tmap(&tkv64);
+    if (p.dq_rowdot) tc::prefetch_tmap(&to);
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&qg_full[i], 1);
       tc::mbar_init(&qg_empty[i], 1);
       tc::mbar_init(&ds_full[i], 4);
       tc::mbar_init(&ds_empty[i], 1);
+      tc::mbar_init(&o_empty[i], 8);
     }
     for (int i = 0; i < KR; ++i) {
       tc::mbar_init(&kv_full[i], 1);
@@ -1950,9 +1956,11 @@ __global__ void __launch_bounds__(NT3, 1)
         const Tile& tl = w.tl;
         const int qb = w.t & 1;
         tc::mbar_wait(&qg_empty[qb], ((w.t >> 1) & 1) ^ 1);
-        tc::mbar_arrive_expect_tx(&qg_full[qb], 2 * TILE);
+        if (p.dq_rowdot) tc::mbar_wait(&o_empty[qb], ((w.t >> 1) & 1) ^ 1);
+        tc::mbar_arrive_expect_tx(&qg_full[qb], (p.dq_rowdot ? 3 : 2) * TILE);
         tc::tma_load_3d(sQG + qb * 2 * TILE, &tqg, &qg_full[qb], tl.h * DH, tl.k0, tl.b);
         tc::tma_load_3d(sQG + qb * 2 * TILE + TILE, &tdo, &qg_full[qb], tl.h * DH, tl.k0, tl.b);
+        if (p.dq_rowdot) tc::tma_load_3d(sO + qb * TILE, &to, &qg_full[qb], tl.h * DH, tl.k0, tl.b);
         for (int j = tl.lo; j < tl.lo + tl.n; ++j) {
           const int li = load_index(w, j);
           if (li < loaded) continue;  // kept from the previous query block
@@ -2058,7 +2066,7 @@ __global__ void __launch_bounds__(NT3, 1)
       const int q = min(tl.k0 + r, p.T - 1);
       const long long off = ((long long)tl.b * p.H + tl.h) * p.T + q;
       l2 = p.LSE[off];
-      dr = p.Dbuf[off];
+      dr = p.dq_rowdot ? 0.f : p.Dbuf[off];
     };
     Walk pw = w;
     walk_fill<true>(p, pw);
@@ -2077,7 +2085,35 @@ __global__ void __launch_bounds__(NT3, 1)
         continue;
       }
       const bool qin = tl.k0 + r < tl.len;
-      const float lse2 = qin ? nl * 1.4426950408889634f : 0.f, dr = qin ? nd : 0.f;
+      float drow = nd;
+      if (p.dq_rowdot) {
+        // D = rowsum(dO * O) of this row from the tile's smem copies (SW128
+        // K-major rows of 128 B); both warpgroups form it, warpgroup 0 stores it
+        // for the dK / dV kernel, which runs after this one
+        const int qb = t & 1;
+        tc::mbar_wait(&qg_full[qb], (t >> 1) & 1);
+        const uint8_t* go = sQG + qb * 2 * TILE + TILE + r * 128;
+        const uint8_t* oo = sO + qb * TILE + r * 128;
+        float acc = 0.f;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const int off = (c ^ (r & 7)) << 4;
+          const uint4 gu = *reinterpret_cast<const uint4*>(go + off);
+          const uint4 ou = *reinterpret_cast<const uint4*>(oo + off);
+          const uint32_t gw[4] = {gu.x, gu.y, gu.z, gu.w}, ow[4] = {ou.x, ou.y, ou.z, ou.w};
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&gw[i]));
+            const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ow[i]));
+            acc = fmaf(a.x, b.x, fmaf(a.y, b.y, acc));
+          }
+        }
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&o_empty[qb]);
+        drow = acc;
+        if (wg == 0 && tl.k0 + r < p.T) p.Dbuf[((long long)tl.b * p.H + tl.h) * p.T + tl.k0 + r] = acc;
+      }
+      const float lse2 = qin ? nl * 1.4426950408889634f : 0.f, dr = qin ? drow : 0.f;
       pw = w;
       do {
         walk_adv(p, pw);
@@ -2159,7 +2195,7 @@ __global__ void __launch_bounds__(NT3, 1)
   if (warp == 1) tc::tmem_dealloc(tmem, 512);
 }
 
-size_t dq_smem_bytes() { return 1024 + 2 * 2 * TILE + KR * 2 * HTILE + 2 * PH + (4 + 2 * KR + 6 + 4 + 2) * 8 + 16; }
+size_t dq_smem_bytes() { return 1024 + 2 * 2 * TILE + KR * 2 * HTILE + 2 * PH + 2 * TILE + (4 + 2 * KR + 6 + 4 + 2 + 2) * 8 + 16; }
 
 // ---------------------------------------------------------------------------
 // Forward v3: 128-query tiles, 64-key half-block items, online softmax with
@@ -2495,8 +2531,16 @@ int swa_bwd_tc(const SwaP& p, cudaStream_t s) {
   CUtensorMap tq, tdo;
   if (!map3(&tq, p.QKV, 3LL * p.H * DH, p.T, p.B, p.ld_qkv, p.bs_qkv)) return KL_EUNSUPPORTED;
   if (!map3(&tdo, p.dO, (long long)p.H * DH, p.T, p.B, p.ld_o, p.bs_o)) return KL_EUNSUPPORTED;
-  int rc = swa_rowdot(p, s);
-  if (rc) return rc;
+  // default v3 path: the dQ kernel forms D = rowsum(dO * O) itself and runs
+  // first (the dK / dV kernel reads D); other paths keep the row-dot pass
+  const bool fuse_d = !getenv("KL_SWA_BWD_V1") && !getenv("KL_SWA_DKV_V2") && !getenv("KL_SWA_DQ_V2") &&
+                      !getenv("KL_SWA_ROWDOT");
+  CUtensorMap to;
+  const bool to_ok = fuse_d && map3(&to, p.O, (long long)p.H * DH, p.T, p.B, p.ld_o, p.bs_o);
+  if (!to_ok) {
+    int rc = swa_rowdot(p, s);
+    if (rc) return rc;
+  }
   SwaP pt = p;
   if (const char* tv = getenv("KL_SWA_TRACE")) pt.trace = (unsigned long long*)strtoull(tv, nullptr, 0);  // testing
   if (!getenv("KL_SWA_BWD_V1")) {
@@ -2505,7 +2549,14 @@ int swa_bwd_tc(const SwaP& p, cudaStream_t s) {
     const size_t s2 = v2::dq_smem_bytes();
     static int dkv_v = -1;
     if (dkv_v < 0) dkv_v = getenv("KL_SWA_DKV_V2") ? 2 : 3;
-    CUtensorMap tq64, tdo64;
+    CUtensorMap tq64, tdo64, tkv64;
+    if (to_ok && map3(&tkv64, p.QKV, 3LL * p.H * DH, p.T, p.B, p.ld_qkv, p.bs_qkv, 64)) {
+      SwaP pq = p;
+      pq.dq_rowdot = 1;
+      const size_t s3 = v3::dq_smem_bytes();
+      cudaFuncSetAttribute(v3::swa_bwd_dq_tc3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s3);
+      launch_k(v3::swa_bwd_dq_tc3_kernel, grid, v3::NT3, s3, s, tq, tdo, tkv64, to, pq);
+    }
     if (dkv_v == 3 && map3(&tq64, p.QKV, 3LL * p.H * DH, p.T, p.B, p.ld_qkv, p.bs_qkv, 64) &&
         map3(&tdo64, p.dO, (long long)p.H * DH, p.T, p.B, p.ld_o, p.bs_o, 64)) {
       const size_t s1 = v3::dkv_smem_bytes();
@@ -2516,11 +2567,12 @@ int swa_bwd_tc(const SwaP& p, cudaStream_t s) {
       cudaFuncSetAttribute(v2::swa_bwd_dkv_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1);
       launch_k(v2::swa_bwd_dkv_tc2_kernel, grid, v2::NT2, s1, s, tq, tdo, p);
     }
-    CUtensorMap tkv64;
-    if (!getenv("KL_SWA_DQ_V2") && map3(&tkv64, p.QKV, 3LL * p.H * DH, p.T, p.B, p.ld_qkv, p.bs_qkv, 64)) {
+    if (to_ok) {
+      // dQ already ran (it formed D)
+    } else if (!getenv("KL_SWA_DQ_V2") && map3(&tkv64, p.QKV, 3LL * p.H * DH, p.T, p.B, p.ld_qkv, p.bs_qkv, 64)) {
       const size_t s3 = v3::dq_smem_bytes();
       cudaFuncSetAttribute(v3::swa_bwd_dq_tc3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s3);
-      launch_k(v3::swa_bwd_dq_tc3_kernel, grid, v3::NT3, s3, s, tq, tdo, tkv64, p);
+      launch_k(v3::swa_bwd_dq_tc3_kernel, grid, v3::NT3, s3, s, tq, tdo, tkv64, tkv64, p);
     } else {
       cudaFuncSetAttribute(v2::swa_bwd_dq_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2);
       launch_k(v2::swa_bwd_dq_tc2_kernel, grid, v2::NT2, s2, s, tq, tdo, p);
