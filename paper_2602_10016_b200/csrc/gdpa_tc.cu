@@ -835,13 +835,12 @@ __global__ void __launch_bounds__(NT6, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      // Load order (matches the MMA issue order, which computes the next
-      // tile's Z before this tile's Y halves): Z stages of the first tile;
-      // then per tile k: Vt half 0 of k, Z stages of k + 1, Vt half 1 of k.
-      int rc = 0, vc = 0;
+      // Z operand stages (S atom | Kt atom) only; the Vt halves come from
+      // warp 10, so the Z stream never waits behind the single Vt buffer's
+      // release by a Y product
+      int rc = 0;
       auto load_z = [&](int k) {
         const int b = k / nT, q0 = (k % nT) * TB;
-
 #pragma unroll 1
         for (int a = 0; a < 8; ++a, ++rc) {
           const int st = rc % RST;
@@ -851,17 +850,6 @@ __global__ void __launch_bounds__(NT6, 1)
           tc::tma_load_3d(sR + st * FSTAGE + ATOM_S, &tk, &rs_full[st], a * 64, 0, b);
         }
       };
-      auto load_v = [&](int k, int h) {
-        const int b = k / nT;
-        tc::mbar_wait(vs_empty, (vc & 1) ^ 1);
-        tc::mbar_arrive_expect_tx(vs_full, 4 * ATOM_S);
-#pragma unroll
-        for (int a = 0; a < 4; ++a) tc::tma_load_3d(sV + a * ATOM_S, &tv, vs_full, (4 * h + a) * 64, 0, b);
-        ++vc;
-      };
-      // Z stages only; the Vt halves come from warp 10, so the Z stream
-      // never waits behind the single Vt buffer's release by a Y product
-      (void)load_v;
       for (int k = i0; k < i1; ++k) {
         T5(k - i0, 0);
         load_z(k);
@@ -951,7 +939,7 @@ __global__ void __launch_bounds__(NT6, 1)
       const int b = k / nT, q0 = (k % nT) * TB;
       int len = __ldg(&p.lengths[b]);
       asm volatile("" : "+r"(len));
-      const bool live = q0 + r < len, inb = q0 + r < p.T;
+      const bool live = q0 + r < len;
       const int z = zc & 1;
       tc::mbar_wait(&z_full[z], (zc >> 1) & 1);
       if (threadIdx.x == 64) T5(k - i0, 9);
@@ -986,7 +974,6 @@ __global__ void __launch_bounds__(NT6, 1)
       const int row0 = q0 + qtr * 32;
       uint8_t* stg = sStg + (warp - 2) * 4096;
       uint64_t* rb = &rbar[warp - 2];
-      (void)inb;
       auto res_issue = [&](int col0) {
         if (lane == 0) {
           tc::bulk_wait_read0();  // the previous tile's TMA store has read the staging tile
@@ -1128,7 +1115,7 @@ __global__ void __launch_bounds__(NT6, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      int rc = 0, kc = 0;
+      int rc = 0;
       for (int k = i0; k < i1; ++k) {
         const int b = k / nT, q0 = (k % nT) * TB;
 #pragma unroll 1
@@ -1142,7 +1129,6 @@ __global__ void __launch_bounds__(NT6, 1)
           tc::tma_load_3d(d + 2 * ATOM_S, &ts, &rs_full[st], a * 64, q0, b);
           tc::tma_load_3d(d + 3 * ATOM_S, &tk, &rs_full[st], a * 64, 0, b);
         }
-        (void)kc;
       }
     }
   } else if (warp == 10) {
