@@ -60,6 +60,7 @@ struct TcParams {
                        // accumulator (no double buffer); each CTA stages 2 x 128 B columns
   int r_glob;          // wide tiles with a residual: the epilogue warps read it from global memory,
                        // coalesced, into their staging boxes (no producer-staged residual tiles)
+  int epi_regs_off;    // KL_GEMM_EPI_REGS=0: wide bf16 tiles drain TMEM through epi_tma (A/B testing)
 };
 
 constexpr int SLD = 66;  // epilogue staging row stride (floats): 64 columns + pad, 8-byte aligned
@@ -585,6 +586,79 @@ __device__ __forceinline__ void epi_tma(const TcParams& p, const Epi& e, const C
   if (FULL && e.bias) __syncwarp();  // bsm rewritten for the next tile
 }
 
+// Wide tiles, bf16 C without bias / activation / residual: the accumulator
+// is released BEFORE the TMA stores, so the next tile's MMAs overlap this
+// tile's stores (a wide tile's 512 columns fill TMEM: there is no second
+// accumulator to overlap with).  The warp's 256 columns: the first 128 are
+// packed straight into its two staging boxes, the last 128 into 64 registers
+// (10 warps cap a thread at 168 registers); then the accumulator barrier,
+// then four box stores.
+template <typename TC>
+__device__ __forceinline__ void epi_wide_regs(const TcParams& p, const Epi& e, const CUtensorMap* tmC, uint32_t tbase,
+                                              uint8_t* stg, int mb, int nb, int zc2, int zc1, int lane_base, int lim,
+                                              int& nbox, int c_lo, uint32_t tempty_leader) {
+  const int lane = threadIdx.x & 31;
+  const bool live = mb * BM + lane_base + lane < lim;
+  if (lane == 0) tc::bulk_wait_read0();  // the previous tile's boxes
+  __syncwarp();
+  uint32_t pk[64];
+  auto put = [&](int s, const uint32_t* r) {
+    uint32_t w[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      w[i] = live ? tc::pack_bf16(__uint_as_float(r[2 * i]) * e.alpha, __uint_as_float(r[2 * i + 1]) * e.alpha) : 0u;
+    if (s < 8) {
+      uint8_t* row = stg + (s >> 2) * 4096 + lane * 128;
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+        *reinterpret_cast<uint4*>(row + ((((s & 3) * 2 + q) ^ (lane & 7)) << 4)) =
+            make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) pk[8 * (s - 8) + i] = w[i];
+    }
+  };
+#pragma unroll
+  for (int s = 0; s < 16; s += 2) {  // 16-column loads, two in flight per wait
+    uint32_t r0[16], r1[16];
+    tc::tmem_ld16_nowait(tbase + c_lo + 16 * s, r0);
+    tc::tmem_ld16_nowait(tbase + c_lo + 16 * s + 16, r1);
+    tc::tmem_wait_ld();
+    tc::reg_fence<16>(r0);
+    tc::reg_fence<16>(r1);
+    put(s, r0);
+    put(s + 1, r1);
+  }
+  tc::fence_before();
+  tc::fence_async_smem();
+  __syncwarp();
+  const int gr = mb * BM + lane_base, gc = nb * p.BN + c_lo;
+  if (lane == 0) {
+    tc::mbar_arrive_cluster(tempty_leader);
+    tc::tma_store_4d(tmC, stg, gc, gr, zc2, zc1);
+    tc::bulk_commit();
+    tc::tma_store_4d(tmC, stg + 4096, gc + 64, gr, zc2, zc1);
+    tc::bulk_commit();
+  }
+#pragma unroll
+  for (int b = 0; b < 2; ++b) {
+    uint8_t* buf = stg + b * 4096;
+    if (lane == 0) tc::bulk_wait_read1();
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      *reinterpret_cast<uint4*>(buf + lane * 128 + ((q ^ (lane & 7)) << 4)) =
+          make_uint4(pk[32 * b + 4 * q], pk[32 * b + 4 * q + 1], pk[32 * b + 4 * q + 2], pk[32 * b + 4 * q + 3]);
+    tc::fence_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      tc::tma_store_4d(tmC, buf, gc + 128 + 64 * b, gr, zc2, zc1);
+      tc::bulk_commit();
+    }
+  }
+  nbox += 4;
+}
+
 // MODE 0: plain store, 1: generic epilogue (lane = column pair), 2/3: TMA-store
 // epilogue (thread = row; see epi_tma) without / with bias and activations.
 // PAIR: a CTA pair (cluster of 2, cta_group::2) computes a 256 x BN tile —
@@ -842,6 +916,11 @@ __global__ void __launch_bounds__(NTHREADS_WIDE, 1)
         // staged in dynamic shared memory after the operand ring
         uint8_t* ebuf = ch == 0 ? reinterpret_cast<uint8_t*>(stage_s) + (warp - 2) * 8192
                                 : sX + (warp - 6) * 8192;
+        if (MODE == 2 && PAIR && sizeof(TC) == 2 && p.wide && !p.reduce_c && !Rs && !p.r_glob && !p.epi_regs_off) {
+          epi_wide_regs<TC>(p, e, &tmC, tbase, ebuf, mb, nb, p.c_has2 ? z2o : 0, p.c_has1 ? z1o : 0, lane_base,
+                            lim, nbox, ch * cw, tc::mapa(&tempty[acc], 0));
+          continue;  // accumulator already released
+        }
         epi_tma<TC, MODE == 3>(p, e, &tmC, &tmX, tbase, ebuf, bsm - c_lo, mb, nb,
                     p.c_has2 ? z2o : 0, p.c_has1 ? z1o : 0, lane_base, lim, Rs, nbox, X, ch * cw, ch * cw + cw,
                     p.r_glob ? R : nullptr);
@@ -1325,6 +1404,11 @@ int gemm_tc(const GemmDesc& g0, const Epi& e0, cudaStream_t s) {
       p.ws = nullptr;
       p.splits = accum_only0 ? std::max(1, std::min(num_sms() / 2 / std::max(tiles, 1), iters / 4)) : 1;
     }
+  }
+  {
+    static int off = -1;
+    if (off < 0) off = (getenv("KL_GEMM_EPI_REGS") && getenv("KL_GEMM_EPI_REGS")[0] == '0') ? 1 : 0;
+    p.epi_regs_off = off;
   }
   const int total = tiles * p.splits;
   const int grid = pair ? 2 * std::min(total, num_sms() / 2) : std::min(total, num_sms());
