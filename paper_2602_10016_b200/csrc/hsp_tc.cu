@@ -392,12 +392,15 @@ struct BwdP {
   int acc_ds;
   bf16* dZ;  // (B, HQ, T)
   bf16* dZlo;
+  int z_tma;   // dZ (hi) rows TMA-stored from the swizzled P/dZ tile (tmZ; T % 8 == 0)
+  int ds_tma;  // dS rows staged through that tile and TMA-stored (tmD; not when accumulating)
 };
 
 template <int D>
 __global__ void __launch_bounds__(NT, 1)
     hsp_bwd_kernel(const __grid_constant__ CUtensorMap tmS, const __grid_constant__ CUtensorMap tmQ,
-                   const __grid_constant__ CUtensorMap tmG, BwdP p) {
+                   const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmZ,
+                   const __grid_constant__ CUtensorMap tmD, BwdP p) {
   constexpr int NA = D / 64;
   constexpr uint32_t BLK = NA * ATOM;
   constexpr uint32_t IDESC_Z = tc::idesc_bf16(TB, TB, 0, 0);
@@ -557,6 +560,10 @@ __global__ void __launch_bounds__(NT, 1)
         tc::fence_after();
         // phase P: P = exp2(Z log2e - lse2) -> smem
         tc::mbar_wait(pz_empty, (pzc & 1) ^ 1);
+        if (p.z_tma | p.ds_tma) {  // this warp's TMA stores out of the tile have read it
+          if (lane == 0) tc::bulk_wait_read0();
+          __syncwarp();
+        }
 #pragma unroll
         for (int c0 = 0; c0 < TB; c0 += 32) {
           float v[32];
@@ -604,7 +611,8 @@ __global__ void __launch_bounds__(NT, 1)
             if (vec && t0 + c0 + 32 <= p.T) {
 #pragma unroll
               for (int c = 0; c < 4; ++c) {
-                *reinterpret_cast<uint4*>(zr + c0 + 8 * c) = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+                if (!p.z_tma)
+                  *reinterpret_cast<uint4*>(zr + c0 + 8 * c) = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
                 *reinterpret_cast<uint4*>(lr + c0 + 8 * c) = make_uint4(lo[4 * c], lo[4 * c + 1], lo[4 * c + 2], lo[4 * c + 3]);
               }
             } else {
@@ -612,7 +620,7 @@ __global__ void __launch_bounds__(NT, 1)
                 const uint32_t w = pk[i >> 1], wl = lo[i >> 1];
                 const unsigned short hs = (i & 1) ? (unsigned short)(w >> 16) : (unsigned short)(w & 0xffffu);
                 const unsigned short ls = (i & 1) ? (unsigned short)(wl >> 16) : (unsigned short)(wl & 0xffffu);
-                reinterpret_cast<unsigned short*>(zr)[c0 + i] = hs;
+                if (!p.z_tma) reinterpret_cast<unsigned short*>(zr)[c0 + i] = hs;
                 reinterpret_cast<unsigned short*>(lr)[c0 + i] = ls;
               }
             }
@@ -624,6 +632,13 @@ __global__ void __launch_bounds__(NT, 1)
         if (lane == 0) {
           tc::mbar_arrive(pz_full);
           tc::mbar_arrive(zdp_empty);
+          // the warp's 32 dZ rows x 128 columns straight out of the swizzled
+          // tile (two 64-column boxes; rows past HQ / columns past T clipped)
+          if (p.z_tma && qt * TB + qtr * 32 < p.HQ) {
+            tc::tma_store_3d(&tmZ, sPZ + qtr * 4096, t0, qt * TB + qtr * 32, b);
+            tc::tma_store_3d(&tmZ, sPZ + ATOM + qtr * 4096, t0 + 64, qt * TB + qtr * 32, b);
+            tc::bulk_commit();
+          }
         }
         ++pzc;
       }
@@ -631,6 +646,36 @@ __global__ void __launch_bounds__(NT, 1)
       tc::mbar_wait(ds_full, n & 1);
       tc::fence_after();
       const int t = t0 + r;
+      if (p.ds_tma) {
+        // dS rows through the (now free) P/dZ tile, 128 columns at a time,
+        // TMA-stored as 64-column boxes of the warp's 32 rows
+#pragma unroll 1
+        for (int h = 0; h < D; h += TB) {
+          if (lane == 0) tc::bulk_wait_read0();
+          __syncwarp();
+#pragma unroll 1
+          for (int c0 = 0; c0 < TB; c0 += 32) {
+            float v[32];
+            uint32_t pk[16];
+            tc::tmem_ld32(trow + T_DS + h + c0, v);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) pk[i] = tc::pack_bf16(v[2 * i], v[2 * i + 1]);
+            store_sw(sPZ, r, c0, pk);
+          }
+          tc::fence_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tc::tma_store_3d(&tmD, sPZ + qtr * 4096, h, t0 + qtr * 32, b);
+            tc::tma_store_3d(&tmD, sPZ + ATOM + qtr * 4096, h + 64, t0 + qtr * 32, b);
+            tc::bulk_commit();
+          }
+        }
+        tc::fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(ds_empty);
+        ++n;
+        continue;
+      }
       bf16* dr = t < p.T ? p.dS + (long long)b * p.ds_bs + (long long)t * p.ds_rs : nullptr;
 #pragma unroll 1
       for (int c0 = 0; c0 < D; c0 += 32) {
@@ -663,6 +708,7 @@ __global__ void __launch_bounds__(NT, 1)
       if (lane == 0) tc::mbar_arrive(ds_empty);
       ++n;
     }
+    if (lane == 0) tc::bulk_wait0();
   }
   tc::fence_before();
   __syncthreads();
@@ -1712,6 +1758,15 @@ extern "C" int kl_hsp_bwd(const kl_hsp_args* a, void* stream) {
     set_error("kl_hsp_bwd: tensor map encode failed (alignment?)");
     return KL_EUNSUPPORTED;
   }
+  // d <= 256: dZ (hi) and (unless accumulating) dS leave by TMA stores
+  // (KL_HSP_BWD_TMA=0 keeps the per-thread row stores: A/B testing)
+  CUtensorMap tZ = tS, tD = tS;
+  static int bwd_tma = -1;
+  if (bwd_tma < 0) bwd_tma = (getenv("KL_HSP_BWD_TMA") && getenv("KL_HSP_BWD_TMA")[0] == '0') ? 0 : 1;
+  if (a->d != 512 && bwd_tma) {
+    p.z_tma = (a->T % 8) == 0 && hsp::map3(&tZ, a->dZ, a->T, a->HQ, a->T, a->B, (long long)a->HQ * a->T, 32);
+    p.ds_tma = !a->accumulate_ds && (a->B == 1 || a->ds_bs >= a->ds_rs * (long long)a->T) && hsp::map3(&tD, a->dS, a->d, a->T, a->ds_rs, a->B, a->ds_bs, 32);
+  }
   cudaStream_t s = (cudaStream_t)stream;
   const int items = p.B * p.tblocks;
   int grid = std::min(items, tc_num_sms());
@@ -1723,11 +1778,11 @@ extern "C" int kl_hsp_bwd(const kl_hsp_args* a, void* stream) {
   } else if (a->d == 256) {
     const size_t smem = hsp::bwd_smem<256>();
     cudaFuncSetAttribute(hsp::hsp_bwd_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    launch_k(hsp::hsp_bwd_kernel<256>, grid, hsp::NT, smem, s, tS, tQ, tG, p);
+    launch_k(hsp::hsp_bwd_kernel<256>, grid, hsp::NT, smem, s, tS, tQ, tG, tZ, tD, p);
   } else {
     const size_t smem = hsp::bwd_smem<128>();
     cudaFuncSetAttribute(hsp::hsp_bwd_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    launch_k(hsp::hsp_bwd_kernel<128>, grid, hsp::NT, smem, s, tS, tQ, tG, p);
+    launch_k(hsp::hsp_bwd_kernel<128>, grid, hsp::NT, smem, s, tS, tQ, tG, tZ, tD, p);
   }
   count_launch();
   count_path(KL_PATH_HSP_BWD_TC);

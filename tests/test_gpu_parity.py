@@ -408,13 +408,15 @@ def test_swa_tc_mask_bitexact_via_lse(T, w, causal):
 
 @pytest.mark.parametrize("dtype", DTYPES)
 @pytest.mark.parametrize("T,d,H,n_seeds", [(37, 32, 2, 6), (1, 32, 2, 6), (300, 128, 2, 40), (257, 256, 4, 32),
-                                           (130, 256, 4, 12), (300, 512, 8, 32), (1000, 512, 8, 12)])
+                                           (130, 256, 4, 12), (256, 256, 4, 140), (384, 128, 2, 40),
+                                           (300, 512, 8, 32), (1000, 512, 8, 12)])
 def test_hsp_vs_oracle(dtype, T, d, H, n_seeds):
     """HSP + CLS pooling vs the oracle; d in {128, 256, 512} in bf16 runs the
     fused tcgen05 pooling kernels (kl_hsp_fwd / kl_hsp_bwd; d = 512 streams
     its operands and forms dS / dQ with GEMMs), with query tiles that straddle
     the seed / CLS boundary and a partial second tile — asserted through the
-    kernel-path counters."""
+    kernel-path counters.  T % 8 == 0 (256, 384) takes the d <= 256
+    backward's TMA-stored dZ / dS rows; the other lengths its row stores."""
     from paper_2602_10016_b200 import functional as F
     from paper_2602_10016_b200 import seqsum as Q
     from paper_2602_10016_b200.tensor import Params
