@@ -106,6 +106,53 @@ extern "C" int kl_tcgen05_available(void) {
   return (major == 10 && minor == 0) ? 1 : 0;
 }
 
+// Batch folding in front of both GEMM paths.  A batch dim the B operand
+// broadcasts over, with the rows of A, C (and R) continuing evenly across it,
+// becomes extra M rows: one tall product instead of nb small ones (a per-sample
+// M = 16 product fills 1/8 of every 128-row tile).  A reduced batch dim whose A
+// columns and B rows continue across it becomes extra K: one long reduction
+// instead of nb k loops each padded to whole 64-wide k blocks (K = 8 per
+// sample pads 8x).  The products and sums are the same; only the fp32
+// summation order of a folded reduction changes.  Only under-filled shapes
+// fold (M < 128 rows, K not a multiple of 64): folding the c4 step's large
+// batched GEMMs changed their tile plans and cost 0.5 ms.  Measured on the
+// steps (KL_GEMM_FOLD = 0 / 1 / 2 / 3): c4 26.51, 26.54 / 26.38, 26.75 /
+// 26.96, 26.68 / 26.14, 26.33 ms; c2 6.27 / 6.21 / 6.24 / 6.25 ms — the K
+// folds are the default, the M folds (which cost c4 time) are opt-in.
+static void fold_batches(GemmDesc& g, const Epi& e) {
+  static int on = -1;
+  // 1: M and K folds, 2: M folds only, 3 (default): K folds only
+  if (on < 0) on = getenv("KL_GEMM_FOLD") ? atoi(getenv("KL_GEMM_FOLD")) : 3;
+  if (!on) return;
+  for (int pass = 0; pass < 2; ++pass) {  // batch dim 2, then 1
+    int& nb = pass == 0 ? g.nb2 : g.nb1;
+    int& red = pass == 0 ? g.red2 : g.red1;
+    long long& as = pass == 0 ? g.a_s2 : g.a_s1;
+    long long& bs = pass == 0 ? g.b_s2 : g.b_s1;
+    long long& cs = pass == 0 ? g.c_s2 : g.c_s1;
+    long long& rs = pass == 0 ? g.r_s2 : g.r_s1;
+    if (nb <= 1) continue;
+    if (!red) {
+      if (on == 3) continue;
+      const long long M = g.M;
+      if (M >= 128 || e.row_limit || bs != 0 || g.a_rs == 0 || as != M * g.a_rs || g.c_rs == 0 || cs != M * g.c_rs ||
+          (g.R && (g.r_rs == 0 || rs != M * g.r_rs)) || M * nb > (1LL << 30))
+        continue;
+      g.M = (int)(M * nb);
+      nb = 1;
+      as = bs = cs = rs = 0;
+    } else {
+      if (on == 2) continue;
+      const long long K = g.K;
+      if (K % 64 == 0 || g.a_cs == 0 || as != K * g.a_cs || g.b_rs == 0 || bs != K * g.b_rs || K * nb > (1LL << 30)) continue;
+      g.K = (int)(K * nb);
+      nb = 1;
+      red = 0;
+      as = bs = cs = rs = 0;
+    }
+  }
+}
+
 extern "C" int kl_gemm(const kl_gemm_args* a, void* stream) {
   if (!a) {
     set_error("kl_gemm: null args");
@@ -147,6 +194,7 @@ extern "C" int kl_gemm(const kl_gemm_args* a, void* stream) {
   e.alpha = a->alpha; e.beta = a->beta; e.bias = a->bias; e.row_limit = a->row_limit;
   e.aux_mode = a->aux_mode; e.n_act = a->n_act; e.act_group = a->act_group > 0 ? a->act_group : 1;
   for (int i = 0; i < KL_MAX_ACT_GROUPS; ++i) e.act_codes[i] = a->act_codes[i];
+  fold_batches(g, e);
   cudaStream_t s = (cudaStream_t)stream;
   bind_device(s);
   if (a->ab_dtype == KL_BF16 && g_gemm_path != 1) {

@@ -285,3 +285,49 @@ def test_tc_wide_pairs(a_k, b_n):
     assert _capi.path_hits()["gemm_wide"] == 1
     ref = C0.double() + (X.double().transpose(1, 2) @ D.double()).sum(0)
     assert rel(C, ref) < 1e-5
+
+
+def test_gemm_fold_reduced_batch_into_k():
+    """A reduced batch dim whose A columns / B rows continue across it runs as
+    one long k loop (kl_gemm's batch folding; K = 40 per sample would pad each
+    64-wide k block): the weight-gradient form sum_z X_z^T G_z, fp32
+    accumulate and bf16 store, against fp64."""
+    from paper_2602_10016_b200._capi import gemm
+
+    g = torch.Generator(device="cuda").manual_seed(21)
+    X = torch.randn(6, 40, 96, device="cuda", generator=g).bfloat16()
+    G = torch.randn(6, 40, 80, device="cuda", generator=g).bfloat16()
+    ref = (X.double().transpose(1, 2) @ G.double()).sum(0)
+    C0 = torch.randn(96, 80, device="cuda", generator=g)
+    C = C0.clone()
+    gemm(X.transpose(1, 2), G, C.view(1, 96, 80), beta=1.0, reduce=(False, True))
+    assert rel(C, C0.double() + ref) < 1e-5
+    Cb = torch.empty(1, 96, 80, device="cuda", dtype=torch.bfloat16)
+    gemm(X.transpose(1, 2), G, Cb, reduce=(False, True))
+    assert rel(Cb[0], ref) < 1e-2
+
+
+def test_gemm_fold_broadcast_batch_into_m():
+    """The opt-in M folds (KL_GEMM_FOLD=1, read once per process: run in a
+    child): a per-sample M = 16 product against a broadcast weight becomes
+    one 2048-row GEMM (KL_GEMM_TRACE shows the folded M) with the same
+    result."""
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "import torch, sys; sys.path.insert(0, '.');"
+        "from paper_2602_10016_b200._capi import gemm;"
+        "g = torch.Generator(device='cuda').manual_seed(3);"
+        "A = torch.randn(128, 16, 64, device='cuda', generator=g).bfloat16();"
+        "W = torch.randn(64, 256, device='cuda', generator=g).bfloat16();"
+        "b = torch.randn(256, device='cuda', generator=g);"
+        "C = gemm(A, W, bias=b, acts=['relu']); torch.cuda.synchronize();"
+        "ref = torch.relu(A.double() @ W.double() + b.double());"
+        "err = ((C.double() - ref).norm() / ref.norm()).item(); print('err', err); assert err < 1e-2")
+    env = dict(os.environ, KL_GEMM_FOLD="1", KL_GEMM_TRACE="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "gemm_tc M=2048 N=256 K=64 nb=1x1" in r.stderr, r.stderr[-2000:]
