@@ -331,3 +331,28 @@ def test_gemm_fold_broadcast_batch_into_m():
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert r.returncode == 0, r.stderr[-2000:]
     assert "gemm_tc M=2048 N=256 K=64 nb=1x1" in r.stderr, r.stderr[-2000:]
+
+
+def test_tc_wide_plain_early_release():
+    """Wide pairs with a plain bf16 store (MODE 2: no bias / activation /
+    residual): the epilogue releases the 512-column accumulator after its
+    TMEM drain, before the TMA stores (epi_wide_regs) — batched, with an M
+    tail and a per-batch row limit."""
+    from paper_2602_10016_b200 import _capi
+    from paper_2602_10016_b200._capi import gemm
+
+    g = torch.Generator(device="cuda").manual_seed(13)
+    M, N, K = 9000, 1024, 512  # 2 x 36 x 2 = 144 pair tiles, M tail of 40 rows
+    A = operand((2, M, K), True, g) * 0.05
+    B = operand((K, N), False, g) * 0.05
+    lim = torch.tensor([M, 3001], device="cuda", dtype=torch.int32)
+    _capi.reset_path_hits()
+    out = gemm(A, B, row_limit=lim)
+    out2 = gemm(A, B, alpha=0.5)
+    torch.cuda.synchronize()
+    assert _capi.path_hits()["gemm_wide"] == 2
+    z = A.double() @ B.double()
+    keep = torch.arange(M, device="cuda")[None, :, None] < lim.view(2, 1, 1)
+    assert rel(out, torch.where(keep, z, 0)) < 1e-2
+    assert float(out[1, 3001:].abs().max()) == 0.0
+    assert rel(out2, 0.5 * z) < 1e-2
